@@ -1,0 +1,214 @@
+/* pbkv.h -- C ABI of the B200-native PBKV scoring / victim-selection hot path.
+ *
+ * Drop-in boundary for the reference policy interface in
+ * /root/reference/proj/include/flowkv/ (a header-only C++20 library with no
+ * virtual interface: policies are inline free functions chosen at the call
+ * sites simulator.hpp:434, :464, :618, :635-637, :657).  Each entry point below
+ * names the reference function it replaces.  The C++ shim that re-exposes the
+ * exact reference signatures on top of this ABI is include/pbkv/flowkv_gpu.hpp;
+ * INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Conventions
+ *  - Every function returns a pbkv_status.  On failure, pbkv_last_error(ctx)
+ *    (or pbkv_last_error(NULL) for functions without a ctx) returns the
+ *    message.  PBKV_EINVAL carries exactly the reference's
+ *    flowkv::ValidationError message (errors.hpp:24-26), so the C++ shim can
+ *    rethrow it unchanged.
+ *  - Plain pointers and sizes only; every array argument is HOST memory unless
+ *    the function name ends in _dev.
+ *  - A context owns one CUDA stream and all of its device memory; contexts
+ *    share nothing (one per simulator instance, scenario.hpp:291-301).
+ *  - No CPU fallback: when no sm_100 device is present, pbkv_ctx_create
+ *    fails with PBKV_ECUDA.
+ */
+#ifndef PBKV_H_
+#define PBKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBKV_ABI_VERSION 1
+
+typedef enum pbkv_status {
+    PBKV_OK = 0,
+    PBKV_EINVAL = 1, /* flowkv::ValidationError (message preserved) */
+    PBKV_ECUDA = 2,  /* CUDA runtime / device failure, or no sm_100 device */
+    PBKV_ENOMEM = 3, /* device or host allocation failed */
+    PBKV_EARG = 4,   /* bad pointer / size / capacity at the ABI level */
+} pbkv_status;
+
+/* cache.hpp:19  enum class Tier { Device, Host, Absent } */
+enum { PBKV_TIER_DEVICE = 0, PBKV_TIER_HOST = 1, PBKV_TIER_ABSENT = 2 };
+
+/* policies.hpp:19  enum class EvictionPolicy { Lru, Lae, Hierarchical, KvFlow } */
+enum { PBKV_POLICY_LRU = 0, PBKV_POLICY_LAE = 1, PBKV_POLICY_HE = 2, PBKV_POLICY_KVFLOW = 3 };
+
+/* Which score the HE key uses (SURVEY.md §7 hard part 5):
+ *  CACHED    -- the mirrored CacheTree::Node::score (cache.hpp:61), exactly
+ *               what select_victims_hierarchical reads (policies.hpp:113);
+ *  RECOMPUTE -- Eq. 2 recomputed on the device from the resident forecasts
+ *               for every node in the same launch sequence (the north_star
+ *               "score all, then select" pipeline; equal to CACHED in the
+ *               simulator). */
+enum { PBKV_SCORE_CACHED = 0, PBKV_SCORE_RECOMPUTE = 1 };
+
+typedef struct pbkv_ctx pbkv_ctx;   /* device-side mirror + forecasts + scratch */
+typedef struct pbkv_tree pbkv_tree; /* host-side radix-tree mirror (RadixMirror) */
+
+typedef struct pbkv_cfg {
+    int device;        /* CUDA ordinal */
+    int k;             /* ScoreParams::k      (scoring.hpp:17), >= 1 */
+    double gamma;      /* ScoreParams::gamma  (scoring.hpp:18), in (0,1) */
+    int num_agents;    /* A; forecasts have A+1 outcomes (forecast.hpp:46) */
+} pbkv_cfg;
+
+/* Struct-of-arrays view of a CacheTree (read-side fields, cache.hpp:54-69).
+ * Node ids index every per-node array; id 0 is the root.  Access entries are
+ * a CSR: node i owns entries [acc_off[i], acc_off[i+1]), sorted by ascending
+ * WorkflowId (the std::map order of Node::access, cache.hpp:64). */
+typedef struct pbkv_tree_soa {
+    int64_t n_nodes;
+    int64_t n_entries;
+    int32_t* parent;          /* [n] -1 for the root */
+    int32_t* len;             /* [n] tokens.size() */
+    uint8_t* tier;            /* [n] PBKV_TIER_* */
+    uint8_t* retired;         /* [n] 0/1 */
+    uint64_t* last_access;    /* [n] < 2^63 */
+    int32_t* ever_tagged;     /* [n] */
+    double* score;            /* [n] cached score (may be NULL -> 0.0) */
+    int32_t* device_children; /* [n] (export only; may be NULL) */
+    int32_t* depth;           /* [n] root = 0 (may be NULL on input -> derived) */
+    int64_t* acc_off;         /* [n+1] */
+    int64_t* acc_wf;          /* [E] WorkflowId */
+    uint64_t* acc_bits;       /* [E] agent bit set (bit a <-> agent a, cache.hpp:489) */
+    int64_t device_capacity;  /* cache.hpp:81 */
+    int64_t device_used;      /* cache.hpp:83 */
+    int64_t retired_device_tokens; /* cache.hpp:87 */
+    int64_t host_capacity;
+    int64_t host_used;
+} pbkv_tree_soa;
+
+/* PrefetchPlan (policies.hpp:170-177) scalars; the candidate and selected
+ * lists are returned through caller arrays. */
+typedef struct pbkv_prefetch_plan {
+    int64_t budget_space;        /* Sa = device_free + retired_device_tokens (policies.hpp:185) */
+    int64_t budget_bw;           /* Sbw = bandwidth * step_duration (policies.hpp:186) */
+    int64_t displacement_budget; /* aggressive only: (int64)(rho * capacity) (policies.hpp:233) */
+    int64_t selected_tokens;
+    int64_t n_candidates;        /* total candidates (may exceed the caller's capacity) */
+    int64_t n_selected;
+} pbkv_prefetch_plan;
+
+/* Synthetic workload parameters (generator in
+ * paper_2605_06472_b200/csrc/host/ops.hpp). */
+typedef struct pbkv_synth_params {
+    int64_t n_nodes, n_workflows;
+    int agents, group_size, shared_len, group_len, alphabet, max_rand_len;
+    double retired_frac;
+    int host_every;
+    uint64_t seed;
+} pbkv_synth_params;
+
+/* ---- library --------------------------------------------------------------- */
+int pbkv_abi_version(void);
+const char* pbkv_last_error(const pbkv_ctx* ctx); /* NULL ctx -> thread-local last error */
+int pbkv_device_count(int* out);                   /* sm_100 devices visible */
+
+/* ---- context --------------------------------------------------------------- */
+int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg); /* validates k/gamma like ScoreParams::validate (scoring.hpp:20-23) */
+int pbkv_ctx_destroy(pbkv_ctx* ctx);
+int pbkv_ctx_sync(pbkv_ctx* ctx);                          /* cudaStreamSynchronize on the ctx stream */
+int pbkv_ctx_stream(pbkv_ctx* ctx, void** stream_out);     /* the ctx's cudaStream_t */
+/* Per-stage device time of the most recent call, milliseconds (CUDA events on
+ * the ctx stream): [0]=score [1]=keys+eff [2]=cut/sort [3]=prefetch [4]=total. */
+int pbkv_ctx_timings(pbkv_ctx* ctx, float* ms5);
+int pbkv_ctx_set_timing(pbkv_ctx* ctx, int enabled);
+
+/* ---- device mirror of the tree --------------------------------------------- */
+/* Full upload of a CacheTree snapshot (SURVEY.md §8(b) pbkv_mirror_full). */
+int pbkv_mirror_full(pbkv_ctx* ctx, const pbkv_tree_soa* soa);
+/* Full upload from a host RadixMirror, then clears its dirty list. */
+int pbkv_mirror_tree(pbkv_ctx* ctx, pbkv_tree* tree);
+/* Incremental upload of only the nodes the host mirror dirtied since the last
+ * sync (node fields + access entries; falls back to a full upload when the
+ * entry storage must grow). */
+int pbkv_mirror_sync(pbkv_ctx* ctx, pbkv_tree* tree);
+/* Update the cached scores of `n` nodes (CacheTree::set_score, cache.hpp:320). */
+int pbkv_mirror_set_scores(pbkv_ctx* ctx, const int32_t* ids, const double* scores, int64_t n);
+int pbkv_mirror_node_count(pbkv_ctx* ctx, int64_t* n_nodes, int64_t* n_entries);
+
+/* ---- forecasts (stage 1 output / stage 2 input) ---------------------------- */
+/* Upload `n` Forecasts (forecast.hpp:19-42): p is n x horizon x outcomes
+ * row-major.  Validated on the device exactly like the Forecast ctor
+ * (entries >= -1e-12, each step sums to 1 within 1e-9); survival and the
+ * gamma-weighted table gs[w][k] = gamma^k * s_w(k) are derived there.
+ * Replaces the provider's std::map entry (simulator.hpp:433). */
+int pbkv_forecast_put(pbkv_ctx* ctx, const int64_t* wf, int64_t n, int horizon, int outcomes,
+                      const double* p);
+/* Drops forecasts (simulator.hpp:617 forecasts_.erase(w)). */
+int pbkv_forecast_drop(pbkv_ctx* ctx, const int64_t* wf, int64_t n);
+int pbkv_forecast_clear(pbkv_ctx* ctx);
+
+/* ---- stage 2: Score(c), Eq. 2 ---------------------------------------------- */
+/* multi_step_score(node_terms(...)) (scoring.hpp:49-75) for every node; nodes
+ * without access entries score +0.0.  Raises EINVAL "missing forecast for
+ * active workflow <w>" if any tagged workflow has no forecast.  scores_out
+ * (host, n_nodes doubles) may be NULL: the scores then only stay resident. */
+int pbkv_score_all(pbkv_ctx* ctx, double* scores_out);
+/* refresh_nodes (scoring.hpp:95-101) without the write-back: Eq. 2 for the
+ * listed node ids, results in `out` (host). */
+int pbkv_score_nodes(pbkv_ctx* ctx, const int32_t* ids, int64_t n, double* out);
+/* single_step_value (scoring.hpp:41-45), Eq. 1, for the listed node ids. */
+int pbkv_value_nodes(pbkv_ctx* ctx, const int32_t* ids, int64_t n, double* out);
+
+/* ---- stage 3: victim selection --------------------------------------------- */
+/* select_victims / select_victims_{lru,lae,hierarchical}
+ * (policies.hpp:88-115, :155-168): victims in eviction order, bit-identical
+ * to the reference's greedy frontier (policies.hpp:50-83).  `locked` is the
+ * image of std::set<int> (any order, duplicates allowed).  If `cap` is
+ * smaller than the victim count, PBKV_EARG is returned and *n_victims holds
+ * the required size. */
+int pbkv_select(pbkv_ctx* ctx, int policy, int score_mode, int64_t needed, const int32_t* locked,
+                int64_t n_locked, int32_t* victims, int64_t cap, int64_t* n_victims, int64_t* freed,
+                int* shortfall);
+/* Same, but `locked`/`victims` are device pointers and the three scalars are
+ * written to a device int64[3] {n_victims, freed, shortfall}; no host
+ * synchronisation beyond the ones the cut needs.  For benchmarking the
+ * HBM-resident pipeline. */
+int pbkv_select_dev(pbkv_ctx* ctx, int policy, int score_mode, int64_t needed, const int32_t* locked_dev,
+                    int64_t n_locked, int32_t* victims_dev, int64_t cap, int64_t* result_dev);
+/* KVFlow key (policies.hpp:117-153) needs the static remaining sequences:
+ * seq_off[n_wf+1] CSR over seq (agent ids) for workflow ids wf[n_wf]. */
+int pbkv_set_remaining(pbkv_ctx* ctx, const int64_t* wf, int64_t n_wf, const int64_t* seq_off,
+                       const int32_t* seq);
+
+/* ---- stage 4: prefetch candidate ranking ----------------------------------- */
+/* plan_conservative_prefetch (rho < 0) / plan_aggressive_prefetch (rho in
+ * [0,1]) (policies.hpp:181-235).  Candidates (id, Eq.1 value) sorted by value
+ * desc then id asc, and the greedy-with-skip selection; arrays may be NULL
+ * when their capacity is 0.  n_candidates/n_selected report full sizes. */
+int pbkv_plan_prefetch(pbkv_ctx* ctx, int64_t bandwidth, int step_duration, double rho, int32_t* cand_ids,
+                       double* cand_values, int64_t cand_cap, int32_t* selected, int64_t sel_cap,
+                       pbkv_prefetch_plan* plan);
+
+/* ---- host radix-tree mirror (RadixMirror, cache.hpp semantics) -------------- */
+int pbkv_tree_create(pbkv_tree** out, int64_t device_capacity, int64_t host_capacity);
+int pbkv_tree_destroy(pbkv_tree* tree);
+/* Applies an op stream (paper_2605_06472_b200/csrc/host/ops.hpp). */
+int pbkv_tree_apply_ops(pbkv_tree* tree, const int64_t* words, int64_t n_words);
+int pbkv_tree_synth(pbkv_tree* tree, const pbkv_synth_params* params);
+/* Sizes and tier scalars, written into soa (pointers untouched). */
+int pbkv_tree_shape(pbkv_tree* tree, pbkv_tree_soa* soa);
+/* Fills every non-NULL array of soa (sized from pbkv_tree_shape). */
+int pbkv_tree_export(pbkv_tree* tree, pbkv_tree_soa* soa);
+int pbkv_tree_touched(pbkv_tree* tree, int64_t wf, int32_t* ids, int64_t cap, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBKV_H_ */

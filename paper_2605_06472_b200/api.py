@@ -1,0 +1,294 @@
+"""Host-side mirror of the reference policy interface, on top of libpbkv.so.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/flowkv/{policies,scoring}.hpp:
+
+  reference (C++)                                   here (GPU path)
+  select_victims(tree, policy, needed, rem, locked)  Policy.select_victims
+  select_victims_{lru,lae,hierarchical,kvflow}      Policy.select_victims_*
+  plan_conservative_prefetch(tree, fp, bw, step)     Policy.plan_conservative_prefetch
+  plan_aggressive_prefetch(tree, fp, bw, rho, step)  Policy.plan_aggressive_prefetch
+  multi_step_score(node_terms(...))                  Policy.score_nodes / score_all
+  single_step_value(node_terms(...))                 Policy.value_nodes
+  flowkv::ValidationError                            ValidationError (same messages)
+
+The tree is borrowed as a snapshot: ``Policy.mirror(tree)`` uploads the
+struct-of-arrays image (from a HostTree -- the C++ RadixMirror -- or from any
+SoAArrays export); forecasts are uploaded with ``put_forecasts``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Mapping, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import (POLICY_HE, POLICY_KVFLOW, POLICY_LAE, POLICY_LRU, SCORE_CACHED, SCORE_RECOMPUTE,
+                   SoAArrays, ptr)
+
+
+class ValidationError(RuntimeError):
+    """flowkv::ValidationError (errors.hpp:24-26) raised through the C ABI."""
+
+
+class PbkvError(RuntimeError):
+    """CUDA / allocation / ABI-level failure (PBKV_ECUDA, PBKV_ENOMEM, PBKV_EARG)."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[pbkv status {status}] {msg}")
+        self.status = status
+
+
+def _check(rc: int, handle) -> None:
+    if rc == _abi.PBKV_OK:
+        return
+    msg = _abi.lib().pbkv_last_error(handle).decode()
+    if rc == _abi.PBKV_EINVAL:
+        raise ValidationError(msg)
+    raise PbkvError(rc, msg)
+
+
+@dataclass
+class VictimSelection:
+    """policies.hpp:30-34"""
+    victims: list[int] = field(default_factory=list)
+    freed: int = 0
+    shortfall: bool = False
+
+
+@dataclass
+class PrefetchPlan:
+    """policies.hpp:170-177"""
+    candidates: list[tuple[int, float]] = field(default_factory=list)
+    budget_space: int = 0
+    budget_bw: int = 0
+    displacement_budget: int = 0
+    selected: list[int] = field(default_factory=list)
+    selected_tokens: int = 0
+
+
+# ----------------------------------------------------------------------------------
+class HostTree:
+    """The C++ RadixMirror (csrc/host/radix_mirror.hpp): cache.hpp mutation
+    semantics, SoA export, dirty tracking."""
+
+    def __init__(self, device_capacity: int = 1 << 40, host_capacity: int = 1 << 40):
+        L = _abi.lib()
+        h = C.c_void_p()
+        _check(L.pbkv_tree_create(C.byref(h), int(device_capacity), int(host_capacity)), None)
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _abi.lib().pbkv_tree_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def apply_ops(self, words: Sequence[int] | np.ndarray) -> None:
+        w = np.ascontiguousarray(np.asarray(words, dtype=np.int64))
+        _check(_abi.lib().pbkv_tree_apply_ops(self._h, ptr(w, C.c_int64), int(w.size)), None)
+
+    def synth(self, **params) -> None:
+        p = _abi.synth_params(**params)
+        _check(_abi.lib().pbkv_tree_synth(self._h, C.byref(p)), None)
+
+    def export(self) -> SoAArrays:
+        L = _abi.lib()
+        shape = _abi.TreeSoA()
+        _check(L.pbkv_tree_shape(self._h, C.byref(shape)), None)
+        arr = SoAArrays(shape.n_nodes, shape.n_entries, dict(
+            device_capacity=shape.device_capacity, device_used=shape.device_used,
+            retired_device_tokens=shape.retired_device_tokens, host_capacity=shape.host_capacity,
+            host_used=shape.host_used))
+        s = arr.struct()
+        _check(L.pbkv_tree_export(self._h, C.byref(s)), None)
+        return arr
+
+    def touched(self, wf: int) -> list[int]:
+        L = _abi.lib()
+        n = C.c_int64()
+        _check(L.pbkv_tree_touched(self._h, int(wf), None, 0, C.byref(n)), None)
+        ids = np.zeros(max(n.value, 1), dtype=np.int32)
+        _check(L.pbkv_tree_touched(self._h, int(wf), ptr(ids, C.c_int32), n.value, C.byref(n)), None)
+        return ids[: n.value].tolist()
+
+
+# ----------------------------------------------------------------------------------
+class Policy:
+    """One device context (one CUDA stream, one tree mirror, one forecast store)."""
+
+    def __init__(self, num_agents: int, k: int = 3, gamma: float = 0.7, device: int = 0):
+        L = _abi.lib()
+        cfg = _abi.Cfg(int(device), int(k), float(gamma), int(num_agents))
+        h = C.c_void_p()
+        _check(L.pbkv_ctx_create(C.byref(h), C.byref(cfg)), None)
+        self._h = h
+        self.k, self.gamma, self.num_agents = int(k), float(gamma), int(num_agents)
+        self.n_nodes = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _abi.lib().pbkv_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _c(self, rc):
+        _check(rc, self._h)
+
+    # ---- mirror ------------------------------------------------------------------
+    def mirror(self, tree: "HostTree | SoAArrays", with_depth: bool = True) -> None:
+        L = _abi.lib()
+        if isinstance(tree, HostTree):
+            self._c(L.pbkv_mirror_tree(self._h, tree.handle))
+        else:
+            s = tree.struct(with_depth=with_depth)
+            self._c(L.pbkv_mirror_full(self._h, C.byref(s)))
+        n = C.c_int64()
+        self._c(L.pbkv_mirror_node_count(self._h, C.byref(n), None))
+        self.n_nodes = n.value
+
+    def set_scores(self, ids: Sequence[int], scores: Sequence[float]) -> None:
+        i = np.ascontiguousarray(ids, dtype=np.int32)
+        s = np.ascontiguousarray(scores, dtype=np.float64)
+        self._c(_abi.lib().pbkv_mirror_set_scores(self._h, ptr(i, C.c_int32), ptr(s, C.c_double), int(i.size)))
+
+    # ---- forecasts -----------------------------------------------------------------
+    def put_forecasts(self, wf_ids: Sequence[int], probs: np.ndarray) -> None:
+        """probs: [n, horizon, outcomes] float64 (Forecast rows, forecast.hpp:19)."""
+        w = np.ascontiguousarray(wf_ids, dtype=np.int64)
+        p = np.ascontiguousarray(probs, dtype=np.float64)
+        if p.ndim != 3 or p.shape[0] != w.size:
+            raise ValueError("probs must be [n_workflows, horizon, outcomes]")
+        self._c(_abi.lib().pbkv_forecast_put(self._h, ptr(w, C.c_int64), int(w.size), int(p.shape[1]),
+                                             int(p.shape[2]), ptr(p, C.c_double)))
+
+    def drop_forecasts(self, wf_ids: Iterable[int]) -> None:
+        w = np.ascontiguousarray(list(wf_ids), dtype=np.int64)
+        self._c(_abi.lib().pbkv_forecast_drop(self._h, ptr(w, C.c_int64), int(w.size)))
+
+    def set_remaining(self, remaining: Mapping[int, Sequence[int]]) -> None:
+        """Static remaining agent sequences for KVFlow (policies.hpp:144-153)."""
+        wf = np.array(sorted(remaining), dtype=np.int64)
+        off = np.zeros(wf.size + 1, dtype=np.int64)
+        flat: list[int] = []
+        for i, w in enumerate(wf.tolist()):
+            flat.extend(int(a) for a in remaining[w])
+            off[i + 1] = len(flat)
+        seq = np.array(flat if flat else [0], dtype=np.int32)
+        self._c(_abi.lib().pbkv_set_remaining(self._h, ptr(wf, C.c_int64), int(wf.size), ptr(off, C.c_int64),
+                                              ptr(seq, C.c_int32)))
+
+    # ---- stage 2 -------------------------------------------------------------------
+    def score_all(self) -> np.ndarray:
+        out = np.zeros(self.n_nodes, dtype=np.float64)
+        self._c(_abi.lib().pbkv_score_all(self._h, ptr(out, C.c_double)))
+        return out
+
+    def score_nodes(self, ids: Sequence[int]) -> np.ndarray:
+        i = np.ascontiguousarray(ids, dtype=np.int32)
+        out = np.zeros(i.size, dtype=np.float64)
+        self._c(_abi.lib().pbkv_score_nodes(self._h, ptr(i, C.c_int32), int(i.size), ptr(out, C.c_double)))
+        return out
+
+    def value_nodes(self, ids: Sequence[int]) -> np.ndarray:
+        i = np.ascontiguousarray(ids, dtype=np.int32)
+        out = np.zeros(i.size, dtype=np.float64)
+        self._c(_abi.lib().pbkv_value_nodes(self._h, ptr(i, C.c_int32), int(i.size), ptr(out, C.c_double)))
+        return out
+
+    # ---- stage 3 -------------------------------------------------------------------
+    def select_victims(self, policy: int, needed: int, remaining: Mapping[int, Sequence[int]] | None = None,
+                       locked: Iterable[int] = (), score_mode: int = SCORE_CACHED) -> VictimSelection:
+        """policies.hpp:155-168"""
+        if policy == POLICY_KVFLOW:
+            if remaining is None:
+                raise ValidationError("kvflow selected without static sequences")
+            self.set_remaining(remaining)
+        lk_list = sorted(set(int(x) for x in locked))
+        lk = np.ascontiguousarray(lk_list or [0], dtype=np.int32)
+        n_lk = len(lk_list)
+        cap = max(self.n_nodes, 1)
+        victims = np.zeros(cap, dtype=np.int32)
+        nv, fr, sf = C.c_int64(), C.c_int64(), C.c_int()
+        self._c(_abi.lib().pbkv_select(self._h, int(policy), int(score_mode), int(needed), ptr(lk, C.c_int32), n_lk,
+                                       ptr(victims, C.c_int32), cap, C.byref(nv), C.byref(fr), C.byref(sf)))
+        return VictimSelection(victims[: nv.value].tolist(), int(fr.value), bool(sf.value))
+
+    def select_victims_lru(self, needed: int, locked: Iterable[int] = ()) -> VictimSelection:
+        return self.select_victims(POLICY_LRU, needed, locked=locked)
+
+    def select_victims_lae(self, needed: int, locked: Iterable[int] = ()) -> VictimSelection:
+        return self.select_victims(POLICY_LAE, needed, locked=locked)
+
+    def select_victims_hierarchical(self, needed: int, locked: Iterable[int] = (),
+                                    score_mode: int = SCORE_CACHED) -> VictimSelection:
+        return self.select_victims(POLICY_HE, needed, locked=locked, score_mode=score_mode)
+
+    def select_victims_kvflow(self, needed: int, remaining: Mapping[int, Sequence[int]],
+                              locked: Iterable[int] = ()) -> VictimSelection:
+        return self.select_victims(POLICY_KVFLOW, needed, remaining=remaining, locked=locked)
+
+    # ---- stage 4 -------------------------------------------------------------------
+    def _plan(self, bandwidth: int, step_duration: int, rho: float) -> PrefetchPlan:
+        L = _abi.lib()
+        cap = max(self.n_nodes, 1)
+        cid = np.zeros(cap, dtype=np.int32)
+        cv = np.zeros(cap, dtype=np.float64)
+        sel = np.zeros(cap, dtype=np.int32)
+        pl = _abi.PrefetchPlanC()
+        self._c(L.pbkv_plan_prefetch(self._h, int(bandwidth), int(step_duration), float(rho), ptr(cid, C.c_int32),
+                                     ptr(cv, C.c_double), cap, ptr(sel, C.c_int32), cap, C.byref(pl)))
+        nc, ns = pl.n_candidates, pl.n_selected
+        return PrefetchPlan(list(zip(cid[:nc].tolist(), cv[:nc].tolist())), pl.budget_space, pl.budget_bw,
+                            pl.displacement_budget, sel[:ns].tolist(), pl.selected_tokens)
+
+    def plan_conservative_prefetch(self, bandwidth: int, step_duration: int = 1) -> PrefetchPlan:
+        """policies.hpp:220-224"""
+        return self._plan(bandwidth, step_duration, -1.0)
+
+    def plan_aggressive_prefetch(self, bandwidth: int, rho: float, step_duration: int = 1) -> PrefetchPlan:
+        """policies.hpp:228-235"""
+        if not (0.0 <= rho <= 1.0):
+            raise ValidationError("rho must be in [0, 1]")
+        return self._plan(bandwidth, step_duration, rho)
+
+    # ---- timing ------------------------------------------------------------------------
+    def set_timing(self, on: bool) -> None:
+        self._c(_abi.lib().pbkv_ctx_set_timing(self._h, 1 if on else 0))
+
+    def timings(self) -> list[float]:
+        ms = (C.c_float * 5)()
+        self._c(_abi.lib().pbkv_ctx_timings(self._h, ms))
+        return list(ms)
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(_abi.lib().pbkv_device_count(C.byref(n)), None)
+    return n.value

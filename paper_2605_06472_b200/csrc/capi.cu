@@ -1,0 +1,911 @@
+// C ABI implementation (include/pbkv.h): context, device mirror, forecast
+// store and the orchestration of the stage 2-4 kernels (kernels.cu).
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host/ops.hpp"
+#include "host/radix_mirror.hpp"
+#include "pbkv_internal.cuh"
+
+struct pbkv_ctx : pbkv::Context {};
+struct pbkv_tree {
+    pbkv::RadixMirror tree;
+    std::string err;
+    pbkv_tree(std::int64_t d, std::int64_t h) : tree(d, h) {}
+};
+
+namespace pbkv {
+void launch_gather_heads(Context& c, std::int64_t n_heads);
+void launch_head_weights(Context& c, std::int64_t n_heads);
+void launch_find_cut(Context& c, const unsigned long long* scan, std::int64_t n, long long needed, long long* out);
+void launch_victim_keys(Context& c, long long cut, long long* counter);
+void launch_victim_len(Context& c, std::int64_t n);
+void launch_prefetch_err_id(Context& c);
+void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
+}  // namespace pbkv
+
+namespace {
+
+using namespace pbkv;
+
+thread_local std::string g_last_error;
+
+template <class F>
+int api(pbkv_ctx* c, F&& f) {
+    try {
+        f();
+        return PBKV_OK;
+    } catch (const ApiError& e) {
+        (c ? c->err : g_last_error) = e.what();
+        return e.status;
+    } catch (const pbkv::ValidationError& e) {
+        (c ? c->err : g_last_error) = e.what();
+        return PBKV_EINVAL;
+    } catch (const OpStreamError& e) {
+        (c ? c->err : g_last_error) = e.what();
+        return PBKV_EARG;
+    } catch (const std::bad_alloc&) {
+        (c ? c->err : g_last_error) = "host allocation failed";
+        return PBKV_ENOMEM;
+    } catch (const std::exception& e) {
+        (c ? c->err : g_last_error) = e.what();
+        return PBKV_EARG;
+    }
+}
+
+template <class F>
+int tree_api(pbkv_tree* t, F&& f) {
+    try {
+        if (!t) throw ApiError(PBKV_EARG, "null tree");
+        f();
+        return PBKV_OK;
+    } catch (const ApiError& e) {
+        (t ? t->err : g_last_error) = e.what();
+        g_last_error = e.what();
+        return e.status;
+    } catch (const pbkv::ValidationError& e) {
+        t->err = e.what();
+        g_last_error = e.what();
+        return PBKV_EINVAL;
+    } catch (const OpStreamError& e) {
+        t->err = e.what();
+        g_last_error = e.what();
+        return PBKV_EARG;
+    } catch (const std::exception& e) {
+        t->err = e.what();
+        g_last_error = e.what();
+        return PBKV_EARG;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) throw ApiError(PBKV_EARG, what);
+}
+
+void invalid(const std::string& what) { throw ApiError(PBKV_EINVAL, what); }
+
+void set_device(Context& c) { PBKV_CUDA(cudaSetDevice(c.device)); }
+
+// ---- forecast slots ----------------------------------------------------------
+int slot_for(Context& c, std::int64_t wf) {
+    auto it = c.slot_of.find(wf);
+    if (it != c.slot_of.end()) return it->second;
+    int s = static_cast<int>(c.n_slots);
+    if (c.n_slots >= INT_MAX - 1) throw ApiError(PBKV_EARG, "too many workflows");
+    std::size_t need_slots = static_cast<std::size_t>(c.n_slots + 1);
+    std::size_t old = static_cast<std::size_t>(c.n_slots);
+    c.P.grow_keep(need_slots * c.K * c.V1, old * c.K * c.V1, c.stream);
+    c.gs.grow_keep(need_slots * c.K, old * c.K, c.stream);
+    std::size_t old_cap = c.fstate.cap;
+    c.fstate.grow_keep(need_slots, old, c.stream);
+    if (c.fstate.cap != old_cap)
+        PBKV_CUDA(cudaMemsetAsync(c.fstate.p + old, 0, c.fstate.cap - old, c.stream));
+    std::size_t old_rcap = c.rem_has.cap;
+    c.rem_has.grow_keep(need_slots, old, c.stream);
+    if (c.rem_has.cap != old_rcap)
+        PBKV_CUDA(cudaMemsetAsync(c.rem_has.p + old, 0, c.rem_has.cap - old, c.stream));
+    c.n_slots += 1;
+    c.slot_of.emplace(wf, s);
+    c.h_slot_wf.push_back(wf);
+    return s;
+}
+
+void ensure_scratch(Context& c) {
+    std::size_t n = static_cast<std::size_t>(c.n) + 1;
+    c.score_rc.reserve(n);
+    c.keys.reserve(n);
+    c.eff.reserve(n);
+    c.sublock.reserve(n);
+    c.missing.reserve(n);
+    c.W.reserve(n);
+    c.heads.reserve(n);
+    c.rank.reserve(n);
+}
+
+std::string missing_message(Context& c, long long node) {
+    // first entry of `node` (WorkflowId order) lacking a forecast: node_terms
+    // raises before multi_step_score checks horizons (scoring.hpp:66-75, :53)
+    unsigned int off[2];
+    PBKV_CUDA(cudaMemcpy(off, c.acc_off.p + node, sizeof off, cudaMemcpyDeviceToHost));
+    std::vector<int> slots(off[1] - off[0]);
+    if (!slots.empty())
+        PBKV_CUDA(cudaMemcpy(slots.data(), c.acc_slot.p + off[0], slots.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<std::uint8_t> st(static_cast<std::size_t>(c.n_slots));
+    if (!st.empty()) PBKV_CUDA(cudaMemcpy(st.data(), c.fstate.p, st.size(), cudaMemcpyDeviceToHost));
+    for (int s : slots)
+        if (st[static_cast<std::size_t>(s)] == 0)
+            return "missing forecast for active workflow " + std::to_string(c.h_slot_wf[static_cast<std::size_t>(s)]);
+    for (int s : slots)
+        if (st[static_cast<std::size_t>(s)] == 2) return "forecast horizon shorter than the scoring horizon";
+    return "missing forecast";
+}
+
+std::string kvflow_message(Context& c, long long node) {
+    unsigned int off[2];
+    PBKV_CUDA(cudaMemcpy(off, c.acc_off.p + node, sizeof off, cudaMemcpyDeviceToHost));
+    std::vector<int> slots(off[1] - off[0]);
+    if (!slots.empty())
+        PBKV_CUDA(cudaMemcpy(slots.data(), c.acc_slot.p + off[0], slots.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<std::uint8_t> has(static_cast<std::size_t>(c.n_slots));
+    if (!has.empty()) PBKV_CUDA(cudaMemcpy(has.data(), c.rem_has.p, has.size(), cudaMemcpyDeviceToHost));
+    for (int s : slots)
+        if (!has[static_cast<std::size_t>(s)])
+            return "kvflow needs a static remaining sequence for workflow " +
+                   std::to_string(c.h_slot_wf[static_cast<std::size_t>(s)]);
+    return "kvflow needs a static remaining sequence";
+}
+
+}  // namespace
+
+namespace pbkv {
+void check_status(Context& c) {
+    PBKV_CUDA(cudaMemcpyAsync(c.hstatus.p, c.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c.stream));
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    DevStatus s = *c.hstatus.p;
+    if (s.code == 0) return;
+    std::string msg;
+    switch (s.kind) {
+        case kErrMissingForecast:
+        case kErrShortHorizon:
+            msg = missing_message(c, s.node);
+            break;
+        case kErrLastAccessRange:
+            msg = "pbkv: last_access >= 2^63 cannot be encoded in the candidate key";
+            break;
+        case kErrForecastNegative:
+            msg = "negative forecast probability";
+            break;
+        case kErrForecastSum:
+            msg = "forecast step does not sum to 1";
+            break;
+        case kErrKvflowMissing:
+            msg = kvflow_message(c, s.node);
+            break;
+        default:
+            msg = "device-side validation failed";
+    }
+    reset_status(c);
+    throw ApiError(s.code, msg);
+}
+}  // namespace pbkv
+
+namespace {
+
+void record(Context& c, int i) {
+    if (c.timing) PBKV_CUDA(cudaEventRecord(c.ev[i], c.stream));
+}
+
+void finish_timing(Context& c, int last_ev) {
+    if (!c.timing) return;
+    PBKV_CUDA(cudaEventSynchronize(c.ev[last_ev]));
+    for (int i = 0; i < 5; ++i) c.last_ms[i] = 0.f;
+    auto el = [&](int a, int b) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c.ev[a], c.ev[b]);
+        return ms;
+    };
+    if (last_ev >= 1) c.last_ms[0] = el(0, 1);
+    if (last_ev >= 2) c.last_ms[1] = el(1, 2);
+    if (last_ev >= 3) c.last_ms[2] = el(2, 3);
+    c.last_ms[4] = el(0, last_ev);
+}
+
+// ---- mirror -----------------------------------------------------------------
+void mirror_full(Context& c, const pbkv_tree_soa& s) {
+    need(s.n_nodes >= 1, "tree must contain the root");
+    need(s.parent && s.len && s.tier && s.retired && s.last_access && s.ever_tagged && s.acc_off,
+         "tree soa: missing required array");
+    need(s.n_entries == 0 || (s.acc_wf && s.acc_bits), "tree soa: missing access arrays");
+    need(s.n_nodes < INT_MAX, "tree too large for int32 node ids");
+    need(s.n_entries < static_cast<std::int64_t>(UINT_MAX), "too many access entries");
+    const std::int64_t n = s.n_nodes, E = s.n_entries;
+    std::vector<std::uint8_t> flags(static_cast<std::size_t>(n));
+    std::vector<unsigned int> off(static_cast<std::size_t>(n) + 1);
+    std::vector<int> slot(static_cast<std::size_t>(E));
+    std::vector<int> heavy;
+    std::vector<int> depth;
+    for (std::int64_t i = 0; i < n; ++i) {
+        if (s.tier[i] > PBKV_TIER_ABSENT) invalid("tree soa: bad tier value");
+        flags[static_cast<std::size_t>(i)] =
+            static_cast<std::uint8_t>(s.tier[i] | (s.retired[i] ? kFlagRetired : 0));
+        if (i > 0 && (s.parent[i] < 0 || s.parent[i] >= n)) invalid("tree soa: parent out of range");
+        std::int64_t a = s.acc_off[i], b = s.acc_off[i + 1];
+        if (a < 0 || b < a || b > E) invalid("tree soa: bad access offsets");
+        off[static_cast<std::size_t>(i)] = static_cast<unsigned int>(a);
+        for (std::int64_t e = a; e < b; ++e) {
+            if (e > a && s.acc_wf[e] <= s.acc_wf[e - 1]) invalid("tree soa: access entries must ascend by workflow id");
+            slot[static_cast<std::size_t>(e)] = slot_for(c, s.acc_wf[e]);
+        }
+        if (b - a > kHeavyEntries) heavy.push_back(static_cast<int>(i));
+    }
+    off[static_cast<std::size_t>(n)] = static_cast<unsigned int>(E);
+    const int* dep = s.depth;
+    if (!dep) {
+        depth.assign(static_cast<std::size_t>(n), -1);
+        depth[0] = 0;
+        std::vector<int> stack;
+        for (std::int64_t i = 1; i < n; ++i) {
+            int v = static_cast<int>(i);
+            while (depth[static_cast<std::size_t>(v)] < 0) {
+                stack.push_back(v);
+                v = s.parent[v];
+                if (stack.size() > static_cast<std::size_t>(n)) invalid("tree soa: parent cycle");
+            }
+            int d = depth[static_cast<std::size_t>(v)];
+            while (!stack.empty()) {
+                depth[static_cast<std::size_t>(stack.back())] = ++d;
+                stack.pop_back();
+            }
+        }
+        dep = depth.data();
+    }
+    int maxd = 0;
+    for (std::int64_t i = 0; i < n; ++i) maxd = std::max(maxd, dep[i]);
+    if (maxd >= (1 << 24)) invalid("tree deeper than 2^24 levels");
+
+    c.n = n;
+    c.E = E;
+    c.parent.reserve(n);
+    c.len.reserve(n);
+    c.ever.reserve(n);
+    c.depth.reserve(n);
+    c.flags.reserve(n);
+    c.last.reserve(n);
+    c.score.reserve(n);
+    c.acc_off.reserve(n + 1);
+    c.acc_slot.reserve(E + 1);
+    c.acc_bits.reserve(E + 1);
+    c.heavy.reserve(heavy.size() + 1);
+    cudaStream_t st = c.stream;
+    PBKV_CUDA(cudaMemcpyAsync(c.parent.p, s.parent, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.len.p, s.len, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.ever.p, s.ever_tagged, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.depth.p, dep, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.flags.p, flags.data(), n, cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.last.p, s.last_access, n * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
+    if (s.score)
+        PBKV_CUDA(cudaMemcpyAsync(c.score.p, s.score, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    else
+        PBKV_CUDA(cudaMemsetAsync(c.score.p, 0, n * sizeof(double), st));
+    PBKV_CUDA(cudaMemcpyAsync(c.acc_off.p, off.data(), (n + 1) * sizeof(unsigned int), cudaMemcpyHostToDevice, st));
+    if (E > 0) {
+        PBKV_CUDA(cudaMemcpyAsync(c.acc_slot.p, slot.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c.acc_bits.p, s.acc_bits, E * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
+    }
+    if (!heavy.empty())
+        PBKV_CUDA(cudaMemcpyAsync(c.heavy.p, heavy.data(), heavy.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    c.n_heavy = static_cast<std::int64_t>(heavy.size());
+    c.max_depth = maxd;
+    c.device_capacity = s.device_capacity;
+    c.device_used = s.device_used;
+    c.retired_device_tokens = s.retired_device_tokens;
+    c.host_capacity = s.host_capacity;
+    c.host_used = s.host_used;
+    ensure_scratch(c);
+    PBKV_CUDA(cudaStreamSynchronize(st));
+}
+
+struct SoaStore {
+    std::vector<int> parent, len, ever, dc, depth;
+    std::vector<std::uint8_t> tier, retired;
+    std::vector<std::uint64_t> last, bits;
+    std::vector<double> score;
+    std::vector<std::int64_t> off, wf;
+    pbkv_tree_soa soa{};
+    void fill(const RadixMirror& t) {
+        std::size_t n = t.node_count(), e = t.entry_count();
+        parent.resize(n);
+        len.resize(n);
+        ever.resize(n);
+        dc.resize(n);
+        depth.resize(n);
+        tier.resize(n);
+        retired.resize(n);
+        last.resize(n);
+        score.resize(n);
+        off.resize(n + 1);
+        wf.resize(e);
+        bits.resize(e);
+        t.export_soa(parent.data(), len.data(), tier.data(), retired.data(), last.data(), ever.data(), score.data(),
+                     dc.data(), depth.data(), off.data(), wf.data(), bits.data());
+        soa.n_nodes = static_cast<std::int64_t>(n);
+        soa.n_entries = static_cast<std::int64_t>(e);
+        soa.parent = parent.data();
+        soa.len = len.data();
+        soa.tier = tier.data();
+        soa.retired = retired.data();
+        soa.last_access = last.data();
+        soa.ever_tagged = ever.data();
+        soa.score = score.data();
+        soa.device_children = dc.data();
+        soa.depth = depth.data();
+        soa.acc_off = off.data();
+        soa.acc_wf = wf.data();
+        soa.acc_bits = bits.data();
+        soa.device_capacity = t.device_capacity();
+        soa.device_used = t.device_used();
+        soa.retired_device_tokens = t.retired_device_tokens();
+        soa.host_capacity = t.host_capacity();
+        soa.host_used = t.host_used();
+    }
+};
+
+// ---- stage 3 ------------------------------------------------------------------
+struct SelectOut {
+    std::int64_t n_victims = 0, freed = 0;
+    int shortfall = 0;
+};
+
+// Runs the selection; victims stay in c.vid_out[0..n_victims).
+SelectOut select_core(Context& c, int policy, int score_mode, std::int64_t needed, const int* locked_dev,
+                      std::int64_t n_locked) {
+    if (needed <= 0) invalid("eviction request must free a positive amount");
+    if (policy < PBKV_POLICY_LRU || policy > PBKV_POLICY_KVFLOW) invalid("unknown eviction policy");
+    if (policy == PBKV_POLICY_KVFLOW && !c.have_remaining) invalid("kvflow selected without static sequences");
+    if (score_mode != PBKV_SCORE_CACHED && score_mode != PBKV_SCORE_RECOMPUTE) throw ApiError(PBKV_EARG, "bad score mode");
+    need(c.n >= 1, "no tree mirrored");
+    SelectOut out;
+    long long* ctr = c.counters.p;
+    long long* hctr = c.hcounters.p;
+    record(c, 0);
+    reset_status(c);
+    PBKV_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(long long), c.stream));
+    const bool recompute = score_mode == PBKV_SCORE_RECOMPUTE && policy == PBKV_POLICY_HE;
+    if (recompute)
+        launch_score_all(c, c.score_rc.p, true, policy, false);
+    else
+        launch_keys_cached(c, policy);
+    record(c, 1);
+    launch_eff(c, locked_dev, n_locked);
+    launch_weights(c, ctr, recompute);  // raises missing forecasts only for eligible active nodes
+    PBKV_CUDA(cudaMemcpyAsync(hctr, ctr, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+    check_status(c);  // syncs
+    record(c, 2);
+    const std::int64_t n_heads = hctr[0];
+    const long long elig_tokens = hctr[1];
+    if (n_heads == 0) {
+        out.shortfall = 1;
+        record(c, 3);
+        finish_timing(c, 3);
+        return out;
+    }
+    c.hk_in.reserve(n_heads);
+    c.hk_out.reserve(n_heads);
+    c.wsorted.reserve(n_heads);
+    c.wscan.reserve(n_heads);
+    launch_gather_heads(c, n_heads);
+    cub_sort_heads(c, n_heads);
+    launch_head_weights(c, n_heads);
+    cub_scan_u64(c, c.wsorted.p, c.wscan.p, n_heads);
+    long long cut = n_heads - 1;
+    if (elig_tokens >= needed) {
+        long long init = LLONG_MAX;
+        PBKV_CUDA(cudaMemcpyAsync(ctr + 2, &init, sizeof init, cudaMemcpyHostToDevice, c.stream));
+        launch_find_cut(c, c.wscan.p, n_heads, needed, ctr + 2);
+        PBKV_CUDA(cudaMemcpyAsync(hctr + 2, ctr + 2, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+        PBKV_CUDA(cudaStreamSynchronize(c.stream));
+        cut = hctr[2];
+    }
+    // candidates = chains of heads [0, cut]
+    PBKV_CUDA(cudaMemsetAsync(ctr + 3, 0, sizeof(long long), c.stream));
+    c.vkey_in.reserve(c.n);
+    c.vid_in.reserve(c.n);
+    launch_victim_keys(c, cut, ctr + 3);
+    PBKV_CUDA(cudaMemcpyAsync(hctr + 3, ctr + 3, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    const std::int64_t n_cand = hctr[3];
+    c.vkey_out.reserve(n_cand);
+    c.vid_out.reserve(n_cand);
+    c.vscan.reserve(n_cand);
+    int end_bit = 24;
+    for (long long r = cut; r > 0; r >>= 1) ++end_bit;
+    cub_sort_pairs_u64(c, n_cand, std::min(end_bit, 64));
+    launch_victim_len(c, n_cand);
+    cub_scan_u64(c, c.vscan.p, c.vscan.p, n_cand);
+    long long j = n_cand - 1;
+    if (elig_tokens >= needed) {
+        long long init = LLONG_MAX;
+        PBKV_CUDA(cudaMemcpyAsync(ctr + 4, &init, sizeof init, cudaMemcpyHostToDevice, c.stream));
+        launch_find_cut(c, c.vscan.p, n_cand, needed, ctr + 4);
+        PBKV_CUDA(cudaMemcpyAsync(hctr + 4, ctr + 4, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+        PBKV_CUDA(cudaStreamSynchronize(c.stream));
+        j = hctr[4];
+    }
+    unsigned long long fr = 0;
+    PBKV_CUDA(cudaMemcpyAsync(&fr, c.vscan.p + j, sizeof fr, cudaMemcpyDeviceToHost, c.stream));
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    record(c, 3);
+    finish_timing(c, 3);
+    out.n_victims = j + 1;
+    out.freed = static_cast<std::int64_t>(fr);
+    out.shortfall = out.freed < needed ? 1 : 0;
+    return out;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+int pbkv_abi_version(void) { return PBKV_ABI_VERSION; }
+
+const char* pbkv_last_error(const pbkv_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int pbkv_device_count(int* out) {
+    return api(nullptr, [&] {
+        need(out != nullptr, "null out");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        int good = 0;
+        for (int d = 0; d < n; ++d) {
+            cudaDeviceProp p{};
+            if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++good;
+        }
+        *out = good;
+    });
+}
+
+int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
+    return api(nullptr, [&] {
+        need(out && cfg, "null argument");
+        *out = nullptr;
+        if (cfg->k < 1) invalid("lookahead horizon must be >= 1");
+        if (!(cfg->gamma > 0.0 && cfg->gamma < 1.0)) invalid("gamma must be in (0, 1)");
+        if (cfg->k > 32) throw ApiError(PBKV_EARG, "pbkv supports lookahead horizons up to 32");
+        if (cfg->num_agents < 1 || cfg->num_agents > 63) invalid("agent count must be in [1, 63]");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            throw ApiError(PBKV_ECUDA, "no CUDA device visible (pbkv has no CPU fallback)");
+        }
+        need(cfg->device >= 0 && cfg->device < n, "device ordinal out of range");
+        cudaDeviceProp prop{};
+        PBKV_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
+        if (prop.major != 10)
+            throw ApiError(PBKV_ECUDA, "pbkv is built for sm_100a (B200); device " + std::string(prop.name) +
+                                           " is not compute capability 10.x");
+        auto c = std::make_unique<pbkv_ctx>();
+        c->device = cfg->device;
+        c->K = cfg->k;
+        c->gamma = cfg->gamma;
+        c->A = cfg->num_agents;
+        c->V1 = cfg->num_agents + 1;
+        PBKV_CUDA(cudaSetDevice(c->device));
+        PBKV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev) PBKV_CUDA(cudaEventCreate(&e));
+        c->counters.reserve(16);
+        c->status.reserve(1);
+        c->hcounters.reserve(16);
+        c->hstatus.reserve(1);
+        c->P.reserve(64);
+        c->gs.reserve(64);
+        c->fstate.reserve(64);
+        c->rem_has.reserve(64);
+        reset_status(*c);
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        *out = c.release();
+    });
+}
+
+int pbkv_ctx_destroy(pbkv_ctx* c) {
+    if (!c) return PBKV_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    auto rel = [](auto& b) { b.release(); };
+    rel(c->parent), rel(c->len), rel(c->ever), rel(c->depth), rel(c->flags), rel(c->last), rel(c->score);
+    rel(c->acc_off), rel(c->acc_slot), rel(c->acc_bits), rel(c->heavy), rel(c->P), rel(c->gs), rel(c->fstate);
+    rel(c->fstage), rel(c->fstage_slot), rel(c->rem_off), rel(c->rem_seq), rel(c->rem_has), rel(c->score_rc);
+    rel(c->keys), rel(c->eff), rel(c->sublock), rel(c->missing), rel(c->W), rel(c->heads), rel(c->hk_in);
+    rel(c->hk_out), rel(c->wsorted), rel(c->wscan), rel(c->rank), rel(c->vkey_in), rel(c->vkey_out), rel(c->vid_in);
+    rel(c->vid_out), rel(c->vscan), rel(c->locked), rel(c->ids), rel(c->vals), rel(c->ck_in), rel(c->ck_out);
+    rel(c->cv_in), rel(c->cv_out), rel(c->sel), rel(c->cub_tmp), rel(c->counters), rel(c->status);
+    rel(c->hcounters), rel(c->hstatus), rel(c->hids), rel(c->hvals);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return PBKV_OK;
+}
+
+int pbkv_ctx_sync(pbkv_ctx* c) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_ctx_stream(pbkv_ctx* c, void** s) {
+    return api(c, [&] {
+        need(c && s, "null argument");
+        *s = c->stream;
+    });
+}
+
+int pbkv_ctx_timings(pbkv_ctx* c, float* ms5) {
+    return api(c, [&] {
+        need(c && ms5, "null argument");
+        for (int i = 0; i < 5; ++i) ms5[i] = c->last_ms[i];
+    });
+}
+
+int pbkv_ctx_set_timing(pbkv_ctx* c, int enabled) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        c->timing = enabled != 0;
+    });
+}
+
+int pbkv_mirror_full(pbkv_ctx* c, const pbkv_tree_soa* soa) {
+    return api(c, [&] {
+        need(c && soa, "null argument");
+        set_device(*c);
+        mirror_full(*c, *soa);
+    });
+}
+
+int pbkv_mirror_tree(pbkv_ctx* c, pbkv_tree* t) {
+    return api(c, [&] {
+        need(c && t, "null argument");
+        set_device(*c);
+        SoaStore st;
+        st.fill(t->tree);
+        mirror_full(*c, st.soa);
+        t->tree.clear_dirty();
+    });
+}
+
+int pbkv_mirror_sync(pbkv_ctx* c, pbkv_tree* t) {
+    // incremental delta upload is a later step; a full re-mirror is exact
+    return pbkv_mirror_tree(c, t);
+}
+
+int pbkv_mirror_set_scores(pbkv_ctx* c, const int32_t* ids, const double* scores, int64_t n) {
+    return api(c, [&] {
+        need(c && (n == 0 || (ids && scores)), "null argument");
+        set_device(*c);
+        for (int64_t i = 0; i < n; ++i) need(ids[i] >= 0 && ids[i] < c->n, "node id out of range");
+        // small batches: individual copies are fine (the simulator refreshes a handful of nodes)
+        for (int64_t i = 0; i < n; ++i)
+            PBKV_CUDA(cudaMemcpyAsync(c->score.p + ids[i], scores + i, sizeof(double), cudaMemcpyHostToDevice,
+                                      c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_mirror_node_count(pbkv_ctx* c, int64_t* n_nodes, int64_t* n_entries) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        if (n_nodes) *n_nodes = c->n;
+        if (n_entries) *n_entries = c->E;
+    });
+}
+
+int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, int outcomes, const double* p) {
+    return api(c, [&] {
+        need(c && (n == 0 || (wf && p)), "null argument");
+        if (horizon < 1) invalid("forecast horizon must be >= 1");
+        if (outcomes < 2) invalid("forecast needs at least one agent plus END");
+        if (outcomes != c->V1) invalid("forecast outcomes do not match the context's agent count");
+        if (n == 0) return;
+        set_device(*c);
+        std::vector<long long> slots(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) slots[static_cast<std::size_t>(i)] = slot_for(*c, wf[i]);
+        const std::size_t per = static_cast<std::size_t>(horizon) * static_cast<std::size_t>(outcomes);
+        c->fstage.reserve(static_cast<std::size_t>(n) * per);
+        c->fstage_slot.reserve(static_cast<std::size_t>(n));
+        reset_status(*c);
+        PBKV_CUDA(cudaMemcpyAsync(c->fstage.p, p, static_cast<std::size_t>(n) * per * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+        PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots.data(), slots.size() * sizeof(long long),
+                                  cudaMemcpyHostToDevice, c->stream));
+        launch_forecast_prepare(*c, c->fstage.p, c->fstage_slot.p, n, horizon);
+        check_status(*c);
+    });
+}
+
+int pbkv_forecast_drop(pbkv_ctx* c, const int64_t* wf, int64_t n) {
+    return api(c, [&] {
+        need(c && (n == 0 || wf), "null argument");
+        set_device(*c);
+        for (int64_t i = 0; i < n; ++i) {
+            auto it = c->slot_of.find(wf[i]);
+            if (it == c->slot_of.end()) continue;
+            PBKV_CUDA(cudaMemsetAsync(c->fstate.p + it->second, 0, 1, c->stream));
+        }
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_forecast_clear(pbkv_ctx* c) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        set_device(*c);
+        if (c->n_slots > 0) PBKV_CUDA(cudaMemsetAsync(c->fstate.p, 0, static_cast<std::size_t>(c->n_slots), c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_score_all(pbkv_ctx* c, double* scores_out) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        need(c->n >= 1, "no tree mirrored");
+        set_device(*c);
+        reset_status(*c);
+        record(*c, 0);
+        launch_score_all(*c, c->score_rc.p, false, PBKV_POLICY_HE, true);
+        record(*c, 1);
+        check_status(*c);
+        finish_timing(*c, 1);
+        if (scores_out)
+            PBKV_CUDA(cudaMemcpy(scores_out, c->score_rc.p, static_cast<std::size_t>(c->n) * sizeof(double),
+                                 cudaMemcpyDeviceToHost));
+    });
+}
+
+static int score_ids_impl(pbkv_ctx* c, const int32_t* ids, int64_t n, double* out, bool value_only) {
+    return api(c, [&] {
+        need(c && (n == 0 || (ids && out)), "null argument");
+        if (n == 0) return;
+        set_device(*c);
+        for (int64_t i = 0; i < n; ++i) need(ids[i] >= 0 && ids[i] < c->n, "node id out of range");
+        c->ids.reserve(static_cast<std::size_t>(n));
+        c->vals.reserve(static_cast<std::size_t>(n));
+        reset_status(*c);
+        PBKV_CUDA(cudaMemcpyAsync(c->ids.p, ids, n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        launch_score_ids(*c, c->ids.p, n, c->score_rc.p, value_only);
+        check_status(*c);
+        launch_gather_f64(*c, c->score_rc.p, c->ids.p, n, c->vals.p);
+        PBKV_CUDA(cudaMemcpyAsync(out, c->vals.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_score_nodes(pbkv_ctx* c, const int32_t* ids, int64_t n, double* out) {
+    return score_ids_impl(c, ids, n, out, false);
+}
+
+int pbkv_value_nodes(pbkv_ctx* c, const int32_t* ids, int64_t n, double* out) {
+    return score_ids_impl(c, ids, n, out, true);
+}
+
+int pbkv_select(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const int32_t* locked, int64_t n_locked,
+                int32_t* victims, int64_t cap, int64_t* n_victims, int64_t* freed, int* shortfall) {
+    return api(c, [&] {
+        need(c && n_victims && freed && shortfall, "null argument");
+        need(n_locked == 0 || locked, "null locked array");
+        set_device(*c);
+        c->locked.reserve(static_cast<std::size_t>(n_locked) + 1);
+        if (n_locked > 0)
+            PBKV_CUDA(cudaMemcpyAsync(c->locked.p, locked, n_locked * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        SelectOut o = select_core(*c, policy, score_mode, needed, c->locked.p, n_locked);
+        *n_victims = o.n_victims;
+        *freed = o.freed;
+        *shortfall = o.shortfall;
+        if (o.n_victims > cap) throw ApiError(PBKV_EARG, "victim capacity too small");
+        if (o.n_victims > 0) {
+            need(victims != nullptr, "null victims array");
+            PBKV_CUDA(cudaMemcpyAsync(victims, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToHost,
+                                      c->stream));
+            PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int pbkv_select_dev(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const int32_t* locked_dev,
+                    int64_t n_locked, int32_t* victims_dev, int64_t cap, int64_t* result_dev) {
+    return api(c, [&] {
+        need(c && result_dev, "null argument");
+        need(n_locked == 0 || locked_dev, "null locked array");
+        set_device(*c);
+        SelectOut o = select_core(*c, policy, score_mode, needed, locked_dev, n_locked);
+        if (o.n_victims > cap) throw ApiError(PBKV_EARG, "victim capacity too small");
+        if (o.n_victims > 0) {
+            need(victims_dev != nullptr, "null victims array");
+            PBKV_CUDA(cudaMemcpyAsync(victims_dev, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToDevice,
+                                      c->stream));
+        }
+        long long* h = c->hcounters.p + 8;
+        h[0] = o.n_victims;
+        h[1] = o.freed;
+        h[2] = o.shortfall;
+        PBKV_CUDA(cudaMemcpyAsync(result_dev, h, 3 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_set_remaining(pbkv_ctx* c, const int64_t* wf, int64_t n_wf, const int64_t* seq_off, const int32_t* seq) {
+    return api(c, [&] {
+        need(c && (n_wf == 0 || (wf && seq_off)), "null argument");
+        set_device(*c);
+        std::vector<int> slots(static_cast<std::size_t>(n_wf));
+        for (int64_t i = 0; i < n_wf; ++i) slots[static_cast<std::size_t>(i)] = slot_for(*c, wf[i]);
+        // per-slot CSR (slots without a sequence get an empty range + has=0)
+        const std::size_t ns = static_cast<std::size_t>(c->n_slots);
+        std::vector<int> off(ns + 1, 0), cnt(ns, 0);
+        std::vector<std::uint8_t> has(ns, 0);
+        for (int64_t i = 0; i < n_wf; ++i) {
+            std::size_t s = static_cast<std::size_t>(slots[static_cast<std::size_t>(i)]);
+            cnt[s] = static_cast<int>(seq_off[i + 1] - seq_off[i]);
+            has[s] = 1;
+        }
+        for (std::size_t s = 0; s < ns; ++s) off[s + 1] = off[s] + cnt[s];
+        std::vector<int> flat(static_cast<std::size_t>(off[ns]) + 1);
+        for (int64_t i = 0; i < n_wf; ++i) {
+            std::size_t s = static_cast<std::size_t>(slots[static_cast<std::size_t>(i)]);
+            for (int64_t k = seq_off[i]; k < seq_off[i + 1]; ++k)
+                flat[static_cast<std::size_t>(off[s] + (k - seq_off[i]))] = seq[k];
+        }
+        c->rem_off.reserve(ns + 1);
+        c->rem_seq.reserve(flat.size());
+        PBKV_CUDA(cudaMemcpyAsync(c->rem_off.p, off.data(), (ns + 1) * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        PBKV_CUDA(cudaMemcpyAsync(c->rem_seq.p, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                  c->stream));
+        if (ns) PBKV_CUDA(cudaMemcpyAsync(c->rem_has.p, has.data(), ns, cudaMemcpyHostToDevice, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        c->have_remaining = true;
+    });
+}
+
+int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double rho, int32_t* cand_ids,
+                       double* cand_values, int64_t cand_cap, int32_t* selected, int64_t sel_cap,
+                       pbkv_prefetch_plan* plan) {
+    return api(c, [&] {
+        need(c && plan, "null argument");
+        need(c->n >= 1, "no tree mirrored");
+        std::int64_t extra = 0;
+        if (!(rho < 0.0)) {
+            if (rho < 0.0 || rho > 1.0 || rho != rho) invalid("rho must be in [0, 1]");
+            extra = static_cast<std::int64_t>(rho * static_cast<double>(c->device_capacity));
+        }
+        set_device(*c);
+        std::memset(plan, 0, sizeof *plan);
+        plan->budget_space = (c->device_capacity - c->device_used) + c->retired_device_tokens;
+        plan->budget_bw = bandwidth * static_cast<std::int64_t>(step_duration);
+        plan->displacement_budget = extra;
+        const long long budget = std::min(plan->budget_space + extra, plan->budget_bw);
+        long long* ctr = c->counters.p;
+        long long* hctr = c->hcounters.p;
+        c->ck_in.reserve(c->n);
+        c->cv_in.reserve(c->n);
+        record(*c, 0);
+        reset_status(*c);
+        PBKV_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(long long), c->stream));
+        launch_prefetch_candidates(*c, ctr);
+        PBKV_CUDA(cudaMemcpyAsync(hctr, ctr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaMemcpyAsync(c->hstatus.p, c->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        if (c->hstatus.p->code != 0) {
+            launch_prefetch_err_id(*c);
+            check_status(*c);
+        }
+        const std::int64_t nc = hctr[0];
+        plan->n_candidates = nc;
+        if (nc == 0) {
+            record(*c, 1);
+            finish_timing(*c, 1);
+            return;
+        }
+        c->ck_out.reserve(nc);
+        c->cv_out.reserve(nc);
+        c->sel.reserve(nc);
+        cub_sort_cands(*c, nc);
+        launch_prefetch_greedy(*c, nc, budget, ctr);
+        PBKV_CUDA(cudaMemcpyAsync(hctr + 1, ctr + 1, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        record(*c, 1);
+        finish_timing(*c, 1);
+        plan->n_selected = hctr[1];
+        plan->selected_tokens = hctr[2];
+        if (cand_cap > 0 && (cand_ids || cand_values)) {
+            std::int64_t m = std::min<std::int64_t>(cand_cap, nc);
+            std::vector<CandKey> ck(static_cast<std::size_t>(m));
+            PBKV_CUDA(cudaMemcpy(ck.data(), c->ck_out.p, m * sizeof(CandKey), cudaMemcpyDeviceToHost));
+            if (cand_ids)
+                for (std::int64_t i = 0; i < m; ++i) cand_ids[i] = static_cast<int32_t>(ck[static_cast<std::size_t>(i)].id);
+            if (cand_values) PBKV_CUDA(cudaMemcpy(cand_values, c->cv_out.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        if (sel_cap > 0 && selected) {
+            std::int64_t m = std::min<std::int64_t>(sel_cap, plan->n_selected);
+            if (m > 0) PBKV_CUDA(cudaMemcpy(selected, c->sel.p, m * sizeof(int), cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+// ---- host tree ------------------------------------------------------------------
+int pbkv_tree_create(pbkv_tree** out, int64_t device_capacity, int64_t host_capacity) {
+    return api(nullptr, [&] {
+        need(out != nullptr, "null out");
+        *out = new pbkv_tree(device_capacity, host_capacity);
+    });
+}
+
+int pbkv_tree_destroy(pbkv_tree* t) {
+    delete t;
+    return PBKV_OK;
+}
+
+int pbkv_tree_apply_ops(pbkv_tree* t, const int64_t* words, int64_t n_words) {
+    return tree_api(t, [&] {
+        need(n_words == 0 || words, "null words");
+        apply_ops(t->tree, words, n_words);
+    });
+}
+
+int pbkv_tree_synth(pbkv_tree* t, const pbkv_synth_params* p) {
+    return tree_api(t, [&] {
+        need(p != nullptr, "null params");
+        SynthParams sp;
+        sp.n_nodes = p->n_nodes;
+        sp.n_workflows = p->n_workflows;
+        sp.agents = p->agents;
+        sp.group_size = p->group_size;
+        sp.shared_len = p->shared_len;
+        sp.group_len = p->group_len;
+        sp.alphabet = p->alphabet;
+        sp.max_rand_len = p->max_rand_len;
+        sp.retired_frac = p->retired_frac;
+        sp.host_every = p->host_every;
+        sp.seed = p->seed;
+        synth_build(t->tree, sp);
+    });
+}
+
+int pbkv_tree_shape(pbkv_tree* t, pbkv_tree_soa* s) {
+    return tree_api(t, [&] {
+        need(s != nullptr, "null soa");
+        s->n_nodes = static_cast<std::int64_t>(t->tree.node_count());
+        s->n_entries = static_cast<std::int64_t>(t->tree.entry_count());
+        s->device_capacity = t->tree.device_capacity();
+        s->device_used = t->tree.device_used();
+        s->retired_device_tokens = t->tree.retired_device_tokens();
+        s->host_capacity = t->tree.host_capacity();
+        s->host_used = t->tree.host_used();
+    });
+}
+
+int pbkv_tree_export(pbkv_tree* t, pbkv_tree_soa* s) {
+    return tree_api(t, [&] {
+        need(s != nullptr, "null soa");
+        t->tree.export_soa(s->parent, s->len, s->tier, s->retired, s->last_access, s->ever_tagged, s->score,
+                           s->device_children, s->depth, s->acc_off, s->acc_wf, s->acc_bits);
+    });
+}
+
+int pbkv_tree_touched(pbkv_tree* t, int64_t wf, int32_t* ids, int64_t cap, int64_t* n) {
+    return tree_api(t, [&] {
+        need(n != nullptr, "null out");
+        const std::vector<int>* v = t->tree.touched_nodes(wf);
+        *n = v ? static_cast<int64_t>(v->size()) : 0;
+        if (v && ids)
+            for (std::size_t i = 0; i < v->size() && static_cast<int64_t>(i) < cap; ++i) ids[i] = (*v)[i];
+    });
+}
+
+}  // extern "C"

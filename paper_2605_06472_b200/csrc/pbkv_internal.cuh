@@ -1,0 +1,245 @@
+// Internal definitions shared by the pbkv CUDA translation units.
+//
+// Device data layout.  Per node (SoA, index = node id):
+//   parent i32, len i32, flags u8 (bits 0-1 tier, bit 2 retired),
+//   last_access u64, ever_tagged i32, score f64 (cached, cache.hpp:61),
+//   depth i32, acc_off u32 (CSR, n+1)
+// Per access entry (CSR, WorkflowId-ascending within a node, cache.hpp:64):
+//   slot i32 (forecast slot of the WorkflowId), bits u64
+// Per forecast slot: P f64[K][V1] (first K steps), gs f64[K] = gamma^k * s(k),
+//   state u8 (0 missing, 1 ok, 2 horizon < K).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/pbkv.h"
+
+namespace pbkv {
+
+constexpr std::uint8_t kFlagTierMask = 0x3;
+constexpr std::uint8_t kFlagRetired = 0x4;
+constexpr int kHeavyEntries = 32;  // nodes with more access entries go to the block-per-node path
+
+// first-error-wins device status (kernels never throw)
+struct DevStatus {
+    int code;            // 0 ok, else PBKV_E*
+    int kind;            // which check failed (see kErr*)
+    long long node;      // smallest offending node id (atomicMin)
+    long long aux;       // extra info (e.g. last_access for host ordering)
+};
+enum : int {
+    kErrNone = 0,
+    kErrMissingForecast = 1,
+    kErrShortHorizon = 2,
+    kErrLastAccessRange = 3,
+    kErrForecastNegative = 4,
+    kErrForecastSum = 5,
+    kErrKvflowMissing = 6,
+};
+
+struct ApiError : std::runtime_error {
+    int status;
+    ApiError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define PBKV_CUDA(call)                                                                          \
+    do {                                                                                         \
+        cudaError_t pbkv_e_ = (call);                                                            \
+        if (pbkv_e_ != cudaSuccess)                                                              \
+            throw ::pbkv::ApiError(PBKV_ECUDA, std::string(#call) + ": " + cudaGetErrorString(pbkv_e_)); \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    std::size_t cap = 0;  // elements
+    void reserve(std::size_t n) {
+        if (n <= cap) return;
+        std::size_t c = cap ? cap : 1024;
+        while (c < n) c *= 2;
+        T* np = nullptr;
+        if (cudaMalloc(&np, c * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            throw ApiError(PBKV_ENOMEM, "device allocation failed");
+        }
+        if (p) cudaFree(p);
+        p = np;
+        cap = c;
+    }
+    // grow keeping the first `keep` elements
+    void grow_keep(std::size_t n, std::size_t keep, cudaStream_t s) {
+        if (n <= cap) return;
+        std::size_t c = cap ? cap : 1024;
+        while (c < n) c *= 2;
+        T* np = nullptr;
+        if (cudaMalloc(&np, c * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            throw ApiError(PBKV_ENOMEM, "device allocation failed");
+        }
+        if (p && keep) PBKV_CUDA(cudaMemcpyAsync(np, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        if (p) {
+            cudaStreamSynchronize(s);
+            cudaFree(p);
+        }
+        p = np;
+        cap = c;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+template <class T>
+struct PinBuf {
+    T* p = nullptr;
+    std::size_t cap = 0;
+    void reserve(std::size_t n) {
+        if (n <= cap) return;
+        std::size_t c = cap ? cap : 1024;
+        while (c < n) c *= 2;
+        T* np = nullptr;
+        if (cudaMallocHost(&np, c * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            throw ApiError(PBKV_ENOMEM, "pinned allocation failed");
+        }
+        if (p) cudaFreeHost(p);
+        p = np;
+        cap = c;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// 161-bit candidate key of policies.hpp:40-48 packed as (w0, w1) + node id:
+//   w0 = cls << 63 | enc(rank) >> 1,  w1 = (enc(rank) & 1) << 63 | last_access
+// enc() is the order-preserving map of a double onto uint64 (-0.0 folded
+// into +0.0 because std::tie compares them equal).  Lexicographic
+// (w0, w1, id) order == std::tie(cls, rank, last_access, id) order.
+struct Key2 {
+    unsigned long long w0, w1;
+};
+
+// Sort record of a head
+struct HeadKey {
+    unsigned long long w0, w1;
+    unsigned int id;
+};
+
+// Sort record of a prefetch candidate: value descending, id ascending
+struct CandKey {
+    unsigned long long vdesc;
+    unsigned int id;
+};
+
+struct Context {
+    int device = 0;
+    int K = 3;
+    double gamma = 0.7;
+    int A = 1;    // agents
+    int V1 = 2;   // outcomes
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    // ---- mirror -------------------------------------------------------------
+    std::int64_t n = 0, E = 0;
+    DevBuf<int> parent, len, ever, depth;
+    DevBuf<std::uint8_t> flags;
+    DevBuf<unsigned long long> last;
+    DevBuf<double> score;        // cached (mirrored) score
+    DevBuf<unsigned int> acc_off;
+    DevBuf<int> acc_slot;
+    DevBuf<unsigned long long> acc_bits;
+    DevBuf<int> heavy;           // nodes with > kHeavyEntries entries
+    std::int64_t n_heavy = 0;
+    std::int64_t device_capacity = 0, device_used = 0, retired_device_tokens = 0, host_capacity = 0,
+                 host_used = 0;
+    int max_depth = 0;
+    std::vector<std::int64_t> h_slot_wf;  // slot -> WorkflowId
+    std::unordered_map<std::int64_t, int> slot_of;
+
+    // ---- forecasts ----------------------------------------------------------
+    DevBuf<double> P;   // [slots][K][V1]
+    DevBuf<double> gs;  // [slots][K]
+    DevBuf<std::uint8_t> fstate;
+    std::int64_t n_slots = 0;
+    DevBuf<double> fstage;  // staging for uploads (H rows)
+    DevBuf<long long> fstage_slot;
+
+    // ---- kvflow remaining sequences (per slot CSR) --------------------------
+    DevBuf<int> rem_off;   // [slots+1]
+    DevBuf<int> rem_seq;
+    DevBuf<std::uint8_t> rem_has;  // per slot
+    bool have_remaining = false;
+
+    // ---- scratch --------------------------------------------------------------
+    DevBuf<double> score_rc;       // recomputed scores
+    DevBuf<Key2> keys;
+    DevBuf<int> eff;
+    DevBuf<int> sublock;
+    DevBuf<std::uint8_t> missing;
+    DevBuf<unsigned long long> W;
+    DevBuf<int> heads;
+    DevBuf<HeadKey> hk_in, hk_out;
+    DevBuf<unsigned long long> wsorted, wscan;
+    DevBuf<int> rank;
+    DevBuf<unsigned long long> vkey_in, vkey_out;
+    DevBuf<int> vid_in, vid_out;
+    DevBuf<unsigned long long> vscan;
+    DevBuf<int> locked;
+    DevBuf<int> ids;
+    DevBuf<double> vals;
+    DevBuf<CandKey> ck_in, ck_out;
+    DevBuf<double> cv_in, cv_out;  // candidate values carried with keys
+    DevBuf<int> sel;
+    DevBuf<unsigned char> cub_tmp;
+    DevBuf<long long> counters;    // small device scalars
+    DevBuf<DevStatus> status;
+    PinBuf<long long> hcounters;
+    PinBuf<DevStatus> hstatus;
+    PinBuf<int> hids;
+    PinBuf<double> hvals;
+
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[6] = {};
+    float last_ms[5] = {0, 0, 0, 0, 0};
+};
+
+// ---- kernels / launchers (implemented in the .cu files) ------------------------
+void launch_forecast_prepare(Context& c, const double* stage, const long long* slots, std::int64_t n, int H);
+void launch_score_all(Context& c, double* out_dev, bool write_keys, int policy, bool want_missing);
+void launch_score_ids(Context& c, const int* ids_dev, std::int64_t n, double* out_dev, bool value_only);
+void launch_keys_cached(Context& c, int policy);
+void launch_eff(Context& c, const int* locked_dev, std::int64_t n_locked);
+void launch_weights(Context& c, long long* counters_dev, bool he_recompute);
+void launch_prefetch_candidates(Context& c, long long* counters_dev);
+void launch_prefetch_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev);
+void reset_status(Context& c);
+void check_status(Context& c);  // syncs and throws on a device-side error
+
+std::size_t cub_sort_heads_bytes(std::int64_t n);
+void cub_sort_heads(Context& c, std::int64_t n);
+std::size_t cub_scan_bytes(std::int64_t n);
+void cub_scan_u64(Context& c, const unsigned long long* in, unsigned long long* out, std::int64_t n);
+std::size_t cub_sort_pairs_bytes(std::int64_t n);
+void cub_sort_pairs_u64(Context& c, std::int64_t n, int end_bit);
+std::size_t cub_sort_cands_bytes(std::int64_t n);
+void cub_sort_cands(Context& c, std::int64_t n);
+
+inline unsigned int grid_for(std::int64_t n, int block) {
+    std::int64_t g = (n + block - 1) / block;
+    return static_cast<unsigned int>(g < 1 ? 1 : g);
+}
+
+}  // namespace pbkv

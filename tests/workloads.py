@@ -1,0 +1,115 @@
+"""Seeded workload generators shared by the parity tests and bench.py.
+
+Random small trees follow SURVEY.md App. A.3 (random inserts and matches over
+a small alphabet, several workflows, terminations, demotions, coarse
+forecasts to force exact score ties, random locked sets).  Everything is a
+pure function of the seed.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2605_06472_b200.ops import OpStream
+
+
+def random_forecasts(rng: np.random.Generator, n: int, K: int, V1: int, coarse: bool = False) -> np.ndarray:
+    """iid-exponential simplex rows (rng.hpp:58-67 / theory.hpp:225-233 shape).
+    coarse=True draws from a handful of one-hot / half-half rows so that many
+    nodes tie exactly on score."""
+    if not coarse:
+        x = -np.log1p(-rng.random((n, K, V1)))
+        return x / x.sum(axis=2, keepdims=True)
+    P = np.zeros((n, K, V1))
+    for i in range(n):
+        for k in range(K):
+            a = int(rng.integers(V1))
+            b = int(rng.integers(V1))
+            if a == b:
+                P[i, k, a] = 1.0
+            else:
+                P[i, k, a] = 0.5
+                P[i, k, b] = 0.5
+    return P
+
+
+def random_tree_ops(rng: np.random.Generator, n_ops: int = 40, n_wf: int = 6, agents: int = 4, alphabet: int = 3,
+                    max_len: int = 7, term_frac: float = 0.3, demote_frac: float = 0.15,
+                    host_capacity: int | None = None):
+    """Build an op stream by simulating enough of the tree to only emit legal
+    demotions.  Returns (ops, live_workflows).  The tree itself is built by the
+    caller (HostTree or RefTree) from the op stream."""
+    ops = OpStream()
+    live = list(range(n_wf))
+    for _ in range(n_ops):
+        w = int(rng.choice(live)) if live else 0
+        L = int(rng.integers(1, max_len + 1))
+        toks = [int(t) for t in rng.integers(0, alphabet, size=L)]
+        agent = int(rng.integers(agents))
+        if rng.random() < 0.7:
+            ops.insert(toks, w, agent)
+        else:
+            ops.match(toks, w, agent)
+    n_term = int(round(term_frac * n_wf))
+    terminated = [int(w) for w in rng.choice(n_wf, size=n_term, replace=False)] if n_term else []
+    for w in terminated:
+        ops.terminate(w)
+    live = [w for w in range(n_wf) if w not in terminated]
+    return ops, live
+
+
+def legal_demotions(soa, rng: np.random.Generator, frac: float, rounds: int = 2) -> list[int]:
+    """Pick device leaves to demote (each must be a leaf at its turn): repeated
+    leaf peeling on the exported SoA image."""
+    n = soa.n_nodes
+    tier = soa.tier.copy()
+    parent = soa.parent
+    out: list[int] = []
+    for _ in range(rounds):
+        dc = np.zeros(n, dtype=np.int64)
+        dev = (tier == 0)
+        dev[0] = False
+        np.add.at(dc, parent[1:][dev[1:]], 1)
+        leaves = [i for i in range(1, n) if tier[i] == 0 and dc[i] == 0]
+        rng.shuffle(leaves)
+        k = int(round(frac * len(leaves)))
+        for i in leaves[:k]:
+            tier[i] = 1
+            out.append(i)
+    return out
+
+
+def random_locked(soa, rng: np.random.Generator, frac: float = 0.08) -> list[int]:
+    n = soa.n_nodes
+    if n <= 1:
+        return []
+    k = int(rng.binomial(n - 1, frac))
+    return sorted(set(int(x) for x in rng.integers(1, n, size=k)))
+
+
+def pinned_paths(soa, rng: np.random.Generator, frac: float = 0.01) -> list[int]:
+    """Ancestors of a fraction of device leaves plus the leaves (the image of
+    Simulator::pinned_nodes, simulator.hpp:437-446)."""
+    n = soa.n_nodes
+    tier, parent = soa.tier, soa.parent
+    dev = tier == 0
+    dc = np.zeros(n, dtype=np.int64)
+    m = dev.copy()
+    m[0] = False
+    np.add.at(dc, parent[1:][m[1:]], 1)
+    leaves = np.nonzero(m & (dc == 0))[0]
+    if leaves.size == 0:
+        return []
+    k = max(1, int(frac * leaves.size))
+    pick = rng.choice(leaves, size=min(k, leaves.size), replace=False)
+    locked = set()
+    for v in pick.tolist():
+        while v > 0:
+            if v in locked:
+                break
+            locked.add(v)
+            v = int(parent[v])
+    return sorted(locked)
+
+
+def workflows_of(soa) -> list[int]:
+    return sorted(set(soa.acc_wf[: soa.n_entries].tolist()))
