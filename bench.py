@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the PBKV decision hot path on B200 (BASELINE.json metric:
+"cache nodes scored+ranked/sec and p99 eviction-decision latency").
+
+One step = one eviction decision over the whole tree, resident in HBM:
+Eq. 2 recomputed for every node from the resident forecasts (stage 2), the
+hierarchical candidate keys, locked-subtree marks and subtree-max reduction,
+and the token-weighted cut + victim order (stage 3) -- pbkv_select_dev in
+PBKV_SCORE_RECOMPUTE mode.  Workload (configs[2]): 1M-node radix tree x 4096
+workflows x K=8, 30% retired, A=16, need = 1% of device tokens, 1% of leaves
+pinned.  `value` = nodes scored+ranked per second (all
+ranks); `e2e` = the same through the host C ABI (forecast upload from pinned
+host memory + pbkv_select with host locked list and host victim output).
+
+--impl reference times the reference's own CPU policy code (oracle/_ref,
+compiled from /root/reference) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for p in (ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+import numpy as np  # noqa: E402
+
+METRIC = "cache nodes scored+ranked/sec and p99 eviction-decision latency"
+CONFIGS = {
+    # name: (n_nodes, n_workflows, K)
+    "c2": (10_000, 256, 4),
+    "c3": (1_000_000, 4096, 8),
+}
+AGENTS = 16
+GAMMA = 0.7
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--needed-frac", type=float, default=0.01)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-decisions", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def workload(cfg: str, rank: int):
+    """Synthetic tree + forecasts + pinned set, deterministic per (config, rank)."""
+    import workloads as WL
+    from paper_2605_06472_b200.api import HostTree
+
+    n_nodes, n_wf, K = CONFIGS[cfg]
+    t = HostTree()
+    t0 = time.perf_counter()
+    t.synth(n_nodes=n_nodes, n_workflows=n_wf, agents=AGENTS, seed=12345 + rank)
+    build_s = time.perf_counter() - t0
+    soa = t.export()
+    rng = np.random.default_rng(12345 + rank)
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, K, AGENTS + 1)
+    locked = np.array(WL.pinned_paths(soa, rng, 0.01), dtype=np.int32)
+    return t, soa, wf, P, locked, K, build_s
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is None:
+            self.result = {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        self.result = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                       "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: int = 0):
+    """The reference policy code (oracle/_ref) on the same workload: per
+    decision, refresh every node's score (refresh_nodes, scoring.hpp:95) and
+    select_victims_hierarchical (policies.hpp:108)."""
+    import workloads as WL
+    from oracle import RefTree, have_ref
+    from paper_2605_06472_b200._abi import POLICY_HE
+
+    if not have_ref():
+        return None
+    n_nodes, n_wf, K = CONFIGS[cfg]
+    t = RefTree()
+    t0 = time.perf_counter()
+    t.synth(n_nodes=n_nodes, n_workflows=n_wf, agents=AGENTS, seed=12345 + rank)
+    build_s = time.perf_counter() - t0
+    soa = t.export()
+    rng = np.random.default_rng(12345 + rank)
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, K, AGENTS + 1)
+    locked = WL.pinned_paths(soa, rng, 0.01)
+    t.set_forecasts(wf, P)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    needed = max(1, int(needed_frac * used))
+    times = []
+    for _ in range(decisions):
+        t0 = time.perf_counter()
+        t.refresh_nodes(None, K, GAMMA)
+        sel = t.select(POLICY_HE, needed, locked)
+        times.append(time.perf_counter() - t0)
+    return {"n_nodes": soa.n_nodes, "times": times, "build_s": build_s, "n_victims": len(sel.victims)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_nodes, n_wf, K = CONFIGS[args.config]
+    steps = max(1, args.steps)
+    warm = max(0, min(args.warmup, 1))
+    r = cpu_reference_decisions(args.config, args.needed_frac, warm + steps)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libflowkv_ref.so not built"}))
+        return
+    times = r["times"][warm:]
+    ms = 1000.0 * statistics.mean(times)
+    val = r["n_nodes"] / statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "nodes/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {n_nodes} nodes x {n_wf} workflows x K={K}, 30% retired, "
+                               f"HE select at {args.needed_frac:.2%} need",
+                   "parallelism": "cpu-1thread"},
+        "p99_decision_ms": 1000.0 * float(np.percentile(times, 99)),
+        "cpu_baseline": {"value": val, "unit": "nodes/s", "cores": 1, "kind": "reference",
+                         "sample": f"{steps} decisions (refresh_nodes over all nodes + select_victims_hierarchical)"
+                                   f" on the {args.config} tree; reference is single-threaded (SPEC.md:235)"},
+        "e2e": {"value": val, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+
+    from paper_2605_06472_b200._abi import POLICY_HE, SCORE_RECOMPUTE
+    from paper_2605_06472_b200.api import Policy
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n_nodes, n_wf, K = CONFIGS[args.config]
+    t, soa, wf, P, locked, K, build_s = workload(args.config, rank)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    needed = max(1, int(args.needed_frac * used))
+
+    pol = Policy(num_agents=AGENTS, k=K, gamma=GAMMA, device=local)
+    pol.mirror(t)
+    pol.put_forecasts(wf, P)
+
+    dev = torch.device("cuda", local)
+    locked_d = torch.from_numpy(locked if locked.size else np.zeros(1, np.int32)).to(dev)
+    victims_d = torch.empty(soa.n_nodes, dtype=torch.int32, device=dev)
+    result_d = torch.zeros(3, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.ExternalStream(pol.stream_handle(), device=dev)
+
+    def step():
+        pol.select_dev(POLICY_HE, SCORE_RECOMPUTE, needed, locked_d.data_ptr(), locked.size, victims_d.data_ptr(),
+                       soa.n_nodes, result_d.data_ptr())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region ---------------------------------------------
+    k0, l0 = pol.launches()
+    per_step = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # evict the working set from L2 between decisions
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            per_step.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    k1, l1 = pol.launches()
+    ms_local = statistics.mean(per_step)
+    p99_local = float(np.percentile(per_step, 99))
+    res = result_d.cpu().tolist()
+
+    # ---- per-stage split (separate pass: events between stages) ---------------------
+    pol.set_timing(True)
+    stage = np.zeros(5)
+    n_stage = max(3, min(10, args.steps))
+    for _ in range(n_stage):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        step()
+        stage += np.array(pol.timings())
+    stage /= n_stage
+    pol.set_timing(False)
+
+    # ---- e2e through the host C ABI -------------------------------------------------
+    P_pinned = torch.from_numpy(np.ascontiguousarray(P)).pin_memory().numpy()
+    locked_list = locked.tolist()
+    e2e_ms = []
+    n_victims_e2e = 0
+    for _ in range(max(1, args.steps)):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        pol.put_forecasts(wf, P_pinned)
+        sel = pol.select_victims_hierarchical(needed, locked=locked_list, score_mode=SCORE_RECOMPUTE)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        n_victims_e2e = len(sel.victims)
+    assert n_victims_e2e == res[0], "e2e and device-resident decisions disagree"
+
+    # ---- aggregate over ranks (max time) --------------------------------------------
+    ms = ms_local
+    p99 = p99_local
+    e2e = statistics.mean(e2e_ms)
+    if dist:
+        tt = torch.tensor([ms_local, p99_local, e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, p99, e2e = tt.tolist()
+    total_nodes = soa.n_nodes * world
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    N, E = soa.n_nodes, soa.n_entries
+    F = wf.size * K * (AGENTS + 2) * 8
+    alg_score = 41 * N + 12 * E + F  # fused score+key stage
+    score_ms = float(stage[0])
+    achieved = alg_score / (score_ms * 1e-3) / 1e9 if score_ms > 0 else None
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        r = cpu_reference_decisions(args.config, args.needed_frac, args.cpu_decisions)
+        if r:
+            cpu = {"value": r["n_nodes"] / statistics.mean(r["times"]), "unit": "nodes/s", "cores": 1,
+                   "kind": "reference",
+                   "sample": f"{len(r['times'])} decisions on the same {args.config} tree "
+                             f"(refresh_nodes all + select_victims_hierarchical), "
+                             f"{statistics.mean(r['times']):.3f} s each; tree build {r['build_s']:.1f} s untimed"}
+    line = {
+        "metric": METRIC, "value": total_nodes / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {n_nodes} nodes x {n_wf} workflows x K={K}, 30% retired, "
+                               f"A={AGENTS}, HE select at {args.needed_frac:.2%} need, 1% leaves pinned",
+                   "n_nodes": N, "n_entries": E, "needed_tokens": needed, "n_victims": res[0],
+                   "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single"},
+        "p99_decision_ms": p99,
+        "p50_decision_ms": float(np.percentile(per_step, 50)),
+        "stage_ms": {"score_keys": float(stage[0]), "lock_eff_weights": float(stage[1]),
+                     "cut_sort": float(stage[2]), "total": float(stage[4])},
+        "roofline": {"bound": "hbm", "kernel": "score_light_kernel<true>+heavy_score_kernel (fused Eq.2 + keys)",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "alg_bytes_per_launch": alg_score},
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_nodes / (e2e * 1e-3), "unit": "nodes/s",
+                "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size + 4 * locked.size),
+                "d2h_bytes_per_step": int(4 * n_victims_e2e + 24), "ms_per_step": e2e},
+        "gpu_launches": int(k1 - k0),
+        "lib_calls": int(l1 - l0),
+        "clocks": clk.result,
+        "tree_build_s": build_s,
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

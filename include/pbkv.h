@@ -127,6 +127,8 @@ int pbkv_ctx_stream(pbkv_ctx* ctx, void** stream_out);     /* the ctx's cudaStre
  * the ctx stream): [0]=score [1]=keys+eff [2]=cut/sort [3]=prefetch [4]=total. */
 int pbkv_ctx_timings(pbkv_ctx* ctx, float* ms5);
 int pbkv_ctx_set_timing(pbkv_ctx* ctx, int enabled);
+/* Cumulative launch counts: pbkv's own kernels, and CUB library calls. */
+int pbkv_ctx_launches(pbkv_ctx* ctx, int64_t* kernels, int64_t* lib_calls);
 
 /* ---- device mirror of the tree --------------------------------------------- */
 /* Full upload of a CacheTree snapshot (SURVEY.md §8(b) pbkv_mirror_full). */

@@ -240,6 +240,14 @@ class Policy:
                                        ptr(victims, C.c_int32), cap, C.byref(nv), C.byref(fr), C.byref(sf)))
         return VictimSelection(victims[: nv.value].tolist(), int(fr.value), bool(sf.value))
 
+    def select_dev(self, policy: int, score_mode: int, needed: int, locked_ptr: int, n_locked: int,
+                   victims_ptr: int, cap: int, result_ptr: int) -> None:
+        """pbkv_select_dev: device-resident inputs/outputs (raw device pointers,
+        e.g. torch tensor data_ptr()); result_ptr -> int64[3] {n_victims, freed, shortfall}."""
+        self._c(_abi.lib().pbkv_select_dev(self._h, int(policy), int(score_mode), int(needed),
+                                           C.c_void_p(locked_ptr or None), int(n_locked),
+                                           C.c_void_p(victims_ptr or None), int(cap), C.c_void_p(result_ptr)))
+
     def select_victims_lru(self, needed: int, locked: Iterable[int] = ()) -> VictimSelection:
         return self.select_victims(POLICY_LRU, needed, locked=locked)
 
@@ -281,6 +289,17 @@ class Policy:
     # ---- timing ------------------------------------------------------------------------
     def set_timing(self, on: bool) -> None:
         self._c(_abi.lib().pbkv_ctx_set_timing(self._h, 1 if on else 0))
+
+    def launches(self) -> tuple[int, int]:
+        """(pbkv kernels launched, CUB library calls) since the context was created."""
+        k, l = C.c_int64(), C.c_int64()
+        self._c(_abi.lib().pbkv_ctx_launches(self._h, C.byref(k), C.byref(l)))
+        return k.value, l.value
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        self._c(_abi.lib().pbkv_ctx_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
 
     def timings(self) -> list[float]:
         ms = (C.c_float * 5)()

@@ -562,6 +562,14 @@ int pbkv_ctx_set_timing(pbkv_ctx* c, int enabled) {
     });
 }
 
+int pbkv_ctx_launches(pbkv_ctx* c, int64_t* kernels, int64_t* lib_calls) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        if (kernels) *kernels = c->launches;
+        if (lib_calls) *lib_calls = c->lib_calls;
+    });
+}
+
 int pbkv_mirror_full(pbkv_ctx* c, const pbkv_tree_soa* soa) {
     return api(c, [&] {
         need(c && soa, "null argument");

@@ -776,6 +776,7 @@ void launch_forecast_prepare(Context& c, const double* stage, const long long* s
     forecast_prepare_kernel<<<grid_for(n, 128), 128, 0, c.stream>>>(stage, slots, n, H, c.V1, c.K, c.gamma, c.P.p,
                                                                    c.gs.p, c.fstate.p, c.status.p);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_score_all(Context& c, double* out_dev, bool write_keys, int policy, bool want_missing) {
@@ -785,12 +786,14 @@ void launch_score_all(Context& c, double* out_dev, bool write_keys, int policy, 
         heavy_score_kernel<false><<<static_cast<unsigned int>(c.n_heavy), kHeavyThreads, heavy_smem(c.K), c.stream>>>(
             s, ka, c.heavy.p, write_keys ? 1 : 0, want_missing ? 1 : 0);
         PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
     }
     if (write_keys)
         score_light_kernel<true><<<sm_grid(c, c.n, 256), 256, 0, c.stream>>>(s, ka, c.n, want_missing ? 1 : 0);
     else
         score_light_kernel<false><<<sm_grid(c, c.n, 256), 256, 0, c.stream>>>(s, ka, c.n, want_missing ? 1 : 0);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_score_ids(Context& c, const int* ids_dev, std::int64_t n, double* out_dev, bool value_only) {
@@ -804,6 +807,7 @@ void launch_score_ids(Context& c, const int* ids_dev, std::int64_t n, double* ou
     else
         score_ids_kernel<false><<<sm_grid(c, n, 256), 256, 0, c.stream>>>(s, ids_dev, n, c.sel.p, nh);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
     PBKV_CUDA(cudaMemcpyAsync(c.hcounters.p + 4, nh, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
     long long heavy = c.hcounters.p[4];
@@ -815,6 +819,7 @@ void launch_score_ids(Context& c, const int* ids_dev, std::int64_t n, double* ou
             heavy_score_kernel<false><<<static_cast<unsigned int>(heavy), kHeavyThreads, heavy_smem(c.K), c.stream>>>(
                 s, ka, c.sel.p, 0, 1);
         PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
     }
 }
 
@@ -822,6 +827,7 @@ void launch_keys_cached(Context& c, int policy) {
     KeyArgs ka = key_args(c, policy);
     keys_cached_kernel<<<sm_grid(c, c.n, 256), 256, 0, c.stream>>>(ka, c.n);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_eff(Context& c, const int* locked_dev, std::int64_t n_locked) {
@@ -829,9 +835,11 @@ void launch_eff(Context& c, const int* locked_dev, std::int64_t n_locked) {
         lock_kernel<<<grid_for(n_locked, 256), 256, 0, c.stream>>>(locked_dev, n_locked, c.parent.p, c.flags.p,
                                                                   c.sublock.p, c.n);
         PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
     }
     eff_kernel<<<sm_grid(c, c.n, 256), 256, 0, c.stream>>>(c.parent.p, c.flags.p, c.keys.p, c.eff.p, c.n);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_weights(Context& c, long long* counters_dev, bool he_recompute) {
@@ -839,6 +847,7 @@ void launch_weights(Context& c, long long* counters_dev, bool he_recompute) {
                                                               c.W.p, c.heads.p, counters_dev, c.status.p, c.n,
                                                               he_recompute ? 1 : 0);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_prefetch_candidates(Context& c, long long* counters_dev) {
@@ -846,6 +855,7 @@ void launch_prefetch_candidates(Context& c, long long* counters_dev) {
     prefetch_cand_kernel<<<sm_grid(c, c.n, 256), 256, 0, c.stream>>>(s, c.parent.p, c.flags.p, c.last.p, c.ck_in.p,
                                                                      c.cv_in.p, counters_dev, c.status.p, c.n);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_prefetch_err_id(Context& c) {
@@ -853,28 +863,33 @@ void launch_prefetch_err_id(Context& c) {
     prefetch_err_id_kernel<<<sm_grid(c, c.n, 256), 256, 0, c.stream>>>(s, c.parent.p, c.flags.p, c.last.p, c.status.p,
                                                                        c.n);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_prefetch_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev) {
     prefetch_greedy_kernel<<<1, kGreedyThreads, 0, c.stream>>>(c.ck_out.p, c.len.p, n_cand, budget, c.sel.p,
                                                                counters_dev);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_gather_heads(Context& c, std::int64_t n_heads) {
     gather_heads_kernel<<<sm_grid(c, n_heads, 256), 256, 0, c.stream>>>(c.heads.p, c.keys.p, c.hk_in.p, n_heads);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_head_weights(Context& c, std::int64_t n_heads) {
     head_weights_kernel<<<sm_grid(c, n_heads, 256), 256, 0, c.stream>>>(c.hk_out.p, c.W.p, c.wsorted.p, c.rank.p,
                                                                         n_heads);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_find_cut(Context& c, const unsigned long long* scan, std::int64_t n, long long needed, long long* out) {
     find_cut_kernel<<<sm_grid(c, n, 256), 256, 0, c.stream>>>(scan, n, needed, out);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_victim_keys(Context& c, long long cut, long long* counter) {
@@ -882,11 +897,13 @@ void launch_victim_keys(Context& c, long long cut, long long* counter) {
                                                                    c.depth.p, cut, c.vkey_in.p, c.vid_in.p, counter,
                                                                    c.n);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_victim_len(Context& c, std::int64_t n) {
     victim_len_kernel<<<sm_grid(c, n, 256), 256, 0, c.stream>>>(c.vid_out.p, c.len.p, c.vscan.p, n);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 namespace {
@@ -900,6 +917,7 @@ __global__ void gather_f64_kernel(const double* src, const int* ids, std::int64_
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst) {
     gather_f64_kernel<<<sm_grid(c, n, 256), 256, 0, c.stream>>>(src, ids, n, dst);
     PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 // ---- CUB wrappers ---------------------------------------------------------------
@@ -925,6 +943,7 @@ std::size_t cub_sort_heads_bytes(std::int64_t n) {
 void cub_sort_heads(Context& c, std::int64_t n) {
     std::size_t b = cub_sort_heads_bytes(n);
     c.cub_tmp.reserve(b);
+    ++c.lib_calls;
     PBKV_CUDA(cub::DeviceRadixSort::SortKeys(c.cub_tmp.p, b, c.hk_in.p, c.hk_out.p, static_cast<int>(n),
                                              HeadDecomposer{}, c.stream));
 }
@@ -939,6 +958,7 @@ std::size_t cub_scan_bytes(std::int64_t n) {
 void cub_scan_u64(Context& c, const unsigned long long* in, unsigned long long* out, std::int64_t n) {
     std::size_t b = cub_scan_bytes(n);
     c.cub_tmp.reserve(b);
+    ++c.lib_calls;
     PBKV_CUDA(cub::DeviceScan::InclusiveSum(c.cub_tmp.p, b, in, out, static_cast<int>(n), c.stream));
 }
 
@@ -953,6 +973,7 @@ std::size_t cub_sort_pairs_bytes(std::int64_t n) {
 void cub_sort_pairs_u64(Context& c, std::int64_t n, int end_bit) {
     std::size_t b = cub_sort_pairs_bytes(n);
     c.cub_tmp.reserve(b);
+    ++c.lib_calls;
     PBKV_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, b, c.vkey_in.p, c.vkey_out.p, c.vid_in.p, c.vid_out.p,
                                               static_cast<int>(n), 0, end_bit, c.stream));
 }
@@ -968,6 +989,7 @@ std::size_t cub_sort_cands_bytes(std::int64_t n) {
 void cub_sort_cands(Context& c, std::int64_t n) {
     std::size_t b = cub_sort_cands_bytes(n);
     c.cub_tmp.reserve(b);
+    ++c.lib_calls;
     PBKV_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, b, c.ck_in.p, c.ck_out.p, c.cv_in.p, c.cv_out.p,
                                               static_cast<int>(n), CandDecomposer{}, c.stream));
 }

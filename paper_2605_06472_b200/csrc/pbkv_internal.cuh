@@ -210,6 +210,9 @@ struct Context {
     PinBuf<int> hids;
     PinBuf<double> hvals;
 
+    // launch accounting (pbkv kernels; CUB library calls counted separately)
+    long long launches = 0, lib_calls = 0;
+
     // timing
     bool timing = false;
     cudaEvent_t ev[6] = {};
