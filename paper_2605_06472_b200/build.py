@@ -17,9 +17,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpbkv.so")
 
-SOURCES = ["capi.cu", "kernels.cu"]
+SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu"]
 HEADERS = [
     "pbkv_internal.cuh",
+    "common.cuh",
     os.path.join("host", "radix_mirror.hpp"),
     os.path.join("host", "ops.hpp"),
 ]

@@ -18,16 +18,6 @@ struct pbkv_tree {
     pbkv_tree(std::int64_t d, std::int64_t h) : tree(d, h) {}
 };
 
-namespace pbkv {
-void launch_gather_heads(Context& c, std::int64_t n_heads);
-void launch_head_weights(Context& c, std::int64_t n_heads);
-void launch_find_cut(Context& c, const unsigned long long* scan, std::int64_t n, long long needed, long long* out);
-void launch_victim_keys(Context& c, long long cut, long long* counter);
-void launch_victim_len(Context& c, std::int64_t n);
-void launch_prefetch_err_id(Context& c);
-void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
-}  // namespace pbkv
-
 namespace {
 
 using namespace pbkv;
@@ -122,8 +112,12 @@ void ensure_scratch(Context& c) {
     c.sublock.reserve(n);
     c.missing.reserve(n);
     c.W.reserve(n);
+    c.C.reserve(n);
     c.heads.reserve(n);
+    c.listB.reserve(n);
+    c.listS.reserve(n);
     c.rank.reserve(n);
+    c.vid_out.reserve(n);
 }
 
 std::string missing_message(Context& c, long long node) {
@@ -162,6 +156,12 @@ std::string kvflow_message(Context& c, long long node) {
 }  // namespace
 
 namespace pbkv {
+void reset_status(Context& c) {
+    DevStatus* h = c.hstatus.p;
+    *h = DevStatus{0, 0, LLONG_MAX, LLONG_MAX};
+    PBKV_CUDA(cudaMemcpyAsync(c.status.p, h, sizeof(DevStatus), cudaMemcpyHostToDevice, c.stream));
+}
+
 void check_status(Context& c) {
     PBKV_CUDA(cudaMemcpyAsync(c.hstatus.p, c.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c.stream));
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
@@ -226,8 +226,11 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     std::vector<std::uint8_t> flags(static_cast<std::size_t>(n));
     std::vector<unsigned int> off(static_cast<std::size_t>(n) + 1);
     std::vector<int> slot(static_cast<std::size_t>(E));
-    std::vector<int> heavy;
+    std::vector<int> medium, heavy, hent_node;
+    std::vector<unsigned int> hent;
+    std::vector<long long> hstart;
     std::vector<int> depth;
+    c.h_entries.assign(static_cast<std::size_t>(n), 0);
     for (std::int64_t i = 0; i < n; ++i) {
         if (s.tier[i] > PBKV_TIER_ABSENT) invalid("tree soa: bad tier value");
         flags[static_cast<std::size_t>(i)] =
@@ -240,7 +243,20 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
             if (e > a && s.acc_wf[e] <= s.acc_wf[e - 1]) invalid("tree soa: access entries must ascend by workflow id");
             slot[static_cast<std::size_t>(e)] = slot_for(c, s.acc_wf[e]);
         }
-        if (b - a > kHeavyEntries) heavy.push_back(static_cast<int>(i));
+        const std::int64_t ne = b - a;
+        c.h_entries[static_cast<std::size_t>(i)] = static_cast<int>(ne);
+        // node classes of the Eq. 2 kernels (score.cu): light <= 2 entries,
+        // medium chain <= kMediumMaxChain, heavy above
+        if (ne * c.K > kMediumMaxChain) {
+            hstart.push_back(static_cast<long long>(hent.size()) * c.K);
+            for (std::int64_t e = a; e < b; ++e) {
+                hent.push_back(static_cast<unsigned int>(e));
+                hent_node.push_back(static_cast<int>(heavy.size()));
+            }
+            heavy.push_back(static_cast<int>(i));
+        } else if (ne > 2) {
+            medium.push_back(static_cast<int>(i));
+        }
     }
     off[static_cast<std::size_t>(n)] = static_cast<unsigned int>(E);
     const int* dep = s.depth;
@@ -296,9 +312,26 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
         PBKV_CUDA(cudaMemcpyAsync(c.acc_slot.p, slot.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
         PBKV_CUDA(cudaMemcpyAsync(c.acc_bits.p, s.acc_bits, E * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
     }
-    if (!heavy.empty())
+    c.medium.reserve(medium.size() + 1);
+    c.hent.reserve(hent.size() + 1);
+    c.hent_node.reserve(hent.size() + 1);
+    c.hstart.reserve(heavy.size() + 1);
+    c.hmiss.reserve(heavy.size() + 1);
+    c.hxs.reserve(hent.size() * static_cast<std::size_t>(c.K) + 1);
+    if (!medium.empty())
+        PBKV_CUDA(cudaMemcpyAsync(c.medium.p, medium.data(), medium.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!heavy.empty()) {
         PBKV_CUDA(cudaMemcpyAsync(c.heavy.p, heavy.data(), heavy.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c.hent.p, hent.data(), hent.size() * sizeof(unsigned int), cudaMemcpyHostToDevice,
+                                  st));
+        PBKV_CUDA(cudaMemcpyAsync(c.hent_node.p, hent_node.data(), hent_node.size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c.hstart.p, hstart.data(), hstart.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                                  st));
+    }
+    c.n_medium = static_cast<std::int64_t>(medium.size());
     c.n_heavy = static_cast<std::int64_t>(heavy.size());
+    c.n_hent = static_cast<std::int64_t>(hent.size());
     c.max_depth = maxd;
     c.device_capacity = s.device_capacity;
     c.device_used = s.device_used;
@@ -355,95 +388,31 @@ struct SoaStore {
 };
 
 // ---- stage 3 ------------------------------------------------------------------
-struct SelectOut {
-    std::int64_t n_victims = 0, freed = 0;
-    int shortfall = 0;
-};
-
-// Runs the selection; victims stay in c.vid_out[0..n_victims).
-SelectOut select_core(Context& c, int policy, int score_mode, std::int64_t needed, const int* locked_dev,
-                      std::int64_t n_locked) {
+// Keys (from the recomputed or the cached score), lock marks, subtree max,
+// then the weighted cut and the victim order (select.cu).  Victims land in
+// c.vid_out[0..n_victims).
+SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t needed, const int* locked_dev,
+                         std::int64_t n_locked, long long* result_dev) {
     if (needed <= 0) invalid("eviction request must free a positive amount");
     if (policy < PBKV_POLICY_LRU || policy > PBKV_POLICY_KVFLOW) invalid("unknown eviction policy");
     if (policy == PBKV_POLICY_KVFLOW && !c.have_remaining) invalid("kvflow selected without static sequences");
-    if (score_mode != PBKV_SCORE_CACHED && score_mode != PBKV_SCORE_RECOMPUTE) throw ApiError(PBKV_EARG, "bad score mode");
+    if (score_mode != PBKV_SCORE_CACHED && score_mode != PBKV_SCORE_RECOMPUTE)
+        throw ApiError(PBKV_EARG, "bad score mode");
     need(c.n >= 1, "no tree mirrored");
-    SelectOut out;
-    long long* ctr = c.counters.p;
-    long long* hctr = c.hcounters.p;
     record(c, 0);
     reset_status(c);
-    PBKV_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(long long), c.stream));
     const bool recompute = score_mode == PBKV_SCORE_RECOMPUTE && policy == PBKV_POLICY_HE;
     if (recompute)
         launch_score_all(c, c.score_rc.p, true, policy, false);
     else
         launch_keys_cached(c, policy);
     record(c, 1);
-    launch_eff(c, locked_dev, n_locked);
-    launch_weights(c, ctr, recompute);  // raises missing forecasts only for eligible active nodes
-    PBKV_CUDA(cudaMemcpyAsync(hctr, ctr, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
-    check_status(c);  // syncs
+    launch_lock_eff(c, locked_dev, n_locked);
     record(c, 2);
-    const std::int64_t n_heads = hctr[0];
-    const long long elig_tokens = hctr[1];
-    if (n_heads == 0) {
-        out.shortfall = 1;
-        record(c, 3);
-        finish_timing(c, 3);
-        return out;
-    }
-    c.hk_in.reserve(n_heads);
-    c.hk_out.reserve(n_heads);
-    c.wsorted.reserve(n_heads);
-    c.wscan.reserve(n_heads);
-    launch_gather_heads(c, n_heads);
-    cub_sort_heads(c, n_heads);
-    launch_head_weights(c, n_heads);
-    cub_scan_u64(c, c.wsorted.p, c.wscan.p, n_heads);
-    long long cut = n_heads - 1;
-    if (elig_tokens >= needed) {
-        long long init = LLONG_MAX;
-        PBKV_CUDA(cudaMemcpyAsync(ctr + 2, &init, sizeof init, cudaMemcpyHostToDevice, c.stream));
-        launch_find_cut(c, c.wscan.p, n_heads, needed, ctr + 2);
-        PBKV_CUDA(cudaMemcpyAsync(hctr + 2, ctr + 2, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
-        PBKV_CUDA(cudaStreamSynchronize(c.stream));
-        cut = hctr[2];
-    }
-    // candidates = chains of heads [0, cut]
-    PBKV_CUDA(cudaMemsetAsync(ctr + 3, 0, sizeof(long long), c.stream));
-    c.vkey_in.reserve(c.n);
-    c.vid_in.reserve(c.n);
-    launch_victim_keys(c, cut, ctr + 3);
-    PBKV_CUDA(cudaMemcpyAsync(hctr + 3, ctr + 3, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
-    PBKV_CUDA(cudaStreamSynchronize(c.stream));
-    const std::int64_t n_cand = hctr[3];
-    c.vkey_out.reserve(n_cand);
-    c.vid_out.reserve(n_cand);
-    c.vscan.reserve(n_cand);
-    int end_bit = 24;
-    for (long long r = cut; r > 0; r >>= 1) ++end_bit;
-    cub_sort_pairs_u64(c, n_cand, std::min(end_bit, 64));
-    launch_victim_len(c, n_cand);
-    cub_scan_u64(c, c.vscan.p, c.vscan.p, n_cand);
-    long long j = n_cand - 1;
-    if (elig_tokens >= needed) {
-        long long init = LLONG_MAX;
-        PBKV_CUDA(cudaMemcpyAsync(ctr + 4, &init, sizeof init, cudaMemcpyHostToDevice, c.stream));
-        launch_find_cut(c, c.vscan.p, n_cand, needed, ctr + 4);
-        PBKV_CUDA(cudaMemcpyAsync(hctr + 4, ctr + 4, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
-        PBKV_CUDA(cudaStreamSynchronize(c.stream));
-        j = hctr[4];
-    }
-    unsigned long long fr = 0;
-    PBKV_CUDA(cudaMemcpyAsync(&fr, c.vscan.p + j, sizeof fr, cudaMemcpyDeviceToHost, c.stream));
-    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    SelectCounts o = run_select(c, needed, recompute, result_dev);
     record(c, 3);
     finish_timing(c, 3);
-    out.n_victims = j + 1;
-    out.freed = static_cast<std::int64_t>(fr);
-    out.shortfall = out.freed < needed ? 1 : 0;
-    return out;
+    return o;
 }
 
 }  // namespace
@@ -499,7 +468,13 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         c->V1 = cfg->num_agents + 1;
         PBKV_CUDA(cudaSetDevice(c->device));
         PBKV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        PBKV_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         for (auto& e : c->ev) PBKV_CUDA(cudaEventCreate(&e));
+        PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        c->selstate.reserve(sel_state_bytes());
+        c->hselstate.reserve(sel_state_bytes());
+        c->hist.reserve(1 << 11);
         c->counters.reserve(16);
         c->status.reserve(1);
         c->hcounters.reserve(16);
@@ -518,19 +493,15 @@ int pbkv_ctx_destroy(pbkv_ctx* c) {
     if (!c) return PBKV_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    auto rel = [](auto& b) { b.release(); };
-    rel(c->parent), rel(c->len), rel(c->ever), rel(c->depth), rel(c->flags), rel(c->last), rel(c->score);
-    rel(c->acc_off), rel(c->acc_slot), rel(c->acc_bits), rel(c->heavy), rel(c->P), rel(c->gs), rel(c->fstate);
-    rel(c->fstage), rel(c->fstage_slot), rel(c->rem_off), rel(c->rem_seq), rel(c->rem_has), rel(c->score_rc);
-    rel(c->keys), rel(c->eff), rel(c->sublock), rel(c->missing), rel(c->W), rel(c->heads), rel(c->hk_in);
-    rel(c->hk_out), rel(c->wsorted), rel(c->wscan), rel(c->rank), rel(c->vkey_in), rel(c->vkey_out), rel(c->vid_in);
-    rel(c->vid_out), rel(c->vscan), rel(c->locked), rel(c->ids), rel(c->vals), rel(c->ck_in), rel(c->ck_out);
-    rel(c->cv_in), rel(c->cv_out), rel(c->sel), rel(c->cub_tmp), rel(c->counters), rel(c->status);
-    rel(c->hcounters), rel(c->hstatus), rel(c->hids), rel(c->hvals);
+    if (c->side) cudaStreamSynchronize(c->side);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    cudaStreamDestroy(c->stream);
-    delete c;
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    cudaStream_t s = c->stream, side = c->side;
+    delete c;  // DevBuf / PinBuf destructors free the device and pinned memory
+    cudaStreamDestroy(s);
+    if (side) cudaStreamDestroy(side);
     return PBKV_OK;
 }
 
@@ -687,7 +658,7 @@ static int score_ids_impl(pbkv_ctx* c, const int32_t* ids, int64_t n, double* ou
         c->vals.reserve(static_cast<std::size_t>(n));
         reset_status(*c);
         PBKV_CUDA(cudaMemcpyAsync(c->ids.p, ids, n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        launch_score_ids(*c, c->ids.p, n, c->score_rc.p, value_only);
+        launch_score_ids(*c, c->ids.p, ids, n, c->score_rc.p, value_only);
         check_status(*c);
         launch_gather_f64(*c, c->score_rc.p, c->ids.p, n, c->vals.p);
         PBKV_CUDA(cudaMemcpyAsync(out, c->vals.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -712,7 +683,7 @@ int pbkv_select(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const i
         c->locked.reserve(static_cast<std::size_t>(n_locked) + 1);
         if (n_locked > 0)
             PBKV_CUDA(cudaMemcpyAsync(c->locked.p, locked, n_locked * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        SelectOut o = select_core(*c, policy, score_mode, needed, c->locked.p, n_locked);
+        SelectCounts o = select_core(*c, policy, score_mode, needed, c->locked.p, n_locked, nullptr);
         *n_victims = o.n_victims;
         *freed = o.freed;
         *shortfall = o.shortfall;
@@ -732,19 +703,14 @@ int pbkv_select_dev(pbkv_ctx* c, int policy, int score_mode, int64_t needed, con
         need(c && result_dev, "null argument");
         need(n_locked == 0 || locked_dev, "null locked array");
         set_device(*c);
-        SelectOut o = select_core(*c, policy, score_mode, needed, locked_dev, n_locked);
+        SelectCounts o = select_core(*c, policy, score_mode, needed, locked_dev, n_locked,
+                                     reinterpret_cast<long long*>(result_dev));
         if (o.n_victims > cap) throw ApiError(PBKV_EARG, "victim capacity too small");
         if (o.n_victims > 0) {
             need(victims_dev != nullptr, "null victims array");
             PBKV_CUDA(cudaMemcpyAsync(victims_dev, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToDevice,
                                       c->stream));
         }
-        long long* h = c->hcounters.p + 8;
-        h[0] = o.n_victims;
-        h[1] = o.freed;
-        h[2] = o.shortfall;
-        PBKV_CUDA(cudaMemcpyAsync(result_dev, h, 3 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
-        PBKV_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 
@@ -805,7 +771,7 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
         record(*c, 0);
         reset_status(*c);
         PBKV_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(long long), c->stream));
-        launch_prefetch_candidates(*c, ctr);
+        launch_prefetch_candidates(*c, reinterpret_cast<unsigned long long*>(ctr));
         PBKV_CUDA(cudaMemcpyAsync(hctr, ctr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         PBKV_CUDA(cudaMemcpyAsync(c->hstatus.p, c->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
@@ -823,8 +789,7 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
         c->ck_out.reserve(nc);
         c->cv_out.reserve(nc);
         c->sel.reserve(nc);
-        cub_sort_cands(*c, nc);
-        launch_prefetch_greedy(*c, nc, budget, ctr);
+        launch_prefetch_sort_greedy(*c, nc, budget, ctr);
         PBKV_CUDA(cudaMemcpyAsync(hctr + 1, ctr + 1, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
         record(*c, 1);

@@ -1,0 +1,224 @@
+// Device helpers shared by the score / select / prefetch kernels.
+#pragma once
+
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/warp/warp_reduce.cuh>
+#include <math_constants.h>
+
+#include "pbkv_internal.cuh"
+
+namespace pbkv {
+namespace dev {
+
+__device__ __forceinline__ void set_error(DevStatus* st, int code, int kind, long long node) {
+    atomicCAS(&st->code, 0, code);
+    if (st->code == code) {
+        atomicCAS(&st->kind, 0, kind);
+        atomicMin(&st->node, node);
+    }
+}
+
+// Forecast::mass_on (forecast.hpp:64-69): sum over set agent bits in
+// ascending agent order.  Loads are issued in batches of 8 so their latency
+// overlaps; the additions stay in the reference order.  Adding a masked-out
+// slot is skipped (not "+0.0"), so the result is the exact reference chain.
+__device__ __forceinline__ double mass_on(const double* __restrict__ row, unsigned long long bits) {
+    double m = 0.0;
+    while (bits) {
+        double v[8];
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (bits) {
+                int a = __ffsll(static_cast<long long>(bits)) - 1;
+                v[j] = __ldg(row + a);
+                bits &= bits - 1;
+                cnt = j + 1;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < cnt) m = __dadd_rn(m, v[j]);
+    }
+    return m;
+}
+
+// two rows (steps k and k+1) with the same agent bits: both batches of loads
+// are in flight before either addition chain starts
+__device__ __forceinline__ void mass_on2(const double* __restrict__ r0, const double* __restrict__ r1,
+                                         unsigned long long bits, double& m0, double& m1) {
+    m0 = 0.0;
+    m1 = 0.0;
+    while (bits) {
+        double v0[8], v1[8];
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (bits) {
+                int a = __ffsll(static_cast<long long>(bits)) - 1;
+                v0[j] = __ldg(r0 + a);
+                v1[j] = __ldg(r1 + a);
+                bits &= bits - 1;
+                cnt = j + 1;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < cnt) {
+                m0 = __dadd_rn(m0, v0[j]);
+                m1 = __dadd_rn(m1, v1[j]);
+            }
+    }
+}
+
+// order-preserving double -> uint64 (policies.hpp:46 compares ranks with <)
+__device__ __forceinline__ unsigned long long enc_rank(double r) {
+    if (r == 0.0) r = 0.0;  // -0.0 == +0.0 under std::tie
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(r));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ Key2 make_key(int cls, double rank, unsigned long long last) {
+    unsigned long long e = enc_rank(rank);
+    Key2 k;
+    k.w0 = (static_cast<unsigned long long>(cls) << 63) | (e >> 1);
+    k.w1 = ((e & 1ull) << 63) | last;
+    return k;
+}
+
+__device__ __forceinline__ bool key_less(const Key2& a, int ia, const Key2& b, int ib) {
+    if (a.w0 != b.w0) return a.w0 < b.w0;
+    if (a.w1 != b.w1) return a.w1 < b.w1;
+    return ia < ib;
+}
+
+__device__ __forceinline__ Key2 load_key(const Key2* keys, int i) {
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(keys) + i);
+    return Key2{v.x, v.y};
+}
+
+// warp-aggregated append: one atomic per warp; returns this lane's slot
+__device__ __forceinline__ long long warp_append(unsigned long long* counter, bool pred) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return -1;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(mask)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!pred) return -1;
+    return static_cast<long long>(base + __popc(mask & ((1u << lane) - 1u)));
+}
+
+// KVFlow steps-to-execution (policies.hpp:121-139): +inf when no tagged agent
+// recurs; sets *missing when a tagged workflow has no remaining sequence.
+__device__ __forceinline__ double kvflow_distance(const unsigned int* __restrict__ off,
+                                                  const int* __restrict__ slot,
+                                                  const unsigned long long* __restrict__ bits,
+                                                  const int* __restrict__ rem_off, const int* __restrict__ rem_seq,
+                                                  const std::uint8_t* __restrict__ rem_has, int n, bool* missing) {
+    double best = CUDART_INF;
+    for (unsigned int e = off[n]; e < off[n + 1]; ++e) {
+        int s = slot[e];
+        if (!rem_has[s]) {
+            *missing = true;
+            return best;
+        }
+        unsigned long long b = bits[e];
+        for (int k = rem_off[s]; k < rem_off[s + 1]; ++k) {
+            int a = rem_seq[k];
+            if (a >= 0 && a < 64 && ((b >> a) & 1ull)) {
+                double d = static_cast<double>(k - rem_off[s] + 1);
+                best = d < best ? d : best;
+                break;
+            }
+        }
+    }
+    return best;
+}
+
+}  // namespace dev
+
+// ---- kernel argument packs -------------------------------------------------------
+struct ScoreArgs {
+    const unsigned int* acc_off;
+    const int* acc_slot;
+    const unsigned long long* acc_bits;
+    const double* P;
+    const double* gs;
+    const std::uint8_t* fstate;
+    int K, V1;
+    unsigned long long amask;
+    double* out;
+    DevStatus* st;
+};
+
+// per-node stage-3 state initialised by whichever kernel scores/keys the node
+struct KeyArgs {
+    const int* parent;
+    const int* len;
+    const std::uint8_t* flags;
+    const unsigned long long* last;
+    const int* ever;
+    const double* score_cached;
+    const unsigned int* acc_off;
+    const int* acc_slot;
+    const unsigned long long* acc_bits;
+    const int* rem_off;
+    const int* rem_seq;
+    const std::uint8_t* rem_has;
+    Key2* keys;
+    int* eff;
+    int* sublock;
+    unsigned long long* W;
+    unsigned int* C;
+    int* rank;
+    std::uint8_t* missing;
+    DevStatus* st;
+    int policy;
+};
+
+namespace dev {
+
+// key of policies.hpp:88-153 for device node n (HE uses `score`)
+__device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score) {
+    const std::uint8_t f = a.flags[n];
+    const bool retired = (f & kFlagRetired) != 0;
+    const unsigned long long last = a.last[n];
+    if (last >> 63) set_error(a.st, PBKV_EINVAL, kErrLastAccessRange, n);
+    Key2 k;
+    switch (a.policy) {
+        case PBKV_POLICY_LRU:
+            k = make_key(0, 0.0, last);
+            break;
+        case PBKV_POLICY_LAE:
+            k = retired ? make_key(0, static_cast<double>(a.ever[n]), last) : make_key(1, 0.0, last);
+            break;
+        case PBKV_POLICY_HE:
+            k = retired ? make_key(0, static_cast<double>(a.ever[n]), last) : make_key(1, score, last);
+            break;
+        default: {  // KVFLOW
+            bool miss = false;
+            double d = retired ? CUDART_INF
+                               : kvflow_distance(a.acc_off, a.acc_slot, a.acc_bits, a.rem_off, a.rem_seq, a.rem_has,
+                                                 n, &miss);
+            if (miss) a.missing[n] = 2;
+            k = isinf(d) ? make_key(0, 0.0, last) : make_key(1, -d, last);
+        }
+    }
+    reinterpret_cast<ulonglong2*>(a.keys)[n] = make_ulonglong2(k.w0, k.w1);
+}
+
+// per-node scratch init for the selection (every node, device or not)
+__device__ __forceinline__ void init_select_state(const KeyArgs& a, int n, bool missing) {
+    a.eff[n] = n;
+    a.sublock[n] = 0;
+    a.W[n] = 0ull;
+    a.C[n] = 0u;
+    a.rank[n] = -1;
+    a.missing[n] = missing ? 1 : 0;
+}
+
+}  // namespace dev
+}  // namespace pbkv

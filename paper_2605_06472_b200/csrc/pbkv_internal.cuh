@@ -24,14 +24,14 @@ namespace pbkv {
 
 constexpr std::uint8_t kFlagTierMask = 0x3;
 constexpr std::uint8_t kFlagRetired = 0x4;
-constexpr int kHeavyEntries = 32;  // nodes with more access entries go to the block-per-node path
+constexpr int kMediumMaxChain = 256;  // entries*K above this -> heavy (CTA) path
 
 // first-error-wins device status (kernels never throw)
 struct DevStatus {
-    int code;            // 0 ok, else PBKV_E*
-    int kind;            // which check failed (see kErr*)
-    long long node;      // smallest offending node id (atomicMin)
-    long long aux;       // extra info (e.g. last_access for host ordering)
+    int code;        // 0 ok, else PBKV_E*
+    int kind;        // which check failed (kErr*)
+    long long node;  // smallest offending node id (atomicMin)
+    long long aux;   // extra info (e.g. last_access for host ordering)
 };
 enum : int {
     kErrNone = 0,
@@ -48,10 +48,10 @@ struct ApiError : std::runtime_error {
     ApiError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
 
-#define PBKV_CUDA(call)                                                                          \
-    do {                                                                                         \
-        cudaError_t pbkv_e_ = (call);                                                            \
-        if (pbkv_e_ != cudaSuccess)                                                              \
+#define PBKV_CUDA(call)                                                                                  \
+    do {                                                                                                 \
+        cudaError_t pbkv_e_ = (call);                                                                    \
+        if (pbkv_e_ != cudaSuccess)                                                                      \
             throw ::pbkv::ApiError(PBKV_ECUDA, std::string(#call) + ": " + cudaGetErrorString(pbkv_e_)); \
     } while (0)
 
@@ -59,6 +59,10 @@ template <class T>
 struct DevBuf {
     T* p = nullptr;
     std::size_t cap = 0;  // elements
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     void reserve(std::size_t n) {
         if (n <= cap) return;
         std::size_t c = cap ? cap : 1024;
@@ -101,6 +105,10 @@ template <class T>
 struct PinBuf {
     T* p = nullptr;
     std::size_t cap = 0;
+    PinBuf() = default;
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    ~PinBuf() { release(); }
     void reserve(std::size_t n) {
         if (n <= cap) return;
         std::size_t c = cap ? cap : 1024;
@@ -126,29 +134,36 @@ struct PinBuf {
 // enc() is the order-preserving map of a double onto uint64 (-0.0 folded
 // into +0.0 because std::tie compares them equal).  Lexicographic
 // (w0, w1, id) order == std::tie(cls, rank, last_access, id) order.
-struct Key2 {
+struct alignas(16) Key2 {
     unsigned long long w0, w1;
 };
 
-// Sort record of a head
+// 160-bit sort record of a head (fallback sort path)
 struct HeadKey {
     unsigned long long w0, w1;
     unsigned int id;
 };
 
-// Sort record of a prefetch candidate: value descending, id ascending
+// sort record of a prefetch candidate: value descending, id ascending
 struct CandKey {
     unsigned long long vdesc;
     unsigned int id;
+};
+
+struct SelectCounts {
+    std::int64_t n_victims = 0, freed = 0;
+    int shortfall = 0;
 };
 
 struct Context {
     int device = 0;
     int K = 3;
     double gamma = 0.7;
-    int A = 1;    // agents
-    int V1 = 2;   // outcomes
+    int A = 1;   // agents
+    int V1 = 2;  // outcomes
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // heavy-node scoring, overlapped with the light pass
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
 
     // ---- mirror -------------------------------------------------------------
@@ -156,14 +171,23 @@ struct Context {
     DevBuf<int> parent, len, ever, depth;
     DevBuf<std::uint8_t> flags;
     DevBuf<unsigned long long> last;
-    DevBuf<double> score;        // cached (mirrored) score
+    DevBuf<double> score;  // cached (mirrored) score
     DevBuf<unsigned int> acc_off;
     DevBuf<int> acc_slot;
     DevBuf<unsigned long long> acc_bits;
-    DevBuf<int> heavy;           // nodes with > kHeavyEntries entries
+    std::vector<int> h_entries;  // entries per node (host copy, for id-list classification)
+    // node classes for Eq. 2
+    DevBuf<int> medium;  // 2 < entries, entries*K <= kMediumMaxChain
+    std::int64_t n_medium = 0;
+    DevBuf<int> heavy;  // entries*K > kMediumMaxChain
     std::int64_t n_heavy = 0;
-    std::int64_t device_capacity = 0, device_used = 0, retired_device_tokens = 0, host_capacity = 0,
-                 host_used = 0;
+    DevBuf<unsigned int> hent;    // heavy entries, node-major
+    DevBuf<int> hent_node;        // heavy index of each heavy entry
+    DevBuf<long long> hstart;     // first product of each heavy node
+    DevBuf<double> hxs;           // products of the heavy entries
+    DevBuf<unsigned int> hmiss;   // per heavy node: missing (1) / short horizon (2)
+    std::int64_t n_hent = 0;
+    std::int64_t device_capacity = 0, device_used = 0, retired_device_tokens = 0, host_capacity = 0, host_used = 0;
     int max_depth = 0;
     std::vector<std::int64_t> h_slot_wf;  // slot -> WorkflowId
     std::unordered_map<std::int64_t, int> slot_of;
@@ -177,38 +201,40 @@ struct Context {
     DevBuf<long long> fstage_slot;
 
     // ---- kvflow remaining sequences (per slot CSR) --------------------------
-    DevBuf<int> rem_off;   // [slots+1]
+    DevBuf<int> rem_off;  // [slots+1]
     DevBuf<int> rem_seq;
     DevBuf<std::uint8_t> rem_has;  // per slot
     bool have_remaining = false;
 
-    // ---- scratch --------------------------------------------------------------
-    DevBuf<double> score_rc;       // recomputed scores
+    // ---- selection scratch ----------------------------------------------------
+    DevBuf<double> score_rc;  // recomputed scores
     DevBuf<Key2> keys;
     DevBuf<int> eff;
     DevBuf<int> sublock;
     DevBuf<std::uint8_t> missing;
     DevBuf<unsigned long long> W;
-    DevBuf<int> heads;
-    DevBuf<HeadKey> hk_in, hk_out;
-    DevBuf<unsigned long long> wsorted, wscan;
+    DevBuf<unsigned int> C;
     DevBuf<int> rank;
-    DevBuf<unsigned long long> vkey_in, vkey_out;
-    DevBuf<int> vid_in, vid_out;
-    DevBuf<unsigned long long> vscan;
+    DevBuf<int> heads, listB, listS;
+    DevBuf<unsigned long long> hist;
+    DevBuf<unsigned char> selstate;
+    PinBuf<unsigned char> hselstate;
+    DevBuf<unsigned long long> sortk_in, sortk_out;
+    DevBuf<int> sorti_in, sorti_out;
+    DevBuf<HeadKey> hk_in, hk_out;
+    DevBuf<unsigned long long> cnt;
+    DevBuf<int> vid_out;  // victims in eviction order
     DevBuf<int> locked;
-    DevBuf<int> ids;
+    DevBuf<int> ids, ids2, ids3;
     DevBuf<double> vals;
     DevBuf<CandKey> ck_in, ck_out;
-    DevBuf<double> cv_in, cv_out;  // candidate values carried with keys
+    DevBuf<double> cv_in, cv_out;
     DevBuf<int> sel;
     DevBuf<unsigned char> cub_tmp;
-    DevBuf<long long> counters;    // small device scalars
+    DevBuf<long long> counters;  // small device scalars
     DevBuf<DevStatus> status;
     PinBuf<long long> hcounters;
     PinBuf<DevStatus> hstatus;
-    PinBuf<int> hids;
-    PinBuf<double> hvals;
 
     // launch accounting (pbkv kernels; CUB library calls counted separately)
     long long launches = 0, lib_calls = 0;
@@ -219,26 +245,20 @@ struct Context {
     float last_ms[5] = {0, 0, 0, 0, 0};
 };
 
-// ---- kernels / launchers (implemented in the .cu files) ------------------------
+// ---- launchers (score.cu / select.cu / prefetch.cu) -------------------------------
 void launch_forecast_prepare(Context& c, const double* stage, const long long* slots, std::int64_t n, int H);
-void launch_score_all(Context& c, double* out_dev, bool write_keys, int policy, bool want_missing);
-void launch_score_ids(Context& c, const int* ids_dev, std::int64_t n, double* out_dev, bool value_only);
+void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool report_missing);
+void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int64_t n, double* out, bool value_only);
+void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
 void launch_keys_cached(Context& c, int policy);
-void launch_eff(Context& c, const int* locked_dev, std::int64_t n_locked);
-void launch_weights(Context& c, long long* counters_dev, bool he_recompute);
-void launch_prefetch_candidates(Context& c, long long* counters_dev);
-void launch_prefetch_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev);
+void launch_lock_eff(Context& c, const int* locked_dev, std::int64_t n_locked);
+SelectCounts run_select(Context& c, std::int64_t needed, bool he_recompute, long long* result_dev);
+std::size_t sel_state_bytes();
+void launch_prefetch_candidates(Context& c, unsigned long long* n_cand_dev);
+void launch_prefetch_err_id(Context& c);
+void launch_prefetch_sort_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev);
 void reset_status(Context& c);
 void check_status(Context& c);  // syncs and throws on a device-side error
-
-std::size_t cub_sort_heads_bytes(std::int64_t n);
-void cub_sort_heads(Context& c, std::int64_t n);
-std::size_t cub_scan_bytes(std::int64_t n);
-void cub_scan_u64(Context& c, const unsigned long long* in, unsigned long long* out, std::int64_t n);
-std::size_t cub_sort_pairs_bytes(std::int64_t n);
-void cub_sort_pairs_u64(Context& c, std::int64_t n, int end_bit);
-std::size_t cub_sort_cands_bytes(std::int64_t n);
-void cub_sort_cands(Context& c, std::int64_t n);
 
 inline unsigned int grid_for(std::int64_t n, int block) {
     std::int64_t g = (n + block - 1) / block;

@@ -1,0 +1,552 @@
+// Stage 2 on sm_100a: Eq. 2 (scoring.hpp:49-62) for every node, bit-exact.
+//
+// Nodes are split by their Eq. 2 chain length L = entries * K:
+//   light  (entries <= 2)     one thread per node, chain in registers
+//   medium (L <= 256)         one warp per node: products in parallel, the
+//                             serial add chain from shared memory
+//   heavy  (L > 256)          products for all heavy entries by the whole grid,
+//                             then one CTA per node evaluates the serial
+//                             rounding chain exactly in parallel per binade
+// The heavy path runs on a side stream, overlapped with the light pass.
+#include "common.cuh"
+
+namespace pbkv {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kLightThreads = 256;
+constexpr int kMediumWarps = 8;
+constexpr int kMediumMaxElems = 256;
+constexpr int kChainThreads = 256;
+constexpr int kChainEPT = 8;  // elements per thread per chunk
+constexpr int kChainChunk = kChainThreads * kChainEPT;
+
+// Eq. 2 of one access entry appended to `total` (scoring.hpp:56-59)
+__device__ __forceinline__ void eq2_entry(const ScoreArgs& s, int slot, unsigned long long b, double& total) {
+    const int K = s.K, V1 = s.V1;
+    const double* pw = s.P + static_cast<std::size_t>(slot) * K * V1;
+    const double* g = s.gs + static_cast<std::size_t>(slot) * K;
+    int k = 0;
+    for (; k + 1 < K; k += 2) {
+        double m0, m1;
+        mass_on2(pw + k * V1, pw + (k + 1) * V1, b, m0, m1);
+        const double g0 = __ldg(g + k), g1 = __ldg(g + k + 1);
+        total = __dadd_rn(total, __dmul_rn(g0, m0));
+        total = __dadd_rn(total, __dmul_rn(g1, m1));
+    }
+    if (k < K) total = __dadd_rn(total, __dmul_rn(__ldg(g + k), mass_on(pw + k * V1, b)));
+}
+
+// ---------------------------------------------------------------------------
+template <bool kKeys>
+__global__ void __launch_bounds__(kLightThreads) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
+                                                                    int report_missing) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int n = static_cast<int>(i);
+        const unsigned int e0 = s.acc_off[n], e1 = s.acc_off[n + 1];
+        const bool light = (e1 - e0) <= 2u;
+        double total = 0.0;
+        bool miss = false, shorth = false;
+        if (light) {
+            for (unsigned int e = e0; e < e1; ++e) {
+                const int slot = __ldg(s.acc_slot + e);
+                const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+                const std::uint8_t fs = __ldg(s.fstate + slot);
+                if (fs != 1) {
+                    (fs == 2 ? shorth : miss) = true;
+                    continue;
+                }
+                eq2_entry(s, slot, b, total);
+            }
+            s.out[n] = total;
+            if (report_missing && (miss || shorth))
+                set_error(s.st, PBKV_EINVAL, miss ? kErrMissingForecast : kErrShortHorizon, n);
+        }
+        if constexpr (kKeys) {
+            ka.eff[n] = n;
+            ka.sublock[n] = 0;
+            ka.W[n] = 0ull;
+            ka.C[n] = 0u;
+            ka.rank[n] = -1;
+            if (light) {
+                ka.missing[n] = (miss || shorth) ? 1 : 0;
+                if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, total);
+            }
+        }
+    }
+}
+
+// one warp per medium node: lane l forms products l, l+32, ... of the chain
+// (element i = entry i/K, step i%K), lane 0 then adds them in order.
+template <bool kKeys, bool kValueOnly>
+__global__ void __launch_bounds__(kMediumWarps * 32) score_medium_kernel(ScoreArgs s, KeyArgs ka, const int* nodes,
+                                                                         std::int64_t n_list, int report_missing,
+                                                                         int report_per_node) {
+    __shared__ double xs[kMediumWarps][kMediumMaxElems];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const std::int64_t w = blockIdx.x * static_cast<std::int64_t>(kMediumWarps) + warp;
+    if (w >= n_list) return;
+    const int n = nodes[w];
+    const int K = kValueOnly ? 1 : s.K;
+    const unsigned int e0 = s.acc_off[n], e1 = s.acc_off[n + 1];
+    const int L = static_cast<int>(e1 - e0) * K;
+    int miss = 0;
+    for (int i = lane; i < L; i += 32) {
+        const unsigned int e = e0 + static_cast<unsigned int>(i / K);
+        const int k = i % K;
+        const int slot = __ldg(s.acc_slot + e);
+        const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+        const std::uint8_t fs = __ldg(s.fstate + slot);
+        double x = 0.0;
+        if (kValueOnly ? fs == 0 : fs != 1) {
+            miss |= (fs == 2 && !kValueOnly) ? 2 : 1;
+        } else {
+            const double* row = s.P + (static_cast<std::size_t>(slot) * s.K + k) * s.V1;
+            x = kValueOnly ? mass_on(row, b) : __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k),
+                                                         mass_on(row, b));
+        }
+        xs[warp][i] = x;
+    }
+    miss = __reduce_or_sync(0xffffffffu, miss);
+    __syncwarp();
+    if (lane == 0) {
+        double t = 0.0;
+        for (int i = 0; i < L; ++i) t = __dadd_rn(t, xs[warp][i]);
+        s.out[n] = t;
+        if ((report_missing || report_per_node) && miss)
+            set_error(s.st, PBKV_EINVAL, (miss & 1) ? kErrMissingForecast : kErrShortHorizon, n);
+        if constexpr (kKeys) {
+            ka.missing[n] = miss ? 1 : 0;
+            if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, t);
+        }
+    }
+}
+
+// products of every heavy entry: element j*K + k of the packed product array
+__global__ void __launch_bounds__(256) heavy_products_kernel(ScoreArgs s, const unsigned int* hent,
+                                                             const int* hent_node, std::int64_t n_hent, double* xs,
+                                                             unsigned int* hmiss) {
+    const int K = s.K;
+    const std::int64_t total = n_hent * K;
+    for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t j = t / K;
+        const int k = static_cast<int>(t - j * K);
+        const unsigned int e = hent[j];
+        const int slot = __ldg(s.acc_slot + e);
+        const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+        const std::uint8_t fs = __ldg(s.fstate + slot);
+        double x = 0.0;
+        if (fs != 1) {
+            atomicOr(&hmiss[hent_node[j]], fs == 2 ? 2u : 1u);
+        } else {
+            const double* row = s.P + (static_cast<std::size_t>(slot) * K + k) * s.V1;
+            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * K + k), mass_on(row, b));
+        }
+        xs[t] = x;
+    }
+}
+
+struct SatAdd {
+    __device__ __forceinline__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
+        unsigned long long r = a + b;
+        const unsigned long long cap = 1ull << 62;
+        return (r > cap || r < a) ? cap : r;
+    }
+};
+
+// The serial chain t <- RN(t + x_i), i = 0..L-1, evaluated exactly in
+// parallel.  Inside one binade [2^(E-1), 2^E) with x_i >= 0,
+// RN(t + x_i) = t + u * RN(x_i / u), u = ulp(t), unless x_i / u has a
+// fractional part of exactly 1/2 (then the tie rounds to even, which depends
+// on t).  So a run of steps is an integer prefix sum in units of u.  Binade
+// crossings, exact ties and negative / NaN / huge x_i are "events", executed
+// one at a time with __dadd_rn.  Bit-identical to scoring.hpp:52-60.
+//
+// kPre:  products read from `xs_g` (heavy path);
+// !kPre: products formed in the CTA per chunk (id-list path: refresh_nodes).
+template <bool kPre, bool kValueOnly, bool kKeys>
+__global__ void __launch_bounds__(kChainThreads) chain_kernel(ScoreArgs s, KeyArgs ka, const int* nodes,
+                                                              const long long* xs_start, const double* xs_g,
+                                                              const unsigned int* hmiss, int report_missing) {
+    using Scan = cub::BlockScan<unsigned long long, kChainThreads>;
+    using RedI = cub::BlockReduce<int, kChainThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ typename RedI::TempStorage red_tmp;
+    __shared__ double xs[kChainChunk];
+    __shared__ double t_sh;
+    __shared__ int ev_sh;
+    __shared__ unsigned long long pclean_sh;
+    __shared__ int miss_sh;
+
+    const int node = nodes[blockIdx.x];
+    const int K = kValueOnly ? 1 : s.K;
+    const unsigned int e0 = s.acc_off[node], e1 = s.acc_off[node + 1];
+    const long long L = static_cast<long long>(e1 - e0) * K;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        t_sh = 0.0;
+        miss_sh = kPre ? static_cast<int>(hmiss[blockIdx.x]) : 0;
+    }
+    __syncthreads();
+
+    for (long long c0 = 0; c0 < L; c0 += kChainChunk) {
+        const int nc = static_cast<int>(min(static_cast<long long>(kChainChunk), L - c0));
+        for (int i = tid; i < nc; i += kChainThreads) {
+            if constexpr (kPre) {
+                xs[i] = xs_g[xs_start[blockIdx.x] + c0 + i];
+            } else {
+                const long long gi = c0 + i;
+                const unsigned int e = e0 + static_cast<unsigned int>(gi / K);
+                const int k = static_cast<int>(gi % K);
+                const int slot = __ldg(s.acc_slot + e);
+                const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+                const std::uint8_t fs = __ldg(s.fstate + slot);
+                double x = 0.0;
+                if (kValueOnly ? fs == 0 : fs != 1) {
+                    atomicOr(&miss_sh, (fs == 2 && !kValueOnly) ? 2 : 1);
+                } else {
+                    const double* row = s.P + (static_cast<std::size_t>(slot) * s.K + k) * s.V1;
+                    x = kValueOnly ? mass_on(row, b)
+                                   : __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k),
+                                               mass_on(row, b));
+                }
+                xs[i] = x;
+            }
+        }
+        __syncthreads();
+        int pos = 0;
+        const int i0 = tid * kChainEPT;
+        while (pos < nc) {
+            const double t = t_sh;
+            if (!(t > 0x1p-900 && t < 0x1p+1000)) {  // zero / tiny / huge running total: one serial step
+                if (tid == 0) t_sh = __dadd_rn(t, xs[pos]);
+                __syncthreads();
+                ++pos;
+                continue;
+            }
+            int E;
+            frexp(t, &E);  // t = f * 2^E, f in [0.5, 1): ulp(t) = 2^(E-53)
+            const double scale = ldexp(1.0, 53 - E);
+            const unsigned long long T = static_cast<unsigned long long>(t * scale);  // in [2^52, 2^53)
+            const unsigned long long room = (1ull << 53) - T;
+            auto qof = [&](int i, unsigned long long& q) -> bool {
+                const double y = xs[i] * scale;  // exact power-of-two scaling
+                if (!(y >= 0.0) || y > 0x1p53) return false;
+                if (fabs(y - trunc(y)) == 0.5) return false;  // exact tie
+                q = static_cast<unsigned long long>(rint(y));
+                return true;
+            };
+            unsigned long long local = 0;
+            int first_bad = nc;
+#pragma unroll
+            for (int k = 0; k < kChainEPT; ++k) {
+                const int i = i0 + k;
+                if (i >= nc || i < pos || i >= first_bad) continue;
+                unsigned long long q;
+                if (!qof(i, q))
+                    first_bad = i;
+                else
+                    local = SatAdd()(local, q);
+            }
+            unsigned long long excl;
+            Scan(scan_tmp).ExclusiveScan(local, excl, 0ull, SatAdd());
+            int my_ev = first_bad;
+            unsigned long long run = excl;
+#pragma unroll
+            for (int k = 0; k < kChainEPT; ++k) {
+                const int i = i0 + k;
+                if (i >= nc || i < pos || i >= my_ev) continue;
+                unsigned long long q = 0;
+                qof(i, q);
+                const unsigned long long nxt = SatAdd()(run, q);
+                if (nxt > room)
+                    my_ev = i;  // crossing at i
+                else
+                    run = nxt;
+            }
+            __syncthreads();
+            const int blk_ev = RedI(red_tmp).Reduce(my_ev, cub::Min());
+            if (tid == 0) ev_sh = blk_ev;
+            __syncthreads();
+            const int ev = ev_sh;
+            if (ev > pos && tid == (ev - 1) / kChainEPT) {
+                unsigned long long p = excl;
+                for (int k = 0; k < kChainEPT; ++k) {
+                    const int i = i0 + k;
+                    if (i >= ev) break;
+                    if (i < pos) continue;
+                    unsigned long long q = 0;
+                    qof(i, q);
+                    p = SatAdd()(p, q);
+                }
+                pclean_sh = p;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const unsigned long long pc = ev > pos ? pclean_sh : 0ull;
+                double tn = static_cast<double>(T + pc) / scale;  // exact: <= 2^53 units of ulp
+                if (ev < nc) tn = __dadd_rn(tn, xs[ev]);        // the event step
+                t_sh = tn;
+            }
+            __syncthreads();
+            pos = ev < nc ? ev + 1 : nc;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const double total = t_sh;
+        s.out[node] = total;
+        const int miss = miss_sh;
+        if (report_missing && miss)
+            set_error(s.st, PBKV_EINVAL, (miss & 1) ? kErrMissingForecast : kErrShortHorizon, node);
+        if constexpr (kKeys) {
+            ka.missing[node] = miss ? 1 : 0;
+            if (node != 0 && (ka.flags[node] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, node, total);
+        }
+    }
+}
+
+// Eq. 1 / Eq. 2 of an id list, one thread per short id (refresh_nodes path)
+template <bool kValueOnly>
+__global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* ids, std::int64_t n, double* out) {
+    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int id = ids[j];
+        const unsigned int e0 = s.acc_off[id], e1 = s.acc_off[id + 1];
+        double v = 0.0;
+        bool miss = false, shorth = false;
+        for (unsigned int e = e0; e < e1; ++e) {
+            const int slot = __ldg(s.acc_slot + e);
+            const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+            const std::uint8_t fs = __ldg(s.fstate + slot);
+            if (kValueOnly) {
+                if (fs == 0) {
+                    miss = true;
+                    continue;
+                }
+                v = __dadd_rn(v, mass_on(s.P + static_cast<std::size_t>(slot) * s.K * s.V1, b));
+            } else {
+                if (fs != 1) {
+                    (fs == 2 ? shorth : miss) = true;
+                    continue;
+                }
+                eq2_entry(s, slot, b, v);
+            }
+        }
+        out[id] = v;
+        if (miss || shorth) set_error(s.st, PBKV_EINVAL, miss ? kErrMissingForecast : kErrShortHorizon, id);
+    }
+}
+
+// survival + gs table + validation of uploaded forecast rows (Forecast ctor,
+// forecast.hpp:19-42).  gs[k] = gamma^k * s(k) with gamma^k by repeated
+// multiplication and the product taken in the reference order (g * s),
+// scoring.hpp:56-58, so that gs[k] * m equals (g * s(k)) * m bit for bit.
+__global__ void forecast_prepare_kernel(const double* stage, const long long* slots, std::int64_t n, int H, int V1,
+                                        int K, double gamma, double* P, double* gs, std::uint8_t* fstate,
+                                        DevStatus* st) {
+    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const double* p = stage + static_cast<std::size_t>(j) * H * V1;
+        const long long slot = slots[j];
+        bool bad = false;
+        for (int k = 0; k < H && !bad; ++k) {
+            double sum = 0.0;
+            for (int a = 0; a < V1; ++a) {
+                const double v = p[k * V1 + a];
+                if (v < -1e-12) {
+                    set_error(st, PBKV_EINVAL, kErrForecastNegative, j);
+                    bad = true;
+                    break;
+                }
+                sum = __dadd_rn(sum, v);
+            }
+            if (!bad && fabs(__dsub_rn(sum, 1.0)) > 1e-9) {
+                set_error(st, PBKV_EINVAL, kErrForecastSum, j);
+                bad = true;
+            }
+        }
+        if (bad) continue;
+        double* dst = P + static_cast<std::size_t>(slot) * K * V1;
+        double* g = gs + static_cast<std::size_t>(slot) * K;
+        double surv = 1.0, gk = 1.0;
+        for (int k = 0; k < K; ++k) {
+            if (k < H) {
+                for (int a = 0; a < V1; ++a) dst[k * V1 + a] = p[k * V1 + a];
+                g[k] = __dmul_rn(gk, surv);
+                surv = __dmul_rn(surv, __dsub_rn(1.0, p[k * V1 + V1 - 1]));
+                if (surv < 0.0) surv = 0.0;
+            } else {
+                for (int a = 0; a < V1; ++a) dst[k * V1 + a] = 0.0;
+                g[k] = 0.0;
+            }
+            gk = __dmul_rn(gk, gamma);
+        }
+        fstate[slot] = H >= K ? 1 : 2;
+    }
+}
+
+__global__ void gather_f64_kernel(const double* src, const int* ids, std::int64_t n, double* dst) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[ids[i]];
+}
+
+unsigned int grid_cap(std::int64_t n, int block) {
+    std::int64_t want = (n + block - 1) / block;
+    const std::int64_t cap = 148LL * 16;
+    if (want > cap) want = cap;
+    return static_cast<unsigned int>(want < 1 ? 1 : want);
+}
+
+}  // namespace
+
+ScoreArgs make_score_args(Context& c, double* out) {
+    ScoreArgs s;
+    s.acc_off = c.acc_off.p;
+    s.acc_slot = c.acc_slot.p;
+    s.acc_bits = c.acc_bits.p;
+    s.P = c.P.p;
+    s.gs = c.gs.p;
+    s.fstate = c.fstate.p;
+    s.K = c.K;
+    s.V1 = c.V1;
+    s.amask = c.A >= 64 ? ~0ull : ((1ull << c.A) - 1ull);
+    s.out = out;
+    s.st = c.status.p;
+    return s;
+}
+
+KeyArgs make_key_args(Context& c, int policy) {
+    KeyArgs k;
+    k.parent = c.parent.p;
+    k.len = c.len.p;
+    k.flags = c.flags.p;
+    k.last = c.last.p;
+    k.ever = c.ever.p;
+    k.score_cached = c.score.p;
+    k.acc_off = c.acc_off.p;
+    k.acc_slot = c.acc_slot.p;
+    k.acc_bits = c.acc_bits.p;
+    k.rem_off = c.rem_off.p;
+    k.rem_seq = c.rem_seq.p;
+    k.rem_has = c.rem_has.p;
+    k.keys = c.keys.p;
+    k.eff = c.eff.p;
+    k.sublock = c.sublock.p;
+    k.W = c.W.p;
+    k.C = c.C.p;
+    k.rank = c.rank.p;
+    k.missing = c.missing.p;
+    k.st = c.status.p;
+    k.policy = policy;
+    return k;
+}
+
+void launch_forecast_prepare(Context& c, const double* stage, const long long* slots, std::int64_t n, int H) {
+    forecast_prepare_kernel<<<grid_for(n, 128), 128, 0, c.stream>>>(stage, slots, n, H, c.V1, c.K, c.gamma, c.P.p,
+                                                                   c.gs.p, c.fstate.p, c.status.p);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+// Eq. 2 for every node.  With write_keys the stage-3 per-node state (keys,
+// eff, W, C, rank, missing) is produced in the same passes.
+void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool report_missing) {
+    ScoreArgs s = make_score_args(c, out);
+    KeyArgs ka = make_key_args(c, policy);
+    const int rm = report_missing ? 1 : 0;
+    // heavy path on the side stream, overlapped with the light pass
+    if (c.n_heavy > 0) {
+        PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy) * sizeof(unsigned int), c.side));
+        heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(s, c.hent.p, c.hent_node.p,
+                                                                               c.n_hent, c.hxs.p, c.hmiss.p);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+        if (write_keys)
+            chain_kernel<true, false, true><<<static_cast<unsigned int>(c.n_heavy), kChainThreads, 0, c.side>>>(
+                s, ka, c.heavy.p, c.hstart.p, c.hxs.p, c.hmiss.p, rm);
+        else
+            chain_kernel<true, false, false><<<static_cast<unsigned int>(c.n_heavy), kChainThreads, 0, c.side>>>(
+                s, ka, c.heavy.p, c.hstart.p, c.hxs.p, c.hmiss.p, rm);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+        PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
+    }
+    if (write_keys)
+        score_light_kernel<true><<<grid_cap(c.n, kLightThreads), kLightThreads, 0, c.stream>>>(s, ka, c.n, rm);
+    else
+        score_light_kernel<false><<<grid_cap(c.n, kLightThreads), kLightThreads, 0, c.stream>>>(s, ka, c.n, rm);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+    if (c.n_medium > 0) {
+        const unsigned int g = static_cast<unsigned int>((c.n_medium + kMediumWarps - 1) / kMediumWarps);
+        if (write_keys)
+            score_medium_kernel<true, false><<<g, kMediumWarps * 32, 0, c.stream>>>(s, ka, c.medium.p, c.n_medium, rm,
+                                                                                   0);
+        else
+            score_medium_kernel<false, false><<<g, kMediumWarps * 32, 0, c.stream>>>(s, ka, c.medium.p, c.n_medium,
+                                                                                    rm, 0);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+    }
+    if (c.n_heavy > 0) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+}
+
+// Eq. 2 / Eq. 1 of an id list, results scattered into out[id]
+void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int64_t n, double* out, bool value_only) {
+    ScoreArgs s = make_score_args(c, out);
+    KeyArgs ka = make_key_args(c, PBKV_POLICY_HE);
+    // classify on the host: ids with long chains go to the CTA chain kernel
+    std::vector<int> longs;
+    std::vector<int> shorts;
+    const int K = value_only ? 1 : c.K;
+    for (std::int64_t j = 0; j < n; ++j) {
+        const int id = h_ids[j];
+        const std::int64_t L = static_cast<std::int64_t>(c.h_entries[static_cast<std::size_t>(id)]) * K;
+        (L > kMediumMaxElems ? longs : shorts).push_back(id);
+    }
+    if (!shorts.empty()) {
+        c.ids2.reserve(shorts.size());
+        PBKV_CUDA(cudaMemcpyAsync(c.ids2.p, shorts.data(), shorts.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                  c.stream));
+        const std::int64_t m = static_cast<std::int64_t>(shorts.size());
+        if (value_only)
+            score_ids_kernel<true><<<grid_cap(m, 256), 256, 0, c.stream>>>(s, c.ids2.p, m, out);
+        else
+            score_ids_kernel<false><<<grid_cap(m, 256), 256, 0, c.stream>>>(s, c.ids2.p, m, out);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+    }
+    if (!longs.empty()) {
+        c.ids3.reserve(longs.size());
+        PBKV_CUDA(cudaMemcpyAsync(c.ids3.p, longs.data(), longs.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                  c.stream));
+        const unsigned int g = static_cast<unsigned int>(longs.size());
+        if (value_only)
+            chain_kernel<false, true, false><<<g, kChainThreads, 0, c.stream>>>(s, ka, c.ids3.p, nullptr, nullptr,
+                                                                                nullptr, 1);
+        else
+            chain_kernel<false, false, false><<<g, kChainThreads, 0, c.stream>>>(s, ka, c.ids3.p, nullptr, nullptr,
+                                                                                 nullptr, 1);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+    }
+    (void)ids_dev;
+}
+
+void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst) {
+    gather_f64_kernel<<<grid_cap(n, 256), 256, 0, c.stream>>>(src, ids, n, dst);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+// Eq. 1 for the host-tier candidates is evaluated inside prefetch.cu with the
+// same helpers; this hook keeps the value path for id lists.
+}  // namespace pbkv
