@@ -267,11 +267,11 @@ def main():
         step()
         stage += np.array(pol.timings())
     stage /= n_stage
+    select_phases = [round(x, 2) for x in pol.phase_times_us()]
     pol.set_timing(False)
 
     # ---- e2e through the host C ABI -------------------------------------------------
     P_pinned = torch.from_numpy(np.ascontiguousarray(P)).pin_memory().numpy()
-    locked_list = locked.tolist()
     e2e_ms = []
     n_victims_e2e = 0
     for _ in range(max(1, args.steps)):
@@ -281,7 +281,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         pol.put_forecasts(wf, P_pinned)
-        sel = pol.select_victims_hierarchical(needed, locked=locked_list, score_mode=SCORE_RECOMPUTE)
+        sel = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
@@ -335,8 +335,9 @@ def main():
                    "parallelism": f"replicas x{world}" if world > 1 else "single"},
         "p99_decision_ms": p99,
         "p50_decision_ms": float(np.percentile(per_step, 50)),
-        "stage_ms": {"score_keys": float(stage[0]), "lock_eff_weights": float(stage[1]),
-                     "cut_sort": float(stage[2]), "total": float(stage[4])},
+        "stage_ms": {"score_keys": float(stage[0]), "select": float(stage[1]), "total": float(stage[4])},
+        "select_phases_us": {"note": "lock, eff, weights, [hist+reduce, pick+compact] x passes, cut-head, "
+                                     "sort, scatter, cut", "us": select_phases},
         "roofline": {"bound": "hbm", "kernel": "score_light_kernel<true>+heavy_score_kernel (fused Eq.2 + keys)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,

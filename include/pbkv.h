@@ -127,6 +127,9 @@ int pbkv_ctx_stream(pbkv_ctx* ctx, void** stream_out);     /* the ctx's cudaStre
  * the ctx stream): [0]=score [1]=keys+eff [2]=cut/sort [3]=prefetch [4]=total. */
 int pbkv_ctx_timings(pbkv_ctx* ctx, float* ms5);
 int pbkv_ctx_set_timing(pbkv_ctx* ctx, int enabled);
+/* %globaltimer stamps (ns) taken by the selection kernel at its phase
+ * boundaries during the most recent selection (diagnostics). */
+int pbkv_ctx_phase_times(pbkv_ctx* ctx, uint64_t* ns, int cap, int* n);
 /* Cumulative launch counts: pbkv's own kernels, and CUB library calls. */
 int pbkv_ctx_launches(pbkv_ctx* ctx, int64_t* kernels, int64_t* lib_calls);
 

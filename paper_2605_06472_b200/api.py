@@ -230,11 +230,19 @@ class Policy:
             if remaining is None:
                 raise ValidationError("kvflow selected without static sequences")
             self.set_remaining(remaining)
-        lk_list = sorted(set(int(x) for x in locked))
-        lk = np.ascontiguousarray(lk_list or [0], dtype=np.int32)
-        n_lk = len(lk_list)
+        if isinstance(locked, np.ndarray):  # fast path: any order, duplicates allowed by the C ABI
+            lk = np.ascontiguousarray(locked, dtype=np.int32)
+            n_lk = int(lk.size)
+            if n_lk == 0:
+                lk = np.zeros(1, dtype=np.int32)
+        else:
+            lk_list = sorted(set(int(x) for x in locked))
+            lk = np.ascontiguousarray(lk_list or [0], dtype=np.int32)
+            n_lk = len(lk_list)
         cap = max(self.n_nodes, 1)
-        victims = np.zeros(cap, dtype=np.int32)
+        victims = getattr(self, "_vbuf", None)
+        if victims is None or victims.size < cap:
+            victims = self._vbuf = np.empty(cap, dtype=np.int32)
         nv, fr, sf = C.c_int64(), C.c_int64(), C.c_int()
         self._c(_abi.lib().pbkv_select(self._h, int(policy), int(score_mode), int(needed), ptr(lk, C.c_int32), n_lk,
                                        ptr(victims, C.c_int32), cap, C.byref(nv), C.byref(fr), C.byref(sf)))
@@ -295,6 +303,14 @@ class Policy:
         k, l = C.c_int64(), C.c_int64()
         self._c(_abi.lib().pbkv_ctx_launches(self._h, C.byref(k), C.byref(l)))
         return k.value, l.value
+
+    def phase_times_us(self) -> list[float]:
+        """Durations between the selection kernel's phase stamps (microseconds)."""
+        buf = (C.c_uint64 * 32)()
+        n = C.c_int()
+        self._c(_abi.lib().pbkv_ctx_phase_times(self._h, buf, 32, C.byref(n)))
+        ts = list(buf)[: min(n.value, 32)]
+        return [(b - a) / 1000.0 for a, b in zip(ts, ts[1:])]
 
     def stream_handle(self) -> int:
         s = C.c_void_p()

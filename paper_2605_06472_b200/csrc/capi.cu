@@ -407,11 +407,9 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
     else
         launch_keys_cached(c, policy);
     record(c, 1);
-    launch_lock_eff(c, locked_dev, n_locked);
+    SelectCounts o = run_select(c, locked_dev, n_locked, needed, recompute, result_dev);
     record(c, 2);
-    SelectCounts o = run_select(c, needed, recompute, result_dev);
-    record(c, 3);
-    finish_timing(c, 3);
+    finish_timing(c, 2);
     return o;
 }
 
@@ -473,8 +471,7 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         c->selstate.reserve(sel_state_bytes());
-        c->hselstate.reserve(sel_state_bytes());
-        c->hist.reserve(1 << 11);
+        c->hselstate.reserve(2 * sel_state_bytes());  // [0] readback, [1] initial-state template
         c->counters.reserve(16);
         c->status.reserve(1);
         c->hcounters.reserve(16);
@@ -530,6 +527,14 @@ int pbkv_ctx_set_timing(pbkv_ctx* c, int enabled) {
     return api(c, [&] {
         need(c, "null ctx");
         c->timing = enabled != 0;
+    });
+}
+
+int pbkv_ctx_phase_times(pbkv_ctx* c, uint64_t* ns, int cap, int* n) {
+    return api(c, [&] {
+        need(c && n, "null argument");
+        *n = static_cast<int>(c->phase_ns.size());
+        for (int i = 0; i < *n && i < cap; ++i) ns[i] = c->phase_ns[static_cast<std::size_t>(i)];
     });
 }
 

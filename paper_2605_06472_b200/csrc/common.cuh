@@ -210,13 +210,11 @@ __device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score)
     reinterpret_cast<ulonglong2*>(a.keys)[n] = make_ulonglong2(k.w0, k.w1);
 }
 
-// per-node scratch init for the selection (every node, device or not)
+// per-node scratch init for the selection (every node, device or not); the
+// per-head fields (W, C, rank) are written by the selection kernel itself
 __device__ __forceinline__ void init_select_state(const KeyArgs& a, int n, bool missing) {
     a.eff[n] = n;
     a.sublock[n] = 0;
-    a.W[n] = 0ull;
-    a.C[n] = 0u;
-    a.rank[n] = -1;
     a.missing[n] = missing ? 1 : 0;
 }
 

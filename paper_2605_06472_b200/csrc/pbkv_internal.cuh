@@ -216,7 +216,9 @@ struct Context {
     DevBuf<unsigned int> C;
     DevBuf<int> rank;
     DevBuf<int> heads, listB, listS;
-    DevBuf<unsigned long long> hist;
+    DevBuf<unsigned long long> hist_w, part_w;
+    DevBuf<unsigned int> hist_c, part_c, seg_off, seg_cnt, cursor;
+    std::vector<unsigned long long> phase_ns;  // select-kernel phase timestamps of the last call
     DevBuf<unsigned char> selstate;
     PinBuf<unsigned char> hselstate;
     DevBuf<unsigned long long> sortk_in, sortk_out;
@@ -251,8 +253,8 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
 void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int64_t n, double* out, bool value_only);
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
 void launch_keys_cached(Context& c, int policy);
-void launch_lock_eff(Context& c, const int* locked_dev, std::int64_t n_locked);
-SelectCounts run_select(Context& c, std::int64_t needed, bool he_recompute, long long* result_dev);
+SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked, std::int64_t needed,
+                        bool he_recompute, long long* result_dev);
 std::size_t sel_state_bytes();
 void launch_prefetch_candidates(Context& c, unsigned long long* n_cand_dev);
 void launch_prefetch_err_id(Context& c);

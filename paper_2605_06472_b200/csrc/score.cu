@@ -68,9 +68,6 @@ __global__ void __launch_bounds__(kLightThreads) score_light_kernel(ScoreArgs s,
         if constexpr (kKeys) {
             ka.eff[n] = n;
             ka.sublock[n] = 0;
-            ka.W[n] = 0ull;
-            ka.C[n] = 0u;
-            ka.rank[n] = -1;
             if (light) {
                 ka.missing[n] = (miss || shorth) ? 1 : 0;
                 if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, total);

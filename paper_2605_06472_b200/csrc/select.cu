@@ -5,16 +5,36 @@
 //   victims = shortest prefix with sum(len) >= needed.
 // The nodes sharing one eff value h ("chain of head h") form a contiguous
 // ancestor path starting at h, so the order is: heads sorted by key, each
-// followed by its chain in d order.  Pipeline:
-//   keys (score.cu or keys_cached) -> lock marks -> eff (CAS walk-up) ->
-//   weights (W[h] tokens, C[h] nodes, head list) -> weighted MSD radix select
-//   on the head keys -> sort of the selected heads only -> chain scatter.
+// followed by its chain in d order.
+//
+// The whole selection after the keys is ONE persistent kernel (two 512-thread
+// CTAs per SM, co-resident by cooperative launch, phases separated by grid
+// barriers):
+//   lock marks -> eff (CAS walk-up) -> chains (each head walks its own chain:
+//   token weight W[h], size C[h]; no atomics) -> weighted MSD radix select on
+//   the head keys: 11-bit digits at the top varying bit of the surviving
+//   candidates, per-CTA partial histograms reduced across the grid; heads
+//   below the chosen digit are placed into their digit's bucket of the
+//   selected list S (counting sort), so S is ordered bucket by bucket ->
+//   every bucket sorted by one CTA in shared memory (bitonic on
+//   order-preserving packed keys) -> chain starts (scan of chain sizes) ->
+//   chain scatter -> cut.
+// No host round trip in the common case.  A bucket larger than one CTA's
+// sort (or keys with >= 64 varying bits) falls back to a device-wide CUB
+// sort of S driven from the host.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <cuda/std/tuple>
 
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pbkv {
 
@@ -25,8 +45,12 @@ KeyArgs make_key_args(Context& c, int policy);
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kPThreads = 512;  // persistent CTA (two per SM)
 constexpr int kDigitBits = 11;
 constexpr int kBins = 1 << kDigitBits;
+constexpr int kMaxPasses = 16;
+constexpr int kBucketCap = 4096;  // bucket sorted by one CTA in shared memory
+constexpr int kScanIPT = 8;       // chain-start scan: items per thread per chunk
 
 unsigned int grid_cap(std::int64_t n, int block) {
     std::int64_t want = (n + block - 1) / block;
@@ -44,71 +68,30 @@ __global__ void __launch_bounds__(kThreads) keys_cached_kernel(KeyArgs ka, std::
     }
 }
 
-// A locked DEVICE node makes itself and all of its ancestors ineligible: in
-// the greedy frontier (policies.hpp:56-79) it is never pushed, so no
-// ancestor's virtual device-child count can reach zero.
-__global__ void lock_kernel(const int* locked, std::int64_t n_locked, const int* parent, const std::uint8_t* flags,
-                            int* sublock, std::int64_t n_nodes) {
-    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < n_locked;
-         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        int v = locked[j];
-        if (v <= 0 || v >= n_nodes) continue;
-        if ((flags[v] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
-        while (v > 0) {
-            if (atomicExch(&sublock[v], 1) == 1) break;
-            v = parent[v];
-        }
-    }
-}
-
-// eff: every device node walks its key up the ancestor chain, CAS-ing the
-// ancestors' argmax id; a walk stops at the first ancestor already holding a
-// larger key (its holder carries it further), so eff ends as the exact
-// subtree maximum.
-__global__ void __launch_bounds__(kThreads) eff_kernel(const int* parent, const std::uint8_t* flags,
-                                                       const Key2* keys, int* eff, std::int64_t n_nodes) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const int n = static_cast<int>(i);
-        if (n == 0 || (flags[n] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
-        const Key2 km = load_key(keys, n);
-        int p = parent[n];
-        while (p > 0) {
-            int cur = *reinterpret_cast<volatile int*>(&eff[p]);
-            bool advanced = false;
-            for (;;) {
-                const Key2 kc = load_key(keys, cur);
-                if (!key_less(kc, cur, km, n)) break;
-                const int old = atomicCAS(&eff[p], cur, n);
-                if (old == cur) {
-                    advanced = true;
-                    break;
-                }
-                cur = old;
-            }
-            if (!advanced) break;
-            p = parent[p];
-        }
-    }
-}
-
-// selection state shared by the select kernels (device memory)
+// selection state (device memory)
 struct SelState {
-    unsigned long long need_rem;   // tokens still needed beyond the selected heads
-    unsigned long long total_tok;  // all eligible tokens
-    unsigned long long n_L, n_L2;  // candidate list sizes (current, next)
-    unsigned long long n_S;        // selected heads
-    unsigned long long or_L[3], and_L[3];    // bitwise OR / AND of the current candidates' keys
-    unsigned long long or_L2[3], and_L2[3];  // ... of the next candidates
-    unsigned long long or_S[3], and_S[3];    // ... of the selected heads
-    int lo_bit;       // digit = key bits [lo_bit, lo_bit + kDigitBits)
-    int bucket;       // chosen digit value
-    int take_all;     // eligible total < needed: every head selected
-    int done;
+    unsigned long long need_final;  // tokens needed from the cut chain
+    unsigned long long total_tok;   // all eligible tokens
+    unsigned long long n_L[2];      // candidate list sizes by pass parity
+    unsigned long long or_L[2][3], and_L[2][3];
+    unsigned long long n_S;
+    unsigned long long or_S[3], and_S[3];
+    int n_pass, take_all, host_sort, s_is_heads;
+    int cut_head, max_bucket;
     unsigned long long n_victims, freed;
-    int shortfall;
-    int cut_head;
+    int shortfall, n_ts;
+    unsigned long long ts[40];  // %globaltimer after each phase (diagnostics)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void stamp(SelState* ss) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ss->n_ts < 40) ss->ts[ss->n_ts++] = gtimer();
+}
 
 __device__ __forceinline__ unsigned long long key_word(const Key2& k, int id, int w) {
     return w == 0 ? k.w0 : (w == 1 ? k.w1 : static_cast<unsigned long long>(static_cast<unsigned int>(id)));
@@ -116,98 +99,26 @@ __device__ __forceinline__ unsigned long long key_word(const Key2& k, int id, in
 
 // bits [lo, lo+n) of the 160-bit key (w0:64 | w1:64 | id:32), bit 0 = id LSB
 __device__ __forceinline__ unsigned int key_bits(const Key2& k, int id, int lo, int n) {
-    unsigned long long out = 0;
-    for (int b = 0; b < n; ++b) {
-        const int pos = lo + b;
-        unsigned long long bit;
-        if (pos < 32)
-            bit = (static_cast<unsigned int>(id) >> pos) & 1u;
-        else if (pos < 96)
-            bit = (k.w1 >> (pos - 32)) & 1ull;
-        else
-            bit = (k.w0 >> (pos - 96)) & 1ull;
-        out |= bit << b;
+    unsigned long long win;
+    if (lo >= 96) {
+        win = k.w0 >> (lo - 96);
+    } else if (lo >= 32) {
+        const int s = lo - 32;
+        win = (k.w1 >> s) | (s ? (k.w0 << (64 - s)) : 0ull);
+    } else {
+        win = (static_cast<unsigned long long>(static_cast<unsigned int>(id)) >> lo) | (k.w1 << (32 - lo));
     }
-    return static_cast<unsigned int>(out);
+    return static_cast<unsigned int>(win & ((1ull << n) - 1ull));
 }
 
-template <class Op>
-__device__ __forceinline__ unsigned long long block_reduce_bits(unsigned long long v, Op op,
-                                                                unsigned long long* sh /*[32]*/) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    const int nw = (blockDim.x + 31) >> 5;
-    if (warp == 0) {
-        v = lane < nw ? sh[lane] : sh[0];
-        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-    }
-    __syncthreads();
-    return v;  // valid in warp 0
-}
-
-struct OrOp {
-    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a | b; }
-};
-struct AndOp {
-    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a & b; }
-};
-
-// token weight and node count of every chain, head list, eligible tokens,
-// OR/AND of the head keys (first radix pass)
-__global__ void __launch_bounds__(kThreads) weights_kernel(const int* len, const std::uint8_t* flags,
-                                                           const int* sublock, const int* eff,
-                                                           const std::uint8_t* missing, const Key2* keys,
-                                                           unsigned long long* W, unsigned int* C, int* heads,
-                                                           SelState* ss, DevStatus* st, std::int64_t n_nodes,
-                                                           int he_recompute) {
-    __shared__ unsigned long long sh[32];
-    unsigned long long tok = 0;
-    unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < n_nodes; base += stride) {
-        const std::int64_t i = base + threadIdx.x;
-        const int n = static_cast<int>(i);
-        bool elig = false;
-        int h = -1;
-        if (i < n_nodes && n != 0 && (flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE && !sublock[n]) {
-            elig = true;
-            if (missing[n] == 2) set_error(st, PBKV_EINVAL, kErrKvflowMissing, n);
-            if (he_recompute && missing[n] && !(flags[n] & kFlagRetired))
-                set_error(st, PBKV_EINVAL, kErrMissingForecast, n);
-            h = eff[n];
-            atomicAdd(&W[h], static_cast<unsigned long long>(len[n]));
-            atomicAdd(&C[h], 1u);
-            tok += static_cast<unsigned long long>(len[n]);
-        }
-        const bool head = elig && h == n;
-        const long long slot = warp_append(&ss->n_L, head);
-        if (head) {
-            heads[slot] = n;
-            const Key2 k = load_key(keys, n);
-            for (int w = 0; w < 3; ++w) {
-                const unsigned long long x = key_word(k, n, w);
-                or3[w] |= x;
-                and3[w] &= x;
-            }
-        }
-    }
-    using Red = cub::BlockReduce<unsigned long long, kThreads>;
-    __shared__ typename Red::TempStorage tmp;
-    const unsigned long long blk = Red(tmp).Sum(tok);
-    if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
+// cross-CTA state is read through L2 (ld.global.cg): the barrier orders the
+// writes but does not invalidate L1
+__device__ __forceinline__ int top_varying_bit_cg(const unsigned long long* o_, const unsigned long long* a_) {
+    unsigned long long o[3], a[3];
     for (int w = 0; w < 3; ++w) {
-        const unsigned long long o = block_reduce_bits(or3[w], OrOp(), sh);
-        const unsigned long long a = block_reduce_bits(and3[w], AndOp(), sh);
-        if (threadIdx.x == 0) {
-            if (o) atomicOr(&ss->or_L[w], o);
-            if (~a) atomicAnd(&ss->and_L[w], a);
-        }
+        o[w] = __ldcg(o_ + w);
+        a[w] = __ldcg(a_ + w);
     }
-}
-
-__device__ __forceinline__ int top_varying_bit(const unsigned long long* o, const unsigned long long* a) {
     const unsigned long long v0 = o[0] ^ a[0], v1 = o[1] ^ a[1], v2 = (o[2] ^ a[2]) & 0xffffffffull;
     if (v0) return 96 + 63 - __clzll(static_cast<long long>(v0));
     if (v1) return 32 + 63 - __clzll(static_cast<long long>(v1));
@@ -215,96 +126,383 @@ __device__ __forceinline__ int top_varying_bit(const unsigned long long* o, cons
     return -1;
 }
 
-// weighted histogram of the next digit over the candidate list
-__global__ void __launch_bounds__(kThreads) hist_kernel(const int* L, const Key2* keys, const unsigned long long* W,
-                                                        SelState* ss, unsigned long long* hist) {
-    __shared__ unsigned long long h[kBins];
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+template <class Op>
+__device__ __forceinline__ unsigned long long block_reduce_bits(unsigned long long v, Op op,
+                                                                unsigned long long* sh /*[32]*/) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
     __syncthreads();
-    const unsigned long long n = ss->n_L;
-    const int top = top_varying_bit(ss->or_L, ss->and_L);
-    const int lo = top - kDigitBits + 1 < 0 ? 0 : top - kDigitBits + 1;
-    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
-        const int x = L[i];
-        const unsigned int d = key_bits(load_key(keys, x), x, lo, kDigitBits);
-        atomicAdd(&h[d], W[x]);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    if (warp == 0) {
+        v = lane < nw ? sh[lane] : Op::identity();
+        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
-        if (h[b]) atomicAdd(&hist[b], h[b]);
+    return v;  // valid in warp 0
 }
 
-// single CTA: the bucket where the cumulative weight reaches need_rem
-__global__ void __launch_bounds__(1024) pick_kernel(SelState* ss, unsigned long long* hist) {
-    using Scan = cub::BlockScan<unsigned long long, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ int pick;
-    const int top = top_varying_bit(ss->or_L, ss->and_L);
-    const int lo = top - kDigitBits + 1 < 0 ? 0 : top - kDigitBits + 1;
-    constexpr int kPer = kBins / 1024;
-    unsigned long long v[kPer], sum = 0;
-    for (int j = 0; j < kPer; ++j) {
-        v[j] = hist[threadIdx.x * kPer + j];
-        sum += v[j];
+struct OrOp {
+    __device__ static unsigned long long identity() { return 0ull; }
+    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a | b; }
+};
+struct AndOp {
+    __device__ static unsigned long long identity() { return ~0ull; }
+    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a & b; }
+};
+struct SumOp {
+    __device__ static unsigned long long identity() { return 0ull; }
+    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a + b; }
+};
+struct MaxOp {
+    __device__ static unsigned long long identity() { return 0ull; }
+    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a > b ? a : b; }
+};
+
+__device__ __forceinline__ void flush_orand(const unsigned long long* or3, const unsigned long long* and3,
+                                            unsigned long long* gor, unsigned long long* gand,
+                                            unsigned long long* sh) {
+    for (int w = 0; w < 3; ++w) {
+        const unsigned long long o = block_reduce_bits(or3[w], OrOp(), sh);
+        if (threadIdx.x == 0 && o) atomicOr(&gor[w], o);
+        const unsigned long long a = block_reduce_bits(and3[w], AndOp(), sh);
+        if (threadIdx.x == 0 && ~a) atomicAnd(&gand[w], a);
     }
-    unsigned long long excl;
-    Scan(tmp).ExclusiveSum(sum, excl);
-    if (threadIdx.x == 0) pick = -1;
-    __syncthreads();
-    const unsigned long long need = ss->need_rem;
-    unsigned long long run = excl;
-    for (int j = 0; j < kPer; ++j) {
-        if (run < need && run + v[j] >= need) {
-            pick = threadIdx.x * kPer + j;
-            ss->need_rem = need - run;
-        }
-        run += v[j];
-    }
+}
+
+// CTA-aggregated append: one global atomic per CTA and call (a grid-wide
+// stream of warp-level atomics on one counter serialises in its L2 slice).
+// Must be called by every thread of the CTA.
+__device__ __forceinline__ long long block_append(unsigned long long* counter, bool pred, unsigned int* wcount,
+                                                  unsigned long long* base_sh) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) wcount[warp] = static_cast<unsigned int>(__popc(mask));
     __syncthreads();
     if (threadIdx.x == 0) {
-        ss->lo_bit = lo;
-        ss->bucket = pick;  // always found: total of L >= need_rem
-        ss->n_L2 = 0;
-        for (int w = 0; w < 3; ++w) {
-            ss->or_L2[w] = 0;
-            ss->and_L2[w] = ~0ull;
+        unsigned int s = 0;
+        for (int w = 0; w < nw; ++w) {
+            const unsigned int c = wcount[w];
+            wcount[w] = s;
+            s += c;
         }
+        *base_sh = s ? atomicAdd(counter, static_cast<unsigned long long>(s)) : 0ull;
     }
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x) hist[b] = 0;  // ready for the next pass
+    __syncthreads();
+    const long long slot =
+        pred ? static_cast<long long>(*base_sh + wcount[warp] + __popc(mask & ((1u << lane) - 1u))) : -1;
+    __syncthreads();
+    return slot;
 }
 
-// split the candidates: below the bucket -> selected S, in the bucket -> L2
-__global__ void __launch_bounds__(kThreads) compact_kernel(const int* L, const Key2* keys, SelState* ss, int* L2,
-                                                           int* S) {
-    __shared__ unsigned long long sh[32];
-    const unsigned long long n = ss->n_L;
-    const int lo = ss->lo_bit, b = ss->bucket;
+// order-preserving packing of the varying bits of (w0, w1, id) into 64 bits
+__device__ __forceinline__ unsigned long long pack_key(const Key2& k, int id, unsigned long long v0,
+                                                       unsigned long long v1, unsigned long long v2) {
+    unsigned long long r = 0;
+    auto ext = [&](unsigned long long word, unsigned long long mask) {
+        while (mask) {
+            const int b = 63 - __clzll(static_cast<long long>(mask));
+            r = (r << 1) | ((word >> b) & 1ull);
+            mask &= ~(1ull << b);
+        }
+    };
+    ext(k.w0, v0);
+    ext(k.w1, v1);
+    ext(static_cast<unsigned long long>(static_cast<unsigned int>(id)), v2);
+    return r;
+}
+
+struct SelArgs {
+    const int* parent;
+    const int* len;
+    const std::uint8_t* flags;
+    const int* depth;
+    const Key2* keys;
+    int* eff;
+    int* sublock;
+    const std::uint8_t* missing;
+    unsigned long long* W;
+    unsigned int* C;
+    int* rank;
+    int* heads;
+    int* listB;
+    int* listS;
+    int* sorted;
+    unsigned long long* start;
+    int* victims;
+    unsigned long long* hist_w;       // [kBins] reduced weights
+    unsigned int* hist_c;             // [kBins] reduced counts
+    unsigned long long* part_w;       // [grid][kBins] per-CTA partials
+    unsigned int* part_c;             // [grid][kBins]
+    unsigned int* seg_off;            // [kMaxPasses][kBins] bucket start in S
+    unsigned int* seg_cnt;            // [kMaxPasses][kBins] bucket size
+    unsigned int* cursor;             // [kMaxPasses][kBins] placement cursors
+    SelState* ss;
+    DevStatus* st;
+    long long* result;
+    const int* locked;
+    long long n_locked;
+    long long n_nodes;
+    long long needed;
+    int he_recompute;
+};
+
+// ---- phases ---------------------------------------------------------------------
+
+// a locked DEVICE node makes itself and all of its ancestors ineligible: in the
+// greedy frontier (policies.hpp:56-79) it is never pushed, so no ancestor's
+// virtual device-child count can reach zero
+__device__ __forceinline__ void phase_lock(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
+    for (std::int64_t j = tid; j < a.n_locked; j += nthr) {
+        int v = a.locked[j];
+        if (v <= 0 || v >= a.n_nodes) continue;
+        if ((a.flags[v] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
+        while (v > 0) {
+            if (atomicExch(&a.sublock[v], 1) == 1) break;
+            v = a.parent[v];
+        }
+    }
+    for (std::int64_t j = tid; j < static_cast<std::int64_t>(kMaxPasses) * kBins; j += nthr) a.cursor[j] = 0;
+}
+
+// eff: every device node walks its key up the ancestor chain, CAS-ing the
+// ancestors' argmax id; a walk stops at the first ancestor already holding a
+// larger key (its holder carries it further), so eff ends as the exact
+// subtree maximum
+__device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
+    for (std::int64_t i = tid; i < a.n_nodes; i += nthr) {
+        const int n = static_cast<int>(i);
+        if (n == 0 || (a.flags[n] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
+        const Key2 km = load_key(a.keys, n);
+        int p = a.parent[n];
+        while (p > 0) {
+            int cur = atomicAdd(&a.eff[p], 0);
+            bool advanced = false;
+            for (;;) {
+                const Key2 kc = load_key(a.keys, cur);
+                if (!key_less(kc, cur, km, n)) break;
+                const int old = atomicCAS(&a.eff[p], cur, n);
+                if (old == cur) {
+                    advanced = true;
+                    break;
+                }
+                cur = old;
+            }
+            if (!advanced) break;
+            p = a.parent[p];
+        }
+    }
+}
+
+// heads (eligible n with eff(n) == n) walk their own chain -- the contiguous
+// eligible ancestors with the same eff -- for its token weight W and size C;
+// head list, eligible tokens, OR/AND of the head keys (first radix pass)
+__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh) {
+    SelState* ss = a.ss;
+    unsigned long long tok = 0;
+    unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes; base += stride) {
+        const std::int64_t i = base + threadIdx.x;
+        const int n = static_cast<int>(i);
+        bool head = false;
+        if (i < a.n_nodes && n != 0 && (a.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE && !__ldcg(&a.sublock[n])) {
+            const std::uint8_t ms = a.missing[n];
+            if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n);
+            if (a.he_recompute && ms && !(a.flags[n] & kFlagRetired))
+                set_error(a.st, PBKV_EINVAL, kErrMissingForecast, n);
+            head = __ldcg(&a.eff[n]) == n;
+        }
+        const long long slot = block_append(&ss->n_L[0], head, reinterpret_cast<unsigned int*>(sh), sh + 31);
+        if (head) {
+            unsigned long long w = 0;
+            unsigned int c = 0;
+            int p = n;
+            do {
+                w += static_cast<unsigned long long>(a.len[p]);
+                ++c;
+                p = a.parent[p];
+            } while (p > 0 && !__ldcg(&a.sublock[p]) && __ldcg(&a.eff[p]) == n);
+            a.W[n] = w;
+            a.C[n] = c;
+            a.rank[n] = -1;
+            tok += w;
+            a.heads[slot] = n;
+            const Key2 k = load_key(a.keys, n);
+            for (int wd = 0; wd < 3; ++wd) {
+                const unsigned long long x = key_word(k, n, wd);
+                or3[wd] |= x;
+                and3[wd] &= x;
+            }
+        }
+    }
+    const unsigned long long blk = block_reduce_bits(tok, SumOp(), sh);
+    if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
+    flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
+}
+
+// per-CTA weight and count histograms of the next digit over the candidates
+__device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsigned long long n_L, int lo,
+                                           unsigned long long* hw, unsigned int* hc) {
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+        hw[b] = 0;
+        hc[b] = 0;
+    }
+    __syncthreads();
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_L;
+         base += stride) {
+        const unsigned long long i = base + threadIdx.x;
+        unsigned int d = 0xffffffffu;
+        unsigned long long w = 0;
+        if (i < n_L) {
+            const int x = __ldcg(&L[i]);
+            d = key_bits(load_key(a.keys, x), x, lo, kDigitBits);
+            w = __ldcg(&a.W[x]);
+        }
+        // equal digits of a warp are summed first: skewed digit distributions
+        // (e.g. every retired head in one bucket) would serialise on one bank
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned long long sum = 0;
+        for (unsigned m = peers; m; m &= m - 1) sum += __shfl_sync(peers, w, __ffs(m) - 1);
+        if (d != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) {
+            atomicAdd(&hw[d], sum);
+            atomicAdd(&hc[d], static_cast<unsigned int>(__popc(peers)));
+        }
+    }
+    __syncthreads();
+    unsigned long long* pw = a.part_w + static_cast<std::size_t>(blockIdx.x) * kBins;
+    unsigned int* pc = a.part_c + static_cast<std::size_t>(blockIdx.x) * kBins;
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+        pw[b] = hw[b];
+        pc[b] = hc[b];
+    }
+}
+
+// bins spread over all CTAs: hist[b] = sum over CTAs of the partials
+__device__ __forceinline__ void phase_hist_reduce(const SelArgs& a) {
+    const int nparts = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int b = blockIdx.x * nwarps + warp; b < kBins; b += gridDim.x * nwarps) {
+        unsigned long long s = 0;
+        unsigned int cnt = 0;
+        for (int p = lane; p < nparts; p += 32) {
+            s += __ldcg(&a.part_w[static_cast<std::size_t>(p) * kBins + b]);
+            cnt += __ldcg(&a.part_c[static_cast<std::size_t>(p) * kBins + b]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) {
+            a.hist_w[b] = s;
+            a.hist_c[b] = cnt;
+        }
+    }
+}
+
+struct PickOut {
+    int bucket;
+    unsigned long long need;       // need remaining inside the bucket
+    unsigned int below_cnt;        // heads placed into S by this pass
+    unsigned int max_cnt;          // largest bucket below
+};
+
+// the digit bucket where the cumulative weight reaches `need`, and the bucket
+// offsets of the heads below it.  Every CTA evaluates the same pick from the
+// reduced histograms (no extra barrier); CTA 0 records the bucket layout.
+__device__ __forceinline__ PickOut phase_pick(const SelArgs& a, unsigned long long need, int pass,
+                                              unsigned long long s_base, void* tmp_raw, unsigned int* off_sh,
+                                              PickOut* out_sh) {
+    using ScanW = cub::BlockScan<unsigned long long, kPThreads>;
+    constexpr int kPer = kBins / kPThreads;
+    unsigned long long vw[kPer], sw = 0;
+    unsigned int vc[kPer];
+    unsigned long long sc = 0;
+    for (int j = 0; j < kPer; ++j) {
+        vw[j] = __ldcg(&a.hist_w[threadIdx.x * kPer + j]);
+        vc[j] = __ldcg(&a.hist_c[threadIdx.x * kPer + j]);
+        sw += vw[j];
+        sc += vc[j];
+    }
+    unsigned long long ew, ec;
+    ScanW(*reinterpret_cast<typename ScanW::TempStorage*>(tmp_raw)).ExclusiveSum(sw, ew);
+    __syncthreads();
+    ScanW(*reinterpret_cast<typename ScanW::TempStorage*>(tmp_raw)).ExclusiveSum(sc, ec);
+    unsigned long long rw = ew, rc = ec;
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        off_sh[d] = static_cast<unsigned int>(s_base + rc);
+        if (rw < need && rw + vw[j] >= need) {
+            out_sh->bucket = d;
+            out_sh->need = need - rw;
+            out_sh->below_cnt = static_cast<unsigned int>(rc);
+        }
+        rw += vw[j];
+        rc += vc[j];
+    }
+    __syncthreads();
+    PickOut r = *out_sh;
+    // largest bucket below the pick (for the sort-capacity decision)
+    unsigned int mx = 0;
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        if (d < r.bucket) mx = max(mx, vc[j]);
+    }
+    mx = static_cast<unsigned int>(block_reduce_bits(mx, MaxOp(), reinterpret_cast<unsigned long long*>(tmp_raw)));
+    __syncthreads();
+    if (threadIdx.x == 0) out_sh->max_cnt = mx;
+    if (blockIdx.x == 0) {
+        unsigned int* so = a.seg_off + static_cast<std::size_t>(pass) * kBins;
+        unsigned int* sc2 = a.seg_cnt + static_cast<std::size_t>(pass) * kBins;
+        for (int j = 0; j < kPer; ++j) {
+            const int d = threadIdx.x * kPer + j;
+            so[d] = off_sh[d];
+            sc2[d] = d < r.bucket ? vc[j] : 0u;
+        }
+    }
+    __syncthreads();
+    r.max_cnt = out_sh->max_cnt;
+    return r;
+}
+
+// below the bucket -> S at its digit's bucket; in the bucket -> next list
+__device__ __forceinline__ void phase_compact(const SelArgs& a, const int* L, unsigned long long n_L, int* L2,
+                                              int nx, int* S, int pass, int lo, int bucket,
+                                              const unsigned int* off_sh, unsigned long long* sh) {
+    SelState* ss = a.ss;
+    unsigned int* cur = a.cursor + static_cast<std::size_t>(pass) * kBins;
     unsigned long long orS[3] = {0, 0, 0}, andS[3] = {~0ull, ~0ull, ~0ull};
     unsigned long long orL[3] = {0, 0, 0}, andL[3] = {~0ull, ~0ull, ~0ull};
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-    for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n;
+    for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_L;
          base += stride) {
         const unsigned long long i = base + threadIdx.x;
-        bool below = false, same = false;
+        int d = -1;
         int x = 0;
         Key2 k{0, 0};
-        if (i < n) {
-            x = L[i];
-            k = load_key(keys, x);
-            const int d = static_cast<int>(key_bits(k, x, lo, kDigitBits));
-            below = d < b;
-            same = d == b;
+        if (i < n_L) {
+            x = __ldcg(&L[i]);
+            k = load_key(a.keys, x);
+            d = static_cast<int>(key_bits(k, x, lo, kDigitBits));
         }
-        const long long s1 = warp_append(&ss->n_S, below);
-        const long long s2 = warp_append(&ss->n_L2, same);
+        const bool below = d >= 0 && d < bucket;
+        const bool same = d == bucket;
+        // placement into the digit's bucket: warp-aggregated cursor
+        const unsigned peers = __match_any_sync(0xffffffffu, below ? d : -1);
         if (below) {
-            S[s1] = x;
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(peers) - 1;
+            unsigned int basepos = 0;
+            if (lane == leader) basepos = atomicAdd(&cur[d], static_cast<unsigned int>(__popc(peers)));
+            basepos = __shfl_sync(peers, basepos, leader);
+            S[off_sh[d] + basepos + __popc(peers & ((1u << lane) - 1u))] = x;
             for (int w = 0; w < 3; ++w) {
                 orS[w] |= key_word(k, x, w);
                 andS[w] &= key_word(k, x, w);
             }
         }
+        const long long s2 = block_append(&ss->n_L[nx], same, reinterpret_cast<unsigned int*>(sh), sh + 31);
         if (same) {
             L2[s2] = x;
             for (int w = 0; w < 3; ++w) {
@@ -313,42 +511,303 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const int* L, const K
             }
         }
     }
-    for (int w = 0; w < 3; ++w) {
-        unsigned long long v = block_reduce_bits(orS[w], OrOp(), sh);
-        if (threadIdx.x == 0 && v) atomicOr(&ss->or_S[w], v);
-        v = block_reduce_bits(andS[w], AndOp(), sh);
-        if (threadIdx.x == 0 && ~v) atomicAnd(&ss->and_S[w], v);
-        v = block_reduce_bits(orL[w], OrOp(), sh);
-        if (threadIdx.x == 0 && v) atomicOr(&ss->or_L2[w], v);
-        v = block_reduce_bits(andL[w], AndOp(), sh);
-        if (threadIdx.x == 0 && ~v) atomicAnd(&ss->and_L2[w], v);
+    flush_orand(orS, andS, ss->or_S, ss->and_S, sh);
+    flush_orand(orL, andL, ss->or_L[nx], ss->and_L[nx], sh);
+}
+
+// bitonic sort of (key, val) pairs in shared memory, n = power of two
+__device__ __forceinline__ void bitonic_sort(unsigned long long* key, int* val, int n) {
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long x = key[i], y = key[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        key[i] = y;
+                        key[ixj] = x;
+                        const int t = val[i];
+                        val[i] = val[ixj];
+                        val[ixj] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
 }
 
-// next pass: L2 -> L (swap of the OR/AND accumulators; lists swapped by host)
-__global__ void advance_kernel(SelState* ss) {
-    ss->n_L = ss->n_L2;
-    for (int w = 0; w < 3; ++w) {
-        ss->or_L[w] = ss->or_L2[w];
-        ss->and_L[w] = ss->and_L2[w];
+// sort S[off, off+cnt) in place (one CTA)
+__device__ __forceinline__ void sort_bucket(const SelArgs& a, int* S, unsigned int off, unsigned int cnt,
+                                            unsigned long long v0, unsigned long long v1, unsigned long long v2,
+                                            int nbits, unsigned long long* key, int* val) {
+    int np = 2;
+    while (static_cast<unsigned int>(np) < cnt) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        if (static_cast<unsigned int>(i) < cnt) {
+            const int x = __ldcg(&S[off + i]);
+            key[i] = pack_key(load_key(a.keys, x), x, v0, v1, v2);
+            val[i] = x;
+        } else {
+            key[i] = 1ull << nbits;  // padding sorts after every packed key (nbits < 64)
+            val[i] = -1;
+        }
+    }
+    __syncthreads();
+    bitonic_sort(key, val, np);
+    for (int i = threadIdx.x; i < static_cast<int>(cnt); i += blockDim.x) S[off + i] = val[i];
+    __syncthreads();
+}
+
+// every eligible node of a selected chain lands at start[rank(head)] + d
+__device__ __forceinline__ void phase_scatter(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
+    for (std::int64_t i = tid; i < a.n_nodes; i += nthr) {
+        const int n = static_cast<int>(i);
+        if (n == 0 || (a.flags[n] & kFlagTierMask) != PBKV_TIER_DEVICE || __ldcg(&a.sublock[n])) continue;
+        const int h = __ldcg(&a.eff[n]);
+        const int r = __ldcg(&a.rank[h]);
+        if (r < 0) continue;
+        a.victims[__ldcg(&a.start[r]) + static_cast<unsigned long long>(a.depth[h] - a.depth[n])] = n;
     }
 }
 
-// the last candidate is the cut head: append it to S
-__global__ void finish_select_kernel(const int* L, const Key2* keys, SelState* ss, int* S) {
-    const int x = L[0];
-    const Key2 k = load_key(keys, x);
-    S[ss->n_S] = x;
-    ss->n_S += 1;
-    for (int w = 0; w < 3; ++w) {
-        ss->or_S[w] |= key_word(k, x, w);
-        ss->and_S[w] &= key_word(k, x, w);
+// the cut inside the last (cut) chain; freed / shortfall
+__device__ __forceinline__ void do_cut(const SelArgs& a) {
+    SelState* ss = a.ss;
+    const unsigned long long nS = __ldcg(&ss->n_S);
+    const int cut = __ldcg(&ss->cut_head);
+    const unsigned long long s0 = __ldcg(&a.start[nS - 1]);
+    const unsigned int c = __ldcg(&a.C[cut]);
+    if (__ldcg(&ss->take_all)) {
+        ss->n_victims = s0 + c;
+        ss->freed = __ldcg(&ss->total_tok);
+    } else {
+        const unsigned long long need = __ldcg(&ss->need_final);
+        const unsigned long long below = static_cast<unsigned long long>(a.needed) - need;
+        unsigned long long acc = 0, j = 0;
+        for (; j < c; ++j) {
+            acc += static_cast<unsigned long long>(a.len[__ldcg(&a.victims[s0 + j])]);
+            if (acc >= need) break;
+        }
+        ss->n_victims = s0 + j + 1;
+        ss->freed = below + acc;
     }
-    ss->cut_head = x;
+    ss->shortfall = ss->freed < static_cast<unsigned long long>(a.needed) ? 1 : 0;
+    a.result[0] = static_cast<long long>(ss->n_victims);
+    a.result[1] = static_cast<long long>(ss->freed);
+    a.result[2] = ss->shortfall;
 }
 
-// sort keys for the selected heads: the varying bits of (w0, w1, id) packed
-// into one uint64 (order-preserving bit extraction) when they fit
+// ---- the persistent kernel --------------------------------------------------------------
+struct PersistSmem {
+    union {
+        struct {
+            unsigned long long w[kBins];
+            unsigned int c[kBins];
+        } hist;
+        typename cub::BlockScan<unsigned long long, kPThreads>::TempStorage scan;
+        struct {
+            unsigned long long key[kBucketCap];
+            int val[kBucketCap];
+        } sort;
+    } u;
+    unsigned int off[kBins];
+    unsigned long long sh[32];
+    unsigned long long bc[4];  // broadcast of shared scalars
+    PickOut pick;
+};
+
+__global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PersistSmem& sm = *reinterpret_cast<PersistSmem*>(smem_raw);
+    cg::grid_group grid = cg::this_grid();
+    SelState* ss = a.ss;
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+
+    stamp(ss);
+    phase_lock(a, tid, nthr);
+    grid.sync();
+    stamp(ss);
+    phase_eff(a, tid, nthr);
+    grid.sync();
+    stamp(ss);
+    phase_chains(a, sm.sh);
+    grid.sync();
+    stamp(ss);
+
+    // shared scalars are read once per CTA and broadcast through shared memory
+    // (thousands of threads reading one L2 line serialise on its slice)
+    if (threadIdx.x == 0) {
+        sm.bc[0] = __ldcg(&ss->n_L[0]);
+        sm.bc[1] = __ldcg(&ss->total_tok);
+    }
+    __syncthreads();
+    const unsigned long long n_heads = sm.bc[0];
+    const unsigned long long total_tok = sm.bc[1];
+    __syncthreads();
+    if (n_heads == 0) {  // nothing evictable
+        if (tid == 0) {
+            ss->n_victims = 0;
+            ss->freed = 0;
+            ss->shortfall = 1;
+            a.result[0] = 0;
+            a.result[1] = 0;
+            a.result[2] = 1;
+        }
+        return;
+    }
+    const bool take_all = total_tok < static_cast<unsigned long long>(a.needed);
+    int* S = a.listS;
+    unsigned long long nS = 0;
+    unsigned int max_bucket = 0;
+    int n_pass = 0;
+    if (take_all) {
+        // every head is a victim; S is the unsorted head list: one bucket
+        S = a.heads;
+        nS = n_heads;
+        max_bucket = static_cast<unsigned int>(n_heads);
+        if (tid == 0) {
+            ss->take_all = 1;
+            ss->s_is_heads = 1;
+            ss->n_S = n_heads;
+            for (int w = 0; w < 3; ++w) {
+                ss->or_S[w] = __ldcg(&ss->or_L[0][w]);
+                ss->and_S[w] = __ldcg(&ss->and_L[0][w]);
+            }
+        }
+    } else {
+        int* L = a.heads;
+        int* L2 = a.listB;
+        int cur = 0;
+        unsigned long long need = static_cast<unsigned long long>(a.needed);
+        for (; n_pass < kMaxPasses; ++n_pass) {
+            if (threadIdx.x == 0) {
+                sm.bc[0] = __ldcg(&ss->n_L[cur]);
+                sm.bc[1] = static_cast<unsigned long long>(top_varying_bit_cg(ss->or_L[cur], ss->and_L[cur]) + 1);
+            }
+            __syncthreads();
+            const unsigned long long nL = sm.bc[0];
+            const int top = static_cast<int>(sm.bc[1]) - 1;
+            __syncthreads();
+            if (nL <= 1) break;
+            const int lo = top - kDigitBits + 1 < 0 ? 0 : top - kDigitBits + 1;
+            if (tid == 0) {  // the next candidate list's accumulators
+                const int nx = cur ^ 1;
+                ss->n_L[nx] = 0;
+                for (int w = 0; w < 3; ++w) {
+                    ss->or_L[nx][w] = 0;
+                    ss->and_L[nx][w] = ~0ull;
+                }
+            }
+            phase_hist(a, L, nL, lo, sm.u.hist.w, sm.u.hist.c);
+            grid.sync();
+            phase_hist_reduce(a);
+            grid.sync();
+            stamp(ss);
+            const PickOut pk = phase_pick(a, need, n_pass, nS, &sm.u.scan, sm.off, &sm.pick);
+            phase_compact(a, L, nL, L2, cur ^ 1, S, n_pass, lo, pk.bucket, sm.off, sm.sh);
+            need = pk.need;
+            nS += pk.below_cnt;
+            max_bucket = max(max_bucket, pk.max_cnt);
+            grid.sync();
+            stamp(ss);
+            int* t = L;
+            L = L2;
+            L2 = t;
+            cur ^= 1;
+        }
+        if (tid == 0) {  // the last candidate is the cut head (its own bucket)
+            const int x = __ldcg(&L[0]);
+            const Key2 k = load_key(a.keys, x);
+            S[nS] = x;
+            ss->n_S = nS + 1;
+            ss->need_final = need;
+            ss->n_pass = n_pass;
+            for (int w = 0; w < 3; ++w) {
+                ss->or_S[w] = __ldcg(&ss->or_S[w]) | key_word(k, x, w);
+                ss->and_S[w] = __ldcg(&ss->and_S[w]) & key_word(k, x, w);
+            }
+            ss->cut_head = x;
+        }
+        nS += 1;
+    }
+    grid.sync();
+    stamp(ss);
+
+    // ---- sort every bucket of S (one CTA per bucket, shared memory) ------------------
+    if (threadIdx.x == 0) {
+        sm.bc[0] = __ldcg(&ss->or_S[0]) ^ __ldcg(&ss->and_S[0]);
+        sm.bc[1] = __ldcg(&ss->or_S[1]) ^ __ldcg(&ss->and_S[1]);
+        sm.bc[2] = (__ldcg(&ss->or_S[2]) ^ __ldcg(&ss->and_S[2])) & 0xffffffffull;
+    }
+    __syncthreads();
+    const unsigned long long v0 = sm.bc[0], v1 = sm.bc[1], v2 = sm.bc[2];
+    __syncthreads();
+    const int nbits = __popcll(v0) + __popcll(v1) + __popcll(v2);
+    if (max_bucket > static_cast<unsigned int>(kBucketCap) || nbits >= 64) {
+        if (tid == 0) {
+            ss->host_sort = 1;  // device-wide sort driven from the host
+            ss->max_bucket = static_cast<int>(max_bucket);
+        }
+        return;
+    }
+    if (take_all) {
+        if (blockIdx.x == 0) sort_bucket(a, S, 0, static_cast<unsigned int>(nS), v0, v1, v2, nbits, sm.u.sort.key,
+                                         sm.u.sort.val);
+    } else {
+        for (int j = blockIdx.x; j < n_pass * kBins; j += gridDim.x) {
+            const unsigned int cnt = __ldcg(&a.seg_cnt[j]);
+            if (cnt < 2) continue;
+            sort_bucket(a, S, __ldcg(&a.seg_off[j]), cnt, v0, v1, v2, nbits, sm.u.sort.key, sm.u.sort.val);
+        }
+    }
+    grid.sync();
+    stamp(ss);
+
+    // ---- chain starts: exclusive scan of the chain sizes over sorted S (CTA 0) --------
+    if (blockIdx.x == 0) {
+        using Scan = cub::BlockScan<unsigned long long, kPThreads>;
+        unsigned long long carry = 0;
+        for (unsigned long long c0 = 0; c0 < nS; c0 += static_cast<unsigned long long>(kPThreads) * kScanIPT) {
+            unsigned long long cnt[kScanIPT], local = 0;
+            int hv[kScanIPT];
+            for (int j = 0; j < kScanIPT; ++j) {
+                const unsigned long long pos = c0 + static_cast<unsigned long long>(threadIdx.x) * kScanIPT + j;
+                cnt[j] = 0;
+                hv[j] = -1;
+                if (pos < nS) {
+                    const int h = __ldcg(&S[pos]);
+                    hv[j] = h;
+                    a.rank[h] = static_cast<int>(pos);
+                    cnt[j] = __ldcg(&a.C[h]);
+                }
+                local += cnt[j];
+            }
+            unsigned long long excl, total;
+            Scan(sm.u.scan).ExclusiveSum(local, excl, total);
+            __syncthreads();
+            excl += carry;
+            for (int j = 0; j < kScanIPT; ++j) {
+                const unsigned long long pos = c0 + static_cast<unsigned long long>(threadIdx.x) * kScanIPT + j;
+                if (pos < nS) a.start[pos] = excl;
+                excl += cnt[j];
+                if (pos == nS - 1 && take_all) ss->cut_head = hv[j];
+            }
+            carry += total;
+        }
+    }
+    grid.sync();
+    stamp(ss);
+    phase_scatter(a, tid, nthr);
+    grid.sync();
+    stamp(ss);
+    if (tid == 0) do_cut(a);
+    stamp(ss);
+}
+
+// ---- fallback path (a bucket larger than one CTA's sort) -----------------------------
 __global__ void pack_keys_kernel(const int* S, const Key2* keys, const SelState* ss, unsigned long long* out,
                                  int* ids) {
     const unsigned long long n = ss->n_S;
@@ -358,19 +817,7 @@ __global__ void pack_keys_kernel(const int* S, const Key2* keys, const SelState*
     for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
         const int x = S[i];
-        const Key2 k = load_key(keys, x);
-        unsigned long long r = 0;
-        auto ext = [&](unsigned long long word, unsigned long long mask) {
-            while (mask) {
-                const int b = 63 - __clzll(static_cast<long long>(mask));
-                r = (r << 1) | ((word >> b) & 1ull);
-                mask &= ~(1ull << b);
-            }
-        };
-        ext(k.w0, v0);
-        ext(k.w1, v1);
-        ext(static_cast<unsigned long long>(static_cast<unsigned int>(x)), v2);
-        out[i] = r;
+        out[i] = pack_key(load_key(keys, x), x, v0, v1, v2);
         ids[i] = x;
     }
 }
@@ -392,8 +839,7 @@ __global__ void heads_from_hk_kernel(const HeadKey* hk, const SelState* ss, int*
         out[i] = static_cast<int>(hk[i].id);
 }
 
-// rank of every selected head and its chain size in sorted order
-__global__ void rank_kernel(const int* sorted, const unsigned int* C, const SelState* ss, int* rank,
+__global__ void rank_kernel(const int* sorted, const unsigned int* C, SelState* ss, int* rank,
                             unsigned long long* cnt) {
     const unsigned long long n = ss->n_S;
     for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
@@ -401,78 +847,16 @@ __global__ void rank_kernel(const int* sorted, const unsigned int* C, const SelS
         const int h = sorted[i];
         rank[h] = static_cast<int>(i);
         cnt[i] = C[h];
+        if (i == n - 1 && ss->take_all) ss->cut_head = h;
     }
 }
 
-// every eligible node of a selected chain lands at start[rank(head)] + d
-__global__ void __launch_bounds__(kThreads) scatter_kernel(const std::uint8_t* flags, const int* sublock,
-                                                           const int* eff, const int* rank, const int* depth,
-                                                           const unsigned long long* start, int* out,
-                                                           std::int64_t n_nodes) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const int n = static_cast<int>(i);
-        if (n == 0 || (flags[n] & kFlagTierMask) != PBKV_TIER_DEVICE || sublock[n]) continue;
-        const int h = eff[n];
-        const int r = rank[h];
-        if (r < 0) continue;
-        out[start[r] + static_cast<unsigned long long>(depth[h] - depth[n])] = n;
-    }
+__global__ void __launch_bounds__(kThreads) scatter_kernel(SelArgs a) {
+    phase_scatter(a, blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x,
+                  static_cast<std::int64_t>(gridDim.x) * blockDim.x);
 }
 
-// the cut inside the last (cut) chain; freed / shortfall
-__global__ void cut_kernel(const int* victims, const int* len, const unsigned long long* start,
-                           const unsigned int* C, SelState* ss, long long needed, long long* result) {
-    const unsigned long long nS = ss->n_S;
-    if (ss->take_all) {
-        const unsigned long long nv = start[nS - 1] + C[ss->cut_head];
-        ss->n_victims = nv;
-        ss->freed = ss->total_tok;
-    } else {
-        const unsigned long long s0 = start[nS - 1];
-        const unsigned int c = C[ss->cut_head];
-        const unsigned long long need = ss->need_rem;
-        const unsigned long long below = static_cast<unsigned long long>(needed) - need;
-        unsigned long long acc = 0, j = 0;
-        for (; j < c; ++j) {
-            acc += static_cast<unsigned long long>(len[victims[s0 + j]]);
-            if (acc >= need) break;
-        }
-        ss->n_victims = s0 + j + 1;
-        ss->freed = below + acc;
-    }
-    ss->shortfall = ss->freed < static_cast<unsigned long long>(needed) ? 1 : 0;
-    result[0] = static_cast<long long>(ss->n_victims);
-    result[1] = static_cast<long long>(ss->freed);
-    result[2] = ss->shortfall;
-}
-
-__global__ void init_state_kernel(SelState* ss, long long needed) {
-    SelState z{};
-    z.need_rem = static_cast<unsigned long long>(needed);
-    for (int w = 0; w < 3; ++w) {
-        z.and_L[w] = ~0ull;
-        z.and_L2[w] = ~0ull;
-        z.and_S[w] = ~0ull;
-    }
-    z.cut_head = -1;
-    *ss = z;
-}
-
-// take-all: every head is selected (eligible tokens < needed)
-__global__ void take_all_kernel(SelState* ss) {
-    ss->take_all = 1;
-    ss->n_S = ss->n_L;
-    for (int w = 0; w < 3; ++w) {
-        ss->or_S[w] = ss->or_L[w];
-        ss->and_S[w] = ss->and_L[w];
-    }
-}
-
-// after sorting in take-all mode the cut head is the last head
-__global__ void set_last_head_kernel(const int* sorted, SelState* ss) { ss->cut_head = sorted[ss->n_S - 1]; }
-
-}  // namespace
+__global__ void cut_kernel(SelArgs a) { do_cut(a); }
 
 struct HeadDecomposer {
     __host__ __device__ ::cuda::std::tuple<unsigned long long&, unsigned long long&, unsigned int&> operator()(
@@ -480,6 +864,22 @@ struct HeadDecomposer {
         return {k.w0, k.w1, k.id};
     }
 };
+
+int persistent_grid(Context& c) {
+    static int cached = 0;
+    if (cached) return cached;
+    int dev_sms = 0;
+    PBKV_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device));
+    const int smem = static_cast<int>(sizeof(PersistSmem));
+    PBKV_CUDA(cudaFuncSetAttribute(select_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per_sm = 0;
+    PBKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_persistent_kernel, kPThreads, smem));
+    if (per_sm < 1) throw ApiError(PBKV_ECUDA, "persistent select kernel cannot be resident");
+    cached = dev_sms * (per_sm >= 2 ? 2 : 1);
+    return cached;
+}
+
+}  // namespace
 
 std::size_t sel_state_bytes() { return sizeof(SelState); }
 
@@ -490,155 +890,143 @@ void launch_keys_cached(Context& c, int policy) {
     ++c.launches;
 }
 
-void launch_lock_eff(Context& c, const int* locked_dev, std::int64_t n_locked) {
-    if (n_locked > 0) {
-        lock_kernel<<<grid_for(n_locked, kThreads), kThreads, 0, c.stream>>>(locked_dev, n_locked, c.parent.p,
-                                                                            c.flags.p, c.sublock.p, c.n);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-    }
-    eff_kernel<<<grid_cap(c.n, kThreads), kThreads, 0, c.stream>>>(c.parent.p, c.flags.p, c.keys.p, c.eff.p, c.n);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-}
-
-// Runs weights -> radix select -> sort -> scatter -> cut.  Victims land in
-// c.vid_out[0..n); result_dev gets {n_victims, freed, shortfall}.  Host
-// synchronisations: one per radix pass (candidate count) and one before the
-// head sort (its size).  Returns the device status checked by the caller.
-SelectCounts run_select(Context& c, std::int64_t needed, bool he_recompute, long long* result_dev) {
+// Runs lock -> eff -> chains -> select -> bucket sorts -> scan -> scatter ->
+// cut.  Victims land in c.vid_out[0..n); result_dev (or an internal buffer)
+// receives {n_victims, freed, shortfall}.  One host synchronisation at the end
+// (plus the fallback sort's when a bucket exceeds one CTA's sort).
+SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked, std::int64_t needed,
+                        bool he_recompute, long long* result_dev) {
     SelState* ss = reinterpret_cast<SelState*>(c.selstate.p);
     SelState* hs = reinterpret_cast<SelState*>(c.hselstate.p);
-    init_state_kernel<<<1, 1, 0, c.stream>>>(ss, needed);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-    weights_kernel<<<grid_cap(c.n, kThreads), kThreads, 0, c.stream>>>(
-        c.len.p, c.flags.p, c.sublock.p, c.eff.p, c.missing.p, c.keys.p, c.W.p, c.C.p, c.heads.p, ss, c.status.p, c.n,
-        he_recompute ? 1 : 0);
-    PBKV_CUDA(cudaGetLastError());
+    // initial state from a pinned template (no kernel)
+    SelState* tmpl = reinterpret_cast<SelState*>(c.hselstate.p + sizeof(SelState));
+    std::memset(tmpl, 0, sizeof(SelState));
+    tmpl->need_final = static_cast<unsigned long long>(needed);
+    for (int w = 0; w < 3; ++w) {
+        tmpl->and_L[0][w] = tmpl->and_L[1][w] = ~0ull;
+        tmpl->and_S[w] = ~0ull;
+    }
+    tmpl->cut_head = -1;
+    PBKV_CUDA(cudaMemcpyAsync(ss, tmpl, sizeof(SelState), cudaMemcpyHostToDevice, c.stream));
+    long long* res = result_dev ? result_dev : c.counters.p + 8;
+    c.sorti_out.reserve(static_cast<std::size_t>(c.n) + 1);
+    c.cnt.reserve(static_cast<std::size_t>(c.n) + 1);
+    const int grid = persistent_grid(c);
+    c.part_w.reserve(static_cast<std::size_t>(grid) * kBins);
+    c.part_c.reserve(static_cast<std::size_t>(grid) * kBins);
+    c.hist_w.reserve(kBins);
+    c.hist_c.reserve(kBins);
+    c.seg_off.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
+    c.seg_cnt.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
+    c.cursor.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
+    SelArgs a;
+    a.parent = c.parent.p;
+    a.len = c.len.p;
+    a.flags = c.flags.p;
+    a.depth = c.depth.p;
+    a.keys = c.keys.p;
+    a.eff = c.eff.p;
+    a.sublock = c.sublock.p;
+    a.missing = c.missing.p;
+    a.W = c.W.p;
+    a.C = c.C.p;
+    a.rank = c.rank.p;
+    a.heads = c.heads.p;
+    a.listB = c.listB.p;
+    a.listS = c.listS.p;
+    a.sorted = c.sorti_out.p;
+    a.start = c.cnt.p;
+    a.victims = c.vid_out.p;
+    a.hist_w = c.hist_w.p;
+    a.hist_c = c.hist_c.p;
+    a.part_w = c.part_w.p;
+    a.part_c = c.part_c.p;
+    a.seg_off = c.seg_off.p;
+    a.seg_cnt = c.seg_cnt.p;
+    a.cursor = c.cursor.p;
+    a.ss = ss;
+    a.st = c.status.p;
+    a.result = res;
+    a.locked = locked_dev;
+    a.n_locked = n_locked;
+    a.n_nodes = c.n;
+    a.needed = needed;
+    a.he_recompute = he_recompute ? 1 : 0;
+    void* args[] = {&a};
+    PBKV_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(select_persistent_kernel), dim3(grid),
+                                          dim3(kPThreads), args, sizeof(PersistSmem), c.stream));
     ++c.launches;
     PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
     check_status(c);  // synchronises
     SelectCounts out;
-    if (hs->n_L == 0) {  // nothing evictable
-        const long long z[3] = {0, 0, 1};
-        PBKV_CUDA(cudaMemcpyAsync(c.hcounters.p + 8, z, sizeof z, cudaMemcpyHostToDevice, c.stream));
-        if (result_dev)
-            PBKV_CUDA(cudaMemcpyAsync(result_dev, c.hcounters.p + 8, sizeof z, cudaMemcpyHostToDevice, c.stream));
-        out.n_victims = 0;
-        out.freed = 0;
-        out.shortfall = 1;
-        return out;
-    }
-    int* L = c.heads.p;
-    int* L2 = c.listB.p;
-    int* S = c.listS.p;
-    const bool take_all = hs->total_tok < static_cast<unsigned long long>(needed);
-    if (take_all) {
-        take_all_kernel<<<1, 1, 0, c.stream>>>(ss);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-        S = L;
-    } else {
-        PBKV_CUDA(cudaMemsetAsync(c.hist.p, 0, kBins * sizeof(unsigned long long), c.stream));
-        unsigned long long nL = hs->n_L;
-        for (int pass = 0; pass < 32 && nL > 1; ++pass) {
-            hist_kernel<<<grid_cap(static_cast<std::int64_t>(nL), kThreads), kThreads, 0, c.stream>>>(L, c.keys.p,
-                                                                                                     c.W.p, ss,
-                                                                                                     c.hist.p);
-            pick_kernel<<<1, 1024, 0, c.stream>>>(ss, c.hist.p);
-            compact_kernel<<<grid_cap(static_cast<std::int64_t>(nL), kThreads), kThreads, 0, c.stream>>>(
-                L, c.keys.p, ss, L2, S);
-            advance_kernel<<<1, 1, 0, c.stream>>>(ss);
-            PBKV_CUDA(cudaGetLastError());
-            c.launches += 4;
-            PBKV_CUDA(cudaMemcpyAsync(&hs->n_L, &ss->n_L, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                      c.stream));
-            PBKV_CUDA(cudaStreamSynchronize(c.stream));
-            nL = hs->n_L;
-            std::swap(L, L2);
+    c.phase_ns.assign(hs->ts, hs->ts + (hs->n_ts < 40 ? hs->n_ts : 40));
+    if (std::getenv("PBKV_DEBUG_SELECT"))
+        std::fprintf(stderr,
+                     "[pbkv select] n_heads=%llu total_tok=%llu take_all=%d host_sort=%d n_S=%llu n_pass=%d "
+                     "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d\n",
+                     hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
+                     hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid);
+    if (hs->host_sort) {
+        // ---- fallback: device-wide sort of the selected heads -----------------------------
+        const std::int64_t nS = static_cast<std::int64_t>(hs->n_S);
+        const int* S = hs->s_is_heads ? c.heads.p : c.listS.p;
+        int nbits = 0;
+        for (int w = 0; w < 3; ++w) {
+            unsigned long long v = hs->or_S[w] ^ hs->and_S[w];
+            if (w == 2) v &= 0xffffffffull;
+            nbits += __builtin_popcountll(v);
         }
-        finish_select_kernel<<<1, 1, 0, c.stream>>>(L, c.keys.p, ss, S);
+        c.sortk_in.reserve(nS);
+        c.sortk_out.reserve(nS);
+        c.sorti_in.reserve(nS);
+        int* sorted = c.sorti_out.p;
+        if (nbits <= 64) {
+            pack_keys_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(S, c.keys.p, ss, c.sortk_in.p,
+                                                                               c.sorti_in.p);
+            PBKV_CUDA(cudaGetLastError());
+            ++c.launches;
+            std::size_t b = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, b, c.sortk_in.p, c.sortk_out.p, c.sorti_in.p, sorted,
+                                            static_cast<int>(nS), 0, nbits);
+            c.cub_tmp.reserve(b);
+            ++c.lib_calls;
+            PBKV_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, b, c.sortk_in.p, c.sortk_out.p, c.sorti_in.p,
+                                                      sorted, static_cast<int>(nS), 0, nbits, c.stream));
+        } else {
+            c.hk_in.reserve(nS);
+            c.hk_out.reserve(nS);
+            gather_headkeys_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(S, c.keys.p, ss, c.hk_in.p);
+            PBKV_CUDA(cudaGetLastError());
+            ++c.launches;
+            std::size_t b = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, b, c.hk_in.p, c.hk_out.p, static_cast<int>(nS), HeadDecomposer{});
+            c.cub_tmp.reserve(b);
+            ++c.lib_calls;
+            PBKV_CUDA(cub::DeviceRadixSort::SortKeys(c.cub_tmp.p, b, c.hk_in.p, c.hk_out.p, static_cast<int>(nS),
+                                                     HeadDecomposer{}, c.stream));
+            heads_from_hk_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(c.hk_out.p, ss, sorted);
+            PBKV_CUDA(cudaGetLastError());
+            ++c.launches;
+        }
+        rank_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(sorted, c.C.p, ss, c.rank.p, c.cnt.p);
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
-    }
-    PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
-    PBKV_CUDA(cudaStreamSynchronize(c.stream));
-    const std::int64_t nS = static_cast<std::int64_t>(hs->n_S);
-    // ---- sort the selected heads by key ----------------------------------------
-    int nbits = 0;
-    for (int w = 0; w < 3; ++w) {
-        unsigned long long v = hs->or_S[w] ^ hs->and_S[w];
-        if (w == 2) v &= 0xffffffffull;
-        nbits += __builtin_popcountll(v);
-    }
-    c.sortk_in.reserve(nS);
-    c.sortk_out.reserve(nS);
-    c.sorti_in.reserve(nS);
-    c.sorti_out.reserve(nS);
-    c.cnt.reserve(nS + 1);
-    c.vid_out.reserve(c.n + 1);
-    int* sorted = c.sorti_out.p;
-    if (nS == 1) {
-        PBKV_CUDA(cudaMemcpyAsync(sorted, S, sizeof(int), cudaMemcpyDeviceToDevice, c.stream));
-    } else if (nbits <= 64) {
-        pack_keys_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(S, c.keys.p, ss, c.sortk_in.p,
-                                                                           c.sorti_in.p);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-        std::size_t b = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, b, c.sortk_in.p, c.sortk_out.p, c.sorti_in.p, c.sorti_out.p,
-                                        static_cast<int>(nS), 0, nbits > 0 ? nbits : 1);
-        c.cub_tmp.reserve(b);
-        ++c.lib_calls;
-        PBKV_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, b, c.sortk_in.p, c.sortk_out.p, c.sorti_in.p,
-                                                  c.sorti_out.p, static_cast<int>(nS), 0, nbits > 0 ? nbits : 1,
-                                                  c.stream));
-    } else {
-        c.hk_in.reserve(nS);
-        c.hk_out.reserve(nS);
-        gather_headkeys_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(S, c.keys.p, ss, c.hk_in.p);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-        std::size_t b = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, b, c.hk_in.p, c.hk_out.p, static_cast<int>(nS), HeadDecomposer{});
-        c.cub_tmp.reserve(b);
-        ++c.lib_calls;
-        PBKV_CUDA(cub::DeviceRadixSort::SortKeys(c.cub_tmp.p, b, c.hk_in.p, c.hk_out.p, static_cast<int>(nS),
-                                                 HeadDecomposer{}, c.stream));
-        heads_from_hk_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(c.hk_out.p, ss, sorted);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-    }
-    if (take_all) {
-        set_last_head_kernel<<<1, 1, 0, c.stream>>>(sorted, ss);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-    }
-    // ---- chain placement ----------------------------------------------------------
-    rank_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(sorted, c.C.p, ss, c.rank.p, c.cnt.p);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-    {
         std::size_t b = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, b, c.cnt.p, c.cnt.p, static_cast<int>(nS));
         c.cub_tmp.reserve(b);
         ++c.lib_calls;
         PBKV_CUDA(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, b, c.cnt.p, c.cnt.p, static_cast<int>(nS), c.stream));
+        scatter_kernel<<<grid_cap(c.n, kThreads), kThreads, 0, c.stream>>>(a);
+        PBKV_CUDA(cudaGetLastError());
+        cut_kernel<<<1, 1, 0, c.stream>>>(a);
+        PBKV_CUDA(cudaGetLastError());
+        c.launches += 2;
+        PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
+        PBKV_CUDA(cudaStreamSynchronize(c.stream));
     }
-    scatter_kernel<<<grid_cap(c.n, kThreads), kThreads, 0, c.stream>>>(c.flags.p, c.sublock.p, c.eff.p, c.rank.p,
-                                                                       c.depth.p, c.cnt.p, c.vid_out.p, c.n);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-    long long* res = result_dev ? result_dev : c.counters.p + 8;
-    cut_kernel<<<1, 1, 0, c.stream>>>(c.vid_out.p, c.len.p, c.cnt.p, c.C.p, ss, needed, res);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-    PBKV_CUDA(cudaMemcpyAsync(c.hcounters.p + 8, res, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
-    PBKV_CUDA(cudaStreamSynchronize(c.stream));
-    out.n_victims = c.hcounters.p[8];
-    out.freed = c.hcounters.p[9];
-    out.shortfall = static_cast<int>(c.hcounters.p[10]);
+    out.n_victims = static_cast<std::int64_t>(hs->n_victims);
+    out.freed = static_cast<std::int64_t>(hs->freed);
+    out.shortfall = hs->shortfall;
     return out;
 }
 

@@ -175,7 +175,7 @@ def test_synthetic_config_parity(gpu, n_nodes, n_wf, K):
     pol.mirror(soa)
     locked = WL.pinned_paths(soa, rng, 0.01)
     used = int(soa.len[soa.tier == 0][1:].sum())
-    for frac in (0.001, 0.01, 0.1, 0.5):
+    for frac in (0.001, 0.01, 0.1, 0.5, 1.5):  # 1.5: shortfall, every eligible node (take-all path)
         needed = max(1, int(frac * used))
         o = Oracle.select(soa, POLICY_HE, needed, locked)
         g = pol.select_victims_hierarchical(needed, locked=locked)
