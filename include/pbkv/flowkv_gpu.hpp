@@ -1,0 +1,375 @@
+// flowkv_gpu.hpp -- C++ drop-in for the reference policy interface, on the
+// pbkv C ABI (include/pbkv.h) and its sm_100a kernels.
+//
+// The reference (/root/reference/proj/include/flowkv) selects policies at
+// call sites through inline free functions (no virtual interface, SURVEY.md
+// §8(b)).  This header declares the same functions, with the same
+// signatures, argument meaning and flowkv::ValidationError messages, in
+// namespace flowkv::gpu:
+//
+//   reference                                          replaced by
+//   refresh_scores            scoring.hpp:80-91        gpu::refresh_scores
+//   refresh_nodes             scoring.hpp:95-101       gpu::refresh_nodes
+//   select_victims            policies.hpp:155-168     gpu::select_victims
+//   select_victims_lru        policies.hpp:88-93       gpu::select_victims_lru
+//   select_victims_lae        policies.hpp:97-104      gpu::select_victims_lae
+//   select_victims_hierarchical policies.hpp:108-115   gpu::select_victims_hierarchical
+//   select_victims_kvflow     policies.hpp:144-153     gpu::select_victims_kvflow
+//   plan_conservative_prefetch policies.hpp:220-224    gpu::plan_conservative_prefetch
+//   plan_aggressive_prefetch  policies.hpp:228-235     gpu::plan_aggressive_prefetch
+//
+// A caller switches by qualifying the call (or, for an unmodified
+// simulator.hpp, by the macro interposition shown in INTEGRATION.md).
+// Include the reference headers first; link libpbkv.so.
+//
+// Tree mirroring: CacheTree has no change log, so every call uploads a full
+// struct-of-arrays image of the tree (SURVEY.md §7 hard part 9: exact, and
+// cheap at the scenario sizes this shim serves).  Large trees use the C ABI
+// directly with an incrementally maintained mirror.  Forecasts are copied at
+// call time (the provider's pointers are only valid during the call,
+// SURVEY.md §8(b) "Ownership").  One pbkv context per thread and
+// (K, gamma, A): scenario cells run on separate threads and share nothing
+// (scenario.hpp:291-301).  There is no CPU fallback: a missing or non-sm_100
+// device surfaces as std::runtime_error from the first call.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <set>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "flowkv/cache.hpp"
+#include "flowkv/errors.hpp"
+#include "flowkv/forecast.hpp"
+#include "flowkv/policies.hpp"
+#include "flowkv/scoring.hpp"
+
+#include "../pbkv.h"
+
+namespace flowkv::gpu {
+
+namespace detail {
+
+// Status -> exception: PBKV_EINVAL carries the reference's ValidationError
+// message verbatim; everything else is a device / ABI failure.
+inline void check(int rc, const pbkv_ctx* ctx) {
+    if (rc == PBKV_OK) return;
+    std::string msg = pbkv_last_error(ctx);
+    if (rc == PBKV_EINVAL) throw ValidationError(msg);
+    throw std::runtime_error("pbkv: " + msg);
+}
+
+inline int device_ordinal() {
+    const char* s = std::getenv("PBKV_DEVICE");
+    return s ? std::atoi(s) : 0;
+}
+
+// per-thread context cache keyed by the score parameters and agent count
+class Contexts {
+public:
+    pbkv_ctx* get(int k, double gamma, int agents) {
+        auto key = std::make_tuple(k, gamma, agents);
+        auto it = ctx_.find(key);
+        if (it != ctx_.end()) return it->second.get();
+        pbkv_cfg cfg{device_ordinal(), k, gamma, agents};
+        pbkv_ctx* c = nullptr;
+        check(pbkv_ctx_create(&c, &cfg), nullptr);
+        ctx_.emplace(key, Handle(c));
+        return c;
+    }
+
+private:
+    struct Del {
+        void operator()(pbkv_ctx* c) const { pbkv_ctx_destroy(c); }
+    };
+    using Handle = std::unique_ptr<pbkv_ctx, Del>;
+    std::map<std::tuple<int, double, int>, Handle> ctx_;
+};
+
+inline Contexts& contexts() {
+    thread_local Contexts c;
+    return c;
+}
+
+// Struct-of-arrays image of a CacheTree (read-side fields, cache.hpp:54-69).
+struct TreeImage {
+    std::vector<std::int32_t> parent, len, ever;
+    std::vector<std::uint8_t> tier, retired;
+    std::vector<std::uint64_t> last, bits;
+    std::vector<double> score;
+    std::vector<std::int64_t> off, wf;
+    pbkv_tree_soa soa{};
+
+    void build(const CacheTree& t) {
+        const std::size_t n = t.node_count();
+        parent.resize(n);
+        len.resize(n);
+        ever.resize(n);
+        tier.resize(n);
+        retired.resize(n);
+        last.resize(n);
+        score.resize(n);
+        off.resize(n + 1);
+        wf.clear();
+        bits.clear();
+        for (std::size_t i = 0; i < n; ++i) {
+            const CacheTree::Node& nd = t.node(static_cast<int>(i));
+            parent[i] = nd.parent;
+            len[i] = static_cast<std::int32_t>(nd.tokens.size());
+            ever[i] = nd.ever_tagged;
+            tier[i] = nd.tier == Tier::Device ? PBKV_TIER_DEVICE
+                                              : (nd.tier == Tier::Host ? PBKV_TIER_HOST : PBKV_TIER_ABSENT);
+            retired[i] = nd.retired ? 1 : 0;
+            last[i] = nd.last_access;
+            score[i] = nd.score;
+            off[i] = static_cast<std::int64_t>(wf.size());
+            for (const auto& [w, b] : nd.access) {  // std::map: ascending WorkflowId (cache.hpp:64)
+                wf.push_back(static_cast<std::int64_t>(w));
+                bits.push_back(b);
+            }
+        }
+        off[n] = static_cast<std::int64_t>(wf.size());
+        soa = pbkv_tree_soa{};
+        soa.n_nodes = static_cast<std::int64_t>(n);
+        soa.n_entries = static_cast<std::int64_t>(wf.size());
+        soa.parent = parent.data();
+        soa.len = len.data();
+        soa.tier = tier.data();
+        soa.retired = retired.data();
+        soa.last_access = last.data();
+        soa.ever_tagged = ever.data();
+        soa.score = score.data();
+        soa.acc_off = off.data();
+        soa.acc_wf = wf.data();
+        soa.acc_bits = bits.data();
+        soa.device_capacity = t.device_capacity();
+        soa.device_used = t.device_used();
+        soa.retired_device_tokens = t.retired_device_tokens();
+        soa.host_capacity = t.host_capacity();
+        soa.host_used = t.host_used();
+    }
+};
+
+inline TreeImage& image() {
+    thread_local TreeImage img;
+    return img;
+}
+
+// Uploads the forecasts of every workflow tagged on `ids`, grouped by
+// horizon.  Returns the agent count of the first forecast (or `fallback`).
+struct ForecastBatch {
+    std::map<int, std::pair<std::vector<std::int64_t>, std::vector<double>>> by_horizon;
+    int outcomes = 0;
+
+    void add(WorkflowId w, const Forecast& f) {
+        if (outcomes == 0) outcomes = f.outcomes();
+        auto& [ids, p] = by_horizon[f.horizon()];
+        ids.push_back(static_cast<std::int64_t>(w));
+        for (int k = 0; k < f.horizon(); ++k)
+            for (int a = 0; a < f.outcomes(); ++a) p.push_back(f.at(k, a));
+    }
+    void upload(pbkv_ctx* c) const {
+        for (const auto& [h, v] : by_horizon)
+            check(pbkv_forecast_put(c, v.first.data(), static_cast<std::int64_t>(v.first.size()), h, outcomes,
+                                    v.second.data()),
+                  c);
+    }
+};
+
+// node_terms (scoring.hpp:66-75) + multi_step_score (scoring.hpp:49-62)
+// preconditions for one node, in the reference's order: the first missing
+// forecast, then params.validate(), then any short horizon.
+inline const char* node_precheck(const CacheTree& tree, int id, const ForecastProvider& fp,
+                                 const ScoreParams& params, std::string& msg, ForecastBatch* batch,
+                                 std::set<WorkflowId>& seen) {
+    const auto& acc = tree.node(id).access;
+    for (const auto& [w, b] : acc) {
+        (void)b;
+        if (!fp(w)) {
+            msg = "missing forecast for active workflow " + std::to_string(w);
+            return msg.c_str();
+        }
+    }
+    if (params.k < 1) return "lookahead horizon must be >= 1";
+    if (!(params.gamma > 0.0 && params.gamma < 1.0)) return "gamma must be in (0, 1)";
+    for (const auto& [w, b] : acc) {
+        (void)b;
+        const Forecast* f = fp(w);
+        if (f->horizon() < params.k) return "forecast horizon shorter than the scoring horizon";
+        if (batch && seen.insert(w).second) batch->add(w, *f);
+    }
+    return nullptr;
+}
+
+// Eq. 2 for `ids` on the device, written back with set_score in order; the
+// first failing node raises after the nodes before it were written (as the
+// reference loop does).
+inline int score_ids(CacheTree& tree, std::span<const int> ids, const ForecastProvider& fp,
+                     const ScoreParams& params) {
+    ForecastBatch batch;
+    std::set<WorkflowId> seen;
+    std::string msg;
+    const char* err = nullptr;
+    std::size_t ok = 0;
+    for (; ok < ids.size(); ++ok) {
+        err = node_precheck(tree, ids[ok], fp, params, msg, &batch, seen);
+        if (err) break;
+    }
+    if (ok > 0) {
+        int agents = batch.outcomes ? batch.outcomes - 1 : 1;
+        pbkv_ctx* c = contexts().get(params.k, params.gamma, agents);
+        TreeImage& img = image();
+        img.build(tree);
+        check(pbkv_mirror_full(c, &img.soa), c);
+        batch.upload(c);
+        std::vector<double> out(ok);
+        check(pbkv_score_nodes(c, ids.data(), static_cast<std::int64_t>(ok), out.data()), c);
+        for (std::size_t i = 0; i < ok; ++i) tree.set_score(ids[i], out[i]);
+    }
+    if (err) throw ValidationError(err);
+    return static_cast<int>(ok);
+}
+
+inline VictimSelection select(const CacheTree& tree, int policy, std::int64_t needed,
+                              const std::map<WorkflowId, std::vector<AgentId>>* remaining,
+                              const std::set<int>& locked) {
+    // selection needs no forecasts; the context's score parameters are unused
+    pbkv_ctx* c = contexts().get(3, 0.7, 63);
+    TreeImage& img = image();
+    img.build(tree);
+    check(pbkv_mirror_full(c, &img.soa), c);
+    if (policy == PBKV_POLICY_KVFLOW) {
+        std::vector<std::int64_t> wf, off{0};
+        std::vector<std::int32_t> seq;
+        for (const auto& [w, s] : *remaining) {
+            wf.push_back(static_cast<std::int64_t>(w));
+            for (AgentId a : s) seq.push_back(static_cast<std::int32_t>(a));
+            off.push_back(static_cast<std::int64_t>(seq.size()));
+        }
+        check(pbkv_set_remaining(c, wf.data(), static_cast<std::int64_t>(wf.size()), off.data(), seq.data()), c);
+    }
+    std::vector<std::int32_t> lk(locked.begin(), locked.end());
+    VictimSelection sel;
+    sel.victims.resize(tree.node_count());
+    std::int64_t nv = 0, freed = 0;
+    int shortfall = 0;
+    check(pbkv_select(c, policy, PBKV_SCORE_CACHED, needed, lk.data(), static_cast<std::int64_t>(lk.size()),
+                      sel.victims.data(), static_cast<std::int64_t>(sel.victims.size()), &nv, &freed, &shortfall),
+          c);
+    sel.victims.resize(static_cast<std::size_t>(nv));
+    sel.freed = freed;
+    sel.shortfall = shortfall != 0;
+    return sel;
+}
+
+inline PrefetchPlan plan(const CacheTree& tree, const ForecastProvider& fp, std::int64_t bandwidth,
+                         int step_duration, double rho) {
+    // candidates: host nodes with a DEVICE parent (policies.hpp:190-193); the
+    // first one (host_index_ order) with a missing forecast raises
+    ForecastBatch batch;
+    std::set<WorkflowId> seen;
+    for (auto [last, id] : tree.host_nodes()) {
+        (void)last;
+        const CacheTree::Node& n = tree.node(id);
+        if (tree.node(n.parent).tier != Tier::Device) continue;
+        for (const auto& [w, b] : n.access) {
+            (void)b;
+            const Forecast* f = fp(w);
+            if (!f) throw ValidationError("missing forecast for active workflow " + std::to_string(w));
+            if (seen.insert(w).second) batch.add(w, *f);
+        }
+    }
+    const int agents = batch.outcomes ? batch.outcomes - 1 : 1;
+    // Eq. 1 reads step 0 only: any horizon >= 1 serves (context K = 1)
+    pbkv_ctx* c = contexts().get(1, 0.7, agents);
+    TreeImage& img = image();
+    img.build(tree);
+    check(pbkv_mirror_full(c, &img.soa), c);
+    batch.upload(c);
+    pbkv_prefetch_plan p{};
+    const std::int64_t cap = static_cast<std::int64_t>(tree.host_nodes().size());
+    std::vector<std::int32_t> cid(static_cast<std::size_t>(cap) + 1), sel(static_cast<std::size_t>(cap) + 1);
+    std::vector<double> cv(static_cast<std::size_t>(cap) + 1);
+    check(pbkv_plan_prefetch(c, bandwidth, step_duration, rho, cid.data(), cv.data(), cap, sel.data(), cap, &p), c);
+    PrefetchPlan out;
+    out.budget_space = p.budget_space;
+    out.budget_bw = p.budget_bw;
+    out.displacement_budget = p.displacement_budget;
+    out.selected_tokens = p.selected_tokens;
+    out.candidates.reserve(static_cast<std::size_t>(p.n_candidates));
+    for (std::int64_t i = 0; i < p.n_candidates; ++i)
+        out.candidates.push_back({cid[static_cast<std::size_t>(i)], cv[static_cast<std::size_t>(i)]});
+    out.selected.assign(sel.begin(), sel.begin() + p.n_selected);
+    return out;
+}
+
+}  // namespace detail
+
+// ---- scoring.hpp -------------------------------------------------------------
+inline int refresh_scores(CacheTree& tree, WorkflowId changed_workflow, const ForecastProvider& forecasts,
+                          const ScoreParams& params) {
+    const std::vector<int>* touched = tree.touched_nodes(changed_workflow);
+    if (!touched) return 0;
+    const std::vector<int> ids = *touched;  // set_score never changes the list
+    return detail::score_ids(tree, ids, forecasts, params);
+}
+
+inline void refresh_nodes(CacheTree& tree, std::span<const int> ids, const ForecastProvider& forecasts,
+                          const ScoreParams& params) {
+    detail::score_ids(tree, ids, forecasts, params);
+}
+
+// ---- policies.hpp ------------------------------------------------------------
+inline VictimSelection select_victims_lru(const CacheTree& tree, std::int64_t needed,
+                                          const std::set<int>& locked = {}) {
+    return detail::select(tree, PBKV_POLICY_LRU, needed, nullptr, locked);
+}
+
+inline VictimSelection select_victims_lae(const CacheTree& tree, std::int64_t needed,
+                                          const std::set<int>& locked = {}) {
+    return detail::select(tree, PBKV_POLICY_LAE, needed, nullptr, locked);
+}
+
+inline VictimSelection select_victims_hierarchical(const CacheTree& tree, std::int64_t needed,
+                                                   const std::set<int>& locked = {}) {
+    return detail::select(tree, PBKV_POLICY_HE, needed, nullptr, locked);
+}
+
+inline VictimSelection select_victims_kvflow(const CacheTree& tree, std::int64_t needed,
+                                             const std::map<WorkflowId, std::vector<AgentId>>& remaining,
+                                             const std::set<int>& locked = {}) {
+    return detail::select(tree, PBKV_POLICY_KVFLOW, needed, &remaining, locked);
+}
+
+inline VictimSelection select_victims(const CacheTree& tree, EvictionPolicy policy, std::int64_t needed,
+                                      const std::map<WorkflowId, std::vector<AgentId>>* remaining,
+                                      const std::set<int>& locked = {}) {
+    switch (policy) {
+        // qualified: argument-dependent lookup would also find flowkv::
+        case EvictionPolicy::Lru: return gpu::select_victims_lru(tree, needed, locked);
+        case EvictionPolicy::Lae: return gpu::select_victims_lae(tree, needed, locked);
+        case EvictionPolicy::Hierarchical: return gpu::select_victims_hierarchical(tree, needed, locked);
+        case EvictionPolicy::KvFlow:
+            if (!remaining) throw ValidationError("kvflow selected without static sequences");
+            return gpu::select_victims_kvflow(tree, needed, *remaining, locked);
+    }
+    throw ValidationError("unknown eviction policy");
+}
+
+inline PrefetchPlan plan_conservative_prefetch(const CacheTree& tree, const ForecastProvider& forecasts,
+                                               std::int64_t bandwidth, int step_duration = 1) {
+    return detail::plan(tree, forecasts, bandwidth, step_duration, -1.0);
+}
+
+inline PrefetchPlan plan_aggressive_prefetch(const CacheTree& tree, const ForecastProvider& forecasts,
+                                             std::int64_t bandwidth, double rho, int step_duration = 1) {
+    if (rho < 0.0 || rho > 1.0) throw ValidationError("rho must be in [0, 1]");
+    return detail::plan(tree, forecasts, bandwidth, step_duration, rho);
+}
+
+}  // namespace flowkv::gpu

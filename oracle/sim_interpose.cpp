@@ -1,0 +1,87 @@
+// sim_interpose.cpp -- the UNMODIFIED reference simulator with its policy call
+// sites redirected to the GPU drop-in (include/pbkv/flowkv_gpu.hpp).
+//
+// TEST INFRASTRUCTURE (parity harness for BASELINE configs 1 and 5).  Built by
+// oracle/Makefile twice from this one file:
+//   _ref/sim_cpu  -- plain reference build (no interposition): the oracle run
+//   _ref/sim_gpu  -- -DPBKV_INTERPOSE: simulator.hpp:434, :464, :618, :636-637,
+//                    :657 call flowkv::gpu::* (the product, libpbkv.so)
+// Technique: SURVEY.md App. A.4 -- the CPU definitions are included first
+// (#pragma once), then the call-site names are macro-renamed only while
+// simulator.hpp is parsed.  No reference source is edited or copied.
+//
+// Usage: sim_{cpu,gpu} <scenario.json> [cell-substring] [max-seeds]
+// Prints one line per (cell, seed):
+//   cell seed hit_rate evictions prefetch_tokens shortfalls events_fnv dump_fnv
+// events_fnv / dump_fnv are FNV-1a 64 of events_to_log() (simulator.hpp:191)
+// and of the final CacheTree::dump() (cache.hpp:330).
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "flowkv/policies.hpp"
+#include "flowkv/scoring.hpp"
+
+#ifdef PBKV_INTERPOSE
+#include "pbkv/flowkv_gpu.hpp"
+#define select_victims gpu::select_victims
+#define select_victims_hierarchical gpu::select_victims_hierarchical
+#define plan_conservative_prefetch gpu::plan_conservative_prefetch
+#define plan_aggressive_prefetch gpu::plan_aggressive_prefetch
+#define refresh_scores gpu::refresh_scores
+#define refresh_nodes gpu::refresh_nodes
+#endif
+#include "flowkv/simulator.hpp"
+#ifdef PBKV_INTERPOSE
+#undef select_victims
+#undef select_victims_hierarchical
+#undef plan_conservative_prefetch
+#undef plan_aggressive_prefetch
+#undef refresh_scores
+#undef refresh_nodes
+#endif
+#include "flowkv/scenario.hpp"
+
+static std::uint64_t fnv1a(const std::string& s) {
+    std::uint64_t h = 1469598103934665603ull;
+    for (unsigned char ch : s) {
+        h ^= ch;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::fprintf(stderr, "usage: %s <scenario.json> [cell-substring] [max-seeds]\n", argv[0]);
+        return 2;
+    }
+    try {
+        flowkv::Scenario sc = flowkv::Scenario::from_file(argv[1]);
+        const std::string filt = argc > 2 ? argv[2] : "";
+        const std::size_t max_seeds = argc > 3 ? std::strtoul(argv[3], nullptr, 10) : sc.seeds.size();
+        for (const auto& cell : sc.cells()) {
+            if (!filt.empty() && cell.id.find(filt) == std::string::npos) continue;
+            for (std::size_t s = 0; s < sc.seeds.size() && s < max_seeds; ++s) {
+                flowkv::SimConfig cfg = sc.config_for(cell, sc.seeds[s]);
+                auto t0 = std::chrono::steady_clock::now();
+                flowkv::RunResult r = flowkv::run(cfg);
+                double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                const auto& m = r.metrics;
+                std::printf("%s %llu %s %lld %lld %lld %016llx %016llx %.3f\n", cell.id.c_str(),
+                            static_cast<unsigned long long>(sc.seeds[s]), flowkv::fmt_double(m.hit_rate).c_str(),
+                            static_cast<long long>(m.evictions), static_cast<long long>(m.prefetch_tokens),
+                            static_cast<long long>(m.shortfalls),
+                            static_cast<unsigned long long>(fnv1a(flowkv::events_to_log(r.events))),
+                            static_cast<unsigned long long>(fnv1a(r.final_dump)), secs);
+                std::fflush(stdout);
+            }
+        }
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+    return 0;
+}

@@ -71,7 +71,7 @@ def build_oracle(verbose: bool = False) -> None:
     odir = os.path.join(ROOT, "oracle")
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/include/flowkv"):
-        targets.append("ref")
+        targets += ["ref", "sim"]  # sim_gpu links the product library built above
     subprocess.run(["make", "-s", "-C", odir, *targets], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
 
