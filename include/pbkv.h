@@ -158,6 +158,44 @@ int pbkv_forecast_put(pbkv_ctx* ctx, const int64_t* wf, int64_t n, int horizon, 
 int pbkv_forecast_drop(pbkv_ctx* ctx, const int64_t* wf, int64_t n);
 int pbkv_forecast_clear(pbkv_ctx* ctx);
 
+/* ---- stage 1: the multi-step predictor ---------------
+ * Replaces the predictor slot Simulator::predict (simulator.hpp:414-421): a
+ * batched forward that emits K next-agent distributions over A agents + END
+ * per workflow and stores them as that workflow's resident forecast (the
+ * same rows pbkv_forecast_put writes; simulator.hpp:433).  The reference has
+ * no code for this model; weights are the caller's.
+ * Shapes: d must be 64 (one UMMA N tile), text_dim a multiple of 64. */
+typedef struct pbkv_predictor_cfg {
+    int num_agents; /* A, must equal the context's */
+    int horizon;    /* K steps emitted per workflow (>= 1) */
+    int dim;        /* d: agent embedding width (64) */
+    int hidden;     /* h1: MLP hidden width (1..256) */
+    int text_dim;   /* H: prefill hidden size (multiple of 64) */
+    int max_prefix; /* longest accepted prefix (agents) */
+} pbkv_predictor_cfg;
+
+typedef struct pbkv_predictor_weights {
+    const float* embed;      /* [A][d]     H^(0), learnable agent embeddings */
+    const float* transition; /* [A][A]     row-normalised transition matrix */
+    const float* sage1;      /* [d][2d]    W^(1) */
+    const float* sage2;      /* [d][2d]    W^(2) */
+    const float* query;      /* [d][d]     W_q */
+    const uint16_t* text;    /* [d][H]     W_t (bf16 bit patterns) */
+    const float* mlp1;       /* [h1][3d]   first MLP layer, input [h_cur|h_path|h_txt] */
+    const float* mlp1_bias;  /* [h1] */
+    const float* mlp2;       /* [K*(A+1)][h1] */
+    const float* mlp2_bias;  /* [K*(A+1)] */
+} pbkv_predictor_weights;
+
+int pbkv_predictor_load(pbkv_ctx* ctx, const pbkv_predictor_cfg* cfg, const pbkv_predictor_weights* w);
+/* Forward for n workflows: prefix CSR (prefix_off[n+1] into prefix; each
+ * prefix is (v_1..v_t), t >= 1, current agent last), x = [n][H] bf16 post-norm
+ * hidden states of the last prefill token (device memory when x_on_device,
+ * else host).  probs_out (host, n x K x (A+1), nullable) receives the FP64
+ * forecasts that were stored. */
+int pbkv_predict(pbkv_ctx* ctx, const int64_t* wf, int64_t n, const int64_t* prefix_off, const int32_t* prefix,
+                 const uint16_t* x, int x_on_device, double* probs_out);
+
 /* ---- stage 2: Score(c), Eq. 2 ---------------------------------------------- */
 /* multi_step_score(node_terms(...)) (scoring.hpp:49-75) for every node; nodes
  * without access entries score +0.0.  Raises EINVAL "missing forecast for

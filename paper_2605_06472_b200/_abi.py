@@ -80,6 +80,21 @@ class SynthParams(C.Structure):
     ]
 
 
+class PredictorCfg(C.Structure):
+    """pbkv_predictor_cfg"""
+    _fields_ = [("num_agents", C.c_int), ("horizon", C.c_int), ("dim", C.c_int), ("hidden", C.c_int),
+                ("text_dim", C.c_int), ("max_prefix", C.c_int)]
+
+
+class PredictorWeights(C.Structure):
+    """pbkv_predictor_weights"""
+    _fields_ = [("embed", C.POINTER(C.c_float)), ("transition", C.POINTER(C.c_float)),
+                ("sage1", C.POINTER(C.c_float)), ("sage2", C.POINTER(C.c_float)),
+                ("query", C.POINTER(C.c_float)), ("text", C.POINTER(C.c_uint16)),
+                ("mlp1", C.POINTER(C.c_float)), ("mlp1_bias", C.POINTER(C.c_float)),
+                ("mlp2", C.POINTER(C.c_float)), ("mlp2_bias", C.POINTER(C.c_float))]
+
+
 def synth_params(n_nodes=10000, n_workflows=256, agents=16, group_size=16, shared_len=32, group_len=8,
                  alphabet=4, max_rand_len=10, retired_frac=0.3, host_every=10, seed=12345) -> SynthParams:
     """SURVEY.md §8(d) synthetic workload (generator: csrc/host/ops.hpp)."""
@@ -186,6 +201,8 @@ def lib() -> C.CDLL:
         "pbkv_set_remaining": ([vp, _i64p, C.c_int64, _i64p, _i32p], C.c_int),
         "pbkv_plan_prefetch": ([vp, C.c_int64, C.c_int, C.c_double, _i32p, _f64p, C.c_int64, _i32p, C.c_int64,
                                 C.POINTER(PrefetchPlanC)], C.c_int),
+        "pbkv_predictor_load": ([vp, C.POINTER(PredictorCfg), C.POINTER(PredictorWeights)], C.c_int),
+        "pbkv_predict": ([vp, _i64p, C.c_int64, _i64p, _i32p, vp, C.c_int, _f64p], C.c_int),
         "pbkv_tree_create": ([C.POINTER(vp), C.c_int64, C.c_int64], C.c_int),
         "pbkv_tree_destroy": ([vp], C.c_int),
         "pbkv_tree_apply_ops": ([vp, _i64p, C.c_int64], C.c_int),

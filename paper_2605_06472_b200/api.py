@@ -204,6 +204,41 @@ class Policy:
         self._c(_abi.lib().pbkv_set_remaining(self._h, ptr(wf, C.c_int64), int(wf.size), ptr(off, C.c_int64),
                                               ptr(seq, C.c_int32)))
 
+    # ---- stage 1 -------------------------------------------------------------------
+    def load_predictor(self, w, max_prefix: int = 64) -> None:
+        """pbkv_predictor_load: weights of the PAPER.md:1040-1066 model
+        (paper_2605_06472_b200.predictor.PredictorWeights)."""
+        cfg = _abi.PredictorCfg(w.num_agents, w.horizon, w.dim, w.hidden, w.text_dim, max_prefix)
+        keep = {f: np.ascontiguousarray(getattr(w, f)) for f in
+                ("embed", "transition", "sage1", "sage2", "query", "mlp1", "mlp1_bias", "mlp2", "mlp2_bias")}
+        keep["text"] = np.ascontiguousarray(w.text, dtype=np.uint16)
+        pw = _abi.PredictorWeights(**{f: ptr(a, C.c_uint16 if f == "text" else C.c_float) for f, a in keep.items()})
+        self._c(_abi.lib().pbkv_predictor_load(self._h, C.byref(cfg), C.byref(pw)))
+        self._pred = (w.horizon, w.num_agents + 1, w.text_dim)
+
+    def predict(self, wf_ids: Sequence[int], prefix_off: np.ndarray, prefix: np.ndarray, x, *,
+                x_device_ptr: int | None = None, want_probs: bool = True) -> np.ndarray | None:
+        """pbkv_predict: one batched forward; the forecasts become resident
+        (replacing put_forecasts).  x: [n, H] bf16 bits (host), or pass
+        x_device_ptr for hidden states already in HBM.  Returns the stored
+        [n, K, A+1] float64 forecasts when want_probs."""
+        K, V1, H = self._pred
+        w = np.ascontiguousarray(wf_ids, dtype=np.int64)
+        off = np.ascontiguousarray(prefix_off, dtype=np.int64)
+        pre = np.ascontiguousarray(prefix if len(prefix) else [0], dtype=np.int32)
+        out = np.zeros((w.size, K, V1), dtype=np.float64) if want_probs else None
+        if x_device_ptr is not None:
+            xp, on_dev = C.c_void_p(int(x_device_ptr)), 1
+        else:
+            xa = np.ascontiguousarray(x, dtype=np.uint16)
+            if xa.shape != (w.size, H):
+                raise ValueError("x must be [n_workflows, text_dim] bf16 bits")
+            xp, on_dev = C.c_void_p(xa.ctypes.data), 0
+        self._c(_abi.lib().pbkv_predict(self._h, ptr(w, C.c_int64), int(w.size), ptr(off, C.c_int64),
+                                        ptr(pre, C.c_int32), xp, on_dev,
+                                        ptr(out, C.c_double) if out is not None else ptr(None, C.c_double)))
+        return out
+
     # ---- stage 2 -------------------------------------------------------------------
     def score_all(self) -> np.ndarray:
         out = np.zeros(self.n_nodes, dtype=np.float64)

@@ -816,6 +816,78 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
     });
 }
 
+// ---- stage 1: predictor ----------------------------------------------------------
+int pbkv_predictor_load(pbkv_ctx* c, const pbkv_predictor_cfg* cfg, const pbkv_predictor_weights* w) {
+    return api(c, [&] {
+        need(c && cfg && w, "null argument");
+        need(w->embed && w->transition && w->sage1 && w->sage2 && w->query && w->text && w->mlp1 && w->mlp1_bias &&
+                 w->mlp2 && w->mlp2_bias,
+             "predictor weights: missing array");
+        if (cfg->num_agents != c->A) invalid("predictor agent count does not match the context's");
+        if (cfg->horizon < 1) invalid("forecast horizon must be >= 1");
+        need(cfg->dim == 64, "predictor dim must be 64 (one UMMA N tile)");
+        need(cfg->text_dim >= 64 && cfg->text_dim % 64 == 0, "predictor text_dim must be a positive multiple of 64");
+        need(cfg->hidden >= 1 && cfg->hidden <= 256, "predictor hidden width must be in [1, 256]");
+        need(cfg->max_prefix >= 1, "predictor max_prefix must be >= 1");
+        need(cfg->horizon * (cfg->num_agents + 1) <= 1024, "predictor K*(A+1) must be <= 1024");
+        set_device(*c);
+        predictor_load(*c, *cfg, *w);
+    });
+}
+
+int pbkv_predict(pbkv_ctx* c, const int64_t* wf, int64_t n, const int64_t* prefix_off, const int32_t* prefix,
+                 const uint16_t* x, int x_on_device, double* probs_out) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        if (!c->pred) throw ApiError(PBKV_EARG, "no predictor loaded (pbkv_predictor_load)");
+        if (n == 0) return;
+        need(wf && prefix_off && prefix && x, "null argument");
+        set_device(*c);
+        const pbkv_predictor_cfg cfg = predictor_cfg(*c);
+        std::vector<int> off(static_cast<std::size_t>(n) + 1);
+        need(prefix_off[0] == 0, "prefix offsets must start at 0");
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t t = prefix_off[i + 1] - prefix_off[i];
+            if (t < 1) invalid("predictor needs a non-empty prefix (current agent last)");
+            if (t > cfg.max_prefix) invalid("prefix longer than the predictor's max_prefix");
+            off[static_cast<std::size_t>(i)] = static_cast<int>(prefix_off[i]);
+        }
+        off[static_cast<std::size_t>(n)] = static_cast<int>(prefix_off[n]);
+        const int64_t np = prefix_off[n];
+        for (int64_t j = 0; j < np; ++j)
+            if (prefix[j] < 0 || prefix[j] >= cfg.num_agents) invalid("prefix agent out of range");
+        std::vector<long long> slots(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) slots[static_cast<std::size_t>(i)] = slot_for(*c, wf[i]);
+        const std::size_t per = static_cast<std::size_t>(cfg.horizon) * (cfg.num_agents + 1);
+        c->fstage.reserve(static_cast<std::size_t>(n) * per);
+        c->fstage_slot.reserve(static_cast<std::size_t>(n));
+        c->pre_off.reserve(static_cast<std::size_t>(n) + 1);
+        c->pre.reserve(static_cast<std::size_t>(np) + 1);
+        cudaStream_t st = c->stream;
+        PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots.data(), slots.size() * sizeof(long long),
+                                  cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c->pre_off.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c->pre.p, prefix, static_cast<std::size_t>(np) * sizeof(int), cudaMemcpyHostToDevice,
+                                  st));
+        const void* xd = x;
+        if (!x_on_device) {
+            const std::size_t xb = static_cast<std::size_t>(n) * cfg.text_dim;
+            c->xstage.reserve(xb);
+            PBKV_CUDA(cudaMemcpyAsync(c->xstage.p, x, xb * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+            xd = c->xstage.p;
+        }
+        reset_status(*c);
+        record(*c, 0);
+        predictor_run(*c, n, c->pre_off.p, c->pre.p, xd, c->fstage_slot.p, probs_out ? c->fstage.p : nullptr);
+        record(*c, 1);
+        if (probs_out)
+            PBKV_CUDA(cudaMemcpyAsync(probs_out, c->fstage.p, static_cast<std::size_t>(n) * per * sizeof(double),
+                                      cudaMemcpyDeviceToHost, st));
+        check_status(*c);
+        finish_timing(*c, 1);
+    });
+}
+
 // ---- host tree ------------------------------------------------------------------
 int pbkv_tree_create(pbkv_tree** out, int64_t device_capacity, int64_t host_capacity) {
     return api(nullptr, [&] {

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -155,6 +156,8 @@ struct SelectCounts {
     int shortfall = 0;
 };
 
+struct PredictorState;  // predict.cu
+
 struct Context {
     int device = 0;
     int K = 3;
@@ -238,6 +241,11 @@ struct Context {
     PinBuf<long long> hcounters;
     PinBuf<DevStatus> hstatus;
 
+    // ---- stage-1 predictor (predict.cu) -----------------------------------------
+    std::shared_ptr<PredictorState> pred;
+    DevBuf<int> pre_off, pre;
+    DevBuf<std::uint16_t> xstage;
+
     // launch accounting (pbkv kernels; CUB library calls counted separately)
     long long launches = 0, lib_calls = 0;
 
@@ -259,6 +267,10 @@ std::size_t sel_state_bytes();
 void launch_prefetch_candidates(Context& c, unsigned long long* n_cand_dev);
 void launch_prefetch_err_id(Context& c);
 void launch_prefetch_sort_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev);
+void predictor_load(Context& c, const pbkv_predictor_cfg& cfg, const pbkv_predictor_weights& w);
+pbkv_predictor_cfg predictor_cfg(const Context& c);
+void predictor_run(Context& c, std::int64_t n, const int* pre_off_dev, const int* pre_dev, const void* x_dev,
+                   const long long* slots_dev, double* probs_dev);
 void reset_status(Context& c);
 void check_status(Context& c);  // syncs and throws on a device-side error
 
