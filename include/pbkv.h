@@ -229,6 +229,51 @@ int pbkv_select_dev(pbkv_ctx* ctx, int policy, int score_mode, int64_t needed, c
 int pbkv_set_remaining(pbkv_ctx* ctx, const int64_t* wf, int64_t n_wf, const int64_t* seq_off,
                        const int32_t* seq);
 
+/* ---- node-set sharding across GPUs (config 4) ---------------
+ * One context per rank over the rank's shard: the subtrees it owns plus a copy
+ * of the spine (ancestors whose subtrees span ranks), local ids increasing in
+ * global id.  The global order is the merge of the ranks' local orders plus
+ * the spine records; host code exchanges the records (paper_2605_06472_b200/
+ * shard.py over torch.distributed / NCCL).  Order key of a record: (w0, w1,
+ * eff_gid, d) = the chain head's CandidateKey (policies.hpp:40-48), then the
+ * distance below the head. */
+typedef struct pbkv_cand {
+    uint64_t w0, w1; /* packed CandidateKey of the chain head (cls, rank, last_access) */
+    int32_t eff_gid; /* global id of the chain head (the key's id component) */
+    int32_t gid;     /* global id of the victim */
+    int32_t d;       /* depth(head) - depth(victim) */
+    int32_t len;     /* tokens freed */
+} pbkv_cand;
+
+typedef struct pbkv_spine_info {
+    uint64_t w0, w1;   /* max key over the rank's device descendants of the spine node */
+    int32_t eff_gid;   /* its global id (-1 when has_eff == 0) */
+    int32_t eff_depth; /* its depth */
+    int32_t has_eff;   /* the rank has device descendants below this spine node */
+    int32_t sublock;   /* a locked node lies below (or is) this spine node on this rank */
+} pbkv_spine_info;
+
+/* Global ids of the local nodes ([n_nodes], increasing) and the local ids of
+ * the spine copies.  Kept across pbkv_mirror_* calls. */
+int pbkv_shard_set(pbkv_ctx* ctx, const int32_t* global_ids, const int32_t* spine, int64_t n_spine);
+/* Local selection (spine excluded) -> records of the local cut in local
+ * order (device array, cap entries) and one pbkv_spine_info per spine node
+ * (device).  result_dev = int64[3] {n_cand, freed_local, shortfall_local}. */
+int pbkv_shard_select(pbkv_ctx* ctx, int policy, int score_mode, int64_t needed, const int32_t* locked_dev,
+                      int64_t n_locked, pbkv_cand* cand_dev, int64_t cap, pbkv_spine_info* spine_dev,
+                      int64_t* result_dev);
+/* Eq. 2 products of the spine nodes' local entries (node-major, WorkflowId
+ * order, K per entry) into out_dev; counts[j] = entries(spine j) * K (host). */
+int pbkv_shard_spine_products(pbkv_ctx* ctx, double* out_dev, int64_t* counts);
+/* Exact serial FP64 chains: out[b] = RN-sum of x_dev[off[b], off[b+1]) in
+ * order (off, out on the host). */
+int pbkv_chain_sum(pbkv_ctx* ctx, const double* x_dev, const int64_t* off, int n_seg, double* out);
+/* Merge of exchanged record runs (each sorted) and the cut at `needed`:
+ * victims_dev receives global ids in eviction order; result_dev = int64[3]
+ * {n_victims, freed, shortfall}. */
+int pbkv_merge_cut(pbkv_ctx* ctx, const pbkv_cand* runs_dev, const int64_t* run_start, const int64_t* run_len,
+                   int n_runs, int64_t needed, int32_t* victims_dev, int64_t* result_dev);
+
 /* ---- stage 4: prefetch candidate ranking ----------------------------------- */
 /* plan_conservative_prefetch (rho < 0) / plan_aggressive_prefetch (rho in
  * [0,1]) (policies.hpp:181-235).  Candidates (id, Eq.1 value) sorted by value

@@ -17,10 +17,11 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpbkv.so")
 
-SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu", "predict.cu"]
+SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu", "predict.cu", "shard.cu"]
 HEADERS = [
     "pbkv_internal.cuh",
     "common.cuh",
+    "chain.cuh",
     os.path.join("host", "radix_mirror.hpp"),
     os.path.join("host", "ops.hpp"),
 ]

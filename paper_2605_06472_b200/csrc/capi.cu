@@ -339,6 +339,10 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     c.host_capacity = s.host_capacity;
     c.host_used = s.host_used;
     ensure_scratch(c);
+    if (!c.spine.empty()) {
+        for (int v : c.spine) need(v >= 0 && v < n, "shard spine id out of range for the mirrored tree");
+        shard_apply_flags(c);
+    }
     PBKV_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -813,6 +817,127 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
             std::int64_t m = std::min<std::int64_t>(sel_cap, plan->n_selected);
             if (m > 0) PBKV_CUDA(cudaMemcpy(selected, c->sel.p, m * sizeof(int), cudaMemcpyDeviceToHost));
         }
+    });
+}
+
+// ---- sharding ---------------------------------------------------------------------
+int pbkv_shard_set(pbkv_ctx* c, const int32_t* global_ids, const int32_t* spine, int64_t n_spine) {
+    return api(c, [&] {
+        need(c && global_ids && (n_spine == 0 || spine), "null argument");
+        need(c->n >= 1, "no tree mirrored");
+        set_device(*c);
+        c->spine.assign(spine, spine + n_spine);
+        std::vector<char> is_sp(static_cast<std::size_t>(c->n), 0);
+        for (int v : c->spine) {
+            need(v >= 0 && v < c->n, "shard spine id out of range");
+            is_sp[static_cast<std::size_t>(v)] = 1;
+        }
+        // local tie-breaks (node id) must agree with global ones among the
+        // nodes that can be candidates: global ids increase with local ids
+        long long prev = LLONG_MIN;
+        for (int64_t i = 1; i < c->n; ++i) {
+            if (is_sp[static_cast<std::size_t>(i)]) continue;
+            need(global_ids[i] > prev, "shard global ids must increase with local ids (non-spine nodes)");
+            prev = global_ids[i];
+        }
+        c->gid.reserve(static_cast<std::size_t>(c->n));
+        PBKV_CUDA(cudaMemcpyAsync(c->gid.p, global_ids, static_cast<std::size_t>(c->n) * sizeof(int),
+                                  cudaMemcpyHostToDevice, c->stream));
+        shard_apply_flags(*c);
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_shard_select(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const int32_t* locked_dev,
+                      int64_t n_locked, pbkv_cand* cand_dev, int64_t cap, pbkv_spine_info* spine_dev,
+                      int64_t* result_dev) {
+    return api(c, [&] {
+        need(c && cand_dev && result_dev, "null argument");
+        need(c->gid.p != nullptr, "pbkv_shard_set not called");
+        need(n_locked == 0 || locked_dev, "null locked array");
+        need(c->spine.empty() || spine_dev, "null spine output");
+        if (policy == PBKV_POLICY_KVFLOW) throw ApiError(PBKV_EARG, "kvflow is not supported on a sharded tree");
+        set_device(*c);
+        long long* res = reinterpret_cast<long long*>(result_dev);
+        SelectCounts o = select_core(*c, policy, score_mode, needed, locked_dev, n_locked, res);
+        if (o.n_victims > cap) throw ApiError(PBKV_EARG, "candidate capacity too small");
+        shard_records(*c, res, cand_dev, cap);
+        shard_spine_report(*c, spine_dev);
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_shard_spine_products(pbkv_ctx* c, double* out_dev, int64_t* counts) {
+    return api(c, [&] {
+        need(c && counts, "null argument");
+        set_device(*c);
+        const std::size_t ns = c->spine.size();
+        std::vector<long long> base(ns + 1, 0);
+        long long mx = 0;
+        for (std::size_t j = 0; j < ns; ++j) {
+            const long long L = static_cast<long long>(c->h_entries[static_cast<std::size_t>(c->spine[j])]) * c->K;
+            counts[j] = L;
+            base[j + 1] = base[j] + L;
+            mx = std::max(mx, L);
+        }
+        if (ns == 0 || base[ns] == 0) return;
+        need(out_dev != nullptr, "null products array");
+        c->spine_base.reserve(ns + 1);
+        c->spine_miss.reserve(1);
+        PBKV_CUDA(cudaMemcpyAsync(c->spine_base.p, base.data(), (ns + 1) * sizeof(long long), cudaMemcpyHostToDevice,
+                                  c->stream));
+        PBKV_CUDA(cudaMemsetAsync(c->spine_miss.p, 0, sizeof(unsigned int), c->stream));
+        shard_spine_products(*c, c->spine_base.p, mx, out_dev, c->spine_miss.p);
+        unsigned int miss = 0;
+        PBKV_CUDA(cudaMemcpyAsync(&miss, c->spine_miss.p, sizeof miss, cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        if (miss) invalid("missing forecast for a workflow tagged on a spine node");
+    });
+}
+
+int pbkv_chain_sum(pbkv_ctx* c, const double* x_dev, const int64_t* off, int n_seg, double* out) {
+    return api(c, [&] {
+        need(c && off && out && n_seg >= 0, "null argument");
+        if (n_seg == 0) return;
+        need(x_dev || off[n_seg] == 0, "null products array");
+        for (int b = 0; b < n_seg; ++b) need(off[b + 1] >= off[b], "chain offsets must not decrease");
+        set_device(*c);
+        c->run_start.reserve(static_cast<std::size_t>(n_seg) + 1);
+        c->vals.reserve(static_cast<std::size_t>(n_seg));
+        PBKV_CUDA(cudaMemcpyAsync(c->run_start.p, off, (static_cast<std::size_t>(n_seg) + 1) * sizeof(long long),
+                                  cudaMemcpyHostToDevice, c->stream));
+        launch_chain_sum(*c, x_dev, c->run_start.p, n_seg, c->vals.p);
+        PBKV_CUDA(cudaMemcpyAsync(out, c->vals.p, static_cast<std::size_t>(n_seg) * sizeof(double),
+                                  cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int pbkv_merge_cut(pbkv_ctx* c, const pbkv_cand* runs_dev, const int64_t* run_start, const int64_t* run_len,
+                   int n_runs, int64_t needed, int32_t* victims_dev, int64_t* result_dev) {
+    return api(c, [&] {
+        need(c && run_start && run_len && victims_dev && result_dev && n_runs >= 0, "null argument");
+        if (needed <= 0) invalid("eviction request must free a positive amount");
+        set_device(*c);
+        long long total = 0, mx = 0;
+        for (int r = 0; r < n_runs; ++r) {
+            need(run_len[r] >= 0 && run_start[r] >= 0, "bad run extent");
+            total += run_len[r];
+            mx = std::max<long long>(mx, run_len[r]);
+        }
+        need(total == 0 || runs_dev, "null runs array");
+        c->merged.reserve(static_cast<std::size_t>(total) + 1);
+        c->run_start.reserve(static_cast<std::size_t>(n_runs) + 1);
+        c->run_len.reserve(static_cast<std::size_t>(n_runs) + 1);
+        if (n_runs > 0) {
+            PBKV_CUDA(cudaMemcpyAsync(c->run_start.p, run_start, n_runs * sizeof(long long), cudaMemcpyHostToDevice,
+                                      c->stream));
+            PBKV_CUDA(cudaMemcpyAsync(c->run_len.p, run_len, n_runs * sizeof(long long), cudaMemcpyHostToDevice,
+                                      c->stream));
+        }
+        shard_merge_cut(*c, runs_dev, c->run_start.p, c->run_len.p, n_runs, mx, total, c->merged.p, needed,
+                        victims_dev, reinterpret_cast<long long*>(result_dev));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -188,6 +188,10 @@ __device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score)
     const unsigned long long last = a.last[n];
     if (last >> 63) set_error(a.st, PBKV_EINVAL, kErrLastAccessRange, n);
     Key2 k;
+    if (f & kFlagExcluded) {  // sharded spine node (shard.cu)
+        reinterpret_cast<ulonglong2*>(a.keys)[n] = make_ulonglong2(0ull, 0ull);
+        return;
+    }
     switch (a.policy) {
         case PBKV_POLICY_LRU:
             k = make_key(0, 0.0, last);

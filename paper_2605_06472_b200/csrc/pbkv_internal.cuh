@@ -25,6 +25,9 @@ namespace pbkv {
 
 constexpr std::uint8_t kFlagTierMask = 0x3;
 constexpr std::uint8_t kFlagRetired = 0x4;
+// spine node of a sharded tree (shard.cu): never a local candidate, key zeroed
+// so that eff() of a spine node is the maximum over its local descendants only
+constexpr std::uint8_t kFlagExcluded = 0x8;
 constexpr int kMediumMaxChain = 256;  // entries*K above this -> heavy (CTA) path
 
 // first-error-wins device status (kernels never throw)
@@ -241,6 +244,13 @@ struct Context {
     PinBuf<long long> hcounters;
     PinBuf<DevStatus> hstatus;
 
+    // ---- sharding (shard.cu) -------------------------------------------------------
+    std::vector<int> spine;  // local ids of the spine copies
+    DevBuf<int> spine_dev, gid;
+    DevBuf<long long> spine_base, run_start, run_len;
+    DevBuf<unsigned int> spine_miss;
+    DevBuf<pbkv_cand> merged;
+
     // ---- stage-1 predictor (predict.cu) -----------------------------------------
     std::shared_ptr<PredictorState> pred;
     DevBuf<int> pre_off, pre;
@@ -259,6 +269,7 @@ struct Context {
 void launch_forecast_prepare(Context& c, const double* stage, const long long* slots, std::int64_t n, int H);
 void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool report_missing);
 void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int64_t n, double* out, bool value_only);
+void launch_chain_sum(Context& c, const double* x, const long long* off, int n_seg, double* out);
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
 void launch_keys_cached(Context& c, int policy);
 SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked, std::int64_t needed,
@@ -271,6 +282,13 @@ void predictor_load(Context& c, const pbkv_predictor_cfg& cfg, const pbkv_predic
 pbkv_predictor_cfg predictor_cfg(const Context& c);
 void predictor_run(Context& c, std::int64_t n, const int* pre_off_dev, const int* pre_dev, const void* x_dev,
                    const long long* slots_dev, double* probs_dev);
+void shard_apply_flags(Context& c);
+void shard_records(Context& c, long long* result_dev, pbkv_cand* out, long long cap);
+void shard_spine_report(Context& c, pbkv_spine_info* out);
+void shard_spine_products(Context& c, const long long* base_dev, long long max_len, double* out, unsigned int* miss);
+void shard_merge_cut(Context& c, const pbkv_cand* src, const long long* run_start_dev, const long long* run_len_dev,
+                     int n_runs, long long max_run, long long total, pbkv_cand* merged, long long needed,
+                     int* victims, long long* result);
 void reset_status(Context& c);
 void check_status(Context& c);  // syncs and throws on a device-side error
 

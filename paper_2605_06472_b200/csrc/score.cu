@@ -8,6 +8,7 @@
 //                             then one CTA per node evaluates the serial
 //                             rounding chain exactly in parallel per binade
 // The heavy path runs on a side stream, overlapped with the light pass.
+#include "chain.cuh"
 #include "common.cuh"
 
 namespace pbkv {
@@ -307,6 +308,38 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ScoreArgs s, KeyAr
     }
 }
 
+// Heavy nodes: one 1024-thread CTA per node runs the exact chain (chain.cuh)
+// over the node's products (heavy_products_kernel).
+template <bool kKeys>
+__global__ void __launch_bounds__(kChainT) heavy_chain_kernel(ScoreArgs s, KeyArgs ka, const int* nodes,
+                                                              const long long* xs_start, const double* xs_g,
+                                                              const unsigned int* hmiss, int report_missing) {
+    extern __shared__ __align__(16) unsigned char chain_raw[];
+    ChainSmem& sm = *reinterpret_cast<ChainSmem*>(chain_raw);
+    const int node = nodes[blockIdx.x];
+    const long long L = static_cast<long long>(s.acc_off[node + 1] - s.acc_off[node]) * s.K;
+    const double total = chain_eval(xs_g + xs_start[blockIdx.x], L, sm);
+    if (threadIdx.x == 0) {
+        s.out[node] = total;
+        const unsigned int miss = hmiss[blockIdx.x];
+        if (report_missing && miss)
+            set_error(s.st, PBKV_EINVAL, (miss & 1) ? kErrMissingForecast : kErrShortHorizon, node);
+        if constexpr (kKeys) {
+            ka.missing[node] = miss ? 1 : 0;
+            if (node != 0 && (ka.flags[node] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, node, total);
+        }
+    }
+}
+
+// Generic exact chains: out[b] = the chain over x[off[b], off[b+1]) (the
+// sharded spine score over all ranks' products, shard.cu).
+__global__ void __launch_bounds__(kChainT) chain_sum_kernel(const double* x, const long long* off, double* out) {
+    extern __shared__ __align__(16) unsigned char chain_raw[];
+    ChainSmem& sm = *reinterpret_cast<ChainSmem*>(chain_raw);
+    const double t = chain_eval(x + off[blockIdx.x], off[blockIdx.x + 1] - off[blockIdx.x], sm);
+    if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+
 // Eq. 1 / Eq. 2 of an id list, one thread per short id (refresh_nodes path)
 template <bool kValueOnly>
 __global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* ids, std::int64_t n, double* out) {
@@ -393,6 +426,18 @@ __global__ void gather_f64_kernel(const double* src, const int* ids, std::int64_
         dst[i] = src[ids[i]];
 }
 
+std::size_t chain_smem_bytes() {
+    static bool init = false;
+    const std::size_t b = sizeof(ChainSmem);
+    if (!init) {
+        PBKV_CUDA(cudaFuncSetAttribute(heavy_chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        PBKV_CUDA(cudaFuncSetAttribute(heavy_chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        PBKV_CUDA(cudaFuncSetAttribute(chain_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        init = true;
+    }
+    return b;
+}
+
 unsigned int grid_cap(std::int64_t n, int block) {
     std::int64_t want = (n + block - 1) / block;
     const std::int64_t cap = 148LL * 16;
@@ -466,12 +511,13 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
                                                                                c.n_hent, c.hxs.p, c.hmiss.p);
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
+        const unsigned int hb = static_cast<unsigned int>(c.n_heavy);
         if (write_keys)
-            chain_kernel<true, false, true><<<static_cast<unsigned int>(c.n_heavy), kChainThreads, 0, c.side>>>(
-                s, ka, c.heavy.p, c.hstart.p, c.hxs.p, c.hmiss.p, rm);
+            heavy_chain_kernel<true><<<hb, kChainT, chain_smem_bytes(), c.side>>>(s, ka, c.heavy.p, c.hstart.p,
+                                                                               c.hxs.p, c.hmiss.p, rm);
         else
-            chain_kernel<true, false, false><<<static_cast<unsigned int>(c.n_heavy), kChainThreads, 0, c.side>>>(
-                s, ka, c.heavy.p, c.hstart.p, c.hxs.p, c.hmiss.p, rm);
+            heavy_chain_kernel<false><<<hb, kChainT, chain_smem_bytes(), c.side>>>(s, ka, c.heavy.p, c.hstart.p,
+                                                                                c.hxs.p, c.hmiss.p, rm);
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
         PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
@@ -536,6 +582,12 @@ void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int
         ++c.launches;
     }
     (void)ids_dev;
+}
+
+void launch_chain_sum(Context& c, const double* x, const long long* off, int n_seg, double* out) {
+    chain_sum_kernel<<<static_cast<unsigned int>(n_seg), kChainT, chain_smem_bytes(), c.stream>>>(x, off, out);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
 }
 
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst) {

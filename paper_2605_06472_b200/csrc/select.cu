@@ -306,7 +306,8 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
         const std::int64_t i = base + threadIdx.x;
         const int n = static_cast<int>(i);
         bool head = false;
-        if (i < a.n_nodes && n != 0 && (a.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE && !__ldcg(&a.sublock[n])) {
+        if (i < a.n_nodes && n != 0 && (a.flags[n] & (kFlagTierMask | kFlagExcluded)) == PBKV_TIER_DEVICE &&
+            !__ldcg(&a.sublock[n])) {
             const std::uint8_t ms = a.missing[n];
             if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n);
             if (a.he_recompute && ms && !(a.flags[n] & kFlagRetired))
@@ -322,7 +323,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
                 w += static_cast<unsigned long long>(a.len[p]);
                 ++c;
                 p = a.parent[p];
-            } while (p > 0 && !__ldcg(&a.sublock[p]) && __ldcg(&a.eff[p]) == n);
+            } while (p > 0 && !(a.flags[p] & kFlagExcluded) && !__ldcg(&a.sublock[p]) && __ldcg(&a.eff[p]) == n);
             a.W[n] = w;
             a.C[n] = c;
             a.rank[n] = -1;
@@ -564,7 +565,8 @@ __device__ __forceinline__ void sort_bucket(const SelArgs& a, int* S, unsigned i
 __device__ __forceinline__ void phase_scatter(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
     for (std::int64_t i = tid; i < a.n_nodes; i += nthr) {
         const int n = static_cast<int>(i);
-        if (n == 0 || (a.flags[n] & kFlagTierMask) != PBKV_TIER_DEVICE || __ldcg(&a.sublock[n])) continue;
+        if (n == 0 || (a.flags[n] & (kFlagTierMask | kFlagExcluded)) != PBKV_TIER_DEVICE || __ldcg(&a.sublock[n]))
+            continue;
         const int h = __ldcg(&a.eff[n]);
         const int r = __ldcg(&a.rank[h]);
         if (r < 0) continue;

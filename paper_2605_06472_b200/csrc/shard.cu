@@ -1,0 +1,234 @@
+// Node-set sharding of stages 2-3 across GPUs (BASELINE config 4).
+//
+// A rank holds the subtrees below the shared "spine" that it owns, plus a
+// copy of the spine itself (the ancestors whose subtrees span ranks).  Local
+// node ids are increasing in global id, so local tie-breaks agree with global
+// ones.  Spine nodes are flagged kFlagExcluded: they never enter the local
+// order, their keys are zeroed so eff(spine) is the maximum over the rank's
+// own descendants, and chains stop below them.  The global victim order is
+// then the merge of the per-rank orders plus the spine records, cut at the
+// shortest prefix with sum(len) >= needed:
+//   - each rank's local cut (shortest local prefix reaching `needed`) bounds
+//     its share of the global prefix, so exchanging only local cuts is exact;
+//   - spine scores (HE) are exact chains over all ranks' products in global
+//     WorkflowId order (ranks own contiguous WorkflowId blocks).
+// Kernels: candidate records of the local cut, spine reports, spine products,
+// merge-path rank merge of the exchanged runs, single-CTA cut.
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+
+namespace pbkv {
+
+using namespace dev;
+
+namespace {
+
+__device__ __forceinline__ bool cand_less(const pbkv_cand& a, const pbkv_cand& b) {
+    if (a.w0 != b.w0) return a.w0 < b.w0;
+    if (a.w1 != b.w1) return a.w1 < b.w1;
+    if (a.eff_gid != b.eff_gid) return a.eff_gid < b.eff_gid;
+    return a.d < b.d;
+}
+
+__global__ void mark_excluded_kernel(std::uint8_t* flags, const int* ids, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[ids[i]] |= kFlagExcluded;
+}
+
+// record of victim i of the local cut: the key of its chain head, the head's
+// global id, its distance below the head, its length, its global id
+__global__ void records_kernel(const int* victims, const long long* result, const Key2* keys, const int* eff,
+                               const int* depth, const int* len, const int* gid, pbkv_cand* out) {
+    const long long n = result[0];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int v = victims[i];
+        const int h = eff[v];
+        const Key2 k = load_key(keys, h);
+        pbkv_cand r;
+        r.w0 = k.w0;
+        r.w1 = k.w1;
+        r.eff_gid = gid[h];
+        r.gid = gid[v];
+        r.d = depth[h] - depth[v];
+        r.len = len[v];
+        out[i] = r;
+    }
+}
+
+// per spine node: the maximum key over the rank's device descendants (eff
+// after the selection's walk) and whether a locked node lies below
+__global__ void spine_report_kernel(const int* spine, int n_spine, const Key2* keys, const int* eff,
+                                    const int* sublock, const int* depth, const int* gid,
+                                    const std::uint8_t* flags, pbkv_spine_info* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_spine) return;
+    const int s = spine[j];
+    const int e = eff[s];
+    pbkv_spine_info r;
+    r.has_eff = (flags[e] & kFlagExcluded) ? 0 : 1;
+    const Key2 k = load_key(keys, e);
+    r.w0 = r.has_eff ? k.w0 : 0ull;
+    r.w1 = r.has_eff ? k.w1 : 0ull;
+    r.eff_gid = r.has_eff ? gid[e] : -1;
+    r.eff_depth = r.has_eff ? depth[e] : -1;
+    r.sublock = sublock[s] ? 1 : 0;
+    out[j] = r;
+}
+
+// Eq. 2 products (gs * mass_on, scoring.hpp:56-57) of the spine nodes' local
+// entries, node-major, entries in WorkflowId order, K per entry
+__global__ void spine_products_kernel(ScoreArgs s, const int* spine, const long long* base, int n_spine, double* out,
+                                      unsigned int* miss) {
+    const int j = blockIdx.y;
+    if (j >= n_spine) return;
+    const int node = spine[j];
+    const unsigned int e0 = s.acc_off[node], e1 = s.acc_off[node + 1];
+    const long long L = static_cast<long long>(e1 - e0) * s.K;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < L;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const unsigned int e = e0 + static_cast<unsigned int>(t / s.K);
+        const int k = static_cast<int>(t % s.K);
+        const int slot = __ldg(s.acc_slot + e);
+        const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+        double x = 0.0;
+        if (__ldg(s.fstate + slot) != 1) {
+            atomicOr(miss, 1u);
+        } else {
+            const double* row = s.P + (static_cast<std::size_t>(slot) * s.K + k) * s.V1;
+            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k), mass_on(row, b));
+        }
+        out[base[j] + t] = x;
+    }
+}
+
+// merge of sorted runs (disjoint unique keys): element i of run r lands at
+// i + sum over other runs of their count of smaller keys
+__global__ void merge_runs_kernel(const pbkv_cand* src, const long long* run_start, const long long* run_len,
+                                  const long long* out_base, int n_runs, pbkv_cand* dst) {
+    const int r = blockIdx.y;
+    const long long n = run_len[r];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const pbkv_cand x = src[run_start[r] + i];
+        long long pos = i;
+        for (int q = 0; q < n_runs; ++q) {
+            if (q == r) continue;
+            const pbkv_cand* b = src + run_start[q];
+            long long lo = 0, hi = run_len[q];
+            while (lo < hi) {
+                const long long mid = (lo + hi) >> 1;
+                if (cand_less(b[mid], x))
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            pos += lo;
+        }
+        dst[pos] = x;
+        (void)out_base;
+    }
+}
+
+// shortest prefix of the merged order with sum(len) >= needed (all if none)
+__global__ void __launch_bounds__(1024) merge_cut_kernel(const pbkv_cand* m, long long n, long long needed,
+                                                         int* victims, long long* result) {
+    using Scan = cub::BlockScan<long long, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long cut_sh, freed_sh;
+    if (threadIdx.x == 0) {
+        cut_sh = n;
+        freed_sh = 0;
+    }
+    __syncthreads();
+    long long carry = 0;
+    for (long long c0 = 0; c0 < n; c0 += 1024) {
+        const long long i = c0 + threadIdx.x;
+        const long long v = i < n ? static_cast<long long>(m[i].len) : 0;
+        long long incl, agg;
+        Scan(tmp).InclusiveSum(v, incl, agg);
+        incl += carry;
+        const bool hit = i < n && incl >= needed && incl - v < needed;  // first index reaching needed
+        if (hit) {
+            cut_sh = i + 1;
+            freed_sh = incl;
+        }
+        __syncthreads();
+        carry += agg;
+        if (cut_sh != n || carry >= needed) break;
+    }
+    __syncthreads();
+    const long long cut = cut_sh;
+    const long long freed = cut == n && freed_sh == 0 ? carry : freed_sh;
+    for (long long i = threadIdx.x; i < cut; i += 1024) victims[i] = m[i].gid;
+    if (threadIdx.x == 0) {
+        result[0] = cut;
+        result[1] = freed;
+        result[2] = freed < needed ? 1 : 0;
+    }
+}
+
+unsigned int grid_for_cap(long long n, int block) {
+    long long g = (n + block - 1) / block;
+    if (g > 148 * 8) g = 148 * 8;
+    return static_cast<unsigned int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+void shard_apply_flags(Context& c) {
+    if (c.spine.empty()) return;
+    c.spine_dev.reserve(c.spine.size());
+    PBKV_CUDA(cudaMemcpyAsync(c.spine_dev.p, c.spine.data(), c.spine.size() * sizeof(int), cudaMemcpyHostToDevice,
+                              c.stream));
+    const int n = static_cast<int>(c.spine.size());
+    mark_excluded_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.flags.p, c.spine_dev.p, n);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void shard_records(Context& c, long long* result_dev, pbkv_cand* out, long long cap_unused) {
+    (void)cap_unused;
+    records_kernel<<<grid_for_cap(c.n, 256), 256, 0, c.stream>>>(c.vid_out.p, result_dev, c.keys.p, c.eff.p,
+                                                                 c.depth.p, c.len.p, c.gid.p, out);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void shard_spine_report(Context& c, pbkv_spine_info* out) {
+    const int n = static_cast<int>(c.spine.size());
+    if (n == 0) return;
+    spine_report_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.spine_dev.p, n, c.keys.p, c.eff.p, c.sublock.p,
+                                                               c.depth.p, c.gid.p, c.flags.p, out);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+ScoreArgs make_score_args(Context& c, double* out);
+
+void shard_spine_products(Context& c, const long long* base_dev, long long max_len, double* out, unsigned int* miss) {
+    const int n = static_cast<int>(c.spine.size());
+    if (n == 0 || max_len == 0) return;
+    ScoreArgs s = make_score_args(c, nullptr);
+    dim3 grid(grid_for_cap(max_len, 256), static_cast<unsigned int>(n));
+    spine_products_kernel<<<grid, 256, 0, c.stream>>>(s, c.spine_dev.p, base_dev, n, out, miss);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void shard_merge_cut(Context& c, const pbkv_cand* src, const long long* run_start_dev, const long long* run_len_dev,
+                     int n_runs, long long max_run, long long total, pbkv_cand* merged, long long needed,
+                     int* victims, long long* result) {
+    if (total > 0) {
+        dim3 grid(grid_for_cap(max_run, 256), static_cast<unsigned int>(n_runs));
+        merge_runs_kernel<<<grid, 256, 0, c.stream>>>(src, run_start_dev, run_len_dev, nullptr, n_runs, merged);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+    }
+    merge_cut_kernel<<<1, 1024, 0, c.stream>>>(merged, total, needed, victims, result);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+}  // namespace pbkv

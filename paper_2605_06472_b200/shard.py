@@ -1,0 +1,419 @@
+"""Node-set sharding of stages 2-3 across GPUs (BASELINE config 4).
+
+One process per GPU.  Each rank keeps its shard of the radix tree resident
+(the subtrees it owns plus a copy of the spine: the ancestors whose subtrees
+span ranks) in its own pbkv context, and per decision:
+
+  1. runs the local selection (pbkv_shard_select): spine excluded, records of
+     its local cut (shortest local prefix with sum(len) >= needed -- an upper
+     bound on its share of the global prefix) and one report per spine node;
+  2. HE with recomputed scores: the Eq. 2 products of its workflows' entries
+     on the spine nodes (pbkv_shard_spine_products) are all-gathered; ranks
+     own contiguous WorkflowId blocks, so rank order IS the reference's
+     summation order (std::map, cache.hpp:64) and every rank evaluates the
+     spine scores' exact chains (pbkv_chain_sum) bit-identically;
+  3. all-gathers counts, records and spine reports (torch.distributed: NCCL
+     over NVLink on GPUs, gloo in the CPU tests);
+  4. turns the reports into the spine's own records (host, a handful of
+     nodes) and merges every run + the spine run with the global cut on the
+     device (pbkv_merge_cut).
+
+No data-path work is duplicated across ranks except the spine (O(#spine)).
+The result equals the single-GPU selection on the whole tree (and hence the
+reference's greedy frontier, policies.hpp:50-83): tests/test_shard.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import POLICY_HE, POLICY_KVFLOW, POLICY_LAE, POLICY_LRU, SCORE_RECOMPUTE, SoAArrays, ptr
+
+CAND_DTYPE = np.dtype([("w0", "<u8"), ("w1", "<u8"), ("eff_gid", "<i4"), ("gid", "<i4"), ("d", "<i4"),
+                       ("len", "<i4")])
+SPINE_DTYPE = np.dtype([("w0", "<u8"), ("w1", "<u8"), ("eff_gid", "<i4"), ("eff_depth", "<i4"),
+                        ("has_eff", "<i4"), ("sublock", "<i4")])
+
+
+class CandC(C.Structure):
+    _fields_ = [("w0", C.c_uint64), ("w1", C.c_uint64), ("eff_gid", C.c_int32), ("gid", C.c_int32),
+                ("d", C.c_int32), ("len", C.c_int32)]
+
+
+class SpineInfoC(C.Structure):
+    _fields_ = [("w0", C.c_uint64), ("w1", C.c_uint64), ("eff_gid", C.c_int32), ("eff_depth", C.c_int32),
+                ("has_eff", C.c_int32), ("sublock", C.c_int32)]
+
+
+# ---- CandidateKey packing (policies.hpp:40-48; common.cuh make_key) -----------------
+def enc_rank(r: float) -> int:
+    if r == 0.0:
+        r = 0.0  # -0.0 == +0.0 under std::tie
+    b = struct.unpack("<Q", struct.pack("<d", r))[0]
+    return (~b) & 0xFFFFFFFFFFFFFFFF if b >> 63 else b | (1 << 63)
+
+
+def make_key(cls: int, rank: float, last: int) -> tuple[int, int]:
+    e = enc_rank(rank)
+    return (cls << 63) | (e >> 1), ((e & 1) << 63) | int(last)
+
+
+def node_key(policy: int, retired: bool, ever: int, last: int, score: float) -> tuple[int, int]:
+    if policy == POLICY_LRU:
+        return make_key(0, 0.0, last)
+    if policy == POLICY_LAE:
+        return make_key(0, float(ever), last) if retired else make_key(1, 0.0, last)
+    if policy == POLICY_HE:
+        return make_key(0, float(ever), last) if retired else make_key(1, score, last)
+    raise ValueError("kvflow is not supported on a sharded tree")
+
+
+# ---- the spine -----------------------------------------------------------------------
+@dataclass
+class Spine:
+    """Global fields of the spine nodes, identical on every rank; index j order
+    is the order of pbkv_shard_set / the reports."""
+    gid: np.ndarray        # int64
+    parent: np.ndarray     # spine index of the parent, -1 for the root
+    depth: np.ndarray
+    len: np.ndarray
+    tier: np.ndarray
+    retired: np.ndarray
+    ever: np.ndarray
+    last: np.ndarray
+    score: np.ndarray      # cached (CacheTree) score
+
+    @property
+    def n(self) -> int:
+        return int(self.gid.size)
+
+
+def spine_records(sp: Spine, reports: np.ndarray, scores: np.ndarray, policy: int,
+                  locked_gids: set[int]) -> np.ndarray:
+    """Records of the eligible spine nodes from the ranks' reports
+    ([P, n_spine] SPINE_DTYPE).  eff(s) = max over s's own key, its spine
+    children's eff and every rank's maximum below s; eligible iff device, not
+    the root, and no locked node below it on any rank (App. B.2)."""
+    n = sp.n
+    eff: list[tuple] = [None] * n  # (w0, w1, gid, depth)
+    sub = [False] * n
+    order = sorted(range(n), key=lambda j: -int(sp.depth[j]))  # children before parents
+    for j in order:
+        k = node_key(policy, bool(sp.retired[j]), int(sp.ever[j]), int(sp.last[j]), float(scores[j]))
+        best = None
+        if int(sp.tier[j]) == 0:
+            best = (k[0], k[1], int(sp.gid[j]), int(sp.depth[j]))
+        for r in range(reports.shape[0]):
+            rep = reports[r, j]
+            if int(rep["has_eff"]):
+                c = (int(rep["w0"]), int(rep["w1"]), int(rep["eff_gid"]), int(rep["eff_depth"]))
+                best = c if best is None or c[:3] > best[:3] else best
+            sub[j] = sub[j] or bool(int(rep["sublock"]))
+        for c_ in range(n):
+            if int(sp.parent[c_]) == j:
+                if eff[c_] is not None and (best is None or eff[c_][:3] > best[:3]):
+                    best = eff[c_]
+                sub[j] = sub[j] or sub[c_]
+        sub[j] = sub[j] or int(sp.gid[j]) in locked_gids
+        eff[j] = best
+    recs = []
+    for j in range(n):
+        if int(sp.parent[j]) < 0 or int(sp.tier[j]) != 0 or sub[j] or eff[j] is None:
+            continue
+        w0, w1, eg, ed = eff[j]
+        recs.append((w0, w1, eg, int(sp.gid[j]), ed - int(sp.depth[j]), int(sp.len[j])))
+    out = np.array(recs, dtype=CAND_DTYPE) if recs else np.zeros(0, dtype=CAND_DTYPE)
+    return np.sort(out, order=["w0", "w1", "eff_gid", "d"])
+
+
+# ---- partition of a global tree ----------------------------------------------------------
+@dataclass
+class Shard:
+    rank: int
+    soa: SoAArrays              # local tree (local ids, increasing in global id)
+    gids: np.ndarray            # int32 [n_local] global id of each local node
+    spine_local: np.ndarray     # int32 local ids of the spine copies, in Spine order
+    wf_lo: int                  # owned WorkflowId block [wf_lo, wf_hi)
+    wf_hi: int
+    spine: Spine = field(repr=False, default=None)
+
+
+def _depths(parent: np.ndarray) -> np.ndarray:
+    n = parent.size
+    depth = np.full(n, -1, dtype=np.int64)
+    depth[0] = 0
+    for i in range(1, n):
+        stack = []
+        v = i
+        while depth[v] < 0:
+            stack.append(v)
+            v = int(parent[v])
+        d = depth[v]
+        for u in reversed(stack):
+            d += 1
+            depth[u] = d
+    return depth
+
+
+def partition(soa: SoAArrays, n_ranks: int, spine_depth: int = 1) -> list[Shard]:
+    """Splits a global tree into n_ranks shards.  Spine = nodes of depth <=
+    spine_depth; the subtrees below it go to ranks in contiguous global-id
+    blocks of roughly equal size.  Requires that every non-spine node is
+    tagged only by workflows of its rank's WorkflowId block (workflows are
+    co-located with their subtrees; true of the synthetic generator, whose
+    group subtrees hold only that group's workflows)."""
+    n = soa.n_nodes
+    parent = soa.parent.astype(np.int64)
+    depth = _depths(parent)
+    is_spine = depth <= spine_depth
+    # subtree root (at spine_depth + 1) of every non-spine node
+    top = np.arange(n)
+    for _ in range(int(depth.max()) + 1):
+        up = (depth[top] > spine_depth + 1)
+        if not up.any():
+            break
+        top = np.where(up, parent[top], top)
+    roots = np.unique(top[~is_spine])
+    sizes = np.bincount(top[~is_spine], minlength=n)[roots]
+    cum = np.cumsum(sizes)
+    total = int(cum[-1]) if cum.size else 0
+    owner_of_root = np.minimum((cum - 1) * n_ranks // max(total, 1), n_ranks - 1) if total else np.zeros(0, int)
+    owner = np.full(n, -1, dtype=np.int64)
+    root_owner = dict(zip(roots.tolist(), owner_of_root.tolist()))
+    nz = np.nonzero(~is_spine)[0]
+    owner[nz] = [root_owner[int(t)] for t in top[nz]]
+    # WorkflowId blocks per rank
+    lo = [None] * n_ranks
+    hi = [None] * n_ranks
+    for i in nz.tolist():
+        a, b = int(soa.acc_off[i]), int(soa.acc_off[i + 1])
+        if a == b:
+            continue
+        r = int(owner[i])
+        w0, w1 = int(soa.acc_wf[a]), int(soa.acc_wf[b - 1])
+        lo[r] = w0 if lo[r] is None else min(lo[r], w0)
+        hi[r] = w1 + 1 if hi[r] is None else max(hi[r], w1 + 1)
+    # block boundaries: rank r owns WorkflowIds in [bound[r], bound[r+1]) (the
+    # whole id line is covered, so workflows tagged only on spine nodes count too)
+    INF = 1 << 62
+    bound = [-INF] + [0] * (n_ranks - 1) + [INF]
+    prev_hi = -INF
+    for r in range(n_ranks):
+        if r > 0:
+            bound[r] = lo[r] if lo[r] is not None else max(prev_hi, bound[r - 1])
+            if bound[r] < prev_hi:
+                raise ValueError("tree is not shardable by WorkflowId blocks (workflows span ranks)")
+        if hi[r] is not None:
+            prev_hi = max(prev_hi, hi[r])
+    lo = bound[:-1]
+    hi = bound[1:]
+    spine_ids = np.nonzero(is_spine)[0]
+    sp_index = {int(g): j for j, g in enumerate(spine_ids.tolist())}
+    spine = Spine(gid=spine_ids.astype(np.int64),
+                  parent=np.array([sp_index.get(int(parent[g]), -1) for g in spine_ids], dtype=np.int64),
+                  depth=depth[spine_ids], len=soa.len[spine_ids].astype(np.int64),
+                  tier=soa.tier[spine_ids].astype(np.int64), retired=soa.retired[spine_ids].astype(np.int64),
+                  ever=soa.ever_tagged[spine_ids].astype(np.int64), last=soa.last_access[spine_ids].astype(np.uint64),
+                  score=soa.score[spine_ids].astype(np.float64))
+    shards = []
+    for r in range(n_ranks):
+        keep = np.nonzero(is_spine | (owner == r))[0]  # sorted global ids
+        loc = np.full(n, -1, dtype=np.int64)
+        loc[keep] = np.arange(keep.size)
+        m = keep.size
+        # access entries: non-spine nodes keep theirs; spine copies keep only this rank's block
+        offs = [0]
+        wfs, bits = [], []
+        for g in keep.tolist():
+            a, b = int(soa.acc_off[g]), int(soa.acc_off[g + 1])
+            w = soa.acc_wf[a:b]
+            bb = soa.acc_bits[a:b]
+            if is_spine[g]:
+                sel = (w >= lo[r]) & (w < hi[r])
+                w, bb = w[sel], bb[sel]
+            elif b > a and (int(w[0]) < lo[r] or int(w[-1]) >= hi[r]):
+                raise ValueError("non-spine node tagged by another rank's workflow")
+            wfs.append(w)
+            bits.append(bb)
+            offs.append(offs[-1] + w.size)
+        E = offs[-1]
+        loc_soa = SoAArrays(m, E, dict(soa.scalars))
+        for f in SoAArrays.FIELDS:
+            setattr(loc_soa, f, getattr(soa, f)[keep].copy())
+        loc_soa.parent = np.where(keep == 0, -1, loc[parent[keep]]).astype(np.int32)
+        loc_soa.depth = depth[keep].astype(np.int32)
+        loc_soa.acc_off = np.array(offs, dtype=np.int64)
+        loc_soa.acc_wf = np.concatenate(wfs).astype(np.int64) if E else np.zeros(1, np.int64)
+        loc_soa.acc_bits = np.concatenate(bits).astype(np.uint64) if E else np.zeros(1, np.uint64)
+        shards.append(Shard(r, loc_soa, keep.astype(np.int32), loc[spine_ids].astype(np.int32), int(lo[r]),
+                            int(hi[r]), spine))
+    return shards
+
+
+# ---- collectives -----------------------------------------------------------------------
+def allgather_var(dist, t, world: int):
+    """all_gather of a 1-D tensor whose length differs per rank: returns the
+    padded [world, max_len] gather and the per-rank lengths."""
+    import torch
+
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n)
+    lens = [int(x.item()) for x in ns]
+    mx = max(lens) if lens else 0
+    pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
+    if t.numel():
+        pad[: t.numel()] = t
+    out = torch.zeros(world * mx, dtype=t.dtype, device=t.device)
+    if mx:
+        dist.all_gather_into_tensor(out, pad) if hasattr(dist, "all_gather_into_tensor") and t.is_cuda \
+            else dist.all_gather(list(out.view(world, mx).unbind(0)), pad)
+    return out.view(world, mx), lens
+
+
+# ---- per-rank driver ------------------------------------------------------------------------
+class ShardedPolicy:
+    """A rank's view of a sharded tree: its pbkv context plus the collective
+    exchange.  `dist` is torch.distributed (initialised by the caller) or None
+    for a single process driving every shard itself (tests: logical shards on
+    one GPU, exchange = concatenation)."""
+
+    def __init__(self, shard: Shard, num_agents: int, k: int, gamma: float, device: int = 0):
+        import torch
+
+        from .api import Policy
+
+        self.shard = shard
+        self.pol = Policy(num_agents=num_agents, k=k, gamma=gamma, device=device)
+        self.pol.mirror(shard.soa)
+        g = np.ascontiguousarray(shard.gids, dtype=np.int32)
+        sl = np.ascontiguousarray(shard.spine_local, dtype=np.int32)
+        self.pol._c(_abi.lib().pbkv_shard_set(self.pol.handle, ptr(g, C.c_int32), ptr(sl if sl.size else None,
+                                                                                     C.c_int32), int(sl.size)))
+        self.dev = torch.device("cuda", device)
+        n = shard.soa.n_nodes
+        self.cand = torch.zeros(n * CAND_DTYPE.itemsize, dtype=torch.uint8, device=self.dev)
+        self.spine_out = torch.zeros(max(1, shard.spine.n) * SPINE_DTYPE.itemsize, dtype=torch.uint8,
+                                     device=self.dev)
+        self.result = torch.zeros(3, dtype=torch.int64, device=self.dev)
+        self.gid_of = {int(l): int(gg) for l, gg in enumerate(shard.gids.tolist())} if n < 200000 else None
+
+    # -- step 1: local selection -----------------------------------------------------------
+    def local_select(self, policy: int, score_mode: int, needed: int, locked_local_dev, n_locked: int):
+        L = _abi.lib()
+        rc = L.pbkv_shard_select(self.pol.handle, int(policy), int(score_mode), int(needed),
+                                 C.cast(C.c_void_p(locked_local_dev or None), C.POINTER(C.c_int32)), int(n_locked),
+                                 C.cast(C.c_void_p(self.cand.data_ptr()), C.POINTER(CandC)),
+                                 int(self.shard.soa.n_nodes),
+                                 C.cast(C.c_void_p(self.spine_out.data_ptr()), C.POINTER(SpineInfoC)),
+                                 C.cast(C.c_void_p(self.result.data_ptr()), C.POINTER(C.c_int64)))
+        self.pol._c(rc)
+        n_cand = int(self.result[0].item())
+        return self.cand[: n_cand * CAND_DTYPE.itemsize], self.spine_out[: self.shard.spine.n * SPINE_DTYPE.itemsize]
+
+    # -- step 2: spine products (HE recompute) ------------------------------------------------
+    def spine_products(self):
+        import torch
+
+        ns = self.shard.spine.n
+        counts = np.zeros(max(ns, 1), dtype=np.int64)
+        total = int(sum(int(self.shard.soa.acc_off[s + 1] - self.shard.soa.acc_off[s])
+                        for s in self.shard.spine_local.tolist())) * self.pol.k
+        out = torch.zeros(max(total, 1), dtype=torch.float64, device=self.dev)
+        self.pol._c(_abi.lib().pbkv_shard_spine_products(self.pol.handle, C.cast(C.c_void_p(out.data_ptr()),
+                                                                                 C.POINTER(C.c_double)),
+                                                         ptr(counts, C.c_int64)))
+        return out[:total], counts[:ns]
+
+    def chain_sums(self, x_dev, offsets: np.ndarray) -> np.ndarray:
+        out = np.zeros(max(offsets.size - 1, 1), dtype=np.float64)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        self.pol._c(_abi.lib().pbkv_chain_sum(self.pol.handle, C.cast(C.c_void_p(x_dev.data_ptr()),
+                                                                      C.POINTER(C.c_double)),
+                                              ptr(off, C.c_int64), int(off.size - 1), ptr(out, C.c_double)))
+        return out[: offsets.size - 1]
+
+    def merge_cut(self, runs_dev, starts: list[int], lens: list[int], needed: int):
+        import torch
+
+        victims = torch.zeros(max(1, sum(lens)), dtype=torch.int32, device=self.dev)
+        res = torch.zeros(3, dtype=torch.int64, device=self.dev)
+        st = np.array(starts, dtype=np.int64)
+        ln = np.array(lens, dtype=np.int64)
+        self.pol._c(_abi.lib().pbkv_merge_cut(self.pol.handle,
+                                              C.cast(C.c_void_p(runs_dev.data_ptr()), C.POINTER(CandC)),
+                                              ptr(st, C.c_int64), ptr(ln, C.c_int64), int(st.size), int(needed),
+                                              C.cast(C.c_void_p(victims.data_ptr()), C.POINTER(C.c_int32)),
+                                              C.cast(C.c_void_p(res.data_ptr()), C.POINTER(C.c_int64))))
+        nv, freed, sf = (int(x) for x in res.tolist())
+        return victims[:nv], freed, bool(sf)
+
+
+def global_select(ranks: list[ShardedPolicy] | ShardedPolicy, policy: int, score_mode: int, needed: int,
+                  locked_gids, dist=None, world: int = 1):
+    """One sharded eviction decision.  With dist=None, `ranks` is the list of
+    every shard's ShardedPolicy in one process (logical shards); otherwise it
+    is this rank's ShardedPolicy and the exchange goes through `dist`."""
+    import torch
+
+    if policy == POLICY_KVFLOW:
+        raise ValueError("kvflow is not supported on a sharded tree")
+    local = ranks if isinstance(ranks, list) else [ranks]
+    sp = local[0].shard.spine
+    locked_set = set(int(x) for x in locked_gids)
+    cands, reps, prods, pcounts = [], [], [], []
+    for rp in local:
+        g2l = {int(g): i for i, g in enumerate(rp.shard.gids.tolist())}
+        loc = np.array([g2l[g] for g in locked_set if g in g2l], dtype=np.int32)
+        ld = torch.from_numpy(loc if loc.size else np.zeros(1, np.int32)).to(rp.dev)
+        c, r = rp.local_select(policy, score_mode, needed, ld.data_ptr(), loc.size)
+        cands.append(c)
+        reps.append(r)
+        if policy == POLICY_HE and score_mode == SCORE_RECOMPUTE and sp.n:
+            x, cnt = rp.spine_products()
+            prods.append(x)
+            pcounts.append(cnt)
+    me = local[0]
+    if dist is None:
+        runs = cands
+        rep_all = np.stack([np.frombuffer(r.cpu().numpy().tobytes(), dtype=SPINE_DTYPE) for r in reps]) \
+            if sp.n else np.zeros((len(reps), 0), SPINE_DTYPE)
+        prod_runs = prods
+        cnt_all = pcounts
+    else:
+        g, lens = allgather_var(dist, cands[0], world)
+        runs = [g[r, : lens[r]] for r in range(world)]
+        rg, _ = allgather_var(dist, reps[0], world)
+        rep_all = np.stack([np.frombuffer(rg[r].cpu().numpy().tobytes(), dtype=SPINE_DTYPE)[: sp.n]
+                            for r in range(world)]) if sp.n else np.zeros((world, 0), SPINE_DTYPE)
+        prod_runs, cnt_all = [], []
+        if prods:
+            pg, plens = allgather_var(dist, prods[0], world)
+            cg, _ = allgather_var(dist, torch.from_numpy(pcounts[0]).to(me.dev), world)
+            prod_runs = [pg[r, : plens[r]] for r in range(world)]
+            cnt_all = [cg[r].cpu().numpy()[: sp.n] for r in range(world)]
+    # spine scores: exact chains over all ranks' products in rank (= WorkflowId) order
+    if prod_runs:
+        pieces, offs = [], [0]
+        for j in range(sp.n):
+            for r in range(len(prod_runs)):
+                base = int(np.sum(cnt_all[r][:j]))
+                pieces.append(prod_runs[r][base: base + int(cnt_all[r][j])])
+            offs.append(offs[-1] + sum(int(cnt_all[r][j]) for r in range(len(prod_runs))))
+        x = torch.cat(pieces) if pieces else torch.zeros(1, dtype=torch.float64, device=me.dev)
+        scores = me.chain_sums(x, np.array(offs, dtype=np.int64))
+    else:
+        scores = sp.score
+    srec = spine_records(sp, rep_all, scores, policy, locked_set)
+    allruns = [r for r in runs] + [torch.from_numpy(srec.view(np.uint8).copy()).to(me.dev)]
+    lens = [int(r.numel() // CAND_DTYPE.itemsize) for r in allruns]
+    starts = list(np.cumsum([0] + lens[:-1]))
+    buf = torch.cat([r.reshape(-1) for r in allruns]) if sum(lens) else torch.zeros(CAND_DTYPE.itemsize,
+                                                                                     dtype=torch.uint8,
+                                                                                     device=me.dev)
+    v, freed, sf = me.merge_cut(buf, [int(s) for s in starts], lens, needed)
+    return v.cpu().numpy().tolist(), freed, sf
