@@ -190,9 +190,115 @@ def run_reference(args, rank, world):
     print(json.dumps(line))
 
 
+def shard_workload(cfg: str, rank: int, world: int, dist, torch, dev):
+    """Weak scaling: rank r holds a C3-shaped shard (synthetic seed 12345 + r)
+    of one global tree whose spine (root + the shared-prefix node) is common
+    to all ranks; global node ids 2 + r*stride + local id, WorkflowIds
+    r*W + local (contiguous blocks per rank).  At 8 ranks: 8 M nodes (config 4)."""
+    import workloads as WL
+    from paper_2605_06472_b200 import shard as SH
+    from paper_2605_06472_b200.api import HostTree
+
+    n_nodes, n_wf, K = CONFIGS[cfg]
+    t = HostTree()
+    t.synth(n_nodes=n_nodes, n_workflows=n_wf, agents=AGENTS, seed=12345 + rank)
+    soa = t.export()
+    depth = SH._depths(soa.parent.astype(np.int64))
+    sp_local = np.nonzero(depth <= 1)[0].astype(np.int32)
+    assert sp_local.tolist() == [0, 1], "synthetic tree: spine must be the root and the shared prefix"
+    stride = 1 << 24
+    gids = (2 + rank * stride + np.arange(soa.n_nodes)).astype(np.int64)
+    gids[0], gids[1] = 0, 1
+    soa.acc_wf[: soa.n_entries] += rank * n_wf
+    # global spine fields (len/tier equal on all ranks; ever summed, last max, retired all)
+    loc = torch.tensor([int(soa.ever_tagged[1]), int(soa.last_access[1]), int(not soa.retired[1])],
+                       dtype=torch.int64, device=dev)
+    ever = loc[0:1].clone(); dist.all_reduce(ever)
+    last = loc[1:2].clone(); dist.all_reduce(last, op=dist.ReduceOp.MAX)
+    alive = loc[2:3].clone(); dist.all_reduce(alive, op=dist.ReduceOp.MAX)
+    spine = SH.Spine(gid=np.array([0, 1]), parent=np.array([-1, 0]), depth=np.array([0, 1]),
+                     len=soa.len[[0, 1]].astype(np.int64), tier=soa.tier[[0, 1]].astype(np.int64),
+                     retired=np.array([0, 0 if int(alive.item()) else 1]), ever=np.array([0, int(ever.item())]),
+                     last=np.array([0, int(last.item())], dtype=np.uint64), score=np.zeros(2))
+    shard = SH.Shard(rank, soa, gids.astype(np.int32), sp_local, rank * n_wf, (rank + 1) * n_wf, spine)
+    rng = np.random.default_rng(12345 + rank)
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, K, AGENTS + 1)
+    locked = gids[np.array(WL.pinned_paths(soa, rng, 0.01), dtype=np.int64)]
+    return shard, wf, P, locked, K
+
+
+def run_sharded(args, rank, world, local, dist, torch):
+    """config 4: one eviction decision over the sharded tree per step (local
+    score + select, spine products all-gather, exact spine chains, record
+    all-gather, merge + cut); max over ranks of the device-event time."""
+    from paper_2605_06472_b200 import shard as SH
+    from paper_2605_06472_b200._abi import POLICY_HE, SCORE_RECOMPUTE
+
+    dev = torch.device("cuda", local)
+    shard, wf, P, locked, K = shard_workload(args.config, rank, world, dist, torch, dev)
+    sp = SH.ShardedPolicy(shard, num_agents=AGENTS, k=K, gamma=GAMMA, device=local)
+    sp.pol.put_forecasts(wf, P)
+    soa = shard.soa
+    used_t = torch.tensor([int(soa.len[soa.tier == 0][1:].sum())], dtype=torch.int64, device=dev)
+    dist.all_reduce(used_t)
+    needed = max(1, int(args.needed_frac * int(used_t.item())))
+    lk = [int(x) for x in locked.tolist()]
+
+    def step():
+        return SH.global_select(sp, POLICY_HE, SCORE_RECOMPUTE, needed, lk, dist=dist, world=world)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    k0, _ = sp.pol.launches()
+    times = []
+    dist.barrier()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = step()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    dist.barrier()
+    k1, _ = sp.pol.launches()
+    tt = torch.tensor([statistics.mean(times), float(np.percentile(times, 99))], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    nn = torch.tensor([soa.n_nodes - (2 if rank else 0)], dtype=torch.int64, device=dev)
+    dist.all_reduce(nn)
+    ms, p99 = tt.tolist()
+    total_nodes = int(nn.item())
+    if rank == 0:
+        n_nodes, n_wf, _ = CONFIGS[args.config]
+        line = {
+            "metric": METRIC, "value": total_nodes / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 4 shape, weak scaling: {world} x ({n_nodes} nodes x {n_wf} workflows) "
+                                   f"x K={K} sharded by subtree, HE select at {args.needed_frac:.2%} of global need",
+                       "n_nodes": total_nodes, "needed_tokens": needed, "n_victims": len(res[0]),
+                       "l2": "flushed between steps (256 MiB write)", "parallelism": f"node-set shards x{world}"},
+            "p99_decision_ms": p99, "gpu_launches": int(k1 - k0), "clocks": clk.result,
+            "cpu_baseline": None,
+            "e2e": None,
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if "PBKV_FORCE_DEVICE" in os.environ:  # testing: several ranks sharing one GPU (with PBKV_DIST_BACKEND=gloo)
+        local = int(os.environ["PBKV_FORCE_DEVICE"])
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -206,7 +312,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PBKV_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (testing)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    if world > 1:
+        run_sharded(args, rank, world, local, dist, torch)
+        return
 
     n_nodes, n_wf, K = CONFIGS[args.config]
     t, soa, wf, P, locked, K, build_s = workload(args.config, rank)

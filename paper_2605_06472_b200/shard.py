@@ -260,7 +260,8 @@ def allgather_var(dist, t, world: int):
     padded [world, max_len] gather and the per-rank lengths."""
     import torch
 
-    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    dev = t.device if dist.get_backend() == "nccl" else torch.device("cpu")
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=dev)
     ns = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(ns, n)
     lens = [int(x.item()) for x in ns]
@@ -270,8 +271,12 @@ def allgather_var(dist, t, world: int):
         pad[: t.numel()] = t
     out = torch.zeros(world * mx, dtype=t.dtype, device=t.device)
     if mx:
-        dist.all_gather_into_tensor(out, pad) if hasattr(dist, "all_gather_into_tensor") and t.is_cuda \
-            else dist.all_gather(list(out.view(world, mx).unbind(0)), pad)
+        if t.is_cuda and dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(out, pad)
+        else:  # gloo: host staging
+            host = [torch.zeros(mx, dtype=t.dtype) for _ in range(world)]
+            dist.all_gather(host, pad.cpu())
+            out.copy_(torch.cat(host))
     return out.view(world, mx), lens
 
 
