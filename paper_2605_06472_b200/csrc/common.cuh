@@ -20,10 +20,13 @@ __device__ __forceinline__ void set_error(DevStatus* st, int code, int kind, lon
 }
 
 // Forecast::mass_on (forecast.hpp:64-69): sum over set agent bits in
-// ascending agent order.  Loads are issued in batches of 8 so their latency
-// overlaps; the additions stay in the reference order.  Adding a masked-out
-// slot is skipped (not "+0.0"), so the result is the exact reference chain.
-__device__ __forceinline__ double mass_on(const double* __restrict__ row, unsigned long long bits) {
+// ascending agent order.  The resident forecast table is agent-major,
+// P[slot][agent][k] (the K steps of one agent are one 64-byte line at K = 8),
+// so step k of agent a is base[a * stride] with base = &P[slot][0][k] and
+// stride = K.  Loads are issued in batches of 8 so their latency overlaps;
+// the additions stay in the reference order.  A masked-out agent is skipped
+// (not "+0.0"), so the result is the exact reference chain.
+__device__ __forceinline__ double mass_on(const double* __restrict__ base, int stride, unsigned long long bits) {
     double m = 0.0;
     while (bits) {
         double v[8];
@@ -32,7 +35,7 @@ __device__ __forceinline__ double mass_on(const double* __restrict__ row, unsign
         for (int j = 0; j < 8; ++j) {
             if (bits) {
                 int a = __ffsll(static_cast<long long>(bits)) - 1;
-                v[j] = __ldg(row + a);
+                v[j] = __ldg(base + static_cast<std::size_t>(a) * stride);
                 bits &= bits - 1;
                 cnt = j + 1;
             }
@@ -42,34 +45,6 @@ __device__ __forceinline__ double mass_on(const double* __restrict__ row, unsign
             if (j < cnt) m = __dadd_rn(m, v[j]);
     }
     return m;
-}
-
-// two rows (steps k and k+1) with the same agent bits: both batches of loads
-// are in flight before either addition chain starts
-__device__ __forceinline__ void mass_on2(const double* __restrict__ r0, const double* __restrict__ r1,
-                                         unsigned long long bits, double& m0, double& m1) {
-    m0 = 0.0;
-    m1 = 0.0;
-    while (bits) {
-        double v0[8], v1[8];
-        int cnt = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (bits) {
-                int a = __ffsll(static_cast<long long>(bits)) - 1;
-                v0[j] = __ldg(r0 + a);
-                v1[j] = __ldg(r1 + a);
-                bits &= bits - 1;
-                cnt = j + 1;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (j < cnt) {
-                m0 = __dadd_rn(m0, v0[j]);
-                m1 = __dadd_rn(m1, v1[j]);
-            }
-    }
 }
 
 // order-preserving double -> uint64 (policies.hpp:46 compares ranks with <)

@@ -6,7 +6,8 @@
 //   depth i32, acc_off u32 (CSR, n+1)
 // Per access entry (CSR, WorkflowId-ascending within a node, cache.hpp:64):
 //   slot i32 (forecast slot of the WorkflowId), bits u64
-// Per forecast slot: P f64[K][V1] (first K steps), gs f64[K] = gamma^k * s(k),
+// Per forecast slot: P f64[V1][K] (agent-major: one agent's K steps contiguous),
+//   gs f64[K] = gamma^k * s(k),
 //   state u8 (0 missing, 1 ok, 2 horizon < K).
 #pragma once
 

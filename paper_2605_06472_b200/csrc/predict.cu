@@ -470,8 +470,9 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a) {
     const int KK = a.K < a.Kp ? a.K : a.Kp;
     for (int idx = threadIdx.x; idx < nw * a.K * a.V1; idx += kHeadThreads) {
         const int i = idx / (a.K * a.V1), r = idx % (a.K * a.V1);
-        const int k = r / a.V1;
-        a.P[static_cast<std::size_t>(a.slots[w0 + i]) * a.K * a.V1 + r] = k < KK ? pp[i * KV + r] : 0.0;
+        const int k = r / a.V1, v = r % a.V1;  // agent-major store: P[slot][v][k]
+        a.P[static_cast<std::size_t>(a.slots[w0 + i]) * a.K * a.V1 + static_cast<std::size_t>(v) * a.K + k] =
+            k < KK ? pp[i * KV + r] : 0.0;
     }
     if (a.probs_out)
         for (int idx = threadIdx.x; idx < nw * KV; idx += kHeadThreads)

@@ -34,7 +34,7 @@ __device__ __forceinline__ double eq1(const ScoreArgs& s, unsigned int e0, unsig
             *miss = true;
             continue;
         }
-        v = __dadd_rn(v, mass_on(s.P + static_cast<std::size_t>(slot) * s.K * s.V1, b));
+        v = __dadd_rn(v, mass_on(s.P + static_cast<std::size_t>(slot) * s.V1 * s.K, s.K, b));
     }
     return v;
 }

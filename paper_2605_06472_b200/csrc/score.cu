@@ -21,29 +21,61 @@ constexpr int kLightThreads = 256;
 constexpr int kMediumWarps = 8;
 constexpr int kMediumMaxElems = 256;
 constexpr int kChainThreads = 256;
+
+unsigned int grid_cap(std::int64_t n, int block) {
+    std::int64_t want = (n + block - 1) / block;
+    const std::int64_t cap = 148LL * 16;
+    if (want > cap) want = cap;
+    return static_cast<unsigned int>(want < 1 ? 1 : want);
+}
 constexpr int kChainEPT = 8;  // elements per thread per chunk
 constexpr int kChainChunk = kChainThreads * kChainEPT;
 
 // Eq. 2 of one access entry appended to `total` (scoring.hpp:56-59)
 __device__ __forceinline__ void eq2_entry(const ScoreArgs& s, int slot, unsigned long long b, double& total) {
-    const int K = s.K, V1 = s.V1;
-    const double* pw = s.P + static_cast<std::size_t>(slot) * K * V1;
+    const int K = s.K;
+    const double* pw = s.P + static_cast<std::size_t>(slot) * s.V1 * K;
     const double* g = s.gs + static_cast<std::size_t>(slot) * K;
-    int k = 0;
-    for (; k + 1 < K; k += 2) {
-        double m0, m1;
-        mass_on2(pw + k * V1, pw + (k + 1) * V1, b, m0, m1);
-        const double g0 = __ldg(g + k), g1 = __ldg(g + k + 1);
-        total = __dadd_rn(total, __dmul_rn(g0, m0));
-        total = __dadd_rn(total, __dmul_rn(g1, m1));
+    for (int k = 0; k < K; ++k) total = __dadd_rn(total, __dmul_rn(__ldg(g + k), mass_on(pw + k, K, b)));
+}
+
+// Eq. 2 of one access entry with the horizon known at compile time: the K
+// step masses are accumulated agent by agent (ascending, forecast.hpp:66-67)
+// in K independent registers, so the K row loads of each agent are in flight
+// together; then total += gs[k] * m[k] in step order (scoring.hpp:56-57).
+template <int kK>
+__device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsigned long long b, double& total) {
+    const double* pw = s.P + static_cast<std::size_t>(slot) * s.V1 * kK;  // [agent][k]
+    const double* g = s.gs + static_cast<std::size_t>(slot) * kK;
+    double m[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) m[k] = 0.0;
+    while (b) {
+        const int a = __ffsll(static_cast<long long>(b)) - 1;
+        b &= b - 1;
+        const double* row = pw + static_cast<std::size_t>(a) * kK;  // the K steps of agent a, contiguous
+        if constexpr (kK % 2 == 0) {
+#pragma unroll
+            for (int k = 0; k < kK; k += 2) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(row + k));
+                m[k] = __dadd_rn(m[k], v.x);
+                m[k + 1] = __dadd_rn(m[k + 1], v.y);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kK; ++k) m[k] = __dadd_rn(m[k], __ldg(row + k));
+        }
     }
-    if (k < K) total = __dadd_rn(total, __dmul_rn(__ldg(g + k), mass_on(pw + k * V1, b)));
+#pragma unroll
+    for (int k = 0; k < kK; ++k) total = __dadd_rn(total, __dmul_rn(__ldg(g + k), m[k]));
 }
 
 // ---------------------------------------------------------------------------
-template <bool kKeys>
-__global__ void __launch_bounds__(kLightThreads) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
-                                                                    int report_missing) {
+// Light nodes (<= 2 entries): one thread per node, Eq. 2 and the stage-3 key
+// in registers.  kK > 0: horizon specialised; kK == 0: any horizon.
+template <bool kKeys, int kK>
+__global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
+                                                                       int report_missing) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int n = static_cast<int>(i);
@@ -60,7 +92,10 @@ __global__ void __launch_bounds__(kLightThreads) score_light_kernel(ScoreArgs s,
                     (fs == 2 ? shorth : miss) = true;
                     continue;
                 }
-                eq2_entry(s, slot, b, total);
+                if constexpr (kK > 0)
+                    eq2_entry_k<kK>(s, slot, b, total);
+                else
+                    eq2_entry(s, slot, b, total);
             }
             s.out[n] = total;
             if (report_missing && (miss || shorth))
@@ -74,6 +109,19 @@ __global__ void __launch_bounds__(kLightThreads) score_light_kernel(ScoreArgs s,
                 if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, total);
             }
         }
+    }
+}
+
+template <bool kKeys>
+void launch_light(Context& c, const ScoreArgs& s, const KeyArgs& ka, int rm) {
+    const unsigned int g = grid_cap(c.n, kLightThreads);
+    switch (c.K) {
+        case 1: score_light_kernel<kKeys, 1><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;
+        case 2: score_light_kernel<kKeys, 2><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;
+        case 3: score_light_kernel<kKeys, 3><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;
+        case 4: score_light_kernel<kKeys, 4><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;
+        case 8: score_light_kernel<kKeys, 8><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;
+        default: score_light_kernel<kKeys, 0><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm);
     }
 }
 
@@ -102,9 +150,9 @@ __global__ void __launch_bounds__(kMediumWarps * 32) score_medium_kernel(ScoreAr
         if (kValueOnly ? fs == 0 : fs != 1) {
             miss |= (fs == 2 && !kValueOnly) ? 2 : 1;
         } else {
-            const double* row = s.P + (static_cast<std::size_t>(slot) * s.K + k) * s.V1;
-            x = kValueOnly ? mass_on(row, b) : __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k),
-                                                         mass_on(row, b));
+            const double* col = s.P + static_cast<std::size_t>(slot) * s.V1 * s.K + k;
+            x = kValueOnly ? mass_on(col, s.K, b)
+                           : __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k), mass_on(col, s.K, b));
         }
         xs[warp][i] = x;
     }
@@ -141,8 +189,8 @@ __global__ void __launch_bounds__(256) heavy_products_kernel(ScoreArgs s, const 
         if (fs != 1) {
             atomicOr(&hmiss[hent_node[j]], fs == 2 ? 2u : 1u);
         } else {
-            const double* row = s.P + (static_cast<std::size_t>(slot) * K + k) * s.V1;
-            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * K + k), mass_on(row, b));
+            const double* col = s.P + static_cast<std::size_t>(slot) * s.V1 * K + k;
+            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * K + k), mass_on(col, K, b));
         }
         xs[t] = x;
     }
@@ -207,10 +255,10 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ScoreArgs s, KeyAr
                 if (kValueOnly ? fs == 0 : fs != 1) {
                     atomicOr(&miss_sh, (fs == 2 && !kValueOnly) ? 2 : 1);
                 } else {
-                    const double* row = s.P + (static_cast<std::size_t>(slot) * s.K + k) * s.V1;
-                    x = kValueOnly ? mass_on(row, b)
+                    const double* col = s.P + static_cast<std::size_t>(slot) * s.V1 * s.K + k;
+                    x = kValueOnly ? mass_on(col, s.K, b)
                                    : __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k),
-                                               mass_on(row, b));
+                                               mass_on(col, s.K, b));
                 }
                 xs[i] = x;
             }
@@ -358,7 +406,7 @@ __global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* 
                     miss = true;
                     continue;
                 }
-                v = __dadd_rn(v, mass_on(s.P + static_cast<std::size_t>(slot) * s.K * s.V1, b));
+                v = __dadd_rn(v, mass_on(s.P + static_cast<std::size_t>(slot) * s.V1 * s.K, s.K, b));
             } else {
                 if (fs != 1) {
                     (fs == 2 ? shorth : miss) = true;
@@ -406,12 +454,12 @@ __global__ void forecast_prepare_kernel(const double* stage, const long long* sl
         double surv = 1.0, gk = 1.0;
         for (int k = 0; k < K; ++k) {
             if (k < H) {
-                for (int a = 0; a < V1; ++a) dst[k * V1 + a] = p[k * V1 + a];
+                for (int a = 0; a < V1; ++a) dst[a * K + k] = p[k * V1 + a];  // agent-major [a][k]
                 g[k] = __dmul_rn(gk, surv);
                 surv = __dmul_rn(surv, __dsub_rn(1.0, p[k * V1 + V1 - 1]));
                 if (surv < 0.0) surv = 0.0;
             } else {
-                for (int a = 0; a < V1; ++a) dst[k * V1 + a] = 0.0;
+                for (int a = 0; a < V1; ++a) dst[a * K + k] = 0.0;
                 g[k] = 0.0;
             }
             gk = __dmul_rn(gk, gamma);
@@ -438,12 +486,6 @@ std::size_t chain_smem_bytes() {
     return b;
 }
 
-unsigned int grid_cap(std::int64_t n, int block) {
-    std::int64_t want = (n + block - 1) / block;
-    const std::int64_t cap = 148LL * 16;
-    if (want > cap) want = cap;
-    return static_cast<unsigned int>(want < 1 ? 1 : want);
-}
 
 }  // namespace
 
@@ -523,9 +565,9 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
         PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
     }
     if (write_keys)
-        score_light_kernel<true><<<grid_cap(c.n, kLightThreads), kLightThreads, 0, c.stream>>>(s, ka, c.n, rm);
+        launch_light<true>(c, s, ka, rm);
     else
-        score_light_kernel<false><<<grid_cap(c.n, kLightThreads), kLightThreads, 0, c.stream>>>(s, ka, c.n, rm);
+        launch_light<false>(c, s, ka, rm);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
     if (c.n_medium > 0) {

@@ -230,10 +230,8 @@ struct SelArgs {
     int* sorted;
     unsigned long long* start;
     int* victims;
-    unsigned long long* hist_w;       // [kBins] reduced weights
-    unsigned int* hist_c;             // [kBins] reduced counts
-    unsigned long long* part_w;       // [grid][kBins] per-CTA partials
-    unsigned int* part_c;             // [grid][kBins]
+    unsigned long long* hist_w;       // [kMaxPasses][kBins] weights (global atomics)
+    unsigned int* hist_c;             // [kMaxPasses][kBins] counts
     unsigned int* seg_off;            // [kMaxPasses][kBins] bucket start in S
     unsigned int* seg_cnt;            // [kMaxPasses][kBins] bucket size
     unsigned int* cursor;             // [kMaxPasses][kBins] placement cursors
@@ -262,7 +260,11 @@ __device__ __forceinline__ void phase_lock(const SelArgs& a, std::int64_t tid, s
             v = a.parent[v];
         }
     }
-    for (std::int64_t j = tid; j < static_cast<std::int64_t>(kMaxPasses) * kBins; j += nthr) a.cursor[j] = 0;
+    for (std::int64_t j = tid; j < static_cast<std::int64_t>(kMaxPasses) * kBins; j += nthr) {
+        a.cursor[j] = 0;
+        a.hist_w[j] = 0;
+        a.hist_c[j] = 0;
+    }
 }
 
 // eff: every device node walks its key up the ancestor chain, CAS-ing the
@@ -276,7 +278,9 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         const Key2 km = load_key(a.keys, n);
         int p = a.parent[n];
         while (p > 0) {
-            int cur = atomicAdd(&a.eff[p], 0);
+            // plain (L2) read first: an atomic read of the hot top-of-tree words
+            // serialises every walker in one L2 slice; CAS only when we would win
+            int cur = __ldcg(&a.eff[p]);
             bool advanced = false;
             for (;;) {
                 const Key2 kc = load_key(a.keys, cur);
@@ -343,7 +347,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
 }
 
 // per-CTA weight and count histograms of the next digit over the candidates
-__device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsigned long long n_L, int lo,
+__device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsigned long long n_L, int lo, int pass,
                                            unsigned long long* hw, unsigned int* hc) {
     for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
         hw[b] = 0;
@@ -372,32 +376,15 @@ __device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsig
         }
     }
     __syncthreads();
-    unsigned long long* pw = a.part_w + static_cast<std::size_t>(blockIdx.x) * kBins;
-    unsigned int* pc = a.part_c + static_cast<std::size_t>(blockIdx.x) * kBins;
+    // per-pass global histogram (zeroed at kernel start): one atomic per
+    // non-empty bin per CTA, no partial arrays and no reduction phase
+    unsigned long long* gw = a.hist_w + static_cast<std::size_t>(pass) * kBins;
+    unsigned int* gc = a.hist_c + static_cast<std::size_t>(pass) * kBins;
     for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
-        pw[b] = hw[b];
-        pc[b] = hc[b];
-    }
-}
-
-// bins spread over all CTAs: hist[b] = sum over CTAs of the partials
-__device__ __forceinline__ void phase_hist_reduce(const SelArgs& a) {
-    const int nparts = gridDim.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (int b = blockIdx.x * nwarps + warp; b < kBins; b += gridDim.x * nwarps) {
-        unsigned long long s = 0;
-        unsigned int cnt = 0;
-        for (int p = lane; p < nparts; p += 32) {
-            s += __ldcg(&a.part_w[static_cast<std::size_t>(p) * kBins + b]);
-            cnt += __ldcg(&a.part_c[static_cast<std::size_t>(p) * kBins + b]);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            s += __shfl_xor_sync(0xffffffffu, s, o);
-            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        }
-        if (lane == 0) {
-            a.hist_w[b] = s;
-            a.hist_c[b] = cnt;
+        const unsigned int c = hc[b];
+        if (c) {
+            atomicAdd(&gw[b], hw[b]);
+            atomicAdd(&gc[b], c);
         }
     }
 }
@@ -421,8 +408,8 @@ __device__ __forceinline__ PickOut phase_pick(const SelArgs& a, unsigned long lo
     unsigned int vc[kPer];
     unsigned long long sc = 0;
     for (int j = 0; j < kPer; ++j) {
-        vw[j] = __ldcg(&a.hist_w[threadIdx.x * kPer + j]);
-        vc[j] = __ldcg(&a.hist_c[threadIdx.x * kPer + j]);
+        vw[j] = __ldcg(&a.hist_w[static_cast<std::size_t>(pass) * kBins + threadIdx.x * kPer + j]);
+        vc[j] = __ldcg(&a.hist_c[static_cast<std::size_t>(pass) * kBins + threadIdx.x * kPer + j]);
         sw += vw[j];
         sc += vc[j];
     }
@@ -516,21 +503,34 @@ __device__ __forceinline__ void phase_compact(const SelArgs& a, const int* L, un
     flush_orand(orL, andL, ss->or_L[nx], ss->and_L[nx], sh);
 }
 
-// bitonic sort of (key, val) pairs in shared memory, n = power of two
-__device__ __forceinline__ void bitonic_sort(unsigned long long* key, int* val, int n) {
+// (w0, w1, id) order with padding (id < 0) after every real key
+__device__ __forceinline__ bool sk_less(unsigned long long a0, unsigned long long a1, int av, unsigned long long b0,
+                                        unsigned long long b1, int bv) {
+    if (av < 0) return false;
+    if (bv < 0) return true;
+    if (a0 != b0) return a0 < b0;
+    if (a1 != b1) return a1 < b1;
+    return av < bv;
+}
+
+// bitonic sort of full keys in shared memory, n = power of two
+__device__ __forceinline__ void bitonic_sort(unsigned long long* k0, unsigned long long* k1, int* val, int n) {
     for (int k = 2; k <= n; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) {
                 const int ixj = i ^ j;
                 if (ixj > i) {
-                    const unsigned long long x = key[i], y = key[ixj];
                     const bool up = (i & k) == 0;
-                    if ((x > y) == up) {
-                        key[i] = y;
-                        key[ixj] = x;
-                        const int t = val[i];
+                    const bool gt = sk_less(k0[ixj], k1[ixj], val[ixj], k0[i], k1[i], val[i]);
+                    if (gt == up) {
+                        const unsigned long long t0 = k0[i], t1 = k1[i];
+                        const int tv = val[i];
+                        k0[i] = k0[ixj];
+                        k1[i] = k1[ixj];
                         val[i] = val[ixj];
-                        val[ixj] = t;
+                        k0[ixj] = t0;
+                        k1[ixj] = t1;
+                        val[ixj] = tv;
                     }
                 }
             }
@@ -541,24 +541,42 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long* key, int* val, 
 
 // sort S[off, off+cnt) in place (one CTA)
 __device__ __forceinline__ void sort_bucket(const SelArgs& a, int* S, unsigned int off, unsigned int cnt,
-                                            unsigned long long v0, unsigned long long v1, unsigned long long v2,
-                                            int nbits, unsigned long long* key, int* val) {
+                                            unsigned long long* k0, unsigned long long* k1, int* val) {
     int np = 2;
     while (static_cast<unsigned int>(np) < cnt) np <<= 1;
     for (int i = threadIdx.x; i < np; i += blockDim.x) {
         if (static_cast<unsigned int>(i) < cnt) {
             const int x = __ldcg(&S[off + i]);
-            key[i] = pack_key(load_key(a.keys, x), x, v0, v1, v2);
+            const Key2 k = load_key(a.keys, x);
+            k0[i] = k.w0;
+            k1[i] = k.w1;
             val[i] = x;
         } else {
-            key[i] = 1ull << nbits;  // padding sorts after every packed key (nbits < 64)
             val[i] = -1;
         }
     }
     __syncthreads();
-    bitonic_sort(key, val, np);
+    bitonic_sort(k0, k1, val, np);
     for (int i = threadIdx.x; i < static_cast<int>(cnt); i += blockDim.x) S[off + i] = val[i];
     __syncthreads();
+}
+
+// small bucket (<= 32 heads): one warp, rank = number of smaller keys
+__device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, int* S, unsigned int off, unsigned int cnt) {
+    const int lane = threadIdx.x & 31;
+    const bool in = static_cast<unsigned int>(lane) < cnt;
+    const int x = in ? __ldcg(&S[off + lane]) : -1;
+    Key2 k{0, 0};
+    if (in) k = load_key(a.keys, x);
+    int rank = 0;
+    for (unsigned int j = 0; j < cnt; ++j) {
+        const unsigned long long b0 = __shfl_sync(0xffffffffu, k.w0, j);
+        const unsigned long long b1 = __shfl_sync(0xffffffffu, k.w1, j);
+        const int bv = __shfl_sync(0xffffffffu, x, j);
+        rank += sk_less(b0, b1, bv, k.w0, k.w1, x) ? 1 : 0;
+    }
+    __syncwarp();
+    if (in) S[off + rank] = x;
 }
 
 // every eligible node of a selected chain lands at start[rank(head)] + d
@@ -610,7 +628,8 @@ struct PersistSmem {
         } hist;
         typename cub::BlockScan<unsigned long long, kPThreads>::TempStorage scan;
         struct {
-            unsigned long long key[kBucketCap];
+            unsigned long long k0[kBucketCap];
+            unsigned long long k1[kBucketCap];
             int val[kBucketCap];
         } sort;
     } u;
@@ -703,9 +722,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
                     ss->and_L[nx][w] = ~0ull;
                 }
             }
-            phase_hist(a, L, nL, lo, sm.u.hist.w, sm.u.hist.c);
-            grid.sync();
-            phase_hist_reduce(a);
+            phase_hist(a, L, nL, lo, n_pass, sm.u.hist.w, sm.u.hist.c);
             grid.sync();
             stamp(ss);
             const PickOut pk = phase_pick(a, need, n_pass, nS, &sm.u.scan, sm.off, &sm.pick);
@@ -747,22 +764,33 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     __syncthreads();
     const unsigned long long v0 = sm.bc[0], v1 = sm.bc[1], v2 = sm.bc[2];
     __syncthreads();
-    const int nbits = __popcll(v0) + __popcll(v1) + __popcll(v2);
-    if (max_bucket > static_cast<unsigned int>(kBucketCap) || nbits >= 64) {
+    if (max_bucket > static_cast<unsigned int>(kBucketCap)) {
         if (tid == 0) {
             ss->host_sort = 1;  // device-wide sort driven from the host
             ss->max_bucket = static_cast<int>(max_bucket);
         }
         return;
     }
+    (void)v0;
+    (void)v1;
+    (void)v2;
     if (take_all) {
-        if (blockIdx.x == 0) sort_bucket(a, S, 0, static_cast<unsigned int>(nS), v0, v1, v2, nbits, sm.u.sort.key,
-                                         sm.u.sort.val);
+        if (blockIdx.x == 0)
+            sort_bucket(a, S, 0, static_cast<unsigned int>(nS), sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
     } else {
-        for (int j = blockIdx.x; j < n_pass * kBins; j += gridDim.x) {
+        // large buckets: one CTA each; small ones: one warp each (no block barriers)
+        const int nb = n_pass * kBins;
+        for (int j = blockIdx.x; j < nb; j += gridDim.x) {
             const unsigned int cnt = __ldcg(&a.seg_cnt[j]);
-            if (cnt < 2) continue;
-            sort_bucket(a, S, __ldcg(&a.seg_off[j]), cnt, v0, v1, v2, nbits, sm.u.sort.key, sm.u.sort.val);
+            if (cnt <= 32u) continue;
+            sort_bucket(a, S, __ldcg(&a.seg_off[j]), cnt, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
+        }
+        const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
+        const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(blockDim.x)) >> 5);
+        for (int j = gwarp; j < nb; j += nwarps) {
+            const unsigned int cnt = __ldcg(&a.seg_cnt[j]);
+            if (cnt < 2u || cnt > 32u) continue;
+            warp_sort_bucket(a, S, __ldcg(&a.seg_off[j]), cnt);
         }
     }
     grid.sync();
@@ -914,10 +942,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     c.sorti_out.reserve(static_cast<std::size_t>(c.n) + 1);
     c.cnt.reserve(static_cast<std::size_t>(c.n) + 1);
     const int grid = persistent_grid(c);
-    c.part_w.reserve(static_cast<std::size_t>(grid) * kBins);
-    c.part_c.reserve(static_cast<std::size_t>(grid) * kBins);
-    c.hist_w.reserve(kBins);
-    c.hist_c.reserve(kBins);
+    c.hist_w.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
+    c.hist_c.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
     c.seg_off.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
     c.seg_cnt.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
     c.cursor.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
@@ -941,8 +967,6 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     a.victims = c.vid_out.p;
     a.hist_w = c.hist_w.p;
     a.hist_c = c.hist_c.p;
-    a.part_w = c.part_w.p;
-    a.part_c = c.part_c.p;
     a.seg_off = c.seg_off.p;
     a.seg_cnt = c.seg_cnt.p;
     a.cursor = c.cursor.p;

@@ -96,8 +96,8 @@ __global__ void spine_products_kernel(ScoreArgs s, const int* spine, const long 
         if (__ldg(s.fstate + slot) != 1) {
             atomicOr(miss, 1u);
         } else {
-            const double* row = s.P + (static_cast<std::size_t>(slot) * s.K + k) * s.V1;
-            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k), mass_on(row, b));
+            const double* col = s.P + static_cast<std::size_t>(slot) * s.V1 * s.K + k;
+            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * s.K + k), mass_on(col, s.K, b));
         }
         out[base[j] + t] = x;
     }
