@@ -132,6 +132,11 @@ int pbkv_ctx_set_timing(pbkv_ctx* ctx, int enabled);
 int pbkv_ctx_phase_times(pbkv_ctx* ctx, uint64_t* ns, int cap, int* n);
 /* Cumulative launch counts: pbkv's own kernels, and CUB library calls. */
 int pbkv_ctx_launches(pbkv_ctx* ctx, int64_t* kernels, int64_t* lib_calls);
+/* Heavy-node deferral in RECOMPUTE decisions: enable/disable,
+ * and how many decisions took the fast path (placed from score intervals)
+ * vs the exact-chain path.  Results are identical either way. */
+int pbkv_ctx_set_defer(pbkv_ctx* ctx, int enabled);
+int pbkv_ctx_defer_stats(pbkv_ctx* ctx, int64_t* fast, int64_t* slow);
 
 /* ---- device mirror of the tree --------------------------------------------- */
 /* Full upload of a CacheTree snapshot (SURVEY.md §8(b) pbkv_mirror_full). */

@@ -333,6 +333,15 @@ class Policy:
     def set_timing(self, on: bool) -> None:
         self._c(_abi.lib().pbkv_ctx_set_timing(self._h, 1 if on else 0))
 
+    def set_defer(self, on: bool) -> None:
+        """Heavy-node deferral in RECOMPUTE decisions (results identical)."""
+        self._c(_abi.lib().pbkv_ctx_set_defer(self._h, 1 if on else 0))
+
+    def defer_stats(self) -> tuple[int, int]:
+        f, s = C.c_int64(), C.c_int64()
+        self._c(_abi.lib().pbkv_ctx_defer_stats(self._h, C.byref(f), C.byref(s)))
+        return f.value, s.value
+
     def launches(self) -> tuple[int, int]:
         """(pbkv kernels launched, CUB library calls) since the context was created."""
         k, l = C.c_int64(), C.c_int64()

@@ -1,6 +1,7 @@
 // C ABI implementation (include/pbkv.h): context, device mirror, forecast
 // store and the orchestration of the stage 2-4 kernels (kernels.cu).
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cstring>
 #include <memory>
@@ -231,6 +232,9 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     std::vector<long long> hstart;
     std::vector<int> depth;
     c.h_entries.assign(static_cast<std::size_t>(n), 0);
+    c.h_heavy_last.clear();
+    c.h_heavy_parent.clear();
+    c.h_heavy_flags.clear();
     for (std::int64_t i = 0; i < n; ++i) {
         if (s.tier[i] > PBKV_TIER_ABSENT) invalid("tree soa: bad tier value");
         flags[static_cast<std::size_t>(i)] =
@@ -254,6 +258,9 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
                 hent_node.push_back(static_cast<int>(heavy.size()));
             }
             heavy.push_back(static_cast<int>(i));
+            c.h_heavy_last.push_back(s.last_access[i]);
+            c.h_heavy_parent.push_back(s.parent[i]);
+            c.h_heavy_flags.push_back(static_cast<std::uint8_t>(s.tier[i] | (s.retired[i] ? kFlagRetired : 0)));
         } else if (ne > 2) {
             medium.push_back(static_cast<int>(i));
         }
@@ -331,6 +338,9 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     }
     c.n_medium = static_cast<std::int64_t>(medium.size());
     c.n_heavy = static_cast<std::int64_t>(heavy.size());
+    c.h_heavy = heavy;
+    c.h_heavy_depth.resize(heavy.size());
+    for (std::size_t j = 0; j < heavy.size(); ++j) c.h_heavy_depth[j] = dep[heavy[j]];
     c.n_hent = static_cast<std::int64_t>(hent.size());
     c.max_depth = maxd;
     c.device_capacity = s.device_capacity;
@@ -395,6 +405,136 @@ struct SoaStore {
 // Keys (from the recomputed or the cached score), lock marks, subtree max,
 // then the weighted cut and the victim order (select.cu).  Victims land in
 // c.vid_out[0..n_victims).
+// ---- deferred heavy nodes ------------------------------------
+// CandidateKey packing (common.cuh make_key) on the host
+unsigned long long host_enc_rank(double r) {
+    if (r == 0.0) r = 0.0;
+    unsigned long long b;
+    std::memcpy(&b, &r, sizeof b);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+struct HKey {  // (w0, w1, id) of policies.hpp:40-48
+    unsigned long long w0 = 0, w1 = 0;
+    int id = -1;
+    bool valid() const { return id >= 0; }
+};
+
+bool hkey_less(const HKey& a, const HKey& b) {
+    if (a.w0 != b.w0) return a.w0 < b.w0;
+    if (a.w1 != b.w1) return a.w1 < b.w1;
+    return a.id < b.id;
+}
+
+HKey make_hkey(int cls, double rank, unsigned long long last, int id) {
+    const unsigned long long e = host_enc_rank(rank);
+    HKey k;
+    k.w0 = (static_cast<unsigned long long>(cls) << 63) | (e >> 1);
+    k.w1 = ((e & 1ull) << 63) | last;
+    k.id = id;
+    return k;
+}
+
+// The selection ran with heavy nodes out of the order (zero keys, not
+// candidates).  Their exact scores lie in [A - B, A + B] (A the approximate
+// sum, B = L * ulp(sum |x|)), so each one's (eff, d) record is either known
+// exactly (a descendant's key beats its whole interval), or is its own key
+// with a known interval.  If every eligible heavy node's record is provably
+// after the last victim's, the cut is exact as computed.  Returns false when
+// that cannot be proved (the caller then runs the exact chains).
+bool place_deferred(Context& c, long long* result_dev, const SelectCounts& o, std::int64_t needed) {
+    if (o.shortfall || o.n_victims == 0) return false;
+    const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
+    const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
+    c.hreport.reserve(bytes);
+    c.hreport_h.reserve(bytes + 2 * nh * sizeof(double));
+    HeavyReport* rep_d = reinterpret_cast<HeavyReport*>(c.hreport.p);
+    launch_heavy_report(c, result_dev, rep_d);
+    PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p, rep_d, bytes, cudaMemcpyDeviceToHost, c.stream));
+    PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p + bytes, c.happrox.p, 2 * nh * sizeof(double), cudaMemcpyDeviceToHost,
+                              c.stream));
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    const HeavyReport* rep = reinterpret_cast<const HeavyReport*>(c.hreport_h.p);
+    const double* ap = reinterpret_cast<const double*>(c.hreport_h.p + bytes);
+    const HeavyReport& tail = rep[nh];
+    if (tail.eff < 0) return false;
+    HKey tkey;
+    tkey.w0 = tail.w0;
+    tkey.w1 = tail.w1;
+    tkey.id = tail.eff;
+    // record order (key, d) of the tail
+    auto after_tail = [&](const HKey& k, int d) {
+        if (hkey_less(tkey, k)) return true;
+        if (hkey_less(k, tkey)) return false;
+        return d > tail.depth_diff;
+    };
+    // heavy nodes deepest first: eff of a heavy node may come from a heavy descendant
+    std::vector<std::size_t> order(nh);
+    for (std::size_t j = 0; j < nh; ++j) order[j] = j;
+    std::sort(order.begin(), order.end(),
+              [&](std::size_t a, std::size_t b) { return c.h_heavy_depth[a] > c.h_heavy_depth[b]; });
+    std::unordered_map<int, std::size_t> idx;
+    for (std::size_t j = 0; j < nh; ++j) idx[c.h_heavy[j]] = j;
+    struct Eff {
+        HKey lo, hi;   // exact when lo == hi
+        int depth = -1;
+        bool any = false;
+    };
+    std::vector<Eff> eff(nh);
+    std::vector<char> sub(nh, 0);
+    for (std::size_t j : order) {
+        const HeavyReport& r = rep[j];
+        const int h = c.h_heavy[j];
+        const int d = c.h_heavy_depth[j];
+        const bool device = (c.h_heavy_flags[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
+        Eff best;
+        if (r.eff >= 0) {
+            best.lo.w0 = best.hi.w0 = r.w0;
+            best.lo.w1 = best.hi.w1 = r.w1;
+            best.lo.id = best.hi.id = r.eff;
+            best.depth = r.eff_depth;
+            best.any = true;
+        }
+        sub[j] = sub[j] || r.sublock;
+        // heavy children already resolved (their eff covers their subtrees)
+        for (std::size_t q = 0; q < nh; ++q) {
+            if (c.h_heavy_parent[q] != h || !eff[q].any) continue;
+            sub[j] = sub[j] || sub[q];
+            if (!best.any || hkey_less(best.hi, eff[q].lo)) {
+                best = eff[q];
+            } else if (!hkey_less(eff[q].hi, best.lo)) {
+                return false;  // overlapping intervals: order unknown
+            }
+        }
+        if (device && h != 0) {
+            const double A = ap[2 * j], S = ap[2 * j + 1];
+            int ex = 0;
+            std::frexp(S, &ex);
+            const double L = static_cast<double>(c.h_entries[static_cast<std::size_t>(h)]) * c.K;
+            const double B = S > 0.0 ? 2.0 * L * std::ldexp(1.0, ex - 53) : 0.0;
+            if (!(std::isfinite(A) && std::isfinite(B))) return false;
+            const bool retired = (c.h_heavy_flags[j] & kFlagRetired) != 0;
+            if (retired) return false;  // not expected for a node with entries
+            Eff own;
+            own.lo = make_hkey(1, A - B, c.h_heavy_last[j], h);
+            own.hi = make_hkey(1, A + B, c.h_heavy_last[j], h);
+            own.depth = d;
+            own.any = true;
+            if (!best.any || hkey_less(best.hi, own.lo)) {
+                best = own;
+            } else if (!hkey_less(own.hi, best.lo)) {
+                return false;  // own interval straddles the descendants' maximum
+            }
+        }
+        eff[j] = best;
+        if (!device || h == 0 || sub[j] || !best.any) continue;
+        if (r.miss) return false;  // eligible with a missing forecast: the exact path raises
+        if (!after_tail(best.lo, best.depth - d)) return false;
+    }
+    (void)needed;
+    return true;
+}
+
 SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t needed, const int* locked_dev,
                          std::int64_t n_locked, long long* result_dev) {
     if (needed <= 0) invalid("eviction request must free a positive amount");
@@ -406,12 +546,29 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
     record(c, 0);
     reset_status(c);
     const bool recompute = score_mode == PBKV_SCORE_RECOMPUTE && policy == PBKV_POLICY_HE;
-    if (recompute)
+    const bool defer = recompute && c.defer_heavy && c.n_heavy > 0 && c.spine.empty();
+    if (defer) {
+        launch_set_deferred(c, true);
+        launch_score_decision(c, policy);
+    } else if (recompute) {
         launch_score_all(c, c.score_rc.p, true, policy, false);
-    else
+    } else {
         launch_keys_cached(c, policy);
+    }
     record(c, 1);
     SelectCounts o = run_select(c, locked_dev, n_locked, needed, recompute, result_dev);
+    if (defer) {
+        const bool placed = place_deferred(c, result_dev ? result_dev : c.counters.p + 8, o, needed);
+        launch_set_deferred(c, false);
+        if (placed) {
+            ++c.defer_fast;
+        } else {  // slow path: exact chains, full selection
+            ++c.defer_slow;
+            reset_status(c);
+            launch_score_all(c, c.score_rc.p, true, policy, false);
+            o = run_select(c, locked_dev, n_locked, needed, recompute, result_dev);
+        }
+    }
     record(c, 2);
     finish_timing(c, 2);
     return o;
@@ -547,6 +704,21 @@ int pbkv_ctx_launches(pbkv_ctx* c, int64_t* kernels, int64_t* lib_calls) {
         need(c, "null ctx");
         if (kernels) *kernels = c->launches;
         if (lib_calls) *lib_calls = c->lib_calls;
+    });
+}
+
+int pbkv_ctx_set_defer(pbkv_ctx* c, int enabled) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        c->defer_heavy = enabled != 0;
+    });
+}
+
+int pbkv_ctx_defer_stats(pbkv_ctx* c, int64_t* fast, int64_t* slow) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        if (fast) *fast = c->defer_fast;
+        if (slow) *slow = c->defer_slow;
     });
 }
 

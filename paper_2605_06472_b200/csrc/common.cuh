@@ -163,7 +163,7 @@ __device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score)
     const unsigned long long last = a.last[n];
     if (last >> 63) set_error(a.st, PBKV_EINVAL, kErrLastAccessRange, n);
     Key2 k;
-    if (f & kFlagExcluded) {  // sharded spine node (shard.cu)
+    if (f & kFlagOutOfOrder) {  // sharded spine node (shard.cu) / deferred heavy node
         reinterpret_cast<ulonglong2*>(a.keys)[n] = make_ulonglong2(0ull, 0ull);
         return;
     }

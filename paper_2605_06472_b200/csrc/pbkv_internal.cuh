@@ -29,6 +29,10 @@ constexpr std::uint8_t kFlagRetired = 0x4;
 // spine node of a sharded tree (shard.cu): never a local candidate, key zeroed
 // so that eff() of a spine node is the maximum over its local descendants only
 constexpr std::uint8_t kFlagExcluded = 0x8;
+// heavy node whose exact Eq. 2 chain is deferred during a decision (DESIGN.md
+// §3.2): handled like an excluded node, then placed from its score interval
+constexpr std::uint8_t kFlagDeferred = 0x10;
+constexpr std::uint8_t kFlagOutOfOrder = kFlagExcluded | kFlagDeferred;
 constexpr int kMediumMaxChain = 256;  // entries*K above this -> heavy (CTA) path
 
 // first-error-wins device status (kernels never throw)
@@ -194,6 +198,15 @@ struct Context {
     DevBuf<double> hxs;           // products of the heavy entries
     DevBuf<unsigned int> hmiss;   // per heavy node: missing (1) / short horizon (2)
     std::int64_t n_hent = 0;
+    std::vector<int> h_heavy;                 // heavy node ids (host copy)
+    std::vector<unsigned long long> h_heavy_last;
+    std::vector<int> h_heavy_depth, h_heavy_parent;
+    std::vector<std::uint8_t> h_heavy_flags;
+    DevBuf<double> happrox;                   // [2*n_heavy]: approximate Eq. 2 sum, sum of |terms|
+    DevBuf<unsigned char> hreport;            // deferred-heavy reports + the tail record
+    PinBuf<unsigned char> hreport_h;
+    bool defer_heavy = true;                  // decision fast path enabled
+    long long defer_fast = 0, defer_slow = 0; // fast / slow path counts
     std::int64_t device_capacity = 0, device_used = 0, retired_device_tokens = 0, host_capacity = 0, host_used = 0;
     int max_depth = 0;
     std::vector<std::int64_t> h_slot_wf;  // slot -> WorkflowId
@@ -273,6 +286,18 @@ void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int
 void launch_chain_sum(Context& c, const double* x, const long long* off, int n_seg, double* out);
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
 void launch_keys_cached(Context& c, int policy);
+void launch_score_decision(Context& c, int policy);  // Eq. 2 + keys with heavy chains deferred
+void launch_set_deferred(Context& c, bool on);
+struct HeavyReport {  // one per heavy node, then one tail record (select.cu)
+    unsigned long long w0, w1;  // key of eff(h) over its non-deferred descendants / of the tail head
+    int eff;                    // node id (-1: none)
+    int eff_depth;
+    int sublock;
+    int miss;                   // missing forecast on one of its entries (1/2)
+    int depth_diff;             // tail record: depth(head) - depth(last victim)
+    int pad;
+};
+void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out);
 SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked, std::int64_t needed,
                         bool he_recompute, long long* result_dev);
 std::size_t sel_state_bytes();

@@ -388,6 +388,41 @@ __global__ void __launch_bounds__(kChainT) chain_sum_kernel(const double* x, con
     if (threadIdx.x == 0) out[blockIdx.x] = t;
 }
 
+// Approximate Eq. 2 of each heavy node: sum and sum of |terms| of its
+// products in any order (FP64 tree reduction).  The exact serial chain E and
+// this sum A both lie within L * ulp(sum|x|) / 2 of the real sum, so
+// |E - A| <= L * ulp(sum|x|): the interval the decision fast path uses.
+__global__ void __launch_bounds__(256) heavy_approx_kernel(const unsigned int* acc_off, const int* nodes,
+                                                           const long long* xs_start, const double* xs_g, int K,
+                                                           double* out) {
+    using Red = cub::BlockReduce<double, 256>;
+    __shared__ typename Red::TempStorage tmp;
+    const int node = nodes[blockIdx.x];
+    const long long L = static_cast<long long>(acc_off[node + 1] - acc_off[node]) * K;
+    const double* x = xs_g + xs_start[blockIdx.x];
+    double s = 0.0, a = 0.0;
+    for (long long i = threadIdx.x; i < L; i += 256) {
+        const double v = __ldcg(x + i);
+        s += v;
+        a += fabs(v);
+    }
+    s = Red(tmp).Sum(s);
+    __syncthreads();
+    a = Red(tmp).Sum(a);
+    if (threadIdx.x == 0) {
+        out[2 * blockIdx.x] = s;
+        out[2 * blockIdx.x + 1] = a;
+    }
+}
+
+__global__ void set_deferred_kernel(std::uint8_t* flags, Key2* keys, const int* nodes, int n, int on) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = nodes[i];
+    flags[v] = on ? (flags[v] | kFlagDeferred) : (flags[v] & ~kFlagDeferred);
+    if (on) reinterpret_cast<ulonglong2*>(keys)[v] = make_ulonglong2(0ull, 0ull);  // out of every eff max
+}
+
 // Eq. 1 / Eq. 2 of an id list, one thread per short id (refresh_nodes path)
 template <bool kValueOnly>
 __global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* ids, std::int64_t n, double* out) {
@@ -582,6 +617,53 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
         ++c.launches;
     }
     if (c.n_heavy > 0) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+}
+
+void launch_set_deferred(Context& c, bool on) {
+    if (c.n_heavy == 0) return;
+    const int n = static_cast<int>(c.n_heavy);
+    set_deferred_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.flags.p, c.keys.p, c.heavy.p, n, on ? 1 : 0);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+// Eq. 2 + keys for a decision with the heavy chains deferred: heavy nodes
+// carry the kFlagDeferred bit (zero key, out of the order); their products
+// and approximate sums are formed on the side stream; the exact chains run
+// only if the fast-path check in select_core cannot place them.
+void launch_score_decision(Context& c, int policy) {
+    ScoreArgs s = make_score_args(c, c.score_rc.p);
+    KeyArgs ka = make_key_args(c, policy);
+    if (c.n_heavy > 0) {
+        c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy));
+        PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy) * sizeof(unsigned int), c.side));
+        heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(s, c.hent.p, c.hent_node.p,
+                                                                               c.n_hent, c.hxs.p, c.hmiss.p);
+        PBKV_CUDA(cudaGetLastError());
+        heavy_approx_kernel<<<static_cast<unsigned int>(c.n_heavy), 256, 0, c.side>>>(c.acc_off.p, c.heavy.p,
+                                                                                       c.hstart.p, c.hxs.p, c.K,
+                                                                                       c.happrox.p);
+        PBKV_CUDA(cudaGetLastError());
+        c.launches += 2;
+        PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
+    }
+    launch_light<true>(c, s, ka, 0);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+    if (c.n_medium > 0) {  // medium nodes on the side stream too, overlapped with the light pass
+        if (c.n_heavy == 0) {
+            PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+            PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        }
+        const unsigned int g = static_cast<unsigned int>((c.n_medium + kMediumWarps - 1) / kMediumWarps);
+        score_medium_kernel<true, false><<<g, kMediumWarps * 32, 0, c.side>>>(s, ka, c.medium.p, c.n_medium, 0, 0);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+        PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
+    }
+    if (c.n_heavy > 0 || c.n_medium > 0) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
 // Eq. 2 / Eq. 1 of an id list, results scattered into out[id]

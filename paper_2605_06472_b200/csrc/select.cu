@@ -310,7 +310,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
         const std::int64_t i = base + threadIdx.x;
         const int n = static_cast<int>(i);
         bool head = false;
-        if (i < a.n_nodes && n != 0 && (a.flags[n] & (kFlagTierMask | kFlagExcluded)) == PBKV_TIER_DEVICE &&
+        if (i < a.n_nodes && n != 0 && (a.flags[n] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
             !__ldcg(&a.sublock[n])) {
             const std::uint8_t ms = a.missing[n];
             if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n);
@@ -327,7 +327,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
                 w += static_cast<unsigned long long>(a.len[p]);
                 ++c;
                 p = a.parent[p];
-            } while (p > 0 && !(a.flags[p] & kFlagExcluded) && !__ldcg(&a.sublock[p]) && __ldcg(&a.eff[p]) == n);
+            } while (p > 0 && !(a.flags[p] & kFlagOutOfOrder) && !__ldcg(&a.sublock[p]) && __ldcg(&a.eff[p]) == n);
             a.W[n] = w;
             a.C[n] = c;
             a.rank[n] = -1;
@@ -583,7 +583,7 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, int* S, unsig
 __device__ __forceinline__ void phase_scatter(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
     for (std::int64_t i = tid; i < a.n_nodes; i += nthr) {
         const int n = static_cast<int>(i);
-        if (n == 0 || (a.flags[n] & (kFlagTierMask | kFlagExcluded)) != PBKV_TIER_DEVICE || __ldcg(&a.sublock[n]))
+        if (n == 0 || (a.flags[n] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE || __ldcg(&a.sublock[n]))
             continue;
         const int h = __ldcg(&a.eff[n]);
         const int r = __ldcg(&a.rank[h]);
@@ -912,6 +912,56 @@ int persistent_grid(Context& c) {
 }  // namespace
 
 std::size_t sel_state_bytes() { return sizeof(SelState); }
+
+namespace {
+// per deferred heavy node: max key over its non-deferred device descendants
+// (eff after the walk; its own key is zeroed), lock status, missing
+// forecasts; plus the record of the last victim of the cut (tail)
+__global__ void heavy_report_kernel(const int* heavy, int n_heavy, const Key2* keys, const int* eff,
+                                    const int* sublock, const int* depth, const std::uint8_t* flags,
+                                    const unsigned int* hmiss, const int* victims, const long long* result,
+                                    HeavyReport* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n_heavy) {
+        const int h = heavy[j];
+        const int e = eff[h];
+        HeavyReport r{};
+        const bool has = !(flags[e] & kFlagOutOfOrder);
+        const Key2 k = load_key(keys, e);
+        r.w0 = has ? k.w0 : 0ull;
+        r.w1 = has ? k.w1 : 0ull;
+        r.eff = has ? e : -1;
+        r.eff_depth = has ? depth[e] : -1;
+        r.sublock = sublock[h] ? 1 : 0;
+        r.miss = static_cast<int>(hmiss[j]);
+        out[j] = r;
+    } else if (j == n_heavy) {
+        HeavyReport r{};
+        const long long n = result[0];
+        r.eff = -1;
+        if (n > 0) {
+            const int v = victims[n - 1];
+            const int h = eff[v];
+            const Key2 k = load_key(keys, h);
+            r.w0 = k.w0;
+            r.w1 = k.w1;
+            r.eff = h;
+            r.eff_depth = depth[h];
+            r.depth_diff = depth[h] - depth[v];
+        }
+        out[j] = r;
+    }
+}
+}  // namespace
+
+void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out) {
+    const int n = static_cast<int>(c.n_heavy);
+    heavy_report_kernel<<<(n + 1 + 127) / 128, 128, 0, c.stream>>>(c.heavy.p, n, c.keys.p, c.eff.p, c.sublock.p,
+                                                                   c.depth.p, c.flags.p, c.hmiss.p, c.vid_out.p,
+                                                                   result_dev, out);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
 
 void launch_keys_cached(Context& c, int policy) {
     KeyArgs ka = make_key_args(c, policy);
