@@ -156,11 +156,11 @@ struct KeyArgs {
 
 namespace dev {
 
-// key of policies.hpp:88-153 for device node n (HE uses `score`)
-__device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score) {
-    const std::uint8_t f = a.flags[n];
+// key of policies.hpp:88-153 for device node n (HE uses `score`), node
+// fields already loaded by the caller
+__device__ __forceinline__ void write_key_v(const KeyArgs& a, int n, double score, std::uint8_t f,
+                                            unsigned long long last, int ever) {
     const bool retired = (f & kFlagRetired) != 0;
-    const unsigned long long last = a.last[n];
     if (last >> 63) set_error(a.st, PBKV_EINVAL, kErrLastAccessRange, n);
     Key2 k;
     if (f & kFlagOutOfOrder) {  // sharded spine node (shard.cu) / deferred heavy node
@@ -172,10 +172,10 @@ __device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score)
             k = make_key(0, 0.0, last);
             break;
         case PBKV_POLICY_LAE:
-            k = retired ? make_key(0, static_cast<double>(a.ever[n]), last) : make_key(1, 0.0, last);
+            k = retired ? make_key(0, static_cast<double>(ever), last) : make_key(1, 0.0, last);
             break;
         case PBKV_POLICY_HE:
-            k = retired ? make_key(0, static_cast<double>(a.ever[n]), last) : make_key(1, score, last);
+            k = retired ? make_key(0, static_cast<double>(ever), last) : make_key(1, score, last);
             break;
         default: {  // KVFLOW
             bool miss = false;
@@ -187,6 +187,10 @@ __device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score)
         }
     }
     reinterpret_cast<ulonglong2*>(a.keys)[n] = make_ulonglong2(k.w0, k.w1);
+}
+
+__device__ __forceinline__ void write_key(const KeyArgs& a, int n, double score) {
+    write_key_v(a, n, score, a.flags[n], a.last[n], a.ever[n]);
 }
 
 // per-node scratch init for the selection (every node, device or not); the

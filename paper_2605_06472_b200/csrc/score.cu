@@ -459,47 +459,60 @@ __global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* 
 // forecast.hpp:19-42).  gs[k] = gamma^k * s(k) with gamma^k by repeated
 // multiplication and the product taken in the reference order (g * s),
 // scoring.hpp:56-58, so that gs[k] * m equals (g * s(k)) * m bit for bit.
-__global__ void forecast_prepare_kernel(const double* stage, const long long* slots, std::int64_t n, int H, int V1,
-                                        int K, double gamma, double* P, double* gs, std::uint8_t* fstate,
-                                        DevStatus* st) {
-    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < n;
-         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+__global__ void __launch_bounds__(256) forecast_prepare_kernel(const double* stage, const long long* slots,
+                                                               std::int64_t n, int H, int V1, int K, double gamma,
+                                                               double* P, double* gs, std::uint8_t* fstate,
+                                                               DevStatus* st) {
+    // one warp per forecast row: lane k validates step k (agent-ordered sum,
+    // forecast.hpp:25-34), the warp transposes the row into the agent-major
+    // table, lane 0 runs the survival / gamma chain (forecast.hpp:35-41)
+    const int lane = threadIdx.x & 31;
+    const std::int64_t nw = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t j = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5; j < n; j += nw) {
         const double* p = stage + static_cast<std::size_t>(j) * H * V1;
         const long long slot = slots[j];
-        bool bad = false;
-        for (int k = 0; k < H && !bad; ++k) {
+        int bad = 0;
+        for (int k = lane; k < H; k += 32) {
             double sum = 0.0;
             for (int a = 0; a < V1; ++a) {
                 const double v = p[k * V1 + a];
                 if (v < -1e-12) {
-                    set_error(st, PBKV_EINVAL, kErrForecastNegative, j);
-                    bad = true;
+                    bad = 1;
                     break;
                 }
                 sum = __dadd_rn(sum, v);
             }
-            if (!bad && fabs(__dsub_rn(sum, 1.0)) > 1e-9) {
-                set_error(st, PBKV_EINVAL, kErrForecastSum, j);
-                bad = true;
-            }
+            if (!bad && fabs(__dsub_rn(sum, 1.0)) > 1e-9) bad = 2;
         }
-        if (bad) continue;
+        // the first failing step wins, as in the ctor's loop
+        const unsigned neg = __ballot_sync(0xffffffffu, bad == 1), off = __ballot_sync(0xffffffffu, bad == 2);
+        if (neg | off) {
+            if (lane == 0) {
+                const int first = __ffs(neg | off) - 1;
+                set_error(st, PBKV_EINVAL, ((neg >> first) & 1u) ? kErrForecastNegative : kErrForecastSum, j);
+            }
+            continue;
+        }
         double* dst = P + static_cast<std::size_t>(slot) * K * V1;
-        double* g = gs + static_cast<std::size_t>(slot) * K;
-        double surv = 1.0, gk = 1.0;
-        for (int k = 0; k < K; ++k) {
-            if (k < H) {
-                for (int a = 0; a < V1; ++a) dst[a * K + k] = p[k * V1 + a];  // agent-major [a][k]
-                g[k] = __dmul_rn(gk, surv);
-                surv = __dmul_rn(surv, __dsub_rn(1.0, p[k * V1 + V1 - 1]));
-                if (surv < 0.0) surv = 0.0;
-            } else {
-                for (int a = 0; a < V1; ++a) dst[a * K + k] = 0.0;
-                g[k] = 0.0;
-            }
-            gk = __dmul_rn(gk, gamma);
+        for (int idx = lane; idx < K * V1; idx += 32) {  // dst[a][k], coalesced stores
+            const int a = idx / K, k = idx % K;
+            dst[idx] = k < H ? p[k * V1 + a] : 0.0;
         }
-        fstate[slot] = H >= K ? 1 : 2;
+        if (lane == 0) {
+            double* g = gs + static_cast<std::size_t>(slot) * K;
+            double surv = 1.0, gk = 1.0;
+            for (int k = 0; k < K; ++k) {
+                if (k < H) {
+                    g[k] = __dmul_rn(gk, surv);
+                    surv = __dmul_rn(surv, __dsub_rn(1.0, p[k * V1 + V1 - 1]));
+                    if (surv < 0.0) surv = 0.0;
+                } else {
+                    g[k] = 0.0;
+                }
+                gk = __dmul_rn(gk, gamma);
+            }
+            fstate[slot] = H >= K ? 1 : 2;
+        }
     }
 }
 
@@ -567,8 +580,8 @@ KeyArgs make_key_args(Context& c, int policy) {
 }
 
 void launch_forecast_prepare(Context& c, const double* stage, const long long* slots, std::int64_t n, int H) {
-    forecast_prepare_kernel<<<grid_for(n, 128), 128, 0, c.stream>>>(stage, slots, n, H, c.V1, c.K, c.gamma, c.P.p,
-                                                                   c.gs.p, c.fstate.p, c.status.p);
+    forecast_prepare_kernel<<<grid_cap(n * 32, 256), 256, 0, c.stream>>>(stage, slots, n, H, c.V1, c.K, c.gamma,
+                                                                        c.P.p, c.gs.p, c.fstate.p, c.status.p);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
 }
