@@ -117,6 +117,8 @@ void ensure_scratch(Context& c) {
     c.heads.reserve(n);
     c.listB.reserve(n);
     c.listS.reserve(n);
+    c.listS2.reserve(n);
+    c.big.reserve(2 * n);
     c.rank.reserve(n);
     c.vid_out.reserve(n);
 }
@@ -417,7 +419,6 @@ unsigned long long host_enc_rank(double r) {
 struct HKey {  // (w0, w1, id) of policies.hpp:40-48
     unsigned long long w0 = 0, w1 = 0;
     int id = -1;
-    bool valid() const { return id >= 0; }
 };
 
 bool hkey_less(const HKey& a, const HKey& b) {

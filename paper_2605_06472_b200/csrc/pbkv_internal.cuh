@@ -235,7 +235,8 @@ struct Context {
     DevBuf<unsigned long long> W;
     DevBuf<unsigned int> C;
     DevBuf<int> rank;
-    DevBuf<int> heads, listB, listS;
+    DevBuf<int> heads, listB, listS, listS2;
+    DevBuf<unsigned int> big;  // [2 * n]: (offset, count) of buckets sorted by rank counting
     DevBuf<unsigned long long> hist_w, part_w;
     DevBuf<unsigned int> hist_c, part_c, seg_off, seg_cnt, cursor;
     std::vector<unsigned long long> phase_ns;  // select-kernel phase timestamps of the last call

@@ -75,12 +75,14 @@ struct SelState {
     unsigned long long n_L[2];      // candidate list sizes by pass parity
     unsigned long long or_L[2][3], and_L[2][3];
     unsigned long long n_S;
+    unsigned int n_big;  // buckets of S sorted by chunked rank counting
     unsigned long long or_S[3], and_S[3];
     int n_pass, take_all, host_sort, s_is_heads;
     int cut_head, max_bucket;
     unsigned long long n_victims, freed;
     int shortfall, n_ts;
     unsigned long long ts[40];  // %globaltimer after each phase (diagnostics)
+    unsigned long long dbg[8];  // per-CTA maxima of phase work (diagnostics)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -227,6 +229,8 @@ struct SelArgs {
     int* heads;
     int* listB;
     int* listS;
+    int* listS2;        // S, sorted (rank-counting / warp sorts write here)
+    unsigned int* big;  // (offset, count) of the buckets with > 32 heads
     int* sorted;
     unsigned long long* start;
     int* victims;
@@ -447,6 +451,11 @@ __device__ __forceinline__ PickOut phase_pick(const SelArgs& a, unsigned long lo
             const int d = threadIdx.x * kPer + j;
             so[d] = off_sh[d];
             sc2[d] = d < r.bucket ? vc[j] : 0u;
+            if (d < r.bucket && vc[j] > 32u) {  // sorted by chunked rank counting
+                const unsigned int q = atomicAdd(&a.ss->n_big, 1u);
+                a.big[2 * q] = off_sh[d];
+                a.big[2 * q + 1] = vc[j];
+            }
         }
     }
     __syncthreads();
@@ -513,56 +522,9 @@ __device__ __forceinline__ bool sk_less(unsigned long long a0, unsigned long lon
     return av < bv;
 }
 
-// bitonic sort of full keys in shared memory, n = power of two
-__device__ __forceinline__ void bitonic_sort(unsigned long long* k0, unsigned long long* k1, int* val, int n) {
-    for (int k = 2; k <= n; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const bool up = (i & k) == 0;
-                    const bool gt = sk_less(k0[ixj], k1[ixj], val[ixj], k0[i], k1[i], val[i]);
-                    if (gt == up) {
-                        const unsigned long long t0 = k0[i], t1 = k1[i];
-                        const int tv = val[i];
-                        k0[i] = k0[ixj];
-                        k1[i] = k1[ixj];
-                        val[i] = val[ixj];
-                        k0[ixj] = t0;
-                        k1[ixj] = t1;
-                        val[ixj] = tv;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-// sort S[off, off+cnt) in place (one CTA)
-__device__ __forceinline__ void sort_bucket(const SelArgs& a, int* S, unsigned int off, unsigned int cnt,
-                                            unsigned long long* k0, unsigned long long* k1, int* val) {
-    int np = 2;
-    while (static_cast<unsigned int>(np) < cnt) np <<= 1;
-    for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        if (static_cast<unsigned int>(i) < cnt) {
-            const int x = __ldcg(&S[off + i]);
-            const Key2 k = load_key(a.keys, x);
-            k0[i] = k.w0;
-            k1[i] = k.w1;
-            val[i] = x;
-        } else {
-            val[i] = -1;
-        }
-    }
-    __syncthreads();
-    bitonic_sort(k0, k1, val, np);
-    for (int i = threadIdx.x; i < static_cast<int>(cnt); i += blockDim.x) S[off + i] = val[i];
-    __syncthreads();
-}
-
 // small bucket (<= 32 heads): one warp, rank = number of smaller keys
-__device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, int* S, unsigned int off, unsigned int cnt) {
+__device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S, int* S2, unsigned int off,
+                                                 unsigned int cnt) {
     const int lane = threadIdx.x & 31;
     const bool in = static_cast<unsigned int>(lane) < cnt;
     const int x = in ? __ldcg(&S[off + lane]) : -1;
@@ -575,8 +537,48 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, int* S, unsig
         const int bv = __shfl_sync(0xffffffffu, x, j);
         rank += sk_less(b0, b1, bv, k.w0, k.w1, x) ? 1 : 0;
     }
-    __syncwarp();
-    if (in) S[off + rank] = x;
+    if (in) S2[off + rank] = x;
+}
+
+// Buckets with > 32 heads: every element's rank is the number of smaller keys
+// in its bucket, counted from shared memory by 8 threads per element.  Tasks
+// are (bucket, chunk of 64 elements), spread over every CTA -- no barrier-
+// heavy single-CTA sort (a 1024-element bitonic took ~35 us in one CTA).
+constexpr int kRankChunk = 64;
+__device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, int* S2, unsigned int n_big,
+                                              unsigned long long* k0, unsigned long long* k1, int* val) {
+    unsigned int task = 0;
+    for (unsigned int b = 0; b < n_big; ++b) {
+        const unsigned int off = __ldcg(&a.big[2 * b]), cnt = __ldcg(&a.big[2 * b + 1]);
+        const unsigned int nch = (cnt + kRankChunk - 1) / kRankChunk;
+        // this CTA's chunks of bucket b: c with (task + c) % gridDim.x == blockIdx.x
+        unsigned int c = (blockIdx.x + gridDim.x - task % gridDim.x) % gridDim.x;
+        if (c < nch) {
+            __syncthreads();
+            for (unsigned int i = threadIdx.x; i < cnt; i += blockDim.x) {
+                const int x = __ldcg(&S[off + i]);
+                const Key2 k = load_key(a.keys, x);
+                k0[i] = k.w0;
+                k1[i] = k.w1;
+                val[i] = x;
+            }
+            __syncthreads();
+            for (; c < nch; c += gridDim.x) {
+                const unsigned int e = c * kRankChunk + threadIdx.x / 8, part = threadIdx.x % 8;
+                const bool in = e < cnt;
+                const unsigned long long a0 = in ? k0[e] : 0ull, a1 = in ? k1[e] : 0ull;
+                const int av = in ? val[e] : -1;
+                unsigned int r = 0;
+                if (in)
+                    for (unsigned int q = part; q < cnt; q += 8) r += sk_less(k0[q], k1[q], val[q], a0, a1, av) ? 1u : 0u;
+                r += __shfl_xor_sync(0xffffffffu, r, 1);
+                r += __shfl_xor_sync(0xffffffffu, r, 2);
+                r += __shfl_xor_sync(0xffffffffu, r, 4);
+                if (in && part == 0) S2[off + r] = av;
+            }
+        }
+        task += nch;
+    }
 }
 
 // every eligible node of a selected chain lands at start[rank(head)] + d
@@ -774,41 +776,66 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     (void)v0;
     (void)v1;
     (void)v2;
+    int* S2 = a.listS2;
     if (take_all) {
-        if (blockIdx.x == 0)
-            sort_bucket(a, S, 0, static_cast<unsigned int>(nS), sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
-    } else {
-        // large buckets: one CTA each; small ones: one warp each (no block barriers)
-        const int nb = n_pass * kBins;
-        for (int j = blockIdx.x; j < nb; j += gridDim.x) {
-            const unsigned int cnt = __ldcg(&a.seg_cnt[j]);
-            if (cnt <= 32u) continue;
-            sort_bucket(a, S, __ldcg(&a.seg_off[j]), cnt, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
+        if (tid == 0 && nS > 0) {  // the whole head list is one bucket
+            a.big[0] = 0u;
+            a.big[1] = static_cast<unsigned int>(nS);
         }
+        grid.sync();
+        rank_sort_big(a, S, S2, nS > 0 ? 1u : 0u, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
+    } else {
+        if (threadIdx.x == 0) sm.bc[3] = __ldcg(&ss->n_big);
+        __syncthreads();
+        const unsigned int n_big = static_cast<unsigned int>(sm.bc[3]);
+        rank_sort_big(a, S, S2, n_big, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
+        // small buckets: one warp each; singletons and the cut head are copied
+        const int nb = n_pass * kBins;
         const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
         const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(blockDim.x)) >> 5);
         for (int j = gwarp; j < nb; j += nwarps) {
             const unsigned int cnt = __ldcg(&a.seg_cnt[j]);
-            if (cnt < 2u || cnt > 32u) continue;
-            warp_sort_bucket(a, S, __ldcg(&a.seg_off[j]), cnt);
+            if (cnt == 0u || cnt > 32u) continue;
+            const unsigned int off = __ldcg(&a.seg_off[j]);
+            if (cnt == 1u) {
+                if ((threadIdx.x & 31) == 0) S2[off] = __ldcg(&S[off]);
+            } else {
+                warp_sort_bucket(a, S, S2, off, cnt);
+            }
         }
+        if (tid == 0) S2[nS - 1] = __ldcg(&S[nS - 1]);  // the cut head (its own bucket)
     }
     grid.sync();
     stamp(ss);
 
-    // ---- chain starts: exclusive scan of the chain sizes over sorted S (CTA 0) --------
-    if (blockIdx.x == 0) {
+    // ---- chain starts: start[p] = sum of the chain sizes before S2[p] ----------------
+    // every CTA scans its own slice of S2; the prefix before the slice is
+    // recomputed redundantly by each CTA (sum of C over S2[0, c0)), which for
+    // the sizes a decision selects is cheaper than a single-CTA scan
+    {
         using Scan = cub::BlockScan<unsigned long long, kPThreads>;
+        const bool spread = nS <= 65536ull;
+        const unsigned long long per = spread ? (nS + gridDim.x - 1) / gridDim.x : nS;
+        const unsigned long long c0 = spread ? blockIdx.x * per : 0ull;
+        const unsigned long long c1 = spread ? min(nS, c0 + per) : (blockIdx.x == 0 ? nS : 0ull);
         unsigned long long carry = 0;
-        for (unsigned long long c0 = 0; c0 < nS; c0 += static_cast<unsigned long long>(kPThreads) * kScanIPT) {
+        if (spread && c0 < c1) {
+            unsigned long long pre = 0;
+            for (unsigned long long i = threadIdx.x; i < c0; i += blockDim.x) pre += __ldcg(&a.C[__ldcg(&S2[i])]);
+            carry = block_reduce_bits(pre, SumOp(), sm.sh);
+            if (threadIdx.x == 0) sm.bc[2] = carry;
+            __syncthreads();
+            carry = sm.bc[2];
+        }
+        for (unsigned long long b0 = c0; b0 < c1; b0 += static_cast<unsigned long long>(kPThreads) * kScanIPT) {
             unsigned long long cnt[kScanIPT], local = 0;
             int hv[kScanIPT];
             for (int j = 0; j < kScanIPT; ++j) {
-                const unsigned long long pos = c0 + static_cast<unsigned long long>(threadIdx.x) * kScanIPT + j;
+                const unsigned long long pos = b0 + static_cast<unsigned long long>(threadIdx.x) * kScanIPT + j;
                 cnt[j] = 0;
                 hv[j] = -1;
-                if (pos < nS) {
-                    const int h = __ldcg(&S[pos]);
+                if (pos < c1) {
+                    const int h = __ldcg(&S2[pos]);
                     hv[j] = h;
                     a.rank[h] = static_cast<int>(pos);
                     cnt[j] = __ldcg(&a.C[h]);
@@ -820,10 +847,10 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             __syncthreads();
             excl += carry;
             for (int j = 0; j < kScanIPT; ++j) {
-                const unsigned long long pos = c0 + static_cast<unsigned long long>(threadIdx.x) * kScanIPT + j;
-                if (pos < nS) a.start[pos] = excl;
+                const unsigned long long pos = b0 + static_cast<unsigned long long>(threadIdx.x) * kScanIPT + j;
+                if (pos < c1) a.start[pos] = excl;
                 excl += cnt[j];
-                if (pos == nS - 1 && take_all) ss->cut_head = hv[j];
+                if (pos < c1 && pos == nS - 1 && take_all) ss->cut_head = hv[j];
             }
             carry += total;
         }
@@ -1012,6 +1039,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     a.heads = c.heads.p;
     a.listB = c.listB.p;
     a.listS = c.listS.p;
+    a.listS2 = c.listS2.p;
+    a.big = c.big.p;
     a.sorted = c.sorti_out.p;
     a.start = c.cnt.p;
     a.victims = c.vid_out.p;
@@ -1039,9 +1068,12 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     if (std::getenv("PBKV_DEBUG_SELECT"))
         std::fprintf(stderr,
                      "[pbkv select] n_heads=%llu total_tok=%llu take_all=%d host_sort=%d n_S=%llu n_pass=%d "
-                     "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d\n",
+                     "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
+                     "dbg(ns): sortCTA=%llu sortWarp=%llu chainstart=%llu maxbucket=%llu nbig=%llu eff=%llu "
+                     "chains=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
-                     hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid);
+                     hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->dbg[0],
+                     hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6]);
     if (hs->host_sort) {
         // ---- fallback: device-wide sort of the selected heads -----------------------------
         const std::int64_t nS = static_cast<std::int64_t>(hs->n_S);
