@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--needed-frac", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-decisions", type=int, default=2)
+    ap.add_argument("--no-pipeline", action="store_true", help="skip the config-2 predictor pipeline line")
     return ap.parse_args()
 
 
@@ -188,6 +189,61 @@ def run_reference(args, rank, world):
         "e2e": {"value": val, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def pipeline_c2(torch, dev, reps: int = 20):
+    """configs[1]: 10K-node tree x 256 workflows x K=4 -- stage 1 (the
+    predictor forward from prefill hidden states resident in HBM, H = 5120)
+    + stage 2 + stage 3 end to end, one decision per step; also the stage-1
+    forward alone at the config-3 batch (4096 workflows, K = 8)."""
+    import workloads as WL
+    from paper_2605_06472_b200._abi import POLICY_HE, SCORE_RECOMPUTE
+    from paper_2605_06472_b200.api import HostTree, Policy
+    from paper_2605_06472_b200.predictor import PredictorWeights, random_inputs
+
+    out = {}
+    for name, (n_nodes, n_wf, K) in (("c2", CONFIGS["c2"]), ("c3_predict", CONFIGS["c3"])):
+        t = HostTree()
+        t.synth(n_nodes=n_nodes, n_workflows=n_wf, agents=AGENTS, seed=777)
+        soa = t.export()
+        wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+        H = 5120
+        w = PredictorWeights.random(num_agents=AGENTS, horizon=K, text_dim=H)
+        off, pre, x = random_inputs(wf.size, AGENTS, H, max_prefix=64)
+        pol = Policy(num_agents=AGENTS, k=K, gamma=GAMMA)
+        pol.mirror(t)
+        pol.load_predictor(w, max_prefix=64)
+        xd = torch.from_numpy(x.view(np.int16)).to(dev)
+        used = int(soa.len[soa.tier == 0][1:].sum())
+        needed = max(1, used // 100)
+        locked_d = torch.zeros(1, dtype=torch.int32, device=dev)
+        victims_d = torch.empty(soa.n_nodes, dtype=torch.int32, device=dev)
+        res_d = torch.zeros(3, dtype=torch.int64, device=dev)
+        stream = torch.cuda.ExternalStream(pol.stream_handle(), device=dev)
+
+        def run(decide):
+            pol.predict(wf, off, pre, None, x_device_ptr=xd.data_ptr(), want_probs=False)
+            if decide:
+                pol.select_dev(POLICY_HE, SCORE_RECOMPUTE, needed, locked_d.data_ptr(), 0, victims_d.data_ptr(),
+                               soa.n_nodes, res_d.data_ptr())
+
+        decide = name == "c2"
+        for _ in range(3):
+            run(decide)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run(decide)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out[name] = {"nodes": soa.n_nodes, "workflows": int(wf.size), "K": K, "H": H,
+                     "ms_mean": statistics.mean(ts), "ms_p99": float(np.percentile(ts, 99)),
+                     "what": "predict + score + select (device-resident x)" if decide else "predict only"}
+    return out
 
 
 def shard_workload(cfg: str, rank: int, world: int, dist, torch, dev):
@@ -374,13 +430,16 @@ def main():
     # ---- per-stage split (separate pass: events between stages) ---------------------
     pol.set_timing(True)
     stage = np.zeros(5)
+    kern = np.zeros(2)
     n_stage = max(3, min(10, args.steps))
     for _ in range(n_stage):
         flush.fill_(1)
         torch.cuda.synchronize()
         step()
         stage += np.array(pol.timings())
+        kern += np.array(pol.kernel_timings())
     stage /= n_stage
+    kern /= n_stage
     select_phases = [round(x, 2) for x in pol.phase_times_us()]
     pol.set_timing(False)
 
@@ -425,9 +484,21 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     N, E = soa.n_nodes, soa.n_entries
     F = wf.size * K * (AGENTS + 2) * 8
-    alg_score = 41 * N + 12 * E + F  # fused score+key stage
-    score_ms = float(stage[0])
-    achieved = alg_score / (score_ms * 1e-3) / 1e9 if score_ms > 0 else None
+    # light Eq. 2 + key pass: per node acc_off 4 + flags 1 +
+    # last 8 + ever 4 read, score 8 + key 16 + eff 4 + sublock 4 + missing 1
+    # written; 12 B per access entry; the forecast rows + gs table once
+    alg_light = 50 * N + 12 * E + F
+    light_ms = float(kern[0])
+    achieved = alg_light / (light_ms * 1e-3) / 1e9 if light_ms > 0 else None
+    # selection: rank inputs 29 B + eff key 21 B per node
+    alg_sel = 50 * N
+    sel_ms = float(kern[1])
+    achieved_sel = alg_sel / (sel_ms * 1e-3) / 1e9 if sel_ms > 0 else None
+    traffic = {}
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        pass
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -452,10 +523,18 @@ def main():
         "stage_ms": {"score_keys": float(stage[0]), "select": float(stage[1]), "total": float(stage[4])},
         "select_phases_us": {"note": "lock, eff, weights, [hist+reduce, pick+compact] x passes, cut-head, "
                                      "sort, scatter, cut", "us": select_phases},
-        "roofline": {"bound": "hbm", "kernel": "score_light_kernel<true>+heavy_score_kernel (fused Eq.2 + keys)",
+        "roofline": {"bound": "hbm", "kernel": "score_light_kernel (Eq. 2 of every light node + stage-3 keys)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
-                     "alg_bytes_per_launch": alg_score},
+                     "frac": (achieved / hbm_peak) if achieved else None,
+                     "traffic": traffic.get("score_light_kernel"), "alg_bytes_per_launch": alg_light,
+                     "launch_ms": light_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "roofline_select": {"bound": "hbm", "kernel": "select_persistent_kernel (latency-bound: grid phases)",
+                            "achieved": achieved_sel, "peak": hbm_peak, "unit": "GB/s",
+                            "frac": (achieved_sel / hbm_peak) if achieved_sel else None,
+                            "traffic": traffic.get("select_persistent_kernel"), "alg_bytes_per_launch": alg_sel,
+                            "launch_ms": sel_ms},
+        "defer": dict(zip(("fast", "exact"), pol.defer_stats())),
+        "pipeline_c2": pipeline_c2(torch, dev) if not args.no_pipeline else None,
         "cpu_baseline": cpu,
         "e2e": {"value": total_nodes / (e2e * 1e-3), "unit": "nodes/s",
                 "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size + 4 * locked.size),

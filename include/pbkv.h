@@ -127,6 +127,10 @@ int pbkv_ctx_stream(pbkv_ctx* ctx, void** stream_out);     /* the ctx's cudaStre
  * the ctx stream): [0]=score [1]=keys+eff [2]=cut/sort [3]=prefetch [4]=total. */
 int pbkv_ctx_timings(pbkv_ctx* ctx, float* ms5);
 int pbkv_ctx_set_timing(pbkv_ctx* ctx, int enabled);
+/* Device time of the dominant kernels of the most recent timed selection
+ * (milliseconds, CUDA events on the ctx stream): [0] the light Eq. 2 + key
+ * pass (score_light_kernel), [1] the persistent selection kernel. */
+int pbkv_ctx_kernel_timings(pbkv_ctx* ctx, float* ms2);
 /* %globaltimer stamps (ns) taken by the selection kernel at its phase
  * boundaries during the most recent selection (diagnostics). */
 int pbkv_ctx_phase_times(pbkv_ctx* ctx, uint64_t* ns, int cap, int* n);

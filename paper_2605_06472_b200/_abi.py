@@ -184,6 +184,7 @@ def lib() -> C.CDLL:
         "pbkv_ctx_set_timing": ([vp, C.c_int], C.c_int),
         "pbkv_ctx_launches": ([vp, _i64p, _i64p], C.c_int),
         "pbkv_ctx_set_defer": ([vp, C.c_int], C.c_int),
+        "pbkv_ctx_kernel_timings": ([vp, C.POINTER(C.c_float)], C.c_int),
         "pbkv_ctx_defer_stats": ([vp, _i64p, _i64p], C.c_int),
         "pbkv_ctx_phase_times": ([vp, _u64p, C.c_int, C.POINTER(C.c_int)], C.c_int),
         "pbkv_mirror_full": ([vp, C.POINTER(TreeSoA)], C.c_int),

@@ -333,6 +333,12 @@ class Policy:
     def set_timing(self, on: bool) -> None:
         self._c(_abi.lib().pbkv_ctx_set_timing(self._h, 1 if on else 0))
 
+    def kernel_timings(self) -> list[float]:
+        """[light Eq. 2 pass ms, persistent selection kernel ms] of the last timed call."""
+        ms = (C.c_float * 2)()
+        self._c(_abi.lib().pbkv_ctx_kernel_timings(self._h, ms))
+        return [float(x) for x in ms]
+
     def set_defer(self, on: bool) -> None:
         """Heavy-node deferral in RECOMPUTE decisions (results identical)."""
         self._c(_abi.lib().pbkv_ctx_set_defer(self._h, 1 if on else 0))

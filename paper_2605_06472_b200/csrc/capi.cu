@@ -205,6 +205,10 @@ void record(Context& c, int i) {
 void finish_timing(Context& c, int last_ev) {
     if (!c.timing) return;
     PBKV_CUDA(cudaEventSynchronize(c.ev[last_ev]));
+    c.kernel_ms[0] = c.kernel_ms[1] = 0.f;
+    if (c.kev_light) cudaEventElapsedTime(&c.kernel_ms[0], c.kev[0], c.kev[1]);
+    if (c.kev_select) cudaEventElapsedTime(&c.kernel_ms[1], c.kev[2], c.kev[3]);
+    c.kev_light = c.kev_select = false;
     for (int i = 0; i < 5; ++i) c.last_ms[i] = 0.f;
     auto el = [&](int a, int b) {
         float ms = 0.f;
@@ -630,6 +634,7 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         PBKV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         PBKV_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         for (auto& e : c->ev) PBKV_CUDA(cudaEventCreate(&e));
+        for (auto& e : c->kev) PBKV_CUDA(cudaEventCreate(&e));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         c->selstate.reserve(sel_state_bytes());
@@ -654,6 +659,8 @@ int pbkv_ctx_destroy(pbkv_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
     for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->kev)
         if (e) cudaEventDestroy(e);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -705,6 +712,14 @@ int pbkv_ctx_launches(pbkv_ctx* c, int64_t* kernels, int64_t* lib_calls) {
         need(c, "null ctx");
         if (kernels) *kernels = c->launches;
         if (lib_calls) *lib_calls = c->lib_calls;
+    });
+}
+
+int pbkv_ctx_kernel_timings(pbkv_ctx* c, float* ms2) {
+    return api(c, [&] {
+        need(c && ms2, "null argument");
+        ms2[0] = c->kernel_ms[0];
+        ms2[1] = c->kernel_ms[1];
     });
 }
 

@@ -278,6 +278,11 @@ struct Context {
     bool timing = false;
     cudaEvent_t ev[6] = {};
     float last_ms[5] = {0, 0, 0, 0, 0};
+    // per-kernel events (timing mode): [0,1] around the light Eq. 2 pass,
+    // [2,3] around the persistent selection kernel
+    cudaEvent_t kev[4] = {};
+    bool kev_light = false, kev_select = false;
+    float kernel_ms[2] = {0, 0};
 };
 
 // ---- launchers (score.cu / select.cu / prefetch.cu) -------------------------------

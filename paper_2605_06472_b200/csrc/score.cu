@@ -115,6 +115,16 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
 template <bool kKeys>
 void launch_light(Context& c, const ScoreArgs& s, const KeyArgs& ka, int rm) {
     const unsigned int g = grid_cap(c.n, kLightThreads);
+    if (c.timing) {
+        PBKV_CUDA(cudaEventRecord(c.kev[0], c.stream));
+        c.kev_light = true;
+    }
+    struct After {
+        Context& c;
+        ~After() {
+            if (c.timing) cudaEventRecord(c.kev[1], c.stream);
+        }
+    } after{c};
     switch (c.K) {
         case 1: score_light_kernel<kKeys, 1><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;
         case 2: score_light_kernel<kKeys, 2><<<g, kLightThreads, 0, c.stream>>>(s, ka, c.n, rm); break;

@@ -545,11 +545,22 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S,
 // are (bucket, chunk of 64 elements), spread over every CTA -- no barrier-
 // heavy single-CTA sort (a 1024-element bitonic took ~35 us in one CTA).
 constexpr int kRankChunk = 64;
+constexpr int kBigSh = 512;  // bucket-list entries cached in shared memory
 __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, int* S2, unsigned int n_big,
                                               unsigned long long* k0, unsigned long long* k1, int* val) {
+    // the bucket list is read once into shared memory (a serial walk of L2
+    // loads per CTA cost ~1 us per bucket)
+    __shared__ unsigned int big_sh[2 * kBigSh];
+    const bool cached = n_big <= static_cast<unsigned int>(kBigSh);
+    if (cached) {
+        __syncthreads();
+        for (unsigned int i = threadIdx.x; i < 2 * n_big; i += blockDim.x) big_sh[i] = __ldcg(&a.big[i]);
+        __syncthreads();
+    }
     unsigned int task = 0;
     for (unsigned int b = 0; b < n_big; ++b) {
-        const unsigned int off = __ldcg(&a.big[2 * b]), cnt = __ldcg(&a.big[2 * b + 1]);
+        const unsigned int off = cached ? big_sh[2 * b] : __ldcg(&a.big[2 * b]);
+        const unsigned int cnt = cached ? big_sh[2 * b + 1] : __ldcg(&a.big[2 * b + 1]);
         const unsigned int nch = (cnt + kRankChunk - 1) / kRankChunk;
         // this CTA's chunks of bucket b: c with (task + c) % gridDim.x == blockIdx.x
         unsigned int c = (blockIdx.x + gridDim.x - task % gridDim.x) % gridDim.x;
@@ -821,7 +832,15 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         unsigned long long carry = 0;
         if (spread && c0 < c1) {
             unsigned long long pre = 0;
-            for (unsigned long long i = threadIdx.x; i < c0; i += blockDim.x) pre += __ldcg(&a.C[__ldcg(&S2[i])]);
+            // batches of 8 independent loads per thread (the prefix is L2-latency bound)
+            for (unsigned long long i0 = static_cast<unsigned long long>(threadIdx.x) * 8; i0 < c0;
+                 i0 += static_cast<unsigned long long>(blockDim.x) * 8) {
+                int hb[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) hb[q] = i0 + q < c0 ? __ldcg(&S2[i0 + q]) : -1;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pre += hb[q] >= 0 ? __ldcg(&a.C[hb[q]]) : 0u;
+            }
             carry = block_reduce_bits(pre, SumOp(), sm.sh);
             if (threadIdx.x == 0) sm.bc[2] = carry;
             __syncthreads();
@@ -1058,8 +1077,13 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     a.needed = needed;
     a.he_recompute = he_recompute ? 1 : 0;
     void* args[] = {&a};
+    if (c.timing) {
+        PBKV_CUDA(cudaEventRecord(c.kev[2], c.stream));
+        c.kev_select = true;
+    }
     PBKV_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(select_persistent_kernel), dim3(grid),
                                           dim3(kPThreads), args, sizeof(PersistSmem), c.stream));
+    if (c.timing) PBKV_CUDA(cudaEventRecord(c.kev[3], c.stream));
     ++c.launches;
     PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
     check_status(c);  // synchronises
