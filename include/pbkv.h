@@ -205,6 +205,29 @@ int pbkv_predictor_load(pbkv_ctx* ctx, const pbkv_predictor_cfg* cfg, const pbkv
 int pbkv_predict(pbkv_ctx* ctx, const int64_t* wf, int64_t n, const int64_t* prefix_off, const int32_t* prefix,
                  const uint16_t* x, int x_on_device, double* probs_out);
 
+/* ---- the reference predictors, batched and bit-exact ------------------------
+ * CallGraph::true_kstep_marginals (callgraph.hpp:136-186), MarkovModel::predict
+ * (predictor.hpp:79-118) and noisy_predict (predictor.hpp:25-35) propagate
+ * alive mass over context states in std::map order.  The model is given as a
+ * state table in that order (include/pbkv/flowkv_gpu.hpp builds it from a
+ * CallGraph or a MarkovModel): rows[s] = the state's one-step distribution
+ * over A agents + END, next[s][a] = the state reached by invoking agent a
+ * (-1: none).  One thread per workflow replays the reference's loops in
+ * binary64; the K-step forecasts become the workflows' resident forecasts. */
+typedef struct pbkv_fmodel {
+    int num_agents;       /* A, must equal the context's */
+    int64_t n_states;
+    const double* rows;   /* [n_states][A+1] */
+    const int32_t* next;  /* [n_states][A] */
+} pbkv_fmodel;
+
+int pbkv_fmodel_load(pbkv_ctx* ctx, const pbkv_fmodel* model);
+/* start_state[i]: table index of workflow i's current context; lambda < 0:
+ * no noise, else noisy_predict(base, lambda).  probs_out (host, nullable):
+ * n x horizon x (A+1). */
+int pbkv_forecast_propagate(pbkv_ctx* ctx, const int64_t* wf, int64_t n, const int32_t* start_state, int horizon,
+                            double lambda, double* probs_out);
+
 /* ---- stage 2: Score(c), Eq. 2 ---------------------------------------------- */
 /* multi_step_score(node_terms(...)) (scoring.hpp:49-75) for every node; nodes
  * without access entries score +0.0.  Raises EINVAL "missing forecast for

@@ -17,6 +17,9 @@
 //   select_victims_kvflow     policies.hpp:144-153     gpu::select_victims_kvflow
 //   plan_conservative_prefetch policies.hpp:220-224    gpu::plan_conservative_prefetch
 //   plan_aggressive_prefetch  policies.hpp:228-235     gpu::plan_aggressive_prefetch
+//   CallGraph::true_kstep_marginals callgraph.hpp:136  gpu::oracle_predict_batch
+//   noisy_predict             predictor.hpp:25-35      gpu::oracle_predict_batch(.., lambda)
+//   MarkovModel::predict      predictor.hpp:79-118     gpu::markov_predict_batch
 //
 // A caller switches by qualifying the call (or, for an unmodified
 // simulator.hpp, by the macro interposition shown in INTEGRATION.md).
@@ -43,11 +46,18 @@
 #include <tuple>
 #include <vector>
 
+#include <algorithm>
+#include <deque>
+
 #include "flowkv/cache.hpp"
 #include "flowkv/errors.hpp"
 #include "flowkv/forecast.hpp"
 #include "flowkv/policies.hpp"
 #include "flowkv/scoring.hpp"
+#ifdef PBKV_WITH_PREDICTORS  // callgraph.hpp / predictor.hpp need nlohmann json.hpp
+#include "flowkv/callgraph.hpp"
+#include "flowkv/predictor.hpp"
+#endif
 
 #include "../pbkv.h"
 
@@ -371,5 +381,154 @@ inline PrefetchPlan plan_aggressive_prefetch(const CacheTree& tree, const Foreca
     if (rho < 0.0 || rho > 1.0) throw ValidationError("rho must be in [0, 1]");
     return detail::plan(tree, forecasts, bandwidth, step_duration, rho);
 }
+
+#ifdef PBKV_WITH_PREDICTORS
+// ---- predictor slot (simulator.hpp:414-421): the reference predictors, batched ----
+// Both propagate alive mass over context states visited in std::map order.
+// The state table is built on the host from the model's public interface
+// (row_for_prefix / row_for) as the closure of the requested start contexts,
+// sorted in the reference's map order; the device replays the propagation
+// bit for bit (csrc/fmodel.cu).
+namespace detail {
+
+template <class Key>
+struct StateTable {
+    std::vector<Key> keys;  // sorted (the std::map order)
+    std::vector<double> rows;
+    std::vector<std::int32_t> next;
+
+    template <class RowFn, class NextFn>
+    void build(const std::vector<Key>& seeds, int A, RowFn&& row_of, NextFn&& next_of) {
+        std::map<Key, std::vector<double>> rowmap;
+        std::deque<Key> q(seeds.begin(), seeds.end());
+        while (!q.empty()) {
+            Key k = q.front();
+            q.pop_front();
+            if (rowmap.count(k)) continue;
+            std::vector<double> r = row_of(k);
+            for (int a = 0; a < A; ++a)
+                if (r[static_cast<std::size_t>(a)] > 0.0) q.push_back(next_of(k, a));
+            rowmap.emplace(std::move(k), std::move(r));
+        }
+        keys.clear();
+        rows.clear();
+        for (auto& [k, r] : rowmap) {
+            keys.push_back(k);
+            rows.insert(rows.end(), r.begin(), r.end());
+        }
+        next.assign(keys.size() * static_cast<std::size_t>(A), -1);
+        for (std::size_t s = 0; s < keys.size(); ++s)
+            for (int a = 0; a < A; ++a) {
+                if (!(rows[s * (A + 1) + static_cast<std::size_t>(a)] > 0.0)) continue;
+                auto it = std::lower_bound(keys.begin(), keys.end(), next_of(keys[s], a));
+                next[s * A + static_cast<std::size_t>(a)] = static_cast<std::int32_t>(it - keys.begin());
+            }
+    }
+    std::int32_t index(const Key& k) const {
+        auto it = std::lower_bound(keys.begin(), keys.end(), k);
+        return (it != keys.end() && *it == k) ? static_cast<std::int32_t>(it - keys.begin()) : -1;
+    }
+};
+
+inline std::vector<Forecast> propagate(int A, const std::vector<double>& rows, const std::vector<std::int32_t>& next,
+                                       const std::vector<std::int32_t>& start, int K, double lambda) {
+    pbkv_ctx* c = contexts().get(K, 0.7, A);
+    pbkv_fmodel m{A, static_cast<std::int64_t>(rows.size() / static_cast<std::size_t>(A + 1)), rows.data(),
+                  next.data()};
+    check(pbkv_fmodel_load(c, &m), c);
+    const std::size_t n = start.size();
+    std::vector<std::int64_t> wf(n);
+    for (std::size_t i = 0; i < n; ++i) wf[i] = -1 - static_cast<std::int64_t>(i);  // scratch forecast slots
+    std::vector<double> probs(n * static_cast<std::size_t>(K) * (A + 1));
+    check(pbkv_forecast_propagate(c, wf.data(), static_cast<std::int64_t>(n), start.data(), K, lambda, probs.data()),
+          c);
+    std::vector<Forecast> out;
+    out.reserve(n);
+    const std::size_t per = static_cast<std::size_t>(K) * (A + 1);
+    for (std::size_t i = 0; i < n; ++i)
+        out.emplace_back(K, A + 1, std::vector<double>(probs.begin() + i * per, probs.begin() + (i + 1) * per));
+    return out;
+}
+
+inline std::uint64_t encode_context(std::span<const AgentId> ctx) {  // callgraph.hpp:216-220
+    std::uint64_t key = 0;
+    for (AgentId a : ctx) key = key * 128 + static_cast<std::uint64_t>(a + 1);
+    return key;
+}
+
+inline std::vector<AgentId> decode_context(std::uint64_t key) {
+    std::vector<AgentId> ctx;
+    while (key != 0) {
+        ctx.push_back(static_cast<AgentId>(key % 128) - 1);
+        key /= 128;
+    }
+    std::reverse(ctx.begin(), ctx.end());
+    return ctx;
+}
+
+}  // namespace detail
+
+// CallGraph::true_kstep_marginals for a batch of prefixes (callgraph.hpp:136-186),
+// then noisy_predict (predictor.hpp:25-35) when lambda >= 0.
+inline std::vector<Forecast> oracle_predict_batch(const CallGraph& g, std::span<const std::vector<AgentId>> prefixes,
+                                                  int K, double lambda = -1.0) {
+    if (K < 1) throw ValidationError("horizon must be >= 1");
+    if (lambda >= 0.0 && lambda > 1.0) throw ValidationError("noise level must be in [0, 1]");
+    const int A = g.num_agents(), n_ctx = g.context_order();
+    auto ctx_of = [&](std::span<const AgentId> p) {
+        const std::size_t n = std::min<std::size_t>(p.size(), static_cast<std::size_t>(n_ctx));
+        return std::vector<AgentId>(p.end() - n, p.end());
+    };
+    std::vector<std::uint64_t> seeds;
+    for (const auto& p : prefixes) {
+        for (std::size_t i = 0; i + 1 < p.size(); ++i)
+            if (!g.edges().count({p[i], p[i + 1]})) throw ValidationError("prefix contains a non-edge transition");
+        if (!p.empty()) g.row_for_prefix(p);  // must be a known state (throws like the reference)
+        seeds.push_back(detail::encode_context(ctx_of(p)));
+    }
+    detail::StateTable<std::uint64_t> t;
+    t.build(
+        seeds, A,
+        [&](std::uint64_t k) {  // key 0: the entry state (empty context, entry row with END mass 0)
+            const std::vector<AgentId> ctx = detail::decode_context(k);
+            return g.row_for_prefix(ctx);
+        },
+        [&](std::uint64_t k, AgentId a) {
+            std::vector<AgentId> ns = detail::decode_context(k);
+            ns.push_back(a);
+            return detail::encode_context(ctx_of(ns));
+        });
+    std::vector<std::int32_t> start;
+    for (std::uint64_t k : seeds) start.push_back(t.index(k));
+    return detail::propagate(A, t.rows, t.next, start, K, lambda);
+}
+
+// MarkovModel::predict for a batch of prefixes (predictor.hpp:79-118).
+inline std::vector<Forecast> markov_predict_batch(const MarkovModel& m, std::span<const std::vector<AgentId>> prefixes,
+                                                  int K) {
+    if (K < 1) throw ValidationError("horizon must be >= 1");
+    const int A = m.num_agents(), order = m.order();
+    auto tail = [&](std::span<const AgentId> p) {
+        const std::size_t n = std::min<std::size_t>(p.size(), static_cast<std::size_t>(order));
+        return std::vector<AgentId>(p.end() - n, p.end());
+    };
+    std::vector<std::vector<AgentId>> seeds;
+    for (const auto& p : prefixes) {
+        if (p.empty()) throw ValidationError("markov prediction needs a non-empty prefix");
+        seeds.push_back(tail(p));
+    }
+    detail::StateTable<std::vector<AgentId>> t;
+    t.build(
+        seeds, A, [&](const std::vector<AgentId>& k) { return m.row_for(k); },
+        [&](const std::vector<AgentId>& k, AgentId a) {
+            std::vector<AgentId> ns = k;
+            ns.push_back(a);
+            return tail(ns);
+        });
+    std::vector<std::int32_t> start;
+    for (const auto& k : seeds) start.push_back(t.index(k));
+    return detail::propagate(A, t.rows, t.next, start, K, -1.0);
+}
+#endif  // PBKV_WITH_PREDICTORS
 
 }  // namespace flowkv::gpu

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpbkv.so")
 
-SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu", "predict.cu", "shard.cu"]
+SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu", "predict.cu", "shard.cu", "fmodel.cu"]
 HEADERS = [
     "pbkv_internal.cuh",
     "common.cuh",

@@ -188,6 +188,9 @@ void check_status(Context& c) {
         case kErrKvflowMissing:
             msg = kvflow_message(c, s.node);
             break;
+        case kErrModelState:
+            msg = "prefix reaches a state with no kernel row";
+            break;
         default:
             msg = "device-side validation failed";
     }
@@ -1126,6 +1129,58 @@ int pbkv_merge_cut(pbkv_ctx* c, const pbkv_cand* runs_dev, const int64_t* run_st
         shard_merge_cut(*c, runs_dev, c->run_start.p, c->run_len.p, n_runs, mx, total, c->merged.p, needed,
                         victims_dev, reinterpret_cast<long long*>(result_dev));
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- reference forecasters (oracle / Markov / noisy) --------------------------------
+int pbkv_fmodel_load(pbkv_ctx* c, const pbkv_fmodel* m) {
+    return api(c, [&] {
+        need(c && m, "null argument");
+        if (m->num_agents != c->A) invalid("model agent count does not match the context's");
+        need(m->n_states >= 1 && m->n_states < (1ll << 24), "model state count out of range");
+        need(m->rows && m->next, "model arrays missing");
+        const std::size_t S = static_cast<std::size_t>(m->n_states), V1 = static_cast<std::size_t>(c->V1);
+        for (std::size_t i = 0; i < S * static_cast<std::size_t>(c->A); ++i)
+            need(m->next[i] >= -1 && m->next[i] < m->n_states, "model next-state index out of range");
+        set_device(*c);
+        c->fm_rows.reserve(S * V1);
+        c->fm_next.reserve(S * static_cast<std::size_t>(c->A));
+        PBKV_CUDA(cudaMemcpyAsync(c->fm_rows.p, m->rows, S * V1 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        PBKV_CUDA(cudaMemcpyAsync(c->fm_next.p, m->next, S * c->A * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        c->fm_states = m->n_states;
+    });
+}
+
+int pbkv_forecast_propagate(pbkv_ctx* c, const int64_t* wf, int64_t n, const int32_t* start_state, int horizon,
+                            double lambda, double* probs_out) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        if (c->fm_states < 1) throw ApiError(PBKV_EARG, "no forecaster model loaded (pbkv_fmodel_load)");
+        if (horizon < 1) invalid("horizon must be >= 1");
+        if (lambda >= 0.0 && lambda > 1.0) invalid("noise level must be in [0, 1]");
+        if (n == 0) return;
+        need(wf && start_state, "null argument");
+        set_device(*c);
+        std::vector<long long> slots(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) slots[static_cast<std::size_t>(i)] = slot_for(*c, wf[i]);
+        const std::size_t per = static_cast<std::size_t>(horizon) * c->V1;
+        c->fstage.reserve(static_cast<std::size_t>(n) * per);
+        c->fstage_slot.reserve(static_cast<std::size_t>(n));
+        c->fm_start.reserve(static_cast<std::size_t>(n));
+        cudaStream_t st = c->stream;
+        PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots.data(), slots.size() * sizeof(long long),
+                                  cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c->fm_start.p, start_state, static_cast<std::size_t>(n) * sizeof(int),
+                                  cudaMemcpyHostToDevice, st));
+        reset_status(*c);
+        launch_propagate(*c, c->fm_start.p, n, horizon, lambda < 0.0 ? -1.0 : lambda);
+        check_status(*c);  // a propagation error precedes the Forecast checks
+        launch_forecast_prepare(*c, c->fstage.p, c->fstage_slot.p, n, horizon);
+        if (probs_out)
+            PBKV_CUDA(cudaMemcpyAsync(probs_out, c->fstage.p, static_cast<std::size_t>(n) * per * sizeof(double),
+                                      cudaMemcpyDeviceToHost, st));
+        check_status(*c);
     });
 }
 

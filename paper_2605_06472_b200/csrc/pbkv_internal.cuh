@@ -50,6 +50,7 @@ enum : int {
     kErrForecastNegative = 4,
     kErrForecastSum = 5,
     kErrKvflowMissing = 6,
+    kErrModelState = 7,
 };
 
 struct ApiError : std::runtime_error {
@@ -266,6 +267,11 @@ struct Context {
     DevBuf<unsigned int> spine_miss;
     DevBuf<pbkv_cand> merged;
 
+    // ---- forward-propagation forecaster (fmodel.cu) ----------------------------------
+    DevBuf<double> fm_rows, fm_mass;
+    DevBuf<int> fm_next, fm_start;
+    std::int64_t fm_states = 0;
+
     // ---- stage-1 predictor (predict.cu) -----------------------------------------
     std::shared_ptr<PredictorState> pred;
     DevBuf<int> pre_off, pre;
@@ -321,6 +327,7 @@ void shard_spine_products(Context& c, const long long* base_dev, long long max_l
 void shard_merge_cut(Context& c, const pbkv_cand* src, const long long* run_start_dev, const long long* run_len_dev,
                      int n_runs, long long max_run, long long total, pbkv_cand* merged, long long needed,
                      int* victims, long long* result);
+void launch_propagate(Context& c, const int* start_dev, std::int64_t n, int H, double lambda);
 void reset_status(Context& c);
 void check_status(Context& c);  // syncs and throws on a device-side error
 

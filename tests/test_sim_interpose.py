@@ -60,3 +60,18 @@ def test_gpu_simulator_matches_reference(gpu, scen, cell, seeds):
     assert len(got) == len(want) > 0
     for g, w in zip(got, want):
         assert g == w, f"GPU-driven simulator diverged from the reference:\n gpu {g}\n ref {w}"
+
+
+FPARITY = os.path.join(ROOT, "oracle", "_ref", "forecast_parity")
+
+
+@pytest.mark.gpu
+def test_reference_predictors_bit_exact_on_gpu(gpu):
+    """CallGraph::true_kstep_marginals, noisy_predict and MarkovModel::predict
+    (orders 1-3) vs the batched GPU forecaster (csrc/fmodel.cu), on every
+    bundled call graph: all probabilities bit-identical."""
+    if not os.path.exists(FPARITY):
+        pytest.fail("oracle/_ref/forecast_parity missing: build with `make -C oracle sim` where /root/reference exists")
+    r = subprocess.run([FPARITY, os.path.join(SCEN, "graphs")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "mismatches=0" in r.stdout.splitlines()[-1]
