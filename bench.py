@@ -162,30 +162,74 @@ def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: 
     return {"n_nodes": soa.n_nodes, "times": times, "build_s": build_s, "n_victims": len(sel.victims)}
 
 
+def reference_threads() -> int:
+    """Host threads for the reference arm: every core, capped so that one
+    C3 tree per thread (~0.5 GB resident) fits comfortably."""
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+
+        n = min(n, max(1, int(psutil.virtual_memory().available // (1 << 30)) // 2))
+    except Exception:
+        pass
+    return max(1, min(n, int(os.environ.get("PBKV_REF_THREADS", "32"))))
+
+
 def run_reference(args, rank, world):
+    """The reference's own CPU policy code (oracle/_ref, the unmodified
+    headers) on the same workload.  The reference is single-threaded per
+    decision; its scenario runner parallelises independent
+    simulations over a thread pool (scenario.hpp:291-301), so the arm runs
+    one independent decision stream per host thread, each on its own tree,
+    and reports the aggregate nodes/s."""
     if rank != 0:
         return
+    import threading
+
     n_nodes, n_wf, K = CONFIGS[args.config]
     steps = max(1, args.steps)
     warm = max(0, min(args.warmup, 1))
-    r = cpu_reference_decisions(args.config, args.needed_frac, warm + steps)
-    if r is None:
+    T = reference_threads()
+    results = [None] * T
+
+    def worker(i):
+        results[i] = cpu_reference_decisions(args.config, args.needed_frac, warm + steps)
+
+    # one stream alone first, then T concurrent streams; the arm reports the
+    # better aggregate (the reference's allocator-heavy maps can scale badly)
+    single = cpu_reference_decisions(args.config, args.needed_frac, warm + steps)
+    if single is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libflowkv_ref.so not built"}))
         return
-    times = r["times"][warm:]
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(T)] if T > 1 else []
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    one = single["n_nodes"] / statistics.mean(single["times"][warm:])
+    many = 0.0
+    if T > 1 and all(r is not None for r in results):
+        many = sum(rr["n_nodes"] / statistics.mean(rr["times"][warm:]) for rr in results)
+    if many > one:
+        val, times = many, [x for rr in results for x in rr["times"][warm:]]
+    else:
+        val, times, T = one, single["times"][warm:], 1
+    r = single
     ms = 1000.0 * statistics.mean(times)
-    val = r["n_nodes"] / statistics.mean(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "nodes/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {n_nodes} nodes x {n_wf} workflows x K={K}, 30% retired, "
                                f"HE select at {args.needed_frac:.2%} need",
-                   "parallelism": "cpu-1thread"},
+                   "parallelism": f"cpu x{T} threads (independent decision streams)"},
         "p99_decision_ms": 1000.0 * float(np.percentile(times, 99)),
-        "cpu_baseline": {"value": val, "unit": "nodes/s", "cores": 1, "kind": "reference",
-                         "sample": f"{steps} decisions (refresh_nodes over all nodes + select_victims_hierarchical)"
-                                   f" on the {args.config} tree; reference is single-threaded (SPEC.md:235)"},
+        "cpu_baseline": {"value": val, "unit": "nodes/s", "cores": T, "kind": "reference",
+                         "sample": f"{T} threads x {steps} decisions (refresh_nodes over all nodes + "
+                                   f"select_victims_hierarchical), one tree per thread; single-thread mean "
+                                   f"{ms:.1f} ms/decision; wall {wall:.1f} s"},
         "e2e": {"value": val, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
