@@ -276,28 +276,48 @@ __device__ __forceinline__ void phase_lock(const SelArgs& a, std::int64_t tid, s
 // larger key (its holder carries it further), so eff ends as the exact
 // subtree maximum
 __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
-    for (std::int64_t i = tid; i < a.n_nodes; i += nthr) {
-        const int n = static_cast<int>(i);
-        if (n == 0 || (a.flags[n] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
-        const Key2 km = load_key(a.keys, n);
-        int p = a.parent[n];
-        while (p > 0) {
-            // plain (L2) read first: an atomic read of the hot top-of-tree words
-            // serialises every walker in one L2 slice; CAS only when we would win
-            int cur = __ldcg(&a.eff[p]);
-            bool advanced = false;
-            for (;;) {
-                const Key2 kc = load_key(a.keys, cur);
-                if (!key_less(kc, cur, km, n)) break;
-                const int old = atomicCAS(&a.eff[p], cur, n);
-                if (old == cur) {
-                    advanced = true;
-                    break;
-                }
-                cur = old;
+    // kWalk walkers per thread advance in lockstep, so each round issues the
+    // loads of all of them together: the walk is a chain of dependent L2
+    // round trips (eff[p] -> key[cur] -> CAS -> parent), not bandwidth
+    constexpr int kWalk = 4;
+    for (std::int64_t base = tid; base < a.n_nodes; base += kWalk * nthr) {
+        int n[kWalk], p[kWalk];
+        Key2 km[kWalk];
+        bool act[kWalk];
+#pragma unroll
+        for (int j = 0; j < kWalk; ++j) {
+            const std::int64_t i = base + j * nthr;
+            n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
+            act[j] = i < a.n_nodes && n[j] != 0 && (a.flags[n[j]] & kFlagTierMask) == PBKV_TIER_DEVICE;
+            p[j] = act[j] ? a.parent[n[j]] : 0;
+            km[j] = act[j] ? load_key(a.keys, n[j]) : Key2{0, 0};
+            act[j] = act[j] && p[j] > 0;
+        }
+        for (;;) {
+            bool any = false;
+            int cur[kWalk];
+#pragma unroll
+            for (int j = 0; j < kWalk; ++j) {
+                // plain (L2) read first; CAS only when we would win
+                cur[j] = act[j] ? __ldcg(&a.eff[p[j]]) : 0;
+                any = any || act[j];
             }
-            if (!advanced) break;
-            p = a.parent[p];
+            if (!any) break;
+            Key2 kc[kWalk];
+#pragma unroll
+            for (int j = 0; j < kWalk; ++j) kc[j] = act[j] ? load_key(a.keys, cur[j]) : Key2{0, 0};
+#pragma unroll
+            for (int j = 0; j < kWalk; ++j) {
+                if (!act[j]) continue;
+                if (!key_less(kc[j], cur[j], km[j], n[j])) {  // a larger key holds p: its holder carries it
+                    act[j] = false;
+                    continue;
+                }
+                if (atomicCAS(&a.eff[p[j]], cur[j], n[j]) == cur[j]) {
+                    p[j] = a.parent[p[j]];
+                    act[j] = p[j] > 0;
+                }  // else: lost a race, re-read eff[p] next round
+            }
         }
     }
 }
@@ -306,45 +326,112 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
 // eligible ancestors with the same eff -- for its token weight W and size C;
 // head list, eligible tokens, OR/AND of the head keys (first radix pass)
 __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh) {
+    // every thread classifies kBatch nodes (independent loads together), the
+    // CTA appends all of its heads with one atomic, then the heads walk their
+    // chains in lockstep
+    constexpr int kBatch = 4;
     SelState* ss = a.ss;
     unsigned long long tok = 0;
     unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes; base += stride) {
-        const std::int64_t i = base + threadIdx.x;
-        const int n = static_cast<int>(i);
-        bool head = false;
-        if (i < a.n_nodes && n != 0 && (a.flags[n] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
-            !__ldcg(&a.sublock[n])) {
-            const std::uint8_t ms = a.missing[n];
-            if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n);
-            if (a.he_recompute && ms && !(a.flags[n] & kFlagRetired))
-                set_error(a.st, PBKV_EINVAL, kErrMissingForecast, n);
-            head = __ldcg(&a.eff[n]) == n;
+    const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
+         base += kBatch * nthr) {
+        int n[kBatch];
+        bool head[kBatch];
+        unsigned int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const std::int64_t i = base + threadIdx.x + j * nthr;
+            n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
+            head[j] = i < a.n_nodes && n[j] != 0 &&
+                      (a.flags[n[j]] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
+                      !__ldcg(&a.sublock[n[j]]);
         }
-        const long long slot = block_append(&ss->n_L[0], head, reinterpret_cast<unsigned int*>(sh), sh + 31);
-        if (head) {
-            unsigned long long w = 0;
-            unsigned int c = 0;
-            int p = n;
-            do {
-                w += static_cast<unsigned long long>(a.len[p]);
-                ++c;
-                p = a.parent[p];
-            } while (p > 0 && !(a.flags[p] & kFlagOutOfOrder) && !__ldcg(&a.sublock[p]) && __ldcg(&a.eff[p]) == n);
-            a.W[n] = w;
-            a.C[n] = c;
-            a.rank[n] = -1;
-            tok += w;
-            a.heads[slot] = n;
-            const Key2 k = load_key(a.keys, n);
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (!head[j]) continue;
+            const std::uint8_t ms = a.missing[n[j]];
+            if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n[j]);
+            if (a.he_recompute && ms && !(a.flags[n[j]] & kFlagRetired))
+                set_error(a.st, PBKV_EINVAL, kErrMissingForecast, n[j]);
+            head[j] = __ldcg(&a.eff[n[j]]) == n[j];
+            cnt += head[j] ? 1u : 0u;
+        }
+        // CTA-wide exclusive offsets of the heads, one global atomic per CTA
+        unsigned int* wcount = reinterpret_cast<unsigned int*>(sh);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        unsigned int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wcount[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned int sum = 0;
+            for (int w = 0; w < nw; ++w) {
+                const unsigned int c = wcount[w];
+                wcount[w] = sum;
+                sum += c;
+            }
+            sh[31] = sum ? atomicAdd(&ss->n_L[0], static_cast<unsigned long long>(sum)) : 0ull;
+        }
+        __syncthreads();
+        unsigned long long slot = sh[31] + wcount[warp] + (incl - cnt);
+        __syncthreads();
+        // chains: walk up while the parent is eligible with the same eff
+        unsigned long long w[kBatch];
+        unsigned int c[kBatch];
+        int p[kBatch];
+        bool act[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            w[j] = 0;
+            c[j] = 0;
+            p[j] = n[j];
+            act[j] = head[j];
+        }
+        for (;;) {
+            bool any = false;
+            int q[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (!act[j]) continue;
+                any = true;
+                w[j] += static_cast<unsigned long long>(a.len[p[j]]);
+                ++c[j];
+                q[j] = a.parent[p[j]];
+            }
+            if (!any) break;
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (!act[j]) continue;
+                const int pp = q[j];
+                act[j] = pp > 0 && !(a.flags[pp] & kFlagOutOfOrder) && !__ldcg(&a.sublock[pp]) &&
+                         __ldcg(&a.eff[pp]) == n[j];
+                p[j] = pp;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (!head[j]) continue;
+            const int h = n[j];
+            a.W[h] = w[j];
+            a.C[h] = c[j];
+            a.rank[h] = -1;
+            tok += w[j];
+            a.heads[slot++] = h;
+            const Key2 k = load_key(a.keys, h);
             for (int wd = 0; wd < 3; ++wd) {
-                const unsigned long long x = key_word(k, n, wd);
+                const unsigned long long x = key_word(k, h, wd);
                 or3[wd] |= x;
                 and3[wd] &= x;
             }
         }
     }
+    (void)tid;
     const unsigned long long blk = block_reduce_bits(tok, SumOp(), sh);
     if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
     flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
