@@ -305,10 +305,18 @@ class ShardedPolicy:
         self.spine_out = torch.zeros(max(1, shard.spine.n) * SPINE_DTYPE.itemsize, dtype=torch.uint8,
                                      device=self.dev)
         self.result = torch.zeros(3, dtype=torch.int64, device=self.dev)
-        self.gid_of = {int(l): int(gg) for l, gg in enumerate(shard.gids.tolist())} if n < 200000 else None
+        self.pmax = None  # max spine-product count over ranks (fixed per mirrored tree)
+
+    def local_ids(self, gids) -> np.ndarray:
+        """Local ids of the given global ids that this shard holds."""
+        g = np.asarray(sorted(set(int(x) for x in gids)), dtype=np.int64)
+        pos = np.searchsorted(self.shard.gids, g)
+        ok = (pos < self.shard.gids.size) & (self.shard.gids[np.minimum(pos, self.shard.gids.size - 1)] == g)
+        return pos[ok].astype(np.int32)
 
     # -- step 1: local selection -----------------------------------------------------------
-    def local_select(self, policy: int, score_mode: int, needed: int, locked_local_dev, n_locked: int):
+    def local_select(self, policy: int, score_mode: int, needed: int, locked_local_dev, n_locked: int,
+                     want_count: bool = True):
         L = _abi.lib()
         rc = L.pbkv_shard_select(self.pol.handle, int(policy), int(score_mode), int(needed),
                                  C.cast(C.c_void_p(locked_local_dev or None), C.POINTER(C.c_int32)), int(n_locked),
@@ -317,6 +325,8 @@ class ShardedPolicy:
                                  C.cast(C.c_void_p(self.spine_out.data_ptr()), C.POINTER(SpineInfoC)),
                                  C.cast(C.c_void_p(self.result.data_ptr()), C.POINTER(C.c_int64)))
         self.pol._c(rc)
+        if not want_count:
+            return None, self.spine_out[: self.shard.spine.n * SPINE_DTYPE.itemsize]
         n_cand = int(self.result[0].item())
         return self.cand[: n_cand * CAND_DTYPE.itemsize], self.spine_out[: self.shard.spine.n * SPINE_DTYPE.itemsize]
 
@@ -367,6 +377,9 @@ def global_select(ranks: list[ShardedPolicy] | ShardedPolicy, policy: int, score
 
     if policy == POLICY_KVFLOW:
         raise ValueError("kvflow is not supported on a sharded tree")
+    if dist is not None:
+        return _global_select_dist(ranks if not isinstance(ranks, list) else ranks[0], policy, score_mode, needed,
+                                   locked_gids, dist, world)
     local = ranks if isinstance(ranks, list) else [ranks]
     sp = local[0].shard.spine
     locked_set = set(int(x) for x in locked_gids)
@@ -421,4 +434,87 @@ def global_select(ranks: list[ShardedPolicy] | ShardedPolicy, policy: int, score
                                                                                      dtype=torch.uint8,
                                                                                      device=me.dev)
     v, freed, sf = me.merge_cut(buf, [int(s) for s in starts], lens, needed)
+    return v.cpu().numpy().tolist(), freed, sf
+
+
+def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed: int, locked_gids, dist,
+                        world: int):
+    """The per-rank decision with two collectives: (1) one all-gather of a
+    fixed-size header [candidate count | spine reports | spine product counts
+    | spine products padded to the largest rank's], (2) one all-gather of the
+    candidate records padded to the largest count.  Everything else is local."""
+    import torch
+
+    sp = rp.shard.spine
+    dev = rp.dev
+    locked_set = set(int(x) for x in locked_gids)
+    loc = rp.local_ids(locked_set)
+    ld = torch.from_numpy(loc if loc.size else np.zeros(1, np.int32)).to(dev)
+    _, rep = rp.local_select(policy, score_mode, needed, ld.data_ptr(), loc.size, want_count=False)
+    he_rc = policy == POLICY_HE and score_mode == SCORE_RECOMPUTE and sp.n > 0
+    if he_rc:
+        prod, pcnt = rp.spine_products()
+        if rp.pmax is None:
+            t = torch.tensor([prod.numel()], dtype=torch.int64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            rp.pmax = int(t.item())
+        pad = torch.zeros(rp.pmax, dtype=torch.float64, device=dev)
+        pad[: prod.numel()] = prod
+        pcnt_t = torch.from_numpy(np.ascontiguousarray(pcnt, dtype=np.int64)).to(dev)
+    else:
+        pad = torch.zeros(0, dtype=torch.float64, device=dev)
+        pcnt_t = torch.zeros(sp.n, dtype=torch.int64, device=dev)
+    head = torch.cat([rp.result[:1].view(torch.uint8), rep.reshape(-1), pcnt_t.view(torch.uint8),
+                      pad.view(torch.uint8)])
+    hdr = torch.empty(world * head.numel(), dtype=torch.uint8, device=dev)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(hdr, head)
+    else:
+        parts = [torch.zeros(head.numel(), dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, head.cpu())
+        hdr.copy_(torch.cat(parts))
+    hdr = hdr.view(world, head.numel())
+    nrep = sp.n * SPINE_DTYPE.itemsize
+    meta = hdr[:, : 8 + nrep + 8 * sp.n].cpu().numpy()  # counts + reports + product counts (small)
+    counts = meta[:, :8].copy().view(np.int64)[:, 0]
+    rep_all = np.stack([np.frombuffer(meta[r, 8: 8 + nrep].tobytes(), dtype=SPINE_DTYPE) for r in range(world)]) \
+        if sp.n else np.zeros((world, 0), SPINE_DTYPE)
+    cnt_all = meta[:, 8 + nrep:].copy().view(np.int64) if sp.n else np.zeros((world, 0), np.int64)
+    # (2) candidate records, padded to the largest count
+    mx = int(counts.max()) if counts.size else 0
+    rec = CAND_DTYPE.itemsize
+    if mx:
+        mine = torch.zeros(mx * rec, dtype=torch.uint8, device=dev)
+        n_me = int(counts[rp.shard.rank])
+        mine[: n_me * rec] = rp.cand[: n_me * rec]
+        allc = torch.empty(world * mx * rec, dtype=torch.uint8, device=dev)
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(allc, mine)
+        else:
+            parts = [torch.zeros(mx * rec, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, mine.cpu())
+            allc.copy_(torch.cat(parts))
+    else:
+        allc = torch.zeros(rec, dtype=torch.uint8, device=dev)
+    # spine scores: exact chains over every rank's products, rank (= WorkflowId) order
+    if he_rc:
+        prods = hdr[:, 8 + nrep + 8 * sp.n:].reshape(world, -1).view(torch.float64)
+        pieces, offs = [], [0]
+        for j in range(sp.n):
+            for r in range(world):
+                b = int(cnt_all[r, :j].sum())
+                pieces.append(prods[r, b: b + int(cnt_all[r, j])])
+            offs.append(offs[-1] + int(cnt_all[:, j].sum()))
+        x = torch.cat(pieces) if pieces else torch.zeros(1, dtype=torch.float64, device=dev)
+        scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))
+    else:
+        scores = sp.score
+    srec = spine_records(sp, rep_all, scores, policy, locked_set)
+    starts = [r * mx for r in range(world)] + [world * mx]
+    lens = [int(c) for c in counts] + [int(srec.size)]
+    buf = torch.cat([allc[: world * mx * rec] if mx else allc[:0],
+                     torch.from_numpy(srec.view(np.uint8).copy()).to(dev)])
+    if buf.numel() == 0:
+        buf = torch.zeros(rec, dtype=torch.uint8, device=dev)
+    v, freed, sf = rp.merge_cut(buf, starts, lens, needed)
     return v.cpu().numpy().tolist(), freed, sf

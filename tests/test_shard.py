@@ -204,3 +204,66 @@ def test_chain_sum_bit_exact(gpu):
         for v in s.tolist():
             t += v
         assert got[i] == t, f"segment {i}: {got[i]!r} != {t!r}"
+
+
+def _dist_gpu_worker(rank, world, port, q):
+    """world ranks on cuda:0 (gloo exchange): the per-rank decision path of
+    global_select(dist=...) against the single-context selection."""
+    import sys
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_06472_b200.api import Policy
+
+        soa = synth(n=12000, w=256, seed=11)
+        rng = np.random.default_rng(11)
+        K, A = 4, 16
+        wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+        Pf = WL.random_forecasts(rng, wf.size, K, A + 1)
+        shards = S.partition(soa, world)
+        me = S.ShardedPolicy(shards[rank], num_agents=A, k=K, gamma=0.7)
+        mine = (wf >= shards[rank].wf_lo) & (wf < shards[rank].wf_hi)
+        me.pol.put_forecasts(wf[mine], Pf[mine])
+        used = int(soa.len[soa.tier == 0][1:].sum())
+        locked = WL.pinned_paths(soa, rng, 0.02)
+        out = []
+        for frac in (0.01, 0.3, 2.0):
+            needed = max(1, int(frac * used))
+            out.append(S.global_select(me, POLICY_HE, SCORE_RECOMPUTE, needed, locked, dist=dist, world=world))
+        want = None
+        if rank == 0:
+            single = Policy(num_agents=A, k=K, gamma=0.7)
+            single.mirror(soa)
+            single.put_forecasts(wf, Pf)
+            want = []
+            for frac in (0.01, 0.3, 2.0):
+                needed = max(1, int(frac * used))
+                r = single.select_victims(POLICY_HE, needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+                want.append((r.victims, r.freed, r.shortfall))
+        q.put((rank, out, want))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, "ERR " + traceback.format_exc(), None))
+        sys.stderr.write(str(e))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_dist_exchange_two_ranks_equals_single(gpu):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 1000
+    procs = [ctx.Process(target=_dist_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert not isinstance(r[1], str), r[1]
+    want = res[0][2]
+    for rank, out, _ in res:
+        assert [tuple(o) for o in out] == [tuple(w) for w in want], f"rank {rank} differs from single"
