@@ -496,25 +496,55 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
             allc.copy_(torch.cat(parts))
     else:
         allc = torch.zeros(rec, dtype=torch.uint8, device=dev)
-    # spine scores: exact chains over every rank's products, rank (= WorkflowId) order
-    if he_rc:
-        prods = hdr[:, 8 + nrep + 8 * sp.n:].reshape(world, -1).view(torch.float64)
-        pieces, offs = [], [0]
-        for j in range(sp.n):
-            for r in range(world):
-                b = int(cnt_all[r, :j].sum())
-                pieces.append(prods[r, b: b + int(cnt_all[r, j])])
-            offs.append(offs[-1] + int(cnt_all[:, j].sum()))
-        x = torch.cat(pieces) if pieces else torch.zeros(1, dtype=torch.float64, device=dev)
-        scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))
-    else:
-        scores = sp.score
-    srec = spine_records(sp, rep_all, scores, policy, locked_set)
     starts = [r * mx for r in range(world)] + [world * mx]
-    lens = [int(c) for c in counts] + [int(srec.size)]
-    buf = torch.cat([allc[: world * mx * rec] if mx else allc[:0],
-                     torch.from_numpy(srec.view(np.uint8).copy()).to(dev)])
-    if buf.numel() == 0:
-        buf = torch.zeros(rec, dtype=torch.uint8, device=dev)
-    v, freed, sf = rp.merge_cut(buf, starts, lens, needed)
+    n_cand = int(counts.sum())
+
+    def cut_with(srec):
+        lens = [int(c) for c in counts] + [int(srec.size)]
+        buf = torch.cat([allc[: world * mx * rec] if mx else allc[:0],
+                         torch.from_numpy(srec.view(np.uint8).copy()).to(dev)])
+        if buf.numel() == 0:
+            buf = torch.zeros(rec, dtype=torch.uint8, device=dev)
+        return rp.merge_cut(buf, starts, lens, needed)
+
+    if not he_rc:
+        v, freed, sf = cut_with(spine_records(sp, rep_all, sp.score, policy, locked_set))
+        return v.cpu().numpy().tolist(), freed, sf
+    # spine scores over every rank's products, rank (= WorkflowId) order
+    prods = hdr[:, 8 + nrep + 8 * sp.n:].reshape(world, -1).view(torch.float64)
+    pieces, offs = [], [0]
+    for j in range(sp.n):
+        for r in range(world):
+            b = int(cnt_all[r, :j].sum())
+            pieces.append(prods[r, b: b + int(cnt_all[r, j])])
+        offs.append(offs[-1] + int(cnt_all[:, j].sum()))
+    x = torch.cat(pieces) if pieces else torch.zeros(1, dtype=torch.float64, device=dev)
+    # fast path: the exact serial chain E and any-order sum A
+    # both lie within L * ulp(sum|x|) / 2 of the real sum.  If the spine
+    # records are after every candidate record for both ends of the interval,
+    # and the cut ends inside the candidates, the exact chains are not needed.
+    seg = torch.repeat_interleave(torch.arange(sp.n, device=dev),
+                                  torch.tensor(np.diff(offs), device=dev)) if offs[-1] else None
+    if seg is not None:
+        A = torch.zeros(sp.n, dtype=torch.float64, device=dev).index_add_(0, seg, x[: offs[-1]]).cpu().numpy()
+        Sa = torch.zeros(sp.n, dtype=torch.float64, device=dev).index_add_(0, seg, x[: offs[-1]].abs()).cpu().numpy()
+    else:
+        A = Sa = np.zeros(sp.n)
+    L = np.diff(offs).astype(np.float64)
+    B = np.array([2.0 * L[j] * np.ldexp(1.0, np.frexp(Sa[j])[1] - 53) if Sa[j] > 0 else 0.0 for j in range(sp.n)])
+    lo = spine_records(sp, rep_all, A - B, policy, locked_set)
+    hi = spine_records(sp, rep_all, A + B, policy, locked_set)
+    fast = np.isfinite(A).all() and lo.size == hi.size and np.array_equal(lo["gid"], hi["gid"])
+    if fast and n_cand and lo.size:
+        last = np.frombuffer(allc.view(world, mx * rec)[:, :].cpu().numpy().tobytes(),
+                             dtype=CAND_DTYPE).reshape(world, mx) if mx else None
+        maxrec = max(tuple(last[r, int(counts[r]) - 1][f] for f in ("w0", "w1", "eff_gid", "d"))
+                     for r in range(world) if counts[r] > 0)
+        fast = all(tuple(int(v) for v in (q["w0"], q["w1"], q["eff_gid"], q["d"])) > maxrec for q in lo)
+    if fast:
+        v, freed, sf = cut_with(lo)
+        if int(v.numel()) <= n_cand and not sf:
+            return v.cpu().numpy().tolist(), freed, sf
+    scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))  # exact chains
+    v, freed, sf = cut_with(spine_records(sp, rep_all, scores, policy, locked_set))
     return v.cpu().numpy().tolist(), freed, sf
