@@ -90,6 +90,7 @@ int slot_for(Context& c, std::int64_t wf) {
     std::size_t need_slots = static_cast<std::size_t>(c.n_slots + 1);
     std::size_t old = static_cast<std::size_t>(c.n_slots);
     c.P.grow_keep(need_slots * c.K * c.V1, old * c.K * c.V1, c.stream);
+    c.Pg.grow_keep(need_slots * c.K * c.V1, old * c.K * c.V1, c.stream);
     c.gs.grow_keep(need_slots * c.K, old * c.K, c.stream);
     std::size_t old_cap = c.fstate.cap;
     c.fstate.grow_keep(need_slots, old, c.stream);

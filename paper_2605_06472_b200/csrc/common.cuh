@@ -121,6 +121,7 @@ struct ScoreArgs {
     const int* acc_slot;
     const unsigned long long* acc_bits;
     const double* P;
+    const double* Pg;  // gs-premultiplied rows (one-agent entries)
     const double* gs;
     const std::uint8_t* fstate;
     int K, V1;

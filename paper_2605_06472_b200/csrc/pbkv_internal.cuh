@@ -214,7 +214,8 @@ struct Context {
     std::unordered_map<std::int64_t, int> slot_of;
 
     // ---- forecasts ----------------------------------------------------------
-    DevBuf<double> P;   // [slots][K][V1]
+    DevBuf<double> P;   // [slots][V1][K] agent-major
+    DevBuf<double> Pg;  // [slots][V1][K]: gs[k] * (0.0 + P[a][k]), the exact Eq. 2 term of a one-agent entry
     DevBuf<double> gs;  // [slots][K]
     DevBuf<std::uint8_t> fstate;
     std::int64_t n_slots = 0;

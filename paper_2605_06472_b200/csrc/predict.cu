@@ -272,6 +272,7 @@ struct HeadArgs {
     int n, A, d, h1, Kp, V1;
     // resident forecast store (score.cu layout): P[slot][K][V1], gs[slot][K], fstate[slot]
     double* P;
+    double* Pg;
     double* gs;
     std::uint8_t* fstate;
     int K;               // scoring horizon of the context
@@ -493,6 +494,15 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a) {
         }
         a.fstate[slot] = a.Kp >= a.K ? 1 : 2;
     }
+    __syncthreads();
+    // one-agent Eq. 2 terms gs[k] * (0.0 + P[a][k]) (see forecast_prepare_kernel)
+    for (int idx = threadIdx.x; idx < nw * a.K * a.V1; idx += kHeadThreads) {
+        const int i = idx / (a.K * a.V1), r = idx % (a.K * a.V1);
+        const int v = r / a.K, k = r % a.K;  // agent-major position
+        const std::size_t base = static_cast<std::size_t>(a.slots[w0 + i]) * a.K * a.V1;
+        const double g = a.gs[static_cast<std::size_t>(a.slots[w0 + i]) * a.K + k];
+        a.Pg[base + r] = __dmul_rn(g, __dadd_rn(0.0, k < KK ? pp[i * KV + k * a.V1 + v] : 0.0));
+    }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -619,6 +629,7 @@ void predictor_run(Context& c, std::int64_t n, const int* pre_off_dev, const int
     a.Kp = cfg.horizon;
     a.V1 = V1;
     a.P = c.P.p;
+    a.Pg = c.Pg.p;
     a.gs = c.gs.p;
     a.fstate = c.fstate.p;
     a.K = c.K;

@@ -45,6 +45,21 @@ __device__ __forceinline__ void eq2_entry(const ScoreArgs& s, int slot, unsigned
 // together; then total += gs[k] * m[k] in step order (scoring.hpp:56-57).
 template <int kK>
 __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsigned long long b, double& total) {
+    if (b && !(b & (b - 1))) {  // one agent: the K terms are precomputed (Pg), one 64-byte line
+        const double* row = s.Pg + (static_cast<std::size_t>(slot) * s.V1 + (__ffsll(static_cast<long long>(b)) - 1)) * kK;
+        if constexpr (kK % 2 == 0) {
+#pragma unroll
+            for (int k = 0; k < kK; k += 2) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(row + k));
+                total = __dadd_rn(total, v.x);
+                total = __dadd_rn(total, v.y);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kK; ++k) total = __dadd_rn(total, __ldg(row + k));
+        }
+        return;
+    }
     const double* pw = s.P + static_cast<std::size_t>(slot) * s.V1 * kK;  // [agent][k]
     const double* g = s.gs + static_cast<std::size_t>(slot) * kK;
     double m[kK];
@@ -471,8 +486,8 @@ __global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* 
 // scoring.hpp:56-58, so that gs[k] * m equals (g * s(k)) * m bit for bit.
 __global__ void __launch_bounds__(256) forecast_prepare_kernel(const double* stage, const long long* slots,
                                                                std::int64_t n, int H, int V1, int K, double gamma,
-                                                               double* P, double* gs, std::uint8_t* fstate,
-                                                               DevStatus* st) {
+                                                               double* P, double* Pg, double* gs,
+                                                               std::uint8_t* fstate, DevStatus* st) {
     // one warp per forecast row: lane k validates step k (agent-ordered sum,
     // forecast.hpp:25-34), the warp transposes the row into the agent-major
     // table, lane 0 runs the survival / gamma chain (forecast.hpp:35-41)
@@ -508,8 +523,8 @@ __global__ void __launch_bounds__(256) forecast_prepare_kernel(const double* sta
             const int a = idx / K, k = idx % K;
             dst[idx] = k < H ? p[k * V1 + a] : 0.0;
         }
+        double* g = gs + static_cast<std::size_t>(slot) * K;
         if (lane == 0) {
-            double* g = gs + static_cast<std::size_t>(slot) * K;
             double surv = 1.0, gk = 1.0;
             for (int k = 0; k < K; ++k) {
                 if (k < H) {
@@ -522,6 +537,13 @@ __global__ void __launch_bounds__(256) forecast_prepare_kernel(const double* sta
                 gk = __dmul_rn(gk, gamma);
             }
             fstate[slot] = H >= K ? 1 : 2;
+        }
+        __syncwarp();
+        // one-agent Eq. 2 terms: mass_on of a single bit is 0.0 + P (forecast.hpp:66-67)
+        double* dg = Pg + static_cast<std::size_t>(slot) * K * V1;
+        for (int idx = lane; idx < K * V1; idx += 32) {
+            const int a = idx / K, k = idx % K;
+            dg[idx] = __dmul_rn(g[k], __dadd_rn(0.0, k < H ? p[k * V1 + a] : 0.0));
         }
     }
 }
@@ -553,6 +575,7 @@ ScoreArgs make_score_args(Context& c, double* out) {
     s.acc_slot = c.acc_slot.p;
     s.acc_bits = c.acc_bits.p;
     s.P = c.P.p;
+    s.Pg = c.Pg.p;
     s.gs = c.gs.p;
     s.fstate = c.fstate.p;
     s.K = c.K;
@@ -591,7 +614,8 @@ KeyArgs make_key_args(Context& c, int policy) {
 
 void launch_forecast_prepare(Context& c, const double* stage, const long long* slots, std::int64_t n, int H) {
     forecast_prepare_kernel<<<grid_cap(n * 32, 256), 256, 0, c.stream>>>(stage, slots, n, H, c.V1, c.K, c.gamma,
-                                                                        c.P.p, c.gs.p, c.fstate.p, c.status.p);
+                                                                        c.P.p, c.Pg.p, c.gs.p, c.fstate.p,
+                                                                        c.status.p);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
 }
