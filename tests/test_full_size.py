@@ -89,3 +89,39 @@ def test_c3_prefetch_plan_equals_oracle(c3):
     assert np.array_equal(np.array([c[1] for c in g.candidates]).view(np.uint64),
                           np.array([c[1] for c in o.candidates]).view(np.uint64))
     assert g.selected == o.selected and g.selected_tokens == o.selected_tokens
+
+
+def test_c4_sharded_8_ways_equals_single_and_oracle(gpu):
+    """BASELINE config 4 shape (8 M nodes x 16 K workflows x K = 8), split
+    into 8 node-set shards (logical ranks on one B200): the sharded decision
+    (local cuts, spine records, merge + cut) equals the single-context
+    decision on the whole tree and the CPU oracle."""
+    from paper_2605_06472_b200 import shard as S
+
+    t = HostTree()
+    t.synth(n_nodes=8_000_000, n_workflows=16384, agents=16, seed=4)
+    soa = t.export()
+    rng = np.random.default_rng(4)
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, 8, 17)
+    locked = WL.pinned_paths(soa, rng, 0.01)
+    shards = S.partition(soa, 8)
+    sps = []
+    for s in shards:
+        sp = S.ShardedPolicy(s, num_agents=16, k=8, gamma=0.7)
+        mine = (wf >= s.wf_lo) & (wf < s.wf_hi)
+        sp.pol.put_forecasts(wf[mine], P[mine])
+        sps.append(sp)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    needed = used // 100
+    got = S.global_select(sps, POLICY_HE, SCORE_RECOMPUTE, needed, locked)
+    del sps
+    single = Policy(num_agents=16, k=8, gamma=0.7)
+    single.mirror(t)
+    single.put_forecasts(wf, P)
+    want = single.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+    assert (got[0], got[1], got[2]) == (want.victims, want.freed, want.shortfall)
+    s2 = soa.copy()
+    s2.score[:] = Oracle.score_nodes(soa, wf, P, 8, 0.7)
+    o = Oracle.select(s2, POLICY_HE, needed, locked)
+    assert (o.victims, o.freed, o.shortfall) == (want.victims, want.freed, want.shortfall)
