@@ -37,6 +37,7 @@ CONFIGS = {
     # name: (n_nodes, n_workflows, K)
     "c2": (10_000, 256, 4),
     "c3": (1_000_000, 4096, 8),
+    "c4": (8_000_000, 16384, 8),  # config 4 on one GPU (the sharded runs use N x c3 shards)
 }
 AGENTS = 16
 GAMMA = 0.7

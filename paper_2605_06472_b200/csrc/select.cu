@@ -289,6 +289,10 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
             const std::int64_t i = base + j * nthr;
             n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
             act[j] = i < a.n_nodes && n[j] != 0 && (a.flags[n[j]] & kFlagTierMask) == PBKV_TIER_DEVICE;
+            if (act[j]) {  // chain weights accumulate by scatter in phase_chains
+                a.W[n[j]] = 0;
+                a.C[n[j]] = 0;
+            }
             p[j] = act[j] ? a.parent[n[j]] : 0;
             km[j] = act[j] ? load_key(a.keys, n[j]) : Key2{0, 0};
             act[j] = act[j] && p[j] > 0;
@@ -326,37 +330,42 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
 // eligible ancestors with the same eff -- for its token weight W and size C;
 // head list, eligible tokens, OR/AND of the head keys (first radix pass)
 __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh) {
-    // every thread classifies kBatch nodes (independent loads together), the
-    // CTA appends all of its heads with one atomic, then the heads walk their
-    // chains in lockstep
+    // Every eligible node n belongs to the chain of eff(n) (the closed form
+    // orders eligible nodes by (eff, d); the nodes sharing an eff form a
+    // contiguous eligible ancestor path from it), so the chain weight W[h] and
+    // size C[h] are scatter-adds from the members -- no pointer-chasing walks.
+    // Heads (eff(n) == n) are appended with one atomic per CTA and iteration.
     constexpr int kBatch = 4;
     SelState* ss = a.ss;
     unsigned long long tok = 0;
     unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
     for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
          base += kBatch * nthr) {
-        int n[kBatch];
-        bool head[kBatch];
+        int n[kBatch], e[kBatch];
+        bool elig[kBatch];
         unsigned int cnt = 0;
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const std::int64_t i = base + threadIdx.x + j * nthr;
             n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
-            head[j] = i < a.n_nodes && n[j] != 0 &&
+            elig[j] = i < a.n_nodes && n[j] != 0 &&
                       (a.flags[n[j]] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
                       !__ldcg(&a.sublock[n[j]]);
+            e[j] = elig[j] ? __ldcg(&a.eff[n[j]]) : -1;
         }
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
-            if (!head[j]) continue;
+            if (!elig[j]) continue;
             const std::uint8_t ms = a.missing[n[j]];
             if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n[j]);
             if (a.he_recompute && ms && !(a.flags[n[j]] & kFlagRetired))
                 set_error(a.st, PBKV_EINVAL, kErrMissingForecast, n[j]);
-            head[j] = __ldcg(&a.eff[n[j]]) == n[j];
-            cnt += head[j] ? 1u : 0u;
+            const unsigned long long l = static_cast<unsigned long long>(a.len[n[j]]);
+            atomicAdd(&a.W[e[j]], l);
+            atomicAdd(&a.C[e[j]], 1u);
+            tok += l;
+            cnt += e[j] == n[j] ? 1u : 0u;
         }
         // CTA-wide exclusive offsets of the heads, one global atomic per CTA
         unsigned int* wcount = reinterpret_cast<unsigned int*>(sh);
@@ -381,47 +390,11 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
         __syncthreads();
         unsigned long long slot = sh[31] + wcount[warp] + (incl - cnt);
         __syncthreads();
-        // chains: walk up while the parent is eligible with the same eff
-        unsigned long long w[kBatch];
-        unsigned int c[kBatch];
-        int p[kBatch];
-        bool act[kBatch];
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
-            w[j] = 0;
-            c[j] = 0;
-            p[j] = n[j];
-            act[j] = head[j];
-        }
-        for (;;) {
-            bool any = false;
-            int q[kBatch];
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                if (!act[j]) continue;
-                any = true;
-                w[j] += static_cast<unsigned long long>(a.len[p[j]]);
-                ++c[j];
-                q[j] = a.parent[p[j]];
-            }
-            if (!any) break;
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                if (!act[j]) continue;
-                const int pp = q[j];
-                act[j] = pp > 0 && !(a.flags[pp] & kFlagOutOfOrder) && !__ldcg(&a.sublock[pp]) &&
-                         __ldcg(&a.eff[pp]) == n[j];
-                p[j] = pp;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            if (!head[j]) continue;
+            if (!elig[j] || e[j] != n[j]) continue;
             const int h = n[j];
-            a.W[h] = w[j];
-            a.C[h] = c[j];
             a.rank[h] = -1;
-            tok += w[j];
             a.heads[slot++] = h;
             const Key2 k = load_key(a.keys, h);
             for (int wd = 0; wd < 3; ++wd) {
@@ -431,7 +404,6 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             }
         }
     }
-    (void)tid;
     const unsigned long long blk = block_reduce_bits(tok, SumOp(), sh);
     if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
     flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
