@@ -225,6 +225,28 @@ void finish_timing(Context& c, int last_ev) {
     c.last_ms[4] = el(0, last_ev);
 }
 
+// children lists (CSR, in the order of `nodes`) of a few out-of-order nodes
+void upload_children(Context& c, const std::vector<int>& nodes, DevBuf<int>& off_d, DevBuf<int>& ch_d) {
+    std::unordered_map<int, int> idx;
+    for (std::size_t j = 0; j < nodes.size(); ++j) idx[nodes[j]] = static_cast<int>(j);
+    std::vector<std::vector<int>> lists(nodes.size());
+    if (!nodes.empty())
+        for (std::size_t i = 1; i < c.h_parent.size(); ++i) {
+            auto it = idx.find(c.h_parent[i]);
+            if (it != idx.end()) lists[static_cast<std::size_t>(it->second)].push_back(static_cast<int>(i));
+        }
+    std::vector<int> off{0}, ch;
+    for (auto& l : lists) {
+        ch.insert(ch.end(), l.begin(), l.end());
+        off.push_back(static_cast<int>(ch.size()));
+    }
+    off_d.reserve(off.size());
+    ch_d.reserve(ch.size() + 1);
+    PBKV_CUDA(cudaMemcpyAsync(off_d.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    if (!ch.empty())
+        PBKV_CUDA(cudaMemcpyAsync(ch_d.p, ch.data(), ch.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+}
+
 // ---- mirror -----------------------------------------------------------------
 void mirror_full(Context& c, const pbkv_tree_soa& s) {
     need(s.n_nodes >= 1, "tree must contain the root");
@@ -349,6 +371,8 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     c.n_medium = static_cast<std::int64_t>(medium.size());
     c.n_heavy = static_cast<std::int64_t>(heavy.size());
     c.h_heavy = heavy;
+    c.h_parent.assign(s.parent, s.parent + n);
+    upload_children(c, heavy, c.hch_off, c.hch);
     c.h_heavy_depth.resize(heavy.size());
     for (std::size_t j = 0; j < heavy.size(); ++j) c.h_heavy_depth[j] = dep[heavy[j]];
     c.n_hent = static_cast<std::int64_t>(hent.size());
@@ -362,6 +386,7 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     if (!c.spine.empty()) {
         for (int v : c.spine) need(v >= 0 && v < n, "shard spine id out of range for the mirrored tree");
         shard_apply_flags(c);
+        upload_children(c, c.spine, c.sch_off, c.sch);
     }
     PBKV_CUDA(cudaStreamSynchronize(st));
 }
@@ -1036,6 +1061,7 @@ int pbkv_shard_set(pbkv_ctx* c, const int32_t* global_ids, const int32_t* spine,
         PBKV_CUDA(cudaMemcpyAsync(c->gid.p, global_ids, static_cast<std::size_t>(c->n) * sizeof(int),
                                   cudaMemcpyHostToDevice, c->stream));
         shard_apply_flags(*c);
+        upload_children(*c, c->spine, c->sch_off, c->sch);
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
     });
 }

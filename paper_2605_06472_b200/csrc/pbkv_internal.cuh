@@ -200,6 +200,10 @@ struct Context {
     DevBuf<unsigned int> hmiss;   // per heavy node: missing (1) / short horizon (2)
     std::int64_t n_hent = 0;
     std::vector<int> h_heavy;                 // heavy node ids (host copy)
+    std::vector<int> h_parent;                // parent of every node (host copy)
+    // children of the out-of-order nodes (CSR in heavy / spine order): the
+    // eff walk stops below them and their reports reduce over these lists
+    DevBuf<int> hch_off, hch, sch_off, sch;
     std::vector<unsigned long long> h_heavy_last;
     std::vector<int> h_heavy_depth, h_heavy_parent;
     std::vector<std::uint8_t> h_heavy_flags;

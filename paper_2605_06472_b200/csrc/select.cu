@@ -289,13 +289,20 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
             const std::int64_t i = base + j * nthr;
             n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
             act[j] = i < a.n_nodes && n[j] != 0 && (a.flags[n[j]] & kFlagTierMask) == PBKV_TIER_DEVICE;
-            if (act[j]) {  // chain weights accumulate by scatter in phase_chains
-                a.W[n[j]] = 0;
-                a.C[n[j]] = 0;
-            }
             p[j] = act[j] ? a.parent[n[j]] : 0;
             km[j] = act[j] ? load_key(a.keys, n[j]) : Key2{0, 0};
-            act[j] = act[j] && p[j] > 0;
+            // out-of-order parents (deferred heavy / spine) are reduced over
+            // their children lists instead: thousands of walkers CAS-ing one
+            // hot word serialised in its L2 slice
+            act[j] = act[j] && p[j] > 0 && !(a.flags[p[j]] & kFlagOutOfOrder);
+        }
+        // eff[p] >= key(p): a walker below its parent's own key stops without
+        // touching eff[p] (the common case -- HE keys grow toward the root)
+#pragma unroll
+        for (int j = 0; j < kWalk; ++j) {
+            if (!act[j]) continue;
+            const Key2 kp = load_key(a.keys, p[j]);
+            act[j] = key_less(kp, p[j], km[j], n[j]);
         }
         for (;;) {
             bool any = false;
@@ -319,7 +326,7 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
                 }
                 if (atomicCAS(&a.eff[p[j]], cur[j], n[j]) == cur[j]) {
                     p[j] = a.parent[p[j]];
-                    act[j] = p[j] > 0;
+                    act[j] = p[j] > 0 && !(a.flags[p[j]] & kFlagOutOfOrder);
                 }  // else: lost a race, re-read eff[p] next round
             }
         }
@@ -1022,25 +1029,68 @@ namespace {
 // per deferred heavy node: max key over its non-deferred device descendants
 // (eff after the walk; its own key is zeroed), lock status, missing
 // forecasts; plus the record of the last victim of the cut (tail)
-__global__ void heavy_report_kernel(const int* heavy, int n_heavy, const Key2* keys, const int* eff,
-                                    const int* sublock, const int* depth, const std::uint8_t* flags,
-                                    const unsigned int* hmiss, const int* victims, const long long* result,
-                                    HeavyReport* out) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int n_heavy, const int* ch_off,
+                                                           const int* ch, const Key2* keys, const int* eff,
+                                                           const int* sublock, const int* depth,
+                                                           const std::uint8_t* flags, const unsigned int* hmiss,
+                                                           const int* victims, const long long* result,
+                                                           HeavyReport* out) {
+    // one CTA per heavy node: max over its in-order device children's eff
+    // (the shared prefix has thousands of children); the last CTA writes the
+    // record of the last victim (tail)
+    const int j = blockIdx.x;
     if (j < n_heavy) {
-        const int h = heavy[j];
-        const int e = eff[h];
-        HeavyReport r{};
-        const bool has = !(flags[e] & kFlagOutOfOrder);
-        const Key2 k = load_key(keys, e);
-        r.w0 = has ? k.w0 : 0ull;
-        r.w1 = has ? k.w1 : 0ull;
-        r.eff = has ? e : -1;
-        r.eff_depth = has ? depth[e] : -1;
-        r.sublock = sublock[h] ? 1 : 0;
-        r.miss = static_cast<int>(hmiss[j]);
-        out[j] = r;
-    } else if (j == n_heavy) {
+        __shared__ unsigned long long s0[8], s1[8];
+        __shared__ int se[8];
+        int e = -1;
+        Key2 best{0, 0};
+        for (int q = ch_off[j] + threadIdx.x; q < ch_off[j + 1]; q += blockDim.x) {
+            const int c = ch[q];
+            if ((flags[c] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE) continue;
+            const int ec = eff[c];
+            const Key2 k = load_key(keys, ec);
+            if (e < 0 || key_less(best, e, k, ec)) {
+                e = ec;
+                best = k;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long b0 = __shfl_xor_sync(0xffffffffu, best.w0, o);
+            const unsigned long long b1 = __shfl_xor_sync(0xffffffffu, best.w1, o);
+            const int be = __shfl_xor_sync(0xffffffffu, e, o);
+            const Key2 bk{b0, b1};
+            if (be >= 0 && (e < 0 || key_less(best, e, bk, be))) {
+                e = be;
+                best = bk;
+            }
+        }
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) {
+            s0[warp] = best.w0;
+            s1[warp] = best.w1;
+            se[warp] = e;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            e = -1;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+                const Key2 bk{s0[w], s1[w]};
+                if (se[w] >= 0 && (e < 0 || key_less(best, e, bk, se[w]))) {
+                    e = se[w];
+                    best = bk;
+                }
+            }
+            const int h = heavy[j];
+            HeavyReport r{};
+            r.w0 = e >= 0 ? best.w0 : 0ull;
+            r.w1 = e >= 0 ? best.w1 : 0ull;
+            r.eff = e;
+            r.eff_depth = e >= 0 ? depth[e] : -1;
+            r.sublock = sublock[h] ? 1 : 0;
+            r.miss = static_cast<int>(hmiss[j]);
+            out[j] = r;
+        }
+    } else if (threadIdx.x == 0) {
         HeavyReport r{};
         const long long n = result[0];
         r.eff = -1;
@@ -1061,7 +1111,8 @@ __global__ void heavy_report_kernel(const int* heavy, int n_heavy, const Key2* k
 
 void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out) {
     const int n = static_cast<int>(c.n_heavy);
-    heavy_report_kernel<<<(n + 1 + 127) / 128, 128, 0, c.stream>>>(c.heavy.p, n, c.keys.p, c.eff.p, c.sublock.p,
+    heavy_report_kernel<<<n + 1, 256, 0, c.stream>>>(c.heavy.p, n, c.hch_off.p, c.hch.p, c.keys.p,
+                                                                   c.eff.p, c.sublock.p,
                                                                    c.depth.p, c.flags.p, c.hmiss.p, c.vid_out.p,
                                                                    result_dev, out);
     PBKV_CUDA(cudaGetLastError());
@@ -1093,6 +1144,9 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     }
     tmpl->cut_head = -1;
     PBKV_CUDA(cudaMemcpyAsync(ss, tmpl, sizeof(SelState), cudaMemcpyHostToDevice, c.stream));
+    // chain weights / sizes accumulate by scatter in phase_chains
+    PBKV_CUDA(cudaMemsetAsync(c.W.p, 0, static_cast<std::size_t>(c.n) * sizeof(unsigned long long), c.stream));
+    PBKV_CUDA(cudaMemsetAsync(c.C.p, 0, static_cast<std::size_t>(c.n) * sizeof(unsigned int), c.stream));
     long long* res = result_dev ? result_dev : c.counters.p + 8;
     c.sorti_out.reserve(static_cast<std::size_t>(c.n) + 1);
     c.cnt.reserve(static_cast<std::size_t>(c.n) + 1);

@@ -59,20 +59,32 @@ __global__ void records_kernel(const int* victims, const long long* result, cons
 
 // per spine node: the maximum key over the rank's device descendants (eff
 // after the selection's walk) and whether a locked node lies below
-__global__ void spine_report_kernel(const int* spine, int n_spine, const Key2* keys, const int* eff,
-                                    const int* sublock, const int* depth, const int* gid,
-                                    const std::uint8_t* flags, pbkv_spine_info* out) {
+__global__ void spine_report_kernel(const int* spine, int n_spine, const int* ch_off, const int* ch,
+                                    const Key2* keys, const int* eff, const int* sublock, const int* depth,
+                                    const int* gid, const std::uint8_t* flags, pbkv_spine_info* out) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_spine) return;
     const int s = spine[j];
-    const int e = eff[s];
+    // max over the in-order device children's eff (the walk stops below the
+    // spine; spine children are combined on the host, shard.py)
+    int e = -1;
+    Key2 best{0, 0};
+    for (int q = ch_off[j]; q < ch_off[j + 1]; ++q) {
+        const int c = ch[q];
+        if ((flags[c] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE) continue;
+        const int ec = eff[c];
+        const Key2 k = load_key(keys, ec);
+        if (e < 0 || key_less(best, e, k, ec)) {
+            e = ec;
+            best = k;
+        }
+    }
     pbkv_spine_info r;
-    r.has_eff = (flags[e] & kFlagExcluded) ? 0 : 1;
-    const Key2 k = load_key(keys, e);
-    r.w0 = r.has_eff ? k.w0 : 0ull;
-    r.w1 = r.has_eff ? k.w1 : 0ull;
-    r.eff_gid = r.has_eff ? gid[e] : -1;
-    r.eff_depth = r.has_eff ? depth[e] : -1;
+    r.has_eff = e >= 0 ? 1 : 0;
+    r.w0 = e >= 0 ? best.w0 : 0ull;
+    r.w1 = e >= 0 ? best.w1 : 0ull;
+    r.eff_gid = e >= 0 ? gid[e] : -1;
+    r.eff_depth = e >= 0 ? depth[e] : -1;
     r.sublock = sublock[s] ? 1 : 0;
     out[j] = r;
 }
@@ -199,8 +211,9 @@ void shard_records(Context& c, long long* result_dev, pbkv_cand* out, long long 
 void shard_spine_report(Context& c, pbkv_spine_info* out) {
     const int n = static_cast<int>(c.spine.size());
     if (n == 0) return;
-    spine_report_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.spine_dev.p, n, c.keys.p, c.eff.p, c.sublock.p,
-                                                               c.depth.p, c.gid.p, c.flags.p, out);
+    spine_report_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.spine_dev.p, n, c.sch_off.p, c.sch.p, c.keys.p,
+                                                               c.eff.p, c.sublock.p, c.depth.p, c.gid.p, c.flags.p,
+                                                               out);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
 }
