@@ -197,27 +197,49 @@ __global__ void __launch_bounds__(kMediumWarps * 32) score_medium_kernel(ScoreAr
 }
 
 // products of every heavy entry: element j*K + k of the packed product array
+// approx (optional, [2*heavy]): any-order sum and sum of |x| per heavy node,
+// accumulated with one double atomic per warp run of the same node
 __global__ void __launch_bounds__(256) heavy_products_kernel(ScoreArgs s, const unsigned int* hent,
                                                              const int* hent_node, std::int64_t n_hent, double* xs,
-                                                             unsigned int* hmiss) {
+                                                             unsigned int* hmiss, double* approx) {
     const int K = s.K;
     const std::int64_t total = n_hent * K;
-    for (std::int64_t t = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::int64_t j = t / K;
-        const int k = static_cast<int>(t - j * K);
-        const unsigned int e = hent[j];
-        const int slot = __ldg(s.acc_slot + e);
-        const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
-        const std::uint8_t fs = __ldg(s.fstate + slot);
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    const std::int64_t rounds = (total + stride - 1) / stride;  // uniform trip count: shuffles stay convergent
+    for (std::int64_t r = 0; r < rounds; ++r) {
+        const std::int64_t t = r * stride + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+        const bool in = t < total;
         double x = 0.0;
-        if (fs != 1) {
-            atomicOr(&hmiss[hent_node[j]], fs == 2 ? 2u : 1u);
-        } else {
-            const double* col = s.P + static_cast<std::size_t>(slot) * s.V1 * K + k;
-            x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * K + k), mass_on(col, K, b));
+        int node = -1;
+        if (in) {
+            const std::int64_t j = t / K;
+            const int k = static_cast<int>(t - j * K);
+            const unsigned int e = hent[j];
+            const int slot = __ldg(s.acc_slot + e);
+            const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+            const std::uint8_t fs = __ldg(s.fstate + slot);
+            node = hent_node[j];
+            if (fs != 1) {
+                atomicOr(&hmiss[node], fs == 2 ? 2u : 1u);
+            } else {
+                const double* col = s.P + static_cast<std::size_t>(slot) * s.V1 * K + k;
+                x = __dmul_rn(__ldg(s.gs + static_cast<std::size_t>(slot) * K + k), mass_on(col, K, b));
+            }
+            xs[t] = x;
         }
-        xs[t] = x;
+        if (approx == nullptr) continue;
+        const unsigned same = __match_any_sync(0xffffffffu, node);
+        double sx = 0.0, sa = 0.0;
+        for (unsigned m = same; m; m &= m - 1) {
+            const int src = __ffs(m) - 1;
+            const double v = __shfl_sync(same, x, src);
+            sx += v;
+            sa += fabs(v);
+        }
+        if (node >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) {
+            atomicAdd(&approx[2 * node], sx);
+            atomicAdd(&approx[2 * node + 1], sa);
+        }
     }
 }
 
@@ -413,32 +435,10 @@ __global__ void __launch_bounds__(kChainT) chain_sum_kernel(const double* x, con
     if (threadIdx.x == 0) out[blockIdx.x] = t;
 }
 
-// Approximate Eq. 2 of each heavy node: sum and sum of |terms| of its
-// products in any order (FP64 tree reduction).  The exact serial chain E and
-// this sum A both lie within L * ulp(sum|x|) / 2 of the real sum, so
-// |E - A| <= L * ulp(sum|x|): the interval the decision fast path uses.
-__global__ void __launch_bounds__(256) heavy_approx_kernel(const unsigned int* acc_off, const int* nodes,
-                                                           const long long* xs_start, const double* xs_g, int K,
-                                                           double* out) {
-    using Red = cub::BlockReduce<double, 256>;
-    __shared__ typename Red::TempStorage tmp;
-    const int node = nodes[blockIdx.x];
-    const long long L = static_cast<long long>(acc_off[node + 1] - acc_off[node]) * K;
-    const double* x = xs_g + xs_start[blockIdx.x];
-    double s = 0.0, a = 0.0;
-    for (long long i = threadIdx.x; i < L; i += 256) {
-        const double v = __ldcg(x + i);
-        s += v;
-        a += fabs(v);
-    }
-    s = Red(tmp).Sum(s);
-    __syncthreads();
-    a = Red(tmp).Sum(a);
-    if (threadIdx.x == 0) {
-        out[2 * blockIdx.x] = s;
-        out[2 * blockIdx.x + 1] = a;
-    }
-}
+// Approximate Eq. 2 of each heavy node (the decision fast path): the sum and
+// the sum of |terms| of its products in any order, accumulated by
+// heavy_products_kernel.  The exact serial chain E and this sum A both lie
+// within L * ulp(sum|x|) / 2 of the real sum, so |E - A| <= L * ulp(sum|x|).
 
 __global__ void set_deferred_kernel(std::uint8_t* flags, Key2* keys, const int* nodes, int n, int on) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -632,7 +632,7 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy) * sizeof(unsigned int), c.side));
         heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(s, c.hent.p, c.hent_node.p,
-                                                                               c.n_hent, c.hxs.p, c.hmiss.p);
+                                                                               c.n_hent, c.hxs.p, c.hmiss.p, nullptr);
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
         const unsigned int hb = static_cast<unsigned int>(c.n_heavy);
@@ -686,14 +686,12 @@ void launch_score_decision(Context& c, int policy) {
         PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy) * sizeof(unsigned int), c.side));
+        PBKV_CUDA(cudaMemsetAsync(c.happrox.p, 0, static_cast<std::size_t>(2 * c.n_heavy) * sizeof(double), c.side));
         heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(s, c.hent.p, c.hent_node.p,
-                                                                               c.n_hent, c.hxs.p, c.hmiss.p);
+                                                                               c.n_hent, c.hxs.p, c.hmiss.p,
+                                                                               c.happrox.p);
         PBKV_CUDA(cudaGetLastError());
-        heavy_approx_kernel<<<static_cast<unsigned int>(c.n_heavy), 256, 0, c.side>>>(c.acc_off.p, c.heavy.p,
-                                                                                       c.hstart.p, c.hxs.p, c.K,
-                                                                                       c.happrox.p);
-        PBKV_CUDA(cudaGetLastError());
-        c.launches += 2;
+        ++c.launches;
         PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
     }
     launch_light<true>(c, s, ka, 0);
