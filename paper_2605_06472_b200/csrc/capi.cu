@@ -298,6 +298,17 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
         }
     }
     off[static_cast<std::size_t>(n)] = static_cast<unsigned int>(E);
+    // medium nodes' entries follow the heavy ones in the product list
+    // (combined index n_heavy + m): their products are formed by the same
+    // grid-wide kernel and each chain is added by one warp (score.cu)
+    for (std::size_t m = 0; m < medium.size(); ++m) {
+        const int i = medium[m];
+        hstart.push_back(static_cast<long long>(hent.size()) * c.K);
+        for (std::int64_t e = s.acc_off[i]; e < s.acc_off[i + 1]; ++e) {
+            hent.push_back(static_cast<unsigned int>(e));
+            hent_node.push_back(static_cast<int>(heavy.size() + m));
+        }
+    }
     const int* dep = s.depth;
     if (!dep) {
         depth.assign(static_cast<std::size_t>(n), -1);
@@ -354,13 +365,14 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     c.medium.reserve(medium.size() + 1);
     c.hent.reserve(hent.size() + 1);
     c.hent_node.reserve(hent.size() + 1);
-    c.hstart.reserve(heavy.size() + 1);
-    c.hmiss.reserve(heavy.size() + 1);
+    c.hstart.reserve(heavy.size() + medium.size() + 1);
+    c.hmiss.reserve(heavy.size() + medium.size() + 1);
     c.hxs.reserve(hent.size() * static_cast<std::size_t>(c.K) + 1);
     if (!medium.empty())
         PBKV_CUDA(cudaMemcpyAsync(c.medium.p, medium.data(), medium.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (!heavy.empty()) {
+    if (!heavy.empty())
         PBKV_CUDA(cudaMemcpyAsync(c.heavy.p, heavy.data(), heavy.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!hent.empty()) {
         PBKV_CUDA(cudaMemcpyAsync(c.hent.p, hent.data(), hent.size() * sizeof(unsigned int), cudaMemcpyHostToDevice,
                                   st));
         PBKV_CUDA(cudaMemcpyAsync(c.hent_node.p, hent_node.data(), hent_node.size() * sizeof(int),

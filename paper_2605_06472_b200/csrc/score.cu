@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kMediumWarps * 32) score_medium_kernel(ScoreAr
 // accumulated with one double atomic per warp run of the same node
 __global__ void __launch_bounds__(256) heavy_products_kernel(ScoreArgs s, const unsigned int* hent,
                                                              const int* hent_node, std::int64_t n_hent, double* xs,
-                                                             unsigned int* hmiss, double* approx) {
+                                                             unsigned int* hmiss, double* approx, int n_heavy) {
     const int K = s.K;
     const std::int64_t total = n_hent * K;
     const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) heavy_products_kernel(ScoreArgs s, const 
             sx += v;
             sa += fabs(v);
         }
-        if (node >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) {
+        if (node >= 0 && node < n_heavy && (threadIdx.x & 31) == __ffs(same) - 1) {
             atomicAdd(&approx[2 * node], sx);
             atomicAdd(&approx[2 * node + 1], sa);
         }
@@ -422,6 +422,38 @@ __global__ void __launch_bounds__(kChainT) heavy_chain_kernel(ScoreArgs s, KeyAr
         if constexpr (kKeys) {
             ka.missing[node] = miss ? 1 : 0;
             if (node != 0 && (ka.flags[node] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, node, total);
+        }
+    }
+}
+
+// Medium nodes (entries * K <= 256): one warp per node adds the node's
+// products (heavy_products_kernel, combined index n_heavy + m) in order;
+// lanes fetch 32 at a time, lane 0 folds them via shuffles.
+template <bool kKeys>
+__global__ void __launch_bounds__(256) medium_chain_kernel(ScoreArgs s, KeyArgs ka, const int* medium,
+                                                           std::int64_t n_medium, std::int64_t n_heavy,
+                                                           const long long* xs_start, const double* xs_g,
+                                                           const unsigned int* hmiss, int report_missing) {
+    const std::int64_t m = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (m >= n_medium) return;
+    const int node = medium[m];
+    const int L = static_cast<int>(s.acc_off[node + 1] - s.acc_off[node]) * s.K;
+    const double* x = xs_g + xs_start[n_heavy + m];
+    double t = 0.0;
+    for (int c0 = 0; c0 < L; c0 += 32) {
+        const double v = c0 + lane < L ? __ldcg(x + c0 + lane) : 0.0;
+        const int cnt = min(32, L - c0);
+        for (int q = 0; q < cnt; ++q) t = __dadd_rn(t, __shfl_sync(0xffffffffu, v, q));
+    }
+    if (lane == 0) {
+        s.out[node] = t;
+        const unsigned int miss = hmiss[n_heavy + m];
+        if (report_missing && miss)
+            set_error(s.st, PBKV_EINVAL, (miss & 1) ? kErrMissingForecast : kErrShortHorizon, node);
+        if constexpr (kKeys) {
+            ka.missing[node] = miss ? 1 : 0;
+            if (node != 0 && (ka.flags[node] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, node, t);
         }
     }
 }
@@ -626,24 +658,39 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
     ScoreArgs s = make_score_args(c, out);
     KeyArgs ka = make_key_args(c, policy);
     const int rm = report_missing ? 1 : 0;
-    // heavy path on the side stream, overlapped with the light pass
-    if (c.n_heavy > 0) {
+    // medium + heavy products and chains on the side stream, overlapped with the light pass
+    const bool side = c.n_heavy + c.n_medium > 0;
+    if (side) {
         PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy) * sizeof(unsigned int), c.side));
-        heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(s, c.hent.p, c.hent_node.p,
-                                                                               c.n_hent, c.hxs.p, c.hmiss.p, nullptr);
+        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy + c.n_medium) * sizeof(unsigned int),
+                                  c.side));
+        heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(
+            s, c.hent.p, c.hent_node.p, c.n_hent, c.hxs.p, c.hmiss.p, nullptr, static_cast<int>(c.n_heavy));
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
-        const unsigned int hb = static_cast<unsigned int>(c.n_heavy);
-        if (write_keys)
-            heavy_chain_kernel<true><<<hb, kChainT, chain_smem_bytes(), c.side>>>(s, ka, c.heavy.p, c.hstart.p,
-                                                                               c.hxs.p, c.hmiss.p, rm);
-        else
-            heavy_chain_kernel<false><<<hb, kChainT, chain_smem_bytes(), c.side>>>(s, ka, c.heavy.p, c.hstart.p,
-                                                                                c.hxs.p, c.hmiss.p, rm);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
+        if (c.n_medium > 0) {
+            const unsigned int g = static_cast<unsigned int>((c.n_medium * 32 + 255) / 256);
+            if (write_keys)
+                medium_chain_kernel<true><<<g, 256, 0, c.side>>>(s, ka, c.medium.p, c.n_medium, c.n_heavy, c.hstart.p,
+                                                                 c.hxs.p, c.hmiss.p, rm);
+            else
+                medium_chain_kernel<false><<<g, 256, 0, c.side>>>(s, ka, c.medium.p, c.n_medium, c.n_heavy,
+                                                                  c.hstart.p, c.hxs.p, c.hmiss.p, rm);
+            PBKV_CUDA(cudaGetLastError());
+            ++c.launches;
+        }
+        if (c.n_heavy > 0) {
+            const unsigned int hb = static_cast<unsigned int>(c.n_heavy);
+            if (write_keys)
+                heavy_chain_kernel<true><<<hb, kChainT, chain_smem_bytes(), c.side>>>(s, ka, c.heavy.p, c.hstart.p,
+                                                                                   c.hxs.p, c.hmiss.p, rm);
+            else
+                heavy_chain_kernel<false><<<hb, kChainT, chain_smem_bytes(), c.side>>>(s, ka, c.heavy.p, c.hstart.p,
+                                                                                    c.hxs.p, c.hmiss.p, rm);
+            PBKV_CUDA(cudaGetLastError());
+            ++c.launches;
+        }
         PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
     }
     if (write_keys)
@@ -652,18 +699,7 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
         launch_light<false>(c, s, ka, rm);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
-    if (c.n_medium > 0) {
-        const unsigned int g = static_cast<unsigned int>((c.n_medium + kMediumWarps - 1) / kMediumWarps);
-        if (write_keys)
-            score_medium_kernel<true, false><<<g, kMediumWarps * 32, 0, c.stream>>>(s, ka, c.medium.p, c.n_medium, rm,
-                                                                                   0);
-        else
-            score_medium_kernel<false, false><<<g, kMediumWarps * 32, 0, c.stream>>>(s, ka, c.medium.p, c.n_medium,
-                                                                                    rm, 0);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-    }
-    if (c.n_heavy > 0) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+    if (side) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
 void launch_set_deferred(Context& c, bool on) {
@@ -681,34 +717,31 @@ void launch_set_deferred(Context& c, bool on) {
 void launch_score_decision(Context& c, int policy) {
     ScoreArgs s = make_score_args(c, c.score_rc.p);
     KeyArgs ka = make_key_args(c, policy);
-    if (c.n_heavy > 0) {
-        c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy));
+    const bool side = c.n_heavy + c.n_medium > 0;
+    if (side) {
+        c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy) + 2);
         PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy) * sizeof(unsigned int), c.side));
+        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy + c.n_medium) * sizeof(unsigned int),
+                                  c.side));
         PBKV_CUDA(cudaMemsetAsync(c.happrox.p, 0, static_cast<std::size_t>(2 * c.n_heavy) * sizeof(double), c.side));
-        heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(s, c.hent.p, c.hent_node.p,
-                                                                               c.n_hent, c.hxs.p, c.hmiss.p,
-                                                                               c.happrox.p);
+        heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(
+            s, c.hent.p, c.hent_node.p, c.n_hent, c.hxs.p, c.hmiss.p, c.happrox.p, static_cast<int>(c.n_heavy));
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
+        if (c.n_medium > 0) {
+            const unsigned int g = static_cast<unsigned int>((c.n_medium * 32 + 255) / 256);
+            medium_chain_kernel<true><<<g, 256, 0, c.side>>>(s, ka, c.medium.p, c.n_medium, c.n_heavy, c.hstart.p,
+                                                             c.hxs.p, c.hmiss.p, 0);
+            PBKV_CUDA(cudaGetLastError());
+            ++c.launches;
+        }
         PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
     }
     launch_light<true>(c, s, ka, 0);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
-    if (c.n_medium > 0) {  // medium nodes on the side stream too, overlapped with the light pass
-        if (c.n_heavy == 0) {
-            PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
-            PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-        }
-        const unsigned int g = static_cast<unsigned int>((c.n_medium + kMediumWarps - 1) / kMediumWarps);
-        score_medium_kernel<true, false><<<g, kMediumWarps * 32, 0, c.side>>>(s, ka, c.medium.p, c.n_medium, 0, 0);
-        PBKV_CUDA(cudaGetLastError());
-        ++c.launches;
-        PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
-    }
-    if (c.n_heavy > 0 || c.n_medium > 0) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+    if (side) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
 // Eq. 2 / Eq. 1 of an id list, results scattered into out[id]
