@@ -89,7 +89,7 @@ __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsign
 // Light nodes (<= 2 entries): one thread per node, Eq. 2 and the stage-3 key
 // in registers.  kK > 0: horizon specialised; kK == 0: any horizon.
 template <bool kKeys, int kK>
-__global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
+__global__ void __launch_bounds__(kLightThreads, 6) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
                                                                        int report_missing) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
