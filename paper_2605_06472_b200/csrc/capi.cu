@@ -83,6 +83,10 @@ void set_device(Context& c) { PBKV_CUDA(cudaSetDevice(c.device)); }
 
 // ---- forecast slots ----------------------------------------------------------
 int slot_for(Context& c, std::int64_t wf) {
+    // dense ids (the simulator allocates WorkflowIds monotonically) hit a
+    // direct table; others fall back to the hash map
+    if (wf >= 0 && wf < static_cast<std::int64_t>(c.slot_dense.size()) && c.slot_dense[static_cast<std::size_t>(wf)] >= 0)
+        return c.slot_dense[static_cast<std::size_t>(wf)];
     auto it = c.slot_of.find(wf);
     if (it != c.slot_of.end()) return it->second;
     int s = static_cast<int>(c.n_slots);
@@ -102,6 +106,11 @@ int slot_for(Context& c, std::int64_t wf) {
         PBKV_CUDA(cudaMemsetAsync(c.rem_has.p + old, 0, c.rem_has.cap - old, c.stream));
     c.n_slots += 1;
     c.slot_of.emplace(wf, s);
+    if (wf >= 0 && wf < (1ll << 24)) {
+        if (static_cast<std::size_t>(wf) >= c.slot_dense.size())
+            c.slot_dense.resize(std::max<std::size_t>(static_cast<std::size_t>(wf) + 1, 2 * c.slot_dense.size()), -1);
+        c.slot_dense[static_cast<std::size_t>(wf)] = s;
+    }
     c.h_slot_wf.push_back(wf);
     return s;
 }
@@ -490,16 +499,9 @@ HKey make_hkey(int cls, double rank, unsigned long long last, int id) {
 // that cannot be proved (the caller then runs the exact chains).
 bool place_deferred(Context& c, long long* result_dev, const SelectCounts& o, std::int64_t needed) {
     if (o.shortfall || o.n_victims == 0) return false;
+    (void)result_dev;  // the reports were fetched with the selection's readback (run_select)
     const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
     const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
-    c.hreport.reserve(bytes);
-    c.hreport_h.reserve(bytes + 2 * nh * sizeof(double));
-    HeavyReport* rep_d = reinterpret_cast<HeavyReport*>(c.hreport.p);
-    launch_heavy_report(c, result_dev, rep_d);
-    PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p, rep_d, bytes, cudaMemcpyDeviceToHost, c.stream));
-    PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p + bytes, c.happrox.p, 2 * nh * sizeof(double), cudaMemcpyDeviceToHost,
-                              c.stream));
-    PBKV_CUDA(cudaStreamSynchronize(c.stream));
     const HeavyReport* rep = reinterpret_cast<const HeavyReport*>(c.hreport_h.p);
     const double* ap = reinterpret_cast<const double*>(c.hreport_h.p + bytes);
     const HeavyReport& tail = rep[nh];
@@ -602,7 +604,9 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
         launch_keys_cached(c, policy);
     }
     record(c, 1);
+    c.report_deferred = defer;
     SelectCounts o = run_select(c, locked_dev, n_locked, needed, recompute, result_dev);
+    c.report_deferred = false;
     if (defer) {
         const bool placed = place_deferred(c, result_dev ? result_dev : c.counters.p + 8, o, needed);
         launch_set_deferred(c, false);

@@ -211,11 +211,13 @@ struct Context {
     DevBuf<unsigned char> hreport;            // deferred-heavy reports + the tail record
     PinBuf<unsigned char> hreport_h;
     bool defer_heavy = true;                  // decision fast path enabled
+    bool report_deferred = false;             // run_select also fetches the heavy reports
     long long defer_fast = 0, defer_slow = 0; // fast / slow path counts
     std::int64_t device_capacity = 0, device_used = 0, retired_device_tokens = 0, host_capacity = 0, host_used = 0;
     int max_depth = 0;
     std::vector<std::int64_t> h_slot_wf;  // slot -> WorkflowId
     std::unordered_map<std::int64_t, int> slot_of;
+    std::vector<int> slot_dense;  // direct slot table for WorkflowIds < 2^24
 
     // ---- forecasts ----------------------------------------------------------
     DevBuf<double> P;   // [slots][V1][K] agent-major

@@ -1199,6 +1199,17 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     if (c.timing) PBKV_CUDA(cudaEventRecord(c.kev[3], c.stream));
     ++c.launches;
     PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
+    if (c.report_deferred) {  // the deferred-heavy reports ride on the same synchronisation
+        const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
+        const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
+        c.hreport.reserve(bytes);
+        c.hreport_h.reserve(bytes + 2 * nh * sizeof(double));
+        HeavyReport* rep_d = reinterpret_cast<HeavyReport*>(c.hreport.p);
+        launch_heavy_report(c, reinterpret_cast<long long*>(res), rep_d);
+        PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p, rep_d, bytes, cudaMemcpyDeviceToHost, c.stream));
+        PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p + bytes, c.happrox.p, 2 * nh * sizeof(double),
+                                  cudaMemcpyDeviceToHost, c.stream));
+    }
     check_status(c);  // synchronises
     SelectCounts out;
     c.phase_ns.assign(hs->ts, hs->ts + (hs->n_ts < 40 ? hs->n_ts : 40));
@@ -1267,6 +1278,13 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         PBKV_CUDA(cudaGetLastError());
         c.launches += 2;
         PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
+        if (c.report_deferred) {  // the victims changed: fetch the tail record again
+            const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
+            const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
+            HeavyReport* rep_d = reinterpret_cast<HeavyReport*>(c.hreport.p);
+            launch_heavy_report(c, reinterpret_cast<long long*>(res), rep_d);
+            PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p, rep_d, bytes, cudaMemcpyDeviceToHost, c.stream));
+        }
         PBKV_CUDA(cudaStreamSynchronize(c.stream));
     }
     out.n_victims = static_cast<std::int64_t>(hs->n_victims);
