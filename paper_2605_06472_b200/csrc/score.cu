@@ -65,31 +65,66 @@ __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsign
     double m[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) m[k] = 0.0;
+    // agents in groups of 4: all rows of a group are loaded before any is
+    // added (one L2 round trip per group instead of per agent), then added in
+    // ascending agent order (forecast.hpp:66-67)
+    constexpr int kG = kK <= 4 ? 4 : 2;
     while (b) {
-        const int a = __ffsll(static_cast<long long>(b)) - 1;
-        b &= b - 1;
-        const double* row = pw + static_cast<std::size_t>(a) * kK;  // the K steps of agent a, contiguous
-        if constexpr (kK % 2 == 0) {
+        const double* row[kG];
+        int cnt = 0;
 #pragma unroll
-            for (int k = 0; k < kK; k += 2) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(row + k));
-                m[k] = __dadd_rn(m[k], v.x);
-                m[k + 1] = __dadd_rn(m[k + 1], v.y);
+        for (int j = 0; j < kG; ++j) {
+            row[j] = nullptr;
+            if (b) {
+                row[j] = pw + static_cast<std::size_t>(__ffsll(static_cast<long long>(b)) - 1) * kK;
+                b &= b - 1;
+                cnt = j + 1;
             }
-        } else {
+        }
+        double v[kG][kK];
 #pragma unroll
-            for (int k = 0; k < kK; ++k) m[k] = __dadd_rn(m[k], __ldg(row + k));
+        for (int j = 0; j < kG; ++j) {
+            if (j >= cnt) continue;
+            if constexpr (kK % 2 == 0) {
+#pragma unroll
+                for (int k = 0; k < kK; k += 2) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(row[j] + k));
+                    v[j][k] = t.x;
+                    v[j][k + 1] = t.y;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kK; ++k) v[j][k] = __ldg(row[j] + k);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            if (j >= cnt) continue;
+#pragma unroll
+            for (int k = 0; k < kK; ++k) m[k] = __dadd_rn(m[k], v[j][k]);
         }
     }
+    double gv[kK];
+    if constexpr (kK % 2 == 0) {
 #pragma unroll
-    for (int k = 0; k < kK; ++k) total = __dadd_rn(total, __dmul_rn(__ldg(g + k), m[k]));
+        for (int k = 0; k < kK; k += 2) {
+            const double2 t = __ldg(reinterpret_cast<const double2*>(g + k));
+            gv[k] = t.x;
+            gv[k + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kK; ++k) gv[k] = __ldg(g + k);
+    }
+#pragma unroll
+    for (int k = 0; k < kK; ++k) total = __dadd_rn(total, __dmul_rn(gv[k], m[k]));
 }
 
 // ---------------------------------------------------------------------------
 // Light nodes (<= 2 entries): one thread per node, Eq. 2 and the stage-3 key
 // in registers.  kK > 0: horizon specialised; kK == 0: any horizon.
 template <bool kKeys, int kK>
-__global__ void __launch_bounds__(kLightThreads, 6) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
+__global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
                                                                        int report_missing) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
