@@ -82,6 +82,18 @@ void invalid(const std::string& what) { throw ApiError(PBKV_EINVAL, what); }
 void set_device(Context& c) { PBKV_CUDA(cudaSetDevice(c.device)); }
 
 // ---- forecast slots ----------------------------------------------------------
+// A slot without a usable forecast (missing, dropped, or horizon < K beyond
+// its last step) holds NaN rows: the light Eq. 2 pass then needs no per-entry
+// state lookup -- a NaN total marks a missing forecast (validated forecasts
+// are finite), and the exact message comes from fstate on the error path.
+std::size_t s_new_slot(const Context& c) { return static_cast<std::size_t>(c.n_slots); }
+
+void poison_slot(Context& c, std::size_t slot) {
+    const std::size_t row = static_cast<std::size_t>(c.K) * c.V1;
+    PBKV_CUDA(cudaMemsetAsync(c.P.p + slot * row, 0xFF, row * sizeof(double), c.stream));
+    PBKV_CUDA(cudaMemsetAsync(c.Pg.p + slot * row, 0xFF, row * sizeof(double), c.stream));
+}
+
 int slot_for(Context& c, std::int64_t wf) {
     // dense ids (the simulator allocates WorkflowIds monotonically) hit a
     // direct table; others fall back to the hash map
@@ -95,6 +107,7 @@ int slot_for(Context& c, std::int64_t wf) {
     std::size_t old = static_cast<std::size_t>(c.n_slots);
     c.P.grow_keep(need_slots * c.K * c.V1, old * c.K * c.V1, c.stream);
     c.Pg.grow_keep(need_slots * c.K * c.V1, old * c.K * c.V1, c.stream);
+    poison_slot(c, s_new_slot(c));
     c.gs.grow_keep(need_slots * c.K, old * c.K, c.stream);
     std::size_t old_cap = c.fstate.cap;
     c.fstate.grow_keep(need_slots, old, c.stream);
@@ -859,6 +872,7 @@ int pbkv_forecast_drop(pbkv_ctx* c, const int64_t* wf, int64_t n) {
             auto it = c->slot_of.find(wf[i]);
             if (it == c->slot_of.end()) continue;
             PBKV_CUDA(cudaMemsetAsync(c->fstate.p + it->second, 0, 1, c->stream));
+            poison_slot(*c, static_cast<std::size_t>(it->second));
         }
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
     });
@@ -868,7 +882,12 @@ int pbkv_forecast_clear(pbkv_ctx* c) {
     return api(c, [&] {
         need(c, "null ctx");
         set_device(*c);
-        if (c->n_slots > 0) PBKV_CUDA(cudaMemsetAsync(c->fstate.p, 0, static_cast<std::size_t>(c->n_slots), c->stream));
+        if (c->n_slots > 0) {
+            const std::size_t rows = static_cast<std::size_t>(c->n_slots) * c->K * c->V1;
+            PBKV_CUDA(cudaMemsetAsync(c->fstate.p, 0, static_cast<std::size_t>(c->n_slots), c->stream));
+            PBKV_CUDA(cudaMemsetAsync(c->P.p, 0xFF, rows * sizeof(double), c->stream));
+            PBKV_CUDA(cudaMemsetAsync(c->Pg.p, 0xFF, rows * sizeof(double), c->stream));
+        }
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
     });
 }

@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a) {
         const int i = idx / (a.K * a.V1), r = idx % (a.K * a.V1);
         const int k = r / a.V1, v = r % a.V1;  // agent-major store: P[slot][v][k]
         a.P[static_cast<std::size_t>(a.slots[w0 + i]) * a.K * a.V1 + static_cast<std::size_t>(v) * a.K + k] =
-            k < KK ? pp[i * KV + r] : 0.0;
+            k < KK ? pp[i * KV + r] : CUDART_NAN;  // horizon < K: unusable rows (see capi.cu poison_slot)
     }
     if (a.probs_out)
         for (int idx = threadIdx.x; idx < nw * KV; idx += kHeadThreads)
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a) {
         const int v = r / a.K, k = r % a.K;  // agent-major position
         const std::size_t base = static_cast<std::size_t>(a.slots[w0 + i]) * a.K * a.V1;
         const double g = a.gs[static_cast<std::size_t>(a.slots[w0 + i]) * a.K + k];
-        a.Pg[base + r] = __dmul_rn(g, __dadd_rn(0.0, k < KK ? pp[i * KV + k * a.V1 + v] : 0.0));
+        a.Pg[base + r] = k < KK ? __dmul_rn(g, __dadd_rn(0.0, pp[i * KV + k * a.V1 + v])) : CUDART_NAN;
     }
 }
 

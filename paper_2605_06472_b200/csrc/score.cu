@@ -137,16 +137,18 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
             for (unsigned int e = e0; e < e1; ++e) {
                 const int slot = __ldg(s.acc_slot + e);
                 const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
-                const std::uint8_t fs = __ldg(s.fstate + slot);
-                if (fs != 1) {
-                    (fs == 2 ? shorth : miss) = true;
-                    continue;
-                }
-                if constexpr (kK > 0)
-                    eq2_entry_k<kK>(s, slot, b, total);
-                else
+                if constexpr (kK > 0) {
+                    eq2_entry_k<kK>(s, slot, b, total);  // unusable slots hold NaN rows
+                } else {
+                    const std::uint8_t fs = __ldg(s.fstate + slot);
+                    if (fs != 1) {
+                        (fs == 2 ? shorth : miss) = true;
+                        continue;
+                    }
                     eq2_entry(s, slot, b, total);
+                }
             }
+            if constexpr (kK > 0) miss = isnan(total);  // the message is resolved from fstate on error
             s.out[n] = total;
             if (report_missing && (miss || shorth))
                 set_error(s.st, PBKV_EINVAL, miss ? kErrMissingForecast : kErrShortHorizon, n);
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(256) forecast_prepare_kernel(const double* sta
         double* dst = P + static_cast<std::size_t>(slot) * K * V1;
         for (int idx = lane; idx < K * V1; idx += 32) {  // dst[a][k], coalesced stores
             const int a = idx / K, k = idx % K;
-            dst[idx] = k < H ? p[k * V1 + a] : 0.0;
+            dst[idx] = k < H ? p[k * V1 + a] : CUDART_NAN;  // horizon < K: unusable (NaN rows)
         }
         double* g = gs + static_cast<std::size_t>(slot) * K;
         if (lane == 0) {
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(256) forecast_prepare_kernel(const double* sta
         double* dg = Pg + static_cast<std::size_t>(slot) * K * V1;
         for (int idx = lane; idx < K * V1; idx += 32) {
             const int a = idx / K, k = idx % K;
-            dg[idx] = __dmul_rn(g[k], __dadd_rn(0.0, k < H ? p[k * V1 + a] : 0.0));
+            dg[idx] = k < H ? __dmul_rn(g[k], __dadd_rn(0.0, p[k * V1 + a])) : CUDART_NAN;
         }
     }
 }
