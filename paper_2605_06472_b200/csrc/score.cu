@@ -130,6 +130,15 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int n = static_cast<int>(i);
         const unsigned int e0 = s.acc_off[n], e1 = s.acc_off[n + 1];
+        // key inputs are independent of the Eq. 2 chain: issued up front
+        std::uint8_t fl = 0;
+        unsigned long long last = 0;
+        int ever = 0;
+        if constexpr (kKeys) {
+            fl = ka.flags[n];
+            last = ka.last[n];
+            ever = ka.ever[n];
+        }
         const bool light = (e1 - e0) <= 2u;
         double total = 0.0;
         bool miss = false, shorth = false;
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
             ka.sublock[n] = 0;
             if (light) {
                 ka.missing[n] = (miss || shorth) ? 1 : 0;
-                if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, total);
+                if (n != 0 && (fl & kFlagTierMask) == PBKV_TIER_DEVICE) write_key_v(ka, n, total, fl, last, ever);
             }
         }
     }
