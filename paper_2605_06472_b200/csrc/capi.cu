@@ -281,6 +281,8 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     std::vector<std::uint8_t> flags(static_cast<std::size_t>(n));
     std::vector<unsigned int> off(static_cast<std::size_t>(n) + 1);
     std::vector<int> slot(static_cast<std::size_t>(E));
+    std::vector<int2> lslot(static_cast<std::size_t>(n));
+    std::vector<ulonglong2> lbits(static_cast<std::size_t>(n));
     std::vector<int> medium, heavy, hent_node;
     std::vector<unsigned int> hent;
     std::vector<long long> hstart;
@@ -303,6 +305,24 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
         }
         const std::int64_t ne = b - a;
         c.h_entries[static_cast<std::size_t>(i)] = static_cast<int>(ne);
+        {
+            int2 ls{-1, -1};
+            ulonglong2 lb{0ull, 0ull};
+            if (ne > 2) {
+                ls.x = ls.y = -2;
+            } else {
+                if (ne >= 1) {
+                    ls.x = slot[static_cast<std::size_t>(a)];
+                    lb.x = s.acc_bits[a];
+                }
+                if (ne == 2) {
+                    ls.y = slot[static_cast<std::size_t>(a + 1)];
+                    lb.y = s.acc_bits[a + 1];
+                }
+            }
+            lslot[static_cast<std::size_t>(i)] = ls;
+            lbits[static_cast<std::size_t>(i)] = lb;
+        }
         // node classes of the Eq. 2 kernels (score.cu): light <= 2 entries,
         // medium chain <= kMediumMaxChain, heavy above
         if (ne * c.K > kMediumMaxChain) {
@@ -365,6 +385,8 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     c.last.reserve(n);
     c.score.reserve(n);
     c.acc_off.reserve(n + 1);
+    c.lslot.reserve(n);
+    c.lbits.reserve(n);
     c.acc_slot.reserve(E + 1);
     c.acc_bits.reserve(E + 1);
     c.heavy.reserve(heavy.size() + 1);
@@ -380,6 +402,8 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     else
         PBKV_CUDA(cudaMemsetAsync(c.score.p, 0, n * sizeof(double), st));
     PBKV_CUDA(cudaMemcpyAsync(c.acc_off.p, off.data(), (n + 1) * sizeof(unsigned int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.lslot.p, lslot.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.lbits.p, lbits.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice, st));
     if (E > 0) {
         PBKV_CUDA(cudaMemcpyAsync(c.acc_slot.p, slot.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
         PBKV_CUDA(cudaMemcpyAsync(c.acc_bits.p, s.acc_bits, E * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));

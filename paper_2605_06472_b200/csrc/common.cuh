@@ -122,6 +122,8 @@ struct ScoreArgs {
     const unsigned long long* acc_bits;
     const double* P;
     const double* Pg;  // gs-premultiplied rows (one-agent entries)
+    const int2* lslot;         // light nodes' entries, node-indexed
+    const ulonglong2* lbits;
     const double* gs;
     const std::uint8_t* fstate;
     int K, V1;

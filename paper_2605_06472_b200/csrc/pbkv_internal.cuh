@@ -188,6 +188,11 @@ struct Context {
     DevBuf<int> acc_slot;
     DevBuf<unsigned long long> acc_bits;
     std::vector<int> h_entries;  // entries per node (host copy, for id-list classification)
+    // node-indexed copy of the (at most two) access entries of every light
+    // node, so the light pass reads them coalesced, without the acc_off hop:
+    // lslot = {slot0, slot1} (-1 none, -2 the node is not light), lbits = bits
+    DevBuf<int2> lslot;
+    DevBuf<ulonglong2> lbits;
     // node classes for Eq. 2
     DevBuf<int> medium;  // 2 < entries, entries*K <= kMediumMaxChain
     std::int64_t n_medium = 0;

@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int n = static_cast<int>(i);
-        const unsigned int e0 = s.acc_off[n], e1 = s.acc_off[n + 1];
+        // the node's (at most two) entries, node-indexed and coalesced
+        const int2 ls = s.lslot[n];
+        const ulonglong2 lb = s.lbits[n];
         // key inputs are independent of the Eq. 2 chain: issued up front
         std::uint8_t fl = 0;
         unsigned long long last = 0;
@@ -139,13 +141,15 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
             last = ka.last[n];
             ever = ka.ever[n];
         }
-        const bool light = (e1 - e0) <= 2u;
+        const bool light = ls.x != -2;
         double total = 0.0;
         bool miss = false, shorth = false;
         if (light) {
-            for (unsigned int e = e0; e < e1; ++e) {
-                const int slot = __ldg(s.acc_slot + e);
-                const unsigned long long b = __ldg(s.acc_bits + e) & s.amask;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int slot = q == 0 ? ls.x : ls.y;
+                if (slot < 0) break;
+                const unsigned long long b = (q == 0 ? lb.x : lb.y) & s.amask;
                 if constexpr (kK > 0) {
                     eq2_entry_k<kK>(s, slot, b, total);  // unusable slots hold NaN rows
                 } else {
@@ -654,6 +658,8 @@ ScoreArgs make_score_args(Context& c, double* out) {
     s.acc_bits = c.acc_bits.p;
     s.P = c.P.p;
     s.Pg = c.Pg.p;
+    s.lslot = c.lslot.p;
+    s.lbits = c.lbits.p;
     s.gs = c.gs.p;
     s.fstate = c.fstate.p;
     s.K = c.K;
