@@ -29,6 +29,9 @@
 
 #include <cmath>
 #include <cstring>
+#include <vector>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 
@@ -505,6 +508,409 @@ __global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// head_mma_kernel: the MLP of the head on tcgen05, one
+// CTA per 128 workflows (= one UMMA M tile, TMEM lane = workflow row).
+//
+// Precision: each fp32 operand is split into bf16 hi + lo (x = hi + lo up to
+// 2^-16 relative) and every layer is the three products hi.hi + hi.lo + lo.hi
+// accumulated in fp32 in TMEM ("bf16x3"): the error is that of an fp32 dot
+// product, not of a bf16 one, so the tolerance of tests/test_predictor.py
+// holds unchanged.  Operands sit in shared memory as K-major 128-byte-swizzled
+// atoms (64 bf16 columns x rows, 8-row / 1024-byte groups); the weights arrive
+// pre-split and pre-swizzled from the host (predictor_load).
+//
+// Shared memory: region A (96 KB) = z hi/lo (3 + 3 atoms), later hidden hi/lo
+// (2 + 2 atoms); region W (96 KB) = W_m1 hi/lo (3 + 3 atoms of h1 rows), later
+// W_m2 hi/lo (2 + 2 atoms of N2 rows, loaded while the layer-1 epilogue runs);
+// after layer 2 both regions hold the logits [128][N2 + 1] fp32 for the
+// softmax epilogue (the per-step column offsets k*V1 are not 16-aligned, so
+// the rows go through shared memory rather than per-step tcgen05.ld).
+constexpr int kMT = 128;          // workflows per CTA
+constexpr int kMmaThreads = 512;  // 16 warps
+constexpr int kMmaH1 = 128;       // hidden width of the MMA head
+constexpr int kMmaMaxN2 = 192;    // 4 W_m2 atoms of N2 rows fit region W
+constexpr std::size_t kAtomRows = 128;  // bytes per swizzled row
+constexpr std::size_t kRegion = 6 * kMT * kAtomRows;  // 96 KB
+
+__host__ __device__ constexpr std::size_t sw128_off(int r, int c) {  // (row, col) in a 64-column atom
+    return static_cast<std::size_t>(r) * 128 + static_cast<std::size_t>(((c >> 3) ^ (r & 7)) << 4) +
+           static_cast<std::size_t>((c & 7) * 2);
+}
+
+__device__ __forceinline__ unsigned int idesc_bf16_n(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned int>(n >> 3) << 17) |
+           (static_cast<unsigned int>(kMT >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16_n(unsigned int tmem_d, unsigned long long a, unsigned long long b,
+                                            unsigned int idesc, unsigned int accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld16(unsigned int taddr, float* v) {
+    unsigned int u[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(u[i]);
+}
+
+// 1-D bulk copy global -> shared (async proxy), completion on `bar` (tx bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned int bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// bf16 hi/lo split of x into two swizzled atoms sets (hi at `hi`, lo at `lo`)
+__device__ __forceinline__ void put_split(unsigned char* hi, unsigned char* lo, std::size_t atom_bytes, int r, int col,
+                                          float x) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+    const std::size_t o = (col >> 6) * atom_bytes + sw128_off(r, col & 63);
+    *reinterpret_cast<__nv_bfloat16*>(hi + o) = h;
+    *reinterpret_cast<__nv_bfloat16*>(lo + o) = l;
+}
+
+// layer: D[128 x N] (+)= A . B^T over `atoms` 64-column K atoms, bf16x3
+__device__ __forceinline__ void issue_layer(unsigned int tmem_d, const unsigned char* a_hi, const unsigned char* a_lo,
+                                            std::size_t a_atom, const unsigned char* b_hi, const unsigned char* b_lo,
+                                            std::size_t b_atom, int atoms, unsigned int idesc) {
+    unsigned int acc = 0;
+    for (int kb = 0; kb < atoms; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long ah = umma_desc_sw128(a_hi + kb * a_atom) + 2ull * k;
+            const unsigned long long al = umma_desc_sw128(a_lo + kb * a_atom) + 2ull * k;
+            const unsigned long long bh = umma_desc_sw128(b_hi + kb * b_atom) + 2ull * k;
+            const unsigned long long bl = umma_desc_sw128(b_lo + kb * b_atom) + 2ull * k;
+            umma_bf16_n(tmem_d, ah, bh, idesc, acc);
+            acc = 1;
+            umma_bf16_n(tmem_d, ah, bl, idesc, 1);
+            umma_bf16_n(tmem_d, al, bh, idesc, 1);
+        }
+}
+
+// PBKV_HEAD_PROF: block 0 prints the cycles of each phase (tools/head_prof.sh)
+#ifdef PBKV_HEAD_PROF
+#define HEAD_STAMP(n) \
+    if (blockIdx.x == 0 && threadIdx.x == 0) tprof[n] = clock64();
+#else
+#define HEAD_STAMP(n)
+#endif
+
+__global__ void __launch_bounds__(kMmaThreads, 1)
+    head_mma_kernel(HeadArgs a, const unsigned char* __restrict__ w1s, const unsigned char* __restrict__ w2s, int N2,
+                    int rows) {
+#ifdef PBKV_HEAD_PROF
+    long long tprof[14];
+#endif
+    HEAD_STAMP(0);
+    constexpr int D = 64, H1 = kMmaH1;
+    constexpr std::size_t kAtomA = kMT * kAtomRows;   // 16 KB
+    constexpr std::size_t kAtomW1 = H1 * kAtomRows;   // 16 KB
+    const std::size_t atomW2 = static_cast<std::size_t>(N2) * kAtomRows;
+    extern __shared__ unsigned char hm_raw[];
+    unsigned char* rA =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(hm_raw) + 1023) & ~std::uintptr_t(1023));
+    unsigned char* rW = rA + kRegion;
+    unsigned int* sCnt = reinterpret_cast<unsigned int*>(rW + kRegion);  // [128][32]: 16-bit agent counts, 2 per word
+    int* sOff = reinterpret_cast<int*>(sCnt + kMT * 32);                    // [129] prefix offsets of the rows
+    int* sCur = sOff + kMT + 1;                                             // [128] current agent
+    float* sH2 = reinterpret_cast<float*>(sCur + kMT + 1);                  // [A <= 32][64]
+    float* sQK = sH2 + 32 * D;                                              // [A][A]
+    long long* sSlot = reinterpret_cast<long long*>(sQK + 32 * 32);         // [128] forecast slots
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(sSlot + kMT);
+    unsigned int* tmem_sh = reinterpret_cast<unsigned int*>(bar + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w0 = blockIdx.x * rows;  // rows (32/64/96/128) of the M = 128 tile carry workflows
+    const int V1 = a.V1, KV = a.Kp * V1;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) mbar_init(&bar[b], 1);  // MMA1, MMA2 done; W_m1, W_m2 landed
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // W_m1 hi/lo (pre-swizzled) by the bulk-copy engine, overlapping the z rows
+        mbar_expect_tx(&bar[2], static_cast<unsigned int>(6 * kAtomW1));
+        for (int b = 0; b < 6; ++b)
+            bulk_load(rW + b * kAtomW1, w1s + b * kAtomW1, static_cast<unsigned int>(kAtomW1), &bar[2]);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    const int nw = min(rows, a.n - w0);
+    for (int i = threadIdx.x; i <= nw; i += kMmaThreads) sOff[i] = a.pre_off[w0 + i];
+    for (int i = threadIdx.x; i < nw; i += kMmaThreads) sSlot[i] = a.slots[w0 + i];
+    for (int i = threadIdx.x; i < a.A * D; i += kMmaThreads) sH2[i] = __ldg(a.H2 + i);
+    for (int i = threadIdx.x; i < a.A * a.A; i += kMmaThreads) sQK[i] = __ldg(a.QK + i);
+    for (int i = threadIdx.x; i < rows * 32; i += kMmaThreads) sCnt[i] = 0u;
+    __syncthreads();
+    HEAD_STAMP(1);
+
+    // ---- z = [h_cur | h_path | h_txt].  The attention logit of a prefix
+    //      position depends on its agent only (the query is the current
+    //      agent's): h_path = sum_v n_v e_v H2[v] / sum_v n_v e_v over the
+    //      agents' counts n_v in the prefix. ----
+    unsigned char* zlo = rA + 3 * kAtomA;
+    {  // h_txt = ReLU(sum of the split-K partials, fixed order), every thread, coalesced
+        const std::size_t stride = static_cast<std::size_t>(a.n) * D;
+        // agent histogram over the rows' (contiguous) prefixes; the last position is the current
+        // agent.  Four positions in flight per thread.
+        const int q0 = sOff[0], q1 = sOff[nw];
+        for (int pb = q0 + threadIdx.x; pb < q1; pb += 4 * kMmaThreads) {
+            int vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) vv[u] = pb + u * kMmaThreads < q1 ? __ldg(a.pre + pb + u * kMmaThreads) : 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int p = pb + u * kMmaThreads;
+                if (p >= q1) break;
+                int lo = 0, hi = nw - 1;  // row: largest i with sOff[i] <= p
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sOff[mid] <= p) lo = mid; else hi = mid - 1;
+                }
+                const int v = vv[u];
+                if (p == sOff[lo + 1] - 1)
+                    sCur[lo] = v;
+                else
+                    atomicAdd(&sCnt[lo * 32 + (v >> 1)], 1u << ((v & 1) * 16));
+            }
+        }
+        HEAD_STAMP(10);
+        const float* pbase = a.part + static_cast<std::size_t>(w0) * D;
+        const int ne = nw * D;
+        for (int e0 = threadIdx.x; e0 < rows * D; e0 += 4 * kMmaThreads) {  // 4 elements in flight per thread
+            float z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+            for (int sp = 0; sp < a.splits; ++sp)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kMmaThreads;
+                    if (e < ne) z[u] += __ldcg(pbase + sp * stride + e);
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * kMmaThreads;
+                if (e < rows * D) put_split(rA, zlo, kAtomA, e >> 6, 128 + (e & 63), fmaxf(z[u], 0.f));
+            }
+        }
+    }
+    HEAD_STAMP(11);
+    __syncthreads();
+    HEAD_STAMP(12);
+    for (int i = warp; i < rows; i += kMmaThreads / 32) {  // h_cur, h_path: one warp per row
+        float zc0 = 0.f, zc1 = 0.f, zp0 = 0.f, zp1 = 0.f;  // dims lane, lane + 32
+        if (i < nw) {
+            const int cur = sCur[i];
+            zc0 = sH2[cur * D + lane];
+            zc1 = sH2[cur * D + lane + 32];
+            const unsigned int wc = sCnt[i * 32 + (lane >> 1)];  // agents lane, lane + 32
+            const unsigned int wc1 = sCnt[i * 32 + 16 + (lane >> 1)];
+            const int c0 = lane < a.A ? static_cast<int>((wc >> ((lane & 1) * 16)) & 0xFFFFu) : 0;
+            const int c1 = lane + 32 < a.A ? static_cast<int>((wc1 >> ((lane & 1) * 16)) & 0xFFFFu) : 0;
+            const float l0 = c0 ? sQK[cur * a.A + lane] : -INFINITY;
+            const float l1 = c1 ? sQK[cur * a.A + (lane + 32)] : -INFINITY;
+            float mx = fmaxf(l0, l1);
+            for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float e0 = c0 ? static_cast<float>(c0) * expf(l0 - mx) : 0.f;
+            const float e1 = c1 ? static_cast<float>(c1) * expf(l1 - mx) : 0.f;
+            float den = e0 + e1;
+            for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+            const float a0 = den > 0.f ? e0 / den : 0.f, a1 = den > 0.f ? e1 / den : 0.f;
+            for (int v = 0; v < a.A; ++v) {
+                const float av = __shfl_sync(0xffffffffu, v < 32 ? a0 : a1, v & 31);
+                zp0 = fmaf(av, sH2[v * D + lane], zp0);
+                zp1 = fmaf(av, sH2[v * D + lane + 32], zp1);
+            }
+        }
+        put_split(rA, zlo, kAtomA, i, lane, zc0);
+        put_split(rA, zlo, kAtomA, i, lane + 32, zc1);
+        put_split(rA, zlo, kAtomA, i, 64 + lane, zp0);
+        put_split(rA, zlo, kAtomA, i, 96 + lane, zp1);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    HEAD_STAMP(2);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned int tmem = *tmem_sh;
+
+    // ---- layer 1: D1[128 x H1] (TMEM columns 0..H1) ----
+    if (threadIdx.x == 0) {
+        mbar_wait(&bar[2], 0);
+        issue_layer(tmem, rA, rA + 3 * kAtomA, kAtomA, rW, rW + 3 * kAtomW1, kAtomW1, 3, idesc_bf16_n(H1));
+        umma_commit(&bar[0]);
+    }
+    __syncwarp();
+    mbar_wait(&bar[0], 0);
+    HEAD_STAMP(3);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x == 0) {  // W_m2 hi/lo into region W (layer 1 has consumed W_m1), overlapping epilogue 1
+        mbar_expect_tx(&bar[3], static_cast<unsigned int>(4 * atomW2));
+        for (int b = 0; b < 4; ++b)
+            bulk_load(rW + b * atomW2, w2s + b * atomW2, static_cast<unsigned int>(atomW2), &bar[3]);
+    }
+    if ((warp & 3) * 32 < rows) {  // epilogue 1: warp -> TMEM lane quarter (warp % 4) x 32 columns (warp / 4)
+        const int q = warp & 3, r = q * 32 + lane, c0 = (warp >> 2) * 32;
+        float v[32];
+        tmem_ld16(tmem + (static_cast<unsigned int>(q * 32) << 16) + static_cast<unsigned int>(c0), v);
+        tmem_ld16(tmem + (static_cast<unsigned int>(q * 32) << 16) + static_cast<unsigned int>(c0 + 16), v + 16);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            put_split(rA, rA + 2 * kAtomA, kAtomA, r, c0 + j, fmaxf(v[j] + __ldg(a.b1 + c0 + j), 0.f));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    HEAD_STAMP(4);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // ---- layer 2: D2[128 x N2] (TMEM columns H1..H1+N2) ----
+    if (threadIdx.x == 0) {
+        mbar_wait(&bar[3], 0);
+        issue_layer(tmem + H1, rA, rA + 2 * kAtomA, kAtomA, rW, rW + 2 * atomW2, atomW2, 2, idesc_bf16_n(N2));
+        umma_commit(&bar[1]);
+    }
+    __syncwarp();
+    mbar_wait(&bar[1], 0);
+    HEAD_STAMP(5);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- logits + b2 -> shared [128][N2 + 1] (regions A and W are free now) ----
+    float* lg = reinterpret_cast<float*>(rA);
+    const int LS = N2 + 1;
+    if ((warp & 3) * 32 < rows) {
+        const int q = warp & 3, r = q * 32 + lane;
+        for (int c0 = (warp >> 2) * 16; c0 < N2; c0 += 64) {
+            float v[16];
+            tmem_ld16(tmem + (static_cast<unsigned int>(q * 32) << 16) + static_cast<unsigned int>(H1 + c0), v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < KV) lg[r * LS + c0 + j] = v[j] + __ldg(a.b2 + c0 + j);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    HEAD_STAMP(6);
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+
+    // ---- per-step softmax (END a regular class), FP64 renormalisation: task = (row, step).
+    //      q_v = e_v / s (fp32) stays in place; sInv = 1 / sum_v double(q_v); every
+    //      store below uses p = double(q_v) * sInv, so P, Pg and probs_out agree bitwise. ----
+    const int KK = a.K < a.Kp ? a.K : a.Kp;
+    double* sInv = reinterpret_cast<double*>(rA + 100 * 1024);  // [128][Kp] 1 / sum (past the logits)
+    double* sGs = sInv + kMT * a.Kp;                             // [128][K]
+    for (int task = threadIdx.x; task < nw * a.Kp; task += kMmaThreads) {
+        const int i = task / a.Kp, k = task % a.Kp;
+        float* l = lg + i * LS + k * V1;
+        float mx = -INFINITY;
+        for (int v = 0; v < V1; ++v) mx = fmaxf(mx, l[v]);
+        float s = 0.f;
+        for (int v = 0; v < V1; ++v) {
+            const float e = expf(l[v] - mx);
+            l[v] = e;
+            s += e;
+        }
+        double tot = 0.0;
+        for (int v = 0; v < V1; ++v) {
+            const float qv = l[v] / s;
+            l[v] = qv;
+            tot += static_cast<double>(qv);
+        }
+        sInv[i * a.Kp + k] = 1.0 / tot;
+    }
+    __syncthreads();
+    HEAD_STAMP(7);
+    // ---- survival / gs chain per workflow (forecast_prepare_kernel semantics) ----
+    if (threadIdx.x < nw) {
+        const int i = threadIdx.x;
+        const long long slot = sSlot[i];
+        double surv = 1.0, gk = 1.0;
+        for (int k = 0; k < a.K; ++k) {
+            double g = 0.0;
+            if (k < KK) {
+                g = __dmul_rn(gk, surv);
+                const double pend = static_cast<double>(lg[i * LS + k * V1 + V1 - 1]) * sInv[i * a.Kp + k];
+                surv = __dmul_rn(surv, __dsub_rn(1.0, pend));
+                if (surv < 0.0) surv = 0.0;
+            }
+            sGs[i * a.K + k] = g;
+            a.gs[static_cast<std::size_t>(slot) * a.K + k] = g;
+            gk = __dmul_rn(gk, a.gamma);
+        }
+        a.fstate[slot] = a.Kp >= a.K ? 1 : 2;
+    }
+    __syncthreads();
+    HEAD_STAMP(8);
+    // ---- coalesced stores, one warp per row: P[slot][v][k] and Pg = gs[k] * (0.0 + P)
+    //      (NaN beyond the horizon), then probs_out[w][k][v] ----
+    const int KV1 = a.K * V1;
+    for (int i = warp; i < nw; i += kMmaThreads / 32) {
+        const std::size_t base = static_cast<std::size_t>(sSlot[i]) * KV1;
+        const float* li = lg + i * LS;
+        const double* inv = sInv + i * a.Kp;
+        const double* gsi = sGs + i * a.K;
+        for (int r = lane; r < KV1; r += 32) {
+            const int v = r / a.K, k = r - v * a.K;  // agent-major position
+            double p = CUDART_NAN, pg = CUDART_NAN;
+            if (k < KK) {
+                p = static_cast<double>(li[k * V1 + v]) * inv[k];
+                pg = __dmul_rn(gsi[k], __dadd_rn(0.0, p));
+            }
+            a.P[base + r] = p;
+            a.Pg[base + r] = pg;
+        }
+        if (a.probs_out) {
+            double* po = a.probs_out + static_cast<std::size_t>(w0 + i) * KV;
+            for (int r = lane; r < KV; r += 32) po[r] = static_cast<double>(li[r]) * inv[r / V1];
+        }
+    }
+    HEAD_STAMP(9);
+#ifdef PBKV_HEAD_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("head phases: tables %lld z %lld mma1 %lld epi1 %lld mma2 %lld logits %lld softmax %lld chain %lld store %lld\n",
+               tprof[1] - tprof[0], tprof[2] - tprof[1], tprof[3] - tprof[2], tprof[4] - tprof[3], tprof[5] - tprof[4],
+               tprof[6] - tprof[5], tprof[7] - tprof[6], tprof[8] - tprof[7], tprof[9] - tprof[8]);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("  z: txt %lld hist %lld sync %lld rows+sync %lld\n", tprof[10] - tprof[1], tprof[11] - tprof[10],
+               tprof[12] - tprof[11], tprof[2] - tprof[12]);
+#endif
+}
+
+std::size_t head_mma_smem() {
+    return 1024 + 2 * kRegion + (kMT * 32 + 2 * (kMT + 1) + 32 * 64 + 32 * 32) * 4 + kMT * 8 + 64;
+}
+
+// rows x cols fp32 (row-major) -> bf16 hi atoms then lo atoms, K-major 128B-swizzled,
+// `rows_pad` rows per atom (zero padding)
+std::vector<unsigned char> split_swizzle(const float* src, int rows, int rows_pad, int cols) {
+    const int atoms = cols / 64;
+    const std::size_t atom = static_cast<std::size_t>(rows_pad) * kAtomRows;
+    std::vector<unsigned char> out(2 * atoms * atom, 0);
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            const float x = src[static_cast<std::size_t>(r) * cols + c];
+            const __nv_bfloat16 h = __float2bfloat16_rn(x);
+            const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+            const std::size_t o = (c / 64) * atom + sw128_off(r, c % 64);
+            std::memcpy(out.data() + o, &h, 2);
+            std::memcpy(out.data() + atoms * atom + o, &l, 2);
+        }
+    return out;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -540,6 +946,8 @@ struct PredictorState {
     DevBuf<std::uint16_t> Wt;
     DevBuf<int> pre_off, pre;
     DevBuf<std::uint16_t> xbuf;
+    DevBuf<unsigned char> w1s, w2s;  // head_mma_kernel operands (bf16 hi/lo, swizzled); empty: fp32 head
+    int n2 = 0;
     CUtensorMap map_w{};
     int sms = 148;
 };
@@ -573,6 +981,19 @@ void predictor_load(Context& c, const pbkv_predictor_cfg& cfg, const pbkv_predic
     up(st->b1, w.mlp1_bias, static_cast<std::size_t>(h1));
     up(st->Wm2T, m2t.data(), m2t.size());
     up(st->b2, w.mlp2_bias, static_cast<std::size_t>(KV));
+    // tcgen05 head: d = 64, h1 = 128, K*V1 <= 192 (else the fp32 head_kernel)
+    if (d == 64 && h1 == kMmaH1 && KV <= kMmaMaxN2 && A <= 32 && cfg.horizon <= 16 && c.K <= 16 &&
+        cfg.max_prefix < 65536) {
+        st->n2 = (KV + 15) & ~15;
+        const auto b1 = split_swizzle(w.mlp1, h1, h1, 3 * d);
+        const auto b2 = split_swizzle(w.mlp2, KV, st->n2, h1);
+        st->w1s.reserve(b1.size());
+        st->w2s.reserve(b2.size());
+        PBKV_CUDA(cudaMemcpyAsync(st->w1s.p, b1.data(), b1.size(), cudaMemcpyHostToDevice, s));
+        PBKV_CUDA(cudaMemcpyAsync(st->w2s.p, b2.data(), b2.size(), cudaMemcpyHostToDevice, s));
+        PBKV_CUDA(cudaFuncSetAttribute(head_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(head_mma_smem())));
+    }
     st->Wt.reserve(static_cast<std::size_t>(d) * H);
     PBKV_CUDA(cudaMemcpyAsync(st->Wt.p, w.text, static_cast<std::size_t>(d) * H * 2, cudaMemcpyHostToDevice, s));
     st->H2.reserve(static_cast<std::size_t>(A) * d);
@@ -635,6 +1056,18 @@ void predictor_run(Context& c, std::int64_t n, const int* pre_off_dev, const int
     a.K = c.K;
     a.gamma = c.gamma;
     a.probs_out = probs_dev;
+    if (st.n2 > 0) {
+        // rows per CTA: a multiple of 32 that spreads the batch over all SMs (the
+        // MMA is nowhere near the bound; the per-row prefix attention is)
+        const std::int64_t per = (n + st.sms - 1) / st.sms;
+        const int rows = static_cast<int>(std::min<std::int64_t>(kMT, std::max<std::int64_t>(32, (per + 31) / 32 * 32)));
+        head_mma_kernel<<<static_cast<unsigned int>((n + rows - 1) / rows), kMmaThreads,
+                          head_mma_smem(), c.stream>>>(a, st.w1s.p, st.w2s.p, st.n2,
+                                                                                     rows);
+        PBKV_CUDA(cudaGetLastError());
+        c.launches += 2;
+        return;
+    }
     const std::size_t hsm = head_smem_bytes(cfg.num_agents, d, cfg.hidden, cfg.horizon * V1);
     PBKV_CUDA(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hsm)));
     head_kernel<<<static_cast<unsigned int>((n + kHeadWf - 1) / kHeadWf), kHeadThreads, hsm, c.stream>>>(a);

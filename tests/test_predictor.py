@@ -42,12 +42,17 @@ def _check(P_gpu, P_ref):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,A,K,H,maxp", [(1, 4, 3, 64, 1), (37, 4, 3, 128, 5), (256, 16, 4, 512, 64),
-                                           (300, 9, 3, 5120, 64), (1000, 16, 8, 5120, 64), (129, 63, 2, 192, 17)])
-def test_predict_matches_fp64(gpu, n, A, K, H, maxp):
+@pytest.mark.parametrize("n,A,K,H,maxp,h1", [(1, 4, 3, 64, 1, 128), (37, 4, 3, 128, 5, 128), (256, 16, 4, 512, 64, 128),
+                                              (300, 9, 3, 5120, 64, 128), (1000, 16, 8, 5120, 64, 128),
+                                              (129, 63, 2, 192, 17, 128), (4096, 16, 8, 5120, 64, 128),
+                                              # fp32 head_kernel shapes (h1 != 128, K*V1 > 192)
+                                              (200, 16, 8, 256, 9, 96), (130, 31, 7, 256, 9, 128)])
+def test_predict_matches_fp64(gpu, n, A, K, H, maxp, h1):
+    """h1 = 128 and K*V1 <= 192 run the tcgen05 head (bf16x3 split
+    products, fp32 accumulation in TMEM); other shapes the fp32 head."""
     from paper_2605_06472_b200.api import Policy
 
-    w = PredictorWeights.random(num_agents=A, horizon=K, text_dim=H, seed=n + A)
+    w = PredictorWeights.random(num_agents=A, horizon=K, hidden=h1, text_dim=H, seed=n + A)
     off, pre, x = random_inputs(n, A, H, max_prefix=maxp, seed=n)
     pol = Policy(num_agents=A, k=K, gamma=0.7)
     pol.load_predictor(w, max_prefix=max(maxp, 1))
