@@ -39,6 +39,33 @@ __device__ __forceinline__ void eq2_entry(const ScoreArgs& s, int slot, unsigned
     for (int k = 0; k < K; ++k) total = __dadd_rn(total, __dmul_rn(__ldg(g + k), mass_on(pw + k, K, b)));
 }
 
+// One 32-byte global load (LDG.E.256, sm_100): a gathered row of 4 doubles
+// costs one L1 wavefront per lane instead of two with 16-byte loads.
+__device__ __forceinline__ void ldg4d(const double* p, double* v) {
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+        : "l"(p));
+}
+
+// kK doubles from a row aligned to min(kK, 4) * 8 bytes, widest loads first
+template <int kK>
+__device__ __forceinline__ void load_row(const double* p, double* v) {
+    if constexpr (kK % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < kK; k += 4) ldg4d(p + k, v + k);
+    } else if constexpr (kK % 2 == 0) {
+#pragma unroll
+        for (int k = 0; k < kK; k += 2) {
+            const double2 t = __ldg(reinterpret_cast<const double2*>(p + k));
+            v[k] = t.x;
+            v[k + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kK; ++k) v[k] = __ldg(p + k);
+    }
+}
+
 // Eq. 2 of one access entry with the horizon known at compile time: the K
 // step masses are accumulated agent by agent (ascending, forecast.hpp:66-67)
 // in K independent registers, so the K row loads of each agent are in flight
@@ -47,17 +74,10 @@ template <int kK>
 __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsigned long long b, double& total) {
     if (b && !(b & (b - 1))) {  // one agent: the K terms are precomputed (Pg), one 64-byte line
         const double* row = s.Pg + (static_cast<std::size_t>(slot) * s.V1 + (__ffsll(static_cast<long long>(b)) - 1)) * kK;
-        if constexpr (kK % 2 == 0) {
+        double v[kK];
+        load_row<kK>(row, v);
 #pragma unroll
-            for (int k = 0; k < kK; k += 2) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(row + k));
-                total = __dadd_rn(total, v.x);
-                total = __dadd_rn(total, v.y);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kK; ++k) total = __dadd_rn(total, __ldg(row + k));
-        }
+        for (int k = 0; k < kK; ++k) total = __dadd_rn(total, v[k]);
         return;
     }
     const double* pw = s.P + static_cast<std::size_t>(slot) * s.V1 * kK;  // [agent][k]
@@ -65,8 +85,8 @@ __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsign
     double m[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) m[k] = 0.0;
-    // agents in groups of 4: all rows of a group are loaded before any is
-    // added (one L2 round trip per group instead of per agent), then added in
+    // agents in groups: all rows of a group are loaded before any is added
+    // (one L2 round trip per group instead of per agent), then added in
     // ascending agent order (forecast.hpp:66-67)
     constexpr int kG = kK <= 4 ? 4 : 2;
     while (b) {
@@ -85,17 +105,7 @@ __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsign
 #pragma unroll
         for (int j = 0; j < kG; ++j) {
             if (j >= cnt) continue;
-            if constexpr (kK % 2 == 0) {
-#pragma unroll
-                for (int k = 0; k < kK; k += 2) {
-                    const double2 t = __ldg(reinterpret_cast<const double2*>(row[j] + k));
-                    v[j][k] = t.x;
-                    v[j][k + 1] = t.y;
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < kK; ++k) v[j][k] = __ldg(row[j] + k);
-            }
+            load_row<kK>(row[j], v[j]);
         }
 #pragma unroll
         for (int j = 0; j < kG; ++j) {
@@ -105,17 +115,7 @@ __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsign
         }
     }
     double gv[kK];
-    if constexpr (kK % 2 == 0) {
-#pragma unroll
-        for (int k = 0; k < kK; k += 2) {
-            const double2 t = __ldg(reinterpret_cast<const double2*>(g + k));
-            gv[k] = t.x;
-            gv[k + 1] = t.y;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kK; ++k) gv[k] = __ldg(g + k);
-    }
+    load_row<kK>(g, gv);
 #pragma unroll
     for (int k = 0; k < kK; ++k) total = __dadd_rn(total, __dmul_rn(gv[k], m[k]));
 }
