@@ -141,6 +141,9 @@ void ensure_scratch(Context& c) {
     c.listB.reserve(n);
     c.listS.reserve(n);
     c.listS2.reserve(n);
+    c.listSK.reserve(n);
+    c.listSC.reserve(n);
+    c.listSC2.reserve(n);
     c.big.reserve(2 * n);
     c.rank.reserve(n);
     c.vid_out.reserve(n);

@@ -249,6 +249,8 @@ struct Context {
     DevBuf<unsigned int> C;
     DevBuf<int> rank;
     DevBuf<int> heads, listB, listS, listS2;
+    DevBuf<ulonglong2> listSK;
+    DevBuf<unsigned int> listSC, listSC2;
     DevBuf<unsigned int> big;  // [2 * n]: (offset, count) of buckets sorted by rank counting
     DevBuf<unsigned long long> hist_w, part_w;
     DevBuf<unsigned int> hist_c, part_c, seg_off, seg_cnt, cursor;

@@ -91,8 +91,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-__device__ __forceinline__ void stamp(SelState* ss) {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && ss->n_ts < 40) ss->ts[ss->n_ts++] = gtimer();
+// stores only (a load of the counter would stall thread 0 while the grid waits on it)
+__device__ __forceinline__ void stamp(SelState* ss, int& nts) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nts < 40) {
+        ss->ts[nts] = gtimer();
+        ss->n_ts = ++nts;
+    }
 }
 
 __device__ __forceinline__ unsigned long long key_word(const Key2& k, int id, int w) {
@@ -197,15 +201,22 @@ __device__ __forceinline__ long long block_append(unsigned long long* counter, b
     return slot;
 }
 
-// order-preserving packing of the varying bits of (w0, w1, id) into 64 bits
+// order-preserving packing of the varying bits of (w0, w1, id) into 64 bits;
+// the masks are walked a run of consecutive set bits at a time (the varying
+// bits are typically one or two runs per word: timestamp and id low bits)
 __device__ __forceinline__ unsigned long long pack_key(const Key2& k, int id, unsigned long long v0,
                                                        unsigned long long v1, unsigned long long v2) {
     unsigned long long r = 0;
     auto ext = [&](unsigned long long word, unsigned long long mask) {
         while (mask) {
-            const int b = 63 - __clzll(static_cast<long long>(mask));
-            r = (r << 1) | ((word >> b) & 1ull);
-            mask &= ~(1ull << b);
+            const int hi = 63 - __clzll(static_cast<long long>(mask));
+            // run of ones ending at bit hi (downward)
+            const unsigned long long above_cleared = ~mask & ((hi == 63) ? ~0ull : ((1ull << (hi + 1)) - 1ull));
+            const int lo = above_cleared ? 64 - __clzll(static_cast<long long>(above_cleared)) : 0;
+            const int len = hi - lo + 1;
+            const unsigned long long run = (len == 64) ? ~0ull : ((1ull << len) - 1ull);
+            r = (len == 64 ? 0ull : (r << len)) | ((word >> lo) & run);
+            mask &= ~(run << lo);
         }
     };
     ext(k.w0, v0);
@@ -230,6 +241,9 @@ struct SelArgs {
     int* listB;
     int* listS;
     int* listS2;        // S, sorted (rank-counting / warp sorts write here)
+    ulonglong2* listSK;     // key of S[i] (written with S by the compaction: the sort reads it coalesced)
+    unsigned int* listSC;   // chain size C of S[i]
+    unsigned int* listSC2;  // chain size of S2[i]
     unsigned int* big;  // (offset, count) of the buckets with > 32 heads
     int* sorted;
     unsigned long long* start;
@@ -439,7 +453,13 @@ __device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsig
         // (e.g. every retired head in one bucket) would serialise on one bank
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         unsigned long long sum = 0;
-        for (unsigned m = peers; m; m &= m - 1) sum += __shfl_sync(peers, w, __ffs(m) - 1);
+        if (peers == 0xffffffffu) {  // one digit across the warp (the skewed case): butterfly
+            sum = w;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        } else {
+            for (unsigned m = peers; m; m &= m - 1) sum += __shfl_sync(peers, w, __ffs(m) - 1);
+        }
         if (d != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) {
             atomicAdd(&hw[d], sum);
             atomicAdd(&hc[d], static_cast<unsigned int>(__popc(peers)));
@@ -557,9 +577,13 @@ __device__ __forceinline__ void phase_compact(const SelArgs& a, const int* L, un
             const int lane = threadIdx.x & 31;
             const int leader = __ffs(peers) - 1;
             unsigned int basepos = 0;
+            const unsigned int cx = __ldcg(&a.C[x]);  // in flight with the cursor atomic
             if (lane == leader) basepos = atomicAdd(&cur[d], static_cast<unsigned int>(__popc(peers)));
             basepos = __shfl_sync(peers, basepos, leader);
-            S[off_sh[d] + basepos + __popc(peers & ((1u << lane) - 1u))] = x;
+            const unsigned int pos = off_sh[d] + basepos + __popc(peers & ((1u << lane) - 1u));
+            S[pos] = x;
+            a.listSK[pos] = make_ulonglong2(k.w0, k.w1);
+            a.listSC[pos] = cx;
             for (int w = 0; w < 3; ++w) {
                 orS[w] |= key_word(k, x, w);
                 andS[w] &= key_word(k, x, w);
@@ -595,7 +619,12 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S,
     const bool in = static_cast<unsigned int>(lane) < cnt;
     const int x = in ? __ldcg(&S[off + lane]) : -1;
     Key2 k{0, 0};
-    if (in) k = load_key(a.keys, x);
+    unsigned int cx = 0;
+    if (in) {
+        const ulonglong2 kk = __ldcg(&a.listSK[off + lane]);
+        k = Key2{kk.x, kk.y};
+        cx = __ldcg(&a.listSC[off + lane]);
+    }
     int rank = 0;
     for (unsigned int j = 0; j < cnt; ++j) {
         const unsigned long long b0 = __shfl_sync(0xffffffffu, k.w0, j);
@@ -603,7 +632,10 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S,
         const int bv = __shfl_sync(0xffffffffu, x, j);
         rank += sk_less(b0, b1, bv, k.w0, k.w1, x) ? 1 : 0;
     }
-    if (in) S2[off + rank] = x;
+    if (in) {
+        S2[off + rank] = x;
+        a.listSC2[off + rank] = cx;
+    }
 }
 
 // Buckets with > 32 heads: every element's rank is the number of smaller keys
@@ -613,7 +645,9 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S,
 constexpr int kRankChunk = 64;
 constexpr int kBigSh = 512;  // bucket-list entries cached in shared memory
 __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, int* S2, unsigned int n_big,
-                                              unsigned long long* k0, unsigned long long* k1, int* val) {
+                                              unsigned long long* k0, unsigned long long* k1, int* val,
+                                              bool packed, bool has_sk, unsigned long long v0,
+                                              unsigned long long v1, unsigned long long v2) {
     // the bucket list is read once into shared memory (a serial walk of L2
     // loads per CTA cost ~1 us per bucket)
     __shared__ unsigned int big_sh[2 * kBigSh];
@@ -632,42 +666,78 @@ __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, in
         unsigned int c = (blockIdx.x + gridDim.x - task % gridDim.x) % gridDim.x;
         if (c < nch) {
             __syncthreads();
+            const unsigned long long tl0 = gtimer();
+            // the bucket's ids, keys and chain sizes: coalesced reads of S / SK / SC
+            // (the head list of take_all has no SK / SC: gathered instead)
             for (unsigned int i = threadIdx.x; i < cnt; i += blockDim.x) {
                 const int x = __ldcg(&S[off + i]);
-                const Key2 k = load_key(a.keys, x);
-                k0[i] = k.w0;
-                k1[i] = k.w1;
+                Key2 k;
+                unsigned int cz = 0;
+                if (has_sk) {
+                    const ulonglong2 kk = __ldcg(&a.listSK[off + i]);
+                    k = Key2{kk.x, kk.y};
+                    if (packed) cz = __ldcg(&a.listSC[off + i]);
+                } else {
+                    k = load_key(a.keys, x);
+                    if (packed) cz = __ldcg(&a.C[x]);
+                }
+                if (packed) {  // k1 is free: it carries the chain sizes
+                    k0[i] = pack_key(k, x, v0, v1, v2);
+                    k1[i] = cz;
+                } else {
+                    k0[i] = k.w0;
+                    k1[i] = k.w1;
+                }
                 val[i] = x;
             }
             __syncthreads();
+            const unsigned long long tl1 = gtimer();
+            if (threadIdx.x == 0) atomicMax(&a.ss->dbg[2], tl1 - tl0);
             for (; c < nch; c += gridDim.x) {
                 const unsigned int e = c * kRankChunk + threadIdx.x / 8, part = threadIdx.x % 8;
                 const bool in = e < cnt;
-                const unsigned long long a0 = in ? k0[e] : 0ull, a1 = in ? k1[e] : 0ull;
+                const unsigned long long a0 = in ? k0[e] : 0ull, a1 = in && !packed ? k1[e] : 0ull;
                 const int av = in ? val[e] : -1;
                 unsigned int r = 0;
-                if (in)
+                if (in && packed) {  // distinct 64-bit order-preserving keys: one compare each
+#pragma unroll 4
+                    for (unsigned int q = part; q < cnt; q += 8) r += k0[q] < a0 ? 1u : 0u;
+                } else if (in) {
                     for (unsigned int q = part; q < cnt; q += 8) r += sk_less(k0[q], k1[q], val[q], a0, a1, av) ? 1u : 0u;
+                }
                 r += __shfl_xor_sync(0xffffffffu, r, 1);
                 r += __shfl_xor_sync(0xffffffffu, r, 2);
                 r += __shfl_xor_sync(0xffffffffu, r, 4);
-                if (in && part == 0) S2[off + r] = av;
+                if (in && part == 0) {
+                    S2[off + r] = av;
+                    a.listSC2[off + r] = packed ? static_cast<unsigned int>(k1[e])
+                                                : (has_sk ? __ldcg(&a.listSC[off + e]) : __ldcg(&a.C[av]));
+                }
             }
+            if (threadIdx.x == 0) atomicMax(&a.ss->dbg[3], gtimer() - tl1);
         }
         task += nch;
     }
 }
 
-// every eligible node of a selected chain lands at start[rank(head)] + d
-__device__ __forceinline__ void phase_scatter(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
-    for (std::int64_t i = tid; i < a.n_nodes; i += nthr) {
-        const int n = static_cast<int>(i);
-        if (n == 0 || (a.flags[n] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE || __ldcg(&a.sublock[n]))
-            continue;
-        const int h = __ldcg(&a.eff[n]);
-        const int r = __ldcg(&a.rank[h]);
-        if (r < 0) continue;
-        a.victims[__ldcg(&a.start[r]) + static_cast<unsigned long long>(a.depth[h] - a.depth[n])] = n;
+// every eligible node of a selected chain lands at start[rank(head)] + d:
+// each selected head walks its own chain (the contiguous eligible ancestors
+// with eff == head, d = depth difference), O(victims) instead of a pass over
+// every node
+__device__ __forceinline__ void phase_scatter(const SelArgs& a, const int* S2, unsigned long long nS,
+                                              std::int64_t tid, std::int64_t nthr) {
+    for (std::int64_t pos = tid; pos < static_cast<std::int64_t>(nS); pos += nthr) {
+        const int h = __ldcg(&S2[pos]);
+        unsigned long long at = __ldcg(&a.start[pos]);
+        int x = h;
+        for (;;) {
+            a.victims[at++] = x;
+            x = a.parent[x];
+            if (x <= 0) break;
+            const bool ok = (a.flags[x] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
+                            !__ldcg(&a.sublock[x]) && __ldcg(&a.eff[x]) == h;
+            if (!ok) break;
+        }
     }
 }
 
@@ -725,17 +795,18 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     SelState* ss = a.ss;
     const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    int nts = 0;
 
-    stamp(ss);
+    stamp(ss, nts);
     phase_lock(a, tid, nthr);
     grid.sync();
-    stamp(ss);
+    stamp(ss, nts);
     phase_eff(a, tid, nthr);
     grid.sync();
-    stamp(ss);
+    stamp(ss, nts);
     phase_chains(a, sm.sh);
     grid.sync();
-    stamp(ss);
+    stamp(ss, nts);
 
     // shared scalars are read once per CTA and broadcast through shared memory
     // (thousands of threads reading one L2 line serialise on its slice)
@@ -803,14 +874,14 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             }
             phase_hist(a, L, nL, lo, n_pass, sm.u.hist.w, sm.u.hist.c);
             grid.sync();
-            stamp(ss);
+            stamp(ss, nts);
             const PickOut pk = phase_pick(a, need, n_pass, nS, &sm.u.scan, sm.off, &sm.pick);
             phase_compact(a, L, nL, L2, cur ^ 1, S, n_pass, lo, pk.bucket, sm.off, sm.sh);
             need = pk.need;
             nS += pk.below_cnt;
             max_bucket = max(max_bucket, pk.max_cnt);
             grid.sync();
-            stamp(ss);
+            stamp(ss, nts);
             int* t = L;
             L = L2;
             L2 = t;
@@ -820,6 +891,8 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             const int x = __ldcg(&L[0]);
             const Key2 k = load_key(a.keys, x);
             S[nS] = x;
+            a.listSK[nS] = make_ulonglong2(k.w0, k.w1);
+            a.listSC[nS] = __ldcg(&a.C[x]);
             ss->n_S = nS + 1;
             ss->need_final = need;
             ss->n_pass = n_pass;
@@ -832,7 +905,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         nS += 1;
     }
     grid.sync();
-    stamp(ss);
+    stamp(ss, nts);
 
     // ---- sort every bucket of S (one CTA per bucket, shared memory) ------------------
     if (threadIdx.x == 0) {
@@ -850,9 +923,8 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         }
         return;
     }
-    (void)v0;
-    (void)v1;
-    (void)v2;
+    // the varying bits of S fit 64 bits (the common case): buckets rank on packed keys
+    const bool packed = __popcll(v0) + __popcll(v1) + __popcll(v2) <= 64;
     int* S2 = a.listS2;
     if (take_all) {
         if (tid == 0 && nS > 0) {  // the whole head list is one bucket
@@ -860,12 +932,20 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             a.big[1] = static_cast<unsigned int>(nS);
         }
         grid.sync();
-        rank_sort_big(a, S, S2, nS > 0 ? 1u : 0u, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
+        rank_sort_big(a, S, S2, nS > 0 ? 1u : 0u, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val, packed,
+                      false, v0, v1, v2);
     } else {
+        const unsigned long long t0 = gtimer();
         if (threadIdx.x == 0) sm.bc[3] = __ldcg(&ss->n_big);
         __syncthreads();
         const unsigned int n_big = static_cast<unsigned int>(sm.bc[3]);
-        rank_sort_big(a, S, S2, n_big, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val);
+        rank_sort_big(a, S, S2, n_big, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val, packed, true, v0,
+                      v1, v2);
+        const unsigned long long t1 = gtimer();
+        if (threadIdx.x == 0) {
+            atomicMax(&ss->dbg[0], t1 - t0);
+            atomicMax(&ss->dbg[4], static_cast<unsigned long long>(n_big));
+        }
         // small buckets: one warp each; singletons and the cut head are copied
         const int nb = n_pass * kBins;
         const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
@@ -875,15 +955,22 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             if (cnt == 0u || cnt > 32u) continue;
             const unsigned int off = __ldcg(&a.seg_off[j]);
             if (cnt == 1u) {
-                if ((threadIdx.x & 31) == 0) S2[off] = __ldcg(&S[off]);
+                if ((threadIdx.x & 31) == 0) {
+                    S2[off] = __ldcg(&S[off]);
+                    a.listSC2[off] = __ldcg(&a.listSC[off]);
+                }
             } else {
                 warp_sort_bucket(a, S, S2, off, cnt);
             }
         }
-        if (tid == 0) S2[nS - 1] = __ldcg(&S[nS - 1]);  // the cut head (its own bucket)
+        if (tid == 0) {  // the cut head (its own bucket)
+            S2[nS - 1] = __ldcg(&S[nS - 1]);
+            a.listSC2[nS - 1] = __ldcg(&a.listSC[nS - 1]);
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(&ss->dbg[1], gtimer() - t1);
     }
     grid.sync();
-    stamp(ss);
+    stamp(ss, nts);
 
     // ---- chain starts: start[p] = sum of the chain sizes before S2[p] ----------------
     // every CTA scans its own slice of S2; the prefix before the slice is
@@ -903,9 +990,9 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
                  i0 += static_cast<unsigned long long>(blockDim.x) * 8) {
                 int hb[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) hb[q] = i0 + q < c0 ? __ldcg(&S2[i0 + q]) : -1;
+                for (int q = 0; q < 8; ++q) hb[q] = i0 + q < c0 ? static_cast<int>(__ldcg(&a.listSC2[i0 + q])) : 0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) pre += hb[q] >= 0 ? __ldcg(&a.C[hb[q]]) : 0u;
+                for (int q = 0; q < 8; ++q) pre += static_cast<unsigned int>(hb[q]);
             }
             carry = block_reduce_bits(pre, SumOp(), sm.sh);
             if (threadIdx.x == 0) sm.bc[2] = carry;
@@ -923,7 +1010,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
                     const int h = __ldcg(&S2[pos]);
                     hv[j] = h;
                     a.rank[h] = static_cast<int>(pos);
-                    cnt[j] = __ldcg(&a.C[h]);
+                    cnt[j] = __ldcg(&a.listSC2[pos]);
                 }
                 local += cnt[j];
             }
@@ -941,12 +1028,12 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         }
     }
     grid.sync();
-    stamp(ss);
-    phase_scatter(a, tid, nthr);
+    stamp(ss, nts);
+    phase_scatter(a, a.listS2, nS, tid, nthr);
     grid.sync();
-    stamp(ss);
+    stamp(ss, nts);
     if (tid == 0) do_cut(a);
-    stamp(ss);
+    stamp(ss, nts);
 }
 
 // ---- fallback path (a bucket larger than one CTA's sort) -----------------------------
@@ -994,7 +1081,7 @@ __global__ void rank_kernel(const int* sorted, const unsigned int* C, SelState* 
 }
 
 __global__ void __launch_bounds__(kThreads) scatter_kernel(SelArgs a) {
-    phase_scatter(a, blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x,
+    phase_scatter(a, a.sorted, a.ss->n_S, blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x,
                   static_cast<std::int64_t>(gridDim.x) * blockDim.x);
 }
 
@@ -1172,6 +1259,9 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     a.listB = c.listB.p;
     a.listS = c.listS.p;
     a.listS2 = c.listS2.p;
+    a.listSK = c.listSK.p;
+    a.listSC = c.listSC.p;
+    a.listSC2 = c.listSC2.p;
     a.big = c.big.p;
     a.sorted = c.sorti_out.p;
     a.start = c.cnt.p;
@@ -1272,7 +1362,7 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         c.cub_tmp.reserve(b);
         ++c.lib_calls;
         PBKV_CUDA(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, b, c.cnt.p, c.cnt.p, static_cast<int>(nS), c.stream));
-        scatter_kernel<<<grid_cap(c.n, kThreads), kThreads, 0, c.stream>>>(a);
+        scatter_kernel<<<grid_cap(nS, kThreads), kThreads, 0, c.stream>>>(a);
         PBKV_CUDA(cudaGetLastError());
         cut_kernel<<<1, 1, 0, c.stream>>>(a);
         PBKV_CUDA(cudaGetLastError());
