@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs
         if constexpr (kKeys) {
             ka.eff[n] = n;
             ka.sublock[n] = 0;
+            ka.W[n] = 0;  // chain weight / size accumulators of the selection
+            ka.C[n] = 0;
             if (light) {
                 ka.missing[n] = (miss || shorth) ? 1 : 0;
                 if (n != 0 && (fl & kFlagTierMask) == PBKV_TIER_DEVICE) write_key_v(ka, n, total, fl, last, ever);

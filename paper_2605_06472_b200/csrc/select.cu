@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(kThreads) keys_cached_kernel(KeyArgs ka, std::
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int n = static_cast<int>(i);
         init_select_state(ka, n, false);
+        ka.W[n] = 0;
+        ka.C[n] = 0;
         if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, ka.score_cached[n]);
     }
 }
@@ -796,6 +798,21 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     int nts = 0;
+    // initial selection state, written by CTA 0 before the first grid barrier
+    // (no other CTA touches it earlier): no host->device copy per decision
+    if (blockIdx.x == 0) {
+        unsigned long long* w = reinterpret_cast<unsigned long long*>(ss);
+        for (unsigned int i = threadIdx.x; i < sizeof(SelState) / 8; i += blockDim.x) w[i] = 0ull;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ss->need_final = static_cast<unsigned long long>(a.needed);
+            for (int q = 0; q < 3; ++q) {
+                ss->and_L[0][q] = ss->and_L[1][q] = ~0ull;
+                ss->and_S[q] = ~0ull;
+            }
+            ss->cut_head = -1;
+        }
+    }
 
     stamp(ss, nts);
     phase_lock(a, tid, nthr);
@@ -1222,18 +1239,9 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     SelState* ss = reinterpret_cast<SelState*>(c.selstate.p);
     SelState* hs = reinterpret_cast<SelState*>(c.hselstate.p);
     // initial state from a pinned template (no kernel)
-    SelState* tmpl = reinterpret_cast<SelState*>(c.hselstate.p + sizeof(SelState));
-    std::memset(tmpl, 0, sizeof(SelState));
-    tmpl->need_final = static_cast<unsigned long long>(needed);
-    for (int w = 0; w < 3; ++w) {
-        tmpl->and_L[0][w] = tmpl->and_L[1][w] = ~0ull;
-        tmpl->and_S[w] = ~0ull;
-    }
-    tmpl->cut_head = -1;
-    PBKV_CUDA(cudaMemcpyAsync(ss, tmpl, sizeof(SelState), cudaMemcpyHostToDevice, c.stream));
-    // chain weights / sizes accumulate by scatter in phase_chains
-    PBKV_CUDA(cudaMemsetAsync(c.W.p, 0, static_cast<std::size_t>(c.n) * sizeof(unsigned long long), c.stream));
-    PBKV_CUDA(cudaMemsetAsync(c.C.p, 0, static_cast<std::size_t>(c.n) * sizeof(unsigned int), c.stream));
+    // the initial state is written by the persistent kernel itself; the chain
+    // weights / sizes (scatter-added in phase_chains) were zeroed by the keying
+    // kernel (score_light_kernel / keys_cached_kernel)
     long long* res = result_dev ? result_dev : c.counters.p + 8;
     c.sorti_out.reserve(static_cast<std::size_t>(c.n) + 1);
     c.cnt.reserve(static_cast<std::size_t>(c.n) + 1);
