@@ -194,7 +194,12 @@ void reset_status(Context& c) {
 void check_status(Context& c) {
     PBKV_CUDA(cudaMemcpyAsync(c.hstatus.p, c.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c.stream));
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
-    DevStatus s = *c.hstatus.p;
+    const DevStatus st = *c.hstatus.p;  // a copy: raising may reuse the pinned word
+    raise_status(c, st);
+}
+
+// throws the API error a device status word describes (no-op when clear)
+void raise_status(Context& c, const DevStatus& s) {
     if (s.code == 0) return;
     std::string msg;
     switch (s.kind) {
@@ -436,6 +441,26 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     upload_children(c, heavy, c.hch_off, c.hch);
     c.h_heavy_depth.resize(heavy.size());
     for (std::size_t j = 0; j < heavy.size(); ++j) c.h_heavy_depth[j] = dep[heavy[j]];
+    {  // deferral placement tables (place_deferred), once per mirror
+        const std::size_t nh = heavy.size();
+        c.h_heavy_order.resize(nh);
+        for (std::size_t j = 0; j < nh; ++j) c.h_heavy_order[j] = j;
+        std::stable_sort(c.h_heavy_order.begin(), c.h_heavy_order.end(),
+                         [&](std::size_t a, std::size_t b) { return c.h_heavy_depth[a] > c.h_heavy_depth[b]; });
+        std::unordered_map<int, int> pos;
+        for (std::size_t j = 0; j < nh; ++j) pos[heavy[j]] = static_cast<int>(j);
+        std::vector<std::vector<int>> kids(nh);
+        for (std::size_t q = 0; q < nh; ++q) {  // heavy children in index order (as the scan below visited them)
+            const auto it = pos.find(c.h_heavy_parent[q]);
+            if (it != pos.end()) kids[static_cast<std::size_t>(it->second)].push_back(static_cast<int>(q));
+        }
+        c.h_heavy_kid_off.assign(1, 0);
+        c.h_heavy_kids.clear();
+        for (std::size_t j = 0; j < nh; ++j) {
+            c.h_heavy_kids.insert(c.h_heavy_kids.end(), kids[j].begin(), kids[j].end());
+            c.h_heavy_kid_off.push_back(static_cast<int>(c.h_heavy_kids.size()));
+        }
+    }
     c.n_hent = static_cast<std::int64_t>(hent.size());
     c.max_depth = maxd;
     c.device_capacity = s.device_capacity;
@@ -556,13 +581,9 @@ bool place_deferred(Context& c, long long* result_dev, const SelectCounts& o, st
         if (hkey_less(k, tkey)) return false;
         return d > tail.depth_diff;
     };
-    // heavy nodes deepest first: eff of a heavy node may come from a heavy descendant
-    std::vector<std::size_t> order(nh);
-    for (std::size_t j = 0; j < nh; ++j) order[j] = j;
-    std::sort(order.begin(), order.end(),
-              [&](std::size_t a, std::size_t b) { return c.h_heavy_depth[a] > c.h_heavy_depth[b]; });
-    std::unordered_map<int, std::size_t> idx;
-    for (std::size_t j = 0; j < nh; ++j) idx[c.h_heavy[j]] = j;
+    // heavy nodes deepest first (eff of a heavy node may come from a heavy
+    // descendant); order and heavy-children lists are built at mirror time
+    const std::vector<std::size_t>& order = c.h_heavy_order;
     struct Eff {
         HKey lo, hi;   // exact when lo == hi
         int depth = -1;
@@ -585,8 +606,9 @@ bool place_deferred(Context& c, long long* result_dev, const SelectCounts& o, st
         }
         sub[j] = sub[j] || r.sublock;
         // heavy children already resolved (their eff covers their subtrees)
-        for (std::size_t q = 0; q < nh; ++q) {
-            if (c.h_heavy_parent[q] != h || !eff[q].any) continue;
+        for (int kq = c.h_heavy_kid_off[j]; kq < c.h_heavy_kid_off[j + 1]; ++kq) {
+            const std::size_t q = static_cast<std::size_t>(c.h_heavy_kids[static_cast<std::size_t>(kq)]);
+            if (!eff[q].any) continue;
             sub[j] = sub[j] || sub[q];
             if (!best.any || hkey_less(best.hi, eff[q].lo)) {
                 best = eff[q];
@@ -632,11 +654,10 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
         throw ApiError(PBKV_EARG, "bad score mode");
     need(c.n >= 1, "no tree mirrored");
     record(c, 0);
-    reset_status(c);
     const bool recompute = score_mode == PBKV_SCORE_RECOMPUTE && policy == PBKV_POLICY_HE;
     const bool defer = recompute && c.defer_heavy && c.n_heavy > 0 && c.spine.empty();
+    launch_decision_prologue(c, defer);  // status reset (+ the deferral)
     if (defer) {
-        launch_set_deferred(c, true);
         launch_score_decision(c, policy);
     } else if (recompute) {
         launch_score_all(c, c.score_rc.p, true, policy, false);
@@ -649,7 +670,8 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
     c.report_deferred = false;
     if (defer) {
         const bool placed = place_deferred(c, result_dev ? result_dev : c.counters.p + 8, o, needed);
-        launch_set_deferred(c, false);
+        if (!c.deferred_cleared) launch_set_deferred(c, false);
+        c.deferred_cleared = false;
         if (placed) {
             ++c.defer_fast;
         } else {  // slow path: exact chains, full selection
@@ -661,6 +683,16 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
     }
     record(c, 2);
     finish_timing(c, 2);
+    static const bool dbg_t = std::getenv("PBKV_DEBUG_TIMING") != nullptr;
+    if (dbg_t && c.timing) {
+        float a = 0, b = 0, d = 0, e = 0;
+        cudaEventElapsedTime(&a, c.ev[0], c.kev[0]);   // decision start -> light start
+        cudaEventElapsedTime(&b, c.kev[1], c.kev[2]);  // light end -> select kernel start
+        cudaEventElapsedTime(&d, c.kev[3], c.ev[2]);   // select kernel end -> decision end
+        cudaEventElapsedTime(&e, c.ev[0], c.ev[2]);
+        std::fprintf(stderr, "[pbkv timing] start->light %.1f us, light->select %.1f us, select->end %.1f us, total %.1f us\n",
+                     a * 1e3, b * 1e3, d * 1e3, e * 1e3);
+    }
     return o;
 }
 

@@ -212,6 +212,10 @@ struct Context {
     std::vector<unsigned long long> h_heavy_last;
     std::vector<int> h_heavy_depth, h_heavy_parent;
     std::vector<std::uint8_t> h_heavy_flags;
+    // place_deferred: heavy nodes deepest first, heavy children of each heavy node (CSR)
+    std::vector<std::size_t> h_heavy_order;
+    bool deferred_cleared = false;  // run_select already enqueued the deferral clear
+    std::vector<int> h_heavy_kid_off, h_heavy_kids;
     DevBuf<double> happrox;                   // [2*n_heavy]: approximate Eq. 2 sum, sum of |terms|
     DevBuf<unsigned char> hreport;            // deferred-heavy reports + the tail record
     PinBuf<unsigned char> hreport_h;
@@ -313,7 +317,9 @@ void launch_chain_sum(Context& c, const double* x, const long long* off, int n_s
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
 void launch_keys_cached(Context& c, int policy);
 void launch_score_decision(Context& c, int policy);  // Eq. 2 + keys with heavy chains deferred
-void launch_set_deferred(Context& c, bool on);
+void launch_set_deferred(Context& c, bool on, const int* skip_if = nullptr);
+void launch_decision_prologue(Context& c, bool defer);
+void raise_status(Context& c, const DevStatus& s);
 struct HeavyReport {  // one per heavy node, then one tail record (select.cu)
     unsigned long long w0, w1;  // key of eff(h) over its non-deferred descendants / of the tail head
     int eff;                    // node id (-1: none)
@@ -323,7 +329,7 @@ struct HeavyReport {  // one per heavy node, then one tail record (select.cu)
     int depth_diff;             // tail record: depth(head) - depth(last victim)
     int pad;
 };
-void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out);
+void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out, double* approx_out);
 SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked, std::int64_t needed,
                         bool he_recompute, long long* result_dev);
 std::size_t sel_state_bytes();

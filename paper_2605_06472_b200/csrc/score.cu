@@ -8,6 +8,8 @@
 //                             then one CTA per node evaluates the serial
 //                             rounding chain exactly in parallel per binade
 // The heavy path runs on a side stream, overlapped with the light pass.
+#include <climits>
+
 #include "chain.cuh"
 #include "common.cuh"
 
@@ -524,12 +526,31 @@ __global__ void __launch_bounds__(kChainT) chain_sum_kernel(const double* x, con
 // heavy_products_kernel.  The exact serial chain E and this sum A both lie
 // within L * ulp(sum|x|) / 2 of the real sum, so |E - A| <= L * ulp(sum|x|).
 
-__global__ void set_deferred_kernel(std::uint8_t* flags, Key2* keys, const int* nodes, int n, int on) {
+__global__ void set_deferred_kernel(std::uint8_t* flags, Key2* keys, const int* nodes, int n, int on,
+                                    const int* skip_if) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || (skip_if && *skip_if)) return;
     const int v = nodes[i];
     flags[v] = on ? (flags[v] | kFlagDeferred) : (flags[v] & ~kFlagDeferred);
     if (on) reinterpret_cast<ulonglong2*>(keys)[v] = make_ulonglong2(0ull, 0ull);  // out of every eff max
+}
+
+// First kernel of a decision: the status word reset (no host->device copy)
+// and, with heavy deferral, the deferred flags / zero keys and the side
+// stream's accumulators (hmiss, approx).
+__global__ void decision_prologue_kernel(DevStatus* st, std::uint8_t* flags, Key2* keys, const int* heavy,
+                                         int n_heavy, int defer, unsigned int* hmiss, int n_hmiss, double* approx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *st = DevStatus{0, 0, LLONG_MAX, LLONG_MAX};
+    if (!defer) return;
+    if (i < n_heavy) {
+        const int v = heavy[i];
+        flags[v] = flags[v] | kFlagDeferred;
+        reinterpret_cast<ulonglong2*>(keys)[v] = make_ulonglong2(0ull, 0ull);  // out of every eff max
+        approx[2 * i] = 0.0;
+        approx[2 * i + 1] = 0.0;
+    }
+    if (i < n_hmiss) hmiss[i] = 0u;
 }
 
 // Eq. 1 / Eq. 2 of an id list, one thread per short id (refresh_nodes path)
@@ -756,10 +777,25 @@ void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool
     if (side) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
-void launch_set_deferred(Context& c, bool on) {
+// skip_if (device): the kernel does nothing when *skip_if != 0 (run_select
+// enqueues the clear before its synchronisation, unless the host-sort
+// fallback -- which still needs the flags -- was taken)
+void launch_set_deferred(Context& c, bool on, const int* skip_if) {
     if (c.n_heavy == 0) return;
     const int n = static_cast<int>(c.n_heavy);
-    set_deferred_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.flags.p, c.keys.p, c.heavy.p, n, on ? 1 : 0);
+    set_deferred_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.flags.p, c.keys.p, c.heavy.p, n, on ? 1 : 0,
+                                                                  skip_if);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_decision_prologue(Context& c, bool defer) {
+    const int nh = defer ? static_cast<int>(c.n_heavy) : 0;
+    const int nm = defer ? static_cast<int>(c.n_heavy + c.n_medium) : 0;
+    if (defer) c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy) + 2);
+    const int n = std::max(1, std::max(nh, nm));
+    decision_prologue_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.status.p, c.flags.p, c.keys.p, c.heavy.p, nh,
+                                                                      defer ? 1 : 0, c.hmiss.p, nm, c.happrox.p);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
 }
@@ -773,12 +809,9 @@ void launch_score_decision(Context& c, int policy) {
     KeyArgs ka = make_key_args(c, policy);
     const bool side = c.n_heavy + c.n_medium > 0;
     if (side) {
-        c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy) + 2);
+        // hmiss / approx were zeroed and the deferral set by decision_prologue_kernel
         PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-        PBKV_CUDA(cudaMemsetAsync(c.hmiss.p, 0, static_cast<std::size_t>(c.n_heavy + c.n_medium) * sizeof(unsigned int),
-                                  c.side));
-        PBKV_CUDA(cudaMemsetAsync(c.happrox.p, 0, static_cast<std::size_t>(2 * c.n_heavy) * sizeof(double), c.side));
         heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(
             s, c.hent.p, c.hent_node.p, c.n_hent, c.hxs.p, c.hmiss.p, c.happrox.p, static_cast<int>(c.n_heavy));
         PBKV_CUDA(cudaGetLastError());

@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int
                                                            const int* sublock, const int* depth,
                                                            const std::uint8_t* flags, const unsigned int* hmiss,
                                                            const int* victims, const long long* result,
-                                                           HeavyReport* out) {
+                                                           HeavyReport* out, const double* approx, double* approx_out) {
     // one CTA per heavy node: max over its in-order device children's eff
     // (the shared prefix has thousands of children); the last CTA writes the
     // record of the last victim (tail)
@@ -1193,6 +1193,10 @@ __global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int
             r.sublock = sublock[h] ? 1 : 0;
             r.miss = static_cast<int>(hmiss[j]);
             out[j] = r;
+            if (approx_out) {
+                approx_out[2 * j] = approx[2 * j];
+                approx_out[2 * j + 1] = approx[2 * j + 1];
+            }
         }
     } else if (threadIdx.x == 0) {
         HeavyReport r{};
@@ -1213,12 +1217,27 @@ __global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int
 }
 }  // namespace
 
-void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out) {
+// Last kernel of a decision: the status word and the selection state are
+// stored straight into pinned host memory (no device->host copy operations on
+// the critical path), and the heavy-node deferral is cleared unless the
+// host-sort fallback still needs it.
+__global__ void __launch_bounds__(256) decision_epilogue_kernel(const DevStatus* st, const SelState* ss,
+                                                                DevStatus* h_st, SelState* h_ss, std::uint8_t* flags,
+                                                                const int* heavy, int n_clear) {
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ss);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(h_ss);
+    for (unsigned int i = threadIdx.x; i < sizeof(SelState) / 8; i += blockDim.x) dst[i] = __ldcg(src + i);
+    if (threadIdx.x == 0) *h_st = *st;
+    if (__ldcg(&ss->host_sort)) return;
+    for (int i = threadIdx.x; i < n_clear; i += blockDim.x) flags[heavy[i]] &= static_cast<std::uint8_t>(~kFlagDeferred);
+}
+
+void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out, double* approx_out) {
     const int n = static_cast<int>(c.n_heavy);
     heavy_report_kernel<<<n + 1, 256, 0, c.stream>>>(c.heavy.p, n, c.hch_off.p, c.hch.p, c.keys.p,
                                                                    c.eff.p, c.sublock.p,
                                                                    c.depth.p, c.flags.p, c.hmiss.p, c.vid_out.p,
-                                                                   result_dev, out);
+                                                                   result_dev, out, c.happrox.p, approx_out);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
 }
@@ -1296,19 +1315,26 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
                                           dim3(kPThreads), args, sizeof(PersistSmem), c.stream));
     if (c.timing) PBKV_CUDA(cudaEventRecord(c.kev[3], c.stream));
     ++c.launches;
-    PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
     if (c.report_deferred) {  // the deferred-heavy reports ride on the same synchronisation
         const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
         const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
-        c.hreport.reserve(bytes);
         c.hreport_h.reserve(bytes + 2 * nh * sizeof(double));
-        HeavyReport* rep_d = reinterpret_cast<HeavyReport*>(c.hreport.p);
-        launch_heavy_report(c, reinterpret_cast<long long*>(res), rep_d);
-        PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p, rep_d, bytes, cudaMemcpyDeviceToHost, c.stream));
-        PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p + bytes, c.happrox.p, 2 * nh * sizeof(double),
-                                  cudaMemcpyDeviceToHost, c.stream));
+        // written by the kernel straight into pinned host memory
+        launch_heavy_report(c, reinterpret_cast<long long*>(res), reinterpret_cast<HeavyReport*>(c.hreport_h.p),
+                            reinterpret_cast<double*>(c.hreport_h.p + bytes));
     }
-    check_status(c);  // synchronises
+    // status + selection state to the host, and the deferral cleared (unless
+    // the host-sort fallback below still needs it), before the host wakes up
+    decision_epilogue_kernel<<<1, 256, 0, c.stream>>>(c.status.p, ss, c.hstatus.p, hs, c.flags.p, c.heavy.p,
+                                                      c.report_deferred ? static_cast<int>(c.n_heavy) : 0);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    {
+        const DevStatus st = *c.hstatus.p;  // a copy: raising may reuse the pinned word
+        raise_status(c, st);
+    }
+    c.deferred_cleared = c.report_deferred && !hs->host_sort;
     SelectCounts out;
     c.phase_ns.assign(hs->ts, hs->ts + (hs->n_ts < 40 ? hs->n_ts : 40));
     if (std::getenv("PBKV_DEBUG_SELECT"))
@@ -1379,9 +1405,9 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         if (c.report_deferred) {  // the victims changed: fetch the tail record again
             const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
             const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
-            HeavyReport* rep_d = reinterpret_cast<HeavyReport*>(c.hreport.p);
-            launch_heavy_report(c, reinterpret_cast<long long*>(res), rep_d);
-            PBKV_CUDA(cudaMemcpyAsync(c.hreport_h.p, rep_d, bytes, cudaMemcpyDeviceToHost, c.stream));
+            launch_heavy_report(c, reinterpret_cast<long long*>(res), reinterpret_cast<HeavyReport*>(c.hreport_h.p),
+                                nullptr);
+            (void)bytes;
         }
         PBKV_CUDA(cudaStreamSynchronize(c.stream));
     }
