@@ -567,8 +567,8 @@ def main():
         "p50_decision_ms": float(np.percentile(per_step, 50)),
         "stage_ms": {"score_keys": float(stage[0]), "select": float(stage[1]), "total": float(stage[4])},
         "kernel_ms": {"score_light": float(kern[0]), "select_persistent": float(kern[1])},
-        "select_phases_us": {"note": "lock, eff, weights, [hist+reduce, pick+compact] x passes, cut-head, "
-                                     "sort, scatter, cut", "us": select_phases},
+        "select_phases_us": {"note": "lock, eff, chains, [hist, pick+compact] x passes, cut-head, "
+                                     "sort, chain-starts, scatter, cut", "us": select_phases},
         "roofline": {"bound": "hbm", "kernel": "score_light_kernel (Eq. 2 of every light node + stage-3 keys)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None,
