@@ -126,7 +126,10 @@ __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsign
 // Light nodes (<= 2 entries): one thread per node, Eq. 2 and the stage-3 key
 // in registers.  kK > 0: horizon specialised; kK == 0: any horizon.
 template <bool kKeys, int kK>
-__global__ void __launch_bounds__(kLightThreads, 4) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
+#ifndef PBKV_LIGHT_MINB
+#define PBKV_LIGHT_MINB 4  // CTAs/SM the registers are sized for (measured: 4 -> 38 us, 5 -> 52, 6 -> 73: spills)
+#endif
+__global__ void __launch_bounds__(kLightThreads, PBKV_LIGHT_MINB) score_light_kernel(ScoreArgs s, KeyArgs ka, std::int64_t n_nodes,
                                                                        int report_missing) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
          i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
