@@ -908,15 +908,16 @@ int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, in
         if (outcomes != c->V1) invalid("forecast outcomes do not match the context's agent count");
         if (n == 0) return;
         set_device(*c);
-        std::vector<long long> slots(static_cast<std::size_t>(n));
-        for (int64_t i = 0; i < n; ++i) slots[static_cast<std::size_t>(i)] = slot_for(*c, wf[i]);
+        c->hslots.reserve(static_cast<std::size_t>(n));  // pinned: the H2D below stays asynchronous
+        long long* slots = c->hslots.p;
+        for (int64_t i = 0; i < n; ++i) slots[i] = slot_for(*c, wf[i]);
         const std::size_t per = static_cast<std::size_t>(horizon) * static_cast<std::size_t>(outcomes);
         c->fstage.reserve(static_cast<std::size_t>(n) * per);
         c->fstage_slot.reserve(static_cast<std::size_t>(n));
         reset_status(*c);
         PBKV_CUDA(cudaMemcpyAsync(c->fstage.p, p, static_cast<std::size_t>(n) * per * sizeof(double),
                                   cudaMemcpyHostToDevice, c->stream));
-        PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots.data(), slots.size() * sizeof(long long),
+        PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots, static_cast<std::size_t>(n) * sizeof(long long),
                                   cudaMemcpyHostToDevice, c->stream));
         launch_forecast_prepare(*c, c->fstage.p, c->fstage_slot.p, n, horizon);
         check_status(*c);
@@ -1001,8 +1002,14 @@ int pbkv_select(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const i
         need(n_locked == 0 || locked, "null locked array");
         set_device(*c);
         c->locked.reserve(static_cast<std::size_t>(n_locked) + 1);
-        if (n_locked > 0)
-            PBKV_CUDA(cudaMemcpyAsync(c->locked.p, locked, n_locked * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        if (n_locked > 0) {
+            // through pinned staging: a pageable source would make the copy
+            // (and every launch behind it) wait for the driver's staging
+            c->hlocked.reserve(static_cast<std::size_t>(n_locked));
+            std::memcpy(c->hlocked.p, locked, static_cast<std::size_t>(n_locked) * sizeof(int));
+            PBKV_CUDA(cudaMemcpyAsync(c->locked.p, c->hlocked.p, n_locked * sizeof(int), cudaMemcpyHostToDevice,
+                                      c->stream));
+        }
         SelectCounts o = select_core(*c, policy, score_mode, needed, c->locked.p, n_locked, nullptr);
         *n_victims = o.n_victims;
         *freed = o.freed;
@@ -1010,9 +1017,11 @@ int pbkv_select(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const i
         if (o.n_victims > cap) throw ApiError(PBKV_EARG, "victim capacity too small");
         if (o.n_victims > 0) {
             need(victims != nullptr, "null victims array");
-            PBKV_CUDA(cudaMemcpyAsync(victims, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToHost,
+            c->hvictims.reserve(static_cast<std::size_t>(o.n_victims));
+            PBKV_CUDA(cudaMemcpyAsync(c->hvictims.p, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToHost,
                                       c->stream));
             PBKV_CUDA(cudaStreamSynchronize(c->stream));
+            std::memcpy(victims, c->hvictims.p, static_cast<std::size_t>(o.n_victims) * sizeof(int));
         }
     });
 }

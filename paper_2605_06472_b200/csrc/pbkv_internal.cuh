@@ -277,6 +277,8 @@ struct Context {
     DevBuf<DevStatus> status;
     PinBuf<long long> hcounters;
     PinBuf<DevStatus> hstatus;
+    PinBuf<int> hlocked, hvictims;  // pinned staging of the host-array select (pbkv_select)
+    PinBuf<long long> hslots;       // pinned staging of the forecast slots (pbkv_forecast_put)
 
     // ---- sharding (shard.cu) -------------------------------------------------------
     std::vector<int> spine;  // local ids of the spine copies
