@@ -503,7 +503,7 @@ def main():
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-        n_victims_e2e = len(sel.victims)
+        n_victims_e2e = len(sel)
     assert n_victims_e2e == res[0], "e2e and device-resident decisions disagree"
 
     # ---- aggregate over ranks (max time) --------------------------------------------

@@ -50,12 +50,37 @@ def _check(rc: int, handle) -> None:
     raise PbkvError(rc, msg)
 
 
-@dataclass
 class VictimSelection:
-    """policies.hpp:30-34"""
-    victims: list[int] = field(default_factory=list)
-    freed: int = 0
-    shortfall: bool = False
+    """policies.hpp:30-34 (victims, freed, shortfall).
+
+    `victim_ids` is the int32 array the C ABI filled; `victims` is the same
+    order as a Python list, built on first access (a 7 K-victim list costs
+    tens of microseconds, more than the copy out of the GPU)."""
+
+    __slots__ = ("victim_ids", "freed", "shortfall", "_list")
+
+    def __init__(self, victims=None, freed: int = 0, shortfall: bool = False):
+        self.victim_ids = np.asarray(victims if victims is not None else [], dtype=np.int32)
+        self.freed = int(freed)
+        self.shortfall = bool(shortfall)
+        self._list = victims if isinstance(victims, list) else None
+
+    @property
+    def victims(self) -> list[int]:
+        if self._list is None:
+            self._list = self.victim_ids.tolist()
+        return self._list
+
+    def __len__(self) -> int:
+        return int(self.victim_ids.size)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, VictimSelection):
+            return NotImplemented
+        return (self.victims, self.freed, self.shortfall) == (other.victims, other.freed, other.shortfall)
+
+    def __repr__(self) -> str:
+        return f"VictimSelection(victims={self.victims!r}, freed={self.freed}, shortfall={self.shortfall})"
 
 
 @dataclass
@@ -281,7 +306,7 @@ class Policy:
         nv, fr, sf = C.c_int64(), C.c_int64(), C.c_int()
         self._c(_abi.lib().pbkv_select(self._h, int(policy), int(score_mode), int(needed), ptr(lk, C.c_int32), n_lk,
                                        ptr(victims, C.c_int32), cap, C.byref(nv), C.byref(fr), C.byref(sf)))
-        return VictimSelection(victims[: nv.value].tolist(), int(fr.value), bool(sf.value))
+        return VictimSelection(victims[: nv.value].copy(), int(fr.value), bool(sf.value))
 
     def select_dev(self, policy: int, score_mode: int, needed: int, locked_ptr: int, n_locked: int,
                    victims_ptr: int, cap: int, result_ptr: int) -> None:

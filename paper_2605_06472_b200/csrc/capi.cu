@@ -1010,17 +1010,33 @@ int pbkv_select(pbkv_ctx* c, int policy, int score_mode, int64_t needed, const i
             PBKV_CUDA(cudaMemcpyAsync(c->locked.p, c->hlocked.p, n_locked * sizeof(int), cudaMemcpyHostToDevice,
                                       c->stream));
         }
-        SelectCounts o = select_core(*c, policy, score_mode, needed, c->locked.p, n_locked, nullptr);
+        // the decision's epilogue kernel stores up to kEpiVictims victim ids
+        // straight into pinned memory, so the common cut needs no copy after
+        // the decision's synchronisation
+        constexpr long long kEpiVictims = 1 << 16;
+        c->hvictims.reserve(static_cast<std::size_t>(kEpiVictims));
+        c->epi_vict = c->hvictims.p;
+        c->epi_cap = std::min<long long>(kEpiVictims, cap);
+        SelectCounts o;
+        try {
+            o = select_core(*c, policy, score_mode, needed, c->locked.p, n_locked, nullptr);
+        } catch (...) {
+            c->epi_vict = nullptr;
+            throw;
+        }
+        c->epi_vict = nullptr;
         *n_victims = o.n_victims;
         *freed = o.freed;
         *shortfall = o.shortfall;
         if (o.n_victims > cap) throw ApiError(PBKV_EARG, "victim capacity too small");
         if (o.n_victims > 0) {
             need(victims != nullptr, "null victims array");
-            c->hvictims.reserve(static_cast<std::size_t>(o.n_victims));
-            PBKV_CUDA(cudaMemcpyAsync(c->hvictims.p, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToHost,
-                                      c->stream));
-            PBKV_CUDA(cudaStreamSynchronize(c->stream));
+            if (o.n_victims > c->epi_cap || !c->epi_vict_valid) {
+                c->hvictims.reserve(static_cast<std::size_t>(o.n_victims));
+                PBKV_CUDA(cudaMemcpyAsync(c->hvictims.p, c->vid_out.p, o.n_victims * sizeof(int),
+                                          cudaMemcpyDeviceToHost, c->stream));
+                PBKV_CUDA(cudaStreamSynchronize(c->stream));
+            }
             std::memcpy(victims, c->hvictims.p, static_cast<std::size_t>(o.n_victims) * sizeof(int));
         }
     });

@@ -278,6 +278,9 @@ struct Context {
     PinBuf<long long> hcounters;
     PinBuf<DevStatus> hstatus;
     PinBuf<int> hlocked, hvictims;  // pinned staging of the host-array select (pbkv_select)
+    int* epi_vict = nullptr;  // pinned victims destination of the decision epilogue (pbkv_select)
+    long long epi_cap = 0;
+    bool epi_vict_valid = false;  // the last epilogue stored the victims there
     PinBuf<long long> hslots;       // pinned staging of the forecast slots (pbkv_forecast_put)
 
     // ---- sharding (shard.cu) -------------------------------------------------------

@@ -1221,13 +1221,21 @@ __global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int
 // stored straight into pinned host memory (no device->host copy operations on
 // the critical path), and the heavy-node deferral is cleared unless the
 // host-sort fallback still needs it.
+// With h_vict, the victim ids too (when they fit h_cap; the host copies
+// larger cuts by DMA).
 __global__ void __launch_bounds__(256) decision_epilogue_kernel(const DevStatus* st, const SelState* ss,
                                                                 DevStatus* h_st, SelState* h_ss, std::uint8_t* flags,
-                                                                const int* heavy, int n_clear) {
+                                                                const int* heavy, int n_clear, const int* victims,
+                                                                int* h_vict, long long h_cap) {
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ss);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(h_ss);
     for (unsigned int i = threadIdx.x; i < sizeof(SelState) / 8; i += blockDim.x) dst[i] = __ldcg(src + i);
     if (threadIdx.x == 0) *h_st = *st;
+    if (h_vict) {
+        const long long nv = static_cast<long long>(__ldcg(&ss->n_victims));
+        if (!__ldcg(&ss->host_sort) && nv <= h_cap)
+            for (long long i = threadIdx.x; i < nv; i += blockDim.x) h_vict[i] = __ldcg(victims + i);
+    }
     if (__ldcg(&ss->host_sort)) return;
     for (int i = threadIdx.x; i < n_clear; i += blockDim.x) flags[heavy[i]] &= static_cast<std::uint8_t>(~kFlagDeferred);
 }
@@ -1326,7 +1334,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     // status + selection state to the host, and the deferral cleared (unless
     // the host-sort fallback below still needs it), before the host wakes up
     decision_epilogue_kernel<<<1, 256, 0, c.stream>>>(c.status.p, ss, c.hstatus.p, hs, c.flags.p, c.heavy.p,
-                                                      c.report_deferred ? static_cast<int>(c.n_heavy) : 0);
+                                                      c.report_deferred ? static_cast<int>(c.n_heavy) : 0,
+                                                      c.vid_out.p, c.epi_vict, c.epi_cap);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
@@ -1335,6 +1344,7 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         raise_status(c, st);
     }
     c.deferred_cleared = c.report_deferred && !hs->host_sort;
+    c.epi_vict_valid = c.epi_vict && !hs->host_sort && static_cast<long long>(hs->n_victims) <= c.epi_cap;
     SelectCounts out;
     c.phase_ns.assign(hs->ts, hs->ts + (hs->n_ts < 40 ? hs->n_ts : 40));
     if (std::getenv("PBKV_DEBUG_SELECT"))

@@ -22,3 +22,18 @@ for _ in range(20):
     pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE); t2 = time.perf_counter()
     tp.append(t1 - t0); ts.append(t2 - t1)
 print(f"locked={locked.size} put_forecasts {np.median(tp)*1e6:.0f} us  select(host) {np.median(ts)*1e6:.0f} us  P bytes {P.nbytes}")
+# raw C ABI call (no Python list conversion) for the same decision
+import ctypes as C
+from paper_2605_06472_b200 import _abi
+from paper_2605_06472_b200._abi import POLICY_HE
+L = _abi.lib()
+lk = np.ascontiguousarray(locked, dtype=np.int32)
+vb = np.empty(soa.n_nodes, dtype=np.int32)
+nv, fr, sf = C.c_int64(), C.c_int64(), C.c_int()
+tc = []
+for _ in range(20):
+    t0 = time.perf_counter()
+    L.pbkv_select(pol._h, POLICY_HE, SCORE_RECOMPUTE, int(needed), lk.ctypes.data_as(C.POINTER(C.c_int32)), int(lk.size),
+                  vb.ctypes.data_as(C.POINTER(C.c_int32)), int(vb.size), C.byref(nv), C.byref(fr), C.byref(sf))
+    tc.append(time.perf_counter() - t0)
+print(f"raw pbkv_select {np.median(tc)*1e6:.0f} us (victims {nv.value})")
