@@ -1358,31 +1358,42 @@ int pbkv_predict(pbkv_ctx* c, const int64_t* wf, int64_t n, const int64_t* prefi
         need(wf && prefix_off && prefix && x, "null argument");
         set_device(*c);
         const pbkv_predictor_cfg cfg = predictor_cfg(*c);
-        std::vector<int> off(static_cast<std::size_t>(n) + 1);
         need(prefix_off[0] == 0, "prefix offsets must start at 0");
+        const int64_t np = prefix_off[n];
+        // one pinned blob -> one asynchronous upload: [slots (i64) | offsets (i32) | prefix (i32)]
+        const std::size_t b_slots = static_cast<std::size_t>(n) * sizeof(long long);
+        const std::size_t b_off = (static_cast<std::size_t>(n) + 1) * sizeof(int);
+        const std::size_t b_pre = static_cast<std::size_t>(np > 0 ? np : 1) * sizeof(int);
+        const std::size_t blob = b_slots + b_off + b_pre;
+        c->hpred_blob.reserve(blob);
+        long long* slots = reinterpret_cast<long long*>(c->hpred_blob.p);
+        int* off = reinterpret_cast<int*>(c->hpred_blob.p + b_slots);
+        int* pre = reinterpret_cast<int*>(c->hpred_blob.p + b_slots + b_off);
         for (int64_t i = 0; i < n; ++i) {
             const int64_t t = prefix_off[i + 1] - prefix_off[i];
             if (t < 1) invalid("predictor needs a non-empty prefix (current agent last)");
             if (t > cfg.max_prefix) invalid("prefix longer than the predictor's max_prefix");
-            off[static_cast<std::size_t>(i)] = static_cast<int>(prefix_off[i]);
+            off[i] = static_cast<int>(prefix_off[i]);
         }
-        off[static_cast<std::size_t>(n)] = static_cast<int>(prefix_off[n]);
-        const int64_t np = prefix_off[n];
-        for (int64_t j = 0; j < np; ++j)
-            if (prefix[j] < 0 || prefix[j] >= cfg.num_agents) invalid("prefix agent out of range");
-        std::vector<long long> slots(static_cast<std::size_t>(n));
-        for (int64_t i = 0; i < n; ++i) slots[static_cast<std::size_t>(i)] = slot_for(*c, wf[i]);
+        off[n] = static_cast<int>(np);
+        if (np > 0) {  // copy, then one vectorisable range reduction
+            std::memcpy(pre, prefix, static_cast<std::size_t>(np) * sizeof(int));
+            int lo = pre[0], hi = pre[0];
+            for (int64_t j = 1; j < np; ++j) {
+                lo = std::min(lo, pre[j]);
+                hi = std::max(hi, pre[j]);
+            }
+            if (lo < 0 || hi >= cfg.num_agents) invalid("prefix agent out of range");
+        }
+        for (int64_t i = 0; i < n; ++i) slots[i] = slot_for(*c, wf[i]);
         const std::size_t per = static_cast<std::size_t>(cfg.horizon) * (cfg.num_agents + 1);
         c->fstage.reserve(static_cast<std::size_t>(n) * per);
-        c->fstage_slot.reserve(static_cast<std::size_t>(n));
-        c->pre_off.reserve(static_cast<std::size_t>(n) + 1);
-        c->pre.reserve(static_cast<std::size_t>(np) + 1);
+        c->pred_blob.reserve(blob);
         cudaStream_t st = c->stream;
-        PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots.data(), slots.size() * sizeof(long long),
-                                  cudaMemcpyHostToDevice, st));
-        PBKV_CUDA(cudaMemcpyAsync(c->pre_off.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        PBKV_CUDA(cudaMemcpyAsync(c->pre.p, prefix, static_cast<std::size_t>(np) * sizeof(int), cudaMemcpyHostToDevice,
-                                  st));
+        PBKV_CUDA(cudaMemcpyAsync(c->pred_blob.p, c->hpred_blob.p, blob, cudaMemcpyHostToDevice, st));
+        const long long* slots_d = reinterpret_cast<const long long*>(c->pred_blob.p);
+        const int* off_d = reinterpret_cast<const int*>(c->pred_blob.p + b_slots);
+        const int* pre_d = reinterpret_cast<const int*>(c->pred_blob.p + b_slots + b_off);
         const void* xd = x;
         if (!x_on_device) {
             const std::size_t xb = static_cast<std::size_t>(n) * cfg.text_dim;
@@ -1392,7 +1403,7 @@ int pbkv_predict(pbkv_ctx* c, const int64_t* wf, int64_t n, const int64_t* prefi
         }
         reset_status(*c);
         record(*c, 0);
-        predictor_run(*c, n, c->pre_off.p, c->pre.p, xd, c->fstage_slot.p, probs_out ? c->fstage.p : nullptr);
+        predictor_run(*c, n, off_d, pre_d, xd, slots_d, probs_out ? c->fstage.p : nullptr);
         record(*c, 1);
         if (probs_out)
             PBKV_CUDA(cudaMemcpyAsync(probs_out, c->fstage.p, static_cast<std::size_t>(n) * per * sizeof(double),
