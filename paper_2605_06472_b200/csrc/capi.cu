@@ -749,7 +749,13 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         c->V1 = cfg->num_agents + 1;
         PBKV_CUDA(cudaSetDevice(c->device));
         PBKV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        PBKV_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        {  // the side stream (medium / heavy chains) outranks the light pass for
+           // free SM slots, so it finishes inside the light pass even when
+           // enqueued after it (launch_score_decision)
+            int lo = 0, hi = 0;
+            PBKV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            PBKV_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+        }
         for (auto& e : c->ev) PBKV_CUDA(cudaEventCreate(&e));
         for (auto& e : c->kev) PBKV_CUDA(cudaEventCreate(&e));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));

@@ -811,9 +811,15 @@ void launch_score_decision(Context& c, int policy) {
     ScoreArgs s = make_score_args(c, c.score_rc.p);
     KeyArgs ka = make_key_args(c, policy);
     const bool side = c.n_heavy + c.n_medium > 0;
+    // the light pass is enqueued first (every API call before it delays its
+    // start); the side stream forks off the same point, has the higher
+    // priority for SM slots, and joins after it
+    if (side) PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    launch_light<true>(c, s, ka, 0);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
     if (side) {
         // hmiss / approx were zeroed and the deferral set by decision_prologue_kernel
-        PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(
             s, c.hent.p, c.hent_node.p, c.n_hent, c.hxs.p, c.hmiss.p, c.happrox.p, static_cast<int>(c.n_heavy));
@@ -827,11 +833,8 @@ void launch_score_decision(Context& c, int policy) {
             ++c.launches;
         }
         PBKV_CUDA(cudaEventRecord(c.ev_join, c.side));
+        PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
     }
-    launch_light<true>(c, s, ka, 0);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-    if (side) PBKV_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
 // Eq. 2 / Eq. 1 of an id list, results scattered into out[id]
