@@ -263,7 +263,100 @@ struct SelArgs {
     long long n_nodes;
     long long needed;
     int he_recompute;
+    // deferred-heavy reports (report_deferred decisions; n_report = 0 otherwise),
+    // written by otherwise idle CTAs during the sort phase and by do_cut (tail)
+    int n_report;
+    const int* heavy;
+    const int* hch_off;
+    const int* hch;
+    const unsigned int* hmiss;
+    HeavyReport* rep_out;   // pinned host memory
+    const double* approx;
+    double* approx_out;     // pinned host memory
 };
+
+// record of heavy node j: max over its in-order device children's eff (the
+// shared prefix has thousands of children), block-wide; eff / sublock read
+// through L2 (written by other CTAs of the persistent kernel)
+__device__ __forceinline__ void report_heavy_block(int j, const int* heavy, const int* ch_off, const int* ch,
+                                                   const Key2* keys, const int* eff, const int* sublock,
+                                                   const int* depth, const std::uint8_t* flags,
+                                                   const unsigned int* hmiss, HeavyReport* out, const double* approx,
+                                                   double* approx_out) {
+    __shared__ unsigned long long s0[32], s1[32];
+    __shared__ int se[32];
+    int e = -1;
+    Key2 best{0, 0};
+    for (int q = ch_off[j] + threadIdx.x; q < ch_off[j + 1]; q += blockDim.x) {
+        const int c = ch[q];
+        if ((flags[c] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE) continue;
+        const int ec = __ldcg(&eff[c]);
+        const Key2 k = load_key(keys, ec);
+        if (e < 0 || key_less(best, e, k, ec)) {
+            e = ec;
+            best = k;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long b0 = __shfl_xor_sync(0xffffffffu, best.w0, o);
+        const unsigned long long b1 = __shfl_xor_sync(0xffffffffu, best.w1, o);
+        const int be = __shfl_xor_sync(0xffffffffu, e, o);
+        const Key2 bk{b0, b1};
+        if (be >= 0 && (e < 0 || key_less(best, e, bk, be))) {
+            e = be;
+            best = bk;
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) {
+        s0[warp] = best.w0;
+        s1[warp] = best.w1;
+        se[warp] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        e = -1;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            const Key2 bk{s0[w], s1[w]};
+            if (se[w] >= 0 && (e < 0 || key_less(best, e, bk, se[w]))) {
+                e = se[w];
+                best = bk;
+            }
+        }
+        const int h = heavy[j];
+        HeavyReport r{};
+        r.w0 = e >= 0 ? best.w0 : 0ull;
+        r.w1 = e >= 0 ? best.w1 : 0ull;
+        r.eff = e;
+        r.eff_depth = e >= 0 ? depth[e] : -1;
+        r.sublock = __ldcg(&sublock[h]) ? 1 : 0;
+        r.miss = static_cast<int>(hmiss[j]);
+        out[j] = r;
+        if (approx_out) {
+            approx_out[2 * j] = approx[2 * j];
+            approx_out[2 * j + 1] = approx[2 * j + 1];
+        }
+    }
+}
+
+// the record of the last victim (tail): its head's key and depths
+__device__ __forceinline__ HeavyReport report_tail(const Key2* keys, const int* eff, const int* depth,
+                                                  const int* victims, long long n) {
+    HeavyReport r{};
+    r.eff = -1;
+    if (n > 0) {
+        const int v = __ldcg(&victims[n - 1]);
+        const int h = __ldcg(&eff[v]);
+        const Key2 k = load_key(keys, h);
+        r.w0 = k.w0;
+        r.w1 = k.w1;
+        r.eff = h;
+        r.eff_depth = depth[h];
+        r.depth_diff = depth[h] - depth[v];
+    }
+    return r;
+}
 
 // ---- phases ---------------------------------------------------------------------
 
@@ -768,6 +861,10 @@ __device__ __forceinline__ void do_cut(const SelArgs& a) {
     a.result[0] = static_cast<long long>(ss->n_victims);
     a.result[1] = static_cast<long long>(ss->freed);
     a.result[2] = ss->shortfall;
+    if (a.n_report > 0) {
+        __threadfence();  // the victims of every CTA are in L2 (grid barrier before the cut)
+        a.rep_out[a.n_report] = report_tail(a.keys, a.eff, a.depth, a.victims, static_cast<long long>(ss->n_victims));
+    }
 }
 
 // ---- the persistent kernel --------------------------------------------------------------
@@ -986,6 +1083,12 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         }
         if ((threadIdx.x & 31) == 0) atomicMax(&ss->dbg[1], gtimer() - t1);
     }
+    // deferred-heavy reports by the CTAs at the top of the grid (the bucket
+    // sorts above occupy the bottom ones)
+    for (int j = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x); j < a.n_report;
+         j += static_cast<int>(gridDim.x))
+        report_heavy_block(j, a.heavy, a.hch_off, a.hch, a.keys, a.eff, a.sublock, a.depth, a.flags, a.hmiss,
+                           a.rep_out, a.approx, a.approx_out);
     grid.sync();
     stamp(ss, nts);
 
@@ -1139,81 +1242,14 @@ __global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int
                                                            const std::uint8_t* flags, const unsigned int* hmiss,
                                                            const int* victims, const long long* result,
                                                            HeavyReport* out, const double* approx, double* approx_out) {
-    // one CTA per heavy node: max over its in-order device children's eff
-    // (the shared prefix has thousands of children); the last CTA writes the
-    // record of the last victim (tail)
+    // one CTA per heavy node; the last CTA writes the record of the last
+    // victim (tail).  The persistent kernel does the same in place
+    // (report_deferred decisions); this kernel serves the host-sort fallback.
     const int j = blockIdx.x;
-    if (j < n_heavy) {
-        __shared__ unsigned long long s0[8], s1[8];
-        __shared__ int se[8];
-        int e = -1;
-        Key2 best{0, 0};
-        for (int q = ch_off[j] + threadIdx.x; q < ch_off[j + 1]; q += blockDim.x) {
-            const int c = ch[q];
-            if ((flags[c] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE) continue;
-            const int ec = eff[c];
-            const Key2 k = load_key(keys, ec);
-            if (e < 0 || key_less(best, e, k, ec)) {
-                e = ec;
-                best = k;
-            }
-        }
-        for (int o = 16; o; o >>= 1) {
-            const unsigned long long b0 = __shfl_xor_sync(0xffffffffu, best.w0, o);
-            const unsigned long long b1 = __shfl_xor_sync(0xffffffffu, best.w1, o);
-            const int be = __shfl_xor_sync(0xffffffffu, e, o);
-            const Key2 bk{b0, b1};
-            if (be >= 0 && (e < 0 || key_less(best, e, bk, be))) {
-                e = be;
-                best = bk;
-            }
-        }
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (lane == 0) {
-            s0[warp] = best.w0;
-            s1[warp] = best.w1;
-            se[warp] = e;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            e = -1;
-            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-                const Key2 bk{s0[w], s1[w]};
-                if (se[w] >= 0 && (e < 0 || key_less(best, e, bk, se[w]))) {
-                    e = se[w];
-                    best = bk;
-                }
-            }
-            const int h = heavy[j];
-            HeavyReport r{};
-            r.w0 = e >= 0 ? best.w0 : 0ull;
-            r.w1 = e >= 0 ? best.w1 : 0ull;
-            r.eff = e;
-            r.eff_depth = e >= 0 ? depth[e] : -1;
-            r.sublock = sublock[h] ? 1 : 0;
-            r.miss = static_cast<int>(hmiss[j]);
-            out[j] = r;
-            if (approx_out) {
-                approx_out[2 * j] = approx[2 * j];
-                approx_out[2 * j + 1] = approx[2 * j + 1];
-            }
-        }
-    } else if (threadIdx.x == 0) {
-        HeavyReport r{};
-        const long long n = result[0];
-        r.eff = -1;
-        if (n > 0) {
-            const int v = victims[n - 1];
-            const int h = eff[v];
-            const Key2 k = load_key(keys, h);
-            r.w0 = k.w0;
-            r.w1 = k.w1;
-            r.eff = h;
-            r.eff_depth = depth[h];
-            r.depth_diff = depth[h] - depth[v];
-        }
-        out[j] = r;
-    }
+    if (j < n_heavy)
+        report_heavy_block(j, heavy, ch_off, ch, keys, eff, sublock, depth, flags, hmiss, out, approx, approx_out);
+    else if (threadIdx.x == 0)
+        out[j] = report_tail(keys, eff, depth, victims, result[0]);
 }
 }  // namespace
 
@@ -1314,6 +1350,20 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     a.n_nodes = c.n;
     a.needed = needed;
     a.he_recompute = he_recompute ? 1 : 0;
+    a.n_report = 0;
+    if (c.report_deferred) {  // the deferred-heavy reports are written in place, to pinned memory
+        const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
+        const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
+        c.hreport_h.reserve(bytes + 2 * nh * sizeof(double));
+        a.n_report = static_cast<int>(c.n_heavy);
+        a.heavy = c.heavy.p;
+        a.hch_off = c.hch_off.p;
+        a.hch = c.hch.p;
+        a.hmiss = c.hmiss.p;
+        a.rep_out = reinterpret_cast<HeavyReport*>(c.hreport_h.p);
+        a.approx = c.happrox.p;
+        a.approx_out = reinterpret_cast<double*>(c.hreport_h.p + bytes);
+    }
     void* args[] = {&a};
     if (c.timing) {
         PBKV_CUDA(cudaEventRecord(c.kev[2], c.stream));
@@ -1323,14 +1373,6 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
                                           dim3(kPThreads), args, sizeof(PersistSmem), c.stream));
     if (c.timing) PBKV_CUDA(cudaEventRecord(c.kev[3], c.stream));
     ++c.launches;
-    if (c.report_deferred) {  // the deferred-heavy reports ride on the same synchronisation
-        const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
-        const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
-        c.hreport_h.reserve(bytes + 2 * nh * sizeof(double));
-        // written by the kernel straight into pinned host memory
-        launch_heavy_report(c, reinterpret_cast<long long*>(res), reinterpret_cast<HeavyReport*>(c.hreport_h.p),
-                            reinterpret_cast<double*>(c.hreport_h.p + bytes));
-    }
     // status + selection state to the host, and the deferral cleared (unless
     // the host-sort fallback below still needs it), before the host wakes up
     decision_epilogue_kernel<<<1, 256, 0, c.stream>>>(c.status.p, ss, c.hstatus.p, hs, c.flags.p, c.heavy.p,
@@ -1412,12 +1454,11 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         PBKV_CUDA(cudaGetLastError());
         c.launches += 2;
         PBKV_CUDA(cudaMemcpyAsync(hs, ss, sizeof(SelState), cudaMemcpyDeviceToHost, c.stream));
-        if (c.report_deferred) {  // the victims changed: fetch the tail record again
+        if (c.report_deferred) {  // the persistent kernel stopped before its reports: all of them here
             const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
             const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
             launch_heavy_report(c, reinterpret_cast<long long*>(res), reinterpret_cast<HeavyReport*>(c.hreport_h.p),
-                                nullptr);
-            (void)bytes;
+                                reinterpret_cast<double*>(c.hreport_h.p + bytes));
         }
         PBKV_CUDA(cudaStreamSynchronize(c.stream));
     }
