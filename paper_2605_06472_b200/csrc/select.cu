@@ -1263,15 +1263,22 @@ __global__ void __launch_bounds__(256) decision_epilogue_kernel(const DevStatus*
                                                                 DevStatus* h_st, SelState* h_ss, std::uint8_t* flags,
                                                                 const int* heavy, int n_clear, const int* victims,
                                                                 int* h_vict, long long h_cap) {
+    if (h_vict) {  // every CTA: 16-byte stores over the victim ids
+        const long long nv = static_cast<long long>(__ldcg(&ss->n_victims));
+        if (!__ldcg(&ss->host_sort) && nv <= h_cap) {
+            const long long n4 = nv >> 2;
+            const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+            const long long nt = static_cast<long long>(gridDim.x) * blockDim.x;
+            for (long long i = t; i < n4; i += nt)
+                reinterpret_cast<int4*>(h_vict)[i] = __ldcg(reinterpret_cast<const int4*>(victims) + i);
+            for (long long i = 4 * n4 + t; i < nv; i += nt) h_vict[i] = __ldcg(victims + i);
+        }
+    }
+    if (blockIdx.x != 0) return;
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ss);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(h_ss);
     for (unsigned int i = threadIdx.x; i < sizeof(SelState) / 8; i += blockDim.x) dst[i] = __ldcg(src + i);
     if (threadIdx.x == 0) *h_st = *st;
-    if (h_vict) {
-        const long long nv = static_cast<long long>(__ldcg(&ss->n_victims));
-        if (!__ldcg(&ss->host_sort) && nv <= h_cap)
-            for (long long i = threadIdx.x; i < nv; i += blockDim.x) h_vict[i] = __ldcg(victims + i);
-    }
     if (__ldcg(&ss->host_sort)) return;
     for (int i = threadIdx.x; i < n_clear; i += blockDim.x) flags[heavy[i]] &= static_cast<std::uint8_t>(~kFlagDeferred);
 }
@@ -1375,7 +1382,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     ++c.launches;
     // status + selection state to the host, and the deferral cleared (unless
     // the host-sort fallback below still needs it), before the host wakes up
-    decision_epilogue_kernel<<<1, 256, 0, c.stream>>>(c.status.p, ss, c.hstatus.p, hs, c.flags.p, c.heavy.p,
+    decision_epilogue_kernel<<<c.epi_vict ? 8 : 1, 256, 0, c.stream>>>(c.status.p, ss, c.hstatus.p, hs, c.flags.p,
+                                                                        c.heavy.p,
                                                       c.report_deferred ? static_cast<int>(c.n_heavy) : 0,
                                                       c.vid_out.p, c.epi_vict, c.epi_cap);
     PBKV_CUDA(cudaGetLastError());
