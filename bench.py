@@ -492,16 +492,20 @@ def main():
     P_pinned = torch.from_numpy(np.ascontiguousarray(P)).pin_memory().numpy()
     e2e_ms = []
     n_victims_e2e = 0
+    e2e_wall = []
     for _ in range(max(1, args.steps)):
         flush.fill_(1)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        tw0 = time.perf_counter()
         e0.record(stream)
         pol.put_forecasts(wf, P_pinned)
+        tw1 = time.perf_counter()
         sel = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
         e1.record(stream)
         e1.synchronize()
+        e2e_wall.append((tw1 - tw0, time.perf_counter() - tw1))
         e2e_ms.append(e0.elapsed_time(e1))
         n_victims_e2e = len(sel)
     assert n_victims_e2e == res[0], "e2e and device-resident decisions disagree"
@@ -584,7 +588,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": total_nodes / (e2e * 1e-3), "unit": "nodes/s",
                 "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size + 4 * locked.size),
-                "d2h_bytes_per_step": int(4 * n_victims_e2e + 24), "ms_per_step": e2e},
+                "d2h_bytes_per_step": int(4 * n_victims_e2e + 24), "ms_per_step": e2e,
+                "host_wall_ms": {"put_forecasts": 1e3 * statistics.median(w[0] for w in e2e_wall),
+                                 "select": 1e3 * statistics.median(w[1] for w in e2e_wall)}},
         "gpu_launches": int(k1 - k0),
         "lib_calls": int(l1 - l0),
         "clocks": clk.result,

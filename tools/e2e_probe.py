@@ -37,3 +37,20 @@ for _ in range(20):
                   vb.ctypes.data_as(C.POINTER(C.c_int32)), int(vb.size), C.byref(nv), C.byref(fr), C.byref(sf))
     tc.append(time.perf_counter() - t0)
 print(f"raw pbkv_select {np.median(tc)*1e6:.0f} us (victims {nv.value})")
+# the bench's e2e loop shape: L2 flush + synchronize before each timed call pair
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+stream = torch.cuda.ExternalStream(pol.stream_handle())
+tw, te = [], []
+for _ in range(20):
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    pol.put_forecasts(wf, Pp)
+    sel = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+    e1.record(stream)
+    e1.synchronize()
+    tw.append(time.perf_counter() - t0)
+    te.append(e0.elapsed_time(e1))
+print(f"flushed e2e: wall {np.median(tw)*1e6:.0f} us, events {np.median(te)*1e3:.0f} us")
