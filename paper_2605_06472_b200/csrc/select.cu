@@ -458,26 +458,35 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
          base += kBatch * nthr) {
-        int n[kBatch], e[kBatch];
+        int n[kBatch], e[kBatch], ln[kBatch];
         bool elig[kBatch];
+        std::uint8_t fl[kBatch], ms[kBatch];
         unsigned int cnt = 0;
+        // every per-node field of the batch in one round trip (coalesced
+        // streams; eligibility is decided after they arrive)
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const std::int64_t i = base + threadIdx.x + j * nthr;
             n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
-            elig[j] = i < a.n_nodes && n[j] != 0 &&
-                      (a.flags[n[j]] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
-                      !__ldcg(&a.sublock[n[j]]);
-            e[j] = elig[j] ? __ldcg(&a.eff[n[j]]) : -1;
+            fl[j] = a.flags[n[j]];
+            elig[j] = !__ldcg(&a.sublock[n[j]]);
+            e[j] = __ldcg(&a.eff[n[j]]);
+            ms[j] = a.missing[n[j]];
+            ln[j] = a.len[n[j]];
         }
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
-            if (!elig[j]) continue;
-            const std::uint8_t ms = a.missing[n[j]];
-            if (ms == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n[j]);
-            if (a.he_recompute && ms && !(a.flags[n[j]] & kFlagRetired))
+            const std::int64_t i = base + threadIdx.x + j * nthr;
+            elig[j] = elig[j] && i < a.n_nodes && n[j] != 0 &&
+                      (fl[j] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE;
+            if (!elig[j]) {
+                e[j] = -1;
+                continue;
+            }
+            if (ms[j] == 2) set_error(a.st, PBKV_EINVAL, kErrKvflowMissing, n[j]);
+            if (a.he_recompute && ms[j] && !(fl[j] & kFlagRetired))
                 set_error(a.st, PBKV_EINVAL, kErrMissingForecast, n[j]);
-            const unsigned long long l = static_cast<unsigned long long>(a.len[n[j]]);
+            const unsigned long long l = static_cast<unsigned long long>(ln[j]);
             atomicAdd(&a.W[e[j]], l);
             atomicAdd(&a.C[e[j]], 1u);
             tok += l;
