@@ -393,13 +393,19 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         int n[kWalk], p[kWalk];
         Key2 km[kWalk];
         bool act[kWalk];
+        std::uint8_t fn[kWalk];
+#pragma unroll
+        for (int j = 0; j < kWalk; ++j) {  // own fields in one round trip (coalesced streams)
+            const std::int64_t i = base + j * nthr;
+            n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
+            fn[j] = a.flags[n[j]];
+            p[j] = a.parent[n[j]];
+            km[j] = load_key(a.keys, n[j]);
+        }
 #pragma unroll
         for (int j = 0; j < kWalk; ++j) {
             const std::int64_t i = base + j * nthr;
-            n[j] = static_cast<int>(i < a.n_nodes ? i : 0);
-            act[j] = i < a.n_nodes && n[j] != 0 && (a.flags[n[j]] & kFlagTierMask) == PBKV_TIER_DEVICE;
-            p[j] = act[j] ? a.parent[n[j]] : 0;
-            km[j] = act[j] ? load_key(a.keys, n[j]) : Key2{0, 0};
+            act[j] = i < a.n_nodes && n[j] != 0 && (fn[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
             // out-of-order parents (deferred heavy / spine) are reduced over
             // their children lists instead: thousands of walkers CAS-ing one
             // hot word serialised in its L2 slice
