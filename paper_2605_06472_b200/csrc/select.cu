@@ -549,13 +549,15 @@ __device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsig
     }
     __syncthreads();
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-    for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_L;
-         base += stride) {
+    const unsigned long long base0 = blockIdx.x * static_cast<unsigned long long>(blockDim.x);
+    int xn = base0 + threadIdx.x < n_L ? __ldcg(&L[base0 + threadIdx.x]) : 0;  // next candidate, one ahead
+    for (unsigned long long base = base0; base < n_L; base += stride) {
         const unsigned long long i = base + threadIdx.x;
         unsigned int d = 0xffffffffu;
         unsigned long long w = 0;
+        const int x = xn;
+        xn = i + stride < n_L ? __ldcg(&L[i + stride]) : 0;
         if (i < n_L) {
-            const int x = __ldcg(&L[i]);
             d = key_bits(load_key(a.keys, x), x, lo, kDigitBits);
             w = __ldcg(&a.W[x]);
         }
@@ -668,14 +670,15 @@ __device__ __forceinline__ void phase_compact(const SelArgs& a, const int* L, un
     unsigned long long orS[3] = {0, 0, 0}, andS[3] = {~0ull, ~0ull, ~0ull};
     unsigned long long orL[3] = {0, 0, 0}, andL[3] = {~0ull, ~0ull, ~0ull};
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-    for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_L;
-         base += stride) {
+    const unsigned long long base0 = blockIdx.x * static_cast<unsigned long long>(blockDim.x);
+    int xn = base0 + threadIdx.x < n_L ? __ldcg(&L[base0 + threadIdx.x]) : 0;  // next candidate, one ahead
+    for (unsigned long long base = base0; base < n_L; base += stride) {
         const unsigned long long i = base + threadIdx.x;
         int d = -1;
-        int x = 0;
+        const int x = xn;
         Key2 k{0, 0};
+        xn = i + stride < n_L ? __ldcg(&L[i + stride]) : 0;
         if (i < n_L) {
-            x = __ldcg(&L[i]);
             k = load_key(a.keys, x);
             d = static_cast<int>(key_bits(k, x, lo, kDigitBits));
         }
