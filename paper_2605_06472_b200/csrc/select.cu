@@ -406,19 +406,24 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         for (int j = 0; j < kWalk; ++j) {
             const std::int64_t i = base + j * nthr;
             act[j] = i < a.n_nodes && n[j] != 0 && (fn[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
-            // out-of-order parents (deferred heavy / spine) are reduced over
-            // their children lists instead: thousands of walkers CAS-ing one
-            // hot word serialised in its L2 slice
-            act[j] = act[j] && p[j] > 0 && !(a.flags[p[j]] & kFlagOutOfOrder);
+            // (out-of-order parents -- deferred heavy / spine -- are reduced
+            // over their children lists instead: thousands of walkers CAS-ing
+            // one hot word serialised in its L2 slice)
+            act[j] = act[j] && p[j] > 0;
         }
-        // eff[p] >= key(p): a walker below its parent's own key stops without
-        // touching eff[p] (the common case -- HE keys grow toward the root)
+        // the parent's flag and key in one round trip.  eff[p] >= key(p): a
+        // walker below its parent's own key stops without touching eff[p]
+        // (the common case -- HE keys grow toward the root)
+        std::uint8_t fp[kWalk];
+        Key2 kp[kWalk];
 #pragma unroll
         for (int j = 0; j < kWalk; ++j) {
-            if (!act[j]) continue;
-            const Key2 kp = load_key(a.keys, p[j]);
-            act[j] = key_less(kp, p[j], km[j], n[j]);
+            fp[j] = act[j] ? a.flags[p[j]] : std::uint8_t(0);
+            kp[j] = act[j] ? load_key(a.keys, p[j]) : Key2{0, 0};
         }
+#pragma unroll
+        for (int j = 0; j < kWalk; ++j)
+            act[j] = act[j] && !(fp[j] & kFlagOutOfOrder) && key_less(kp[j], p[j], km[j], n[j]);
         for (;;) {
             bool any = false;
             int cur[kWalk];
