@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PBKV_ABI_VERSION 1
+#define PBKV_ABI_VERSION 2
 
 typedef enum pbkv_status {
     PBKV_OK = 0,
@@ -145,11 +145,56 @@ int pbkv_ctx_defer_stats(pbkv_ctx* ctx, int64_t* fast, int64_t* slow);
 /* ---- device mirror of the tree --------------------------------------------- */
 /* Full upload of a CacheTree snapshot (SURVEY.md §8(b) pbkv_mirror_full). */
 int pbkv_mirror_full(pbkv_ctx* ctx, const pbkv_tree_soa* soa);
-/* Full upload from a host RadixMirror, then clears its dirty list. */
+
+/* One node of an incremental mirror update (SURVEY.md §8(b) pbkv_mirror_delta):
+ * the node's CURRENT read-side fields (cache.hpp:54-69) after whatever
+ * CacheTree mutation touched it -- match_prefix / insert_suffix / split
+ * (cache.hpp:121-219, :531-569), on_workflow_terminated (:224-250),
+ * demote / promote / drop (:254-301), set_score (:320-325).  Its access
+ * entries are acc_wf / acc_bits[acc_begin, acc_end) of the batch, ascending
+ * WorkflowId (the std::map order of Node::access, cache.hpp:64); they replace
+ * the node's previous entries.  A record whose id equals the mirror's node
+ * count appends a node (node ids stay dense, as CacheTree's do).
+ * depth is the node's depth (root = 0).  split() moves a whole subtree one
+ * level down: a batch that changes a node's depth must carry every node of
+ * its subtree (include/pbkv/tracked_tree.hpp does this). */
+typedef struct pbkv_node_delta {
+    int32_t id;
+    int32_t parent;      /* -1 only for the root */
+    int32_t len;         /* tokens.size() */
+    int32_t ever_tagged;
+    int32_t depth;
+    uint8_t tier;        /* PBKV_TIER_* */
+    uint8_t retired;     /* 0/1 */
+    uint8_t pad[2];
+    uint64_t last_access; /* < 2^63 */
+    double score;        /* cached score (cache.hpp:61) */
+    int64_t acc_begin, acc_end;
+} pbkv_node_delta;
+
+/* CacheTree tier accounting (cache.hpp:81-87) after the batch. */
+typedef struct pbkv_tree_totals {
+    int64_t device_capacity, device_used, retired_device_tokens, host_capacity, host_used;
+} pbkv_tree_totals;
+
+/* Incremental upload: applies n node records in one pinned H2D copy and one
+ * kernel on the context stream (asynchronous; later calls on the context are
+ * ordered after it).  Records are applied in batch order; a node may appear
+ * more than once (the last record wins).  totals may be NULL (unchanged). */
+int pbkv_mirror_delta(pbkv_ctx* ctx, const pbkv_node_delta* nodes, int64_t n, const int64_t* acc_wf,
+                      const uint64_t* acc_bits, const pbkv_tree_totals* totals);
+/* Debug audit (the analogue of CacheTree::audit, cache.hpp:350-416): compares
+ * every mirrored field of the device mirror against a full snapshot.
+ * *mismatch = -1 when identical, else the smallest differing node id (or
+ * n_nodes when only the node count / totals differ). */
+int pbkv_mirror_verify(pbkv_ctx* ctx, const pbkv_tree_soa* soa, int64_t* mismatch);
+
+/* Host trees (pbkv_tree: a flowkv::CacheTree with a change log,
+ * include/pbkv/tracked_tree.hpp).  pbkv_mirror_tree uploads the whole tree;
+ * pbkv_mirror_sync uploads only the nodes changed since this context last
+ * mirrored the same tree (pbkv_mirror_delta), or the whole tree when the
+ * context mirrors another tree or the change log no longer reaches back. */
 int pbkv_mirror_tree(pbkv_ctx* ctx, pbkv_tree* tree);
-/* Incremental upload of only the nodes the host mirror dirtied since the last
- * sync (node fields + access entries; falls back to a full upload when the
- * entry storage must grow). */
 int pbkv_mirror_sync(pbkv_ctx* ctx, pbkv_tree* tree);
 /* Update the cached scores of `n` nodes (CacheTree::set_score, cache.hpp:320). */
 int pbkv_mirror_set_scores(pbkv_ctx* ctx, const int32_t* ids, const double* scores, int64_t n);
@@ -315,7 +360,9 @@ int pbkv_plan_prefetch(pbkv_ctx* ctx, int64_t bandwidth, int step_duration, doub
                        double* cand_values, int64_t cand_cap, int32_t* selected, int64_t sel_cap,
                        pbkv_prefetch_plan* plan);
 
-/* ---- host radix-tree mirror (RadixMirror, cache.hpp semantics) -------------- */
+/* ---- host trees: the reference flowkv::CacheTree (cache.hpp) with a change
+ * log for incremental device sync (include/pbkv/tracked_tree.hpp).  For the
+ * tests, the bench and Python callers; C++ callers use the class directly. */
 int pbkv_tree_create(pbkv_tree** out, int64_t device_capacity, int64_t host_capacity);
 int pbkv_tree_destroy(pbkv_tree* tree);
 /* Applies an op stream (paper_2605_06472_b200/csrc/host/ops.hpp). */
@@ -326,6 +373,10 @@ int pbkv_tree_shape(pbkv_tree* tree, pbkv_tree_soa* soa);
 /* Fills every non-NULL array of soa (sized from pbkv_tree_shape). */
 int pbkv_tree_export(pbkv_tree* tree, pbkv_tree_soa* soa);
 int pbkv_tree_touched(pbkv_tree* tree, int64_t wf, int32_t* ids, int64_t cap, int64_t* n);
+/* Current change-log position, and the distinct nodes changed since `pos`
+ * (ascending, up to cap ids; ids may be NULL): *n_changed = their count, or
+ * -1 when the log no longer reaches back to pos. */
+int pbkv_tree_log(pbkv_tree* tree, int64_t pos, int64_t* end, int32_t* ids, int64_t cap, int64_t* n_changed);
 
 #ifdef __cplusplus
 }

@@ -25,10 +25,13 @@
 // simulator.hpp, by the macro interposition shown in INTEGRATION.md).
 // Include the reference headers first; link libpbkv.so.
 //
-// Tree mirroring: CacheTree has no change log, so every call uploads a full
-// struct-of-arrays image of the tree (SURVEY.md §7 hard part 9: exact, and
-// cheap at the scenario sizes this shim serves).  Large trees use the C ABI
-// directly with an incrementally maintained mirror.  Forecasts are copied at
+// Tree mirroring: a tree that is a TrackedCacheTree (tracked_tree.hpp --
+// the reference CacheTree with a change log; an unmodified simulator.hpp
+// holds one via `#define CacheTree TrackedCacheTree`) is
+// mirrored incrementally: each call uploads only the nodes changed since
+// that context last saw the tree (pbkv_mirror_delta).  A plain CacheTree has
+// no change log, so its calls upload a full struct-of-arrays image (exact;
+// SURVEY.md §7 hard part 9).  Forecasts are copied at
 // call time (the provider's pointers are only valid during the call,
 // SURVEY.md §8(b) "Ownership").  One pbkv context per thread and
 // (K, gamma, A): scenario cells run on separate threads and share nothing
@@ -60,6 +63,7 @@
 #endif
 
 #include "../pbkv.h"
+#include "tracked_tree.hpp"
 
 namespace flowkv::gpu {
 
@@ -79,26 +83,38 @@ inline int device_ordinal() {
     return s ? std::atoi(s) : 0;
 }
 
-// per-thread context cache keyed by the score parameters and agent count
+// per-thread context cache keyed by the score parameters and agent count;
+// each context remembers which tracked tree (uid) its mirror holds and the
+// change-log position it has applied
 class Contexts {
 public:
-    pbkv_ctx* get(int k, double gamma, int agents) {
+    struct Entry {
+        pbkv_ctx* ctx = nullptr;
+        std::uint64_t uid = 0;
+        std::int64_t pos = 0;
+    };
+    Entry& get(int k, double gamma, int agents) {
         auto key = std::make_tuple(k, gamma, agents);
         auto it = ctx_.find(key);
-        if (it != ctx_.end()) return it->second.get();
+        if (it != ctx_.end()) return it->second.e;
         pbkv_cfg cfg{device_ordinal(), k, gamma, agents};
         pbkv_ctx* c = nullptr;
         check(pbkv_ctx_create(&c, &cfg), nullptr);
-        ctx_.emplace(key, Handle(c));
-        return c;
+        Slot& s = ctx_[key];
+        s.h.reset(c);
+        s.e.ctx = c;
+        return s.e;
     }
 
 private:
     struct Del {
         void operator()(pbkv_ctx* c) const { pbkv_ctx_destroy(c); }
     };
-    using Handle = std::unique_ptr<pbkv_ctx, Del>;
-    std::map<std::tuple<int, double, int>, Handle> ctx_;
+    struct Slot {
+        std::unique_ptr<pbkv_ctx, Del> h;
+        Entry e;
+    };
+    std::map<std::tuple<int, double, int>, Slot> ctx_;
 };
 
 inline Contexts& contexts() {
@@ -106,68 +122,19 @@ inline Contexts& contexts() {
     return c;
 }
 
-// Struct-of-arrays image of a CacheTree (read-side fields, cache.hpp:54-69).
-struct TreeImage {
-    std::vector<std::int32_t> parent, len, ever;
-    std::vector<std::uint8_t> tier, retired;
-    std::vector<std::uint64_t> last, bits;
-    std::vector<double> score;
-    std::vector<std::int64_t> off, wf;
-    pbkv_tree_soa soa{};
-
-    void build(const CacheTree& t) {
-        const std::size_t n = t.node_count();
-        parent.resize(n);
-        len.resize(n);
-        ever.resize(n);
-        tier.resize(n);
-        retired.resize(n);
-        last.resize(n);
-        score.resize(n);
-        off.resize(n + 1);
-        wf.clear();
-        bits.clear();
-        for (std::size_t i = 0; i < n; ++i) {
-            const CacheTree::Node& nd = t.node(static_cast<int>(i));
-            parent[i] = nd.parent;
-            len[i] = static_cast<std::int32_t>(nd.tokens.size());
-            ever[i] = nd.ever_tagged;
-            tier[i] = nd.tier == Tier::Device ? PBKV_TIER_DEVICE
-                                              : (nd.tier == Tier::Host ? PBKV_TIER_HOST : PBKV_TIER_ABSENT);
-            retired[i] = nd.retired ? 1 : 0;
-            last[i] = nd.last_access;
-            score[i] = nd.score;
-            off[i] = static_cast<std::int64_t>(wf.size());
-            for (const auto& [w, b] : nd.access) {  // std::map: ascending WorkflowId (cache.hpp:64)
-                wf.push_back(static_cast<std::int64_t>(w));
-                bits.push_back(b);
-            }
-        }
-        off[n] = static_cast<std::int64_t>(wf.size());
-        soa = pbkv_tree_soa{};
-        soa.n_nodes = static_cast<std::int64_t>(n);
-        soa.n_entries = static_cast<std::int64_t>(wf.size());
-        soa.parent = parent.data();
-        soa.len = len.data();
-        soa.tier = tier.data();
-        soa.retired = retired.data();
-        soa.last_access = last.data();
-        soa.ever_tagged = ever.data();
-        soa.score = score.data();
-        soa.acc_off = off.data();
-        soa.acc_wf = wf.data();
-        soa.acc_bits = bits.data();
-        soa.device_capacity = t.device_capacity();
-        soa.device_used = t.device_used();
-        soa.retired_device_tokens = t.retired_device_tokens();
-        soa.host_capacity = t.host_capacity();
-        soa.host_used = t.host_used();
-    }
-};
-
-inline TreeImage& image() {
+// Brings the context's device mirror up to date with `tree`: the changed
+// nodes of a tracked tree, or a full image of a plain CacheTree.
+inline void mirror(Contexts::Entry& e, const CacheTree& tree) {
     thread_local TreeImage img;
-    return img;
+    thread_local DeltaBatch batch;
+    thread_local std::vector<int> ids;
+    if (const TrackedCacheTree* tt = tracked(tree)) {
+        check(sync_mirror(e.ctx, *tt, e.uid, e.pos, ids, batch, img), e.ctx);
+        return;
+    }
+    img.build(tree);
+    e.uid = 0;
+    check(pbkv_mirror_full(e.ctx, &img.soa), e.ctx);
 }
 
 // Uploads the forecasts of every workflow tagged on `ids`, grouped by
@@ -232,14 +199,19 @@ inline int score_ids(CacheTree& tree, std::span<const int> ids, const ForecastPr
     }
     if (ok > 0) {
         int agents = batch.outcomes ? batch.outcomes - 1 : 1;
-        pbkv_ctx* c = contexts().get(params.k, params.gamma, agents);
-        TreeImage& img = image();
-        img.build(tree);
-        check(pbkv_mirror_full(c, &img.soa), c);
+        Contexts::Entry& e = contexts().get(params.k, params.gamma, agents);
+        pbkv_ctx* c = e.ctx;
+        mirror(e, tree);
         batch.upload(c);
         std::vector<double> out(ok);
         check(pbkv_score_nodes(c, ids.data(), static_cast<std::int64_t>(ok), out.data()), c);
-        for (std::size_t i = 0; i < ok; ++i) tree.set_score(ids[i], out[i]);
+        // a tracked tree logs the write-back (set_score is not virtual)
+        if (const TrackedCacheTree* tt = tracked(tree)) {
+            auto* wt = const_cast<TrackedCacheTree*>(tt);
+            for (std::size_t i = 0; i < ok; ++i) wt->set_score(ids[i], out[i]);
+        } else {
+            for (std::size_t i = 0; i < ok; ++i) tree.set_score(ids[i], out[i]);
+        }
     }
     if (err) throw ValidationError(err);
     return static_cast<int>(ok);
@@ -249,10 +221,9 @@ inline VictimSelection select(const CacheTree& tree, int policy, std::int64_t ne
                               const std::map<WorkflowId, std::vector<AgentId>>* remaining,
                               const std::set<int>& locked) {
     // selection needs no forecasts; the context's score parameters are unused
-    pbkv_ctx* c = contexts().get(3, 0.7, 63);
-    TreeImage& img = image();
-    img.build(tree);
-    check(pbkv_mirror_full(c, &img.soa), c);
+    Contexts::Entry& e = contexts().get(3, 0.7, 63);
+    pbkv_ctx* c = e.ctx;
+    mirror(e, tree);
     if (policy == PBKV_POLICY_KVFLOW) {
         std::vector<std::int64_t> wf, off{0};
         std::vector<std::int32_t> seq;
@@ -296,10 +267,9 @@ inline PrefetchPlan plan(const CacheTree& tree, const ForecastProvider& fp, std:
     }
     const int agents = batch.outcomes ? batch.outcomes - 1 : 1;
     // Eq. 1 reads step 0 only: any horizon >= 1 serves (context K = 1)
-    pbkv_ctx* c = contexts().get(1, 0.7, agents);
-    TreeImage& img = image();
-    img.build(tree);
-    check(pbkv_mirror_full(c, &img.soa), c);
+    Contexts::Entry& e = contexts().get(1, 0.7, agents);
+    pbkv_ctx* c = e.ctx;
+    mirror(e, tree);
     batch.upload(c);
     pbkv_prefetch_plan p{};
     const std::int64_t cap = static_cast<std::int64_t>(tree.host_nodes().size());
@@ -432,7 +402,7 @@ struct StateTable {
 
 inline std::vector<Forecast> propagate(int A, const std::vector<double>& rows, const std::vector<std::int32_t>& next,
                                        const std::vector<std::int32_t>& start, int K, double lambda) {
-    pbkv_ctx* c = contexts().get(K, 0.7, A);
+    pbkv_ctx* c = contexts().get(K, 0.7, A).ctx;
     pbkv_fmodel m{A, static_cast<std::int64_t>(rows.size() / static_cast<std::size_t>(A + 1)), rows.data(),
                   next.data()};
     check(pbkv_fmodel_load(c, &m), c);

@@ -5,7 +5,9 @@
 // oracle/Makefile twice from this one file:
 //   _ref/sim_cpu  -- plain reference build (no interposition): the oracle run
 //   _ref/sim_gpu  -- -DPBKV_INTERPOSE: simulator.hpp:434, :464, :618, :636-637,
-//                    :657 call flowkv::gpu::* (the product, libpbkv.so)
+//                    :657 call flowkv::gpu::* (the product, libpbkv.so), and
+//                    the simulator's CacheTree (:349) is a TrackedCacheTree,
+//                    so the device mirror is updated incrementally
 // Technique: SURVEY.md App. A.4 -- the CPU definitions are included first
 // (#pragma once), then the call-site names are macro-renamed only while
 // simulator.hpp is parsed.  No reference source is edited or copied.
@@ -26,6 +28,9 @@
 
 #ifdef PBKV_INTERPOSE
 #include "pbkv/flowkv_gpu.hpp"
+// the simulator's tree carries a change log: every policy call mirrors only
+// the nodes changed since the previous call (pbkv_mirror_delta)
+#define CacheTree TrackedCacheTree
 #define select_victims gpu::select_victims
 #define select_victims_hierarchical gpu::select_victims_hierarchical
 #define plan_conservative_prefetch gpu::plan_conservative_prefetch
@@ -35,6 +40,7 @@
 #endif
 #include "flowkv/simulator.hpp"
 #ifdef PBKV_INTERPOSE
+#undef CacheTree
 #undef select_victims
 #undef select_victims_hierarchical
 #undef plan_conservative_prefetch

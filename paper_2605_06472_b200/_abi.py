@@ -53,6 +53,26 @@ class TreeSoA(C.Structure):
     ]
 
 
+class NodeDelta(C.Structure):
+    """pbkv_node_delta"""
+    _fields_ = [("id", C.c_int32), ("parent", C.c_int32), ("len", C.c_int32), ("ever_tagged", C.c_int32),
+                ("depth", C.c_int32), ("tier", C.c_uint8), ("retired", C.c_uint8), ("pad", C.c_uint8 * 2),
+                ("last_access", C.c_uint64), ("score", C.c_double), ("acc_begin", C.c_int64),
+                ("acc_end", C.c_int64)]
+
+
+NODE_DELTA_DTYPE = np.dtype([("id", np.int32), ("parent", np.int32), ("len", np.int32), ("ever_tagged", np.int32),
+                             ("depth", np.int32), ("tier", np.uint8), ("retired", np.uint8), ("pad", np.uint8, 2),
+                             ("last_access", np.uint64), ("score", np.float64), ("acc_begin", np.int64),
+                             ("acc_end", np.int64)], align=True)
+
+
+class TreeTotals(C.Structure):
+    """pbkv_tree_totals"""
+    _fields_ = [("device_capacity", C.c_int64), ("device_used", C.c_int64), ("retired_device_tokens", C.c_int64),
+                ("host_capacity", C.c_int64), ("host_used", C.c_int64)]
+
+
 class PrefetchPlanC(C.Structure):
     _fields_ = [
         ("budget_space", C.c_int64),
@@ -190,6 +210,8 @@ def lib() -> C.CDLL:
         "pbkv_mirror_full": ([vp, C.POINTER(TreeSoA)], C.c_int),
         "pbkv_mirror_tree": ([vp, vp], C.c_int),
         "pbkv_mirror_sync": ([vp, vp], C.c_int),
+        "pbkv_mirror_delta": ([vp, vp, C.c_int64, _i64p, _u64p, C.POINTER(TreeTotals)], C.c_int),
+        "pbkv_mirror_verify": ([vp, C.POINTER(TreeSoA), _i64p], C.c_int),
         "pbkv_mirror_set_scores": ([vp, _i32p, _f64p, C.c_int64], C.c_int),
         "pbkv_mirror_node_count": ([vp, _i64p, _i64p], C.c_int),
         "pbkv_forecast_put": ([vp, _i64p, C.c_int64, C.c_int, C.c_int, _f64p], C.c_int),
@@ -213,6 +235,7 @@ def lib() -> C.CDLL:
         "pbkv_tree_shape": ([vp, C.POINTER(TreeSoA)], C.c_int),
         "pbkv_tree_export": ([vp, C.POINTER(TreeSoA)], C.c_int),
         "pbkv_tree_touched": ([vp, C.c_int64, _i32p, C.c_int64, _i64p], C.c_int),
+        "pbkv_tree_log": ([vp, C.c_int64, _i64p, _i32p, C.c_int64, _i64p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -12,9 +12,12 @@ Names, argument meaning and error behaviour follow
   single_step_value(node_terms(...))                 Policy.value_nodes
   flowkv::ValidationError                            ValidationError (same messages)
 
-The tree is borrowed as a snapshot: ``Policy.mirror(tree)`` uploads the
-struct-of-arrays image (from a HostTree -- the C++ RadixMirror -- or from any
-SoAArrays export); forecasts are uploaded with ``put_forecasts``.
+The tree is mirrored on the device: ``Policy.mirror(tree)`` uploads the whole
+struct-of-arrays image (from a HostTree -- the reference flowkv::CacheTree
+with a change log -- or from any SoAArrays export), ``Policy.sync(tree)``
+uploads only the nodes changed since (pbkv_mirror_delta), and
+``Policy.apply_delta`` takes caller-built node records; forecasts are
+uploaded with ``put_forecasts``.
 """
 from __future__ import annotations
 
@@ -96,8 +99,9 @@ class PrefetchPlan:
 
 # ----------------------------------------------------------------------------------
 class HostTree:
-    """The C++ RadixMirror (csrc/host/radix_mirror.hpp): cache.hpp mutation
-    semantics, SoA export, dirty tracking."""
+    """The reference flowkv::CacheTree (cache.hpp) wrapped in TrackedCacheTree
+    (include/pbkv/tracked_tree.hpp): the reference mutation semantics, an SoA
+    export and a change log for incremental device sync."""
 
     def __init__(self, device_capacity: int = 1 << 40, host_capacity: int = 1 << 40):
         L = _abi.lib()
@@ -139,6 +143,18 @@ class HostTree:
         s = arr.struct()
         _check(L.pbkv_tree_export(self._h, C.byref(s)), None)
         return arr
+
+    def log(self, pos: int = 0) -> tuple[int, list[int] | None]:
+        """(change-log end, ascending ids of the nodes changed since pos --
+        None when the log no longer reaches back to pos)."""
+        L = _abi.lib()
+        end, n = C.c_int64(), C.c_int64()
+        _check(L.pbkv_tree_log(self._h, int(pos), C.byref(end), None, 0, C.byref(n)), None)
+        if n.value < 0:
+            return end.value, None
+        ids = np.zeros(max(n.value, 1), dtype=np.int32)
+        _check(L.pbkv_tree_log(self._h, int(pos), C.byref(end), ptr(ids, C.c_int32), n.value, C.byref(n)), None)
+        return end.value, ids[: n.value].tolist()
 
     def touched(self, wf: int) -> list[int]:
         L = _abi.lib()
@@ -197,6 +213,38 @@ class Policy:
         n = C.c_int64()
         self._c(L.pbkv_mirror_node_count(self._h, C.byref(n), None))
         self.n_nodes = n.value
+
+    def sync(self, tree: "HostTree") -> None:
+        """pbkv_mirror_sync: upload only the nodes changed since this context
+        last mirrored `tree` (a full upload the first time)."""
+        L = _abi.lib()
+        self._c(L.pbkv_mirror_sync(self._h, tree.handle))
+        n = C.c_int64()
+        self._c(L.pbkv_mirror_node_count(self._h, C.byref(n), None))
+        self.n_nodes = n.value
+
+    def apply_delta(self, records: np.ndarray, acc_wf: np.ndarray, acc_bits: np.ndarray,
+                    totals: Mapping[str, int] | None = None) -> None:
+        """pbkv_mirror_delta: records is a NODE_DELTA_DTYPE array."""
+        L = _abi.lib()
+        r = np.ascontiguousarray(records, dtype=_abi.NODE_DELTA_DTYPE)
+        w = np.ascontiguousarray(acc_wf if len(acc_wf) else [0], dtype=np.int64)
+        b = np.ascontiguousarray(acc_bits if len(acc_bits) else [0], dtype=np.uint64)
+        t = _abi.TreeTotals(**totals) if totals else None
+        self._c(L.pbkv_mirror_delta(self._h, C.c_void_p(r.ctypes.data), int(r.size), ptr(w, C.c_int64),
+                                    ptr(b, C.c_uint64), C.byref(t) if t is not None else None))
+        n = C.c_int64()
+        self._c(L.pbkv_mirror_node_count(self._h, C.byref(n), None))
+        self.n_nodes = n.value
+
+    def verify(self, tree: "HostTree | SoAArrays") -> int:
+        """pbkv_mirror_verify against a full snapshot: -1 when the device
+        mirror equals it field by field, else the first differing node id."""
+        soa = tree.export() if isinstance(tree, HostTree) else tree
+        s = soa.struct(with_depth=isinstance(tree, HostTree))
+        m = C.c_int64()
+        self._c(_abi.lib().pbkv_mirror_verify(self._h, C.byref(s), C.byref(m)))
+        return m.value
 
     def set_scores(self, ids: Sequence[int], scores: Sequence[float]) -> None:
         i = np.ascontiguousarray(ids, dtype=np.int32)

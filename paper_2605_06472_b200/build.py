@@ -17,14 +17,20 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpbkv.so")
 
-SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu", "predict.cu", "shard.cu", "fmodel.cu"]
+SOURCES = ["capi.cu", "score.cu", "select.cu", "prefetch.cu", "predict.cu", "shard.cu", "fmodel.cu",
+           os.path.join("host", "host_tree.cpp")]
 HEADERS = [
     "pbkv_internal.cuh",
     "common.cuh",
     "chain.cuh",
-    os.path.join("host", "radix_mirror.hpp"),
     os.path.join("host", "ops.hpp"),
+    os.path.join("host", "internal_abi.h"),
 ]
+# The host trees (host/host_tree.cpp) ARE the reference flowkv::CacheTree:
+# its header-only sources are compiled in from the reference tree (never
+# copied into this repo).  The GPU box has no /root/reference; it runs the
+# library built here.
+REF_INCLUDE = "/root/reference/proj/include"
 
 NVCC_FLAGS = [
     "-std=c++20",
@@ -34,9 +40,9 @@ NVCC_FLAGS = [
     "arch=compute_100a,code=sm_100a",
     "-Xcompiler",
     "-fPIC",
-    "-shared",
     "--expt-relaxed-constexpr",
 ]
+LINK_FLAGS = ["-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC"]
 
 
 def _nvcc() -> str:
@@ -54,11 +60,37 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 
 def build_product(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiles to its own object (in parallel, rebuilt
+    when it or a shared header changed), then one nvcc link into libpbkv.so."""
+    from concurrent.futures import ThreadPoolExecutor
+
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pbkv.h")]
-    if not force and not _stale(LIB, deps):
+    shared = [os.path.join(CSRC, h) for h in HEADERS] + [
+        os.path.join(ROOT, "include", "pbkv.h"), os.path.join(ROOT, "include", "pbkv", "tracked_tree.hpp")]
+    if not os.path.isdir(REF_INCLUDE):
+        if os.path.exists(LIB):
+            return LIB  # GPU box: the prebuilt library travelled with the snapshot
+        raise RuntimeError(f"libpbkv.so is not built and {REF_INCLUDE} (the CacheTree headers) is absent")
+    odir = os.path.join(PKG, "_build")
+    os.makedirs(odir, exist_ok=True)
+    objs = [os.path.join(odir, os.path.basename(s) + ".o") for s in srcs]
+    todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, [s] + shared)]
+    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + REF_INCLUDE]
+
+    def compile_one(so):
+        src, obj = so
+        cmd = [_nvcc(), *NVCC_FLAGS, *inc, "-c", "-o", obj + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
+
+    if todo:
+        with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
+            list(ex.map(compile_one, todo))
+    if not todo and not force and not _stale(LIB, objs):
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *srcs]
+    cmd = [_nvcc(), *LINK_FLAGS, "-o", LIB + ".tmp", *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

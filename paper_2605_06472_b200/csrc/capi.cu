@@ -8,16 +8,10 @@
 #include <string>
 #include <vector>
 
-#include "host/ops.hpp"
-#include "host/radix_mirror.hpp"
+#include "host/internal_abi.h"
 #include "pbkv_internal.cuh"
 
 struct pbkv_ctx : pbkv::Context {};
-struct pbkv_tree {
-    pbkv::RadixMirror tree;
-    std::string err;
-    pbkv_tree(std::int64_t d, std::int64_t h) : tree(d, h) {}
-};
 
 namespace {
 
@@ -33,42 +27,11 @@ int api(pbkv_ctx* c, F&& f) {
     } catch (const ApiError& e) {
         (c ? c->err : g_last_error) = e.what();
         return e.status;
-    } catch (const pbkv::ValidationError& e) {
-        (c ? c->err : g_last_error) = e.what();
-        return PBKV_EINVAL;
-    } catch (const OpStreamError& e) {
-        (c ? c->err : g_last_error) = e.what();
-        return PBKV_EARG;
     } catch (const std::bad_alloc&) {
         (c ? c->err : g_last_error) = "host allocation failed";
         return PBKV_ENOMEM;
     } catch (const std::exception& e) {
         (c ? c->err : g_last_error) = e.what();
-        return PBKV_EARG;
-    }
-}
-
-template <class F>
-int tree_api(pbkv_tree* t, F&& f) {
-    try {
-        if (!t) throw ApiError(PBKV_EARG, "null tree");
-        f();
-        return PBKV_OK;
-    } catch (const ApiError& e) {
-        (t ? t->err : g_last_error) = e.what();
-        g_last_error = e.what();
-        return e.status;
-    } catch (const pbkv::ValidationError& e) {
-        t->err = e.what();
-        g_last_error = e.what();
-        return PBKV_EINVAL;
-    } catch (const OpStreamError& e) {
-        t->err = e.what();
-        g_last_error = e.what();
-        return PBKV_EARG;
-    } catch (const std::exception& e) {
-        t->err = e.what();
-        g_last_error = e.what();
         return PBKV_EARG;
     }
 }
@@ -152,11 +115,11 @@ void ensure_scratch(Context& c) {
 std::string missing_message(Context& c, long long node) {
     // first entry of `node` (WorkflowId order) lacking a forecast: node_terms
     // raises before multi_step_score checks horizons (scoring.hpp:66-75, :53)
-    unsigned int off[2];
-    PBKV_CUDA(cudaMemcpy(off, c.acc_off.p + node, sizeof off, cudaMemcpyDeviceToHost));
-    std::vector<int> slots(off[1] - off[0]);
+    uint2 rg;
+    PBKV_CUDA(cudaMemcpy(&rg, c.acc_rng.p + node, sizeof rg, cudaMemcpyDeviceToHost));
+    std::vector<int> slots(rg.y - rg.x);
     if (!slots.empty())
-        PBKV_CUDA(cudaMemcpy(slots.data(), c.acc_slot.p + off[0], slots.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        PBKV_CUDA(cudaMemcpy(slots.data(), c.acc_slot.p + rg.x, slots.size() * sizeof(int), cudaMemcpyDeviceToHost));
     std::vector<std::uint8_t> st(static_cast<std::size_t>(c.n_slots));
     if (!st.empty()) PBKV_CUDA(cudaMemcpy(st.data(), c.fstate.p, st.size(), cudaMemcpyDeviceToHost));
     for (int s : slots)
@@ -168,11 +131,11 @@ std::string missing_message(Context& c, long long node) {
 }
 
 std::string kvflow_message(Context& c, long long node) {
-    unsigned int off[2];
-    PBKV_CUDA(cudaMemcpy(off, c.acc_off.p + node, sizeof off, cudaMemcpyDeviceToHost));
-    std::vector<int> slots(off[1] - off[0]);
+    uint2 rg;
+    PBKV_CUDA(cudaMemcpy(&rg, c.acc_rng.p + node, sizeof rg, cudaMemcpyDeviceToHost));
+    std::vector<int> slots(rg.y - rg.x);
     if (!slots.empty())
-        PBKV_CUDA(cudaMemcpy(slots.data(), c.acc_slot.p + off[0], slots.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        PBKV_CUDA(cudaMemcpy(slots.data(), c.acc_slot.p + rg.x, slots.size() * sizeof(int), cudaMemcpyDeviceToHost));
     std::vector<std::uint8_t> has(static_cast<std::size_t>(c.n_slots));
     if (!has.empty()) PBKV_CUDA(cudaMemcpy(has.data(), c.rem_has.p, has.size(), cudaMemcpyDeviceToHost));
     for (int s : slots)
@@ -278,150 +241,48 @@ void upload_children(Context& c, const std::vector<int>& nodes, DevBuf<int>& off
 }
 
 // ---- mirror -----------------------------------------------------------------
-void mirror_full(Context& c, const pbkv_tree_soa& s) {
-    need(s.n_nodes >= 1, "tree must contain the root");
-    need(s.parent && s.len && s.tier && s.retired && s.last_access && s.ever_tagged && s.acc_off,
-         "tree soa: missing required array");
-    need(s.n_entries == 0 || (s.acc_wf && s.acc_bits), "tree soa: missing access arrays");
-    need(s.n_nodes < INT_MAX, "tree too large for int32 node ids");
-    need(s.n_entries < static_cast<std::int64_t>(UINT_MAX), "too many access entries");
-    const std::int64_t n = s.n_nodes, E = s.n_entries;
-    std::vector<std::uint8_t> flags(static_cast<std::size_t>(n));
-    std::vector<unsigned int> off(static_cast<std::size_t>(n) + 1);
-    std::vector<int> slot(static_cast<std::size_t>(E));
-    std::vector<int2> lslot(static_cast<std::size_t>(n));
-    std::vector<ulonglong2> lbits(static_cast<std::size_t>(n));
+// Eq. 2 class of a node with `ne` entries (score.cu): light <= 2 entries,
+// medium chain <= kMediumMaxChain, heavy above
+enum NodeClass : int { kLight = 0, kMedium = 1, kHeavy = 2 };
+NodeClass class_of(const Context& c, std::int64_t ne) {
+    if (ne * c.K > kMediumMaxChain) return kHeavy;
+    return ne > 2 ? kMedium : kLight;
+}
+
+// The class-derived tables, rebuilt from the host copies of the node fields:
+// the medium / heavy lists, the products list of their entries (heavy first,
+// then medium: combined index n_heavy + m, score.cu), the deferral placement
+// tables of the heavy nodes (place_deferred) and, when `children`, the
+// children lists of the heavy nodes (an O(n) scan over the parents).
+void rebuild_classes(Context& c, bool children) {
     std::vector<int> medium, heavy, hent_node;
     std::vector<unsigned int> hent;
     std::vector<long long> hstart;
-    std::vector<int> depth;
-    c.h_entries.assign(static_cast<std::size_t>(n), 0);
-    c.h_heavy_last.clear();
-    c.h_heavy_parent.clear();
-    c.h_heavy_flags.clear();
-    for (std::int64_t i = 0; i < n; ++i) {
-        if (s.tier[i] > PBKV_TIER_ABSENT) invalid("tree soa: bad tier value");
-        flags[static_cast<std::size_t>(i)] =
-            static_cast<std::uint8_t>(s.tier[i] | (s.retired[i] ? kFlagRetired : 0));
-        if (i > 0 && (s.parent[i] < 0 || s.parent[i] >= n)) invalid("tree soa: parent out of range");
-        std::int64_t a = s.acc_off[i], b = s.acc_off[i + 1];
-        if (a < 0 || b < a || b > E) invalid("tree soa: bad access offsets");
-        off[static_cast<std::size_t>(i)] = static_cast<unsigned int>(a);
-        for (std::int64_t e = a; e < b; ++e) {
-            if (e > a && s.acc_wf[e] <= s.acc_wf[e - 1]) invalid("tree soa: access entries must ascend by workflow id");
-            slot[static_cast<std::size_t>(e)] = slot_for(c, s.acc_wf[e]);
-        }
-        const std::int64_t ne = b - a;
-        c.h_entries[static_cast<std::size_t>(i)] = static_cast<int>(ne);
-        {
-            int2 ls{-1, -1};
-            ulonglong2 lb{0ull, 0ull};
-            if (ne > 2) {
-                ls.x = ls.y = -2;
-            } else {
-                if (ne >= 1) {
-                    ls.x = slot[static_cast<std::size_t>(a)];
-                    lb.x = s.acc_bits[a];
-                }
-                if (ne == 2) {
-                    ls.y = slot[static_cast<std::size_t>(a + 1)];
-                    lb.y = s.acc_bits[a + 1];
-                }
-            }
-            lslot[static_cast<std::size_t>(i)] = ls;
-            lbits[static_cast<std::size_t>(i)] = lb;
-        }
-        // node classes of the Eq. 2 kernels (score.cu): light <= 2 entries,
-        // medium chain <= kMediumMaxChain, heavy above
-        if (ne * c.K > kMediumMaxChain) {
-            hstart.push_back(static_cast<long long>(hent.size()) * c.K);
-            for (std::int64_t e = a; e < b; ++e) {
-                hent.push_back(static_cast<unsigned int>(e));
-                hent_node.push_back(static_cast<int>(heavy.size()));
-            }
-            heavy.push_back(static_cast<int>(i));
-            c.h_heavy_last.push_back(s.last_access[i]);
-            c.h_heavy_parent.push_back(s.parent[i]);
-            c.h_heavy_flags.push_back(static_cast<std::uint8_t>(s.tier[i] | (s.retired[i] ? kFlagRetired : 0)));
-        } else if (ne > 2) {
-            medium.push_back(static_cast<int>(i));
-        }
+    for (std::int64_t i = 0; i < c.n; ++i) {
+        const NodeClass k = class_of(c, c.h_entries[static_cast<std::size_t>(i)]);
+        if (k == kHeavy) heavy.push_back(static_cast<int>(i));
+        else if (k == kMedium) medium.push_back(static_cast<int>(i));
     }
-    off[static_cast<std::size_t>(n)] = static_cast<unsigned int>(E);
-    // medium nodes' entries follow the heavy ones in the product list
-    // (combined index n_heavy + m): their products are formed by the same
-    // grid-wide kernel and each chain is added by one warp (score.cu)
-    for (std::size_t m = 0; m < medium.size(); ++m) {
-        const int i = medium[m];
+    auto add_entries = [&](int node, int idx) {
         hstart.push_back(static_cast<long long>(hent.size()) * c.K);
-        for (std::int64_t e = s.acc_off[i]; e < s.acc_off[i + 1]; ++e) {
-            hent.push_back(static_cast<unsigned int>(e));
-            hent_node.push_back(static_cast<int>(heavy.size() + m));
+        const unsigned int b = c.h_acc_beg[static_cast<std::size_t>(node)];
+        const int ne = c.h_entries[static_cast<std::size_t>(node)];
+        for (int e = 0; e < ne; ++e) {
+            hent.push_back(b + static_cast<unsigned int>(e));
+            hent_node.push_back(idx);
         }
-    }
-    const int* dep = s.depth;
-    if (!dep) {
-        depth.assign(static_cast<std::size_t>(n), -1);
-        depth[0] = 0;
-        std::vector<int> stack;
-        for (std::int64_t i = 1; i < n; ++i) {
-            int v = static_cast<int>(i);
-            while (depth[static_cast<std::size_t>(v)] < 0) {
-                stack.push_back(v);
-                v = s.parent[v];
-                if (stack.size() > static_cast<std::size_t>(n)) invalid("tree soa: parent cycle");
-            }
-            int d = depth[static_cast<std::size_t>(v)];
-            while (!stack.empty()) {
-                depth[static_cast<std::size_t>(stack.back())] = ++d;
-                stack.pop_back();
-            }
-        }
-        dep = depth.data();
-    }
-    int maxd = 0;
-    for (std::int64_t i = 0; i < n; ++i) maxd = std::max(maxd, dep[i]);
-    if (maxd >= (1 << 24)) invalid("tree deeper than 2^24 levels");
-
-    c.n = n;
-    c.E = E;
-    c.parent.reserve(n);
-    c.len.reserve(n);
-    c.ever.reserve(n);
-    c.depth.reserve(n);
-    c.flags.reserve(n);
-    c.last.reserve(n);
-    c.score.reserve(n);
-    c.acc_off.reserve(n + 1);
-    c.lslot.reserve(n);
-    c.lbits.reserve(n);
-    c.acc_slot.reserve(E + 1);
-    c.acc_bits.reserve(E + 1);
-    c.heavy.reserve(heavy.size() + 1);
+    };
+    for (std::size_t j = 0; j < heavy.size(); ++j) add_entries(heavy[j], static_cast<int>(j));
+    for (std::size_t m = 0; m < medium.size(); ++m) add_entries(medium[m], static_cast<int>(heavy.size() + m));
     cudaStream_t st = c.stream;
-    PBKV_CUDA(cudaMemcpyAsync(c.parent.p, s.parent, n * sizeof(int), cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.len.p, s.len, n * sizeof(int), cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.ever.p, s.ever_tagged, n * sizeof(int), cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.depth.p, dep, n * sizeof(int), cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.flags.p, flags.data(), n, cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.last.p, s.last_access, n * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
-    if (s.score)
-        PBKV_CUDA(cudaMemcpyAsync(c.score.p, s.score, n * sizeof(double), cudaMemcpyHostToDevice, st));
-    else
-        PBKV_CUDA(cudaMemsetAsync(c.score.p, 0, n * sizeof(double), st));
-    PBKV_CUDA(cudaMemcpyAsync(c.acc_off.p, off.data(), (n + 1) * sizeof(unsigned int), cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.lslot.p, lslot.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st));
-    PBKV_CUDA(cudaMemcpyAsync(c.lbits.p, lbits.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice, st));
-    if (E > 0) {
-        PBKV_CUDA(cudaMemcpyAsync(c.acc_slot.p, slot.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
-        PBKV_CUDA(cudaMemcpyAsync(c.acc_bits.p, s.acc_bits, E * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
-    }
     c.medium.reserve(medium.size() + 1);
+    c.heavy.reserve(heavy.size() + 1);
     c.hent.reserve(hent.size() + 1);
     c.hent_node.reserve(hent.size() + 1);
     c.hstart.reserve(heavy.size() + medium.size() + 1);
     c.hmiss.reserve(heavy.size() + medium.size() + 1);
     c.hxs.reserve(hent.size() * static_cast<std::size_t>(c.K) + 1);
+    // the host vectors die at return: the copies complete before it
     if (!medium.empty())
         PBKV_CUDA(cudaMemcpyAsync(c.medium.p, medium.data(), medium.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     if (!heavy.empty())
@@ -434,93 +295,533 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
         PBKV_CUDA(cudaMemcpyAsync(c.hstart.p, hstart.data(), hstart.size() * sizeof(long long), cudaMemcpyHostToDevice,
                                   st));
     }
+    const bool heavy_changed = heavy != c.h_heavy;
     c.n_medium = static_cast<std::int64_t>(medium.size());
     c.n_heavy = static_cast<std::int64_t>(heavy.size());
+    c.n_hent = static_cast<std::int64_t>(hent.size());
     c.h_heavy = heavy;
+    if (children || heavy_changed) upload_children(c, heavy, c.hch_off, c.hch);
+    // deferral placement tables (place_deferred)
+    const std::size_t nh = heavy.size();
+    c.h_heavy_last.resize(nh);
+    c.h_heavy_parent.resize(nh);
+    c.h_heavy_flags.resize(nh);
+    c.h_heavy_depth.resize(nh);
+    for (std::size_t j = 0; j < nh; ++j) {
+        const std::size_t v = static_cast<std::size_t>(heavy[j]);
+        c.h_heavy_last[j] = c.h_last[v];
+        c.h_heavy_parent[j] = c.h_parent[v];
+        c.h_heavy_flags[j] = c.h_flags[v];
+        c.h_heavy_depth[j] = c.h_depth[v];
+    }
+    c.h_heavy_order.resize(nh);
+    for (std::size_t j = 0; j < nh; ++j) c.h_heavy_order[j] = j;
+    std::stable_sort(c.h_heavy_order.begin(), c.h_heavy_order.end(),
+                     [&](std::size_t a, std::size_t b) { return c.h_heavy_depth[a] > c.h_heavy_depth[b]; });
+    std::unordered_map<int, int> pos;
+    for (std::size_t j = 0; j < nh; ++j) pos[heavy[j]] = static_cast<int>(j);
+    std::vector<std::vector<int>> kids(nh);
+    for (std::size_t q = 0; q < nh; ++q) {  // heavy children in index order
+        const auto it = pos.find(c.h_heavy_parent[q]);
+        if (it != pos.end()) kids[static_cast<std::size_t>(it->second)].push_back(static_cast<int>(q));
+    }
+    c.h_heavy_kid_off.assign(1, 0);
+    c.h_heavy_kids.clear();
+    for (std::size_t j = 0; j < nh; ++j) {
+        c.h_heavy_kids.insert(c.h_heavy_kids.end(), kids[j].begin(), kids[j].end());
+        c.h_heavy_kid_off.push_back(static_cast<int>(c.h_heavy_kids.size()));
+    }
+    PBKV_CUDA(cudaStreamSynchronize(st));
+}
+
+void set_totals(Context& c, const pbkv_tree_totals& t) {
+    c.device_capacity = t.device_capacity;
+    c.device_used = t.device_used;
+    c.retired_device_tokens = t.retired_device_tokens;
+    c.host_capacity = t.host_capacity;
+    c.host_used = t.host_used;
+}
+
+void mirror_full(Context& c, const pbkv_tree_soa& s) {
+    need(s.n_nodes >= 1, "tree must contain the root");
+    need(s.parent && s.len && s.tier && s.retired && s.last_access && s.ever_tagged && s.acc_off,
+         "tree soa: missing required array");
+    need(s.n_entries == 0 || (s.acc_wf && s.acc_bits), "tree soa: missing access arrays");
+    need(s.n_nodes < INT_MAX, "tree too large for int32 node ids");
+    need(s.n_entries < static_cast<std::int64_t>(UINT_MAX / 2), "too many access entries");
+    const std::int64_t n = s.n_nodes, E = s.n_entries;
+    const std::size_t nz = static_cast<std::size_t>(n);
+    std::vector<uint2> rng(nz);
+    std::vector<int> slot(static_cast<std::size_t>(E));
+    std::vector<int2> lslot(nz);
+    std::vector<ulonglong2> lbits(nz);
+    c.h_entries.assign(nz, 0);
+    c.h_acc_beg.assign(nz, 0);
+    c.h_acc_cap.assign(nz, 0);
+    c.h_flags.assign(nz, 0);
+    c.h_last.assign(s.last_access, s.last_access + n);
     c.h_parent.assign(s.parent, s.parent + n);
-    upload_children(c, heavy, c.hch_off, c.hch);
-    c.h_heavy_depth.resize(heavy.size());
-    for (std::size_t j = 0; j < heavy.size(); ++j) c.h_heavy_depth[j] = dep[heavy[j]];
-    {  // deferral placement tables (place_deferred), once per mirror
-        const std::size_t nh = heavy.size();
-        c.h_heavy_order.resize(nh);
-        for (std::size_t j = 0; j < nh; ++j) c.h_heavy_order[j] = j;
-        std::stable_sort(c.h_heavy_order.begin(), c.h_heavy_order.end(),
-                         [&](std::size_t a, std::size_t b) { return c.h_heavy_depth[a] > c.h_heavy_depth[b]; });
-        std::unordered_map<int, int> pos;
-        for (std::size_t j = 0; j < nh; ++j) pos[heavy[j]] = static_cast<int>(j);
-        std::vector<std::vector<int>> kids(nh);
-        for (std::size_t q = 0; q < nh; ++q) {  // heavy children in index order (as the scan below visited them)
-            const auto it = pos.find(c.h_heavy_parent[q]);
-            if (it != pos.end()) kids[static_cast<std::size_t>(it->second)].push_back(static_cast<int>(q));
+    for (std::int64_t i = 0; i < n; ++i) {
+        const std::size_t iz = static_cast<std::size_t>(i);
+        if (s.tier[i] > PBKV_TIER_ABSENT) invalid("tree soa: bad tier value");
+        c.h_flags[iz] = static_cast<std::uint8_t>(s.tier[i] | (s.retired[i] ? kFlagRetired : 0));
+        if (i > 0 && (s.parent[i] < 0 || s.parent[i] >= n)) invalid("tree soa: parent out of range");
+        std::int64_t a = s.acc_off[i], b = s.acc_off[i + 1];
+        if (a < 0 || b < a || b > E) invalid("tree soa: bad access offsets");
+        for (std::int64_t e = a; e < b; ++e) {
+            if (e > a && s.acc_wf[e] <= s.acc_wf[e - 1]) invalid("tree soa: access entries must ascend by workflow id");
+            slot[static_cast<std::size_t>(e)] = slot_for(c, s.acc_wf[e]);
         }
-        c.h_heavy_kid_off.assign(1, 0);
-        c.h_heavy_kids.clear();
-        for (std::size_t j = 0; j < nh; ++j) {
-            c.h_heavy_kids.insert(c.h_heavy_kids.end(), kids[j].begin(), kids[j].end());
-            c.h_heavy_kid_off.push_back(static_cast<int>(c.h_heavy_kids.size()));
+        const std::int64_t ne = b - a;
+        rng[iz] = make_uint2(static_cast<unsigned int>(a), static_cast<unsigned int>(b));
+        c.h_entries[iz] = static_cast<int>(ne);
+        c.h_acc_beg[iz] = static_cast<unsigned int>(a);
+        c.h_acc_cap[iz] = static_cast<unsigned int>(ne);
+        int2 ls{-1, -1};
+        ulonglong2 lb{0ull, 0ull};
+        if (ne > 2) {
+            ls.x = ls.y = -2;
+        } else {
+            if (ne >= 1) {
+                ls.x = slot[static_cast<std::size_t>(a)];
+                lb.x = s.acc_bits[a];
+            }
+            if (ne == 2) {
+                ls.y = slot[static_cast<std::size_t>(a + 1)];
+                lb.y = s.acc_bits[a + 1];
+            }
+        }
+        lslot[iz] = ls;
+        lbits[iz] = lb;
+    }
+    if (s.depth) {
+        c.h_depth.assign(s.depth, s.depth + n);
+    } else {
+        c.h_depth.assign(nz, -1);
+        c.h_depth[0] = 0;
+        std::vector<int> stack;
+        for (std::int64_t i = 1; i < n; ++i) {
+            int v = static_cast<int>(i);
+            while (c.h_depth[static_cast<std::size_t>(v)] < 0) {
+                stack.push_back(v);
+                v = s.parent[v];
+                if (stack.size() > nz) invalid("tree soa: parent cycle");
+            }
+            int d = c.h_depth[static_cast<std::size_t>(v)];
+            while (!stack.empty()) {
+                c.h_depth[static_cast<std::size_t>(stack.back())] = ++d;
+                stack.pop_back();
+            }
         }
     }
-    c.n_hent = static_cast<std::int64_t>(hent.size());
+    int maxd = 0;
+    for (int d : c.h_depth) maxd = std::max(maxd, d);
+    if (maxd >= (1 << 24)) invalid("tree deeper than 2^24 levels");
+
+    c.n = n;
+    c.E = E;
+    c.pool_top = E;
+    c.parent.reserve(nz);
+    c.len.reserve(nz);
+    c.ever.reserve(nz);
+    c.depth.reserve(nz);
+    c.flags.reserve(nz);
+    c.last.reserve(nz);
+    c.score.reserve(nz);
+    c.acc_rng.reserve(nz);
+    c.lslot.reserve(nz);
+    c.lbits.reserve(nz);
+    c.acc_slot.reserve(static_cast<std::size_t>(E) + 1);
+    c.acc_bits.reserve(static_cast<std::size_t>(E) + 1);
+    cudaStream_t st = c.stream;
+    PBKV_CUDA(cudaMemcpyAsync(c.parent.p, s.parent, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.len.p, s.len, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.ever.p, s.ever_tagged, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.depth.p, c.h_depth.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.flags.p, c.h_flags.data(), n, cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.last.p, s.last_access, n * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
+    if (s.score)
+        PBKV_CUDA(cudaMemcpyAsync(c.score.p, s.score, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    else
+        PBKV_CUDA(cudaMemsetAsync(c.score.p, 0, n * sizeof(double), st));
+    PBKV_CUDA(cudaMemcpyAsync(c.acc_rng.p, rng.data(), n * sizeof(uint2), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.lslot.p, lslot.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st));
+    PBKV_CUDA(cudaMemcpyAsync(c.lbits.p, lbits.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice, st));
+    if (E > 0) {
+        PBKV_CUDA(cudaMemcpyAsync(c.acc_slot.p, slot.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaMemcpyAsync(c.acc_bits.p, s.acc_bits, E * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
+    }
+    c.h_heavy.clear();
+    rebuild_classes(c, true);
     c.max_depth = maxd;
-    c.device_capacity = s.device_capacity;
-    c.device_used = s.device_used;
-    c.retired_device_tokens = s.retired_device_tokens;
-    c.host_capacity = s.host_capacity;
-    c.host_used = s.host_used;
+    set_totals(c, pbkv_tree_totals{s.device_capacity, s.device_used, s.retired_device_tokens, s.host_capacity,
+                                   s.host_used});
     ensure_scratch(c);
     if (!c.spine.empty()) {
         for (int v : c.spine) need(v >= 0 && v < n, "shard spine id out of range for the mirrored tree");
         shard_apply_flags(c);
         upload_children(c, c.spine, c.sch_off, c.sch);
     }
+    c.mirror_uid = 0;  // a snapshot of no tracked tree
     PBKV_CUDA(cudaStreamSynchronize(st));
 }
 
-struct SoaStore {
-    std::vector<int> parent, len, ever, dc, depth;
-    std::vector<std::uint8_t> tier, retired;
-    std::vector<std::uint64_t> last, bits;
-    std::vector<double> score;
-    std::vector<std::int64_t> off, wf;
-    pbkv_tree_soa soa{};
-    void fill(const RadixMirror& t) {
-        std::size_t n = t.node_count(), e = t.entry_count();
-        parent.resize(n);
-        len.resize(n);
-        ever.resize(n);
-        dc.resize(n);
-        depth.resize(n);
-        tier.resize(n);
-        retired.resize(n);
-        last.resize(n);
-        score.resize(n);
-        off.resize(n + 1);
-        wf.resize(e);
-        bits.resize(e);
-        t.export_soa(parent.data(), len.data(), tier.data(), retired.data(), last.data(), ever.data(), score.data(),
-                     dc.data(), depth.data(), off.data(), wf.data(), bits.data());
-        soa.n_nodes = static_cast<std::int64_t>(n);
-        soa.n_entries = static_cast<std::int64_t>(e);
-        soa.parent = parent.data();
-        soa.len = len.data();
-        soa.tier = tier.data();
-        soa.retired = retired.data();
-        soa.last_access = last.data();
-        soa.ever_tagged = ever.data();
-        soa.score = score.data();
-        soa.device_children = dc.data();
-        soa.depth = depth.data();
-        soa.acc_off = off.data();
-        soa.acc_wf = wf.data();
-        soa.acc_bits = bits.data();
-        soa.device_capacity = t.device_capacity();
-        soa.device_used = t.device_used();
-        soa.retired_device_tokens = t.retired_device_tokens();
-        soa.host_capacity = t.host_capacity();
-        soa.host_used = t.host_used();
-    }
+// ---- incremental mirror (pbkv_mirror_delta) ----------------------------------
+// Device record of one updated node: every mirrored field, the node's entry
+// segment in the pool and its light-pass copies (lslot / lbits).
+struct DeltaRec {
+    int id, parent, len, ever, depth;
+    unsigned int beg, cnt;
+    int ls0, ls1;
+    unsigned int flags;
+    unsigned long long last, lb0, lb1;
+    double score;
 };
+
+struct MirrorPtrs {
+    int *parent, *len, *ever, *depth;
+    std::uint8_t* flags;
+    unsigned long long* last;
+    double* score;
+    uint2* rng;
+    int2* lslot;
+    ulonglong2* lbits;
+    int* slot;
+    unsigned long long* bits;
+};
+
+// records, then entries (dst position in the pool computed on the host),
+// grid-stride: one launch per batch whatever its shape
+__global__ void __launch_bounds__(256) mirror_delta_kernel(const DeltaRec* rec, long long n_rec,
+                                                           const unsigned int* edst, const int* eslot,
+                                                           const unsigned long long* ebits, long long n_ent,
+                                                           MirrorPtrs m) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_rec; i += stride) {
+        const DeltaRec r = rec[i];
+        m.parent[r.id] = r.parent;
+        m.len[r.id] = r.len;
+        m.ever[r.id] = r.ever;
+        m.depth[r.id] = r.depth;
+        m.flags[r.id] = static_cast<std::uint8_t>(r.flags);
+        m.last[r.id] = r.last;
+        m.score[r.id] = r.score;
+        m.rng[r.id] = make_uint2(r.beg, r.beg + r.cnt);
+        m.lslot[r.id] = make_int2(r.ls0, r.ls1);
+        m.lbits[r.id] = make_ulonglong2(r.lb0, r.lb1);
+    }
+    for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j < n_ent; j += stride) {
+        const unsigned int d = edst[j];
+        m.slot[d] = eslot[j];
+        m.bits[d] = ebits[j];
+    }
+}
+
+// pool repack: node i's entries move to new_beg[i] (dst buffers are fresh)
+__global__ void __launch_bounds__(256) pool_repack_kernel(const uint2* rng_old, const unsigned int* new_beg,
+                                                          long long n, const int* slot_old,
+                                                          const unsigned long long* bits_old, int* slot_new,
+                                                          unsigned long long* bits_new, uint2* rng_new) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint2 r = rng_old[i];
+        const unsigned int b = new_beg[i];
+        for (unsigned int e = r.x; e < r.y; ++e) {
+            slot_new[b + (e - r.x)] = slot_old[e];
+            bits_new[b + (e - r.x)] = bits_old[e];
+        }
+        rng_new[i] = make_uint2(b, b + (r.y - r.x));
+    }
+}
+
+MirrorPtrs mirror_ptrs(Context& c) {
+    return MirrorPtrs{c.parent.p, c.len.p,   c.ever.p,  c.depth.p, c.flags.p,    c.last.p,
+                      c.score.p,  c.acc_rng.p, c.lslot.p, c.lbits.p, c.acc_slot.p, c.acc_bits.p};
+}
+
+// Dead pool space above half: pack every node's segment tightly (a device
+// copy into fresh buffers; the host knows every segment's size).
+void repack_pool(Context& c) {
+    const std::size_t nz = static_cast<std::size_t>(c.n);
+    std::vector<unsigned int> nb(nz);
+    unsigned int top = 0;
+    for (std::size_t i = 0; i < nz; ++i) {
+        nb[i] = top;
+        top += static_cast<unsigned int>(c.h_entries[i]);
+    }
+    DevBuf<int> slot_new;
+    DevBuf<unsigned long long> bits_new;
+    DevBuf<uint2> rng_new;
+    DevBuf<unsigned int> nb_d;
+    slot_new.reserve(std::max<std::size_t>(top, 1) + (top >> 2));
+    bits_new.reserve(slot_new.cap);
+    rng_new.reserve(std::max<std::size_t>(c.acc_rng.cap, nz));
+    nb_d.reserve(nz);
+    PBKV_CUDA(cudaMemcpyAsync(nb_d.p, nb.data(), nz * sizeof(unsigned int), cudaMemcpyHostToDevice, c.stream));
+    pool_repack_kernel<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.acc_rng.p, nb_d.p, c.n, c.acc_slot.p,
+                                                                c.acc_bits.p, slot_new.p, bits_new.p, rng_new.p);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    std::swap(c.acc_slot.p, slot_new.p);
+    std::swap(c.acc_slot.cap, slot_new.cap);
+    std::swap(c.acc_bits.p, bits_new.p);
+    std::swap(c.acc_bits.cap, bits_new.cap);
+    std::swap(c.acc_rng.p, rng_new.p);
+    std::swap(c.acc_rng.cap, rng_new.cap);
+    for (std::size_t i = 0; i < nz; ++i) {
+        c.h_acc_beg[i] = nb[i];
+        c.h_acc_cap[i] = static_cast<unsigned int>(c.h_entries[i]);
+    }
+    c.pool_top = top;
+}
+
+void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, const std::int64_t* acc_wf,
+                  const std::uint64_t* acc_bits, const pbkv_tree_totals* totals) {
+    need(c.n >= 1, "no tree mirrored");
+    need(n_rec == 0 || d, "null delta records");
+    // the last record of a node wins
+    std::unordered_map<int, std::int64_t> last_of;
+    last_of.reserve(static_cast<std::size_t>(n_rec) * 2);
+    int max_id = -1;
+    for (std::int64_t i = 0; i < n_rec; ++i) {
+        const pbkv_node_delta& r = d[i];
+        need(r.id >= 0 && r.id < INT_MAX - 1, "delta: node id out of range");
+        if (r.tier > PBKV_TIER_ABSENT) invalid("tree delta: bad tier value");
+        if (r.acc_begin < 0 || r.acc_end < r.acc_begin) invalid("tree delta: bad access range");
+        need(r.acc_end == r.acc_begin || (acc_wf && acc_bits), "delta: null access arrays");
+        for (std::int64_t e = r.acc_begin + 1; e < r.acc_end; ++e)
+            if (acc_wf[e] <= acc_wf[e - 1]) invalid("tree delta: access entries must ascend by workflow id");
+        if (r.depth < 0 || r.depth >= (1 << 24)) invalid("tree delta: bad depth");
+        last_of[r.id] = i;
+        max_id = std::max(max_id, r.id);
+    }
+    const std::int64_t n_old = c.n;
+    const std::int64_t n_new = std::max<std::int64_t>(n_old, static_cast<std::int64_t>(max_id) + 1);
+    for (std::int64_t id = n_old; id < n_new; ++id)
+        need(last_of.count(static_cast<int>(id)) != 0, "delta: appended node ids must be dense");
+    for (const auto& [id, i] : last_of) {
+        const pbkv_node_delta& r = d[i];
+        if (id == 0) {
+            need(r.parent == -1, "delta: the root has no parent");
+        } else if (r.parent < 0 || r.parent >= n_new) {
+            invalid("tree delta: parent out of range");
+        }
+    }
+    if (!c.spine.empty()) {  // sharded shards keep their global-id map: no structural updates
+        need(n_new == n_old, "delta: sharded contexts cannot append nodes");
+        for (const auto& [id, i] : last_of)
+            need(d[i].parent == c.h_parent[static_cast<std::size_t>(id)], "delta: sharded contexts cannot move nodes");
+    }
+    // order records by id (appended nodes last, ascending)
+    std::vector<std::int64_t> order;
+    order.reserve(last_of.size());
+    for (const auto& [id, i] : last_of) order.push_back(i);
+    std::sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) { return d[a].id < d[b].id; });
+
+    // grow the mirror (keeping contents) and the host copies
+    cudaStream_t st = c.stream;
+    if (n_new > n_old) {
+        const std::size_t nn = static_cast<std::size_t>(n_new), no = static_cast<std::size_t>(n_old);
+        c.parent.grow_keep(nn, no, st);
+        c.len.grow_keep(nn, no, st);
+        c.ever.grow_keep(nn, no, st);
+        c.depth.grow_keep(nn, no, st);
+        c.flags.grow_keep(nn, no, st);
+        c.last.grow_keep(nn, no, st);
+        c.score.grow_keep(nn, no, st);
+        c.acc_rng.grow_keep(nn, no, st);
+        c.lslot.grow_keep(nn, no, st);
+        c.lbits.grow_keep(nn, no, st);
+        c.h_entries.resize(nn, 0);
+        c.h_acc_beg.resize(nn, 0);
+        c.h_acc_cap.resize(nn, 0);
+        c.h_parent.resize(nn, -1);
+        c.h_depth.resize(nn, 0);
+        c.h_flags.resize(nn, 0);
+        c.h_last.resize(nn, 0);
+    }
+    // placement of every record's entries; class / structure bookkeeping
+    std::int64_t n_ent = 0;
+    for (std::int64_t i : order) n_ent += d[i].acc_end - d[i].acc_begin;
+    std::vector<DeltaRec> recs(order.size());
+    std::vector<unsigned int> edst(static_cast<std::size_t>(n_ent));
+    std::vector<int> eslot(static_cast<std::size_t>(n_ent));
+    std::vector<unsigned long long> ebits(static_cast<std::size_t>(n_ent));
+    bool classes = false, children = false;
+    std::int64_t E = c.E, q = 0;
+    std::unordered_map<int, char> heavy_set;
+    for (int h : c.h_heavy) heavy_set[h] = 1;
+    for (std::size_t k = 0; k < order.size(); ++k) {
+        const pbkv_node_delta& r = d[order[k]];
+        const std::size_t id = static_cast<std::size_t>(r.id);
+        const bool fresh = r.id >= n_old;
+        const std::int64_t ne = r.acc_end - r.acc_begin;
+        need(ne < INT_MAX, "delta: too many entries on one node");
+        const int ne_old = fresh ? 0 : c.h_entries[id];
+        const NodeClass k_old = class_of(c, ne_old), k_new = class_of(c, ne);
+        unsigned int beg = c.h_acc_beg[id];
+        if (fresh || ne > static_cast<std::int64_t>(c.h_acc_cap[id])) {  // (re)allocate at the pool top
+            const std::int64_t cap = fresh ? std::max<std::int64_t>(ne, 1) : std::max<std::int64_t>(2 * ne, 4);
+            need(c.pool_top + cap < static_cast<std::int64_t>(UINT_MAX / 2), "too many access entries");
+            beg = static_cast<unsigned int>(c.pool_top);
+            c.pool_top += cap;
+            c.h_acc_cap[id] = static_cast<unsigned int>(cap);
+        }
+        if (k_old != k_new || (k_new != kLight && (beg != c.h_acc_beg[id] || ne != ne_old))) classes = true;
+        if (k_new == kHeavy || k_old == kHeavy) classes = true;  // placement tables read its fields
+        const int p_old = fresh ? -2 : c.h_parent[id];
+        if (p_old != r.parent &&
+            ((p_old >= 0 && heavy_set.count(p_old)) || (r.parent >= 0 && heavy_set.count(r.parent))))
+            children = true;
+        E += ne - ne_old;
+        c.h_entries[id] = static_cast<int>(ne);
+        c.h_acc_beg[id] = beg;
+        c.h_parent[id] = r.parent;
+        c.h_depth[id] = r.depth;
+        c.h_flags[id] = static_cast<std::uint8_t>(r.tier | (r.retired ? kFlagRetired : 0));
+        c.h_last[id] = r.last_access;
+        c.max_depth = std::max(c.max_depth, static_cast<int>(r.depth));
+        DeltaRec& o = recs[k];
+        o.id = r.id;
+        o.parent = r.parent;
+        o.len = r.len;
+        o.ever = r.ever_tagged;
+        o.depth = r.depth;
+        o.beg = beg;
+        o.cnt = static_cast<unsigned int>(ne);
+        o.flags = c.h_flags[id];
+        o.last = r.last_access;
+        o.score = r.score;
+        o.ls0 = o.ls1 = ne > 2 ? -2 : -1;
+        o.lb0 = o.lb1 = 0ull;
+        for (std::int64_t e = 0; e < ne; ++e, ++q) {
+            const int sl = slot_for(c, acc_wf[r.acc_begin + e]);
+            const unsigned long long b = acc_bits[r.acc_begin + e];
+            edst[static_cast<std::size_t>(q)] = beg + static_cast<unsigned int>(e);
+            eslot[static_cast<std::size_t>(q)] = sl;
+            ebits[static_cast<std::size_t>(q)] = b;
+            if (ne <= 2 && e == 0) {
+                o.ls0 = sl;
+                o.lb0 = b;
+            }
+            if (ne == 2 && e == 1) {
+                o.ls1 = sl;
+                o.lb1 = b;
+            }
+        }
+    }
+    c.n = n_new;
+    c.E = E;
+    if (c.pool_top > static_cast<std::int64_t>(c.acc_slot.cap)) {
+        const std::size_t keep = c.acc_slot.cap;
+        c.acc_slot.grow_keep(static_cast<std::size_t>(c.pool_top), keep, st);
+        c.acc_bits.grow_keep(static_cast<std::size_t>(c.pool_top), keep, st);
+    }
+    // one pinned blob, one copy, one kernel
+    auto align16 = [](std::size_t x) { return (x + 15) & ~std::size_t(15); };
+    const std::size_t b_rec = align16(recs.size() * sizeof(DeltaRec));
+    const std::size_t b_dst = align16(edst.size() * sizeof(unsigned int));
+    const std::size_t b_slot = align16(eslot.size() * sizeof(int));
+    const std::size_t b_bits = ebits.size() * sizeof(unsigned long long);
+    const std::size_t blob = b_rec + b_dst + b_slot + b_bits;
+    if (c.delta_pending) {  // the previous batch's copy still reads the pinned staging
+        PBKV_CUDA(cudaEventSynchronize(c.ev_delta));
+        c.delta_pending = false;
+    }
+    if (!recs.empty()) {
+        c.hdelta.reserve(blob);
+        c.ddelta.reserve(blob);
+        unsigned char* h = c.hdelta.p;
+        std::memcpy(h, recs.data(), recs.size() * sizeof(DeltaRec));
+        if (!edst.empty()) {
+            std::memcpy(h + b_rec, edst.data(), edst.size() * sizeof(unsigned int));
+            std::memcpy(h + b_rec + b_dst, eslot.data(), eslot.size() * sizeof(int));
+            std::memcpy(h + b_rec + b_dst + b_slot, ebits.data(), b_bits);
+        }
+        PBKV_CUDA(cudaMemcpyAsync(c.ddelta.p, h, blob, cudaMemcpyHostToDevice, st));
+        PBKV_CUDA(cudaEventRecord(c.ev_delta, st));
+        c.delta_pending = true;
+        const unsigned char* dp = c.ddelta.p;
+        const long long nr = static_cast<long long>(recs.size());
+        mirror_delta_kernel<<<grid_for(std::max<long long>(nr, n_ent), 256), 256, 0, st>>>(
+            reinterpret_cast<const DeltaRec*>(dp), nr, reinterpret_cast<const unsigned int*>(dp + b_rec),
+            reinterpret_cast<const int*>(dp + b_rec + b_dst),
+            reinterpret_cast<const unsigned long long*>(dp + b_rec + b_dst + b_slot), n_ent, mirror_ptrs(c));
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
+    }
+    if (totals) set_totals(c, *totals);
+    if (n_new > n_old) ensure_scratch(c);
+    if (classes || children) rebuild_classes(c, children);
+    if (!c.spine.empty()) shard_apply_flags(c);
+    // dead space above half of the pool: repack (rare; amortised O(1) per entry)
+    if (c.pool_top > 2 * c.E + (1 << 16)) repack_pool(c);
+}
+
+// device mirror vs a full snapshot, field by field (pbkv_mirror_verify)
+std::int64_t mirror_verify(Context& c, const pbkv_tree_soa& s) {
+    need(s.parent && s.len && s.tier && s.retired && s.last_access && s.ever_tagged && s.acc_off,
+         "tree soa: missing required array");
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    const std::int64_t n = std::min<std::int64_t>(c.n, s.n_nodes);
+    const std::size_t nz = static_cast<std::size_t>(c.n);
+    std::vector<int> parent(nz), len(nz), ever(nz), depth(nz);
+    std::vector<std::uint8_t> flags(nz);
+    std::vector<unsigned long long> last(nz);
+    std::vector<double> score(nz);
+    std::vector<uint2> rng(nz);
+    std::vector<int2> lslot(nz);
+    std::vector<ulonglong2> lbits(nz);
+    std::vector<int> slot(static_cast<std::size_t>(c.pool_top) + 1);
+    std::vector<unsigned long long> bits(static_cast<std::size_t>(c.pool_top) + 1);
+    auto get = [&](void* dst, const void* src, std::size_t bytes) {
+        if (bytes) PBKV_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    };
+    get(parent.data(), c.parent.p, nz * sizeof(int));
+    get(len.data(), c.len.p, nz * sizeof(int));
+    get(ever.data(), c.ever.p, nz * sizeof(int));
+    get(depth.data(), c.depth.p, nz * sizeof(int));
+    get(flags.data(), c.flags.p, nz);
+    get(last.data(), c.last.p, nz * sizeof(unsigned long long));
+    get(score.data(), c.score.p, nz * sizeof(double));
+    get(rng.data(), c.acc_rng.p, nz * sizeof(uint2));
+    get(lslot.data(), c.lslot.p, nz * sizeof(int2));
+    get(lbits.data(), c.lbits.p, nz * sizeof(ulonglong2));
+    get(slot.data(), c.acc_slot.p, static_cast<std::size_t>(c.pool_top) * sizeof(int));
+    get(bits.data(), c.acc_bits.p, static_cast<std::size_t>(c.pool_top) * sizeof(unsigned long long));
+    for (std::int64_t i = 0; i < n; ++i) {
+        const std::size_t iz = static_cast<std::size_t>(i);
+        const std::uint8_t f = static_cast<std::uint8_t>(s.tier[i] | (s.retired[i] ? kFlagRetired : 0));
+        bool ok = parent[iz] == s.parent[i] && len[iz] == s.len[i] && ever[iz] == s.ever_tagged[i] &&
+                  (flags[iz] & (kFlagTierMask | kFlagRetired)) == f && last[iz] == s.last_access[i] &&
+                  (!s.depth || depth[iz] == s.depth[i]) && c.h_depth[iz] == depth[iz] &&
+                  (!s.score || std::memcmp(&score[iz], &s.score[i], sizeof(double)) == 0);
+        const std::int64_t a = s.acc_off[i], b = s.acc_off[i + 1];
+        ok = ok && static_cast<std::int64_t>(rng[iz].y) - rng[iz].x == b - a && c.h_entries[iz] == b - a &&
+             rng[iz].x == c.h_acc_beg[iz] && rng[iz].y <= static_cast<unsigned int>(c.pool_top);
+        for (std::int64_t e = 0; ok && e < b - a; ++e) {
+            const std::size_t pe = rng[iz].x + static_cast<std::size_t>(e);
+            const int sl = slot[pe];
+            ok = sl >= 0 && sl < c.n_slots && c.h_slot_wf[static_cast<std::size_t>(sl)] == s.acc_wf[a + e] &&
+                 bits[pe] == s.acc_bits[a + e];
+        }
+        if (ok) {  // the light pass's node-indexed copies
+            const std::int64_t ne = b - a;
+            if (ne > 2) {
+                ok = lslot[iz].x == -2 && lslot[iz].y == -2;
+            } else {
+                ok = lslot[iz].x == (ne >= 1 ? slot[rng[iz].x] : -1) && lslot[iz].y == (ne == 2 ? slot[rng[iz].x + 1] : -1) &&
+                     lbits[iz].x == (ne >= 1 ? s.acc_bits[a] : 0ull) && lbits[iz].y == (ne == 2 ? s.acc_bits[a + 1] : 0ull);
+            }
+        }
+        if (!ok) return i;
+    }
+    if (c.n != s.n_nodes || c.device_used != s.device_used || c.retired_device_tokens != s.retired_device_tokens ||
+        c.device_capacity != s.device_capacity || c.host_used != s.host_used || c.host_capacity != s.host_capacity)
+        return n;
+    return -1;
+}
 
 // ---- stage 3 ------------------------------------------------------------------
 // Keys (from the recomputed or the cached score), lock marks, subtree max,
@@ -760,6 +1061,7 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         for (auto& e : c->kev) PBKV_CUDA(cudaEventCreate(&e));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming));
         c->selstate.reserve(sel_state_bytes());
         c->hselstate.reserve(2 * sel_state_bytes());  // [0] readback, [1] initial-state template
         c->counters.reserve(16);
@@ -787,6 +1089,7 @@ int pbkv_ctx_destroy(pbkv_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_delta) cudaEventDestroy(c->ev_delta);
     cudaStream_t s = c->stream, side = c->side;
     delete c;  // DevBuf / PinBuf destructors free the device and pinned memory
     cudaStreamDestroy(s);
@@ -869,20 +1172,23 @@ int pbkv_mirror_full(pbkv_ctx* c, const pbkv_tree_soa* soa) {
     });
 }
 
-int pbkv_mirror_tree(pbkv_ctx* c, pbkv_tree* t) {
+int pbkv_mirror_delta(pbkv_ctx* c, const pbkv_node_delta* nodes, int64_t n, const int64_t* acc_wf,
+                      const uint64_t* acc_bits, const pbkv_tree_totals* totals) {
     return api(c, [&] {
-        need(c && t, "null argument");
+        need(c != nullptr, "null ctx");
+        need(n >= 0, "negative record count");
         set_device(*c);
-        SoaStore st;
-        st.fill(t->tree);
-        mirror_full(*c, st.soa);
-        t->tree.clear_dirty();
+        mirror_delta(*c, nodes, n, acc_wf, acc_bits, totals);
     });
 }
 
-int pbkv_mirror_sync(pbkv_ctx* c, pbkv_tree* t) {
-    // incremental delta upload is a later step; a full re-mirror is exact
-    return pbkv_mirror_tree(c, t);
+int pbkv_mirror_verify(pbkv_ctx* c, const pbkv_tree_soa* soa, int64_t* mismatch) {
+    return api(c, [&] {
+        need(c && soa && mismatch, "null argument");
+        need(c->n >= 1, "no tree mirrored");
+        set_device(*c);
+        *mismatch = mirror_verify(*c, *soa);
+    });
 }
 
 int pbkv_mirror_set_scores(pbkv_ctx* c, const int32_t* ids, const double* scores, int64_t n) {
@@ -1419,74 +1725,14 @@ int pbkv_predict(pbkv_ctx* c, const int64_t* wf, int64_t n, const int64_t* prefi
     });
 }
 
-// ---- host tree ------------------------------------------------------------------
-int pbkv_tree_create(pbkv_tree** out, int64_t device_capacity, int64_t host_capacity) {
-    return api(nullptr, [&] {
-        need(out != nullptr, "null out");
-        *out = new pbkv_tree(device_capacity, host_capacity);
-    });
-}
+// ---- internal (host_tree.cpp): the tracked-tree tag of pbkv_mirror_sync ---------
+void pbkv_internal_set_error(const char* msg) { g_last_error = msg ? msg : ""; }
 
-int pbkv_tree_destroy(pbkv_tree* t) {
-    delete t;
+int pbkv_internal_mirror_tag(pbkv_ctx* c, uint64_t** uid, int64_t** pos) {
+    if (!c) return PBKV_EARG;
+    *uid = &c->mirror_uid;
+    *pos = &c->mirror_pos;
     return PBKV_OK;
-}
-
-int pbkv_tree_apply_ops(pbkv_tree* t, const int64_t* words, int64_t n_words) {
-    return tree_api(t, [&] {
-        need(n_words == 0 || words, "null words");
-        apply_ops(t->tree, words, n_words);
-    });
-}
-
-int pbkv_tree_synth(pbkv_tree* t, const pbkv_synth_params* p) {
-    return tree_api(t, [&] {
-        need(p != nullptr, "null params");
-        SynthParams sp;
-        sp.n_nodes = p->n_nodes;
-        sp.n_workflows = p->n_workflows;
-        sp.agents = p->agents;
-        sp.group_size = p->group_size;
-        sp.shared_len = p->shared_len;
-        sp.group_len = p->group_len;
-        sp.alphabet = p->alphabet;
-        sp.max_rand_len = p->max_rand_len;
-        sp.retired_frac = p->retired_frac;
-        sp.host_every = p->host_every;
-        sp.seed = p->seed;
-        synth_build(t->tree, sp);
-    });
-}
-
-int pbkv_tree_shape(pbkv_tree* t, pbkv_tree_soa* s) {
-    return tree_api(t, [&] {
-        need(s != nullptr, "null soa");
-        s->n_nodes = static_cast<std::int64_t>(t->tree.node_count());
-        s->n_entries = static_cast<std::int64_t>(t->tree.entry_count());
-        s->device_capacity = t->tree.device_capacity();
-        s->device_used = t->tree.device_used();
-        s->retired_device_tokens = t->tree.retired_device_tokens();
-        s->host_capacity = t->tree.host_capacity();
-        s->host_used = t->tree.host_used();
-    });
-}
-
-int pbkv_tree_export(pbkv_tree* t, pbkv_tree_soa* s) {
-    return tree_api(t, [&] {
-        need(s != nullptr, "null soa");
-        t->tree.export_soa(s->parent, s->len, s->tier, s->retired, s->last_access, s->ever_tagged, s->score,
-                           s->device_children, s->depth, s->acc_off, s->acc_wf, s->acc_bits);
-    });
-}
-
-int pbkv_tree_touched(pbkv_tree* t, int64_t wf, int32_t* ids, int64_t cap, int64_t* n) {
-    return tree_api(t, [&] {
-        need(n != nullptr, "null out");
-        const std::vector<int>* v = t->tree.touched_nodes(wf);
-        *n = v ? static_cast<int64_t>(v->size()) : 0;
-        if (v && ids)
-            for (std::size_t i = 0; i < v->size() && static_cast<int64_t>(i) < cap; ++i) ids[i] = (*v)[i];
-    });
 }
 
 }  // extern "C"

@@ -88,13 +88,14 @@ __device__ __forceinline__ long long warp_append(unsigned long long* counter, bo
 
 // KVFlow steps-to-execution (policies.hpp:121-139): +inf when no tagged agent
 // recurs; sets *missing when a tagged workflow has no remaining sequence.
-__device__ __forceinline__ double kvflow_distance(const unsigned int* __restrict__ off,
+__device__ __forceinline__ double kvflow_distance(const uint2* __restrict__ rng,
                                                   const int* __restrict__ slot,
                                                   const unsigned long long* __restrict__ bits,
                                                   const int* __restrict__ rem_off, const int* __restrict__ rem_seq,
                                                   const std::uint8_t* __restrict__ rem_has, int n, bool* missing) {
     double best = CUDART_INF;
-    for (unsigned int e = off[n]; e < off[n + 1]; ++e) {
+    const uint2 rg = rng[n];
+    for (unsigned int e = rg.x; e < rg.y; ++e) {
         int s = slot[e];
         if (!rem_has[s]) {
             *missing = true;
@@ -117,7 +118,7 @@ __device__ __forceinline__ double kvflow_distance(const unsigned int* __restrict
 
 // ---- kernel argument packs -------------------------------------------------------
 struct ScoreArgs {
-    const unsigned int* acc_off;
+    const uint2* acc_rng;  // [n] {begin, end} of the node's entries in the pool
     const int* acc_slot;
     const unsigned long long* acc_bits;
     const double* P;
@@ -140,7 +141,7 @@ struct KeyArgs {
     const unsigned long long* last;
     const int* ever;
     const double* score_cached;
-    const unsigned int* acc_off;
+    const uint2* acc_rng;
     const int* acc_slot;
     const unsigned long long* acc_bits;
     const int* rem_off;
@@ -183,7 +184,7 @@ __device__ __forceinline__ void write_key_v(const KeyArgs& a, int n, double scor
         default: {  // KVFLOW
             bool miss = false;
             double d = retired ? CUDART_INF
-                               : kvflow_distance(a.acc_off, a.acc_slot, a.acc_bits, a.rem_off, a.rem_seq, a.rem_has,
+                               : kvflow_distance(a.acc_rng, a.acc_slot, a.acc_bits, a.rem_off, a.rem_seq, a.rem_has,
                                                  n, &miss);
             if (miss) a.missing[n] = 2;
             k = isinf(d) ? make_key(0, 0.0, last) : make_key(1, -d, last);

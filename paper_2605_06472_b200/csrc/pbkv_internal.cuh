@@ -3,7 +3,7 @@
 // Device data layout.  Per node (SoA, index = node id):
 //   parent i32, len i32, flags u8 (bits 0-1 tier, bit 2 retired),
 //   last_access u64, ever_tagged i32, score f64 (cached, cache.hpp:61),
-//   depth i32, acc_off u32 (CSR, n+1)
+//   depth i32, acc_rng u32x2 ({begin, end} of the node's entries in the pool)
 // Per access entry (CSR, WorkflowId-ascending within a node, cache.hpp:64):
 //   slot i32 (forecast slot of the WorkflowId), bits u64
 // Per forecast slot: P f64[V1][K] (agent-major: one agent's K steps contiguous),
@@ -184,12 +184,33 @@ struct Context {
     DevBuf<std::uint8_t> flags;
     DevBuf<unsigned long long> last;
     DevBuf<double> score;  // cached (mirrored) score
-    DevBuf<unsigned int> acc_off;
+    // access entries live in a pool: node i owns [acc_rng[i].x, acc_rng[i].y),
+    // WorkflowId-ascending, inside a segment of capacity h_acc_cap[i] that
+    // starts at acc_rng[i].x.  An incremental update (pbkv_mirror_delta)
+    // rewrites a node's segment in place, or moves it to the pool top when it
+    // outgrows its capacity; the pool is repacked when dead space dominates.
+    DevBuf<uint2> acc_rng;
     DevBuf<int> acc_slot;
     DevBuf<unsigned long long> acc_bits;
     std::vector<int> h_entries;  // entries per node (host copy, for id-list classification)
+    std::vector<unsigned int> h_acc_beg, h_acc_cap;
+    std::int64_t pool_top = 0;   // first unused pool position
+    // host copies of the node fields the host-side planning reads (classes,
+    // deferral placement, sharding)
+    std::vector<int> h_depth;
+    std::vector<std::uint8_t> h_flags;
+    std::vector<unsigned long long> h_last;
+    // pinned staging + completion event of pbkv_mirror_delta's upload
+    PinBuf<unsigned char> hdelta;
+    DevBuf<unsigned char> ddelta;
+    cudaEvent_t ev_delta = nullptr;
+    bool delta_pending = false;
+    // mirror bookkeeping of pbkv_mirror_sync: which host tree this context
+    // mirrors (TrackedCacheTree uid) and the change-log position it has applied
+    std::uint64_t mirror_uid = 0;
+    std::int64_t mirror_pos = 0;
     // node-indexed copy of the (at most two) access entries of every light
-    // node, so the light pass reads them coalesced, without the acc_off hop:
+    // node, so the light pass reads them coalesced, without the acc_rng hop:
     // lslot = {slot0, slot1} (-1 none, -2 the node is not light), lbits = bits
     DevBuf<int2> lslot;
     DevBuf<ulonglong2> lbits;

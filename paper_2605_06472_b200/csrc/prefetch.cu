@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) prefetch_cand_kernel(ScoreArgs s, const i
         if (i < n_nodes && n != 0 && (flags[n] & kFlagTierMask) == PBKV_TIER_HOST &&
             (flags[parent[n]] & kFlagTierMask) == PBKV_TIER_DEVICE) {
             bool miss = false;
-            v = eq1(s, s.acc_off[n], s.acc_off[n + 1], &miss);
+            v = eq1(s, s.acc_rng[n].x, s.acc_rng[n].y, &miss);
             if (miss) {
                 // the reference raises on the first host node in (last_access,
                 // id) order (host_index_, cache.hpp:434): keep the minimum
@@ -82,7 +82,7 @@ __global__ void prefetch_err_id_kernel(ScoreArgs s, const int* parent, const std
         if ((flags[parent[n]] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
         if (last[n] != static_cast<unsigned long long>(st->aux)) continue;
         bool miss = false;
-        eq1(s, s.acc_off[n], s.acc_off[n + 1], &miss);
+        eq1(s, s.acc_rng[n].x, s.acc_rng[n].y, &miss);
         if (miss) atomicMin(&st->node, static_cast<long long>(n));
     }
 }

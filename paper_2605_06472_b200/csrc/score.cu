@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(kMediumWarps * 32) score_medium_kernel(ScoreAr
     if (w >= n_list) return;
     const int n = nodes[w];
     const int K = kValueOnly ? 1 : s.K;
-    const unsigned int e0 = s.acc_off[n], e1 = s.acc_off[n + 1];
+    const uint2 rg = s.acc_rng[n];
+    const unsigned int e0 = rg.x, e1 = rg.y;
     const int L = static_cast<int>(e1 - e0) * K;
     int miss = 0;
     for (int i = lane; i < L; i += 32) {
@@ -334,7 +335,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(ScoreArgs s, KeyAr
 
     const int node = nodes[blockIdx.x];
     const int K = kValueOnly ? 1 : s.K;
-    const unsigned int e0 = s.acc_off[node], e1 = s.acc_off[node + 1];
+    const uint2 rg = s.acc_rng[node];
+    const unsigned int e0 = rg.x, e1 = rg.y;
     const long long L = static_cast<long long>(e1 - e0) * K;
     const int tid = threadIdx.x;
     if (tid == 0) {
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(kChainT) heavy_chain_kernel(ScoreArgs s, KeyAr
     extern __shared__ __align__(16) unsigned char chain_raw[];
     ChainSmem& sm = *reinterpret_cast<ChainSmem*>(chain_raw);
     const int node = nodes[blockIdx.x];
-    const long long L = static_cast<long long>(s.acc_off[node + 1] - s.acc_off[node]) * s.K;
+    const long long L = static_cast<long long>(s.acc_rng[node].y - s.acc_rng[node].x) * s.K;
     const double total = chain_eval(xs_g + xs_start[blockIdx.x], L, sm);
     if (threadIdx.x == 0) {
         s.out[node] = total;
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(256) medium_chain_kernel(ScoreArgs s, KeyArgs 
     const int lane = threadIdx.x & 31;
     if (m >= n_medium) return;
     const int node = medium[m];
-    const int L = static_cast<int>(s.acc_off[node + 1] - s.acc_off[node]) * s.K;
+    const int L = static_cast<int>(s.acc_rng[node].y - s.acc_rng[node].x) * s.K;
     const double* x = xs_g + xs_start[n_heavy + m];
     double t = 0.0;
     for (int c0 = 0; c0 < L; c0 += 32) {
@@ -562,7 +564,8 @@ __global__ void __launch_bounds__(256) score_ids_kernel(ScoreArgs s, const int* 
     for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < n;
          j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
         const int id = ids[j];
-        const unsigned int e0 = s.acc_off[id], e1 = s.acc_off[id + 1];
+        const uint2 rg = s.acc_rng[id];
+        const unsigned int e0 = rg.x, e1 = rg.y;
         double v = 0.0;
         bool miss = false, shorth = false;
         for (unsigned int e = e0; e < e1; ++e) {
@@ -679,7 +682,7 @@ std::size_t chain_smem_bytes() {
 
 ScoreArgs make_score_args(Context& c, double* out) {
     ScoreArgs s;
-    s.acc_off = c.acc_off.p;
+    s.acc_rng = c.acc_rng.p;
     s.acc_slot = c.acc_slot.p;
     s.acc_bits = c.acc_bits.p;
     s.P = c.P.p;
@@ -704,7 +707,7 @@ KeyArgs make_key_args(Context& c, int policy) {
     k.last = c.last.p;
     k.ever = c.ever.p;
     k.score_cached = c.score.p;
-    k.acc_off = c.acc_off.p;
+    k.acc_rng = c.acc_rng.p;
     k.acc_slot = c.acc_slot.p;
     k.acc_bits = c.acc_bits.p;
     k.rem_off = c.rem_off.p;

@@ -96,7 +96,8 @@ __global__ void spine_products_kernel(ScoreArgs s, const int* spine, const long 
     const int j = blockIdx.y;
     if (j >= n_spine) return;
     const int node = spine[j];
-    const unsigned int e0 = s.acc_off[node], e1 = s.acc_off[node + 1];
+    const uint2 rg = s.acc_rng[node];
+    const unsigned int e0 = rg.x, e1 = rg.y;
     const long long L = static_cast<long long>(e1 - e0) * s.K;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < L;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {

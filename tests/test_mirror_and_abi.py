@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 30
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
-    assert _abi.lib().pbkv_abi_version() == 1
+    assert _abi.lib().pbkv_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_gpu():

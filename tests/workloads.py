@@ -113,3 +113,71 @@ def pinned_paths(soa, rng: np.random.Generator, frac: float = 0.01) -> list[int]
 
 def workflows_of(soa) -> list[int]:
     return sorted(set(soa.acc_wf[: soa.n_entries].tolist()))
+
+
+def churn_ops(rng: np.random.Generator, soa, live: list[int], next_wf: list[int], *, n_insert: int = 6,
+              n_match: int = 3, p_term: float = 0.3, n_demote: int = 4, n_promote: int = 2, n_drop: int = 1,
+              n_score: int = 3, alphabet: int = 3, max_len: int = 7, agents: int = 4) -> OpStream:
+    """One batch of tree mutations between two decisions, legal against the
+    current snapshot `soa` (every CacheTree mutator: inserts / matches that
+    split nodes, a termination, demotions of device leaves, promotions and
+    drops of host nodes, cached-score writes).  `live` / `next_wf` are
+    updated in place (terminated workflows leave, fresh ones join)."""
+    ops = OpStream()
+    n = soa.n_nodes
+    # demotions of current device leaves, promotions / drops of host nodes
+    # under device parents: legal against the snapshot, so they come first
+    tier, parent = soa.tier, soa.parent
+    dev = tier == 0
+    dc = np.zeros(n, dtype=np.int64)
+    m = dev.copy()
+    m[0] = False
+    np.add.at(dc, parent[1:][m[1:]], 1)
+    leaves = np.nonzero(m & (dc == 0))[0]
+    hosts = [i for i in range(1, n) if tier[i] == 1 and tier[parent[i]] == 0]
+    rng.shuffle(hosts)
+    promote = hosts[:n_promote]
+    keep = {int(parent[i]) for i in promote}  # parents of promoted nodes stay on the device
+    leaves = np.array([i for i in leaves.tolist() if i not in keep], dtype=np.int64)
+    if leaves.size:
+        for i in rng.choice(leaves, size=min(n_demote, leaves.size), replace=False).tolist():
+            ops.demote(int(i))
+    for i in promote:
+        ops.promote(int(i))
+    for i in hosts[n_promote:n_promote + n_drop]:
+        ops.drop(int(i))
+    for _ in range(n_insert + n_match):
+        if not live:
+            live.append(next_wf[0])
+            next_wf[0] += 1
+        w = int(rng.choice(live))
+        toks = [int(t) for t in rng.integers(0, alphabet, size=int(rng.integers(1, max_len + 1)))]
+        agent = int(rng.integers(agents))
+        if rng.random() < n_insert / max(1, n_insert + n_match):
+            ops.insert(toks, w, agent, int(rng.integers(1, 6)) if rng.random() < 0.2 else -1)
+        else:
+            ops.match(toks, w, agent)
+    if live and rng.random() < p_term:
+        w = int(rng.choice(live))
+        live.remove(w)
+        ops.terminate(w)
+        live.append(next_wf[0])
+        next_wf[0] += 1
+    for i in rng.integers(1, max(n, 2), size=n_score if n > 1 else 0).tolist():
+        ops.set_score(int(i), float(rng.random()))
+    return ops
+
+
+def changed_nodes(prev, cur) -> set[int]:
+    """Ids whose mirrored fields (cache.hpp:54-69 read side, depth) or access
+    entries differ between two snapshots, plus every new id."""
+    out = set(range(prev.n_nodes, cur.n_nodes))
+    n = prev.n_nodes
+    for f in ("parent", "len", "tier", "retired", "last_access", "ever_tagged", "depth"):
+        a, b = getattr(prev, f)[:n], getattr(cur, f)[:n]
+        out.update(np.nonzero(a != b)[0].tolist())
+    out.update(np.nonzero(prev.score[:n].view(np.uint64) != cur.score[:n].view(np.uint64))[0].tolist())
+    for i in range(n):
+        if prev.entries_of(i) != cur.entries_of(i):
+            out.add(i)
+    return out
