@@ -82,6 +82,34 @@ def workload(cfg: str, rank: int):
     return t, soa, wf, P, locked, K, build_s
 
 
+def churn_batch(rng, t, live: list[int], victims: np.ndarray, n_wf: int, n_insert: int = 16, n_match: int = 8,
+                n_demote: int = 64):
+    """One serving-loop batch of tree mutations between two decisions, in the
+    synthetic generator's token namespaces (csrc/host/ops.hpp): the previous
+    decision's first victims demoted (in eviction order each is a device
+    leaf), then inserts and matches of live workflows along their own
+    shared + group + private paths, then one termination."""
+    from paper_2605_06472_b200.ops import OpStream
+
+    ops = OpStream()
+    for v in victims[:n_demote].tolist():
+        ops.demote(int(v))
+    for j in range(n_insert + n_match):
+        w = int(live[int(rng.integers(len(live)))])
+        toks = [(1 << 60) | i for i in range(32)] + [(2 << 60) | ((w // 16) << 20) | i for i in range(8)]
+        toks.append((3 << 60) | w)
+        toks += [int(x) for x in rng.integers(0, 4, size=int(rng.integers(1, 11)))]
+        agent = int(rng.integers(AGENTS))
+        if j < n_insert:
+            ops.insert(toks, w, agent)
+        else:
+            ops.match(toks, w, agent)
+    if len(live) > 1:
+        w = live.pop(int(rng.integers(len(live))))
+        ops.terminate(w)
+    return ops, None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -488,31 +516,57 @@ def main():
     select_phases = [round(x, 2) for x in pol.phase_times_us()]
     pol.set_timing(False)
 
-    # ---- e2e through the host C ABI -------------------------------------------------
-    P_pinned = torch.from_numpy(np.ascontiguousarray(P)).pin_memory().numpy()
+    # ---- e2e through the host C ABI, with the tree changing between decisions ----------
+    # Before every decision the host tree (the reference CacheTree, tracked)
+    # takes a serving-loop batch of mutations (churn_batch: inserts of live
+    # workflows, a termination, the previous decision's first victims
+    # demoted); the timed call then uploads only the changed nodes
+    # (pbkv_mirror_sync -> pbkv_mirror_delta), the forecasts from ordinary
+    # (pageable) host memory, and takes the decision with a host locked list
+    # and host victim output.
+    rng_e2e = np.random.default_rng(4242)
+    live = [int(w) for w in wf.tolist() if w >= int(0.3 * n_wf)]
+    pol.sync(t)  # the tracked tree's first sync is a full upload
     e2e_ms = []
-    n_victims_e2e = 0
     e2e_wall = []
-    for _ in range(args.warmup):  # the e2e path has its own first-call costs (pinned staging)
-        pol.put_forecasts(wf, P_pinned)
-        pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
-    torch.cuda.synchronize()
-    for _ in range(max(1, args.steps)):
+    delta_nodes = []
+    n_victims_e2e = 0
+    last_victims = np.zeros(0, dtype=np.int32)
+    for it in range(args.warmup + max(1, args.steps)):
+        ops, n_changed = churn_batch(rng_e2e, t, live, last_victims, n_wf)
+        t.apply_ops(ops.words)
+        ids = t.log(pos_prev)[1] if it else None
         flush.fill_(1)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         tw0 = time.perf_counter()
         e0.record(stream)
-        pol.put_forecasts(wf, P_pinned)
+        pol.sync(t)
         tw1 = time.perf_counter()
+        pol.put_forecasts(wf, P)
+        tw2 = time.perf_counter()
         sel = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
         e1.record(stream)
         e1.synchronize()
-        e2e_wall.append((tw1 - tw0, time.perf_counter() - tw1))
-        e2e_ms.append(e0.elapsed_time(e1))
+        tw3 = time.perf_counter()
+        pos_prev = t.log_end()
+        last_victims = sel.victim_ids
+        if it >= args.warmup:
+            e2e_wall.append((tw1 - tw0, tw2 - tw1, tw3 - tw2))
+            e2e_ms.append(max(e0.elapsed_time(e1), 1e3 * (tw3 - tw0)))
+            delta_nodes.append(len(ids) if ids is not None else 0)
         n_victims_e2e = len(sel)
-    assert n_victims_e2e == res[0], "e2e and device-resident decisions disagree"
+    # the last e2e decision, checked against a fresh device-resident decision
+    # on a full re-mirror of the same tree (victim ids in order)
+    pol_chk = Policy(num_agents=AGENTS, k=K, gamma=GAMMA, device=local)
+    pol_chk.mirror(t.export())
+    pol_chk.put_forecasts(wf, P)
+    chk = pol_chk.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+    assert np.array_equal(chk.victim_ids, sel.victim_ids) and chk.freed == sel.freed, \
+        "e2e decision (incremental mirror) differs from a full re-mirror"
+    mirror_ok = pol.verify(t) == -1
+    pol_chk.close()
 
     # ---- aggregate over ranks (max time) --------------------------------------------
     ms = ms_local
@@ -591,10 +645,19 @@ def main():
         "pipeline_c2": pipeline_c2(torch, dev) if not args.no_pipeline else None,
         "cpu_baseline": cpu,
         "e2e": {"value": total_nodes / (e2e * 1e-3), "unit": "nodes/s",
-                "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size + 4 * locked.size),
+                "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size + 4 * locked.size
+                                          + statistics.mean(delta_nodes) * (56 + 16 * E / N)),
                 "d2h_bytes_per_step": int(4 * n_victims_e2e + 24), "ms_per_step": e2e,
-                "host_wall_ms": {"put_forecasts": 1e3 * statistics.median(w[0] for w in e2e_wall),
-                                 "select": 1e3 * statistics.median(w[1] for w in e2e_wall)}},
+                "p99_ms": float(np.percentile(e2e_ms, 99)),
+                "what": "per decision: tree delta sync (pbkv_mirror_sync of the nodes changed by a churn batch: "
+                        "16 inserts + 8 matches of live workflows, 1 termination, the previous decision's first 64 "
+                        "victims demoted) + forecasts from pageable host memory + select with host locked list / "
+                        "host victims; max(device events, host wall)",
+                "delta_nodes_mean": statistics.mean(delta_nodes),
+                "mirror_verified": mirror_ok,
+                "host_wall_ms": {"sync": 1e3 * statistics.median(w[0] for w in e2e_wall),
+                                 "put_forecasts": 1e3 * statistics.median(w[1] for w in e2e_wall),
+                                 "select": 1e3 * statistics.median(w[2] for w in e2e_wall)}},
         "gpu_launches": int(k1 - k0),
         "lib_calls": int(l1 - l0),
         "clocks": clk.result,

@@ -156,6 +156,12 @@ class HostTree:
         _check(L.pbkv_tree_log(self._h, int(pos), C.byref(end), ptr(ids, C.c_int32), n.value, C.byref(n)), None)
         return end.value, ids[: n.value].tolist()
 
+    def log_end(self) -> int:
+        """Current change-log position."""
+        end, n = C.c_int64(), C.c_int64()
+        _check(_abi.lib().pbkv_tree_log(self._h, 1 << 62, C.byref(end), None, 0, C.byref(n)), None)
+        return end.value
+
     def touched(self, wf: int) -> list[int]:
         L = _abi.lib()
         n = C.c_int64()

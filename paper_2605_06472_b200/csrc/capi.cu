@@ -1062,6 +1062,7 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming));
+        PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_rows, cudaEventDisableTiming));
         c->selstate.reserve(sel_state_bytes());
         c->hselstate.reserve(2 * sel_state_bytes());  // [0] readback, [1] initial-state template
         c->counters.reserve(16);
@@ -1090,6 +1091,7 @@ int pbkv_ctx_destroy(pbkv_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_delta) cudaEventDestroy(c->ev_delta);
+    if (c->ev_rows) cudaEventDestroy(c->ev_rows);
     cudaStream_t s = c->stream, side = c->side;
     delete c;  // DevBuf / PinBuf destructors free the device and pinned memory
     cudaStreamDestroy(s);
@@ -1227,8 +1229,21 @@ int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, in
         c->fstage.reserve(static_cast<std::size_t>(n) * per);
         c->fstage_slot.reserve(static_cast<std::size_t>(n));
         reset_status(*c);
-        PBKV_CUDA(cudaMemcpyAsync(c->fstage.p, p, static_cast<std::size_t>(n) * per * sizeof(double),
-                                  cudaMemcpyHostToDevice, c->stream));
+        // pageable rows go through pinned staging, so the copy stays
+        // asynchronous; pinned (or registered) caller memory is copied directly
+        const std::size_t bytes = static_cast<std::size_t>(n) * per * sizeof(double);
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        const double* src = p;
+        if (!pinned) {
+            PBKV_CUDA(cudaEventSynchronize(c->ev_rows));  // the previous staged copy has drained
+            c->hrows.reserve(static_cast<std::size_t>(n) * per);
+            std::memcpy(c->hrows.p, p, bytes);
+            src = c->hrows.p;
+        }
+        PBKV_CUDA(cudaMemcpyAsync(c->fstage.p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+        if (!pinned) PBKV_CUDA(cudaEventRecord(c->ev_rows, c->stream));
         PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots, static_cast<std::size_t>(n) * sizeof(long long),
                                   cudaMemcpyHostToDevice, c->stream));
         launch_forecast_prepare(*c, c->fstage.p, c->fstage_slot.p, n, horizon);

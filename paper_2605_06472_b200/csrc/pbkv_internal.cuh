@@ -303,6 +303,8 @@ struct Context {
     long long epi_cap = 0;
     bool epi_vict_valid = false;  // the last epilogue stored the victims there
     PinBuf<long long> hslots;       // pinned staging of the forecast slots (pbkv_forecast_put)
+    PinBuf<double> hrows;           // pinned staging of pageable forecast rows (pbkv_forecast_put)
+    cudaEvent_t ev_rows = nullptr;  // the staged rows' copy has completed
     PinBuf<unsigned char> hpred_blob;  // pinned staging of pbkv_predict's slots / offsets / prefix
     DevBuf<unsigned char> pred_blob;
 
