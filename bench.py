@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-decisions", type=int, default=2)
     ap.add_argument("--no-pipeline", action="store_true", help="skip the config-2 predictor pipeline line")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the need sweep (0.1/1/10/50%%) and --no-defer line")
+    ap.add_argument("--no-prefetch", action="store_true", help="skip the stage-4 prefetch plan object")
     return ap.parse_args()
 
 
@@ -159,7 +161,8 @@ class ClockSampler:
                        "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: int = 0):
+def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: int = 0,
+                            plan_bandwidth: int | None = None):
     """The reference policy code (oracle/_ref) on the same workload: per
     decision, refresh every node's score (refresh_nodes, scoring.hpp:95) and
     select_victims_hierarchical (policies.hpp:108)."""
@@ -188,7 +191,17 @@ def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: 
         t.refresh_nodes(None, K, GAMMA)
         sel = t.select(POLICY_HE, needed, locked)
         times.append(time.perf_counter() - t0)
-    return {"n_nodes": soa.n_nodes, "times": times, "build_s": build_s, "n_victims": len(sel.victims)}
+    out = {"n_nodes": soa.n_nodes, "times": times, "build_s": build_s, "n_victims": len(sel.victims)}
+    if plan_bandwidth is not None:  # plan_conservative_prefetch (policies.hpp:220) on the same tree
+        pt = []
+        for _ in range(max(1, decisions)):
+            t0 = time.perf_counter()
+            pl = t.plan(plan_bandwidth)
+            pt.append(time.perf_counter() - t0)
+        out["plan_times"] = pt
+        out["plan_selected"] = list(pl.selected)
+        out["plan_candidates"] = [c[0] for c in pl.candidates]
+    return out
 
 
 def reference_threads() -> int:
@@ -516,6 +529,104 @@ def main():
     select_phases = [round(x, 2) for x in pol.phase_times_us()]
     pol.set_timing(False)
 
+    # ---- need sweep (0.1 / 1 / 10 / 50% of device tokens) -----------
+    # 50% reaches deep into the active-by-score region; lib_calls counts any
+    # library (CUB) fallback sort inside those decisions.  --no-defer: the same
+    # 1% decision with every heavy node's exact Eq. 2 chain computed inside
+    # the timed step (no interval placement).
+    sweep = {}
+    reps = max(3, min(10, args.steps))
+
+    def timed(fn, n):
+        out = []
+        for _ in range(n):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            fn()
+            a1.record(stream)
+            a1.synchronize()
+            out.append(a0.elapsed_time(a1))
+        return out
+
+    if not args.no_sweep:
+        for frac in (0.001, 0.01, 0.1, 0.5):
+            nd = max(1, int(frac * used))
+
+            def dec(nd=nd):
+                pol.select_dev(POLICY_HE, SCORE_RECOMPUTE, nd, locked_d.data_ptr(), locked.size,
+                               victims_d.data_ptr(), soa.n_nodes, result_d.data_ptr())
+
+            dec()
+            q0, ql0 = pol.launches()
+            f0 = pol.defer_stats()
+            ts = timed(dec, reps)
+            q1, ql1 = pol.launches()
+            f1 = pol.defer_stats()
+            rr = result_d.cpu().tolist()
+            sweep[f"{frac:.3%}"] = {"needed_tokens": nd, "n_victims": rr[0], "ms_mean": statistics.mean(ts),
+                                    "ms_p99": float(np.percentile(ts, 99)),
+                                    "nodes_per_s": soa.n_nodes / (statistics.mean(ts) * 1e-3),
+                                    "gpu_launches_per_step": (q1 - q0) / reps, "lib_calls": int(ql1 - ql0),
+                                    "defer_fast_exact": [f1[0] - f0[0], f1[1] - f0[1]]}
+        pol.set_defer(False)
+        step()
+        ts = timed(step, reps)
+        pol.set_defer(True)
+        sweep["1.000%_no_defer"] = {"needed_tokens": needed, "ms_mean": statistics.mean(ts),
+                                    "ms_p99": float(np.percentile(ts, 99)),
+                                    "what": "every heavy node's exact Eq. 2 chain inside the step"}
+
+    # ---- stage 4: conservative prefetch plan (policies.hpp:220) ----------------------
+    prefetch = None
+    if not args.no_prefetch:
+        host = (soa.tier == 1)
+        host[0] = False
+        par_dev = np.zeros_like(host)
+        par_dev[1:] = soa.tier[soa.parent[1:]] == 0
+        hc = host & par_dev
+        n_host_c = int(hc.sum())
+        e_host = int((soa.acc_off[1:] - soa.acc_off[:-1])[hc].sum())
+        bw = max(1, used // 50)
+        pol.plan_conservative_prefetch(bw)
+        pol.set_timing(True)
+        pk, pw = [], []
+        for _ in range(reps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            plan = pol.plan_conservative_prefetch(bw)
+            pw.append(1e3 * (time.perf_counter() - w0))
+            pk.append(pol.kernel_timings()[1])
+        pol.set_timing(False)
+        # algorithmic bytes of one plan (SURVEY.md §8(d) stage 4): the tier
+        # byte of every node; per host candidate node its parent id + parent
+        # tier, entry range and len; 12 B per entry; its forecast rows' step-0
+        # column; the sorted candidates written (id 4 + value 8)
+        alg_pf = soa.n_nodes + n_host_c * (4 + 1 + 8 + 4) + 12 * e_host + wf.size * (AGENTS + 1) * 8 \
+            + 12 * len(plan.candidates)
+        pk_ms = statistics.mean(pk)
+        prefetch = {
+            "what": f"plan_conservative_prefetch, bandwidth {bw} tokens (2% of device tokens), {args.config} tree "
+                    f"({n_host_c} host nodes under device parents)",
+            "n_candidates": len(plan.candidates), "n_selected": len(plan.selected),
+            "selected_tokens": plan.selected_tokens,
+            "kernel_ms": pk_ms, "kernel_p99_ms": float(np.percentile(pk, 99)),
+            "e2e": {"ms_mean": statistics.mean(pw), "ms_p99": float(np.percentile(pw, 99)),
+                    "what": "host wall of the public call: kernel + one synchronisation + the plan copied from "
+                            "pinned memory into the caller's arrays", "h2d_bytes": 48,
+                    "d2h_bytes": 12 * len(plan.candidates) + 4 * len(plan.selected) + 32},
+            "roofline": {"bound": "hbm", "kernel": "prefetch_plan_kernel", "achieved": alg_pf / (pk_ms * 1e-3) / 1e9,
+                         "peak": float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0))
+                         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0,
+                         "unit": "GB/s", "alg_bytes_per_launch": alg_pf},
+            "lib_calls": 0,
+        }
+        prefetch["roofline"]["frac"] = prefetch["roofline"]["achieved"] / prefetch["roofline"]["peak"]
+        prefetch["_plan"] = plan
+
     # ---- e2e through the host C ABI, with the tree changing between decisions ----------
     # Before every decision the host tree (the reference CacheTree, tracked)
     # takes a serving-loop batch of mutations (churn_batch: inserts of live
@@ -609,7 +720,16 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        r = cpu_reference_decisions(args.config, args.needed_frac, args.cpu_decisions)
+        r = cpu_reference_decisions(args.config, args.needed_frac, args.cpu_decisions,
+                                    plan_bandwidth=max(1, used // 50) if prefetch else None)
+        if r and prefetch and "plan_times" in r:
+            plan = prefetch["_plan"]
+            prefetch["cpu_baseline"] = {"value": 1e3 * statistics.mean(r["plan_times"]), "unit": "ms/plan",
+                                        "cores": 1, "kind": "reference",
+                                        "sample": f"{len(r['plan_times'])} plan_conservative_prefetch calls on the "
+                                                  f"same {args.config} tree"}
+            prefetch["parity_vs_reference"] = (r["plan_selected"] == list(plan.selected)
+                                               and r["plan_candidates"] == [c[0] for c in plan.candidates])
         if r:
             cpu = {"value": r["n_nodes"] / statistics.mean(r["times"]), "unit": "nodes/s", "cores": 1,
                    "kind": "reference",
@@ -642,6 +762,8 @@ def main():
                             "traffic": traffic.get("select_persistent_kernel"), "alg_bytes_per_launch": alg_sel,
                             "launch_ms": sel_ms},
         "defer": dict(zip(("fast", "exact"), pol.defer_stats())),
+        "need_sweep": sweep or None,
+        "prefetch": {k: v for k, v in prefetch.items() if not k.startswith("_")} if prefetch else None,
         "pipeline_c2": pipeline_c2(torch, dev) if not args.no_pipeline else None,
         "cpu_baseline": cpu,
         "e2e": {"value": total_nodes / (e2e * 1e-3), "unit": "nodes/s",

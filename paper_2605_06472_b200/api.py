@@ -77,6 +77,11 @@ class VictimSelection:
     def __len__(self) -> int:
         return int(self.victim_ids.size)
 
+    def __bool__(self) -> bool:
+        # A selection is a result, not a container: an empty one (shortfall,
+        # no victims) stays truthy, as the dataclass it replaces was.
+        return True
+
     def __eq__(self, other) -> bool:
         if not isinstance(other, VictimSelection):
             return NotImplemented

@@ -104,7 +104,8 @@ def build_oracle(verbose: bool = False) -> None:
     odir = os.path.join(ROOT, "oracle")
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/include/flowkv"):
-        targets += ["ref", "sim"]  # sim_gpu links the product library built above
+        targets += ["ref", "ref-tests", "sim"]  # sim_gpu links the product library built above;
+        # ref-tests: the reference's own Catch2 suite, run by tests/test_oracle.py
     subprocess.run(["make", "-s", "-C", odir, *targets], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
 

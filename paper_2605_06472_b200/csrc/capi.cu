@@ -218,8 +218,8 @@ void finish_timing(Context& c, int last_ev) {
     c.last_ms[4] = el(0, last_ev);
 }
 
-// children lists (CSR, in the order of `nodes`) of a few out-of-order nodes
-void upload_children(Context& c, const std::vector<int>& nodes, DevBuf<int>& off_d, DevBuf<int>& ch_d) {
+// children (ascending ids) of each of `nodes`: an O(n) scan of the host parents
+std::vector<std::vector<int>> scan_children(const Context& c, const std::vector<int>& nodes) {
     std::unordered_map<int, int> idx;
     for (std::size_t j = 0; j < nodes.size(); ++j) idx[nodes[j]] = static_cast<int>(j);
     std::vector<std::vector<int>> lists(nodes.size());
@@ -228,6 +228,13 @@ void upload_children(Context& c, const std::vector<int>& nodes, DevBuf<int>& off
             auto it = idx.find(c.h_parent[i]);
             if (it != idx.end()) lists[static_cast<std::size_t>(it->second)].push_back(static_cast<int>(i));
         }
+    return lists;
+}
+
+// children lists (CSR, in the order of `nodes`) of a few out-of-order nodes
+// (the spine of a shard; set once per mirror)
+void upload_children(Context& c, const std::vector<int>& nodes, DevBuf<int>& off_d, DevBuf<int>& ch_d) {
+    const std::vector<std::vector<int>> lists = scan_children(c, nodes);
     std::vector<int> off{0}, ch;
     for (auto& l : lists) {
         ch.insert(ch.end(), l.begin(), l.end());
@@ -235,6 +242,7 @@ void upload_children(Context& c, const std::vector<int>& nodes, DevBuf<int>& off
     }
     off_d.reserve(off.size());
     ch_d.reserve(ch.size() + 1);
+    // pageable sources: the copies have read them when the calls return
     PBKV_CUDA(cudaMemcpyAsync(off_d.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
     if (!ch.empty())
         PBKV_CUDA(cudaMemcpyAsync(ch_d.p, ch.data(), ch.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
@@ -249,20 +257,65 @@ NodeClass class_of(const Context& c, std::int64_t ne) {
     return ne > 2 ? kMedium : kLight;
 }
 
-// The class-derived tables, rebuilt from the host copies of the node fields:
-// the medium / heavy lists, the products list of their entries (heavy first,
-// then medium: combined index n_heavy + m, score.cu), the deferral placement
-// tables of the heavy nodes (place_deferred) and, when `children`, the
-// children lists of the heavy nodes (an O(n) scan over the parents).
-void rebuild_classes(Context& c, bool children) {
-    std::vector<int> medium, heavy, hent_node;
+void insert_sorted(std::vector<int>& v, int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it == v.end() || *it != x) v.insert(it, x);
+}
+void erase_sorted(std::vector<int>& v, int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it != v.end() && *it == x) v.erase(it);
+}
+
+// Host arrays bound for device buffers, copied through one pinned staging
+// buffer (c.hclass) with no host synchronisation: the next batch waits for
+// ev_class before it rewrites the staging.
+struct ClassStager {
+    Context& c;
+    struct Item {
+        void* dst;
+        const void* src;
+        std::size_t bytes;
+    };
+    std::vector<Item> items;
+    std::size_t total = 0;
+    explicit ClassStager(Context& cc) : c(cc) {}
+    template <class T>
+    void add(DevBuf<T>& d, const std::vector<T>& v) {
+        d.reserve(v.size() + 1);
+        if (v.empty()) return;
+        items.push_back(Item{d.p, v.data(), v.size() * sizeof(T)});
+        total += (v.size() * sizeof(T) + 15) & ~std::size_t(15);
+    }
+    void flush() {
+        if (c.class_pending) {
+            PBKV_CUDA(cudaEventSynchronize(c.ev_class));
+            c.class_pending = false;
+        }
+        if (items.empty()) return;
+        c.hclass.reserve(total);
+        std::size_t o = 0;
+        for (const Item& it : items) {
+            std::memcpy(c.hclass.p + o, it.src, it.bytes);
+            PBKV_CUDA(cudaMemcpyAsync(it.dst, c.hclass.p + o, it.bytes, cudaMemcpyHostToDevice, c.stream));
+            o += (it.bytes + 15) & ~std::size_t(15);
+        }
+        PBKV_CUDA(cudaEventRecord(c.ev_class, c.stream));
+        c.class_pending = true;
+    }
+};
+
+// The class-derived device tables, from the host class lists (h_medium,
+// h_heavy, h_heavy_ch) in O(medium + heavy entries): the medium / heavy
+// lists, the products list of their entries (heavy first, then medium:
+// combined index n_heavy + m, score.cu), the children lists of the heavy
+// nodes and the deferral placement tables (place_deferred).
+void refresh_heavy_tables(Context& c);
+void upload_classes(Context& c) {
+    const std::vector<int>& heavy = c.h_heavy;
+    const std::vector<int>& medium = c.h_medium;
+    std::vector<int> hent_node;
     std::vector<unsigned int> hent;
     std::vector<long long> hstart;
-    for (std::int64_t i = 0; i < c.n; ++i) {
-        const NodeClass k = class_of(c, c.h_entries[static_cast<std::size_t>(i)]);
-        if (k == kHeavy) heavy.push_back(static_cast<int>(i));
-        else if (k == kMedium) medium.push_back(static_cast<int>(i));
-    }
     auto add_entries = [&](int node, int idx) {
         hstart.push_back(static_cast<long long>(hent.size()) * c.K);
         const unsigned int b = c.h_acc_beg[static_cast<std::size_t>(node)];
@@ -274,34 +327,32 @@ void rebuild_classes(Context& c, bool children) {
     };
     for (std::size_t j = 0; j < heavy.size(); ++j) add_entries(heavy[j], static_cast<int>(j));
     for (std::size_t m = 0; m < medium.size(); ++m) add_entries(medium[m], static_cast<int>(heavy.size() + m));
-    cudaStream_t st = c.stream;
-    c.medium.reserve(medium.size() + 1);
-    c.heavy.reserve(heavy.size() + 1);
-    c.hent.reserve(hent.size() + 1);
-    c.hent_node.reserve(hent.size() + 1);
-    c.hstart.reserve(heavy.size() + medium.size() + 1);
+    std::vector<int> ch_off{0}, ch;
+    for (int h : heavy) {
+        const auto it = c.h_heavy_ch.find(h);
+        if (it != c.h_heavy_ch.end()) ch.insert(ch.end(), it->second.begin(), it->second.end());
+        ch_off.push_back(static_cast<int>(ch.size()));
+    }
+    ClassStager st(c);
+    st.add(c.medium, medium);
+    st.add(c.heavy, heavy);
+    st.add(c.hent, hent);
+    st.add(c.hent_node, hent_node);
+    st.add(c.hstart, hstart);
+    st.add(c.hch_off, ch_off);
+    st.add(c.hch, ch);
     c.hmiss.reserve(heavy.size() + medium.size() + 1);
     c.hxs.reserve(hent.size() * static_cast<std::size_t>(c.K) + 1);
-    // the host vectors die at return: the copies complete before it
-    if (!medium.empty())
-        PBKV_CUDA(cudaMemcpyAsync(c.medium.p, medium.data(), medium.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (!heavy.empty())
-        PBKV_CUDA(cudaMemcpyAsync(c.heavy.p, heavy.data(), heavy.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (!hent.empty()) {
-        PBKV_CUDA(cudaMemcpyAsync(c.hent.p, hent.data(), hent.size() * sizeof(unsigned int), cudaMemcpyHostToDevice,
-                                  st));
-        PBKV_CUDA(cudaMemcpyAsync(c.hent_node.p, hent_node.data(), hent_node.size() * sizeof(int),
-                                  cudaMemcpyHostToDevice, st));
-        PBKV_CUDA(cudaMemcpyAsync(c.hstart.p, hstart.data(), hstart.size() * sizeof(long long), cudaMemcpyHostToDevice,
-                                  st));
-    }
-    const bool heavy_changed = heavy != c.h_heavy;
+    st.flush();
     c.n_medium = static_cast<std::int64_t>(medium.size());
     c.n_heavy = static_cast<std::int64_t>(heavy.size());
     c.n_hent = static_cast<std::int64_t>(hent.size());
-    c.h_heavy = heavy;
-    if (children || heavy_changed) upload_children(c, heavy, c.hch_off, c.hch);
-    // deferral placement tables (place_deferred)
+    refresh_heavy_tables(c);
+}
+
+// deferral placement tables of the heavy nodes (place_deferred), O(heavy)
+void refresh_heavy_tables(Context& c) {
+    const std::vector<int>& heavy = c.h_heavy;
     const std::size_t nh = heavy.size();
     c.h_heavy_last.resize(nh);
     c.h_heavy_parent.resize(nh);
@@ -331,7 +382,22 @@ void rebuild_classes(Context& c, bool children) {
         c.h_heavy_kids.insert(c.h_heavy_kids.end(), kids[j].begin(), kids[j].end());
         c.h_heavy_kid_off.push_back(static_cast<int>(c.h_heavy_kids.size()));
     }
-    PBKV_CUDA(cudaStreamSynchronize(st));
+}
+
+// Every node classified (O(n), full mirrors only), the heavy nodes'
+// children by a scan, then the device tables.
+void classify_all(Context& c) {
+    c.h_medium.clear();
+    c.h_heavy.clear();
+    for (std::int64_t i = 0; i < c.n; ++i) {
+        const NodeClass k = class_of(c, c.h_entries[static_cast<std::size_t>(i)]);
+        if (k == kHeavy) c.h_heavy.push_back(static_cast<int>(i));
+        else if (k == kMedium) c.h_medium.push_back(static_cast<int>(i));
+    }
+    const std::vector<std::vector<int>> lists = scan_children(c, c.h_heavy);
+    c.h_heavy_ch.clear();
+    for (std::size_t j = 0; j < c.h_heavy.size(); ++j) c.h_heavy_ch[c.h_heavy[j]] = lists[j];
+    upload_classes(c);
 }
 
 void set_totals(Context& c, const pbkv_tree_totals& t) {
@@ -451,8 +517,7 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
         PBKV_CUDA(cudaMemcpyAsync(c.acc_slot.p, slot.data(), E * sizeof(int), cudaMemcpyHostToDevice, st));
         PBKV_CUDA(cudaMemcpyAsync(c.acc_bits.p, s.acc_bits, E * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
     }
-    c.h_heavy.clear();
-    rebuild_classes(c, true);
+    classify_all(c);
     c.max_depth = maxd;
     set_totals(c, pbkv_tree_totals{s.device_capacity, s.device_used, s.retired_device_tokens, s.host_capacity,
                                    s.host_used});
@@ -648,10 +713,17 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     std::vector<unsigned int> edst(static_cast<std::size_t>(n_ent));
     std::vector<int> eslot(static_cast<std::size_t>(n_ent));
     std::vector<unsigned long long> ebits(static_cast<std::size_t>(n_ent));
-    bool classes = false, children = false;
+    // class bookkeeping: `products` when the device class tables change (a
+    // class transition, a medium / heavy segment moved or resized, a heavy
+    // node's children), `tables` when only a heavy node's placement fields do
+    bool products = false, tables = false;
+    struct ClassMove {
+        int id;
+        NodeClass from, to;
+    };
+    std::vector<ClassMove> cls_moves;
+    std::vector<std::pair<int, int>> reparented;  // (node, old parent) (-2: fresh)
     std::int64_t E = c.E, q = 0;
-    std::unordered_map<int, char> heavy_set;
-    for (int h : c.h_heavy) heavy_set[h] = 1;
     for (std::size_t k = 0; k < order.size(); ++k) {
         const pbkv_node_delta& r = d[order[k]];
         const std::size_t id = static_cast<std::size_t>(r.id);
@@ -668,12 +740,11 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
             c.pool_top += cap;
             c.h_acc_cap[id] = static_cast<unsigned int>(cap);
         }
-        if (k_old != k_new || (k_new != kLight && (beg != c.h_acc_beg[id] || ne != ne_old))) classes = true;
-        if (k_new == kHeavy || k_old == kHeavy) classes = true;  // placement tables read its fields
+        if (k_old != k_new) cls_moves.push_back(ClassMove{r.id, k_old, k_new});
+        if (k_old != k_new || (k_new != kLight && (beg != c.h_acc_beg[id] || ne != ne_old))) products = true;
+        if (k_new == kHeavy || k_old == kHeavy) tables = true;  // placement tables read its fields
         const int p_old = fresh ? -2 : c.h_parent[id];
-        if (p_old != r.parent &&
-            ((p_old >= 0 && heavy_set.count(p_old)) || (r.parent >= 0 && heavy_set.count(r.parent))))
-            children = true;
+        if (p_old != r.parent) reparented.emplace_back(r.id, p_old);
         E += ne - ne_old;
         c.h_entries[id] = static_cast<int>(ne);
         c.h_acc_beg[id] = beg;
@@ -753,7 +824,46 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     }
     if (totals) set_totals(c, *totals);
     if (n_new > n_old) ensure_scratch(c);
-    if (classes || children) rebuild_classes(c, children);
+    // class lists and heavy children, updated by the changed nodes only
+    std::vector<int> newly_heavy;
+    for (const ClassMove& m : cls_moves) {
+        if (m.from == kMedium) erase_sorted(c.h_medium, m.id);
+        if (m.from == kHeavy) {
+            erase_sorted(c.h_heavy, m.id);
+            c.h_heavy_ch.erase(m.id);
+        }
+        if (m.to == kMedium) insert_sorted(c.h_medium, m.id);
+        if (m.to == kHeavy) {
+            insert_sorted(c.h_heavy, m.id);
+            newly_heavy.push_back(m.id);
+        }
+    }
+    if (!newly_heavy.empty()) {  // rare (a node crossing the heavy threshold): one O(n) scan
+        const std::vector<std::vector<int>> lists = scan_children(c, newly_heavy);
+        for (std::size_t j = 0; j < newly_heavy.size(); ++j) c.h_heavy_ch[newly_heavy[j]] = lists[j];
+    }
+    for (const auto& [id, p_old] : reparented) {
+        auto is_new = [&](int p) { return std::find(newly_heavy.begin(), newly_heavy.end(), p) != newly_heavy.end(); };
+        if (p_old >= 0 && !is_new(p_old)) {
+            const auto it = c.h_heavy_ch.find(p_old);
+            if (it != c.h_heavy_ch.end()) {
+                erase_sorted(it->second, id);
+                products = true;
+            }
+        }
+        const int p_new = c.h_parent[static_cast<std::size_t>(id)];
+        if (p_new >= 0 && !is_new(p_new)) {
+            const auto it = c.h_heavy_ch.find(p_new);
+            if (it != c.h_heavy_ch.end()) {
+                insert_sorted(it->second, id);
+                products = true;
+            }
+        }
+    }
+    if (products)
+        upload_classes(c);
+    else if (tables)
+        refresh_heavy_tables(c);
     if (!c.spine.empty()) shard_apply_flags(c);
     // dead space above half of the pool: repack (rare; amortised O(1) per entry)
     if (c.pool_top > 2 * c.E + (1 << 16)) repack_pool(c);
@@ -1062,6 +1172,7 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming));
+        PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_class, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_rows, cudaEventDisableTiming));
         c->selstate.reserve(sel_state_bytes());
         c->hselstate.reserve(2 * sel_state_bytes());  // [0] readback, [1] initial-state template
@@ -1091,6 +1202,7 @@ int pbkv_ctx_destroy(pbkv_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_delta) cudaEventDestroy(c->ev_delta);
+    if (c->ev_class) cudaEventDestroy(c->ev_class);
     if (c->ev_rows) cudaEventDestroy(c->ev_rows);
     cudaStream_t s = c->stream, side = c->side;
     delete c;  // DevBuf / PinBuf destructors free the device and pinned memory
@@ -1436,50 +1548,21 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
         plan->budget_bw = bandwidth * static_cast<std::int64_t>(step_duration);
         plan->displacement_budget = extra;
         const long long budget = std::min(plan->budget_space + extra, plan->budget_bw);
-        long long* ctr = c->counters.p;
-        long long* hctr = c->hcounters.p;
-        c->ck_in.reserve(c->n);
-        c->cv_in.reserve(c->n);
         record(*c, 0);
         reset_status(*c);
-        PBKV_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(long long), c->stream));
-        launch_prefetch_candidates(*c, reinterpret_cast<unsigned long long*>(ctr));
-        PBKV_CUDA(cudaMemcpyAsync(hctr, ctr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        PBKV_CUDA(cudaMemcpyAsync(c->hstatus.p, c->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
-        PBKV_CUDA(cudaStreamSynchronize(c->stream));
-        if (c->hstatus.p->code != 0) {
-            launch_prefetch_err_id(*c);
-            check_status(*c);
-        }
-        const std::int64_t nc = hctr[0];
-        plan->n_candidates = nc;
-        if (nc == 0) {
-            record(*c, 1);
-            finish_timing(*c, 1);
-            return;
-        }
-        c->ck_out.reserve(nc);
-        c->cv_out.reserve(nc);
-        c->sel.reserve(nc);
-        launch_prefetch_sort_greedy(*c, nc, budget, ctr);
-        PBKV_CUDA(cudaMemcpyAsync(hctr + 1, ctr + 1, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        PrefetchOut o;
+        run_prefetch_plan(*c, budget, &o);  // one synchronisation
         record(*c, 1);
         finish_timing(*c, 1);
-        plan->n_selected = hctr[1];
-        plan->selected_tokens = hctr[2];
-        if (cand_cap > 0 && (cand_ids || cand_values)) {
-            std::int64_t m = std::min<std::int64_t>(cand_cap, nc);
-            std::vector<CandKey> ck(static_cast<std::size_t>(m));
-            PBKV_CUDA(cudaMemcpy(ck.data(), c->ck_out.p, m * sizeof(CandKey), cudaMemcpyDeviceToHost));
-            if (cand_ids)
-                for (std::int64_t i = 0; i < m; ++i) cand_ids[i] = static_cast<int32_t>(ck[static_cast<std::size_t>(i)].id);
-            if (cand_values) PBKV_CUDA(cudaMemcpy(cand_values, c->cv_out.p, m * sizeof(double), cudaMemcpyDeviceToHost));
-        }
-        if (sel_cap > 0 && selected) {
-            std::int64_t m = std::min<std::int64_t>(sel_cap, plan->n_selected);
-            if (m > 0) PBKV_CUDA(cudaMemcpy(selected, c->sel.p, m * sizeof(int), cudaMemcpyDeviceToHost));
-        }
+        const std::int64_t nc = o.ctr[0];
+        plan->n_candidates = nc;
+        plan->n_selected = o.ctr[1];
+        plan->selected_tokens = o.ctr[2];
+        const std::int64_t mc = std::min<std::int64_t>(cand_cap, nc);
+        if (mc > 0 && cand_ids) std::memcpy(cand_ids, o.cand, static_cast<std::size_t>(mc) * sizeof(int32_t));
+        if (mc > 0 && cand_values) std::memcpy(cand_values, o.val, static_cast<std::size_t>(mc) * sizeof(double));
+        const std::int64_t ms = std::min<std::int64_t>(sel_cap, plan->n_selected);
+        if (ms > 0 && selected) std::memcpy(selected, o.sel, static_cast<std::size_t>(ms) * sizeof(int32_t));
     });
 }
 

@@ -154,10 +154,13 @@ struct HeadKey {
     unsigned int id;
 };
 
-// sort record of a prefetch candidate: value descending, id ascending
-struct CandKey {
-    unsigned long long vdesc;
-    unsigned int id;
+// a prefetch plan in pinned host memory (prefetch.cu run_prefetch_plan):
+// ctr = {n_candidates, n_selected, selected_tokens, error}
+struct PrefetchOut {
+    const long long* ctr;
+    const int* cand;
+    const double* val;
+    const int* sel;
 };
 
 struct SelectCounts {
@@ -205,6 +208,11 @@ struct Context {
     DevBuf<unsigned char> ddelta;
     cudaEvent_t ev_delta = nullptr;
     bool delta_pending = false;
+    // staging of the class tables (medium / heavy lists, products list,
+    // heavy children): reused once ev_class has passed
+    PinBuf<unsigned char> hclass;
+    cudaEvent_t ev_class = nullptr;
+    bool class_pending = false;
     // mirror bookkeeping of pbkv_mirror_sync: which host tree this context
     // mirrors (TrackedCacheTree uid) and the change-log position it has applied
     std::uint64_t mirror_uid = 0;
@@ -225,7 +233,11 @@ struct Context {
     DevBuf<double> hxs;           // products of the heavy entries
     DevBuf<unsigned int> hmiss;   // per heavy node: missing (1) / short horizon (2)
     std::int64_t n_hent = 0;
-    std::vector<int> h_heavy;                 // heavy node ids (host copy)
+    std::vector<int> h_heavy;                 // heavy node ids, ascending (host copy)
+    std::vector<int> h_medium;                // medium node ids, ascending (host copy)
+    // children of every heavy node, ascending ids: kept up to date by the
+    // delta path (a parent change updates the two lists it touches)
+    std::unordered_map<int, std::vector<int>> h_heavy_ch;
     std::vector<int> h_parent;                // parent of every node (host copy)
     // children of the out-of-order nodes (CSR in heavy / spine order): the
     // eff walk stops below them and their reports reduce over these lists
@@ -290,9 +302,12 @@ struct Context {
     DevBuf<int> locked;
     DevBuf<int> ids, ids2, ids3;
     DevBuf<double> vals;
-    DevBuf<CandKey> ck_in, ck_out;
-    DevBuf<double> cv_in, cv_out;
-    DevBuf<int> sel;
+    // stage 4 scratch (prefetch.cu)
+    DevBuf<unsigned long long> pf_hi, pf_bkey, pf_bhi, pf_shi;
+    DevBuf<unsigned int> pf_id, pf_bid, pf_hist, pf_big;
+    DevBuf<int> pf_sid;
+    DevBuf<unsigned char> pf_state;
+    PinBuf<unsigned char> hplan, hplan_init;
     DevBuf<unsigned char> cub_tmp;
     DevBuf<long long> counters;  // small device scalars
     DevBuf<DevStatus> status;
@@ -363,9 +378,7 @@ void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out, do
 SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked, std::int64_t needed,
                         bool he_recompute, long long* result_dev);
 std::size_t sel_state_bytes();
-void launch_prefetch_candidates(Context& c, unsigned long long* n_cand_dev);
-void launch_prefetch_err_id(Context& c);
-void launch_prefetch_sort_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev);
+void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out);
 void predictor_load(Context& c, const pbkv_predictor_cfg& cfg, const pbkv_predictor_weights& w);
 pbkv_predictor_cfg predictor_cfg(const Context& c);
 void predictor_run(Context& c, std::int64_t n, const int* pre_off_dev, const int* pre_dev, const void* x_dev,

@@ -1,12 +1,30 @@
-// Stage 4 on sm_100a: conservative / aggressive prefetch candidate ranking
-// (policies.hpp:181-235).  Candidates = host-tier nodes with a device parent
-// and single-step value (Eq. 1, scoring.hpp:41-45) > 0, ranked by (value
-// desc, id asc); the greedy-with-skip fill runs in one CTA.
-#include <cub/device/device_radix_sort.cuh>
-
-#include <cuda/std/tuple>
+// Stage 4 on sm_100a: conservative / aggressive prefetch planning
+// (policies.hpp:181-235) as ONE cooperative kernel with no library calls and
+// one host synchronisation per plan:
+//   1. candidates: host-tier nodes whose parent is on the device, with the
+//      single-step value v (Eq. 1, scoring.hpp:41-45, summed in entry order)
+//      > 0 (policies.hpp:190-197).  A missing forecast raises on the first
+//      host node in host_index_ order, i.e. least (last_access, id)
+//      (cache.hpp:97);
+//   2. (v desc, id asc) order (policies.hpp:199-202): the sort key
+//      (~enc(v), id) has its varying bits packed order-preservingly into 64
+//      bits; a 12-bit MSD histogram places every candidate into its digit's
+//      bucket, then every bucket is ranked in place -- one warp for <= 32
+//      elements, else rank counting from shared-memory tiles, (bucket, 64-
+//      element chunk) tasks spread over every CTA;
+//   3. greedy fill with skip (policies.hpp:203-210) by one warp: a warp-wide
+//      prefix sum of the next lanes' token lengths takes every lane that still
+//      fits at once; the first lane that does not is skipped; lanes longer
+//      than the remaining budget are skipped together (the budget only
+//      shrinks); the walk stops once the budget is below the shortest
+//      candidate;
+//   4. the plan (sorted candidates, values, selection, counters) is stored
+//      straight into pinned host memory by the kernel.
+#include <cooperative_groups.h>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pbkv {
 
@@ -16,15 +34,63 @@ ScoreArgs make_score_args(Context& c, double* out);
 
 namespace {
 
-unsigned int grid_cap(std::int64_t n, int block) {
-    std::int64_t want = (n + block - 1) / block;
-    const std::int64_t cap = 148LL * 16;
-    if (want > cap) want = cap;
-    return static_cast<unsigned int>(want < 1 ? 1 : want);
-}
+constexpr int kPT = 512;              // threads per CTA (two CTAs per SM)
+constexpr int kPBits = 12;            // MSD digit
+constexpr int kPBins = 1 << kPBits;
+constexpr int kPer = kPBins / kPT;    // bins per thread in the offset scan
+constexpr int kTile = 4096;           // rank-counting tile (keys in shared memory)
+constexpr int kChunk = kPT / 8;       // elements per rank task (8 threads each)
 
-// Eq. 1 chain of a node, in access order (the reference sums the terms in
-// WorkflowId order, scoring.hpp:43-44)
+struct PfState {
+    unsigned long long n_cand;
+    unsigned long long or_hi, and_hi;
+    unsigned int or_id, and_id;
+    int min_len;
+    unsigned int n_big;
+};
+
+struct PfArgs {
+    ScoreArgs s;
+    const int* parent;
+    const std::uint8_t* flags;
+    const unsigned long long* last;
+    const int* len;
+    long long n_nodes;
+    long long budget;
+    unsigned long long* c_hi;  // candidates in append order: ~enc(v), id
+    unsigned int* c_id;
+    unsigned long long* b_key;  // bucketed: sort key (packed, or ~enc(v)), ~enc(v), id
+    unsigned long long* b_hi;
+    unsigned int* b_id;
+    unsigned long long* s_hi;  // sorted
+    int* s_id;
+    unsigned int* hist;     // [kPBins]
+    unsigned int* cursor;   // [kPBins]
+    unsigned int* seg_off;  // [kPBins]
+    unsigned int* big;      // (offset, count) of the buckets ranked by tiles
+    PfState* ps;
+    DevStatus* st;
+    int* h_cand;  // pinned host outputs
+    double* h_val;
+    int* h_sel;
+    long long* h_ctr;  // n_candidates, n_selected, selected_tokens, error flag
+};
+
+struct PfSmem {
+    union {
+        unsigned int hist[kPBins];
+        struct {
+            unsigned long long k[kTile];
+            unsigned int id[kTile];
+        } tile;
+        typename cub::BlockScan<unsigned int, kPT>::TempStorage scan;
+    } u;
+    unsigned int off[kPBins];
+    unsigned long long red[32];
+    unsigned long long bc[4];
+};
+
+// Eq. 1 of a node, in access order (scoring.hpp:43-44): mass on step 0
 __device__ __forceinline__ double eq1(const ScoreArgs& s, unsigned int e0, unsigned int e1, bool* miss) {
     double v = 0.0;
     for (unsigned int e = e0; e < e1; ++e) {
@@ -39,134 +105,497 @@ __device__ __forceinline__ double eq1(const ScoreArgs& s, unsigned int e0, unsig
     return v;
 }
 
-__global__ void __launch_bounds__(256) prefetch_cand_kernel(ScoreArgs s, const int* parent, const std::uint8_t* flags,
-                                                            const unsigned long long* last, CandKey* ck, double* cv,
-                                                            unsigned long long* n_cand, DevStatus* st,
-                                                            std::int64_t n_nodes) {
-    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-    for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < n_nodes; base += stride) {
-        const std::int64_t i = base + threadIdx.x;
-        const int n = static_cast<int>(i);
-        bool take = false;
-        double v = 0.0;
-        if (i < n_nodes && n != 0 && (flags[n] & kFlagTierMask) == PBKV_TIER_HOST &&
-            (flags[parent[n]] & kFlagTierMask) == PBKV_TIER_DEVICE) {
-            bool miss = false;
-            v = eq1(s, s.acc_rng[n].x, s.acc_rng[n].y, &miss);
-            if (miss) {
-                // the reference raises on the first host node in (last_access,
-                // id) order (host_index_, cache.hpp:434): keep the minimum
-                atomicCAS(&st->code, 0, PBKV_EINVAL);
-                atomicCAS(&st->kind, 0, kErrMissingForecast);
-                atomicMin(reinterpret_cast<unsigned long long*>(&st->aux), last[n]);
-            } else {
-                take = v > 0.0;
-            }
-        }
-        const long long slot = warp_append(n_cand, take);
-        if (take) {
-            ck[slot] = CandKey{~enc_rank(v), static_cast<unsigned int>(n)};
-            cv[slot] = v;
-        }
-    }
+// a host node whose Eq. 1 is computed by the reference (parent on the device)
+__device__ __forceinline__ bool host_candidate(const PfArgs& a, int n) {
+    return n != 0 && (a.flags[n] & kFlagTierMask) == PBKV_TIER_HOST &&
+           (a.flags[a.parent[n]] & kFlagTierMask) == PBKV_TIER_DEVICE;
 }
 
-// error path: among host candidates with the minimal last_access that miss a
-// forecast, the smallest id
-__global__ void prefetch_err_id_kernel(ScoreArgs s, const int* parent, const std::uint8_t* flags,
-                                       const unsigned long long* last, DevStatus* st, std::int64_t n_nodes) {
-    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n_nodes;
-         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const int n = static_cast<int>(i);
-        if (n == 0 || (flags[n] & kFlagTierMask) != PBKV_TIER_HOST) continue;
-        if ((flags[parent[n]] & kFlagTierMask) != PBKV_TIER_DEVICE) continue;
-        if (last[n] != static_cast<unsigned long long>(st->aux)) continue;
-        bool miss = false;
-        eq1(s, s.acc_rng[n].x, s.acc_rng[n].y, &miss);
-        if (miss) atomicMin(&st->node, static_cast<long long>(n));
+// order-preserving extraction of the bits of `w` under `mask` (a run of set
+// mask bits at a time, high to low)
+__device__ __forceinline__ unsigned long long pext_runs(unsigned long long w, unsigned long long mask) {
+    unsigned long long r = 0;
+    while (mask) {
+        const int hi = 63 - __clzll(static_cast<long long>(mask));
+        const unsigned long long above_cleared = ~mask & ((hi == 63) ? ~0ull : ((1ull << (hi + 1)) - 1ull));
+        const int lo = above_cleared ? 64 - __clzll(static_cast<long long>(above_cleared)) : 0;
+        const int n = hi - lo + 1;
+        const unsigned long long run = (n == 64) ? ~0ull : ((1ull << n) - 1ull);
+        r = (n == 64 ? 0ull : (r << n)) | ((w >> lo) & run);
+        mask &= ~(run << lo);
     }
+    return r;
 }
 
-// greedy fill with skip (policies.hpp:203-210): per round the block finds the
-// first remaining candidate with len <= budget - selected_tokens, selects it
-// and resumes after it
-constexpr int kGreedyThreads = 1024;
-__global__ void __launch_bounds__(kGreedyThreads) prefetch_greedy_kernel(const CandKey* sorted, const int* len,
-                                                                         std::int64_t n, long long budget, int* sel,
-                                                                         long long* counters) {
-    using Red = cub::BlockReduce<long long, kGreedyThreads>;
-    __shared__ typename Red::TempStorage tmp;
-    __shared__ long long pick_sh, rem_sh, nsel_sh;
-    if (threadIdx.x == 0) {
-        rem_sh = budget;
-        nsel_sh = 0;
+// the candidates' varying key bits: (~enc(v)) bits under vhi, then id bits
+// under vid; packed when they fit 64 bits (the usual case), else the rank
+// counting compares (hi, id) and the digit comes from the hi bits alone
+struct Packer {
+    unsigned long long vhi;
+    unsigned int vid;
+    int nhi, nid, nbits;
+    bool packed;
+    __device__ void init(const PfState* ps) {
+        vhi = __ldcg(&ps->or_hi) ^ __ldcg(&ps->and_hi);
+        vid = __ldcg(&ps->or_id) ^ __ldcg(&ps->and_id);
+        nhi = __popcll(vhi);
+        nid = __popc(vid);
+        nbits = nhi + nid;
+        packed = nbits <= 64;
     }
-    __syncthreads();
-    long long start = 0;
-    while (start < n) {
-        const long long rem = rem_sh;
-        const long long i = start + threadIdx.x;
-        long long mine = LLONG_MAX;
-        if (i < n && static_cast<long long>(len[sorted[i].id]) <= rem) mine = i;
-        long long pick = Red(tmp).Reduce(mine, cub::Min());
-        if (threadIdx.x == 0) pick_sh = pick;
-        __syncthreads();
-        pick = pick_sh;
-        if (pick == LLONG_MAX) {
-            start += kGreedyThreads;
-        } else {
-            if (threadIdx.x == 0) {
-                const int id = static_cast<int>(sorted[pick].id);
-                sel[nsel_sh] = id;
-                nsel_sh += 1;
-                rem_sh -= len[id];
-            }
-            start = pick + 1;
-        }
-        __syncthreads();
+    __device__ unsigned long long key(unsigned long long hi, unsigned int id) const {
+        if (!packed) return hi;
+        const unsigned long long ph = pext_runs(hi, vhi), pi = pext_runs(id, vid);
+        return (nid == 64 ? 0ull : (ph << nid)) | pi;
     }
-    if (threadIdx.x == 0) {
-        counters[1] = nsel_sh;
-        counters[2] = budget - rem_sh;
-    }
-}
-
-struct CandDecomposer {
-    __host__ __device__ ::cuda::std::tuple<unsigned long long&, unsigned int&> operator()(CandKey& k) const {
-        return {k.vdesc, k.id};
+    __device__ unsigned int digit(unsigned long long key) const {
+        if (packed) return static_cast<unsigned int>(nbits <= kPBits ? key : key >> (nbits - kPBits));
+        const unsigned long long ph = pext_runs(key, vhi);
+        return static_cast<unsigned int>(ph >> (nhi - kPBits));
     }
 };
 
+__device__ __forceinline__ bool pf_less(bool packed, unsigned long long ka, unsigned int ia, unsigned long long kb,
+                                        unsigned int ib) {
+    if (packed) return ka < kb;  // distinct ids: packed keys are distinct
+    return ka != kb ? ka < kb : ia < ib;
+}
+
+__device__ __forceinline__ double dec_value(unsigned long long hi) {
+    const unsigned long long e = ~hi;  // enc(v) (common.cuh enc_rank)
+    const unsigned long long b = (e >> 63) ? (e & 0x7fffffffffffffffull) : ~e;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+template <class T, class Op>
+__device__ __forceinline__ T block_all(T v, Op op, unsigned long long* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) sh[warp] = static_cast<unsigned long long>(v);
+    __syncthreads();
+    T r = static_cast<T>(sh[0]);
+    for (int w = 1; w < kPT / 32; ++w) r = op(r, static_cast<T>(sh[w]));
+    __syncthreads();
+    return r;
+}
+
+// ---- phase 1: candidates ------------------------------------------------------------
+__device__ __forceinline__ void pf_candidates(const PfArgs& a, PfSmem& sm) {
+    const long long tid = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x;
+    const long long nthr = static_cast<long long>(gridDim.x) * kPT;
+    for (long long j = tid; j < kPBins; j += nthr) {
+        a.hist[j] = 0;
+        a.cursor[j] = 0;
+    }
+    unsigned long long or_hi = 0, and_hi = ~0ull;
+    unsigned int or_id = 0, and_id = ~0u;
+    int min_len = INT_MAX;
+    for (long long base = blockIdx.x * static_cast<long long>(kPT); base < a.n_nodes; base += nthr) {
+        const long long i = base + threadIdx.x;
+        const int n = static_cast<int>(i);
+        bool take = false;
+        double v = 0.0;
+        if (i < a.n_nodes && host_candidate(a, n)) {
+            const uint2 rg = a.s.acc_rng[n];
+            bool miss = false;
+            v = eq1(a.s, rg.x, rg.y, &miss);
+            if (miss) {
+                atomicCAS(&a.st->code, 0, PBKV_EINVAL);
+                atomicCAS(&a.st->kind, 0, kErrMissingForecast);
+                atomicMin(reinterpret_cast<unsigned long long*>(&a.st->aux), a.last[n]);
+            } else {
+                take = v > 0.0;  // policies.hpp:196
+            }
+        }
+        const long long slot = warp_append(&a.ps->n_cand, take);
+        if (take) {
+            const unsigned long long hi = ~enc_rank(v);
+            a.c_hi[slot] = hi;
+            a.c_id[slot] = static_cast<unsigned int>(n);
+            or_hi |= hi;
+            and_hi &= hi;
+            or_id |= static_cast<unsigned int>(n);
+            and_id &= static_cast<unsigned int>(n);
+            min_len = min(min_len, a.len[n]);
+        }
+    }
+    struct Or {
+        __device__ unsigned long long operator()(unsigned long long x, unsigned long long y) const { return x | y; }
+    };
+    struct And {
+        __device__ unsigned long long operator()(unsigned long long x, unsigned long long y) const { return x & y; }
+    };
+    struct Min {
+        __device__ long long operator()(long long x, long long y) const { return x < y ? x : y; }
+    };
+    const unsigned long long bo = block_all<unsigned long long>(or_hi, Or(), sm.red);
+    const unsigned long long ba = block_all<unsigned long long>(and_hi, And(), sm.red);
+    const unsigned long long bio = block_all<unsigned long long>(or_id, Or(), sm.red);
+    const unsigned long long bia = block_all<unsigned long long>(0xffffffff00000000ull | and_id, And(), sm.red);
+    const long long bm = block_all<long long>(min_len, Min(), sm.red);
+    if (threadIdx.x == 0) {
+        if (bo) atomicOr(&a.ps->or_hi, bo);
+        if (~ba) atomicAnd(&a.ps->and_hi, ba);
+        if (bio) atomicOr(&a.ps->or_id, static_cast<unsigned int>(bio));
+        if (static_cast<unsigned int>(bia) != ~0u) atomicAnd(&a.ps->and_id, static_cast<unsigned int>(bia));
+        if (bm != INT_MAX) atomicMin(&a.ps->min_len, static_cast<int>(bm));
+    }
+}
+
+// error path: among the host nodes with the least last_access that miss a
+// forecast, the smallest id (the first raise of policies.hpp:190-195)
+__device__ __forceinline__ void pf_error_id(const PfArgs& a) {
+    const unsigned long long lmin = static_cast<unsigned long long>(__ldcg(&a.st->aux));
+    const long long nthr = static_cast<long long>(gridDim.x) * kPT;
+    for (long long i = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x; i < a.n_nodes; i += nthr) {
+        const int n = static_cast<int>(i);
+        if (!host_candidate(a, n) || a.last[n] != lmin) continue;
+        const uint2 rg = a.s.acc_rng[n];
+        bool miss = false;
+        eq1(a.s, rg.x, rg.y, &miss);
+        if (miss) atomicMin(&a.st->node, static_cast<long long>(n));
+    }
+}
+
+// ---- phase 2: digit histogram -------------------------------------------------------
+__device__ __forceinline__ void pf_hist(const PfArgs& a, const Packer& pk, unsigned long long n, PfSmem& sm) {
+    for (int b = threadIdx.x; b < kPBins; b += kPT) sm.u.hist[b] = 0;
+    __syncthreads();
+    const unsigned long long nthr = static_cast<unsigned long long>(gridDim.x) * kPT;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(kPT) + threadIdx.x; i < n; i += nthr) {
+        const unsigned int d = pk.digit(pk.key(__ldcg(&a.c_hi[i]), __ldcg(&a.c_id[i])));
+        atomicAdd(&sm.u.hist[d], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kPBins; b += kPT) {
+        const unsigned int c = sm.u.hist[b];
+        if (c) atomicAdd(&a.hist[b], c);
+    }
+}
+
+// ---- phase 3: bucket offsets, scatter -------------------------------------------------
+__device__ __forceinline__ void pf_scatter(const PfArgs& a, const Packer& pk, unsigned long long n, PfSmem& sm) {
+    unsigned int v[kPer], s = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        v[j] = __ldcg(&a.hist[threadIdx.x * kPer + j]);
+        s += v[j];
+    }
+    unsigned int ex;
+    cub::BlockScan<unsigned int, kPT>(sm.u.scan).ExclusiveSum(s, ex);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        sm.off[d] = ex;
+        if (blockIdx.x == 0) {
+            a.seg_off[d] = ex;
+            if (v[j] > 32u) {
+                const unsigned int q = atomicAdd(&a.ps->n_big, 1u);
+                a.big[2 * q] = ex;
+                a.big[2 * q + 1] = v[j];
+            }
+        }
+        ex += v[j];
+    }
+    __syncthreads();
+    const unsigned long long nthr = static_cast<unsigned long long>(gridDim.x) * kPT;
+    for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(kPT); base < n; base += nthr) {
+        const unsigned long long i = base + threadIdx.x;
+        const bool in = i < n;
+        unsigned long long hi = 0, key = 0;
+        unsigned int id = 0;
+        int d = -1;
+        if (in) {
+            hi = __ldcg(&a.c_hi[i]);
+            id = __ldcg(&a.c_id[i]);
+            key = pk.key(hi, id);
+            d = static_cast<int>(pk.digit(key));
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (in) {
+            const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+            unsigned int b = 0;
+            if (lane == leader) b = atomicAdd(&a.cursor[d], static_cast<unsigned int>(__popc(peers)));
+            b = __shfl_sync(peers, b, leader);
+            const unsigned int pos = sm.off[d] + b + __popc(peers & ((1u << lane) - 1u));
+            a.b_key[pos] = key;
+            a.b_hi[pos] = hi;
+            a.b_id[pos] = id;
+        }
+    }
+}
+
+// ---- phase 4: rank every bucket -------------------------------------------------------
+__device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSmem& sm) {
+    // buckets of 2..32: one warp each; singletons copied
+    const int lane = threadIdx.x & 31;
+    const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(kPT) + threadIdx.x) >> 5);
+    const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(kPT)) >> 5);
+    for (int d = gwarp; d < kPBins; d += nwarps) {
+        const unsigned int cnt = __ldcg(&a.hist[d]);
+        if (cnt == 0u || cnt > 32u) continue;
+        const unsigned int off = __ldcg(&a.seg_off[d]);
+        const bool in = static_cast<unsigned int>(lane) < cnt;
+        const unsigned long long k = in ? __ldcg(&a.b_key[off + lane]) : 0ull;
+        const unsigned int id = in ? __ldcg(&a.b_id[off + lane]) : 0u;
+        unsigned int r = 0;
+        for (unsigned int j = 0; j < cnt; ++j) {
+            const unsigned long long kj = __shfl_sync(0xffffffffu, k, j);
+            const unsigned int ij = __shfl_sync(0xffffffffu, id, j);
+            r += pf_less(pk.packed, kj, ij, k, id) ? 1u : 0u;
+        }
+        if (in) {
+            a.s_id[off + r] = static_cast<int>(id);
+            a.s_hi[off + r] = __ldcg(&a.b_hi[off + lane]);
+        }
+    }
+    // larger buckets: rank = number of smaller keys, counted from shared-memory
+    // tiles by 8 threads per element.  Tasks are (bucket, 64-element chunk);
+    // the first task of every bucket comes from a block scan of the chunk
+    // counts (sm.off, free after the scatter), task t -> CTA t % grid.
+    if (threadIdx.x == 0) sm.bc[0] = __ldcg(&a.ps->n_big);
+    __syncthreads();
+    const unsigned int n_big = static_cast<unsigned int>(sm.bc[0]);
+    if (n_big == 0) return;
+    {
+        unsigned int v[kPer], s = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const unsigned int b = threadIdx.x * kPer + j;
+            v[j] = b < n_big ? (__ldcg(&a.big[2 * b + 1]) + kChunk - 1) / kChunk : 0u;
+            s += v[j];
+        }
+        unsigned int ex, tot;
+        __syncthreads();
+        cub::BlockScan<unsigned int, kPT>(sm.u.scan).ExclusiveSum(s, ex, tot);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            sm.off[threadIdx.x * kPer + j] = ex;
+            ex += v[j];
+        }
+        if (threadIdx.x == 0) sm.bc[1] = tot;
+        __syncthreads();
+    }
+    const unsigned int n_task = static_cast<unsigned int>(sm.bc[1]);
+    unsigned int held = ~0u;  // bucket whose first tile is in shared memory
+    for (unsigned int t = blockIdx.x; t < n_task; t += gridDim.x) {
+        unsigned int lo = 0, hi = n_big - 1;  // last bucket with off[b] <= t
+        while (lo < hi) {
+            const unsigned int mid = (lo + hi + 1) >> 1;
+            if (sm.off[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const unsigned int b = lo, c = t - sm.off[b];
+        const unsigned int off = __ldcg(&a.big[2 * b]), cnt = __ldcg(&a.big[2 * b + 1]);
+        const unsigned int e = c * kChunk + threadIdx.x / 8, part = threadIdx.x % 8;
+        const bool in = e < cnt;
+        const unsigned long long mk = in ? __ldcg(&a.b_key[off + e]) : 0ull;
+        const unsigned int mi = in ? __ldcg(&a.b_id[off + e]) : 0u;
+        unsigned int r = 0;
+        for (unsigned int t0 = 0; t0 < cnt; t0 += kTile) {
+            const unsigned int tn = min(static_cast<unsigned int>(kTile), cnt - t0);
+            if (!(t0 == 0 && held == b)) {
+                __syncthreads();
+                for (unsigned int q = threadIdx.x; q < tn; q += kPT) {
+                    sm.u.tile.k[q] = __ldcg(&a.b_key[off + t0 + q]);
+                    sm.u.tile.id[q] = __ldcg(&a.b_id[off + t0 + q]);
+                }
+                __syncthreads();
+                held = t0 == 0 ? b : ~0u;
+            }
+            if (in) {
+                if (pk.packed) {
+#pragma unroll 4
+                    for (unsigned int q = part; q < tn; q += 8) r += sm.u.tile.k[q] < mk ? 1u : 0u;
+                } else {
+                    for (unsigned int q = part; q < tn; q += 8)
+                        r += pf_less(false, sm.u.tile.k[q], sm.u.tile.id[q], mk, mi) ? 1u : 0u;
+                }
+            }
+        }
+        r += __shfl_xor_sync(0xffffffffu, r, 1);
+        r += __shfl_xor_sync(0xffffffffu, r, 2);
+        r += __shfl_xor_sync(0xffffffffu, r, 4);
+        if (in && part == 0) {
+            a.s_id[off + r] = static_cast<int>(mi);
+            a.s_hi[off + r] = __ldcg(&a.b_hi[off + e]);
+        }
+    }
+}
+
+// ---- phase 5: greedy fill (one warp) and the plan to the host --------------------------
+__device__ __forceinline__ void pf_greedy(const PfArgs& a, unsigned long long n) {
+    const int lane = threadIdx.x & 31;
+    long long rem = a.budget, nsel = 0, tok = 0;
+    const long long min_len = __ldcg(&a.ps->min_len);
+    for (unsigned long long base = 0; base < n && rem >= min_len; base += 32) {
+        const unsigned long long i = base + lane;
+        const bool in = i < n;
+        const int id = in ? __ldcg(&a.s_id[i]) : 0;
+        const long long l = in ? static_cast<long long>(a.len[id]) : 0;
+        unsigned todo = __ballot_sync(0xffffffffu, in);
+        while (todo) {
+            // a lane longer than the remaining budget is skipped for good
+            todo &= __ballot_sync(0xffffffffu, l <= rem);
+            if (!todo) break;
+            const bool mine = (todo >> lane) & 1u;
+            long long x = mine ? l : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            // every lane whose running total still fits is taken (a prefix of todo)
+            const bool fit = mine && x <= rem;
+            const unsigned fm = __ballot_sync(0xffffffffu, fit);
+            if (fit) a.h_sel[nsel + __popc(fm & ((1u << lane) - 1u))] = id;
+            const long long used = fm ? __shfl_sync(0xffffffffu, x, 31 - __clz(fm)) : 0;
+            rem -= used;
+            tok += used;
+            nsel += __popc(fm);
+            todo &= ~fm;
+            if (todo) todo &= todo - 1u;  // the first lane past them does not fit: skipped
+        }
+    }
+    if (lane == 0) {
+        a.h_ctr[1] = nsel;
+        a.h_ctr[2] = tok;
+    }
+}
+
+__global__ void __launch_bounds__(kPT, 2) prefetch_plan_kernel(PfArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PfSmem& sm = *reinterpret_cast<PfSmem*>(smem_raw);
+    cg::grid_group grid = cg::this_grid();
+    pf_candidates(a, sm);
+    grid.sync();
+    if (threadIdx.x == 0) {
+        sm.bc[0] = static_cast<unsigned long long>(__ldcg(&a.st->code));
+        sm.bc[1] = __ldcg(&a.ps->n_cand);
+    }
+    __syncthreads();
+    const bool err = sm.bc[0] != 0;
+    const unsigned long long n = sm.bc[1];
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.h_ctr[3] = err ? 1 : 0;
+    if (err) {
+        pf_error_id(a);
+        return;
+    }
+    if (n == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.h_ctr[0] = a.h_ctr[1] = a.h_ctr[2] = 0;
+        return;
+    }
+    Packer pk;
+    pk.init(a.ps);
+    pf_hist(a, pk, n, sm);
+    grid.sync();
+    pf_scatter(a, pk, n, sm);
+    grid.sync();
+    pf_sort(a, pk, sm);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        pf_greedy(a, n);
+        if (threadIdx.x == 0) a.h_ctr[0] = static_cast<long long>(n);
+        return;
+    }
+    // the sorted candidates and their values into pinned host memory
+    const long long t = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x - 32;
+    const long long nt = static_cast<long long>(gridDim.x) * kPT - 32;
+    for (long long i = t; i < static_cast<long long>(n); i += nt) {
+        a.h_cand[i] = __ldcg(&a.s_id[i]);
+        a.h_val[i] = dec_value(__ldcg(&a.s_hi[i]));
+    }
+}
+
+int plan_grid(Context& c, std::int64_t n_nodes) {
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        PBKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+        PBKV_CUDA(cudaFuncSetAttribute(prefetch_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(PfSmem))));
+        PBKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prefetch_plan_kernel, kPT,
+                                                                sizeof(PfSmem)));
+        if (per_sm < 1) throw ApiError(PBKV_ECUDA, "prefetch plan kernel cannot be resident");
+        per_sm = per_sm >= 2 ? 2 : 1;
+    }
+    // small trees: fewer CTAs (cheaper grid barriers); one node per thread
+    // and pass up to the full co-resident grid
+    const std::int64_t want = (n_nodes + 4LL * kPT - 1) / (4LL * kPT);
+    const std::int64_t cap = static_cast<std::int64_t>(sms) * per_sm;
+    return static_cast<int>(std::max<std::int64_t>(8, std::min(want, cap)));
+}
+
 }  // namespace
 
-void launch_prefetch_candidates(Context& c, unsigned long long* n_cand_dev) {
-    ScoreArgs s = make_score_args(c, nullptr);
-    prefetch_cand_kernel<<<grid_cap(c.n, 256), 256, 0, c.stream>>>(s, c.parent.p, c.flags.p, c.last.p, c.ck_in.p,
-                                                                   c.cv_in.p, n_cand_dev, c.status.p, c.n);
-    PBKV_CUDA(cudaGetLastError());
+// One plan: status + state reset, the cooperative kernel, one synchronisation.
+// The plan lands in pinned host memory: c.hplan = [ctr 3 x i64 | cand ids
+// (cap) | values (cap) | selected (cap)].
+void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
+    const std::size_t n = static_cast<std::size_t>(c.n) + 1;
+    c.pf_hi.reserve(n);
+    c.pf_id.reserve(n);
+    c.pf_bkey.reserve(n);
+    c.pf_bhi.reserve(n);
+    c.pf_bid.reserve(n);
+    c.pf_shi.reserve(n);
+    c.pf_sid.reserve(n);
+    c.pf_hist.reserve(3 * kPBins);
+    c.pf_big.reserve(2 * kPBins);
+    c.pf_state.reserve(sizeof(PfState));
+    const std::size_t b_ctr = 4 * sizeof(long long), b_ids = ((n * 4 + 15) & ~std::size_t(15));
+    const std::size_t b_val = n * 8;
+    c.hplan.reserve(b_ctr + 2 * b_ids + b_val);
+    unsigned char* hp = c.hplan.p;
+    PfArgs a;
+    a.s = make_score_args(c, nullptr);
+    a.parent = c.parent.p;
+    a.flags = c.flags.p;
+    a.last = c.last.p;
+    a.len = c.len.p;
+    a.n_nodes = c.n;
+    a.budget = budget;
+    a.c_hi = c.pf_hi.p;
+    a.c_id = c.pf_id.p;
+    a.b_key = c.pf_bkey.p;
+    a.b_hi = c.pf_bhi.p;
+    a.b_id = c.pf_bid.p;
+    a.s_hi = c.pf_shi.p;
+    a.s_id = c.pf_sid.p;
+    a.hist = c.pf_hist.p;
+    a.cursor = c.pf_hist.p + kPBins;
+    a.seg_off = c.pf_hist.p + 2 * kPBins;
+    a.big = c.pf_big.p;
+    a.ps = reinterpret_cast<PfState*>(c.pf_state.p);
+    a.st = c.status.p;
+    a.h_ctr = reinterpret_cast<long long*>(hp);
+    a.h_cand = reinterpret_cast<int*>(hp + b_ctr);
+    a.h_sel = reinterpret_cast<int*>(hp + b_ctr + b_ids);
+    a.h_val = reinterpret_cast<double*>(hp + b_ctr + 2 * b_ids);
+    // initial state from the pinned template (and_* all ones, min_len max)
+    PfState* init = reinterpret_cast<PfState*>(c.hplan_init.p);
+    if (!init) {
+        c.hplan_init.reserve(sizeof(PfState));
+        init = reinterpret_cast<PfState*>(c.hplan_init.p);
+        *init = PfState{0, 0, ~0ull, 0u, ~0u, INT_MAX, 0u};
+    }
+    PBKV_CUDA(cudaMemcpyAsync(a.ps, init, sizeof(PfState), cudaMemcpyHostToDevice, c.stream));
+    void* args[] = {&a};
+    if (c.timing) {  // kernel_ms[1] (pbkv_ctx_kernel_timings): the plan kernel alone
+        PBKV_CUDA(cudaEventRecord(c.kev[2], c.stream));
+        c.kev_select = true;
+    }
+    PBKV_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(prefetch_plan_kernel), dim3(plan_grid(c, c.n)),
+                                          dim3(kPT), args, sizeof(PfSmem), c.stream));
+    if (c.timing) PBKV_CUDA(cudaEventRecord(c.kev[3], c.stream));
     ++c.launches;
-}
-
-void launch_prefetch_err_id(Context& c) {
-    ScoreArgs s = make_score_args(c, nullptr);
-    prefetch_err_id_kernel<<<grid_cap(c.n, 256), 256, 0, c.stream>>>(s, c.parent.p, c.flags.p, c.last.p, c.status.p,
-                                                                     c.n);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
-}
-
-void launch_prefetch_sort_greedy(Context& c, std::int64_t n_cand, long long budget, long long* counters_dev) {
-    std::size_t b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, c.ck_in.p, c.ck_out.p, c.cv_in.p, c.cv_out.p, static_cast<int>(n_cand),
-                                    CandDecomposer{});
-    c.cub_tmp.reserve(b);
-    ++c.lib_calls;
-    PBKV_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, b, c.ck_in.p, c.ck_out.p, c.cv_in.p, c.cv_out.p,
-                                              static_cast<int>(n_cand), CandDecomposer{}, c.stream));
-    prefetch_greedy_kernel<<<1, kGreedyThreads, 0, c.stream>>>(c.ck_out.p, c.len.p, n_cand, budget, c.sel.p,
-                                                               counters_dev);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
+    PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    if (a.h_ctr[3]) check_status(c);  // the error path: the full status word
+    out->ctr = a.h_ctr;
+    out->cand = a.h_cand;
+    out->val = a.h_val;
+    out->sel = a.h_sel;
 }
 
 }  // namespace pbkv

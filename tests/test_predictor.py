@@ -2,7 +2,8 @@
 the FP64 restatement of PAPER.md:1040-1066 (oracle/predictor_ref.py).
 
 Parity is UNPINNED (no reference code exists): the tolerance is the
-builder's, stated here -- max |p_gpu - p_fp64| <= 2e-3 per probability, and
+builder's, stated here -- max |p_gpu - p_fp64| <= 1e-5 per probability (measured: 4.0e-6 on the
+tcgen05 bf16x3 head, 4.6e-7 on the fp32 head), and
 the arg-max outcome of every step agrees wherever the FP64 top-2 gap exceeds
 1e-3.  The stored forecasts must pass the Forecast ctor checks
 (forecast.hpp:25-34) and then drive Eq. 2 bit-exactly (same rows on CPU and GPU).
@@ -13,7 +14,7 @@ import pytest
 import predictor_ref as PR
 from paper_2605_06472_b200.predictor import PredictorWeights, random_inputs
 
-TOL = 2e-3
+TOL = 1e-5
 
 
 def test_param_count_matches_paper():
