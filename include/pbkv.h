@@ -359,6 +359,11 @@ int pbkv_merge_cut(pbkv_ctx* ctx, const pbkv_cand* runs_dev, const int64_t* run_
 int pbkv_plan_prefetch(pbkv_ctx* ctx, int64_t bandwidth, int step_duration, double rho, int32_t* cand_ids,
                        double* cand_values, int64_t cand_cap, int32_t* selected, int64_t sel_cap,
                        pbkv_prefetch_plan* plan);
+/* The arrays of the context's last plan (held in pinned host memory until
+ * the next plan): callers that size their arrays from plan->n_candidates /
+ * n_selected call pbkv_plan_prefetch with zero capacities, then this. */
+int pbkv_plan_fetch(pbkv_ctx* ctx, int32_t* cand_ids, double* cand_values, int64_t cand_cap, int32_t* selected,
+                    int64_t sel_cap);
 
 /* ---- host trees: the reference flowkv::CacheTree (cache.hpp) with a change
  * log for incremental device sync (include/pbkv/tracked_tree.hpp).  For the

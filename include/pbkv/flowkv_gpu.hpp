@@ -272,10 +272,10 @@ inline PrefetchPlan plan(const CacheTree& tree, const ForecastProvider& fp, std:
     mirror(e, tree);
     batch.upload(c);
     pbkv_prefetch_plan p{};
-    const std::int64_t cap = static_cast<std::int64_t>(tree.host_nodes().size());
-    std::vector<std::int32_t> cid(static_cast<std::size_t>(cap) + 1), sel(static_cast<std::size_t>(cap) + 1);
-    std::vector<double> cv(static_cast<std::size_t>(cap) + 1);
-    check(pbkv_plan_prefetch(c, bandwidth, step_duration, rho, cid.data(), cv.data(), cap, sel.data(), cap, &p), c);
+    check(pbkv_plan_prefetch(c, bandwidth, step_duration, rho, nullptr, nullptr, 0, nullptr, 0, &p), c);
+    std::vector<std::int32_t> cid(static_cast<std::size_t>(p.n_candidates)), sel(static_cast<std::size_t>(p.n_selected));
+    std::vector<double> cv(static_cast<std::size_t>(p.n_candidates));
+    check(pbkv_plan_fetch(c, cid.data(), cv.data(), p.n_candidates, sel.data(), p.n_selected), c);
     PrefetchPlan out;
     out.budget_space = p.budget_space;
     out.budget_bw = p.budget_bw;

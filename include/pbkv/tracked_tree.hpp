@@ -37,6 +37,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -406,13 +409,25 @@ struct DeltaBatch {
 /// pbkv status and sets *full_upload accordingly.
 inline int sync_mirror(pbkv_ctx* c, const TrackedCacheTree& t, std::uint64_t& uid, std::int64_t& pos,
                        std::vector<int>& ids, DeltaBatch& batch, TreeImage& img, bool* full_upload = nullptr) {
-    if (uid == t.uid() && t.changes_since(pos, ids)) {
-        if (full_upload) *full_upload = false;
-        batch.build(t, ids);
-        const int rc = pbkv_mirror_delta(c, batch.nodes.data(), static_cast<std::int64_t>(batch.nodes.size()),
-                                         batch.wf.data(), batch.bits.data(), &batch.totals);
-        if (rc == PBKV_OK) pos = t.log_end();
-        return rc;
+    if (uid == t.uid()) {
+        static const bool prof = std::getenv("PBKV_PROFILE_SYNC") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        if (t.changes_since(pos, ids)) {
+            if (full_upload) *full_upload = false;
+            const auto t1 = std::chrono::steady_clock::now();
+            batch.build(t, ids);
+            const auto t2 = std::chrono::steady_clock::now();
+            const int rc = pbkv_mirror_delta(c, batch.nodes.data(), static_cast<std::int64_t>(batch.nodes.size()),
+                                             batch.wf.data(), batch.bits.data(), &batch.totals);
+            const auto t3 = std::chrono::steady_clock::now();
+            if (prof) {
+                auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+                std::fprintf(stderr, "[pbkv sync] ids=%zu entries=%zu log=%.1fus batch=%.1fus delta=%.1fus\n",
+                             ids.size(), batch.wf.size(), us(t0, t1), us(t1, t2), us(t2, t3));
+            }
+            if (rc == PBKV_OK) pos = t.log_end();
+            return rc;
+        }
     }
     if (full_upload) *full_upload = true;
     img.build(t, &t.depths());

@@ -91,15 +91,61 @@ class VictimSelection:
         return f"VictimSelection(victims={self.victims!r}, freed={self.freed}, shortfall={self.shortfall})"
 
 
-@dataclass
 class PrefetchPlan:
-    """policies.hpp:170-177"""
-    candidates: list[tuple[int, float]] = field(default_factory=list)
-    budget_space: int = 0
-    budget_bw: int = 0
-    displacement_budget: int = 0
-    selected: list[int] = field(default_factory=list)
-    selected_tokens: int = 0
+    """policies.hpp:170-177.
+
+    `candidate_ids` / `candidate_values` / `selected_ids` are the arrays the C
+    ABI filled; `candidates` (a list of (id, value) pairs, best first) and
+    `selected` are built from them on first access."""
+
+    __slots__ = ("candidate_ids", "candidate_values", "selected_ids", "budget_space", "budget_bw",
+                 "displacement_budget", "selected_tokens", "_cand", "_sel")
+
+    def __init__(self, candidates=None, budget_space: int = 0, budget_bw: int = 0, displacement_budget: int = 0,
+                 selected=None, selected_tokens: int = 0):
+        cand = list(candidates) if candidates is not None else []
+        self.candidate_ids = np.array([c[0] for c in cand], dtype=np.int32)
+        self.candidate_values = np.array([c[1] for c in cand], dtype=np.float64)
+        self.selected_ids = np.asarray(selected if selected is not None else [], dtype=np.int32)
+        self.budget_space = int(budget_space)
+        self.budget_bw = int(budget_bw)
+        self.displacement_budget = int(displacement_budget)
+        self.selected_tokens = int(selected_tokens)
+        self._cand = cand if candidates is not None else None
+        self._sel = list(selected) if selected is not None else None
+
+    @classmethod
+    def from_arrays(cls, cid, cv, sel, budget_space, budget_bw, displacement_budget, selected_tokens):
+        p = cls.__new__(cls)
+        p.candidate_ids, p.candidate_values, p.selected_ids = cid, cv, sel
+        p.budget_space, p.budget_bw = int(budget_space), int(budget_bw)
+        p.displacement_budget, p.selected_tokens = int(displacement_budget), int(selected_tokens)
+        p._cand = p._sel = None
+        return p
+
+    @property
+    def candidates(self) -> list[tuple[int, float]]:
+        if self._cand is None:
+            self._cand = list(zip(self.candidate_ids.tolist(), self.candidate_values.tolist()))
+        return self._cand
+
+    @property
+    def selected(self) -> list[int]:
+        if self._sel is None:
+            self._sel = self.selected_ids.tolist()
+        return self._sel
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, PrefetchPlan):
+            return NotImplemented
+        return (self.candidates, self.budget_space, self.budget_bw, self.displacement_budget, self.selected,
+                self.selected_tokens) == (other.candidates, other.budget_space, other.budget_bw,
+                                          other.displacement_budget, other.selected, other.selected_tokens)
+
+    def __repr__(self) -> str:
+        return (f"PrefetchPlan(candidates={self.candidates!r}, budget_space={self.budget_space}, "
+                f"budget_bw={self.budget_bw}, displacement_budget={self.displacement_budget}, "
+                f"selected={self.selected!r}, selected_tokens={self.selected_tokens})")
 
 
 # ----------------------------------------------------------------------------------
@@ -392,16 +438,16 @@ class Policy:
     # ---- stage 4 -------------------------------------------------------------------
     def _plan(self, bandwidth: int, step_duration: int, rho: float) -> PrefetchPlan:
         L = _abi.lib()
-        cap = max(self.n_nodes, 1)
-        cid = np.zeros(cap, dtype=np.int32)
-        cv = np.zeros(cap, dtype=np.float64)
-        sel = np.zeros(cap, dtype=np.int32)
         pl = _abi.PrefetchPlanC()
-        self._c(L.pbkv_plan_prefetch(self._h, int(bandwidth), int(step_duration), float(rho), ptr(cid, C.c_int32),
-                                     ptr(cv, C.c_double), cap, ptr(sel, C.c_int32), cap, C.byref(pl)))
+        self._c(L.pbkv_plan_prefetch(self._h, int(bandwidth), int(step_duration), float(rho), None, None, 0, None, 0,
+                                     C.byref(pl)))
         nc, ns = pl.n_candidates, pl.n_selected
-        return PrefetchPlan(list(zip(cid[:nc].tolist(), cv[:nc].tolist())), pl.budget_space, pl.budget_bw,
-                            pl.displacement_budget, sel[:ns].tolist(), pl.selected_tokens)
+        cid = np.empty(nc, dtype=np.int32)
+        cv = np.empty(nc, dtype=np.float64)
+        sel = np.empty(ns, dtype=np.int32)
+        self._c(L.pbkv_plan_fetch(self._h, ptr(cid, C.c_int32), ptr(cv, C.c_double), nc, ptr(sel, C.c_int32), ns))
+        return PrefetchPlan.from_arrays(cid, cv, sel, pl.budget_space, pl.budget_bw, pl.displacement_budget,
+                                        pl.selected_tokens)
 
     def plan_conservative_prefetch(self, bandwidth: int, step_duration: int = 1) -> PrefetchPlan:
         """policies.hpp:220-224"""

@@ -1,6 +1,7 @@
 // C ABI implementation (include/pbkv.h): context, device mirror, forecast
 // store and the orchestration of the stage 2-4 kernels (kernels.cu).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <climits>
 #include <cstring>
@@ -643,6 +644,15 @@ void repack_pool(Context& c) {
 
 void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, const std::int64_t* acc_wf,
                   const std::uint64_t* acc_bits, const pbkv_tree_totals* totals) {
+    static const bool prof = std::getenv("PBKV_PROFILE_SYNC") != nullptr;
+    auto prev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!prof) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  [delta] %s %.1fus\n", what, std::chrono::duration<double, std::micro>(now - prev).count());
+        prev = now;
+    };
+    if (prof) lap("start");
     need(c.n >= 1, "no tree mirrored");
     need(n_rec == 0 || d, "null delta records");
     // the last record of a node wins
@@ -684,6 +694,7 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     for (const auto& [id, i] : last_of) order.push_back(i);
     std::sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) { return d[a].id < d[b].id; });
 
+    lap("validate+order");
     // grow the mirror (keeping contents) and the host copies
     cudaStream_t st = c.stream;
     if (n_new > n_old) {
@@ -782,6 +793,7 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
             }
         }
     }
+    lap("records");
     c.n = n_new;
     c.E = E;
     if (c.pool_top > static_cast<std::int64_t>(c.acc_slot.cap)) {
@@ -822,8 +834,10 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
     }
+    lap("upload");
     if (totals) set_totals(c, *totals);
     if (n_new > n_old) ensure_scratch(c);
+    lap("scratch");
     // class lists and heavy children, updated by the changed nodes only
     std::vector<int> newly_heavy;
     for (const ClassMove& m : cls_moves) {
@@ -860,10 +874,12 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
             }
         }
     }
+    lap("class lists");
     if (products)
         upload_classes(c);
     else if (tables)
         refresh_heavy_tables(c);
+    lap(products ? "upload_classes" : "heavy tables");
     if (!c.spine.empty()) shard_apply_flags(c);
     // dead space above half of the pool: repack (rare; amortised O(1) per entry)
     if (c.pool_top > 2 * c.E + (1 << 16)) repack_pool(c);
@@ -1531,6 +1547,19 @@ int pbkv_set_remaining(pbkv_ctx* c, const int64_t* wf, int64_t n_wf, const int64
     });
 }
 
+namespace {
+// the last plan's arrays (pinned host memory) into the caller's
+void copy_plan(const Context& c, int32_t* cand_ids, double* cand_values, int64_t cand_cap, int32_t* selected,
+               int64_t sel_cap) {
+    const PrefetchOut& o = c.plan_out;
+    const std::int64_t mc = std::min<std::int64_t>(cand_cap, o.ctr[0]);
+    if (mc > 0 && cand_ids) std::memcpy(cand_ids, o.cand, static_cast<std::size_t>(mc) * sizeof(int32_t));
+    if (mc > 0 && cand_values) std::memcpy(cand_values, o.val, static_cast<std::size_t>(mc) * sizeof(double));
+    const std::int64_t ms = std::min<std::int64_t>(sel_cap, o.ctr[1]);
+    if (ms > 0 && selected) std::memcpy(selected, o.sel, static_cast<std::size_t>(ms) * sizeof(int32_t));
+}
+}  // namespace
+
 int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double rho, int32_t* cand_ids,
                        double* cand_values, int64_t cand_cap, int32_t* selected, int64_t sel_cap,
                        pbkv_prefetch_plan* plan) {
@@ -1550,6 +1579,7 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
         const long long budget = std::min(plan->budget_space + extra, plan->budget_bw);
         record(*c, 0);
         reset_status(*c);
+        c->plan_valid = false;
         PrefetchOut o;
         run_prefetch_plan(*c, budget, &o);  // one synchronisation
         record(*c, 1);
@@ -1558,11 +1588,18 @@ int pbkv_plan_prefetch(pbkv_ctx* c, int64_t bandwidth, int step_duration, double
         plan->n_candidates = nc;
         plan->n_selected = o.ctr[1];
         plan->selected_tokens = o.ctr[2];
-        const std::int64_t mc = std::min<std::int64_t>(cand_cap, nc);
-        if (mc > 0 && cand_ids) std::memcpy(cand_ids, o.cand, static_cast<std::size_t>(mc) * sizeof(int32_t));
-        if (mc > 0 && cand_values) std::memcpy(cand_values, o.val, static_cast<std::size_t>(mc) * sizeof(double));
-        const std::int64_t ms = std::min<std::int64_t>(sel_cap, plan->n_selected);
-        if (ms > 0 && selected) std::memcpy(selected, o.sel, static_cast<std::size_t>(ms) * sizeof(int32_t));
+        c->plan_out = o;
+        c->plan_valid = true;
+        copy_plan(*c, cand_ids, cand_values, cand_cap, selected, sel_cap);
+    });
+}
+
+int pbkv_plan_fetch(pbkv_ctx* c, int32_t* cand_ids, double* cand_values, int64_t cand_cap, int32_t* selected,
+                    int64_t sel_cap) {
+    return api(c, [&] {
+        need(c != nullptr, "null ctx");
+        need(c->plan_valid, "no prefetch plan to fetch");
+        copy_plan(*c, cand_ids, cand_values, cand_cap, selected, sel_cap);
     });
 }
 

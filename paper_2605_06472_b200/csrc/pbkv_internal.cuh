@@ -303,11 +303,13 @@ struct Context {
     DevBuf<int> ids, ids2, ids3;
     DevBuf<double> vals;
     // stage 4 scratch (prefetch.cu)
-    DevBuf<unsigned long long> pf_hi, pf_bkey, pf_bhi, pf_shi;
-    DevBuf<unsigned int> pf_id, pf_bid, pf_hist, pf_big;
-    DevBuf<int> pf_sid;
+    DevBuf<unsigned long long> pf_hi, pf_bkey, pf_bhi, pf_hlen;
+    DevBuf<unsigned int> pf_id, pf_len, pf_bid, pf_blen, pf_hist, pf_big;
+    DevBuf<int> pf_sid, pf_slen, pf_cmin;
     DevBuf<unsigned char> pf_state;
     PinBuf<unsigned char> hplan, hplan_init;
+    PrefetchOut plan_out{};  // the last plan (views into hplan)
+    bool plan_valid = false;
     DevBuf<unsigned char> cub_tmp;
     DevBuf<long long> counters;  // small device scalars
     DevBuf<DevStatus> status;

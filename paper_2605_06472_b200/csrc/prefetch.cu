@@ -12,12 +12,15 @@
 //      bucket, then every bucket is ranked in place -- one warp for <= 32
 //      elements, else rank counting from shared-memory tiles, (bucket, 64-
 //      element chunk) tasks spread over every CTA;
-//   3. greedy fill with skip (policies.hpp:203-210) by one warp: a warp-wide
-//      prefix sum of the next lanes' token lengths takes every lane that still
-//      fits at once; the first lane that does not is skipped; lanes longer
-//      than the remaining budget are skipped together (the budget only
-//      shrinks); the walk stops once the budget is below the shortest
-//      candidate;
+//   3. greedy fill with skip (policies.hpp:203-210), exact and mostly
+//      parallel: while the running token total of the sorted candidates stays
+//      within the budget every candidate is taken, so the sort phase, which
+//      knows each candidate's token prefix (bucket prefix from the histogram
+//      + the lengths of the smaller keys in its bucket, summed by the rank
+//      count), selects that whole prefix at once and marks the first
+//      candidate that overflows it; one warp then continues from there with
+//      the small remaining budget, skipping 32-candidate chunks whose shortest
+//      length exceeds it and taking runs that fit by a warp prefix sum;
 //   4. the plan (sorted candidates, values, selection, counters) is stored
 //      straight into pinned host memory by the kernel.
 #include <cooperative_groups.h>
@@ -47,6 +50,8 @@ struct PfState {
     unsigned int or_id, and_id;
     int min_len;
     unsigned int n_big;
+    unsigned long long f;      // sorted position of the first candidate overflowing the budget
+    long long tok_f;           // tokens of the candidates before it (all selected)
 };
 
 struct PfArgs {
@@ -57,17 +62,22 @@ struct PfArgs {
     const int* len;
     long long n_nodes;
     long long budget;
-    unsigned long long* c_hi;  // candidates in append order: ~enc(v), id
+    unsigned long long* c_hi;  // candidates in append order: ~enc(v), id, len
     unsigned int* c_id;
-    unsigned long long* b_key;  // bucketed: sort key (packed, or ~enc(v)), ~enc(v), id
+    unsigned int* c_len;
+    unsigned long long* b_key;  // bucketed: sort key (packed, or ~enc(v)), ~enc(v), id, len
     unsigned long long* b_hi;
     unsigned int* b_id;
-    unsigned long long* s_hi;  // sorted
-    int* s_id;
-    unsigned int* hist;     // [kPBins]
+    unsigned int* b_len;
+    int* s_id;  // sorted ids and lengths (the greedy tail)
+    int* s_len;
+    int* chunk_min;  // shortest length of every 32 sorted candidates
+    unsigned int* hist;     // [kPBins] counts
+    unsigned long long* hist_len;  // [kPBins] token sums
     unsigned int* cursor;   // [kPBins]
-    unsigned int* seg_off;  // [kPBins]
-    unsigned int* big;      // (offset, count) of the buckets ranked by tiles
+    unsigned int* seg_off;  // [kPBins] first sorted position of every bucket
+    unsigned long long* seg_lpre;  // [kPBins] tokens of the buckets before it
+    unsigned int* big;      // (bucket, offset, count) of the buckets ranked by tiles
     PfState* ps;
     DevStatus* st;
     int* h_cand;  // pinned host outputs
@@ -78,12 +88,17 @@ struct PfArgs {
 
 struct PfSmem {
     union {
-        unsigned int hist[kPBins];
+        struct {
+            unsigned int c[kPBins];
+            unsigned long long l[kPBins];
+        } hist;
         struct {
             unsigned long long k[kTile];
             unsigned int id[kTile];
+            unsigned int len[kTile];
         } tile;
         typename cub::BlockScan<unsigned int, kPT>::TempStorage scan;
+        typename cub::BlockScan<unsigned long long, kPT>::TempStorage scan64;
     } u;
     unsigned int off[kPBins];
     unsigned long long red[32];
@@ -186,8 +201,10 @@ __device__ __forceinline__ void pf_candidates(const PfArgs& a, PfSmem& sm) {
     const long long nthr = static_cast<long long>(gridDim.x) * kPT;
     for (long long j = tid; j < kPBins; j += nthr) {
         a.hist[j] = 0;
+        a.hist_len[j] = 0;
         a.cursor[j] = 0;
     }
+    for (long long j = tid; j <= (a.n_nodes >> 5); j += nthr) a.chunk_min[j] = INT_MAX;
     unsigned long long or_hi = 0, and_hi = ~0ull;
     unsigned int or_id = 0, and_id = ~0u;
     int min_len = INT_MAX;
@@ -213,6 +230,7 @@ __device__ __forceinline__ void pf_candidates(const PfArgs& a, PfSmem& sm) {
             const unsigned long long hi = ~enc_rank(v);
             a.c_hi[slot] = hi;
             a.c_id[slot] = static_cast<unsigned int>(n);
+            a.c_len[slot] = static_cast<unsigned int>(a.len[n]);
             or_hi |= hi;
             and_hi &= hi;
             or_id |= static_cast<unsigned int>(n);
@@ -258,45 +276,63 @@ __device__ __forceinline__ void pf_error_id(const PfArgs& a) {
     }
 }
 
-// ---- phase 2: digit histogram -------------------------------------------------------
+// ---- phase 2: digit histogram (counts and token sums) ----------------------------------
 __device__ __forceinline__ void pf_hist(const PfArgs& a, const Packer& pk, unsigned long long n, PfSmem& sm) {
-    for (int b = threadIdx.x; b < kPBins; b += kPT) sm.u.hist[b] = 0;
+    for (int b = threadIdx.x; b < kPBins; b += kPT) {
+        sm.u.hist.c[b] = 0;
+        sm.u.hist.l[b] = 0;
+    }
     __syncthreads();
     const unsigned long long nthr = static_cast<unsigned long long>(gridDim.x) * kPT;
     for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(kPT) + threadIdx.x; i < n; i += nthr) {
         const unsigned int d = pk.digit(pk.key(__ldcg(&a.c_hi[i]), __ldcg(&a.c_id[i])));
-        atomicAdd(&sm.u.hist[d], 1u);
+        atomicAdd(&sm.u.hist.c[d], 1u);
+        atomicAdd(&sm.u.hist.l[d], static_cast<unsigned long long>(__ldcg(&a.c_len[i])));
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kPBins; b += kPT) {
-        const unsigned int c = sm.u.hist[b];
-        if (c) atomicAdd(&a.hist[b], c);
+        const unsigned int c = sm.u.hist.c[b];
+        if (c) {
+            atomicAdd(&a.hist[b], c);
+            atomicAdd(&a.hist_len[b], sm.u.hist.l[b]);
+        }
     }
 }
 
 // ---- phase 3: bucket offsets, scatter -------------------------------------------------
 __device__ __forceinline__ void pf_scatter(const PfArgs& a, const Packer& pk, unsigned long long n, PfSmem& sm) {
     unsigned int v[kPer], s = 0;
+    unsigned long long vl[kPer], sl = 0;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
         v[j] = __ldcg(&a.hist[threadIdx.x * kPer + j]);
+        vl[j] = __ldcg(&a.hist_len[threadIdx.x * kPer + j]);
         s += v[j];
+        sl += vl[j];
     }
     unsigned int ex;
     cub::BlockScan<unsigned int, kPT>(sm.u.scan).ExclusiveSum(s, ex);
+    unsigned long long exl = 0;
+    if (blockIdx.x == 0) {
+        __syncthreads();
+        cub::BlockScan<unsigned long long, kPT>(sm.u.scan64).ExclusiveSum(sl, exl);
+    }
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
         const int d = threadIdx.x * kPer + j;
         sm.off[d] = ex;
         if (blockIdx.x == 0) {
             a.seg_off[d] = ex;
+            a.seg_lpre[d] = exl;
             if (v[j] > 32u) {
                 const unsigned int q = atomicAdd(&a.ps->n_big, 1u);
-                a.big[2 * q] = ex;
-                a.big[2 * q + 1] = v[j];
+                a.big[3 * q] = static_cast<unsigned int>(d);
+                a.big[3 * q + 1] = ex;
+                a.big[3 * q + 2] = v[j];
             }
         }
         ex += v[j];
+        exl += vl[j];
     }
     __syncthreads();
     const unsigned long long nthr = static_cast<unsigned long long>(gridDim.x) * kPT;
@@ -304,11 +340,12 @@ __device__ __forceinline__ void pf_scatter(const PfArgs& a, const Packer& pk, un
         const unsigned long long i = base + threadIdx.x;
         const bool in = i < n;
         unsigned long long hi = 0, key = 0;
-        unsigned int id = 0;
+        unsigned int id = 0, ln = 0;
         int d = -1;
         if (in) {
             hi = __ldcg(&a.c_hi[i]);
             id = __ldcg(&a.c_id[i]);
+            ln = __ldcg(&a.c_len[i]);
             key = pk.key(hi, id);
             d = static_cast<int>(pk.digit(key));
         }
@@ -322,13 +359,34 @@ __device__ __forceinline__ void pf_scatter(const PfArgs& a, const Packer& pk, un
             a.b_key[pos] = key;
             a.b_hi[pos] = hi;
             a.b_id[pos] = id;
+            a.b_len[pos] = ln;
         }
+    }
+}
+
+// a ranked candidate: its sorted position and the tokens of the candidates
+// before it.  The plan arrays are written here; a candidate whose running
+// total fits the budget is selected (no candidate before it was skipped), the
+// first one past it is recorded for the greedy tail.
+__device__ __forceinline__ void pf_place(const PfArgs& a, unsigned int pos, unsigned int id, unsigned long long hi,
+                                         unsigned int ln, unsigned long long before) {
+    a.s_id[pos] = static_cast<int>(id);
+    a.s_len[pos] = static_cast<int>(ln);
+    a.h_cand[pos] = static_cast<int>(id);
+    a.h_val[pos] = dec_value(hi);
+    atomicMin(&a.chunk_min[pos >> 5], static_cast<int>(ln));
+    const long long b = static_cast<long long>(before), e = b + static_cast<long long>(ln);
+    if (e <= a.budget) {
+        a.h_sel[pos] = static_cast<int>(id);
+    } else if (b <= a.budget) {
+        a.ps->f = pos;
+        a.ps->tok_f = b;
     }
 }
 
 // ---- phase 4: rank every bucket -------------------------------------------------------
 __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSmem& sm) {
-    // buckets of 2..32: one warp each; singletons copied
+    // buckets of 1..32: one warp each (rank and token prefix by shuffles)
     const int lane = threadIdx.x & 31;
     const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(kPT) + threadIdx.x) >> 5);
     const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(kPT)) >> 5);
@@ -336,24 +394,29 @@ __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSme
         const unsigned int cnt = __ldcg(&a.hist[d]);
         if (cnt == 0u || cnt > 32u) continue;
         const unsigned int off = __ldcg(&a.seg_off[d]);
+        const unsigned long long lpre = __ldcg(&a.seg_lpre[d]);
         const bool in = static_cast<unsigned int>(lane) < cnt;
         const unsigned long long k = in ? __ldcg(&a.b_key[off + lane]) : 0ull;
         const unsigned int id = in ? __ldcg(&a.b_id[off + lane]) : 0u;
+        const unsigned int ln = in ? __ldcg(&a.b_len[off + lane]) : 0u;
         unsigned int r = 0;
+        unsigned long long before = 0;
         for (unsigned int j = 0; j < cnt; ++j) {
             const unsigned long long kj = __shfl_sync(0xffffffffu, k, j);
             const unsigned int ij = __shfl_sync(0xffffffffu, id, j);
-            r += pf_less(pk.packed, kj, ij, k, id) ? 1u : 0u;
+            const unsigned int lj = __shfl_sync(0xffffffffu, ln, j);
+            if (pf_less(pk.packed, kj, ij, k, id)) {
+                ++r;
+                before += lj;
+            }
         }
-        if (in) {
-            a.s_id[off + r] = static_cast<int>(id);
-            a.s_hi[off + r] = __ldcg(&a.b_hi[off + lane]);
-        }
+        if (in) pf_place(a, off + r, id, __ldcg(&a.b_hi[off + lane]), ln, lpre + before);
     }
-    // larger buckets: rank = number of smaller keys, counted from shared-memory
-    // tiles by 8 threads per element.  Tasks are (bucket, 64-element chunk);
-    // the first task of every bucket comes from a block scan of the chunk
-    // counts (sm.off, free after the scatter), task t -> CTA t % grid.
+    // larger buckets: rank = number of smaller keys, token prefix = their
+    // lengths, counted from shared-memory tiles by 8 threads per element.
+    // Tasks are (bucket, 64-element chunk); the first task of every bucket
+    // comes from a block scan of the chunk counts (sm.off, free after the
+    // scatter), task t -> CTA t % grid.
     if (threadIdx.x == 0) sm.bc[0] = __ldcg(&a.ps->n_big);
     __syncthreads();
     const unsigned int n_big = static_cast<unsigned int>(sm.bc[0]);
@@ -363,7 +426,7 @@ __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSme
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             const unsigned int b = threadIdx.x * kPer + j;
-            v[j] = b < n_big ? (__ldcg(&a.big[2 * b + 1]) + kChunk - 1) / kChunk : 0u;
+            v[j] = b < n_big ? (__ldcg(&a.big[3 * b + 2]) + kChunk - 1) / kChunk : 0u;
             s += v[j];
         }
         unsigned int ex, tot;
@@ -387,12 +450,13 @@ __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSme
             else hi = mid - 1;
         }
         const unsigned int b = lo, c = t - sm.off[b];
-        const unsigned int off = __ldcg(&a.big[2 * b]), cnt = __ldcg(&a.big[2 * b + 1]);
+        const unsigned int dg = __ldcg(&a.big[3 * b]), off = __ldcg(&a.big[3 * b + 1]), cnt = __ldcg(&a.big[3 * b + 2]);
         const unsigned int e = c * kChunk + threadIdx.x / 8, part = threadIdx.x % 8;
         const bool in = e < cnt;
         const unsigned long long mk = in ? __ldcg(&a.b_key[off + e]) : 0ull;
         const unsigned int mi = in ? __ldcg(&a.b_id[off + e]) : 0u;
         unsigned int r = 0;
+        unsigned long long before = 0;
         for (unsigned int t0 = 0; t0 < cnt; t0 += kTile) {
             const unsigned int tn = min(static_cast<unsigned int>(kTile), cnt - t0);
             if (!(t0 == 0 && held == b)) {
@@ -400,6 +464,7 @@ __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSme
                 for (unsigned int q = threadIdx.x; q < tn; q += kPT) {
                     sm.u.tile.k[q] = __ldcg(&a.b_key[off + t0 + q]);
                     sm.u.tile.id[q] = __ldcg(&a.b_id[off + t0 + q]);
+                    sm.u.tile.len[q] = __ldcg(&a.b_len[off + t0 + q]);
                 }
                 __syncthreads();
                 held = t0 == 0 ? b : ~0u;
@@ -407,33 +472,77 @@ __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSme
             if (in) {
                 if (pk.packed) {
 #pragma unroll 4
-                    for (unsigned int q = part; q < tn; q += 8) r += sm.u.tile.k[q] < mk ? 1u : 0u;
+                    for (unsigned int q = part; q < tn; q += 8) {
+                        const bool lt = sm.u.tile.k[q] < mk;
+                        r += lt ? 1u : 0u;
+                        before += lt ? sm.u.tile.len[q] : 0u;
+                    }
                 } else {
-                    for (unsigned int q = part; q < tn; q += 8)
-                        r += pf_less(false, sm.u.tile.k[q], sm.u.tile.id[q], mk, mi) ? 1u : 0u;
+                    for (unsigned int q = part; q < tn; q += 8) {
+                        const bool lt = pf_less(false, sm.u.tile.k[q], sm.u.tile.id[q], mk, mi);
+                        r += lt ? 1u : 0u;
+                        before += lt ? sm.u.tile.len[q] : 0u;
+                    }
                 }
             }
         }
-        r += __shfl_xor_sync(0xffffffffu, r, 1);
-        r += __shfl_xor_sync(0xffffffffu, r, 2);
-        r += __shfl_xor_sync(0xffffffffu, r, 4);
-        if (in && part == 0) {
-            a.s_id[off + r] = static_cast<int>(mi);
-            a.s_hi[off + r] = __ldcg(&a.b_hi[off + e]);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+            before += __shfl_xor_sync(0xffffffffu, before, o);
         }
+        if (in && part == 0)
+            pf_place(a, off + r, mi, __ldcg(&a.b_hi[off + e]), __ldcg(&a.b_len[off + e]),
+                     __ldcg(&a.seg_lpre[dg]) + before);
     }
 }
 
-// ---- phase 5: greedy fill (one warp) and the plan to the host --------------------------
-__device__ __forceinline__ void pf_greedy(const PfArgs& a, unsigned long long n) {
+// ---- phase 5: the greedy tail (one warp) ------------------------------------------------
+// From the first candidate past the all-fitting prefix (skipped: it
+// overflows), with the remaining budget: chunks of 32 sorted candidates whose
+// shortest length exceeds the budget are skipped 32 chunks per step; inside a
+// chunk a prefix sum takes every lane that still fits, the first that does
+// not is skipped (policies.hpp:203-210).
+__device__ __forceinline__ void pf_greedy_tail(const PfArgs& a, unsigned long long n) {
     const int lane = threadIdx.x & 31;
-    long long rem = a.budget, nsel = 0, tok = 0;
+    const unsigned long long f = __ldcg(&a.ps->f);
+    long long nsel, tok;
+    if (f < n) {
+        nsel = static_cast<long long>(f);
+        tok = __ldcg(&a.ps->tok_f);
+    } else if (a.budget >= 0) {  // every candidate fits
+        nsel = static_cast<long long>(n);
+        tok = 0;
+        for (unsigned long long i = lane; i < n; i += 32) tok += __ldcg(&a.s_len[i]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tok += __shfl_xor_sync(0xffffffffu, tok, o);
+    } else {
+        nsel = 0;
+        tok = 0;
+    }
+    long long rem = a.budget - tok;
     const long long min_len = __ldcg(&a.ps->min_len);
-    for (unsigned long long base = 0; base < n && rem >= min_len; base += 32) {
-        const unsigned long long i = base + lane;
-        const bool in = i < n;
+    unsigned long long c = f < n ? (f + 1) >> 5 : (n + 31) >> 5;
+    unsigned int first = f < n ? static_cast<unsigned int>((f + 1) & 31u) : 0u;
+    const unsigned long long n_chunks = (n + 31) >> 5;
+    while (c < n_chunks && rem >= min_len) {
+        // the next chunk that can hold a candidate of length <= rem
+        const unsigned long long cc = c + lane;
+        const int cm = cc < n_chunks ? __ldcg(&a.chunk_min[cc]) : 0;
+        const unsigned m = __ballot_sync(0xffffffffu, cc >= n_chunks || cm <= rem);
+        if (!m) {
+            c += 32;
+            first = 0;
+            continue;
+        }
+        const int s = __ffs(m) - 1;
+        if (s) first = 0;
+        c += s;
+        if (c >= n_chunks) break;
+        const unsigned long long i = c * 32 + lane;
+        const bool in = i < n && static_cast<unsigned int>(lane) >= first;
         const int id = in ? __ldcg(&a.s_id[i]) : 0;
-        const long long l = in ? static_cast<long long>(a.len[id]) : 0;
+        const long long l = in ? __ldcg(&a.s_len[i]) : 0;
         unsigned todo = __ballot_sync(0xffffffffu, in);
         while (todo) {
             // a lane longer than the remaining budget is skipped for good
@@ -457,8 +566,11 @@ __device__ __forceinline__ void pf_greedy(const PfArgs& a, unsigned long long n)
             todo &= ~fm;
             if (todo) todo &= todo - 1u;  // the first lane past them does not fit: skipped
         }
+        ++c;
+        first = 0;
     }
     if (lane == 0) {
+        a.h_ctr[0] = static_cast<long long>(n);
         a.h_ctr[1] = nsel;
         a.h_ctr[2] = tok;
     }
@@ -495,18 +607,7 @@ __global__ void __launch_bounds__(kPT, 2) prefetch_plan_kernel(PfArgs a) {
     grid.sync();
     pf_sort(a, pk, sm);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-        pf_greedy(a, n);
-        if (threadIdx.x == 0) a.h_ctr[0] = static_cast<long long>(n);
-        return;
-    }
-    // the sorted candidates and their values into pinned host memory
-    const long long t = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x - 32;
-    const long long nt = static_cast<long long>(gridDim.x) * kPT - 32;
-    for (long long i = t; i < static_cast<long long>(n); i += nt) {
-        a.h_cand[i] = __ldcg(&a.s_id[i]);
-        a.h_val[i] = dec_value(__ldcg(&a.s_hi[i]));
-    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) pf_greedy_tail(a, n);
 }
 
 int plan_grid(Context& c, std::int64_t n_nodes) {
@@ -536,13 +637,17 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     const std::size_t n = static_cast<std::size_t>(c.n) + 1;
     c.pf_hi.reserve(n);
     c.pf_id.reserve(n);
+    c.pf_len.reserve(n);
     c.pf_bkey.reserve(n);
     c.pf_bhi.reserve(n);
     c.pf_bid.reserve(n);
-    c.pf_shi.reserve(n);
+    c.pf_blen.reserve(n);
     c.pf_sid.reserve(n);
+    c.pf_slen.reserve(n);
+    c.pf_cmin.reserve((n >> 5) + 2);
     c.pf_hist.reserve(3 * kPBins);
-    c.pf_big.reserve(2 * kPBins);
+    c.pf_hlen.reserve(2 * kPBins);
+    c.pf_big.reserve(3 * kPBins);
     c.pf_state.reserve(sizeof(PfState));
     const std::size_t b_ctr = 4 * sizeof(long long), b_ids = ((n * 4 + 15) & ~std::size_t(15));
     const std::size_t b_val = n * 8;
@@ -558,14 +663,19 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     a.budget = budget;
     a.c_hi = c.pf_hi.p;
     a.c_id = c.pf_id.p;
+    a.c_len = c.pf_len.p;
     a.b_key = c.pf_bkey.p;
     a.b_hi = c.pf_bhi.p;
     a.b_id = c.pf_bid.p;
-    a.s_hi = c.pf_shi.p;
+    a.b_len = c.pf_blen.p;
     a.s_id = c.pf_sid.p;
+    a.s_len = c.pf_slen.p;
+    a.chunk_min = c.pf_cmin.p;
     a.hist = c.pf_hist.p;
     a.cursor = c.pf_hist.p + kPBins;
     a.seg_off = c.pf_hist.p + 2 * kPBins;
+    a.hist_len = c.pf_hlen.p;
+    a.seg_lpre = c.pf_hlen.p + kPBins;
     a.big = c.pf_big.p;
     a.ps = reinterpret_cast<PfState*>(c.pf_state.p);
     a.st = c.status.p;
@@ -578,7 +688,7 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     if (!init) {
         c.hplan_init.reserve(sizeof(PfState));
         init = reinterpret_cast<PfState*>(c.hplan_init.p);
-        *init = PfState{0, 0, ~0ull, 0u, ~0u, INT_MAX, 0u};
+        *init = PfState{0, 0, ~0ull, 0u, ~0u, INT_MAX, 0u, ~0ull, 0};
     }
     PBKV_CUDA(cudaMemcpyAsync(a.ps, init, sizeof(PfState), cudaMemcpyHostToDevice, c.stream));
     void* args[] = {&a};
