@@ -289,6 +289,11 @@ struct Context {
     DevBuf<ulonglong2> listSK;
     DevBuf<unsigned int> listSC, listSC2;
     DevBuf<unsigned int> big;  // [2 * n]: (offset, count) of buckets sorted by rank counting
+    // small-cut path (select.cu): node sample, low list, histogram tables
+    DevBuf<unsigned char> samp;
+    DevBuf<int> low;
+    DevBuf<unsigned int> small_u32;
+    DevBuf<unsigned long long> small_u64;
     DevBuf<unsigned long long> hist_w, part_w;
     DevBuf<unsigned int> hist_c, part_c, seg_off, seg_cnt, cursor;
     std::vector<unsigned long long> phase_ns;  // select-kernel phase timestamps of the last call
@@ -303,7 +308,7 @@ struct Context {
     DevBuf<int> ids, ids2, ids3;
     DevBuf<double> vals;
     // stage 4 scratch (prefetch.cu)
-    DevBuf<unsigned long long> pf_hi, pf_bkey, pf_bhi, pf_hlen;
+    DevBuf<unsigned long long> pf_hi, pf_bkey, pf_bhi, pf_hlen, pf_shi;
     DevBuf<unsigned int> pf_id, pf_len, pf_bid, pf_blen, pf_hist, pf_big;
     DevBuf<int> pf_sid, pf_slen, pf_cmin;
     DevBuf<unsigned char> pf_state;

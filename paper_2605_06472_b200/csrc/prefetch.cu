@@ -25,6 +25,9 @@
 //      straight into pinned host memory by the kernel.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -52,7 +55,17 @@ struct PfState {
     unsigned int n_big;
     unsigned long long f;      // sorted position of the first candidate overflowing the budget
     long long tok_f;           // tokens of the candidates before it (all selected)
+    long long tot_len;         // tokens of all candidates
+    unsigned long long ts[8];  // %globaltimer after each phase (CTA 0; diagnostics)
 };
+
+__device__ __forceinline__ void pf_stamp(PfState* ps, int i) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ps->ts[i] = t;
+    }
+}
 
 struct PfArgs {
     ScoreArgs s;
@@ -69,8 +82,9 @@ struct PfArgs {
     unsigned long long* b_hi;
     unsigned int* b_id;
     unsigned int* b_len;
-    int* s_id;  // sorted ids and lengths (the greedy tail)
+    int* s_id;  // sorted ids, lengths and keys
     int* s_len;
+    unsigned long long* s_hi;
     int* chunk_min;  // shortest length of every 32 sorted candidates
     unsigned int* hist;     // [kPBins] counts
     unsigned long long* hist_len;  // [kPBins] token sums
@@ -99,6 +113,7 @@ struct PfSmem {
         } tile;
         typename cub::BlockScan<unsigned int, kPT>::TempStorage scan;
         typename cub::BlockScan<unsigned long long, kPT>::TempStorage scan64;
+        int queue[kPT / 32][512];  // phase 1: host-tier nodes per warp
     } u;
     unsigned int off[kPBins];
     unsigned long long red[32];
@@ -196,6 +211,46 @@ __device__ __forceinline__ T block_all(T v, Op op, unsigned long long* sh) {
 }
 
 // ---- phase 1: candidates ------------------------------------------------------------
+// Every thread reads the tier bytes of 16 consecutive nodes in one 16-byte
+// load; the host-tier ones (a few percent) are queued per warp in shared
+// memory and then evaluated 32 at a time, one per lane (parent tier, Eq. 1):
+// the scan costs one coalesced load per 16 nodes, the per-candidate chains of
+// dependent loads run on full warps.
+__device__ __forceinline__ void pf_eval(const PfArgs& a, int n, bool valid, unsigned long long& or_hi,
+                                        unsigned long long& and_hi, unsigned int& or_id, unsigned int& and_id,
+                                        int& min_len) {
+    bool take = false;
+    double v = 0.0;
+    if (valid) {
+        const int p = a.parent[n];
+        const uint2 rg = a.s.acc_rng[n];
+        if ((a.flags[p] & kFlagTierMask) == PBKV_TIER_DEVICE) {
+            bool miss = false;
+            v = eq1(a.s, rg.x, rg.y, &miss);
+            if (miss) {
+                atomicCAS(&a.st->code, 0, PBKV_EINVAL);
+                atomicCAS(&a.st->kind, 0, kErrMissingForecast);
+                atomicMin(reinterpret_cast<unsigned long long*>(&a.st->aux), a.last[n]);
+            } else {
+                take = v > 0.0;  // policies.hpp:196
+            }
+        }
+    }
+    const long long slot = warp_append(&a.ps->n_cand, take);
+    if (take) {
+        const unsigned long long hi = ~enc_rank(v);
+        const int ln = a.len[n];
+        a.c_hi[slot] = hi;
+        a.c_id[slot] = static_cast<unsigned int>(n);
+        a.c_len[slot] = static_cast<unsigned int>(ln);
+        or_hi |= hi;
+        and_hi &= hi;
+        or_id |= static_cast<unsigned int>(n);
+        and_id &= static_cast<unsigned int>(n);
+        min_len = min(min_len, ln);
+    }
+}
+
 __device__ __forceinline__ void pf_candidates(const PfArgs& a, PfSmem& sm) {
     const long long tid = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x;
     const long long nthr = static_cast<long long>(gridDim.x) * kPT;
@@ -208,35 +263,43 @@ __device__ __forceinline__ void pf_candidates(const PfArgs& a, PfSmem& sm) {
     unsigned long long or_hi = 0, and_hi = ~0ull;
     unsigned int or_id = 0, and_id = ~0u;
     int min_len = INT_MAX;
-    for (long long base = blockIdx.x * static_cast<long long>(kPT); base < a.n_nodes; base += nthr) {
-        const long long i = base + threadIdx.x;
-        const int n = static_cast<int>(i);
-        bool take = false;
-        double v = 0.0;
-        if (i < a.n_nodes && host_candidate(a, n)) {
-            const uint2 rg = a.s.acc_rng[n];
-            bool miss = false;
-            v = eq1(a.s, rg.x, rg.y, &miss);
-            if (miss) {
-                atomicCAS(&a.st->code, 0, PBKV_EINVAL);
-                atomicCAS(&a.st->kind, 0, kErrMissingForecast);
-                atomicMin(reinterpret_cast<unsigned long long*>(&a.st->aux), a.last[n]);
-            } else {
-                take = v > 0.0;  // policies.hpp:196
-            }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int* q = sm.u.queue[warp];
+    for (long long base = blockIdx.x * static_cast<long long>(kPT) * 16; base < a.n_nodes; base += nthr * 16) {
+        const long long i0 = base + threadIdx.x * 16ll;
+        unsigned int hm = 0;  // host-tier bytes of this thread's 16 nodes
+        if (i0 + 16 <= a.n_nodes) {
+            const uint4 f = __ldg(reinterpret_cast<const uint4*>(a.flags + i0));
+            const unsigned int w[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+                hm |= (((w[b >> 2] >> (8 * (b & 3))) & kFlagTierMask) == PBKV_TIER_HOST ? 1u : 0u) << b;
+        } else {
+            for (int b = 0; b < 16; ++b)
+                if (i0 + b < a.n_nodes && (a.flags[i0 + b] & kFlagTierMask) == PBKV_TIER_HOST) hm |= 1u << b;
         }
-        const long long slot = warp_append(&a.ps->n_cand, take);
-        if (take) {
-            const unsigned long long hi = ~enc_rank(v);
-            a.c_hi[slot] = hi;
-            a.c_id[slot] = static_cast<unsigned int>(n);
-            a.c_len[slot] = static_cast<unsigned int>(a.len[n]);
-            or_hi |= hi;
-            and_hi &= hi;
-            or_id |= static_cast<unsigned int>(n);
-            and_id &= static_cast<unsigned int>(n);
-            min_len = min(min_len, a.len[n]);
+        if (i0 == 0) hm &= ~1u;  // the root is never a candidate
+        // warp-wide queue of the host nodes (<= 512)
+        const unsigned int cnt = __popc(hm);
+        unsigned int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
+        const unsigned int total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned int at = incl - cnt;
+        while (hm) {
+            const int b = __ffs(hm) - 1;
+            hm &= hm - 1;
+            q[at++] = static_cast<int>(i0 + b);
+        }
+        __syncwarp();
+        for (unsigned int k = 0; k < total; k += 32) {
+            const bool valid = k + lane < total;
+            pf_eval(a, valid ? q[k + lane] : 0, valid, or_hi, and_hi, or_id, and_id, min_len);
+        }
+        __syncwarp();
     }
     struct Or {
         __device__ unsigned long long operator()(unsigned long long x, unsigned long long y) const { return x | y; }
@@ -315,7 +378,9 @@ __device__ __forceinline__ void pf_scatter(const PfArgs& a, const Packer& pk, un
     unsigned long long exl = 0;
     if (blockIdx.x == 0) {
         __syncthreads();
-        cub::BlockScan<unsigned long long, kPT>(sm.u.scan64).ExclusiveSum(sl, exl);
+        unsigned long long tl;
+        cub::BlockScan<unsigned long long, kPT>(sm.u.scan64).ExclusiveSum(sl, exl, tl);
+        if (threadIdx.x == 0) a.ps->tot_len = static_cast<long long>(tl);
     }
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -372,13 +437,10 @@ __device__ __forceinline__ void pf_place(const PfArgs& a, unsigned int pos, unsi
                                          unsigned int ln, unsigned long long before) {
     a.s_id[pos] = static_cast<int>(id);
     a.s_len[pos] = static_cast<int>(ln);
-    a.h_cand[pos] = static_cast<int>(id);
-    a.h_val[pos] = dec_value(hi);
+    a.s_hi[pos] = hi;
     atomicMin(&a.chunk_min[pos >> 5], static_cast<int>(ln));
     const long long b = static_cast<long long>(before), e = b + static_cast<long long>(ln);
-    if (e <= a.budget) {
-        a.h_sel[pos] = static_cast<int>(id);
-    } else if (b <= a.budget) {
+    if (e > a.budget && b <= a.budget) {
         a.ps->f = pos;
         a.ps->tok_f = b;
     }
@@ -512,10 +574,7 @@ __device__ __forceinline__ void pf_greedy_tail(const PfArgs& a, unsigned long lo
         tok = __ldcg(&a.ps->tok_f);
     } else if (a.budget >= 0) {  // every candidate fits
         nsel = static_cast<long long>(n);
-        tok = 0;
-        for (unsigned long long i = lane; i < n; i += 32) tok += __ldcg(&a.s_len[i]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) tok += __shfl_xor_sync(0xffffffffu, tok, o);
+        tok = __ldcg(&a.ps->tot_len);
     } else {
         nsel = 0;
         tok = 0;
@@ -580,8 +639,10 @@ __global__ void __launch_bounds__(kPT, 2) prefetch_plan_kernel(PfArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PfSmem& sm = *reinterpret_cast<PfSmem*>(smem_raw);
     cg::grid_group grid = cg::this_grid();
+    pf_stamp(a.ps, 0);
     pf_candidates(a, sm);
     grid.sync();
+    pf_stamp(a.ps, 1);
     if (threadIdx.x == 0) {
         sm.bc[0] = static_cast<unsigned long long>(__ldcg(&a.st->code));
         sm.bc[1] = __ldcg(&a.ps->n_cand);
@@ -603,11 +664,43 @@ __global__ void __launch_bounds__(kPT, 2) prefetch_plan_kernel(PfArgs a) {
     pk.init(a.ps);
     pf_hist(a, pk, n, sm);
     grid.sync();
+    pf_stamp(a.ps, 2);
     pf_scatter(a, pk, n, sm);
     grid.sync();
+    pf_stamp(a.ps, 3);
     pf_sort(a, pk, sm);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x < 32) pf_greedy_tail(a, n);
+    pf_stamp(a.ps, 4);
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        pf_greedy_tail(a, n);
+        pf_stamp(a.ps, 5);
+        return;
+    }
+    // the sorted plan into pinned host memory with 16-byte stores: ids,
+    // values, and the all-fitting prefix of the selection (= the first f ids)
+    const long long t = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x - 32;
+    const long long nt = static_cast<long long>(gridDim.x) * kPT - 32;
+    const long long nn = static_cast<long long>(n);
+    const unsigned long long f = __ldcg(&a.ps->f);
+    const long long nf = f < n ? static_cast<long long>(f) : (a.budget >= 0 ? nn : 0);
+    for (long long i = t; i < (nn >> 2); i += nt) {
+        const int4 v = __ldcg(reinterpret_cast<const int4*>(a.s_id) + i);
+        reinterpret_cast<int4*>(a.h_cand)[i] = v;
+    }
+    for (long long i = t; i < (nn >> 1); i += nt) {
+        const ulonglong2 h = __ldcg(reinterpret_cast<const ulonglong2*>(a.s_hi) + i);
+        reinterpret_cast<double2*>(a.h_val)[i] = make_double2(dec_value(h.x), dec_value(h.y));
+    }
+    for (long long i = t; i < (nf >> 2); i += nt) {
+        const int4 v = __ldcg(reinterpret_cast<const int4*>(a.s_id) + i);
+        reinterpret_cast<int4*>(a.h_sel)[i] = v;
+    }
+    if (t < 4) {  // the ragged ends
+        const long long ic = (nn & ~3ll) + t, iv = (nn & ~1ll) + t, is = (nf & ~3ll) + t;
+        if (ic < nn) a.h_cand[ic] = __ldcg(&a.s_id[ic]);
+        if (t < 2 && iv < nn) a.h_val[iv] = dec_value(__ldcg(&a.s_hi[iv]));
+        if (is < nf) a.h_sel[is] = __ldcg(&a.s_id[is]);
+    }
 }
 
 int plan_grid(Context& c, std::int64_t n_nodes) {
@@ -644,6 +737,7 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     c.pf_blen.reserve(n);
     c.pf_sid.reserve(n);
     c.pf_slen.reserve(n);
+    c.pf_shi.reserve(n);
     c.pf_cmin.reserve((n >> 5) + 2);
     c.pf_hist.reserve(3 * kPBins);
     c.pf_hlen.reserve(2 * kPBins);
@@ -670,6 +764,7 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     a.b_len = c.pf_blen.p;
     a.s_id = c.pf_sid.p;
     a.s_len = c.pf_slen.p;
+    a.s_hi = c.pf_shi.p;
     a.chunk_min = c.pf_cmin.p;
     a.hist = c.pf_hist.p;
     a.cursor = c.pf_hist.p + kPBins;
@@ -688,7 +783,7 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     if (!init) {
         c.hplan_init.reserve(sizeof(PfState));
         init = reinterpret_cast<PfState*>(c.hplan_init.p);
-        *init = PfState{0, 0, ~0ull, 0u, ~0u, INT_MAX, 0u, ~0ull, 0};
+        *init = PfState{0, 0, ~0ull, 0u, ~0u, INT_MAX, 0u, ~0ull, 0, 0, {}};
     }
     PBKV_CUDA(cudaMemcpyAsync(a.ps, init, sizeof(PfState), cudaMemcpyHostToDevice, c.stream));
     void* args[] = {&a};
@@ -702,6 +797,14 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     ++c.launches;
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
     if (a.h_ctr[3]) check_status(c);  // the error path: the full status word
+    if (std::getenv("PBKV_DEBUG_PLAN")) {
+        PfState h{};
+        PBKV_CUDA(cudaMemcpy(&h, a.ps, sizeof h, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[pbkv plan] grid=%d n_cand=%llu n_big=%u f=%llu min_len=%d us: cand %.1f hist %.1f "
+                     "scatter %.1f sort %.1f tail %.1f\n", plan_grid(c, c.n), h.n_cand, h.n_big, h.f, h.min_len,
+                     (h.ts[1] - h.ts[0]) * 1e-3, (h.ts[2] - h.ts[1]) * 1e-3, (h.ts[3] - h.ts[2]) * 1e-3,
+                     (h.ts[4] - h.ts[3]) * 1e-3, (h.ts[5] - h.ts[4]) * 1e-3);
+    }
     out->ctr = a.h_ctr;
     out->cand = a.h_cand;
     out->val = a.h_val;

@@ -51,6 +51,10 @@ constexpr int kBins = 1 << kDigitBits;
 constexpr int kMaxPasses = 16;
 constexpr int kBucketCap = 4096;  // bucket sorted by one CTA in shared memory
 constexpr int kScanIPT = 8;       // chain-start scan: items per thread per chunk
+// small-cut path: a node sample bounds the cut from above
+constexpr int kSamp = 2048;            // sample records (the eff phase appends ~1024)
+constexpr unsigned int kSampTarget = 1024;
+constexpr long long kSmallMax = 1 << 18;  // estimated heads below the bound for the small path
 
 unsigned int grid_cap(std::int64_t n, int block) {
     std::int64_t want = (n + block - 1) / block;
@@ -83,6 +87,11 @@ struct SelState {
     int cut_head, max_bucket;
     unsigned long long n_victims, freed;
     int shortfall, n_ts;
+    unsigned int n_samp;        // sample records appended by the eff phase
+    int path;                   // 0 full radix path, 1 small-cut path, 2 small path abandoned
+    unsigned long long n_low;   // heads at or below the sample bound
+    unsigned long long or_low[3], and_low[3];
+    unsigned long long est_low; // the sample's estimate of n_low (diagnostics)
     unsigned long long ts[40];  // %globaltimer after each phase (diagnostics)
     unsigned long long dbg[8];  // per-CTA maxima of phase work (diagnostics)
 };
@@ -227,6 +236,21 @@ __device__ __forceinline__ unsigned long long pack_key(const Key2& k, int id, un
     return r;
 }
 
+// one sampled eligible node (eff phase): key, id, token length
+struct SampRec {
+    unsigned long long w0, w1;
+    int id, len;
+};
+
+__device__ __forceinline__ unsigned int mix32(unsigned int x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
 struct SelArgs {
     const int* parent;
     const int* len;
@@ -273,6 +297,18 @@ struct SelArgs {
     HeavyReport* rep_out;   // pinned host memory
     const double* approx;
     double* approx_out;     // pinned host memory
+    // small-cut path
+    SampRec* samp;          // [kSamp]
+    unsigned int samp_mask; // node n is sampled when hash(n) & mask == 0
+    int* low;               // heads at or below the bound
+    unsigned int* sm_c;     // [kBins] counts, cursors, bucket offsets, big list [2*kBins]
+    unsigned int* sm_cur;
+    unsigned int* sm_off;
+    unsigned int* sm_big;
+    unsigned long long* sm_w;   // [kBins] weights, chain sizes, and their bucket prefixes
+    unsigned long long* sm_cs;
+    unsigned long long* sm_wpre;
+    unsigned long long* sm_cpre;
 };
 
 // record of heavy node j: max over its in-order device children's eff (the
@@ -378,6 +414,12 @@ __device__ __forceinline__ void phase_lock(const SelArgs& a, std::int64_t tid, s
         a.hist_w[j] = 0;
         a.hist_c[j] = 0;
     }
+    for (std::int64_t j = tid; j < kBins; j += nthr) {
+        a.sm_c[j] = 0;
+        a.sm_cur[j] = 0;
+        a.sm_w[j] = 0;
+        a.sm_cs[j] = 0;
+    }
 }
 
 // eff: every device node walks its key up the ancestor chain, CAS-ing the
@@ -406,6 +448,11 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         for (int j = 0; j < kWalk; ++j) {
             const std::int64_t i = base + j * nthr;
             act[j] = i < a.n_nodes && n[j] != 0 && (fn[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
+            // the node sample of the small-cut bound: its own key and length
+            if (act[j] && !(fn[j] & kFlagOutOfOrder) && (mix32(static_cast<unsigned int>(n[j])) & a.samp_mask) == 0u) {
+                const unsigned int q = atomicAdd(&a.ss->n_samp, 1u);
+                if (q < static_cast<unsigned int>(kSamp)) a.samp[q] = SampRec{km[j].w0, km[j].w1, n[j], a.len[n[j]]};
+            }
             // (out-of-order parents -- deferred heavy / spine -- are reduced
             // over their children lists instead: thousands of walkers CAS-ing
             // one hot word serialised in its L2 slice)
@@ -456,7 +503,7 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
 // heads (eligible n with eff(n) == n) walk their own chain -- the contiguous
 // eligible ancestors with the same eff -- for its token weight W and size C;
 // head list, eligible tokens, OR/AND of the head keys (first radix pass)
-__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh) {
+__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh, bool small, Key2 tk, int tid_) {
     // Every eligible node n belongs to the chain of eff(n) (the closed form
     // orders eligible nodes by (eff, d); the nodes sharing an eff form a
     // contiguous eligible ancestor path from it), so the chain weight W[h] and
@@ -466,11 +513,13 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     SelState* ss = a.ss;
     unsigned long long tok = 0;
     unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
+    unsigned long long orl[3] = {0, 0, 0}, andl[3] = {~0ull, ~0ull, ~0ull};
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
          base += kBatch * nthr) {
         int n[kBatch], e[kBatch], ln[kBatch];
-        bool elig[kBatch];
+        bool elig[kBatch], lw[kBatch];
+        Key2 kh[kBatch];
         std::uint8_t fl[kBatch], ms[kBatch];
         unsigned int cnt = 0;
         // every per-node field of the batch in one round trip (coalesced
@@ -503,6 +552,17 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             tok += l;
             cnt += e[j] == n[j] ? 1u : 0u;
         }
+        // head keys; heads at or below the small-cut bound (low list), counted
+        // in the upper half of the same scan word
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            lw[j] = false;
+            if (elig[j] && e[j] == n[j]) {
+                kh[j] = load_key(a.keys, n[j]);
+                lw[j] = small && !key_less(tk, tid_, kh[j], n[j]);
+                cnt += lw[j] ? 0x10000u : 0u;
+            }
+        }
         // CTA-wide exclusive offsets of the heads, one global atomic per CTA
         unsigned int* wcount = reinterpret_cast<unsigned int*>(sh);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -521,28 +581,39 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
                 wcount[w] = sum;
                 sum += c;
             }
-            sh[31] = sum ? atomicAdd(&ss->n_L[0], static_cast<unsigned long long>(sum)) : 0ull;
+            sh[31] = (sum & 0xffffu) ? atomicAdd(&ss->n_L[0], static_cast<unsigned long long>(sum & 0xffffu)) : 0ull;
+            sh[30] = (sum >> 16) ? atomicAdd(&ss->n_low, static_cast<unsigned long long>(sum >> 16)) : 0ull;
         }
         __syncthreads();
-        unsigned long long slot = sh[31] + wcount[warp] + (incl - cnt);
+        const unsigned int ex = wcount[warp] + (incl - cnt);
+        unsigned long long slot = sh[31] + (ex & 0xffffu);
+        unsigned long long lslot = sh[30] + (ex >> 16);
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             if (!elig[j] || e[j] != n[j]) continue;
             const int h = n[j];
-            a.rank[h] = -1;
             a.heads[slot++] = h;
-            const Key2 k = load_key(a.keys, h);
+            const Key2 k = kh[j];
             for (int wd = 0; wd < 3; ++wd) {
                 const unsigned long long x = key_word(k, h, wd);
                 or3[wd] |= x;
                 and3[wd] &= x;
+            }
+            if (lw[j]) {
+                a.low[lslot++] = h;
+                for (int wd = 0; wd < 3; ++wd) {
+                    const unsigned long long x = key_word(k, h, wd);
+                    orl[wd] |= x;
+                    andl[wd] &= x;
+                }
             }
         }
     }
     const unsigned long long blk = block_reduce_bits(tok, SumOp(), sh);
     if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
     flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
+    if (small) flush_orand(orl, andl, ss->or_low, ss->and_low, sh);
 }
 
 // per-CTA weight and count histograms of the next digit over the candidates
@@ -896,6 +967,7 @@ struct PersistSmem {
         struct {
             unsigned long long w[kBins];
             unsigned int c[kBins];
+            unsigned long long cs[kBins];  // small path: chain sizes per bucket
         } hist;
         typename cub::BlockScan<unsigned long long, kPThreads>::TempStorage scan;
         struct {
@@ -909,6 +981,401 @@ struct PersistSmem {
     unsigned long long bc[4];  // broadcast of shared scalars
     PickOut pick;
 };
+
+// ---- small-cut path ------------------------------------------------
+// A cut that takes a small share of the eligible tokens lies among the
+// lowest keys.  The eff phase samples ~1/R of the eligible nodes (key, len);
+// every CTA sorts that sample itself (identical result, no barrier) and picks
+// a bound T whose estimated weight below it -- R x the sampled tokens with key
+// <= T -- is twice `needed` plus a sampling margin.  The chains phase then
+// lists the heads with key <= T (the low list) next to the head list.  If the
+// low list's exact chain weight reaches `needed` (checked from its histogram)
+// the cut lies inside it, and the decision is: one 11-bit MSD histogram of
+// the low list, placement into buckets, every bucket ranked in place -- the
+// rank count also sums the chain weights W and sizes C of the smaller keys,
+// so with the per-bucket prefixes each head knows its cumulative token count
+// and its victim offset, and the head whose count crosses `needed` is the cut
+// -- then the chain scatter.  Otherwise (the sample missed; rare) the full
+// radix path below runs.  Results are identical either way.
+struct SmallBound {
+    Key2 k;
+    int id;
+    bool ok;
+};
+
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* sh,
+                                                              unsigned long long* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    unsigned long long pre = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+        const unsigned long long t = sh[w];
+        if (w < warp) pre += t;
+        tot += t;
+    }
+    __syncthreads();
+    *total = tot;
+    return pre + x - v;
+}
+
+__device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
+    SmallBound r{{0, 0}, -1, false};
+    if (threadIdx.x == 0) sm.bc[0] = __ldcg(&a.ss->n_samp);
+    __syncthreads();
+    const unsigned int ns = static_cast<unsigned int>(sm.bc[0]);
+    __syncthreads();
+    if (ns == 0 || ns > static_cast<unsigned int>(kSamp)) return r;
+    unsigned int p2 = 1;
+    while (p2 < ns) p2 <<= 1;
+    unsigned long long* k0 = sm.u.sort.k0;
+    unsigned long long* k1 = sm.u.sort.k1;
+    int* vid = sm.u.sort.val;
+    int* vlen = sm.u.sort.val + kSamp;
+    for (unsigned int i = threadIdx.x; i < p2; i += blockDim.x) {
+        if (i < ns) {
+            k0[i] = __ldcg(&a.samp[i].w0);
+            k1[i] = __ldcg(&a.samp[i].w1);
+            vid[i] = __ldcg(&a.samp[i].id);
+            vlen[i] = __ldcg(&a.samp[i].len);
+        } else {
+            k0[i] = ~0ull;
+            k1[i] = ~0ull;
+            vid[i] = -1;
+            vlen[i] = 0;
+        }
+    }
+    __syncthreads();
+    // bitonic sort by (w0, w1, id), padding last
+    for (unsigned int k = 2; k <= p2; k <<= 1) {
+        for (unsigned int j = k >> 1; j > 0; j >>= 1) {
+            for (unsigned int t = threadIdx.x; t < (p2 >> 1); t += blockDim.x) {
+                const unsigned int i = (t / j) * 2 * j + (t % j), l = i + j;
+                const bool up = (i & k) == 0;
+                const bool gt = sk_less(k0[l], k1[l], vid[l], k0[i], k1[i], vid[i]);
+                if (gt == up) {
+                    const unsigned long long a0 = k0[i], a1 = k1[i];
+                    const int av = vid[i], al = vlen[i];
+                    k0[i] = k0[l];
+                    k1[i] = k1[l];
+                    vid[i] = vid[l];
+                    vlen[i] = vlen[l];
+                    k0[l] = a0;
+                    k1[l] = a1;
+                    vid[l] = av;
+                    vlen[l] = al;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // running sampled tokens; the first sample whose estimate R x tokens
+    // reaches 2 x needed, moved up by a sampling margin of 3 sqrt(i) + 8
+    const unsigned long long R = static_cast<unsigned long long>(a.samp_mask) + 1ull;
+    const unsigned int per = (ns + blockDim.x - 1) / blockDim.x;
+    const unsigned int i0 = threadIdx.x * per;
+    unsigned long long loc = 0;
+    for (unsigned int i = i0; i < i0 + per && i < ns; ++i) loc += static_cast<unsigned long long>(vlen[i]);
+    unsigned long long tot;
+    unsigned long long run = block_excl_scan(loc, sm.sh, &tot);
+    if (threadIdx.x == 0) sm.bc[1] = ~0ull;
+    __syncthreads();
+    const unsigned long long target = 2ull * static_cast<unsigned long long>(a.needed);
+    for (unsigned int i = i0; i < i0 + per && i < ns; ++i) {
+        const unsigned long long prev = run;
+        run += static_cast<unsigned long long>(vlen[i]);
+        if (prev * R < target && run * R >= target) sm.bc[1] = i;  // unique
+    }
+    __syncthreads();
+    const unsigned long long first = sm.bc[1];
+    if (first != ~0ull) {
+        const unsigned long long m = first + 8ull + static_cast<unsigned long long>(3.0 * sqrt(static_cast<double>(first + 1)));
+        if (m < ns && (m + 1) * R <= static_cast<unsigned long long>(kSmallMax)) {
+            r.k = Key2{k0[m], k1[m]};
+            r.id = vid[m];
+            r.ok = true;
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.ss->est_low = (m + 1) * R;
+        }
+    }
+    __syncthreads();  // the sort buffers are reused by the phases that follow
+    return r;
+}
+
+// S1: histogram of the low list (count, chain weight, chain size per 11-bit digit)
+__device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long n_low, int lo, unsigned long long v0,
+                                           unsigned long long v1, unsigned long long v2, PersistSmem& sm) {
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+        sm.u.hist.w[b] = 0;
+        sm.u.hist.c[b] = 0;
+        sm.u.hist.cs[b] = 0;
+    }
+    __syncthreads();
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n_low;
+         i += stride) {
+        const int x = __ldcg(&a.low[i]);
+        const unsigned long long pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
+        const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kBins - 1);
+        atomicAdd(&sm.u.hist.w[d], __ldcg(&a.W[x]));
+        atomicAdd(&sm.u.hist.c[d], 1u);
+        atomicAdd(&sm.u.hist.cs[d], static_cast<unsigned long long>(__ldcg(&a.C[x])));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+        const unsigned int c = sm.u.hist.c[b];
+        if (c) {
+            atomicAdd(&a.sm_c[b], c);
+            atomicAdd(&a.sm_w[b], sm.u.hist.w[b]);
+            atomicAdd(&a.sm_cs[b], sm.u.hist.cs[b]);
+        }
+    }
+}
+
+// a ranked head of the low list: sorted position, chain start, the cut
+__device__ __forceinline__ void small_place_head(const SelArgs& a, unsigned int pos, int x, unsigned long long cw,
+                                                 unsigned long long w_before, unsigned long long c_before) {
+    const unsigned int cx = static_cast<unsigned int>(cw & 0xffffffull);
+    const unsigned long long wx = cw >> 24;
+    a.listS2[pos] = x;
+    a.listSC2[pos] = cx;
+    a.start[pos] = c_before;
+    const unsigned long long need = static_cast<unsigned long long>(a.needed);
+    if (w_before < need && w_before + wx >= need) {
+        SelState* ss = a.ss;
+        ss->n_S = pos + 1ull;
+        ss->cut_head = x;
+        ss->need_final = need - w_before;
+    }
+}
+
+// S2..S5.  Returns false (uniformly) when the low list cannot hold the cut or
+// does not fit the small path's limits; nothing has been written then.
+__device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& grid, int& nts,
+                           unsigned long long total_tok) {
+    SelState* ss = a.ss;
+    if (threadIdx.x == 0) {
+        sm.bc[0] = __ldcg(&ss->n_low);
+        sm.bc[1] = __ldcg(&ss->or_low[0]) ^ __ldcg(&ss->and_low[0]);
+        sm.bc[2] = __ldcg(&ss->or_low[1]) ^ __ldcg(&ss->and_low[1]);
+        sm.bc[3] = (__ldcg(&ss->or_low[2]) ^ __ldcg(&ss->and_low[2])) & 0xffffffffull;
+    }
+    __syncthreads();
+    const unsigned long long n_low = sm.bc[0];
+    const unsigned long long v0 = sm.bc[1], v1 = sm.bc[2], v2 = sm.bc[3];
+    __syncthreads();
+    const int nbits = __popcll(v0) + __popcll(v1) + __popcll(v2);
+    // packed keys, chain weight < 2^40 and chain size < 2^24 packed in one word
+    if (n_low == 0 || nbits > 64 || total_tok >= (1ull << 40) || a.n_nodes >= (1ll << 24)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ss->path = 2;
+        return false;
+    }
+    const int lo = nbits > kDigitBits ? nbits - kDigitBits : 0;
+    small_hist(a, n_low, lo, v0, v1, v2, sm);
+    grid.sync();
+    stamp(ss, nts);
+    // S2: bucket offsets; the check that the cut lies inside the low list
+    constexpr int kPer = kBins / kPThreads;
+    unsigned int vc[kPer], sc = 0, mx = 0;
+    unsigned long long vw[kPer], vs[kPer], sw = 0, scs = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        vc[j] = __ldcg(&a.sm_c[d]);
+        vw[j] = __ldcg(&a.sm_w[d]);
+        vs[j] = __ldcg(&a.sm_cs[d]);
+        sc += vc[j];
+        sw += vw[j];
+        scs += vs[j];
+        mx = max(mx, vc[j]);
+    }
+    unsigned long long tot_c, tot_w, tot_s;
+    unsigned long long ex_c = block_excl_scan(sc, sm.sh, &tot_c);
+    unsigned long long ex_w = block_excl_scan(sw, sm.sh, &tot_w);
+    unsigned long long ex_s = block_excl_scan(scs, sm.sh, &tot_s);
+    const unsigned int mx_all = static_cast<unsigned int>(block_reduce_bits(mx, MaxOp(), sm.sh));
+    if (threadIdx.x == 0) sm.bc[0] = mx_all;
+    __syncthreads();
+    const bool ok = tot_w >= static_cast<unsigned long long>(a.needed) && sm.bc[0] <= static_cast<unsigned int>(kBucketCap);
+    __syncthreads();
+    if (!ok) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ss->path = 2;
+        return false;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        sm.off[d] = static_cast<unsigned int>(ex_c);
+        if (blockIdx.x == 0) {
+            a.sm_off[d] = static_cast<unsigned int>(ex_c);
+            a.sm_wpre[d] = ex_w;
+            a.sm_cpre[d] = ex_s;
+            if (vc[j] > 32u) {
+                const unsigned int q = atomicAdd(&ss->n_big, 1u);
+                a.sm_big[3 * q] = static_cast<unsigned int>(d);
+                a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
+                a.sm_big[3 * q + 2] = vc[j];
+            }
+        }
+        ex_c += vc[j];
+        ex_w += vw[j];
+        ex_s += vs[j];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ss->path = 1;
+    __syncthreads();
+    {
+        const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+        for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_low;
+             base += stride) {
+            const unsigned long long i = base + threadIdx.x;
+            const bool in = i < n_low;
+            int x = 0, d = -1;
+            unsigned long long pk = 0, cw = 0;
+            if (in) {
+                x = __ldcg(&a.low[i]);
+                pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
+                d = static_cast<int>((pk >> lo) & (kBins - 1));
+                cw = (__ldcg(&a.W[x]) << 24) | static_cast<unsigned long long>(__ldcg(&a.C[x]));
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (in) {
+                const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+                unsigned int b = 0;
+                if (lane == leader) b = atomicAdd(&a.sm_cur[d], static_cast<unsigned int>(__popc(peers)));
+                b = __shfl_sync(peers, b, leader);
+                const unsigned int pos = sm.off[d] + b + __popc(peers & ((1u << lane) - 1u));
+                a.listS[pos] = x;
+                a.listSK[pos] = make_ulonglong2(pk, cw);
+            }
+        }
+    }
+    grid.sync();
+    stamp(ss, nts);
+    // S3: rank every bucket with the token / chain-size prefixes of the smaller keys
+    {
+        const int lane = threadIdx.x & 31;
+        const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
+        const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(blockDim.x)) >> 5);
+        for (int d = gwarp; d < kBins; d += nwarps) {
+            const unsigned int cnt = __ldcg(&a.sm_c[d]);
+            if (cnt == 0u || cnt > 32u) continue;
+            const unsigned int off = __ldcg(&a.sm_off[d]);
+            const bool in = static_cast<unsigned int>(lane) < cnt;
+            ulonglong2 kc = make_ulonglong2(0ull, 0ull);
+            int x = 0;
+            if (in) {
+                kc = __ldcg(&a.listSK[off + lane]);
+                x = __ldcg(&a.listS[off + lane]);
+            }
+            unsigned int r = 0;
+            unsigned long long wb = 0, cb = 0;
+            for (unsigned int j = 0; j < cnt; ++j) {
+                const unsigned long long kj = __shfl_sync(0xffffffffu, kc.x, j);
+                const unsigned long long cj = __shfl_sync(0xffffffffu, kc.y, j);
+                if (kj < kc.x) {
+                    ++r;
+                    wb += cj >> 24;
+                    cb += cj & 0xffffffull;
+                }
+            }
+            if (in) small_place_head(a, off + r, x, kc.y, __ldcg(&a.sm_wpre[d]) + wb, __ldcg(&a.sm_cpre[d]) + cb);
+        }
+        // larger buckets: rank counting from a shared-memory tile, 8 threads per
+        // element; tasks (bucket, 64-element chunk) over every CTA
+        if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->n_big);
+        __syncthreads();
+        const unsigned int n_big = static_cast<unsigned int>(sm.bc[0]);
+        __syncthreads();
+        if (n_big > 0) {
+            constexpr int kChunkS = kPThreads / 8;
+            unsigned int tv[kPer], ts = 0;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const unsigned int b = threadIdx.x * kPer + j;
+                tv[j] = b < n_big ? (__ldcg(&a.sm_big[3 * b + 2]) + kChunkS - 1) / kChunkS : 0u;
+                ts += tv[j];
+            }
+            unsigned long long ttot;
+            unsigned long long tex = block_excl_scan(ts, sm.sh, &ttot);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                sm.off[threadIdx.x * kPer + j] = static_cast<unsigned int>(tex);
+                tex += tv[j];
+            }
+            __syncthreads();
+            unsigned int held = ~0u;
+            for (unsigned int t = blockIdx.x; t < static_cast<unsigned int>(ttot); t += gridDim.x) {
+                unsigned int blo = 0, bhi = n_big - 1;
+                while (blo < bhi) {
+                    const unsigned int mid = (blo + bhi + 1) >> 1;
+                    if (sm.off[mid] <= t) blo = mid;
+                    else bhi = mid - 1;
+                }
+                const unsigned int b = blo, c = t - sm.off[b];
+                const unsigned int dg = __ldcg(&a.sm_big[3 * b]), off = __ldcg(&a.sm_big[3 * b + 1]),
+                                   cnt = __ldcg(&a.sm_big[3 * b + 2]);
+                if (held != b) {
+                    __syncthreads();
+                    for (unsigned int q = threadIdx.x; q < cnt; q += blockDim.x) {
+                        const ulonglong2 kc = __ldcg(&a.listSK[off + q]);
+                        sm.u.sort.k0[q] = kc.x;
+                        sm.u.sort.k1[q] = kc.y;
+                    }
+                    __syncthreads();
+                    held = b;
+                }
+                const unsigned int e = c * kChunkS + threadIdx.x / 8, part = threadIdx.x % 8;
+                const bool in = e < cnt;
+                const unsigned long long mk = in ? sm.u.sort.k0[e] : 0ull;
+                unsigned int r = 0;
+                unsigned long long wb = 0, cb = 0;
+                if (in) {
+                    for (unsigned int q = part; q < cnt; q += 8) {
+                        if (sm.u.sort.k0[q] < mk) {
+                            const unsigned long long cq = sm.u.sort.k1[q];
+                            ++r;
+                            wb += cq >> 24;
+                            cb += cq & 0xffffffull;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    r += __shfl_xor_sync(0xffffffffu, r, o);
+                    wb += __shfl_xor_sync(0xffffffffu, wb, o);
+                    cb += __shfl_xor_sync(0xffffffffu, cb, o);
+                }
+                if (in && part == 0)
+                    small_place_head(a, off + r, __ldcg(&a.listS[off + e]), sm.u.sort.k1[e],
+                                     __ldcg(&a.sm_wpre[dg]) + wb, __ldcg(&a.sm_cpre[dg]) + cb);
+            }
+        }
+        // deferred-heavy reports by the CTAs at the top of the grid
+        for (int j = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x); j < a.n_report;
+             j += static_cast<int>(gridDim.x))
+            report_heavy_block(j, a.heavy, a.hch_off, a.hch, a.keys, a.eff, a.sublock, a.depth, a.flags, a.hmiss,
+                               a.rep_out, a.approx, a.approx_out);
+    }
+    grid.sync();
+    stamp(ss, nts);
+    if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->n_S);
+    __syncthreads();
+    const unsigned long long nS = sm.bc[0];
+    __syncthreads();
+    phase_scatter(a, a.listS2, nS, blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x,
+                  static_cast<std::int64_t>(gridDim.x) * blockDim.x);
+    grid.sync();
+    stamp(ss, nts);
+    if (blockIdx.x == 0 && threadIdx.x == 0) do_cut(a);
+    stamp(ss, nts);
+    return true;
+}
 
 __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -941,7 +1408,9 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     phase_eff(a, tid, nthr);
     grid.sync();
     stamp(ss, nts);
-    phase_chains(a, sm.sh);
+    // the small-cut bound from the node sample (every CTA, identical)
+    const SmallBound sb = small_bound(a, sm);
+    phase_chains(a, sm.sh, sb.ok, sb.k, sb.id);
     grid.sync();
     stamp(ss, nts);
 
@@ -967,6 +1436,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         return;
     }
     const bool take_all = total_tok < static_cast<unsigned long long>(a.needed);
+    if (!take_all && sb.ok && small_path(a, sm, grid, nts, total_tok)) return;
     int* S = a.listS;
     unsigned long long nS = 0;
     unsigned int max_bucket = 0;
@@ -1381,6 +1851,25 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     a.needed = needed;
     a.he_recompute = he_recompute ? 1 : 0;
     a.n_report = 0;
+    {  // small-cut path: ~kSampTarget sampled nodes, its scratch
+        unsigned int R = 1;
+        while (static_cast<std::int64_t>(R) * kSampTarget < c.n) R <<= 1;
+        a.samp_mask = R - 1;
+        c.samp.reserve(kSamp * sizeof(SampRec));
+        c.low.reserve(static_cast<std::size_t>(c.n) + 1);
+        c.small_u32.reserve(6 * kBins);
+        c.small_u64.reserve(4 * kBins);
+        a.samp = reinterpret_cast<SampRec*>(c.samp.p);
+        a.low = c.low.p;
+        a.sm_c = c.small_u32.p;
+        a.sm_cur = c.small_u32.p + kBins;
+        a.sm_off = c.small_u32.p + 2 * kBins;
+        a.sm_big = c.small_u32.p + 3 * kBins;
+        a.sm_w = c.small_u64.p;
+        a.sm_cs = c.small_u64.p + kBins;
+        a.sm_wpre = c.small_u64.p + 2 * kBins;
+        a.sm_cpre = c.small_u64.p + 3 * kBins;
+    }
     if (c.report_deferred) {  // the deferred-heavy reports are written in place, to pinned memory
         const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
         const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
@@ -1424,10 +1913,12 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         std::fprintf(stderr,
                      "[pbkv select] n_heads=%llu total_tok=%llu take_all=%d host_sort=%d n_S=%llu n_pass=%d "
                      "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
+                     "path=%d n_samp=%u n_low=%llu est_low=%llu n_big=%u "
                      "dbg(ns): sortCTA=%llu sortWarp=%llu chainstart=%llu maxbucket=%llu nbig=%llu eff=%llu "
                      "chains=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
-                     hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->dbg[0],
+                     hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->path,
+                     hs->n_samp, hs->n_low, hs->est_low, hs->n_big, hs->dbg[0],
                      hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6]);
     if (hs->host_sort) {
         // ---- fallback: device-wide sort of the selected heads -----------------------------
