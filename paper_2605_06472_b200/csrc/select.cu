@@ -87,7 +87,9 @@ struct SelState {
     int cut_head, max_bucket;
     unsigned long long n_victims, freed;
     int shortfall, n_ts;
-    unsigned int n_samp;        // sample records appended by the eff phase
+    unsigned int n_samp;        // (unused)
+    int bound_id;               // small-cut bound (key, id); -1: no small path
+    unsigned long long bound_w0, bound_w1;
     int path;                   // 0 full radix path, 1 small-cut path, 2 small path abandoned
     unsigned long long n_low;   // heads at or below the sample bound
     unsigned long long or_low[3], and_low[3];
@@ -420,6 +422,22 @@ __device__ __forceinline__ void phase_lock(const SelArgs& a, std::int64_t tid, s
         a.sm_w[j] = 0;
         a.sm_cs[j] = 0;
     }
+    // the node sample of the small-cut bound: node j*R + jitter(j) for every
+    // j, its key and length (out-of-order / non-device nodes: an empty record
+    // that sorts last)
+    const std::int64_t R = static_cast<std::int64_t>(a.samp_mask) + 1;
+    const std::int64_t ns = (a.n_nodes + R - 1) / R;
+    for (std::int64_t j = tid; j < ns; j += nthr) {
+        std::int64_t n = j * R + static_cast<std::int64_t>(mix32(static_cast<unsigned int>(j)) & a.samp_mask);
+        if (n >= a.n_nodes) n = j * R;
+        const std::uint8_t f = a.flags[n];
+        SampRec r{~0ull, ~0ull, -1, 0};
+        if (n != 0 && (f & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE) {
+            const Key2 k = load_key(a.keys, static_cast<int>(n));
+            r = SampRec{k.w0, k.w1, static_cast<int>(n), a.len[n]};
+        }
+        a.samp[j] = r;
+    }
 }
 
 // eff: every device node walks its key up the ancestor chain, CAS-ing the
@@ -448,11 +466,6 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         for (int j = 0; j < kWalk; ++j) {
             const std::int64_t i = base + j * nthr;
             act[j] = i < a.n_nodes && n[j] != 0 && (fn[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
-            // the node sample of the small-cut bound: its own key and length
-            if (act[j] && !(fn[j] & kFlagOutOfOrder) && (mix32(static_cast<unsigned int>(n[j])) & a.samp_mask) == 0u) {
-                const unsigned int q = atomicAdd(&a.ss->n_samp, 1u);
-                if (q < static_cast<unsigned int>(kSamp)) a.samp[q] = SampRec{km[j].w0, km[j].w1, n[j], a.len[n[j]]};
-            }
             // (out-of-order parents -- deferred heavy / spine -- are reduced
             // over their children lists instead: thousands of walkers CAS-ing
             // one hot word serialised in its L2 slice)
@@ -518,8 +531,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
          base += kBatch * nthr) {
         int n[kBatch], e[kBatch], ln[kBatch];
-        bool elig[kBatch], lw[kBatch];
-        Key2 kh[kBatch];
+        bool elig[kBatch], lw[kBatch] = {false, false, false, false};
         std::uint8_t fl[kBatch], ms[kBatch];
         unsigned int cnt = 0;
         // every per-node field of the batch in one round trip (coalesced
@@ -552,15 +564,16 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             tok += l;
             cnt += e[j] == n[j] ? 1u : 0u;
         }
-        // head keys; heads at or below the small-cut bound (low list), counted
-        // in the upper half of the same scan word
+        // heads at or below the small-cut bound (low list), counted in the
+        // upper half of the same scan word
+        if (small) {
 #pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            lw[j] = false;
-            if (elig[j] && e[j] == n[j]) {
-                kh[j] = load_key(a.keys, n[j]);
-                lw[j] = small && !key_less(tk, tid_, kh[j], n[j]);
-                cnt += lw[j] ? 0x10000u : 0u;
+            for (int j = 0; j < kBatch; ++j) {
+                lw[j] = false;
+                if (elig[j] && e[j] == n[j]) {
+                    lw[j] = !key_less(tk, tid_, load_key(a.keys, n[j]), n[j]);
+                    cnt += lw[j] ? 0x10000u : 0u;
+                }
             }
         }
         // CTA-wide exclusive offsets of the heads, one global atomic per CTA
@@ -594,13 +607,13 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             if (!elig[j] || e[j] != n[j]) continue;
             const int h = n[j];
             a.heads[slot++] = h;
-            const Key2 k = kh[j];
+            const Key2 k = load_key(a.keys, h);
             for (int wd = 0; wd < 3; ++wd) {
                 const unsigned long long x = key_word(k, h, wd);
                 or3[wd] |= x;
                 and3[wd] &= x;
             }
-            if (lw[j]) {
+            if (small && lw[j]) {
                 a.low[lslot++] = h;
                 for (int wd = 0; wd < 3; ++wd) {
                     const unsigned long long x = key_word(k, h, wd);
@@ -1028,10 +1041,8 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 
 __device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
     SmallBound r{{0, 0}, -1, false};
-    if (threadIdx.x == 0) sm.bc[0] = __ldcg(&a.ss->n_samp);
-    __syncthreads();
-    const unsigned int ns = static_cast<unsigned int>(sm.bc[0]);
-    __syncthreads();
+    const unsigned long long R0 = static_cast<unsigned long long>(a.samp_mask) + 1ull;
+    const unsigned int ns = static_cast<unsigned int>((static_cast<unsigned long long>(a.n_nodes) + R0 - 1) / R0);
     if (ns == 0 || ns > static_cast<unsigned int>(kSamp)) return r;
     unsigned int p2 = 1;
     while (p2 < ns) p2 <<= 1;
@@ -1173,7 +1184,10 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     const int nbits = __popcll(v0) + __popcll(v1) + __popcll(v2);
     // packed keys, chain weight < 2^40 and chain size < 2^24 packed in one word
     if (n_low == 0 || nbits > 64 || total_tok >= (1ull << 40) || a.n_nodes >= (1ll << 24)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) ss->path = 2;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ss->path = 2;
+            ss->dbg[7] = static_cast<unsigned long long>(nbits);
+        }
         return false;
     }
     const int lo = nbits > kDigitBits ? nbits - kDigitBits : 0;
@@ -1203,9 +1217,12 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     if (threadIdx.x == 0) sm.bc[0] = mx_all;
     __syncthreads();
     const bool ok = tot_w >= static_cast<unsigned long long>(a.needed) && sm.bc[0] <= static_cast<unsigned int>(kBucketCap);
-    __syncthreads();
     if (!ok) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) ss->path = 2;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ss->path = tot_w >= static_cast<unsigned long long>(a.needed) ? 4 : 3;  // bucket too large / bound too low
+            ss->dbg[5] = tot_w;
+            ss->dbg[6] = sm.bc[0];
+        }
         return false;
     }
 #pragma unroll
@@ -1396,6 +1413,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             for (int q = 0; q < 3; ++q) {
                 ss->and_L[0][q] = ss->and_L[1][q] = ~0ull;
                 ss->and_S[q] = ~0ull;
+                ss->and_low[q] = ~0ull;
             }
             ss->cut_head = -1;
         }
@@ -1405,11 +1423,31 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     phase_lock(a, tid, nthr);
     grid.sync();
     stamp(ss, nts);
-    phase_eff(a, tid, nthr);
+    // CTA 0 sorts the node sample and sets the small-cut bound while the
+    // other CTAs walk eff
+    if (blockIdx.x == 0) {
+        const SmallBound b = small_bound(a, sm);
+        if (threadIdx.x == 0) {
+            ss->bound_w0 = b.k.w0;
+            ss->bound_w1 = b.k.w1;
+            ss->bound_id = b.ok ? b.id : -1;
+        }
+    } else {
+        phase_eff(a, tid - kPThreads, nthr - kPThreads);
+    }
     grid.sync();
     stamp(ss, nts);
-    // the small-cut bound from the node sample (every CTA, identical)
-    const SmallBound sb = small_bound(a, sm);
+    SmallBound sb;
+    if (threadIdx.x == 0) {
+        sm.bc[0] = __ldcg(&ss->bound_w0);
+        sm.bc[1] = __ldcg(&ss->bound_w1);
+        sm.bc[2] = static_cast<unsigned long long>(static_cast<long long>(__ldcg(&ss->bound_id)));
+    }
+    __syncthreads();
+    sb.k = Key2{sm.bc[0], sm.bc[1]};
+    sb.id = static_cast<int>(static_cast<long long>(sm.bc[2]));
+    sb.ok = sb.id >= 0;
+    __syncthreads();
     phase_chains(a, sm.sh, sb.ok, sb.k, sb.id);
     grid.sync();
     stamp(ss, nts);
@@ -1915,11 +1953,11 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
                      "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
                      "path=%d n_samp=%u n_low=%llu est_low=%llu n_big=%u "
                      "dbg(ns): sortCTA=%llu sortWarp=%llu chainstart=%llu maxbucket=%llu nbig=%llu eff=%llu "
-                     "chains=%llu\n",
+                     "chains=%llu nbits=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
                      hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->path,
                      hs->n_samp, hs->n_low, hs->est_low, hs->n_big, hs->dbg[0],
-                     hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6]);
+                     hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6], hs->dbg[7]);
     if (hs->host_sort) {
         // ---- fallback: device-wide sort of the selected heads -----------------------------
         const std::int64_t nS = static_cast<std::int64_t>(hs->n_S);

@@ -7,28 +7,29 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda"]
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"]
 if len(sys.argv) > 3:
     cmd += ["-k", f"regex:{sys.argv[3]}"]
 txt = subprocess.run(cmd, capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(txt)))
-col, fname, out = None, "", []
-for r in rows:
-    if len(r) == 2 and r[0] == "File Path":
+fname, col, agg = "", None, {}
+for r in csv.reader(io.StringIO(txt)):
+    if len(r) >= 2 and r[0] == "File Path":
         fname = r[1].split("/")[-1]
         continue
     if r and r[0] == "Line No":
         col = next((i for i, h in enumerate(r) if h.startswith("Warp Stall Sampling (All")), None)
         continue
-    if col is None or len(r) <= col:
+    if col is None or len(r) <= col or not r[0].isdigit():
         continue
     try:
         s = int(r[col])
     except ValueError:
         continue
-    if s:
-        out.append((s, f"{fname}:{r[0]}", r[1].strip()[:100]))
-tot = sum(o[0] for o in out) or 1
+    key = (fname, int(r[0]))
+    if key not in agg:
+        agg[key] = [0, r[1].strip()[:90]]
+    agg[key][0] += s
+tot = sum(v[0] for v in agg.values())
 print("total samples", tot)
-for s, loc, src in sorted(out, reverse=True)[:top]:
-    print(f"{s:7d} {100 * s / tot:5.1f}% {loc:18s} {src}")
+for (f, ln), (s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print(f"{s:8d} {100.0 * s / max(tot, 1):5.1f}%  {f}:{ln}  {src}")
