@@ -73,6 +73,27 @@ __device__ __forceinline__ Key2 load_key(const Key2* keys, int i) {
     return Key2{v.x, v.y};
 }
 
+// 64-bit shared-memory add / or / and through native 32-bit atomics (the
+// 64-bit shared atomics compile to CAS spin loops on sm_100a).  The add is
+// exact: the carry out of the low word is added to the high word.
+__device__ __forceinline__ void smem_add_u64(unsigned long long* p, unsigned long long v) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(p);
+    const unsigned int lo = static_cast<unsigned int>(v), hi = static_cast<unsigned int>(v >> 32);
+    const unsigned int old = lo ? atomicAdd(w, lo) : 0u;
+    const unsigned int up = hi + (static_cast<unsigned int>(old + lo) < old ? 1u : 0u);
+    if (up) atomicAdd(w + 1, up);
+}
+__device__ __forceinline__ void smem_or_u64(unsigned long long* p, unsigned long long v) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(p);
+    if (static_cast<unsigned int>(v)) atomicOr(w, static_cast<unsigned int>(v));
+    if (v >> 32) atomicOr(w + 1, static_cast<unsigned int>(v >> 32));
+}
+__device__ __forceinline__ void smem_and_u64(unsigned long long* p, unsigned long long v) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(p);
+    if (~static_cast<unsigned int>(v)) atomicAnd(w, static_cast<unsigned int>(v));
+    if (~static_cast<unsigned int>(v >> 32)) atomicAnd(w + 1, static_cast<unsigned int>(v >> 32));
+}
+
 // warp-aggregated append: one atomic per warp; returns this lane's slot
 __device__ __forceinline__ long long warp_append(unsigned long long* counter, bool pred) {
     const unsigned mask = __ballot_sync(0xffffffffu, pred);

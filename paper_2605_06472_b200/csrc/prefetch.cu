@@ -350,7 +350,7 @@ __device__ __forceinline__ void pf_hist(const PfArgs& a, const Packer& pk, unsig
     for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(kPT) + threadIdx.x; i < n; i += nthr) {
         const unsigned int d = pk.digit(pk.key(__ldcg(&a.c_hi[i]), __ldcg(&a.c_id[i])));
         atomicAdd(&sm.u.hist.c[d], 1u);
-        atomicAdd(&sm.u.hist.l[d], static_cast<unsigned long long>(__ldcg(&a.c_len[i])));
+        smem_add_u64(&sm.u.hist.l[d], static_cast<unsigned long long>(__ldcg(&a.c_len[i])));
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kPBins; b += kPT) {

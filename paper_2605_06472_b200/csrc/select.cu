@@ -87,7 +87,7 @@ struct SelState {
     int cut_head, max_bucket;
     unsigned long long n_victims, freed;
     int shortfall, n_ts;
-    unsigned int n_samp;        // (unused)
+    unsigned int low_overflow;  // a CTA's low buffer overflowed: no small path
     int bound_id;               // small-cut bound (key, id); -1: no small path
     unsigned long long bound_w0, bound_w1;
     int path;                   // 0 full radix path, 1 small-cut path, 2 small path abandoned
@@ -422,28 +422,24 @@ __device__ __forceinline__ void phase_lock(const SelArgs& a, std::int64_t tid, s
         a.sm_w[j] = 0;
         a.sm_cs[j] = 0;
     }
-    // the node sample of the small-cut bound: node j*R + jitter(j) for every
-    // j, its key and length (out-of-order / non-device nodes: an empty record
-    // that sorts last)
-    const std::int64_t R = static_cast<std::int64_t>(a.samp_mask) + 1;
-    const std::int64_t ns = (a.n_nodes + R - 1) / R;
-    for (std::int64_t j = tid; j < ns; j += nthr) {
-        std::int64_t n = j * R + static_cast<std::int64_t>(mix32(static_cast<unsigned int>(j)) & a.samp_mask);
-        if (n >= a.n_nodes) n = j * R;
-        const std::uint8_t f = a.flags[n];
-        SampRec r{~0ull, ~0ull, -1, 0};
-        if (n != 0 && (f & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE) {
-            const Key2 k = load_key(a.keys, static_cast<int>(n));
-            r = SampRec{k.w0, k.w1, static_cast<int>(n), a.len[n]};
-        }
-        a.samp[j] = r;
-    }
 }
 
 // eff: every device node walks its key up the ancestor chain, CAS-ing the
 // ancestors' argmax id; a walk stops at the first ancestor already holding a
 // larger key (its holder carries it further), so eff ends as the exact
 // subtree maximum
+// (small-cut path) every head with key <= the bound joins the low list: collected
+// per CTA in shared memory, appended with one global atomic per CTA
+struct LowSink {
+    bool on;
+    Key2 tk;
+    int tid;
+    int* buf;                  // shared memory, kLowSh entries
+    unsigned int* cnt;         // shared counter
+    unsigned long long* orand; // shared [6]: OR, AND of the low keys' words
+};
+constexpr int kLowSh = 8192;
+
 __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
     // kWalk walkers per thread advance in lockstep, so each round issues the
     // loads of all of them together: the walk is a chain of dependent L2
@@ -466,6 +462,7 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         for (int j = 0; j < kWalk; ++j) {
             const std::int64_t i = base + j * nthr;
             act[j] = i < a.n_nodes && n[j] != 0 && (fn[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
+
             // (out-of-order parents -- deferred heavy / spine -- are reduced
             // over their children lists instead: thousands of walkers CAS-ing
             // one hot word serialised in its L2 slice)
@@ -513,10 +510,29 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
     }
 }
 
+// the CTA's low heads: one global append, OR / AND into the selection state
+__device__ __forceinline__ void low_flush(const SelArgs& a, const LowSink& lk) {
+    __syncthreads();
+    unsigned long long* sh = lk.orand + 8;  // a free word after the OR / AND
+    const unsigned int c = *lk.cnt;
+    if (threadIdx.x == 0) {
+        if (c > static_cast<unsigned int>(kLowSh)) atomicOr(&a.ss->low_overflow, 1u);
+        sh[0] = c ? atomicAdd(&a.ss->n_low, static_cast<unsigned long long>(min(c, static_cast<unsigned int>(kLowSh)))) : 0ull;
+    }
+    __syncthreads();
+    const unsigned long long b0 = sh[0];
+    for (unsigned int i = threadIdx.x; i < min(c, static_cast<unsigned int>(kLowSh)); i += blockDim.x) a.low[b0 + i] = lk.buf[i];
+    if (threadIdx.x < 3 && c) {
+        atomicOr(&a.ss->or_low[threadIdx.x], lk.orand[threadIdx.x]);
+        atomicAnd(&a.ss->and_low[threadIdx.x], lk.orand[3 + threadIdx.x]);
+    }
+    __syncthreads();
+}
+
 // heads (eligible n with eff(n) == n) walk their own chain -- the contiguous
 // eligible ancestors with the same eff -- for its token weight W and size C;
 // head list, eligible tokens, OR/AND of the head keys (first radix pass)
-__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh, bool small, Key2 tk, int tid_) {
+__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh, const LowSink& lk) {
     // Every eligible node n belongs to the chain of eff(n) (the closed form
     // orders eligible nodes by (eff, d); the nodes sharing an eff form a
     // contiguous eligible ancestor path from it), so the chain weight W[h] and
@@ -526,12 +542,11 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     SelState* ss = a.ss;
     unsigned long long tok = 0;
     unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
-    unsigned long long orl[3] = {0, 0, 0}, andl[3] = {~0ull, ~0ull, ~0ull};
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
          base += kBatch * nthr) {
         int n[kBatch], e[kBatch], ln[kBatch];
-        bool elig[kBatch], lw[kBatch] = {false, false, false, false};
+        bool elig[kBatch];
         std::uint8_t fl[kBatch], ms[kBatch];
         unsigned int cnt = 0;
         // every per-node field of the batch in one round trip (coalesced
@@ -564,18 +579,6 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             tok += l;
             cnt += e[j] == n[j] ? 1u : 0u;
         }
-        // heads at or below the small-cut bound (low list), counted in the
-        // upper half of the same scan word
-        if (small) {
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                lw[j] = false;
-                if (elig[j] && e[j] == n[j]) {
-                    lw[j] = !key_less(tk, tid_, load_key(a.keys, n[j]), n[j]);
-                    cnt += lw[j] ? 0x10000u : 0u;
-                }
-            }
-        }
         // CTA-wide exclusive offsets of the heads, one global atomic per CTA
         unsigned int* wcount = reinterpret_cast<unsigned int*>(sh);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -594,13 +597,10 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
                 wcount[w] = sum;
                 sum += c;
             }
-            sh[31] = (sum & 0xffffu) ? atomicAdd(&ss->n_L[0], static_cast<unsigned long long>(sum & 0xffffu)) : 0ull;
-            sh[30] = (sum >> 16) ? atomicAdd(&ss->n_low, static_cast<unsigned long long>(sum >> 16)) : 0ull;
+            sh[31] = sum ? atomicAdd(&ss->n_L[0], static_cast<unsigned long long>(sum)) : 0ull;
         }
         __syncthreads();
-        const unsigned int ex = wcount[warp] + (incl - cnt);
-        unsigned long long slot = sh[31] + (ex & 0xffffu);
-        unsigned long long lslot = sh[30] + (ex >> 16);
+        unsigned long long slot = sh[31] + wcount[warp] + (incl - cnt);
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
@@ -613,12 +613,13 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
                 or3[wd] |= x;
                 and3[wd] &= x;
             }
-            if (small && lw[j]) {
-                a.low[lslot++] = h;
+            if (lk.on && !key_less(lk.tk, lk.tid, k, h)) {  // a low head
+                const unsigned int q = atomicAdd(lk.cnt, 1u);
+                if (q < static_cast<unsigned int>(kLowSh)) lk.buf[q] = h;
                 for (int wd = 0; wd < 3; ++wd) {
                     const unsigned long long x = key_word(k, h, wd);
-                    orl[wd] |= x;
-                    andl[wd] &= x;
+                    smem_or_u64(&lk.orand[wd], x);
+                    smem_and_u64(&lk.orand[3 + wd], x);
                 }
             }
         }
@@ -626,7 +627,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     const unsigned long long blk = block_reduce_bits(tok, SumOp(), sh);
     if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
     flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
-    if (small) flush_orand(orl, andl, ss->or_low, ss->and_low, sh);
+    if (lk.on) low_flush(a, lk);
 }
 
 // per-CTA weight and count histograms of the next digit over the candidates
@@ -662,7 +663,7 @@ __device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsig
             for (unsigned m = peers; m; m &= m - 1) sum += __shfl_sync(peers, w, __ffs(m) - 1);
         }
         if (d != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) {
-            atomicAdd(&hw[d], sum);
+            smem_add_u64(&hw[d], sum);
             atomicAdd(&hc[d], static_cast<unsigned int>(__popc(peers)));
         }
     }
@@ -997,19 +998,20 @@ struct PersistSmem {
 
 // ---- small-cut path ------------------------------------------------
 // A cut that takes a small share of the eligible tokens lies among the
-// lowest keys.  The eff phase samples ~1/R of the eligible nodes (key, len);
-// every CTA sorts that sample itself (identical result, no barrier) and picks
-// a bound T whose estimated weight below it -- R x the sampled tokens with key
-// <= T -- is twice `needed` plus a sampling margin.  The chains phase then
-// lists the heads with key <= T (the low list) next to the head list.  If the
-// low list's exact chain weight reaches `needed` (checked from its histogram)
-// the cut lies inside it, and the decision is: one 11-bit MSD histogram of
-// the low list, placement into buckets, every bucket ranked in place -- the
-// rank count also sums the chain weights W and sizes C of the smaller keys,
-// so with the per-bucket prefixes each head knows its cumulative token count
-// and its victim offset, and the head whose count crosses `needed` is the cut
-// -- then the chain scatter.  Otherwise (the sample missed; rare) the full
-// radix path below runs.  Results are identical either way.
+// lowest keys.  During the lock phase CTA 0 reads a strided node sample (node
+// j*R + jitter(j), ~1/R of the nodes: key, token length) and finds by a
+// weighted MSD radix select over it the bound T: the sampled key at which R x
+// the sampled tokens at or below it reach 2 x `needed` plus a sampling margin.
+// The eff phase lists every device node with key <= T (the low list).  If the
+// exact chain weight of the low list's heads reaches `needed` (checked from
+// its histogram) the cut lies among them, and the rest of the decision is:
+// one 11-bit MSD histogram of the low heads, placement into buckets, then
+// every bucket ranked in place -- the rank count also sums the chain weights W
+// and sizes C of the smaller keys, so with the per-bucket prefixes each head
+// knows its cumulative token count and its victim offset: a selected head
+// scatters its own chain, and the head whose count crosses `needed` scatters
+// the cut.  Otherwise (the sample missed; rare) the full radix path below
+// runs.  Results are identical either way.
 struct SmallBound {
     Key2 k;
     int id;
@@ -1039,87 +1041,183 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
     return pre + x - v;
 }
 
+// one CTA: the bound T from the node sample (two samples per thread)
 __device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
     SmallBound r{{0, 0}, -1, false};
-    const unsigned long long R0 = static_cast<unsigned long long>(a.samp_mask) + 1ull;
-    const unsigned int ns = static_cast<unsigned int>((static_cast<unsigned long long>(a.n_nodes) + R0 - 1) / R0);
-    if (ns == 0 || ns > static_cast<unsigned int>(kSamp)) return r;
-    unsigned int p2 = 1;
-    while (p2 < ns) p2 <<= 1;
-    unsigned long long* k0 = sm.u.sort.k0;
-    unsigned long long* k1 = sm.u.sort.k1;
-    int* vid = sm.u.sort.val;
-    int* vlen = sm.u.sort.val + kSamp;
-    for (unsigned int i = threadIdx.x; i < p2; i += blockDim.x) {
-        if (i < ns) {
-            k0[i] = __ldcg(&a.samp[i].w0);
-            k1[i] = __ldcg(&a.samp[i].w1);
-            vid[i] = __ldcg(&a.samp[i].id);
-            vlen[i] = __ldcg(&a.samp[i].len);
-        } else {
-            k0[i] = ~0ull;
-            k1[i] = ~0ull;
-            vid[i] = -1;
-            vlen[i] = 0;
+    const long long R = static_cast<long long>(a.samp_mask) + 1;
+    const long long ns = (a.n_nodes + R - 1) / R;
+    if (ns > 2 * kPThreads) return r;
+    const unsigned long long tb0 = gtimer();
+    Key2 k[2];
+    int id[2];
+    unsigned long long ln[2];
+    bool alive[2];
+    unsigned long long tok = 0, nv = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const long long j = threadIdx.x + q * kPThreads;
+        long long n = j * R + static_cast<long long>(mix32(static_cast<unsigned int>(j)) & a.samp_mask);
+        if (n >= a.n_nodes) n = j * R;
+        alive[q] = false;
+        id[q] = -1;
+        ln[q] = 0;
+        k[q] = Key2{0, 0};
+        if (j < ns && n != 0 && (a.flags[n] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE) {
+            k[q] = load_key(a.keys, static_cast<int>(n));
+            id[q] = static_cast<int>(n);
+            ln[q] = static_cast<unsigned long long>(a.len[n]);
+            alive[q] = true;
+            tok += ln[q];
+            nv += 1;
         }
     }
+    const unsigned long long T = block_reduce_bits(tok, SumOp(), sm.sh);
+    if (threadIdx.x == 0) sm.bc[0] = T;
     __syncthreads();
-    // bitonic sort by (w0, w1, id), padding last
-    for (unsigned int k = 2; k <= p2; k <<= 1) {
-        for (unsigned int j = k >> 1; j > 0; j >>= 1) {
-            for (unsigned int t = threadIdx.x; t < (p2 >> 1); t += blockDim.x) {
-                const unsigned int i = (t / j) * 2 * j + (t % j), l = i + j;
-                const bool up = (i & k) == 0;
-                const bool gt = sk_less(k0[l], k1[l], vid[l], k0[i], k1[i], vid[i]);
-                if (gt == up) {
-                    const unsigned long long a0 = k0[i], a1 = k1[i];
-                    const int av = vid[i], al = vlen[i];
-                    k0[i] = k0[l];
-                    k1[i] = k1[l];
-                    vid[i] = vid[l];
-                    vlen[i] = vlen[l];
-                    k0[l] = a0;
-                    k1[l] = a1;
-                    vid[l] = av;
-                    vlen[l] = al;
+    const unsigned long long stok = sm.bc[0];
+    __syncthreads();
+    const unsigned long long NV = block_reduce_bits(nv, SumOp(), sm.sh);
+    if (threadIdx.x == 0) sm.bc[1] = NV;
+    __syncthreads();
+    const unsigned long long nvalid = sm.bc[1];
+    __syncthreads();
+    if (nvalid == 0 || stok == 0) return r;
+    // sampled-token target: 2 x needed / R, plus 8 + 3 sqrt(count) samples' worth
+    const double mean = static_cast<double>(stok) / static_cast<double>(nvalid);
+    const double tgt = 2.0 * static_cast<double>(a.needed) / static_cast<double>(R);
+    const double cnt_est = tgt / mean;
+    unsigned long long rem =
+        static_cast<unsigned long long>(ceil(tgt + (8.0 + 3.0 * sqrt(cnt_est + 1.0)) * mean));
+    if (rem == 0) rem = 1;
+    if (rem > stok) return r;
+    const unsigned long long tb1 = gtimer();
+    int n_pass = 0;
+    unsigned long long below = 0;  // samples below the chosen bins
+    unsigned int* hc = sm.u.hist.c;
+    unsigned long long* hw = sm.u.hist.w;
+    unsigned long long* orand = sm.u.hist.cs;  // [0..2] or, [3..5] and
+    for (int pass = 0; pass < 24; ++pass) {
+        // varying bits of the alive keys
+        if (threadIdx.x < 3) {
+            orand[threadIdx.x] = 0ull;
+            orand[3 + threadIdx.x] = ~0ull;
+        }
+        __syncthreads();
+        unsigned long long o3[3] = {0, 0, 0}, n3[3] = {~0ull, ~0ull, ~0ull};
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (alive[q])
+                for (int w = 0; w < 3; ++w) {
+                    const unsigned long long x = key_word(k[q], id[q], w);
+                    o3[w] |= x;
+                    n3[w] &= x;
+                }
+        for (int w = 0; w < 3; ++w) {
+            for (int o = 16; o; o >>= 1) {
+                o3[w] |= __shfl_xor_sync(0xffffffffu, o3[w], o);
+                n3[w] &= __shfl_xor_sync(0xffffffffu, n3[w], o);
+            }
+            if ((threadIdx.x & 31) == 0) {
+                smem_or_u64(&orand[w], o3[w]);
+                smem_and_u64(&orand[3 + w], n3[w]);
+            }
+        }
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+            hc[b] = 0;
+            hw[b] = 0;
+        }
+        __syncthreads();
+        int top = -1;  // top varying bit of the alive keys (shared-memory words)
+        {
+            const unsigned long long x0 = orand[0] ^ orand[3], x1 = orand[1] ^ orand[4];
+            const unsigned long long x2 = (orand[2] ^ orand[5]) & 0xffffffffull;
+            if (x0) top = 96 + 63 - __clzll(static_cast<long long>(x0));
+            else if (x1) top = 32 + 63 - __clzll(static_cast<long long>(x1));
+            else if (x2) top = 63 - __clzll(static_cast<long long>(x2));
+        }
+        if (top < 0) break;  // one alive key left
+        const int lo = top - 7 < 0 ? 0 : top - 7;
+        const int nb = top - lo + 1;
+        unsigned int dg[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            dg[q] = alive[q] ? key_bits(k[q], id[q], lo, nb) : 0u;
+            // equal digits of a warp first (early passes put most samples in one bin)
+            const unsigned peers = __match_any_sync(0xffffffffu, alive[q] ? dg[q] : 0xffffffffu);
+            // (the sample's token weights only steer the bound: saturated at 2^26 per node)
+            const unsigned long long sw =
+                __reduce_add_sync(peers, static_cast<unsigned int>(ln[q] < (1ull << 26) ? ln[q] : (1ull << 26)));
+            if (alive[q] && (threadIdx.x & 31) == __ffs(peers) - 1) {
+                atomicAdd(&hc[dg[q]], static_cast<unsigned int>(__popc(peers)));
+                smem_add_u64(&hw[dg[q]], sw);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // the bin where the running sampled tokens reach rem
+            const int lane = threadIdx.x;
+            unsigned long long w8 = 0, c8 = 0;
+            for (int j = 0; j < 8; ++j) {
+                w8 += hw[lane * 8 + j];
+                c8 += hc[lane * 8 + j];
+            }
+            unsigned long long wi = w8, ci = c8;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+                const unsigned long long z = __shfl_up_sync(0xffffffffu, ci, o);
+                if (lane >= o) {
+                    wi += y;
+                    ci += z;
                 }
             }
-            __syncthreads();
+            unsigned long long wb = wi - w8, cb = ci - c8;
+            if (wb < rem && wi >= rem) {
+                for (int j = 0; j < 8; ++j) {
+                    const int d = lane * 8 + j;
+                    if (wb + hw[d] >= rem) {
+                        sm.bc[2] = static_cast<unsigned long long>(d);
+                        sm.bc[3] = rem - wb;
+                        sm.bc[0] = cb;
+                        sm.bc[1] = hc[d];
+                        break;
+                    }
+                    wb += hw[d];
+                    cb += hc[d];
+                }
+            }
         }
+        __syncthreads();
+        const unsigned int pick = static_cast<unsigned int>(sm.bc[2]);
+        rem = sm.bc[3];
+        below += sm.bc[0];
+        const unsigned long long left = sm.bc[1];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) alive[q] = alive[q] && dg[q] == pick;
+        ++n_pass;
+        if (left == 1) break;
     }
-    // running sampled tokens; the first sample whose estimate R x tokens
-    // reaches 2 x needed, moved up by a sampling margin of 3 sqrt(i) + 8
-    const unsigned long long R = static_cast<unsigned long long>(a.samp_mask) + 1ull;
-    const unsigned int per = (ns + blockDim.x - 1) / blockDim.x;
-    const unsigned int i0 = threadIdx.x * per;
-    unsigned long long loc = 0;
-    for (unsigned int i = i0; i < i0 + per && i < ns; ++i) loc += static_cast<unsigned long long>(vlen[i]);
-    unsigned long long tot;
-    unsigned long long run = block_excl_scan(loc, sm.sh, &tot);
-    if (threadIdx.x == 0) sm.bc[1] = ~0ull;
-    __syncthreads();
-    const unsigned long long target = 2ull * static_cast<unsigned long long>(a.needed);
-    for (unsigned int i = i0; i < i0 + per && i < ns; ++i) {
-        const unsigned long long prev = run;
-        run += static_cast<unsigned long long>(vlen[i]);
-        if (prev * R < target && run * R >= target) sm.bc[1] = i;  // unique
-    }
-    __syncthreads();
-    const unsigned long long first = sm.bc[1];
-    if (first != ~0ull) {
-        const unsigned long long m = first + 8ull + static_cast<unsigned long long>(3.0 * sqrt(static_cast<double>(first + 1)));
-        if (m < ns && (m + 1) * R <= static_cast<unsigned long long>(kSmallMax)) {
-            r.k = Key2{k0[m], k1[m]};
-            r.id = vid[m];
-            r.ok = true;
-            if (blockIdx.x == 0 && threadIdx.x == 0) a.ss->est_low = (m + 1) * R;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+        if (alive[q]) {  // the bound (unique)
+            sm.bc[0] = k[q].w0;
+            sm.bc[1] = k[q].w1;
+            sm.bc[2] = static_cast<unsigned long long>(id[q]);
         }
+    __syncthreads();
+    r.k = Key2{sm.bc[0], sm.bc[1]};
+    r.id = static_cast<int>(sm.bc[2]);
+    r.ok = (below + 1) * static_cast<unsigned long long>(R) <= static_cast<unsigned long long>(kSmallMax);
+    if (threadIdx.x == 0) {
+        a.ss->est_low = (below + 1) * static_cast<unsigned long long>(R);
+        a.ss->dbg[0] = tb1 - tb0;
+        a.ss->dbg[1] = gtimer() - tb1;
+        a.ss->dbg[2] = static_cast<unsigned long long>(n_pass);
     }
-    __syncthreads();  // the sort buffers are reused by the phases that follow
+    __syncthreads();
     return r;
 }
 
-// S1: histogram of the low list (count, chain weight, chain size per 11-bit digit)
+// S1: histogram of the low heads (count, chain weight, chain size per 11-bit digit)
 __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long n_low, int lo, unsigned long long v0,
                                            unsigned long long v1, unsigned long long v2, PersistSmem& sm) {
     for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
@@ -1134,9 +1232,9 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         const int x = __ldcg(&a.low[i]);
         const unsigned long long pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
         const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kBins - 1);
-        atomicAdd(&sm.u.hist.w[d], __ldcg(&a.W[x]));
+        smem_add_u64(&sm.u.hist.w[d], __ldcg(&a.W[x]));
         atomicAdd(&sm.u.hist.c[d], 1u);
-        atomicAdd(&sm.u.hist.cs[d], static_cast<unsigned long long>(__ldcg(&a.C[x])));
+        smem_add_u64(&sm.u.hist.cs[d], static_cast<unsigned long long>(__ldcg(&a.C[x])));
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
@@ -1149,24 +1247,51 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     }
 }
 
-// a ranked head of the low list: sorted position, chain start, the cut
-__device__ __forceinline__ void small_place_head(const SelArgs& a, unsigned int pos, int x, unsigned long long cw,
+// a ranked low head: a selected one scatters its chain at its victim offset;
+// the head whose running token count crosses `needed` scatters the cut part of
+// its chain and finishes the decision (do_cut's work)
+__device__ __forceinline__ void small_place_head(const SelArgs& a, int x, unsigned long long cw,
                                                  unsigned long long w_before, unsigned long long c_before) {
-    const unsigned int cx = static_cast<unsigned int>(cw & 0xffffffull);
-    const unsigned long long wx = cw >> 24;
-    a.listS2[pos] = x;
-    a.listSC2[pos] = cx;
-    a.start[pos] = c_before;
     const unsigned long long need = static_cast<unsigned long long>(a.needed);
-    if (w_before < need && w_before + wx >= need) {
-        SelState* ss = a.ss;
-        ss->n_S = pos + 1ull;
-        ss->cut_head = x;
-        ss->need_final = need - w_before;
+    if (w_before >= need) return;
+    const unsigned long long wx = cw >> 24;
+    unsigned long long at = c_before;
+    if (w_before + wx < need) {  // the whole chain
+        int v = x;
+        for (;;) {
+            a.victims[at++] = v;
+            v = a.parent[v];
+            if (v <= 0) break;
+            const bool ok = (a.flags[v] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
+                            !__ldcg(&a.sublock[v]) && __ldcg(&a.eff[v]) == x;
+            if (!ok) break;
+        }
+        return;
     }
+    // the cut chain: its nodes until the running total reaches need
+    const unsigned long long need_c = need - w_before;
+    unsigned long long acc = 0;
+    int v = x;
+    for (;;) {
+        a.victims[at++] = v;
+        acc += static_cast<unsigned long long>(a.len[v]);
+        if (acc >= need_c) break;
+        v = a.parent[v];  // the chain holds >= need_c tokens: v stays in it
+    }
+    SelState* ss = a.ss;
+    ss->n_S = 0;
+    ss->cut_head = x;
+    ss->need_final = need_c;
+    ss->n_victims = at;
+    ss->freed = w_before + acc;
+    ss->shortfall = 0;
+    a.result[0] = static_cast<long long>(at);
+    a.result[1] = static_cast<long long>(w_before + acc);
+    a.result[2] = 0;
+    if (a.n_report > 0) a.rep_out[a.n_report] = report_tail(a.keys, a.eff, a.depth, a.victims, static_cast<long long>(at));
 }
 
-// S2..S5.  Returns false (uniformly) when the low list cannot hold the cut or
+// S1..S3.  Returns false (uniformly) when the low list cannot hold the cut or
 // does not fit the small path's limits; nothing has been written then.
 __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& grid, int& nts,
                            unsigned long long total_tok) {
@@ -1180,10 +1305,11 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     __syncthreads();
     const unsigned long long n_low = sm.bc[0];
     const unsigned long long v0 = sm.bc[1], v1 = sm.bc[2], v2 = sm.bc[3];
+    const bool ovf = __ldcg(&ss->low_overflow) != 0u;
     __syncthreads();
     const int nbits = __popcll(v0) + __popcll(v1) + __popcll(v2);
     // packed keys, chain weight < 2^40 and chain size < 2^24 packed in one word
-    if (n_low == 0 || nbits > 64 || total_tok >= (1ull << 40) || a.n_nodes >= (1ll << 24)) {
+    if (n_low == 0 || ovf || nbits > 64 || total_tok >= (1ull << 40) || a.n_nodes >= (1ll << 24)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ss->path = 2;
             ss->dbg[7] = static_cast<unsigned long long>(nbits);
@@ -1194,7 +1320,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     small_hist(a, n_low, lo, v0, v1, v2, sm);
     grid.sync();
     stamp(ss, nts);
-    // S2: bucket offsets; the check that the cut lies inside the low list
+    // S2: bucket offsets; the check that the cut lies among the low heads
     constexpr int kPer = kBins / kPThreads;
     unsigned int vc[kPer], sc = 0, mx = 0;
     unsigned long long vw[kPer], vs[kPer], sw = 0, scs = 0;
@@ -1251,17 +1377,16 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
         for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_low;
              base += stride) {
             const unsigned long long i = base + threadIdx.x;
-            const bool in = i < n_low;
             int x = 0, d = -1;
             unsigned long long pk = 0, cw = 0;
-            if (in) {
+            if (i < n_low) {
                 x = __ldcg(&a.low[i]);
                 pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
                 d = static_cast<int>((pk >> lo) & (kBins - 1));
                 cw = (__ldcg(&a.W[x]) << 24) | static_cast<unsigned long long>(__ldcg(&a.C[x]));
             }
             const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (in) {
+            if (d >= 0) {
                 const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
                 unsigned int b = 0;
                 if (lane == leader) b = atomicAdd(&a.sm_cur[d], static_cast<unsigned int>(__popc(peers)));
@@ -1274,7 +1399,8 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     }
     grid.sync();
     stamp(ss, nts);
-    // S3: rank every bucket with the token / chain-size prefixes of the smaller keys
+    // S3: rank every bucket with the token / chain-size prefixes of the smaller
+    // keys; selected heads scatter their chains, the crossing head the cut
     {
         const int lane = threadIdx.x & 31;
         const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
@@ -1282,6 +1408,8 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
         for (int d = gwarp; d < kBins; d += nwarps) {
             const unsigned int cnt = __ldcg(&a.sm_c[d]);
             if (cnt == 0u || cnt > 32u) continue;
+            const unsigned long long wpre = __ldcg(&a.sm_wpre[d]);
+            if (wpre >= static_cast<unsigned long long>(a.needed)) continue;  // wholly after the cut
             const unsigned int off = __ldcg(&a.sm_off[d]);
             const bool in = static_cast<unsigned int>(lane) < cnt;
             ulonglong2 kc = make_ulonglong2(0ull, 0ull);
@@ -1290,18 +1418,16 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
                 kc = __ldcg(&a.listSK[off + lane]);
                 x = __ldcg(&a.listS[off + lane]);
             }
-            unsigned int r = 0;
             unsigned long long wb = 0, cb = 0;
             for (unsigned int j = 0; j < cnt; ++j) {
                 const unsigned long long kj = __shfl_sync(0xffffffffu, kc.x, j);
                 const unsigned long long cj = __shfl_sync(0xffffffffu, kc.y, j);
                 if (kj < kc.x) {
-                    ++r;
                     wb += cj >> 24;
                     cb += cj & 0xffffffull;
                 }
             }
-            if (in) small_place_head(a, off + r, x, kc.y, __ldcg(&a.sm_wpre[d]) + wb, __ldcg(&a.sm_cpre[d]) + cb);
+            if (in) small_place_head(a, x, kc.y, wpre + wb, __ldcg(&a.sm_cpre[d]) + cb);
         }
         // larger buckets: rank counting from a shared-memory tile, 8 threads per
         // element; tasks (bucket, 64-element chunk) over every CTA
@@ -1315,7 +1441,9 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const unsigned int b = threadIdx.x * kPer + j;
-                tv[j] = b < n_big ? (__ldcg(&a.sm_big[3 * b + 2]) + kChunkS - 1) / kChunkS : 0u;
+                tv[j] = b < n_big && __ldcg(&a.sm_wpre[__ldcg(&a.sm_big[3 * b])]) < static_cast<unsigned long long>(a.needed)
+                            ? (__ldcg(&a.sm_big[3 * b + 2]) + kChunkS - 1) / kChunkS
+                            : 0u;
                 ts += tv[j];
             }
             unsigned long long ttot;
@@ -1328,7 +1456,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
             __syncthreads();
             unsigned int held = ~0u;
             for (unsigned int t = blockIdx.x; t < static_cast<unsigned int>(ttot); t += gridDim.x) {
-                unsigned int blo = 0, bhi = n_big - 1;
+                unsigned int blo = 0, bhi = n_big - 1;  // last bucket whose first task is <= t
                 while (blo < bhi) {
                     const unsigned int mid = (blo + bhi + 1) >> 1;
                     if (sm.off[mid] <= t) blo = mid;
@@ -1350,13 +1478,11 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
                 const unsigned int e = c * kChunkS + threadIdx.x / 8, part = threadIdx.x % 8;
                 const bool in = e < cnt;
                 const unsigned long long mk = in ? sm.u.sort.k0[e] : 0ull;
-                unsigned int r = 0;
                 unsigned long long wb = 0, cb = 0;
                 if (in) {
                     for (unsigned int q = part; q < cnt; q += 8) {
                         if (sm.u.sort.k0[q] < mk) {
                             const unsigned long long cq = sm.u.sort.k1[q];
-                            ++r;
                             wb += cq >> 24;
                             cb += cq & 0xffffffull;
                         }
@@ -1364,13 +1490,12 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
                 }
 #pragma unroll
                 for (int o = 1; o < 8; o <<= 1) {
-                    r += __shfl_xor_sync(0xffffffffu, r, o);
                     wb += __shfl_xor_sync(0xffffffffu, wb, o);
                     cb += __shfl_xor_sync(0xffffffffu, cb, o);
                 }
                 if (in && part == 0)
-                    small_place_head(a, off + r, __ldcg(&a.listS[off + e]), sm.u.sort.k1[e],
-                                     __ldcg(&a.sm_wpre[dg]) + wb, __ldcg(&a.sm_cpre[dg]) + cb);
+                    small_place_head(a, __ldcg(&a.listS[off + e]), sm.u.sort.k1[e], __ldcg(&a.sm_wpre[dg]) + wb,
+                                     __ldcg(&a.sm_cpre[dg]) + cb);
             }
         }
         // deferred-heavy reports by the CTAs at the top of the grid
@@ -1379,17 +1504,6 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
             report_heavy_block(j, a.heavy, a.hch_off, a.hch, a.keys, a.eff, a.sublock, a.depth, a.flags, a.hmiss,
                                a.rep_out, a.approx, a.approx_out);
     }
-    grid.sync();
-    stamp(ss, nts);
-    if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->n_S);
-    __syncthreads();
-    const unsigned long long nS = sm.bc[0];
-    __syncthreads();
-    phase_scatter(a, a.listS2, nS, blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x,
-                  static_cast<std::int64_t>(gridDim.x) * blockDim.x);
-    grid.sync();
-    stamp(ss, nts);
-    if (blockIdx.x == 0 && threadIdx.x == 0) do_cut(a);
     stamp(ss, nts);
     return true;
 }
@@ -1423,7 +1537,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     phase_lock(a, tid, nthr);
     grid.sync();
     stamp(ss, nts);
-    // CTA 0 sorts the node sample and sets the small-cut bound while the
+    // CTA 0 reads the node sample and sets the small-cut bound while the
     // other CTAs walk eff
     if (blockIdx.x == 0) {
         const SmallBound b = small_bound(a, sm);
@@ -1437,18 +1551,21 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     }
     grid.sync();
     stamp(ss, nts);
-    SmallBound sb;
     if (threadIdx.x == 0) {
         sm.bc[0] = __ldcg(&ss->bound_w0);
         sm.bc[1] = __ldcg(&ss->bound_w1);
         sm.bc[2] = static_cast<unsigned long long>(static_cast<long long>(__ldcg(&ss->bound_id)));
+        reinterpret_cast<unsigned int*>(sm.u.sort.val)[0] = 0u;  // low-list counter
     }
+    if (threadIdx.x < 6) sm.u.sort.k1[threadIdx.x] = threadIdx.x < 3 ? 0ull : ~0ull;  // low OR / AND
     __syncthreads();
-    sb.k = Key2{sm.bc[0], sm.bc[1]};
-    sb.id = static_cast<int>(static_cast<long long>(sm.bc[2]));
-    sb.ok = sb.id >= 0;
-    __syncthreads();
-    phase_chains(a, sm.sh, sb.ok, sb.k, sb.id);
+    {
+        const int bid = static_cast<int>(static_cast<long long>(sm.bc[2]));
+        const LowSink lk{bid >= 0, Key2{sm.bc[0], sm.bc[1]}, bid, reinterpret_cast<int*>(sm.u.sort.k0),
+                         reinterpret_cast<unsigned int*>(sm.u.sort.val), sm.u.sort.k1};
+        __syncthreads();
+        phase_chains(a, sm.sh, lk);
+    }
     grid.sync();
     stamp(ss, nts);
 
@@ -1474,7 +1591,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         return;
     }
     const bool take_all = total_tok < static_cast<unsigned long long>(a.needed);
-    if (!take_all && sb.ok && small_path(a, sm, grid, nts, total_tok)) return;
+    if (!take_all && __ldcg(&ss->bound_id) >= 0 && small_path(a, sm, grid, nts, total_tok)) return;
     int* S = a.listS;
     unsigned long long nS = 0;
     unsigned int max_bucket = 0;
@@ -1951,12 +2068,12 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         std::fprintf(stderr,
                      "[pbkv select] n_heads=%llu total_tok=%llu take_all=%d host_sort=%d n_S=%llu n_pass=%d "
                      "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
-                     "path=%d n_samp=%u n_low=%llu est_low=%llu n_big=%u "
+                     "path=%d low_ovf=%u n_low=%llu est_low=%llu n_big=%u "
                      "dbg(ns): sortCTA=%llu sortWarp=%llu chainstart=%llu maxbucket=%llu nbig=%llu eff=%llu "
                      "chains=%llu nbits=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
                      hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->path,
-                     hs->n_samp, hs->n_low, hs->est_low, hs->n_big, hs->dbg[0],
+                     hs->low_overflow, hs->n_low, hs->est_low, hs->n_big, hs->dbg[0],
                      hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6], hs->dbg[7]);
     if (hs->host_sort) {
         // ---- fallback: device-wide sort of the selected heads -----------------------------
