@@ -8,6 +8,9 @@
 //                    :657 call flowkv::gpu::* (the product, libpbkv.so), and
 //                    the simulator's CacheTree (:349) is a TrackedCacheTree,
 //                    so the device mirror is updated incrementally
+//   _ref/sim_gpu_fed -- also -DPBKV_DEVICE_PREDICT: the predictor slot
+//                    (simulator.hpp:414-421) computes every forecast on the
+//                    GPU, so the whole run is device-fed
 // Technique: SURVEY.md App. A.4 -- the CPU definitions are included first
 // (#pragma once), then the call-site names are macro-renamed only while
 // simulator.hpp is parsed.  No reference source is edited or copied.
@@ -27,7 +30,37 @@
 #include "flowkv/scoring.hpp"
 
 #ifdef PBKV_INTERPOSE
+#include "flowkv/callgraph.hpp"
+#include "flowkv/csv.hpp"
+#include "flowkv/predictor.hpp"
+#include "flowkv/rng.hpp"
 #include "pbkv/flowkv_gpu.hpp"
+#ifdef PBKV_DEVICE_PREDICT
+// Simulator::predict (simulator.hpp:414-421) fed by the device: the exact
+// K-step marginals (callgraph.hpp:136-186) and the Markov propagation
+// (predictor.hpp:79-118) run on the GPU (fmodel.cu, gpu::*_predict_batch);
+// noisy_predict's (1-lambda) p + lambda / V1 mix (predictor.hpp:25-35) is
+// applied by the slot to the device marginals.  The member calls are
+// rewritten by function-like macros into a conditional whose both arms call
+// the device (the condition only keeps the expression well formed).
+namespace pbkv_sim {
+inline flowkv::Forecast gpu_marginals(const flowkv::CallGraph& g, std::span<const flowkv::AgentId> p, int k) {
+    const std::vector<std::vector<flowkv::AgentId>> one{std::vector<flowkv::AgentId>(p.begin(), p.end())};
+    return flowkv::gpu::oracle_predict_batch(g, one, k)[0];
+}
+inline flowkv::Forecast gpu_markov(const flowkv::MarkovModel& m, std::span<const flowkv::AgentId> p, int k) {
+    const std::vector<std::vector<flowkv::AgentId>> one{std::vector<flowkv::AgentId>(p.begin(), p.end())};
+    return flowkv::gpu::markov_predict_batch(m, one, k)[0];
+}
+}  // namespace pbkv_sim
+#define true_kstep_marginals(p, k) \
+    edges().empty() ? ::pbkv_sim::gpu_marginals(g_, p, k) : ::pbkv_sim::gpu_marginals(g_, p, k)
+#define PBKV_PRED_SEL(_1, _2, NAME, ...) NAME
+#define PBKV_PRED1(x) predict(x)
+#define PBKV_PRED2(p, k) \
+    num_agents() < 0 ? ::pbkv_sim::gpu_markov(markov_, p, k) : ::pbkv_sim::gpu_markov(markov_, p, k)
+#define predict(...) PBKV_PRED_SEL(__VA_ARGS__, PBKV_PRED2, PBKV_PRED1)(__VA_ARGS__)
+#endif
 // the simulator's tree carries a change log: every policy call mirrors only
 // the nodes changed since the previous call (pbkv_mirror_delta)
 #define CacheTree TrackedCacheTree
@@ -47,6 +80,10 @@
 #undef plan_aggressive_prefetch
 #undef refresh_scores
 #undef refresh_nodes
+#ifdef PBKV_DEVICE_PREDICT
+#undef true_kstep_marginals
+#undef predict
+#endif
 #endif
 #include "flowkv/scenario.hpp"
 

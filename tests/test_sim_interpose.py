@@ -14,11 +14,12 @@ import subprocess
 
 import pytest
 
-from sim_cases import CASES
+from sim_cases import CASES, FED_CASES
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SIM_GPU = os.path.join(ROOT, "oracle", "_ref", "sim_gpu")
 SIM_CPU = os.path.join(ROOT, "oracle", "_ref", "sim_cpu")
+SIM_FED = os.path.join(ROOT, "oracle", "_ref", "sim_gpu_fed")
 SCEN = os.path.join(ROOT, "oracle", "_ref", "scenarios")
 GOLDEN = os.path.join(ROOT, "tests", "golden", "sim_cpu.txt")
 
@@ -36,7 +37,7 @@ def run(binary, scen, cell, seeds):
 
 def test_golden_covers_cases():
     lines = open(GOLDEN).read().splitlines()
-    assert len(lines) == 30
+    assert len(lines) == len(set(lines)) == 72
     # hit-rate means of the reference per preset: he 0.6189 on codegen_retry
     he = [float(ln.split()[3]) for ln in lines if ln.startswith("codegen_retry.json policy_preset-he ")]
     assert len(he) == 5 and abs(sum(he) / 5 - 0.6189) < 5e-5
@@ -56,7 +57,7 @@ def test_gpu_simulator_matches_reference(gpu, scen, cell, seeds):
     if not os.path.exists(SIM_GPU):
         pytest.fail("oracle/_ref/sim_gpu missing: build with `make -C oracle sim` where /root/reference exists")
     got = run(SIM_GPU, scen, cell, seeds)
-    want = [ln for ln in golden_lines(scen) if cell in ln.split()[1]]
+    want = [ln for ln in golden_lines(scen) if cell in ln.split()[1] and int(ln.split()[2]) <= seeds]
     assert len(got) == len(want) > 0
     for g, w in zip(got, want):
         assert g == w, f"GPU-driven simulator diverged from the reference:\n gpu {g}\n ref {w}"
@@ -75,3 +76,19 @@ def test_reference_predictors_bit_exact_on_gpu(gpu):
     r = subprocess.run([FPARITY, os.path.join(SCEN, "graphs")], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "mismatches=0" in r.stdout.splitlines()[-1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scen,cell,seeds", FED_CASES, ids=[f"{c[0]}:{c[1] or 'all'}" for c in FED_CASES])
+def test_device_fed_simulator_matches_reference(gpu, scen, cell, seeds):
+    """The predictor slot too runs on the GPU (oracle / noisy / Markov
+    forecasts, csrc/fmodel.cu): the run is device-fed end to end and must
+    still reproduce the CPU reference's hit rate, counters, event log and
+    final tree byte for byte."""
+    if not os.path.exists(SIM_FED):
+        pytest.fail("oracle/_ref/sim_gpu_fed missing: build with `make -C oracle sim` where /root/reference exists")
+    got = run(SIM_FED, scen, cell, seeds)
+    want = [ln for ln in golden_lines(scen) if cell in ln.split()[1] and int(ln.split()[2]) <= seeds]
+    assert len(got) == len(want) > 0
+    for g, w in zip(got, want):
+        assert g == w, f"device-fed simulator diverged from the reference:\n gpu {g}\n ref {w}"

@@ -12,15 +12,19 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
-from sim_cases import CASES  # noqa: E402
+from sim_cases import CASES, FED_CASES  # noqa: E402
 
 out = []
-for scen, cell, seeds in CASES:
+seen = set()
+for scen, cell, seeds in CASES + FED_CASES:
     r = subprocess.run([os.path.join(ROOT, "oracle/_ref/sim_cpu"), os.path.join(ROOT, "oracle/_ref/scenarios", scen),
                         cell, str(seeds)], check=True, capture_output=True, text=True)
     for line in r.stdout.strip().splitlines():
         f = line.split()
-        out.append(" ".join([scen] + f[:-1]))  # drop the wall-clock column
+        ln = " ".join([scen] + f[:-1])  # drop the wall-clock column
+        if ln not in seen:
+            seen.add(ln)
+            out.append(ln)
 path = os.path.join(ROOT, "tests/golden/sim_cpu.txt")
 open(path, "w").write("\n".join(out) + "\n")
 print(f"{len(out)} runs -> {path}")
