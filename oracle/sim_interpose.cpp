@@ -26,8 +26,61 @@
 #include <cstdlib>
 #include <string>
 
+#include <algorithm>
+#include <type_traits>
+#include <vector>
+
 #include "flowkv/policies.hpp"
 #include "flowkv/scoring.hpp"
+
+// Per-call wall time of every policy call site, in both builds (printed to
+// stderr as "timing <op> <calls> <p50_us> <p99_us> <total_ms>" after the runs,
+// when PBKV_SIM_TIMING is set): the drop-in's per-call latency against the
+// reference's on the same scenario (BASELINE configs 1 and 5).
+namespace pbkv_sim {
+enum Op { kSelect, kSelectHE, kPlan, kRefreshScores, kRefreshNodes, kPredict, kNumOps };
+inline const char* op_name(int o) {
+    static const char* n[] = {"select_victims", "select_victims_hierarchical", "plan_prefetch", "refresh_scores",
+                              "refresh_nodes", "predict"};
+    return n[o];
+}
+inline std::vector<double>& samples(int o) {
+    static std::vector<double> v[kNumOps];
+    return v[o];
+}
+template <class F>
+inline auto timed(int op, F&& f) {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto done = [&] {
+        samples(op).push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    };
+    if constexpr (std::is_void_v<decltype(f())>) {
+        f();
+        done();
+    } else {
+        auto r = f();
+        done();
+        return r;
+    }
+}
+inline void report() {
+    for (int o = 0; o < kNumOps; ++o) {
+        std::vector<double> v = samples(o);
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        double tot = 0;
+        for (double x : v) tot += x;
+        std::fprintf(stderr, "timing %s %zu %.2f %.2f %.3f\n", op_name(o), v.size(), v[v.size() / 2],
+                     v[std::min(v.size() - 1, static_cast<std::size_t>(0.99 * static_cast<double>(v.size())))],
+                     tot * 1e-3);
+    }
+}
+}  // namespace pbkv_sim
+#ifdef PBKV_INTERPOSE
+#define PBKV_NS ::flowkv::gpu
+#else
+#define PBKV_NS ::flowkv
+#endif
 
 #ifdef PBKV_INTERPOSE
 #include "flowkv/callgraph.hpp"
@@ -46,11 +99,11 @@
 namespace pbkv_sim {
 inline flowkv::Forecast gpu_marginals(const flowkv::CallGraph& g, std::span<const flowkv::AgentId> p, int k) {
     const std::vector<std::vector<flowkv::AgentId>> one{std::vector<flowkv::AgentId>(p.begin(), p.end())};
-    return flowkv::gpu::oracle_predict_batch(g, one, k)[0];
+    return timed(kPredict, [&] { return flowkv::gpu::oracle_predict_batch(g, one, k)[0]; });
 }
 inline flowkv::Forecast gpu_markov(const flowkv::MarkovModel& m, std::span<const flowkv::AgentId> p, int k) {
     const std::vector<std::vector<flowkv::AgentId>> one{std::vector<flowkv::AgentId>(p.begin(), p.end())};
-    return flowkv::gpu::markov_predict_batch(m, one, k)[0];
+    return timed(kPredict, [&] { return flowkv::gpu::markov_predict_batch(m, one, k)[0]; });
 }
 }  // namespace pbkv_sim
 #define true_kstep_marginals(p, k) \
@@ -64,14 +117,25 @@ inline flowkv::Forecast gpu_markov(const flowkv::MarkovModel& m, std::span<const
 // the simulator's tree carries a change log: every policy call mirrors only
 // the nodes changed since the previous call (pbkv_mirror_delta)
 #define CacheTree TrackedCacheTree
-#define select_victims gpu::select_victims
-#define select_victims_hierarchical gpu::select_victims_hierarchical
-#define plan_conservative_prefetch gpu::plan_conservative_prefetch
-#define plan_aggressive_prefetch gpu::plan_aggressive_prefetch
-#define refresh_scores gpu::refresh_scores
-#define refresh_nodes gpu::refresh_nodes
 #endif
+// the policy call sites (simulator.hpp:434, :464, :618, :636-637, :657):
+// PBKV_NS::* -- flowkv::gpu::* (the drop-in) or flowkv::* (the reference)
+#define select_victims(...) ::pbkv_sim::timed(::pbkv_sim::kSelect, [&] { return PBKV_NS::select_victims(__VA_ARGS__); })
+#define select_victims_hierarchical(...) \
+    ::pbkv_sim::timed(::pbkv_sim::kSelectHE, [&] { return PBKV_NS::select_victims_hierarchical(__VA_ARGS__); })
+#define plan_conservative_prefetch(...) \
+    ::pbkv_sim::timed(::pbkv_sim::kPlan, [&] { return PBKV_NS::plan_conservative_prefetch(__VA_ARGS__); })
+#define plan_aggressive_prefetch(...) \
+    ::pbkv_sim::timed(::pbkv_sim::kPlan, [&] { return PBKV_NS::plan_aggressive_prefetch(__VA_ARGS__); })
+#define refresh_scores(...) ::pbkv_sim::timed(::pbkv_sim::kRefreshScores, [&] { return PBKV_NS::refresh_scores(__VA_ARGS__); })
+#define refresh_nodes(...) ::pbkv_sim::timed(::pbkv_sim::kRefreshNodes, [&] { return PBKV_NS::refresh_nodes(__VA_ARGS__); })
 #include "flowkv/simulator.hpp"
+#undef select_victims
+#undef select_victims_hierarchical
+#undef plan_conservative_prefetch
+#undef plan_aggressive_prefetch
+#undef refresh_scores
+#undef refresh_nodes
 #ifdef PBKV_INTERPOSE
 #undef CacheTree
 #undef select_victims
@@ -126,5 +190,6 @@ int main(int argc, char** argv) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;
     }
+    if (std::getenv("PBKV_SIM_TIMING")) pbkv_sim::report();
     return 0;
 }
