@@ -365,6 +365,16 @@ int pbkv_plan_prefetch(pbkv_ctx* ctx, int64_t bandwidth, int step_duration, doub
 int pbkv_plan_fetch(pbkv_ctx* ctx, int32_t* cand_ids, double* cand_values, int64_t cand_cap, int32_t* selected,
                     int64_t sel_cap);
 
+/* One conservative prefetch round (simulator.hpp:632-681) as one device
+ * decision: for the plan's selected candidates in order, promoted[i] = 1 when
+ * the reference would admit candidate i, and its victims (demoted first, in
+ * order) are victims[victim_end[i-1] .. victim_end[i]).  device_free is the
+ * tree's free device space before the round.  The caller applies the
+ * demotions / promotions to its tree (make_room_on_host etc. as the
+ * reference). */
+int pbkv_prefetch_round(pbkv_ctx* ctx, const int32_t* selected, int64_t n_sel, int64_t device_free, int32_t* promoted,
+                        int64_t* victim_end, int32_t* victims, int64_t cap, int64_t* n_victims);
+
 /* ---- host trees: the reference flowkv::CacheTree (cache.hpp) with a change
  * log for incremental device sync (include/pbkv/tracked_tree.hpp).  For the
  * tests, the bench and Python callers; C++ callers use the class directly. */

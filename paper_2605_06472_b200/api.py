@@ -449,6 +449,24 @@ class Policy:
         return PrefetchPlan.from_arrays(cid, cv, sel, pl.budget_space, pl.budget_bw, pl.displacement_budget,
                                         pl.selected_tokens)
 
+    def prefetch_round(self, selected: Sequence[int], device_free: int) -> tuple[list[int], list[list[int]]]:
+        """One conservative prefetch round (simulator.hpp:632-681) as one device
+        decision: (promoted flags, victims demoted before each candidate)."""
+        sel = np.ascontiguousarray(np.asarray(selected, dtype=np.int32))
+        n = int(sel.size)
+        prom = np.zeros(max(n, 1), dtype=np.int32)
+        vend = np.zeros(max(n, 1), dtype=np.int64)
+        cap = max(int(self.n_nodes), 1)
+        vict = np.zeros(cap, dtype=np.int32)
+        nv = C.c_int64()
+        self._c(_abi.lib().pbkv_prefetch_round(self._h, ptr(sel, C.c_int32), n, int(device_free), ptr(prom, C.c_int32),
+                                                ptr(vend, C.c_int64), ptr(vict, C.c_int32), cap, C.byref(nv)))
+        out, b = [], 0
+        for i in range(n):
+            out.append(vict[b:vend[i]].tolist())
+            b = int(vend[i])
+        return prom[:n].tolist(), out
+
     def plan_conservative_prefetch(self, bandwidth: int, step_duration: int = 1) -> PrefetchPlan:
         """policies.hpp:220-224"""
         return self._plan(bandwidth, step_duration, -1.0)

@@ -428,6 +428,7 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     c.h_flags.assign(nz, 0);
     c.h_last.assign(s.last_access, s.last_access + n);
     c.h_parent.assign(s.parent, s.parent + n);
+    c.h_len.assign(s.len, s.len + n);
     for (std::int64_t i = 0; i < n; ++i) {
         const std::size_t iz = static_cast<std::size_t>(i);
         if (s.tier[i] > PBKV_TIER_ABSENT) invalid("tree soa: bad tier value");
@@ -716,6 +717,7 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
         c.h_depth.resize(nn, 0);
         c.h_flags.resize(nn, 0);
         c.h_last.resize(nn, 0);
+        c.h_len.resize(nn, 0);
     }
     // placement of every record's entries; class / structure bookkeeping
     std::int64_t n_ent = 0;
@@ -763,6 +765,7 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
         c.h_depth[id] = r.depth;
         c.h_flags[id] = static_cast<std::uint8_t>(r.tier | (r.retired ? kFlagRetired : 0));
         c.h_last[id] = r.last_access;
+        c.h_len[id] = r.len;
         c.max_depth = std::max(c.max_depth, static_cast<int>(r.depth));
         DeltaRec& o = recs[k];
         o.id = r.id;
@@ -1600,6 +1603,97 @@ int pbkv_plan_fetch(pbkv_ctx* c, int32_t* cand_ids, double* cand_values, int64_t
         need(c != nullptr, "null ctx");
         need(c->plan_valid, "no prefetch plan to fetch");
         copy_plan(*c, cand_ids, cand_values, cand_cap, selected, sel_cap);
+    });
+}
+
+// ---- the prefetch round (simulator.hpp:632-681), conservative mode -------------------
+// The reference admits the plan's candidates one by one: when candidate i does
+// not fit in free device space it runs select_victims_hierarchical(need_i)
+// under locks on the remaining candidates' ancestry and the pinned paths, and
+// takes that order's retired prefix (a conservative round never displaces
+// active cache); short of need_i the candidate is skipped.  Every lock is
+// active (a candidate has value > 0, so its parent and ancestors carry active
+// access tags; pinned paths belong to decoding workflows), a lock only makes
+// ancestors ineligible, and retired subtrees hold only retired nodes -- so the
+// retired nodes' order is the same under every candidate's lock set, and a
+// promoted candidate (active) never enters it.  The greedy frontier resumes
+// where a demoted prefix ended.  Hence the whole round is ONE hierarchical
+// decision for the round's total length followed by a scan that hands each
+// candidate the next retired victims (device_free bookkeeping as the
+// reference: demotions add, promotions subtract).
+int pbkv_prefetch_round(pbkv_ctx* c, const int32_t* selected, int64_t n_sel, int64_t device_free, int32_t* promoted,
+                        int64_t* victim_end, int32_t* victims, int64_t cap, int64_t* n_victims) {
+    return api(c, [&] {
+        need(c && n_victims && (n_sel == 0 || (selected && promoted && victim_end)), "null argument");
+        need(c->n >= 1, "no tree mirrored");
+        set_device(*c);
+        *n_victims = 0;
+        std::int64_t total = 0;
+        for (int64_t i = 0; i < n_sel; ++i) {
+            need(selected[i] > 0 && selected[i] < c->n, "prefetch round: candidate id out of range");
+            total += c->h_len[static_cast<std::size_t>(selected[i])];
+        }
+        std::vector<int> order;  // the hierarchical victim order for the round's total length
+        if (total > 0) {
+            constexpr long long kEpiVictims = 1 << 16;
+            c->hvictims.reserve(static_cast<std::size_t>(kEpiVictims));
+            c->epi_vict = c->hvictims.p;
+            c->epi_cap = kEpiVictims;
+            SelectCounts o;
+            try {
+                o = select_core(*c, PBKV_POLICY_HE, PBKV_SCORE_CACHED, total, nullptr, 0, nullptr);
+            } catch (...) {
+                c->epi_vict = nullptr;
+                throw;
+            }
+            c->epi_vict = nullptr;
+            if (o.n_victims > c->epi_cap || !c->epi_vict_valid) {
+                c->hvictims.reserve(static_cast<std::size_t>(o.n_victims));
+                PBKV_CUDA(cudaMemcpyAsync(c->hvictims.p, c->vid_out.p, o.n_victims * sizeof(int), cudaMemcpyDeviceToHost,
+                                          c->stream));
+                PBKV_CUDA(cudaStreamSynchronize(c->stream));
+            }
+            order.assign(c->hvictims.p, c->hvictims.p + o.n_victims);
+        }
+        // the reference's per-candidate loop over the one order
+        std::size_t at = 0;
+        std::int64_t out = 0, free_tok = device_free;
+        for (int64_t i = 0; i < n_sel; ++i) {
+            const std::size_t id = static_cast<std::size_t>(selected[i]);
+            promoted[i] = 0;
+            const bool host = (c->h_flags[id] & kFlagTierMask) == PBKV_TIER_HOST;
+            const int p = c->h_parent[id];
+            const bool dev_parent = p >= 0 && (c->h_flags[static_cast<std::size_t>(p)] & kFlagTierMask) == PBKV_TIER_DEVICE;
+            if (host && dev_parent) {  // simulator.hpp:647-648
+                const std::int64_t len = c->h_len[id];
+                const std::int64_t needt = len - free_tok;
+                bool admit = true;
+                if (needt > 0) {  // :650-671: the retired prefix of the order from `at`
+                    std::size_t q = at;
+                    std::int64_t freed = 0;
+                    while (q < order.size() && freed < needt &&
+                           (c->h_flags[static_cast<std::size_t>(order[q])] & kFlagRetired)) {
+                        freed += c->h_len[static_cast<std::size_t>(order[q])];
+                        ++q;
+                    }
+                    if (freed < needt) {
+                        admit = false;  // :671 cannot admit this candidate safely
+                    } else {
+                        if (out + static_cast<std::int64_t>(q - at) > cap) throw ApiError(PBKV_EARG, "victim capacity too small");
+                        if (q > at) std::memcpy(victims + out, order.data() + at, (q - at) * sizeof(int32_t));
+                        out += static_cast<std::int64_t>(q - at);
+                        at = q;
+                        free_tok += freed;
+                    }
+                }
+                if (admit) {
+                    promoted[i] = 1;
+                    free_tok -= len;
+                }
+            }
+            victim_end[i] = out;
+        }
+        *n_victims = out;
     });
 }
 

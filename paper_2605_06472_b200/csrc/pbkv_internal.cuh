@@ -201,6 +201,7 @@ struct Context {
     // host copies of the node fields the host-side planning reads (classes,
     // deferral placement, sharding)
     std::vector<int> h_depth;
+    std::vector<int> h_len;  // token length of every node (host copy: the prefetch round's scan)
     std::vector<std::uint8_t> h_flags;
     std::vector<unsigned long long> h_last;
     // pinned staging + completion event of pbkv_mirror_delta's upload
