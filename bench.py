@@ -162,7 +162,7 @@ class ClockSampler:
 
 
 def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: int = 0,
-                            plan_bandwidth: int | None = None):
+                            plan_bandwidth: int | None = None, round_probe=None):
     """The reference policy code (oracle/_ref) on the same workload: per
     decision, refresh every node's score (refresh_nodes, scoring.hpp:95) and
     select_victims_hierarchical (policies.hpp:108)."""
@@ -201,6 +201,20 @@ def cpu_reference_decisions(cfg: str, needed_frac: float, decisions: int, rank: 
         out["plan_times"] = pt
         out["plan_selected"] = list(pl.selected)
         out["plan_candidates"] = [c[0] for c in pl.candidates]
+    if round_probe is not None and round_probe[0] is not None:
+        # one candidate step of the reference prefetch round: HE selection of
+        # the candidate's length under the ancestry locks of every candidate
+        first, sel_ids = round_probe
+        par = soa.parent
+        locked = set()
+        for s in sel_ids.tolist():
+            v = int(par[s])
+            while v > 0:
+                locked.add(v)
+                v = int(par[v])
+        t0 = time.perf_counter()
+        t.select(POLICY_HE, max(1, int(soa.len[first])), sorted(locked))
+        out["round_candidate_s"] = time.perf_counter() - t0
     return out
 
 
@@ -626,6 +640,24 @@ def main():
         }
         prefetch["roofline"]["frac"] = prefetch["roofline"]["achieved"] / prefetch["roofline"]["peak"]
         prefetch["_plan"] = plan
+        # the round that applies the plan (simulator.hpp:632-681) with the
+        # device full (device_free = 0: every candidate needs victims), fused
+        # into one hierarchical decision + the retired-prefix scan
+        sel_ids = plan.selected_ids
+        pol.prefetch_round(sel_ids, 0)
+        rw = []
+        for _ in range(reps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            prom, vics = pol.prefetch_round(sel_ids, 0)
+            rw.append(1e3 * (time.perf_counter() - w0))
+        prefetch["round"] = {
+            "what": "pbkv_prefetch_round over the plan's selected candidates with device_free = 0 (host wall of "
+                    "the public call: one hierarchical decision + the per-candidate retired-prefix scan)",
+            "candidates": int(sel_ids.size), "promoted": int(sum(prom)), "victims": int(sum(len(v) for v in vics)),
+            "ms_mean": statistics.mean(rw), "ms_p99": float(np.percentile(rw, 99))}
+        prefetch["_round_first"] = (int(sel_ids[0]) if sel_ids.size else None, sel_ids)
 
     # ---- e2e through the host C ABI, with the tree changing between decisions ----------
     # Before every decision the host tree (the reference CacheTree, tracked)
@@ -721,7 +753,15 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         r = cpu_reference_decisions(args.config, args.needed_frac, args.cpu_decisions,
-                                    plan_bandwidth=max(1, used // 50) if prefetch else None)
+                                    plan_bandwidth=max(1, used // 50) if prefetch else None,
+                                    round_probe=prefetch["_round_first"] if prefetch else None)
+        if r and prefetch and "round_candidate_s" in r:
+            prefetch["round"]["cpu_reference"] = {
+                "per_candidate_ms": 1e3 * r["round_candidate_s"], "cores": 1, "kind": "reference",
+                "round_estimate_s": r["round_candidate_s"] * len(prefetch["_round_first"][1]),
+                "sample": "one select_victims_hierarchical under the round's ancestry locks (simulator.hpp:652-657), "
+                          "the per-candidate step of the reference loop; the round estimate multiplies it by the "
+                          "candidate count"}
         if r and prefetch and "plan_times" in r:
             plan = prefetch["_plan"]
             prefetch["cpu_baseline"] = {"value": 1e3 * statistics.mean(r["plan_times"]), "unit": "ms/plan",

@@ -92,7 +92,7 @@ def _case(seed, n_ops=(20, 90), n_wf=(3, 10)):
     nw = int(rng.integers(*n_wf))
     agents = int(rng.integers(2, 6))
     ops, live = WL.random_tree_ops(rng, n_ops=int(rng.integers(*n_ops)), n_wf=nw, agents=agents, alphabet=3,
-                                   max_len=7, term_frac=0.4)
+                                   max_len=7, term_frac=0.4 if seed % 3 else 0.1)
     t = HostTree()
     t.apply_ops(ops.words)
     dev_cap = int(t.export().scalars["device_used"]) + int(rng.integers(0, 12))
@@ -130,8 +130,16 @@ def test_prefetch_round_equals_reference_loop(gpu, seed):
     if not selected:
         pytest.skip("empty plan")
     pinned = _active_pinned(soa, rng, 2)
+    free = soa.scalars["device_capacity"] - soa.scalars["device_used"]
     want_p, want_v = reference_round(ops.words, dev_cap, wf, P, selected, pinned)
-    got_p, got_v = pol.prefetch_round(selected, soa.scalars["device_capacity"] - soa.scalars["device_used"])
+    got_p, got_v = pol.prefetch_round(selected, free)
+    assert got_p == want_p
+    assert got_v == want_v
+    # every candidate of the ranking (more demand than the conservative budget
+    # admits): the round must skip exactly where the reference does
+    every = [c[0] for c in plan.candidates]
+    want_p, want_v = reference_round(ops.words, dev_cap, wf, P, every, pinned)
+    got_p, got_v = pol.prefetch_round(every, free)
     assert got_p == want_p
     assert got_v == want_v
 
