@@ -37,7 +37,7 @@ CONFIGS = {
     # name: (n_nodes, n_workflows, K)
     "c2": (10_000, 256, 4),
     "c3": (1_000_000, 4096, 8),
-    "c4": (8_000_000, 16384, 8),  # config 4 on one GPU (the sharded runs use N x c3 shards)
+    "c4": (8_000_000, 16384, 8),  # config 4: one GPU, or strong-scaled over N ranks (run_sharded)
 }
 AGENTS = 16
 GAMMA = 0.7
@@ -346,59 +346,51 @@ def pipeline_c2(torch, dev, reps: int = 20):
     return out
 
 
-def shard_workload(cfg: str, rank: int, world: int, dist, torch, dev):
-    """Weak scaling: rank r holds a C3-shaped shard (synthetic seed 12345 + r)
-    of one global tree whose spine (root + the shared-prefix node) is common
-    to all ranks; global node ids 2 + r*stride + local id, WorkflowIds
-    r*W + local (contiguous blocks per rank).  At 8 ranks: 8 M nodes (config 4)."""
+def shard_workload(cfg: str, rank: int, world: int):
+    """Strong scaling of config 4: every rank generates the same global
+    8 M-node x 16 K-workflow tree (deterministic synthetic generator), the
+    tree is partitioned by subtree into `world` node-set shards (spine = the
+    root and the shared prefix, replicated; workflows co-located with their
+    group subtrees: contiguous WorkflowId blocks), and the rank keeps its own
+    shard resident.  Forecasts: the rank's own workflows."""
     import workloads as WL
     from paper_2605_06472_b200 import shard as SH
     from paper_2605_06472_b200.api import HostTree
 
     n_nodes, n_wf, K = CONFIGS[cfg]
     t = HostTree()
-    t.synth(n_nodes=n_nodes, n_workflows=n_wf, agents=AGENTS, seed=12345 + rank)
+    t0 = time.perf_counter()
+    t.synth(n_nodes=n_nodes, n_workflows=n_wf, agents=AGENTS, seed=4)
     soa = t.export()
-    depth = SH._depths(soa.parent.astype(np.int64))
-    sp_local = np.nonzero(depth <= 1)[0].astype(np.int32)
-    assert sp_local.tolist() == [0, 1], "synthetic tree: spine must be the root and the shared prefix"
-    stride = 1 << 24
-    gids = (2 + rank * stride + np.arange(soa.n_nodes)).astype(np.int64)
-    gids[0], gids[1] = 0, 1
-    soa.acc_wf[: soa.n_entries] += rank * n_wf
-    # global spine fields (len/tier equal on all ranks; ever summed, last max, retired all)
-    loc = torch.tensor([int(soa.ever_tagged[1]), int(soa.last_access[1]), int(not soa.retired[1])],
-                       dtype=torch.int64, device=dev)
-    ever = loc[0:1].clone(); dist.all_reduce(ever)
-    last = loc[1:2].clone(); dist.all_reduce(last, op=dist.ReduceOp.MAX)
-    alive = loc[2:3].clone(); dist.all_reduce(alive, op=dist.ReduceOp.MAX)
-    spine = SH.Spine(gid=np.array([0, 1]), parent=np.array([-1, 0]), depth=np.array([0, 1]),
-                     len=soa.len[[0, 1]].astype(np.int64), tier=soa.tier[[0, 1]].astype(np.int64),
-                     retired=np.array([0, 0 if int(alive.item()) else 1]), ever=np.array([0, int(ever.item())]),
-                     last=np.array([0, int(last.item())], dtype=np.uint64), score=np.zeros(2))
-    shard = SH.Shard(rank, soa, gids.astype(np.int32), sp_local, rank * n_wf, (rank + 1) * n_wf, spine)
-    rng = np.random.default_rng(12345 + rank)
+    del t
+    build_s = time.perf_counter() - t0
+    rng = np.random.default_rng(4)
     wf = np.array(WL.workflows_of(soa), dtype=np.int64)
     P = WL.random_forecasts(rng, wf.size, K, AGENTS + 1)
-    locked = gids[np.array(WL.pinned_paths(soa, rng, 0.01), dtype=np.int64)]
-    return shard, wf, P, locked, K
+    locked = np.array(WL.pinned_paths(soa, rng, 0.01), dtype=np.int64)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    shard = SH.partition(soa, world, only=rank)[0]
+    mine = (wf >= shard.wf_lo) & (wf < shard.wf_hi)
+    return shard, wf[mine], P[mine], locked, K, used, soa.n_nodes, build_s
 
 
 def run_sharded(args, rank, world, local, dist, torch):
-    """config 4: one eviction decision over the sharded tree per step (local
-    score + select, spine products all-gather, exact spine chains, record
-    all-gather, merge + cut); max over ranks of the device-event time."""
+    """config 4, strong scaling: one eviction decision over the whole 8 M-node
+    tree per step, its node set sharded over the ranks (local score + select,
+    spine products and records exchanged with two NCCL all-gathers, exact
+    spine chains or their interval placement, merge + cut); max over ranks of
+    the device-event time.  e2e: the same decision through the public sharded
+    API with every rank's forecasts uploaded from host memory and the victim
+    list returned to the host."""
     from paper_2605_06472_b200 import shard as SH
     from paper_2605_06472_b200._abi import POLICY_HE, SCORE_RECOMPUTE
 
+    cfg = "c4" if args.config == "c3" else args.config
     dev = torch.device("cuda", local)
-    shard, wf, P, locked, K = shard_workload(args.config, rank, world, dist, torch, dev)
+    shard, wf, P, locked, K, used, n_global, build_s = shard_workload(cfg, rank, world)
     sp = SH.ShardedPolicy(shard, num_agents=AGENTS, k=K, gamma=GAMMA, device=local)
     sp.pol.put_forecasts(wf, P)
-    soa = shard.soa
-    used_t = torch.tensor([int(soa.len[soa.tier == 0][1:].sum())], dtype=torch.int64, device=dev)
-    dist.all_reduce(used_t)
-    needed = max(1, int(args.needed_frac * int(used_t.item())))
+    needed = max(1, int(args.needed_frac * used))
     lk = [int(x) for x in locked.tolist()]
 
     def step():
@@ -425,25 +417,47 @@ def run_sharded(args, rank, world, local, dist, torch):
             times.append(e0.elapsed_time(e1))
     dist.barrier()
     k1, _ = sp.pol.launches()
-    tt = torch.tensor([statistics.mean(times), float(np.percentile(times, 99))], dtype=torch.float64, device=dev)
+    # e2e: forecasts from (pageable) host memory + the decision, host wall
+    e2e = []
+    for _ in range(max(3, min(10, args.steps))):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        dist.barrier()
+        w0 = time.perf_counter()
+        sp.pol.put_forecasts(wf, P)
+        res = step()
+        e2e.append(1e3 * (time.perf_counter() - w0))
+    dist.barrier()
+    tt = torch.tensor([statistics.mean(times), float(np.percentile(times, 99)), statistics.mean(e2e)],
+                      dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    nn = torch.tensor([soa.n_nodes - (2 if rank else 0)], dtype=torch.int64, device=dev)
-    dist.all_reduce(nn)
-    ms, p99 = tt.tolist()
-    total_nodes = int(nn.item())
+    ms, p99, e2e_ms = tt.tolist()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # the reference on one host core: C3 per-node rate (a C4 decision is ~8 s)
+        r = cpu_reference_decisions("c3", args.needed_frac, 1)
+        if r:
+            cpu = {"value": r["n_nodes"] / statistics.mean(r["times"]), "unit": "nodes/s", "cores": 1,
+                   "kind": "reference",
+                   "sample": f"1 decision on the c3 tree (refresh_nodes all + select_victims_hierarchical), "
+                             f"{statistics.mean(r['times']):.3f} s; the reference is single-threaded per decision"}
     if rank == 0:
-        n_nodes, n_wf, _ = CONFIGS[args.config]
+        n_nodes, n_wf, _ = CONFIGS[cfg]
         line = {
-            "metric": METRIC, "value": total_nodes / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world,
+            "metric": METRIC, "value": n_global / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config 4 shape, weak scaling: {world} x ({n_nodes} nodes x {n_wf} workflows) "
-                                   f"x K={K} sharded by subtree, HE select at {args.needed_frac:.2%} of global need",
-                       "n_nodes": total_nodes, "needed_tokens": needed, "n_victims": len(res[0]),
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 4: {n_nodes} nodes x {n_wf} workflows x K={K} sharded by subtree over "
+                                   f"{world} GPUs, HE select at {args.needed_frac:.2%} of global need",
+                       "n_nodes": n_global, "needed_tokens": needed, "n_victims": len(res[0]),
                        "l2": "flushed between steps (256 MiB write)", "parallelism": f"node-set shards x{world}"},
             "p99_decision_ms": p99, "gpu_launches": int(k1 - k0), "clocks": clk.result,
-            "cpu_baseline": None,
-            "e2e": None,
+            "cpu_baseline": cpu,
+            "e2e": {"value": n_global / (e2e_ms * 1e-3), "unit": "nodes/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size), "d2h_bytes_per_step": int(4 * len(res[0]) + 24),
+                    "what": "per rank: forecasts from host memory + the sharded decision (victims to the host); "
+                            "max over ranks of the host wall"},
+            "tree_build_s": build_s,
         }
         print(json.dumps(line))
     dist.barrier()

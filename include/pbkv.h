@@ -130,6 +130,11 @@ int pbkv_ctx_set_timing(pbkv_ctx* ctx, int enabled);
 /* Device time of the dominant kernels of the most recent timed selection
  * (milliseconds, CUDA events on the ctx stream): [0] the light Eq. 2 + key
  * pass (score_light_kernel), [1] the persistent selection kernel. */
+/* Orders the context's stream after all work enqueued so far on `stream` (a
+ * cudaStream_t; NULL = the legacy default stream), without a host
+ * synchronisation: callers that produce device inputs on their own stream
+ * (e.g. PyTorch's current stream) call this before passing them. */
+int pbkv_ctx_wait_stream(pbkv_ctx* ctx, void* stream);
 int pbkv_ctx_kernel_timings(pbkv_ctx* ctx, float* ms2);
 /* %globaltimer stamps (ns) taken by the selection kernel at its phase
  * boundaries during the most recent selection (diagnostics). */

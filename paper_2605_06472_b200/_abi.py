@@ -226,6 +226,7 @@ def lib() -> C.CDLL:
         "pbkv_set_remaining": ([vp, _i64p, C.c_int64, _i64p, _i32p], C.c_int),
         "pbkv_plan_prefetch": ([vp, C.c_int64, C.c_int, C.c_double, _i32p, _f64p, C.c_int64, _i32p, C.c_int64,
                                 C.POINTER(PrefetchPlanC)], C.c_int),
+        "pbkv_ctx_wait_stream": ([vp, vp], C.c_int),
         "pbkv_prefetch_round": ([vp, _i32p, C.c_int64, C.c_int64, _i32p, _i64p, _i32p, C.c_int64, _i64p], C.c_int),
         "pbkv_plan_fetch": ([vp, _i32p, _f64p, C.c_int64, _i32p, C.c_int64], C.c_int),
         "pbkv_predictor_load": ([vp, C.POINTER(PredictorCfg), C.POINTER(PredictorWeights)], C.c_int),

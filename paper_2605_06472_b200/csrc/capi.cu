@@ -1192,6 +1192,7 @@ int pbkv_ctx_create(pbkv_ctx** out, const pbkv_cfg* cfg) {
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_delta, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_class, cudaEventDisableTiming));
+        PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_caller, cudaEventDisableTiming));
         PBKV_CUDA(cudaEventCreateWithFlags(&c->ev_rows, cudaEventDisableTiming));
         c->selstate.reserve(sel_state_bytes());
         c->hselstate.reserve(2 * sel_state_bytes());  // [0] readback, [1] initial-state template
@@ -1222,6 +1223,7 @@ int pbkv_ctx_destroy(pbkv_ctx* c) {
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_delta) cudaEventDestroy(c->ev_delta);
     if (c->ev_class) cudaEventDestroy(c->ev_class);
+    if (c->ev_caller) cudaEventDestroy(c->ev_caller);
     if (c->ev_rows) cudaEventDestroy(c->ev_rows);
     cudaStream_t s = c->stream, side = c->side;
     delete c;  // DevBuf / PinBuf destructors free the device and pinned memory
@@ -1271,6 +1273,15 @@ int pbkv_ctx_launches(pbkv_ctx* c, int64_t* kernels, int64_t* lib_calls) {
         need(c, "null ctx");
         if (kernels) *kernels = c->launches;
         if (lib_calls) *lib_calls = c->lib_calls;
+    });
+}
+
+int pbkv_ctx_wait_stream(pbkv_ctx* c, void* stream) {
+    return api(c, [&] {
+        need(c, "null ctx");
+        set_device(*c);
+        PBKV_CUDA(cudaEventRecord(c->ev_caller, static_cast<cudaStream_t>(stream)));
+        PBKV_CUDA(cudaStreamWaitEvent(c->stream, c->ev_caller, 0));
     });
 }
 

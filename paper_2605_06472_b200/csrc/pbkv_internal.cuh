@@ -213,6 +213,7 @@ struct Context {
     // heavy children): reused once ev_class has passed
     PinBuf<unsigned char> hclass;
     cudaEvent_t ev_class = nullptr;
+    cudaEvent_t ev_caller = nullptr;  // pbkv_ctx_wait_stream
     bool class_pending = false;
     // mirror bookkeeping of pbkv_mirror_sync: which host tree this context
     // mirrors (TrackedCacheTree uid) and the change-log position it has applied

@@ -157,7 +157,7 @@ def _depths(parent: np.ndarray) -> np.ndarray:
         anc = np.where(more, anc[anc], 0)
 
 
-def partition(soa: SoAArrays, n_ranks: int, spine_depth: int = 1) -> list[Shard]:
+def partition(soa: SoAArrays, n_ranks: int, spine_depth: int = 1, only: int | None = None) -> list[Shard]:
     """Splits a global tree into n_ranks shards.  Spine = nodes of depth <=
     spine_depth; the subtrees below it go to ranks in contiguous global-id
     blocks of roughly equal size.  Requires that every non-spine node is
@@ -226,6 +226,8 @@ def partition(soa: SoAArrays, n_ranks: int, spine_depth: int = 1) -> list[Shard]
                   last=soa.last_access[spine_ids].astype(np.uint64), score=soa.score[spine_ids].astype(np.float64))
     shards = []
     for r in range(n_ranks):
+        if only is not None and r != only:  # one rank's shard (every rank partitions the same tree)
+            continue
         keep = np.nonzero(is_spine | (owner == r))[0]  # sorted global ids
         loc = np.full(n, -1, dtype=np.int64)
         loc[keep] = np.arange(keep.size)
@@ -302,7 +304,15 @@ class ShardedPolicy:
         self.spine_out = torch.zeros(max(1, shard.spine.n) * SPINE_DTYPE.itemsize, dtype=torch.uint8,
                                      device=self.dev)
         self.result = torch.zeros(3, dtype=torch.int64, device=self.dev)
-        self.pmax = None  # max spine-product count over ranks (fixed per mirrored tree)
+        self.pmax = None  # max spine-product count over ranks (refreshed every decision)
+
+    def order_after_torch(self) -> None:
+        """The pbkv stream waits for torch's current stream (inputs built and
+        outputs zero-filled there), with no host synchronisation."""
+        import torch
+
+        self.pol._c(_abi.lib().pbkv_ctx_wait_stream(self.pol.handle,
+                                                      C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)))
 
     def local_ids(self, gids) -> np.ndarray:
         """Local ids of the given global ids that this shard holds."""
@@ -315,6 +325,7 @@ class ShardedPolicy:
     def local_select(self, policy: int, score_mode: int, needed: int, locked_local_dev, n_locked: int,
                      want_count: bool = True):
         L = _abi.lib()
+        self.order_after_torch()
         rc = L.pbkv_shard_select(self.pol.handle, int(policy), int(score_mode), int(needed),
                                  C.cast(C.c_void_p(locked_local_dev or None), C.POINTER(C.c_int32)), int(n_locked),
                                  C.cast(C.c_void_p(self.cand.data_ptr()), C.POINTER(CandC)),
@@ -336,6 +347,7 @@ class ShardedPolicy:
         total = int(sum(int(self.shard.soa.acc_off[s + 1] - self.shard.soa.acc_off[s])
                         for s in self.shard.spine_local.tolist())) * self.pol.k
         out = torch.zeros(max(total, 1), dtype=torch.float64, device=self.dev)
+        self.order_after_torch()
         self.pol._c(_abi.lib().pbkv_shard_spine_products(self.pol.handle, C.cast(C.c_void_p(out.data_ptr()),
                                                                                  C.POINTER(C.c_double)),
                                                          ptr(counts, C.c_int64)))
@@ -344,6 +356,7 @@ class ShardedPolicy:
     def chain_sums(self, x_dev, offsets: np.ndarray) -> np.ndarray:
         out = np.zeros(max(offsets.size - 1, 1), dtype=np.float64)
         off = np.ascontiguousarray(offsets, dtype=np.int64)
+        self.order_after_torch()
         self.pol._c(_abi.lib().pbkv_chain_sum(self.pol.handle, C.cast(C.c_void_p(x_dev.data_ptr()),
                                                                       C.POINTER(C.c_double)),
                                               ptr(off, C.c_int64), int(off.size - 1), ptr(out, C.c_double)))
@@ -356,6 +369,7 @@ class ShardedPolicy:
         res = torch.zeros(3, dtype=torch.int64, device=self.dev)
         st = np.array(starts, dtype=np.int64)
         ln = np.array(lens, dtype=np.int64)
+        self.order_after_torch()
         self.pol._c(_abi.lib().pbkv_merge_cut(self.pol.handle,
                                               C.cast(C.c_void_p(runs_dev.data_ptr()), C.POINTER(CandC)),
                                               ptr(st, C.c_int64), ptr(ln, C.c_int64), int(st.size), int(needed),
@@ -451,10 +465,12 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     he_rc = policy == POLICY_HE and score_mode == SCORE_RECOMPUTE and sp.n > 0
     if he_rc:
         prod, pcnt = rp.spine_products()
-        if rp.pmax is None:
-            t = torch.tensor([prod.numel()], dtype=torch.int64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            rp.pmax = int(t.item())
+        # the largest rank's product count, every decision (it moves with the
+        # workflows tagging the spine; a stale maximum would desynchronise the
+        # header sizes across ranks)
+        t = torch.tensor([prod.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rp.pmax = int(t.item())
         pad = torch.zeros(rp.pmax, dtype=torch.float64, device=dev)
         pad[: prod.numel()] = prod
         pcnt_t = torch.from_numpy(np.ascontiguousarray(pcnt, dtype=np.int64)).to(dev)
