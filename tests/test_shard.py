@@ -197,6 +197,8 @@ def test_chain_sum_bit_exact(gpu):
 
     h = _P()
     h.pol = pol
+    h.dev = torch.device("cuda", 0)
+    h.order_after_torch = lambda: SH.ShardedPolicy.order_after_torch(h)
     xt = torch.from_numpy(x).cuda()
     got = SH.ShardedPolicy.chain_sums(h, xt, off)
     for i, s in enumerate(segs):
