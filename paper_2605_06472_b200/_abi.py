@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libpbkv.so")
+LIB_PATH = os.environ.get("PBKV_LIB") or os.path.join(PKG, "libpbkv.so")  # PBKV_LIB: variant builds (tools)
 
 PBKV_OK, PBKV_EINVAL, PBKV_ECUDA, PBKV_ENOMEM, PBKV_EARG = 0, 1, 2, 3, 4
 TIER_DEVICE, TIER_HOST, TIER_ABSENT = 0, 1, 2
