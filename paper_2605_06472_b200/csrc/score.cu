@@ -74,7 +74,11 @@ __device__ __forceinline__ void load_row(const double* p, double* v) {
 // together; then total += gs[k] * m[k] in step order (scoring.hpp:56-57).
 template <int kK>
 __device__ __forceinline__ void eq2_entry_k(const ScoreArgs& s, int slot, unsigned long long b, double& total) {
-    if (b && !(b & (b - 1))) {  // one agent: the K terms are precomputed (Pg), one 64-byte line
+    if (!b) {  // no agent inside [0, A): no row is read, so the slot's state is checked here
+        if (__ldg(s.fstate + slot) != 1) total = CUDART_NAN;  // missing / short: raised like a poisoned row
+        return;
+    }
+    if (!(b & (b - 1))) {  // one agent: the K terms are precomputed (Pg), one 64-byte line
         const double* row = s.Pg + (static_cast<std::size_t>(slot) * s.V1 + (__ffsll(static_cast<long long>(b)) - 1)) * kK;
         double v[kK];
         load_row<kK>(row, v);

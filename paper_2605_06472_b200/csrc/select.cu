@@ -1321,6 +1321,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     grid.sync();
     stamp(ss, nts);
     // S2: bucket offsets; the check that the cut lies among the low heads
+    const unsigned long long s2t0 = gtimer();
     constexpr int kPer = kBins / kPThreads;
     unsigned int vc[kPer], sc = 0, mx = 0;
     unsigned long long vw[kPer], vs[kPer], sw = 0, scs = 0;
@@ -1370,7 +1371,10 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
         ex_w += vw[j];
         ex_s += vs[j];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) ss->path = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ss->path = 1;
+        ss->dbg[3] = gtimer() - s2t0;  // S2 offsets (CTA 0)
+    }
     __syncthreads();
     {
         const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
@@ -1397,6 +1401,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
             }
         }
     }
+    if (threadIdx.x == 0) atomicMax(&ss->dbg[4], gtimer() - s2t0);  // S2 total, slowest CTA
     grid.sync();
     stamp(ss, nts);
     // S3: rank every bucket with the token / chain-size prefixes of the smaller

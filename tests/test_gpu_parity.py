@@ -217,3 +217,15 @@ def test_errors_match_reference(gpu):
     pol2.put_forecasts([8], np.array([[[0.5, 0.3, 0.2]]]))
     with pytest.raises(ValidationError, match="missing forecast for active workflow 7"):
         pol2.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
+    # an entry whose agent bits all fall outside [0, A) reads no forecast row:
+    # the missing forecast must still raise (scoring.hpp:70-71)
+    t3 = HostTree()
+    t3.apply_ops(OpStream().insert([5, 6], 9, 3).insert([5, 7], 10, 0).words)
+    for K in (1, 3, 8):
+        pol3 = Policy(num_agents=2, k=K, gamma=0.7)
+        pol3.mirror(t3)
+        pol3.put_forecasts([10], np.full((1, K, 3), 1.0 / 3.0))
+        with pytest.raises(ValidationError, match="^missing forecast for active workflow 9$"):
+            pol3.score_all()
+        with pytest.raises(ValidationError, match="missing forecast for active workflow 9"):
+            pol3.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
