@@ -88,6 +88,9 @@ struct SelState {
     unsigned long long n_victims, freed;
     int shortfall, n_ts;
     unsigned int low_overflow;  // a CTA's low buffer overflowed: no small path
+    unsigned int small_done;    // S1 CTAs finished (the last one lays out the buckets)
+    unsigned int small_ok;      // 1 the small path proceeds, 2 it is abandoned
+    unsigned int n_task;        // rank tasks of the small path's big buckets
     int bound_id;               // small-cut bound (key, id); -1: no small path
     unsigned long long bound_w0, bound_w1;
     int path;                   // 0 full radix path, 1 small-cut path, 2 small path abandoned
@@ -307,6 +310,7 @@ struct SelArgs {
     unsigned int* sm_cur;
     unsigned int* sm_off;
     unsigned int* sm_big;
+    unsigned int* sm_task;  // [kBins] first rank task of each big bucket
     unsigned long long* sm_w;   // [kBins] weights, chain sizes, and their bucket prefixes
     unsigned long long* sm_cs;
     unsigned long long* sm_wpre;
@@ -1245,6 +1249,90 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
             atomicAdd(&a.sm_cs[b], sm.u.hist.cs[b]);
         }
     }
+    // the last CTA to finish turns the histogram into the bucket layout once:
+    // offsets, token / chain-size prefixes, the check that the cut lies among
+    // the low heads, the list of buckets ranked by tiles and their first tasks
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sm.bc[0] = atomicAdd(&a.ss->small_done, 1u);
+    __syncthreads();
+    if (sm.bc[0] != gridDim.x - 1) return;
+    __threadfence();
+    constexpr int kPer = kBins / kPThreads;
+    constexpr int kChunkS = kPThreads / 8;
+    unsigned int vc[kPer], mx = 0;
+    unsigned long long vw[kPer], vs[kPer], sc = 0, sw = 0, ss_ = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        vc[j] = __ldcg(&a.sm_c[d]);
+        vw[j] = __ldcg(&a.sm_w[d]);
+        vs[j] = __ldcg(&a.sm_cs[d]);
+        sc += vc[j];
+        sw += vw[j];
+        ss_ += vs[j];
+        mx = max(mx, vc[j]);
+    }
+    unsigned long long tot_c, tot_w, tot_s;
+    unsigned long long ex_c = block_excl_scan(sc, sm.sh, &tot_c);
+    unsigned long long ex_w = block_excl_scan(sw, sm.sh, &tot_w);
+    unsigned long long ex_s = block_excl_scan(ss_, sm.sh, &tot_s);
+    const unsigned int mx_all = static_cast<unsigned int>(block_reduce_bits(mx, MaxOp(), sm.sh));
+    if (threadIdx.x == 0) sm.bc[1] = mx_all;
+    __syncthreads();
+    const unsigned long long need = static_cast<unsigned long long>(a.needed);
+    const bool ok = tot_w >= need && sm.bc[1] <= static_cast<unsigned int>(kBucketCap);
+    if (!ok) {
+        if (threadIdx.x == 0) {
+            a.ss->small_ok = 2;
+            a.ss->path = tot_w >= need ? 4 : 3;  // bucket too large / bound too low
+            a.ss->dbg[5] = tot_w;
+            a.ss->dbg[6] = sm.bc[1];
+        }
+        return;
+    }
+    // the buckets ranked by tiles: > 32 heads and not wholly after the cut;
+    // their positions and first tasks by block scans (no atomics)
+    unsigned long long nbig = 0, ntask = 0;
+    unsigned int isbig[kPer];
+    {
+        unsigned long long wb = ex_w;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            isbig[j] = (vc[j] > 32u && wb < need) ? 1u : 0u;
+            nbig += isbig[j];
+            ntask += isbig[j] ? (vc[j] + kChunkS - 1) / kChunkS : 0u;
+            wb += vw[j];
+        }
+    }
+    unsigned long long tot_big, tot_task;
+    unsigned long long ex_big = block_excl_scan(nbig, sm.sh, &tot_big);
+    unsigned long long ex_task = block_excl_scan(ntask, sm.sh, &tot_task);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int d = threadIdx.x * kPer + j;
+        a.sm_off[d] = static_cast<unsigned int>(ex_c);
+        a.sm_wpre[d] = ex_w;
+        a.sm_cpre[d] = ex_s;
+        if (isbig[j]) {
+            const unsigned long long q = ex_big++;
+            a.sm_big[3 * q] = static_cast<unsigned int>(d);
+            a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
+            a.sm_big[3 * q + 2] = vc[j];
+            a.sm_task[q] = static_cast<unsigned int>(ex_task);
+            ex_task += (vc[j] + kChunkS - 1) / kChunkS;
+        }
+        ex_c += vc[j];
+        ex_w += vw[j];
+        ex_s += vs[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.ss->n_big = static_cast<unsigned int>(tot_big);
+        a.ss->n_task = static_cast<unsigned int>(tot_task);
+        a.ss->small_ok = 1;
+        a.ss->path = 1;
+    }
 }
 
 // a ranked low head: a selected one scatters its chain at its victim offset;
@@ -1320,62 +1408,12 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
     small_hist(a, n_low, lo, v0, v1, v2, sm);
     grid.sync();
     stamp(ss, nts);
-    // S2: bucket offsets; the check that the cut lies among the low heads
+    // S2: the layout the last S1 CTA wrote; the check that the cut lies among
+    // the low heads (uniform: every CTA reads the same flag)
     const unsigned long long s2t0 = gtimer();
-    constexpr int kPer = kBins / kPThreads;
-    unsigned int vc[kPer], sc = 0, mx = 0;
-    unsigned long long vw[kPer], vs[kPer], sw = 0, scs = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int d = threadIdx.x * kPer + j;
-        vc[j] = __ldcg(&a.sm_c[d]);
-        vw[j] = __ldcg(&a.sm_w[d]);
-        vs[j] = __ldcg(&a.sm_cs[d]);
-        sc += vc[j];
-        sw += vw[j];
-        scs += vs[j];
-        mx = max(mx, vc[j]);
-    }
-    unsigned long long tot_c, tot_w, tot_s;
-    unsigned long long ex_c = block_excl_scan(sc, sm.sh, &tot_c);
-    unsigned long long ex_w = block_excl_scan(sw, sm.sh, &tot_w);
-    unsigned long long ex_s = block_excl_scan(scs, sm.sh, &tot_s);
-    const unsigned int mx_all = static_cast<unsigned int>(block_reduce_bits(mx, MaxOp(), sm.sh));
-    if (threadIdx.x == 0) sm.bc[0] = mx_all;
+    if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->small_ok);
     __syncthreads();
-    const bool ok = tot_w >= static_cast<unsigned long long>(a.needed) && sm.bc[0] <= static_cast<unsigned int>(kBucketCap);
-    if (!ok) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            ss->path = tot_w >= static_cast<unsigned long long>(a.needed) ? 4 : 3;  // bucket too large / bound too low
-            ss->dbg[5] = tot_w;
-            ss->dbg[6] = sm.bc[0];
-        }
-        return false;
-    }
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int d = threadIdx.x * kPer + j;
-        sm.off[d] = static_cast<unsigned int>(ex_c);
-        if (blockIdx.x == 0) {
-            a.sm_off[d] = static_cast<unsigned int>(ex_c);
-            a.sm_wpre[d] = ex_w;
-            a.sm_cpre[d] = ex_s;
-            if (vc[j] > 32u) {
-                const unsigned int q = atomicAdd(&ss->n_big, 1u);
-                a.sm_big[3 * q] = static_cast<unsigned int>(d);
-                a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
-                a.sm_big[3 * q + 2] = vc[j];
-            }
-        }
-        ex_c += vc[j];
-        ex_w += vw[j];
-        ex_s += vs[j];
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ss->path = 1;
-        ss->dbg[3] = gtimer() - s2t0;  // S2 offsets (CTA 0)
-    }
-    __syncthreads();
+    if (sm.bc[0] != 1) return false;
     {
         const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
         for (unsigned long long base = blockIdx.x * static_cast<unsigned long long>(blockDim.x); base < n_low;
@@ -1395,7 +1433,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
                 unsigned int b = 0;
                 if (lane == leader) b = atomicAdd(&a.sm_cur[d], static_cast<unsigned int>(__popc(peers)));
                 b = __shfl_sync(peers, b, leader);
-                const unsigned int pos = sm.off[d] + b + __popc(peers & ((1u << lane) - 1u));
+                const unsigned int pos = __ldcg(&a.sm_off[d]) + b + __popc(peers & ((1u << lane) - 1u));
                 a.listS[pos] = x;
                 a.listSK[pos] = make_ulonglong2(pk, cw);
             }
@@ -1435,30 +1473,19 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
             if (in) small_place_head(a, x, kc.y, wpre + wb, __ldcg(&a.sm_cpre[d]) + cb);
         }
         // larger buckets: rank counting from a shared-memory tile, 8 threads per
-        // element; tasks (bucket, 64-element chunk) over every CTA
-        if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->n_big);
+        // element; tasks (bucket, 64-element chunk) over every CTA, the first
+        // task of every bucket precomputed by the last S1 CTA
+        if (threadIdx.x == 0) {
+            sm.bc[0] = __ldcg(&ss->n_big);
+            sm.bc[1] = __ldcg(&ss->n_task);
+        }
         __syncthreads();
         const unsigned int n_big = static_cast<unsigned int>(sm.bc[0]);
+        const unsigned long long ttot = sm.bc[1];
+        for (unsigned int q = threadIdx.x; q < n_big; q += blockDim.x) sm.off[q] = __ldcg(&a.sm_task[q]);
         __syncthreads();
         if (n_big > 0) {
             constexpr int kChunkS = kPThreads / 8;
-            unsigned int tv[kPer], ts = 0;
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                const unsigned int b = threadIdx.x * kPer + j;
-                tv[j] = b < n_big && __ldcg(&a.sm_wpre[__ldcg(&a.sm_big[3 * b])]) < static_cast<unsigned long long>(a.needed)
-                            ? (__ldcg(&a.sm_big[3 * b + 2]) + kChunkS - 1) / kChunkS
-                            : 0u;
-                ts += tv[j];
-            }
-            unsigned long long ttot;
-            unsigned long long tex = block_excl_scan(ts, sm.sh, &ttot);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                sm.off[threadIdx.x * kPer + j] = static_cast<unsigned int>(tex);
-                tex += tv[j];
-            }
-            __syncthreads();
             unsigned int held = ~0u;
             for (unsigned int t = blockIdx.x; t < static_cast<unsigned int>(ttot); t += gridDim.x) {
                 unsigned int blo = 0, bhi = n_big - 1;  // last bucket whose first task is <= t
@@ -2017,7 +2044,7 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.samp_mask = R - 1;
         c.samp.reserve(kSamp * sizeof(SampRec));
         c.low.reserve(static_cast<std::size_t>(c.n) + 1);
-        c.small_u32.reserve(6 * kBins);
+        c.small_u32.reserve(7 * kBins);
         c.small_u64.reserve(4 * kBins);
         a.samp = reinterpret_cast<SampRec*>(c.samp.p);
         a.low = c.low.p;
@@ -2025,6 +2052,7 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.sm_cur = c.small_u32.p + kBins;
         a.sm_off = c.small_u32.p + 2 * kBins;
         a.sm_big = c.small_u32.p + 3 * kBins;
+        a.sm_task = c.small_u32.p + 6 * kBins;
         a.sm_w = c.small_u64.p;
         a.sm_cs = c.small_u64.p + kBins;
         a.sm_wpre = c.small_u64.p + 2 * kBins;
