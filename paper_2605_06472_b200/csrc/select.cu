@@ -444,10 +444,37 @@ struct LowSink {
 };
 constexpr int kLowSh = 8192;
 
-__device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, std::int64_t nthr) {
-    // kWalk walkers per thread advance in lockstep, so each round issues the
-    // loads of all of them together: the walk is a chain of dependent L2
-    // round trips (eff[p] -> key[cur] -> CAS -> parent), not bandwidth
+// One hop of a walker: n's key km is carried to ancestor p when it beats
+// eff[p]'s key (plain read first, CAS only when it would win; a lost race
+// re-reads next time).  Returns false when the walk is over.
+__device__ __forceinline__ bool eff_hop(const SelArgs& a, int n, int& p, const Key2& km, int cur, const Key2& kc) {
+    if (!key_less(kc, cur, km, n)) return false;  // a larger key holds p: its holder carries it
+    if (atomicCAS(&a.eff[p], cur, n) == cur) {
+        p = a.parent[p];
+        return p > 0 && !(a.flags[p] & kFlagOutOfOrder);
+    }
+    return true;
+}
+
+// Per-CTA walk queue of the eff phase (shared memory, the sort union)
+struct WalkQueue {
+    int* n;
+    int* p;
+    unsigned long long* k0;
+    unsigned long long* k1;
+    unsigned int* count;  // pushed
+    unsigned int* head;   // popped
+    int cap;
+};
+
+__device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, std::int64_t nthr, const WalkQueue& q) {
+    // (1) every device node whose key beats its parent's own key starts a walk
+    // (eff[p] >= key(p): below that it cannot change anything -- the common
+    // case, HE keys grow toward the root).  kWalk nodes per thread have their
+    // fields in flight together.  The walkers go to the CTA's queue.
+    // (2) the CTA's threads drain the queue, kSlot walkers each, refilling a
+    // slot as soon as its walk ends: the phase lasts about the longest walk
+    // instead of the longest walk of every warp's lockstep group.
     constexpr int kWalk = 4;
     for (std::int64_t base = tid; base < a.n_nodes; base += kWalk * nthr) {
         int n[kWalk], p[kWalk];
@@ -466,51 +493,75 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
         for (int j = 0; j < kWalk; ++j) {
             const std::int64_t i = base + j * nthr;
             act[j] = i < a.n_nodes && n[j] != 0 && (fn[j] & kFlagTierMask) == PBKV_TIER_DEVICE;
-
             // (out-of-order parents -- deferred heavy / spine -- are reduced
             // over their children lists instead: thousands of walkers CAS-ing
             // one hot word serialised in its L2 slice)
             act[j] = act[j] && p[j] > 0;
         }
-        // the parent's flag and key in one round trip.  eff[p] >= key(p): a
-        // walker below its parent's own key stops without touching eff[p]
-        // (the common case -- HE keys grow toward the root)
         std::uint8_t fp[kWalk];
         Key2 kp[kWalk];
 #pragma unroll
-        for (int j = 0; j < kWalk; ++j) {
+        for (int j = 0; j < kWalk; ++j) {  // the parent's flag and key in one round trip
             fp[j] = act[j] ? a.flags[p[j]] : std::uint8_t(0);
             kp[j] = act[j] ? load_key(a.keys, p[j]) : Key2{0, 0};
         }
 #pragma unroll
-        for (int j = 0; j < kWalk; ++j)
-            act[j] = act[j] && !(fp[j] & kFlagOutOfOrder) && key_less(kp[j], p[j], km[j], n[j]);
-        for (;;) {
-            bool any = false;
-            int cur[kWalk];
-#pragma unroll
-            for (int j = 0; j < kWalk; ++j) {
-                // plain (L2) read first; CAS only when we would win
-                cur[j] = act[j] ? __ldcg(&a.eff[p[j]]) : 0;
-                any = any || act[j];
-            }
-            if (!any) break;
-            Key2 kc[kWalk];
-#pragma unroll
-            for (int j = 0; j < kWalk; ++j) kc[j] = act[j] ? load_key(a.keys, cur[j]) : Key2{0, 0};
-#pragma unroll
-            for (int j = 0; j < kWalk; ++j) {
-                if (!act[j]) continue;
-                if (!key_less(kc[j], cur[j], km[j], n[j])) {  // a larger key holds p: its holder carries it
-                    act[j] = false;
-                    continue;
+        for (int j = 0; j < kWalk; ++j) {
+            if (!(act[j] && !(fp[j] & kFlagOutOfOrder) && key_less(kp[j], p[j], km[j], n[j]))) continue;
+            const unsigned int at = atomicAdd(q.count, 1u);
+            if (at < static_cast<unsigned int>(q.cap)) {
+                q.n[at] = n[j];
+                q.p[at] = p[j];
+                q.k0[at] = km[j].w0;
+                q.k1[at] = km[j].w1;
+            } else {  // queue full (rare): walk here
+                int pp = p[j];
+                for (;;) {
+                    const int cur = __ldcg(&a.eff[pp]);
+                    if (!eff_hop(a, n[j], pp, km[j], cur, load_key(a.keys, cur))) break;
                 }
-                if (atomicCAS(&a.eff[p[j]], cur[j], n[j]) == cur[j]) {
-                    p[j] = a.parent[p[j]];
-                    act[j] = p[j] > 0 && !(a.flags[p[j]] & kFlagOutOfOrder);
-                }  // else: lost a race, re-read eff[p] next round
             }
         }
+    }
+    __syncthreads();
+    const unsigned int total = min(*q.count, static_cast<unsigned int>(q.cap));
+    constexpr int kSlot = 4;
+    int sn[kSlot], sp[kSlot];
+    Key2 sk[kSlot];
+    bool sa[kSlot];
+#pragma unroll
+    for (int j = 0; j < kSlot; ++j) sa[j] = false;
+    bool more = true;  // the queue may still hold walkers
+    for (;;) {
+        if (more) {
+#pragma unroll
+            for (int j = 0; j < kSlot; ++j) {
+                if (sa[j]) continue;
+                const unsigned int at = atomicAdd(q.head, 1u);
+                if (at >= total) {
+                    more = false;
+                    break;
+                }
+                sn[j] = q.n[at];
+                sp[j] = q.p[at];
+                sk[j] = Key2{q.k0[at], q.k1[at]};
+                sa[j] = true;
+            }
+        }
+        bool any = false;
+        int cur[kSlot];
+#pragma unroll
+        for (int j = 0; j < kSlot; ++j) {
+            cur[j] = sa[j] ? __ldcg(&a.eff[sp[j]]) : 0;
+            any = any || sa[j];
+        }
+        if (!any) break;
+        Key2 kc[kSlot];
+#pragma unroll
+        for (int j = 0; j < kSlot; ++j) kc[j] = sa[j] ? load_key(a.keys, cur[j]) : Key2{0, 0};
+#pragma unroll
+        for (int j = 0; j < kSlot; ++j)
+            if (sa[j]) sa[j] = eff_hop(a, sn[j], sp[j], sk[j], cur[j], kc[j]);
     }
 }
 
@@ -997,6 +1048,7 @@ struct PersistSmem {
     unsigned int off[kBins];
     unsigned long long sh[32];
     unsigned long long bc[4];  // broadcast of shared scalars
+    unsigned int qctl[2];      // eff walk queue: pushed, popped
     PickOut pick;
 };
 
@@ -1566,11 +1618,11 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     }
 
     stamp(ss, nts);
-    phase_lock(a, tid, nthr);
-    grid.sync();
-    stamp(ss, nts);
-    // CTA 0 reads the node sample and sets the small-cut bound while the
-    // other CTAs walk eff
+    // One phase: CTA 0 reads the node sample and sets the small-cut bound
+    // while the other CTAs mark the locks and walk eff (independent: eff is
+    // the subtree maximum of every device node, eligibility comes in the
+    // chains phase).  Only CTA 0 touches the selection state before the
+    // barrier (it initialised it above).
     if (blockIdx.x == 0) {
         const SmallBound b = small_bound(a, sm);
         if (threadIdx.x == 0) {
@@ -1579,7 +1631,16 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             ss->bound_id = b.ok ? b.id : -1;
         }
     } else {
-        phase_eff(a, tid - kPThreads, nthr - kPThreads);
+        if (threadIdx.x == 0) {
+            sm.qctl[0] = 0u;
+            sm.qctl[1] = 0u;
+        }
+        __syncthreads();
+        constexpr int kQ = kBucketCap / 2;  // walkers queued per CTA (~400 at C3; overflow walks inline)
+        const WalkQueue q{sm.u.sort.val, sm.u.sort.val + kQ, sm.u.sort.k0, sm.u.sort.k1, &sm.qctl[0], &sm.qctl[1],
+                          kQ};
+        phase_lock(a, tid - kPThreads, nthr - kPThreads);
+        phase_eff(a, tid - kPThreads, nthr - kPThreads, q);
     }
     grid.sync();
     stamp(ss, nts);
