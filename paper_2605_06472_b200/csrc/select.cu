@@ -51,7 +51,11 @@ constexpr int kBins = 1 << kDigitBits;
 constexpr int kMaxPasses = 16;
 constexpr int kBucketCap = 4096;  // bucket sorted by one CTA in shared memory
 constexpr int kScanIPT = 8;       // chain-start scan: items per thread per chunk
-// small-cut path: a node sample bounds the cut from above
+// small-cut path: a node sample bounds the cut from above;
+// the low heads are bucketed by a 9-bit digit (one bin per thread of the
+// layout scan)
+constexpr int kSBits = 9;
+constexpr int kSBins = 1 << kSBits;
 constexpr int kSamp = 2048;            // sample records (the eff phase appends ~1024)
 constexpr unsigned int kSampTarget = 1024;
 constexpr long long kSmallMax = 1 << 18;  // estimated heads below the bound for the small path
@@ -306,6 +310,7 @@ struct SelArgs {
     SampRec* samp;          // [kSamp]
     unsigned int samp_mask; // node n is sampled when hash(n) & mask == 0
     int* low;               // heads at or below the bound
+    unsigned long long* gbar;  // grid barrier arrival counter (GridBar)
     unsigned int* sm_c;     // [kBins] counts, cursors, bucket offsets, big list [2*kBins]
     unsigned int* sm_cur;
     unsigned int* sm_off;
@@ -1030,6 +1035,33 @@ __device__ __forceinline__ void do_cut(const SelArgs& a) {
     }
 }
 
+// ---- grid barrier ------------------------------------------------------------------------
+// Arrival counter shared by every launch of the persistent kernel (64-bit,
+// never reset): a CTA's arrival returns the running count, whose quotient by
+// the grid size names the barrier.  The waiting CTAs back off with
+// __nanosleep, so the tail of a phase -- often one CTA's serial work -- does
+// not compete with 295 spinning loads for the memory system.
+struct GridBar {
+    unsigned long long* count;
+    __device__ __forceinline__ void sync() const {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned long long old = atomicAdd(count, 1ull);
+            const unsigned long long target = (old / gridDim.x + 1ull) * gridDim.x;
+            unsigned int ns = 32;
+            for (;;) {
+                unsigned long long v;
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+                if (v >= target) break;
+                __nanosleep(ns);
+                ns = ns < 256 ? ns * 2 : 256;
+            }
+        }
+        __syncthreads();
+    }
+};
+
 // ---- the persistent kernel --------------------------------------------------------------
 struct PersistSmem {
     union {
@@ -1276,7 +1308,7 @@ __device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
 // S1: histogram of the low heads (count, chain weight, chain size per 11-bit digit)
 __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long n_low, int lo, unsigned long long v0,
                                            unsigned long long v1, unsigned long long v2, PersistSmem& sm) {
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+    for (int b = threadIdx.x; b < kSBins; b += blockDim.x) {
         sm.u.hist.w[b] = 0;
         sm.u.hist.c[b] = 0;
         sm.u.hist.cs[b] = 0;
@@ -1287,13 +1319,13 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
          i += stride) {
         const int x = __ldcg(&a.low[i]);
         const unsigned long long pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
-        const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kBins - 1);
+        const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kSBins - 1);
         smem_add_u64(&sm.u.hist.w[d], __ldcg(&a.W[x]));
         atomicAdd(&sm.u.hist.c[d], 1u);
         smem_add_u64(&sm.u.hist.cs[d], static_cast<unsigned long long>(__ldcg(&a.C[x])));
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+    for (int b = threadIdx.x; b < kSBins; b += blockDim.x) {
         const unsigned int c = sm.u.hist.c[b];
         if (c) {
             atomicAdd(&a.sm_c[b], c);
@@ -1310,7 +1342,8 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     __syncthreads();
     if (sm.bc[0] != gridDim.x - 1) return;
     __threadfence();
-    constexpr int kPer = kBins / kPThreads;
+    const unsigned long long tl0 = gtimer();
+    constexpr int kPer = kSBins / kPThreads;
     constexpr int kChunkS = kPThreads / 8;
     unsigned int vc[kPer], mx = 0;
     unsigned long long vw[kPer], vs[kPer], sc = 0, sw = 0, ss_ = 0;
@@ -1384,6 +1417,8 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         a.ss->n_task = static_cast<unsigned int>(tot_task);
         a.ss->small_ok = 1;
         a.ss->path = 1;
+        a.ss->dbg[5] = tl0 - a.ss->ts[a.ss->n_ts - 1];  // S1 start -> the last CTA's layout
+        a.ss->dbg[6] = gtimer() - tl0;                 // the layout itself
     }
 }
 
@@ -1433,7 +1468,7 @@ __device__ __forceinline__ void small_place_head(const SelArgs& a, int x, unsign
 
 // S1..S3.  Returns false (uniformly) when the low list cannot hold the cut or
 // does not fit the small path's limits; nothing has been written then.
-__device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& grid, int& nts,
+__device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& grid, int& nts,
                            unsigned long long total_tok) {
     SelState* ss = a.ss;
     if (threadIdx.x == 0) {
@@ -1456,7 +1491,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
         }
         return false;
     }
-    const int lo = nbits > kDigitBits ? nbits - kDigitBits : 0;
+    const int lo = nbits > kSBits ? nbits - kSBits : 0;
     small_hist(a, n_low, lo, v0, v1, v2, sm);
     grid.sync();
     stamp(ss, nts);
@@ -1476,7 +1511,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
             if (i < n_low) {
                 x = __ldcg(&a.low[i]);
                 pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
-                d = static_cast<int>((pk >> lo) & (kBins - 1));
+                d = static_cast<int>((pk >> lo) & (kSBins - 1));
                 cw = (__ldcg(&a.W[x]) << 24) | static_cast<unsigned long long>(__ldcg(&a.C[x]));
             }
             const unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -1500,7 +1535,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
         const int lane = threadIdx.x & 31;
         const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
         const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(blockDim.x)) >> 5);
-        for (int d = gwarp; d < kBins; d += nwarps) {
+        for (int d = gwarp; d < kSBins; d += nwarps) {
             const unsigned int cnt = __ldcg(&a.sm_c[d]);
             if (cnt == 0u || cnt > 32u) continue;
             const unsigned long long wpre = __ldcg(&a.sm_wpre[d]);
@@ -1595,7 +1630,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, cg::grid_group& gr
 __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PersistSmem& sm = *reinterpret_cast<PersistSmem*>(smem_raw);
-    cg::grid_group grid = cg::this_grid();
+    const GridBar grid{a.gbar};
     SelState* ss = a.ss;
     const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
@@ -2108,6 +2143,11 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         c.small_u32.reserve(7 * kBins);
         c.small_u64.reserve(4 * kBins);
         a.samp = reinterpret_cast<SampRec*>(c.samp.p);
+        if (!c.gbar.p) {  // zeroed once; every launch keeps it consistent
+            c.gbar.reserve(1);
+            PBKV_CUDA(cudaMemsetAsync(c.gbar.p, 0, sizeof(unsigned long long), c.stream));
+        }
+        a.gbar = c.gbar.p;
         a.low = c.low.p;
         a.sm_c = c.small_u32.p;
         a.sm_cur = c.small_u32.p + kBins;
