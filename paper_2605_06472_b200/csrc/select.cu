@@ -461,12 +461,10 @@ __device__ __forceinline__ bool eff_hop(const SelArgs& a, int n, int& p, const K
     return true;
 }
 
-// Per-CTA walk queue of the eff phase (shared memory, the sort union)
+// Per-CTA walk queue of the eff phase (shared memory, the sort union): the
+// walker ids; parent and key are reloaded when a slot takes one (L2 hits)
 struct WalkQueue {
     int* n;
-    int* p;
-    unsigned long long* k0;
-    unsigned long long* k1;
     unsigned int* count;  // pushed
     unsigned int* head;   // popped
     int cap;
@@ -516,9 +514,6 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
             const unsigned int at = atomicAdd(q.count, 1u);
             if (at < static_cast<unsigned int>(q.cap)) {
                 q.n[at] = n[j];
-                q.p[at] = p[j];
-                q.k0[at] = km[j].w0;
-                q.k1[at] = km[j].w1;
             } else {  // queue full (rare): walk here
                 int pp = p[j];
                 for (;;) {
@@ -548,10 +543,15 @@ __device__ __forceinline__ void phase_eff(const SelArgs& a, std::int64_t tid, st
                     break;
                 }
                 sn[j] = q.n[at];
-                sp[j] = q.p[at];
-                sk[j] = Key2{q.k0[at], q.k1[at]};
                 sa[j] = true;
+                sp[j] = -1;  // parent and key loaded below, together
             }
+#pragma unroll
+            for (int j = 0; j < kSlot; ++j)
+                if (sa[j] && sp[j] < 0) {
+                    sp[j] = a.parent[sn[j]];
+                    sk[j] = load_key(a.keys, sn[j]);
+                }
         }
         bool any = false;
         int cur[kSlot];
@@ -1322,15 +1322,18 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kSBins - 1);
         smem_add_u64(&sm.u.hist.w[d], __ldcg(&a.W[x]));
         atomicAdd(&sm.u.hist.c[d], 1u);
-        smem_add_u64(&sm.u.hist.cs[d], static_cast<unsigned long long>(__ldcg(&a.C[x])));
+        atomicAdd(reinterpret_cast<unsigned int*>(sm.u.hist.cs) + d, __ldcg(&a.C[x]));  // < 2^24 (nodes)
     }
     __syncthreads();
+    // two global atomics per non-empty bin: the token weight, and the head
+    // count with the chain-size sum packed in one word (both < 2^32: they
+    // count nodes)
+    const unsigned int* csum = reinterpret_cast<const unsigned int*>(sm.u.hist.cs);
     for (int b = threadIdx.x; b < kSBins; b += blockDim.x) {
         const unsigned int c = sm.u.hist.c[b];
         if (c) {
-            atomicAdd(&a.sm_c[b], c);
             atomicAdd(&a.sm_w[b], sm.u.hist.w[b]);
-            atomicAdd(&a.sm_cs[b], sm.u.hist.cs[b]);
+            atomicAdd(&a.sm_cs[b], (static_cast<unsigned long long>(c) << 32) | csum[b]);
         }
     }
     // the last CTA to finish turns the histogram into the bucket layout once:
@@ -1341,84 +1344,108 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     if (threadIdx.x == 0) sm.bc[0] = atomicAdd(&a.ss->small_done, 1u);
     __syncthreads();
     if (sm.bc[0] != gridDim.x - 1) return;
+    // one bin per thread (kSBins == kPThreads): warp scans, the warps' totals
+    // through shared memory -- two block barriers per scan stage, coalesced
+    // loads and stores, a handful of registers
+    static_assert(kSBins == kPThreads, "the layout maps one bin to one thread");
     __threadfence();
-    const unsigned long long tl0 = gtimer();
-    constexpr int kPer = kSBins / kPThreads;
+    const int d = threadIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kChunkS = kPThreads / 8;
-    unsigned int vc[kPer], mx = 0;
-    unsigned long long vw[kPer], vs[kPer], sc = 0, sw = 0, ss_ = 0;
+    constexpr int kW = kPThreads / 32;
+    unsigned long long* wt = sm.u.hist.w;  // [kW][4] warp totals (the histogram is no longer needed)
+    const unsigned long long packed = __ldcg(&a.sm_cs[d]);
+    const unsigned long long vw = __ldcg(&a.sm_w[d]);
+    const unsigned int vc = static_cast<unsigned int>(packed >> 32);
+    const unsigned long long vs = packed & 0xffffffffull;
+    // stage 1: counts, tokens, chain sizes (exclusive prefixes), max count
+    unsigned long long xc = vc, xw = vw, xs = vs;
+    unsigned int mx = vc;
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int d = threadIdx.x * kPer + j;
-        vc[j] = __ldcg(&a.sm_c[d]);
-        vw[j] = __ldcg(&a.sm_w[d]);
-        vs[j] = __ldcg(&a.sm_cs[d]);
-        sc += vc[j];
-        sw += vw[j];
-        ss_ += vs[j];
-        mx = max(mx, vc[j]);
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long yc = __shfl_up_sync(0xffffffffu, xc, o);
+        const unsigned long long yw = __shfl_up_sync(0xffffffffu, xw, o);
+        const unsigned long long ys = __shfl_up_sync(0xffffffffu, xs, o);
+        if (lane >= o) {
+            xc += yc;
+            xw += yw;
+            xs += ys;
+        }
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    unsigned long long tot_c, tot_w, tot_s;
-    unsigned long long ex_c = block_excl_scan(sc, sm.sh, &tot_c);
-    unsigned long long ex_w = block_excl_scan(sw, sm.sh, &tot_w);
-    unsigned long long ex_s = block_excl_scan(ss_, sm.sh, &tot_s);
-    const unsigned int mx_all = static_cast<unsigned int>(block_reduce_bits(mx, MaxOp(), sm.sh));
-    if (threadIdx.x == 0) sm.bc[1] = mx_all;
+    if (lane == 31) {
+        wt[warp * 4 + 0] = xc;
+        wt[warp * 4 + 1] = xw;
+        wt[warp * 4 + 2] = xs;
+        wt[warp * 4 + 3] = mx;
+    }
     __syncthreads();
+    unsigned long long pc = 0, pw = 0, ps = 0, tw = 0;
+    unsigned int mxa = 0;
+    for (int w = 0; w < kW; ++w) {
+        if (w < warp) {
+            pc += wt[w * 4 + 0];
+            pw += wt[w * 4 + 1];
+            ps += wt[w * 4 + 2];
+        }
+        tw += wt[w * 4 + 1];
+        mxa = max(mxa, static_cast<unsigned int>(wt[w * 4 + 3]));
+    }
+    const unsigned long long ex_c = pc + xc - vc, ex_w = pw + xw - vw, ex_s = ps + xs - vs;
     const unsigned long long need = static_cast<unsigned long long>(a.needed);
-    const bool ok = tot_w >= need && sm.bc[1] <= static_cast<unsigned int>(kBucketCap);
-    if (!ok) {
+    if (!(tw >= need && mxa <= static_cast<unsigned int>(kBucketCap))) {  // uniform
         if (threadIdx.x == 0) {
             a.ss->small_ok = 2;
-            a.ss->path = tot_w >= need ? 4 : 3;  // bucket too large / bound too low
-            a.ss->dbg[5] = tot_w;
-            a.ss->dbg[6] = sm.bc[1];
+            a.ss->path = tw >= need ? 4 : 3;  // bucket too large / bound too low
+            a.ss->dbg[5] = tw;
+            a.ss->dbg[6] = mxa;
         }
         return;
     }
-    // the buckets ranked by tiles: > 32 heads and not wholly after the cut;
-    // their positions and first tasks by block scans (no atomics)
-    unsigned long long nbig = 0, ntask = 0;
-    unsigned int isbig[kPer];
-    {
-        unsigned long long wb = ex_w;
+    // stage 2: the buckets ranked by tiles (> 32 heads, not wholly after the
+    // cut): their list positions and first rank tasks
+    const bool big = vc > 32u && ex_w < need;
+    const unsigned long long tk = big ? (vc + kChunkS - 1) / kChunkS : 0u;
+    unsigned long long xb = big ? 1u : 0u, xt = tk;
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            isbig[j] = (vc[j] > 32u && wb < need) ? 1u : 0u;
-            nbig += isbig[j];
-            ntask += isbig[j] ? (vc[j] + kChunkS - 1) / kChunkS : 0u;
-            wb += vw[j];
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long yb = __shfl_up_sync(0xffffffffu, xb, o);
+        const unsigned long long yt = __shfl_up_sync(0xffffffffu, xt, o);
+        if (lane >= o) {
+            xb += yb;
+            xt += yt;
         }
     }
-    unsigned long long tot_big, tot_task;
-    unsigned long long ex_big = block_excl_scan(nbig, sm.sh, &tot_big);
-    unsigned long long ex_task = block_excl_scan(ntask, sm.sh, &tot_task);
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int d = threadIdx.x * kPer + j;
-        a.sm_off[d] = static_cast<unsigned int>(ex_c);
-        a.sm_wpre[d] = ex_w;
-        a.sm_cpre[d] = ex_s;
-        if (isbig[j]) {
-            const unsigned long long q = ex_big++;
-            a.sm_big[3 * q] = static_cast<unsigned int>(d);
-            a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
-            a.sm_big[3 * q + 2] = vc[j];
-            a.sm_task[q] = static_cast<unsigned int>(ex_task);
-            ex_task += (vc[j] + kChunkS - 1) / kChunkS;
-        }
-        ex_c += vc[j];
-        ex_w += vw[j];
-        ex_s += vs[j];
+    __syncthreads();  // wt is rewritten
+    if (lane == 31) {
+        wt[warp * 4 + 0] = xb;
+        wt[warp * 4 + 1] = xt;
     }
     __syncthreads();
+    unsigned long long pb = 0, pt = 0, tb = 0, tt = 0;
+    for (int w = 0; w < kW; ++w) {
+        if (w < warp) {
+            pb += wt[w * 4 + 0];
+            pt += wt[w * 4 + 1];
+        }
+        tb += wt[w * 4 + 0];
+        tt += wt[w * 4 + 1];
+    }
+    a.sm_c[d] = vc;
+    a.sm_off[d] = static_cast<unsigned int>(ex_c);
+    a.sm_wpre[d] = ex_w;
+    a.sm_cpre[d] = ex_s;
+    if (big) {
+        const unsigned long long q = pb + xb - 1u;
+        a.sm_big[3 * q] = static_cast<unsigned int>(d);
+        a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
+        a.sm_big[3 * q + 2] = vc;
+        a.sm_task[q] = static_cast<unsigned int>(pt + xt - tk);
+    }
     if (threadIdx.x == 0) {
-        a.ss->n_big = static_cast<unsigned int>(tot_big);
-        a.ss->n_task = static_cast<unsigned int>(tot_task);
+        a.ss->n_big = static_cast<unsigned int>(tb);
+        a.ss->n_task = static_cast<unsigned int>(tt);
         a.ss->small_ok = 1;
         a.ss->path = 1;
-        a.ss->dbg[5] = tl0 - a.ss->ts[a.ss->n_ts - 1];  // S1 start -> the last CTA's layout
-        a.ss->dbg[6] = gtimer() - tl0;                 // the layout itself
     }
 }
 
@@ -1671,9 +1698,9 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             sm.qctl[1] = 0u;
         }
         __syncthreads();
-        constexpr int kQ = kBucketCap / 2;  // walkers queued per CTA (~400 at C3; overflow walks inline)
-        const WalkQueue q{sm.u.sort.val, sm.u.sort.val + kQ, sm.u.sort.k0, sm.u.sort.k1, &sm.qctl[0], &sm.qctl[1],
-                          kQ};
+        // walkers queued per CTA: ~400 at C3, ~3 K at C4 on one GPU (overflow walks inline)
+        constexpr int kQ = static_cast<int>(sizeof(sm.u.sort) / sizeof(int));
+        const WalkQueue q{reinterpret_cast<int*>(&sm.u.sort), &sm.qctl[0], &sm.qctl[1], kQ};
         phase_lock(a, tid - kPThreads, nthr - kPThreads);
         phase_eff(a, tid - kPThreads, nthr - kPThreads, q);
     }
@@ -2091,7 +2118,11 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
     long long* res = result_dev ? result_dev : c.counters.p + 8;
     c.sorti_out.reserve(static_cast<std::size_t>(c.n) + 1);
     c.cnt.reserve(static_cast<std::size_t>(c.n) + 1);
-    const int grid = persistent_grid(c);
+    int grid = persistent_grid(c);
+    {
+        static const int forced = std::getenv("PBKV_SELECT_GRID") ? std::atoi(std::getenv("PBKV_SELECT_GRID")) : 0;
+        if (forced > 0) grid = std::min(grid, forced);  // (experiments; measured: no gain at 10 K nodes)
+    }
     c.hist_w.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
     c.hist_c.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
     c.seg_off.reserve(static_cast<std::size_t>(kMaxPasses) * kBins);
@@ -2143,10 +2174,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         c.small_u32.reserve(7 * kBins);
         c.small_u64.reserve(4 * kBins);
         a.samp = reinterpret_cast<SampRec*>(c.samp.p);
-        if (!c.gbar.p) {  // zeroed once; every launch keeps it consistent
-            c.gbar.reserve(1);
-            PBKV_CUDA(cudaMemsetAsync(c.gbar.p, 0, sizeof(unsigned long long), c.stream));
-        }
+        c.gbar.reserve(1);  // the grid barrier's arrival counter, zeroed per launch (grid sizes vary)
+        PBKV_CUDA(cudaMemsetAsync(c.gbar.p, 0, sizeof(unsigned long long), c.stream));
         a.gbar = c.gbar.p;
         a.low = c.low.p;
         a.sm_c = c.small_u32.p;
