@@ -14,7 +14,7 @@
 //                  the current agent only), fp32, one CTA
 //   txt_gemm_kernel  h_txt pre-activation = x W_t^T: the one dense contraction
 //                  (M = workflows, N = d, K = H).  TMA (128B swizzle) feeds a
-//                  6-stage shared-memory ring; one elected thread issues
+//                  4-stage shared-memory ring (kStages); one elected thread issues
 //                  tcgen05.mma kind::f16 (bf16 in, fp32 accumulate in TMEM);
 //                  four epilogue warps drain TMEM with tcgen05.ld.  Split-K
 //                  over blockIdx.y so every SM streams x (the GEMM is HBM-bound
