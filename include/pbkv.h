@@ -213,6 +213,10 @@ int pbkv_mirror_node_count(pbkv_ctx* ctx, int64_t* n_nodes, int64_t* n_entries);
  * Replaces the provider's std::map entry (simulator.hpp:433). */
 int pbkv_forecast_put(pbkv_ctx* ctx, const int64_t* wf, int64_t n, int horizon, int outcomes,
                       const double* p);
+/* pbkv_forecast_put without its synchronisation: the validation status
+ * (forecast.hpp:25-34) is kept on the device and raised by the next call
+ * that reads the status word (a score, select or plan call). */
+int pbkv_forecast_put_async(pbkv_ctx* ctx, const int64_t* wf, int64_t n, int horizon, int outcomes, const double* p);
 /* Drops forecasts (simulator.hpp:617 forecasts_.erase(w)). */
 int pbkv_forecast_drop(pbkv_ctx* ctx, const int64_t* wf, int64_t n);
 int pbkv_forecast_clear(pbkv_ctx* ctx);

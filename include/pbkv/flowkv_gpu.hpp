@@ -152,8 +152,10 @@ struct ForecastBatch {
     }
     void upload(pbkv_ctx* c) const {
         for (const auto& [h, v] : by_horizon)
-            check(pbkv_forecast_put(c, v.first.data(), static_cast<std::int64_t>(v.first.size()), h, outcomes,
-                                    v.second.data()),
+            // rows of Forecast objects (validated by their constructor): no
+            // synchronisation here, the next call reads the status word
+            check(pbkv_forecast_put_async(c, v.first.data(), static_cast<std::int64_t>(v.first.size()), h, outcomes,
+                                          v.second.data()),
                   c);
     }
 };

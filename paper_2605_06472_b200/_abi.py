@@ -215,6 +215,7 @@ def lib() -> C.CDLL:
         "pbkv_mirror_set_scores": ([vp, _i32p, _f64p, C.c_int64], C.c_int),
         "pbkv_mirror_node_count": ([vp, _i64p, _i64p], C.c_int),
         "pbkv_forecast_put": ([vp, _i64p, C.c_int64, C.c_int, C.c_int, _f64p], C.c_int),
+        "pbkv_forecast_put_async": ([vp, _i64p, C.c_int64, C.c_int, C.c_int, _f64p], C.c_int),
         "pbkv_forecast_drop": ([vp, _i64p, C.c_int64], C.c_int),
         "pbkv_forecast_clear": ([vp], C.c_int),
         "pbkv_score_all": ([vp, _f64p], C.c_int),

@@ -150,6 +150,7 @@ std::string kvflow_message(Context& c, long long node) {
 
 namespace pbkv {
 void reset_status(Context& c) {
+    if (c.status_pending) return;  // an asynchronous upload's status is still to be read
     DevStatus* h = c.hstatus.p;
     *h = DevStatus{0, 0, LLONG_MAX, LLONG_MAX};
     PBKV_CUDA(cudaMemcpyAsync(c.status.p, h, sizeof(DevStatus), cudaMemcpyHostToDevice, c.stream));
@@ -158,12 +159,14 @@ void reset_status(Context& c) {
 void check_status(Context& c) {
     PBKV_CUDA(cudaMemcpyAsync(c.hstatus.p, c.status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c.stream));
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
+    c.status_pending = false;
     const DevStatus st = *c.hstatus.p;  // a copy: raising may reuse the pinned word
     raise_status(c, st);
 }
 
 // throws the API error a device status word describes (no-op when clear)
 void raise_status(Context& c, const DevStatus& s) {
+    c.status_pending = false;  // the word has been read
     if (s.code == 0) return;
     std::string msg;
     switch (s.kind) {
@@ -1356,7 +1359,8 @@ int pbkv_mirror_node_count(pbkv_ctx* c, int64_t* n_nodes, int64_t* n_entries) {
     });
 }
 
-int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, int outcomes, const double* p) {
+static int forecast_put_impl(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, int outcomes, const double* p,
+                             bool async) {
     return api(c, [&] {
         need(c && (n == 0 || (wf && p)), "null argument");
         if (horizon < 1) invalid("forecast horizon must be >= 1");
@@ -1370,7 +1374,8 @@ int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, in
         const std::size_t per = static_cast<std::size_t>(horizon) * static_cast<std::size_t>(outcomes);
         c->fstage.reserve(static_cast<std::size_t>(n) * per);
         c->fstage_slot.reserve(static_cast<std::size_t>(n));
-        reset_status(*c);
+        if (!c->status_pending) reset_status(*c);
+        if (async) c->status_pending = true;  // checked by the next call that reads the status word
         // pageable rows go through pinned staging, so the copy stays
         // asynchronous; pinned (or registered) caller memory is copied directly
         const std::size_t bytes = static_cast<std::size_t>(n) * per * sizeof(double);
@@ -1389,8 +1394,16 @@ int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, in
         PBKV_CUDA(cudaMemcpyAsync(c->fstage_slot.p, slots, static_cast<std::size_t>(n) * sizeof(long long),
                                   cudaMemcpyHostToDevice, c->stream));
         launch_forecast_prepare(*c, c->fstage.p, c->fstage_slot.p, n, horizon);
-        check_status(*c);
+        if (!async) check_status(*c);
     });
+}
+
+int pbkv_forecast_put(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, int outcomes, const double* p) {
+    return forecast_put_impl(c, wf, n, horizon, outcomes, p, false);
+}
+
+int pbkv_forecast_put_async(pbkv_ctx* c, const int64_t* wf, int64_t n, int horizon, int outcomes, const double* p) {
+    return forecast_put_impl(c, wf, n, horizon, outcomes, p, true);
 }
 
 int pbkv_forecast_drop(pbkv_ctx* c, const int64_t* wf, int64_t n) {
@@ -1447,12 +1460,19 @@ static int score_ids_impl(pbkv_ctx* c, const int32_t* ids, int64_t n, double* ou
         c->ids.reserve(static_cast<std::size_t>(n));
         c->vals.reserve(static_cast<std::size_t>(n));
         reset_status(*c);
-        PBKV_CUDA(cudaMemcpyAsync(c->ids.p, ids, n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        // ids in and values + status out through pinned staging: one synchronisation
+        c->hids.reserve(static_cast<std::size_t>(n));
+        c->hvals.reserve(static_cast<std::size_t>(n));
+        std::memcpy(c->hids.p, ids, static_cast<std::size_t>(n) * sizeof(int));
+        PBKV_CUDA(cudaMemcpyAsync(c->ids.p, c->hids.p, n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
         launch_score_ids(*c, c->ids.p, ids, n, c->score_rc.p, value_only);
-        check_status(*c);
         launch_gather_f64(*c, c->score_rc.p, c->ids.p, n, c->vals.p);
-        PBKV_CUDA(cudaMemcpyAsync(out, c->vals.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaMemcpyAsync(c->hvals.p, c->vals.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        PBKV_CUDA(cudaMemcpyAsync(c->hstatus.p, c->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        const DevStatus st = *c->hstatus.p;
+        raise_status(*c, st);
+        std::memcpy(out, c->hvals.p, static_cast<std::size_t>(n) * sizeof(double));
     });
 }
 

@@ -316,6 +316,9 @@ struct Context {
     DevBuf<int> pf_sid, pf_slen, pf_cmin;
     DevBuf<unsigned char> pf_state;
     PinBuf<unsigned char> hplan, hplan_init;
+    PinBuf<int> hids;         // id lists in (score_ids_impl)
+    PinBuf<double> hvals;     // values out (score_ids_impl)
+    bool status_pending = false;  // an asynchronous forecast upload's status is still unread
     PrefetchOut plan_out{};  // the last plan (views into hplan)
     bool plan_valid = false;
     DevBuf<unsigned char> cub_tmp;

@@ -797,6 +797,7 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
     ++c.launches;
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
     if (a.h_ctr[3]) check_status(c);  // the error path: the full status word
+    else c.status_pending = false;    // the kernel read a clear status word
     if (std::getenv("PBKV_DEBUG_PLAN")) {
         PfState h{};
         PBKV_CUDA(cudaMemcpy(&h, a.ps, sizeof h, cudaMemcpyDeviceToHost));

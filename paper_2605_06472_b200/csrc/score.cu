@@ -550,7 +550,7 @@ __global__ void set_deferred_kernel(std::uint8_t* flags, Key2* keys, const int* 
 __global__ void decision_prologue_kernel(DevStatus* st, std::uint8_t* flags, Key2* keys, const int* heavy,
                                          int n_heavy, int defer, unsigned int* hmiss, int n_hmiss, double* approx) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *st = DevStatus{0, 0, LLONG_MAX, LLONG_MAX};
+    if (i == 0 && st) *st = DevStatus{0, 0, LLONG_MAX, LLONG_MAX};  // (kept when an async upload's is unread)
     if (!defer) return;
     if (i < n_heavy) {
         const int v = heavy[i];
@@ -804,8 +804,9 @@ void launch_decision_prologue(Context& c, bool defer) {
     const int nm = defer ? static_cast<int>(c.n_heavy + c.n_medium) : 0;
     if (defer) c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy) + 2);
     const int n = std::max(1, std::max(nh, nm));
-    decision_prologue_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.status.p, c.flags.p, c.keys.p, c.heavy.p, nh,
-                                                                      defer ? 1 : 0, c.hmiss.p, nm, c.happrox.p);
+    decision_prologue_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.status_pending ? nullptr : c.status.p, c.flags.p,
+                                                                      c.keys.p, c.heavy.p, nh, defer ? 1 : 0, c.hmiss.p,
+                                                                      nm, c.happrox.p);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
 }

@@ -1106,29 +1106,6 @@ struct SmallBound {
     bool ok;
 };
 
-__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* sh,
-                                                              unsigned long long* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    unsigned long long x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    __syncthreads();
-    if (lane == 31) sh[warp] = x;
-    __syncthreads();
-    unsigned long long pre = 0, tot = 0;
-    for (int w = 0; w < nw; ++w) {
-        const unsigned long long t = sh[w];
-        if (w < warp) pre += t;
-        tot += t;
-    }
-    __syncthreads();
-    *total = tot;
-    return pre + x - v;
-}
-
 // one CTA: the bound T from the node sample (two samples per thread)
 __device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
     SmallBound r{{0, 0}, -1, false};
@@ -1685,6 +1662,8 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     // the subtree maximum of every device node, eligibility comes in the
     // chains phase).  Only CTA 0 touches the selection state before the
     // barrier (it initialised it above).
+    // (a grid of one CTA -- small trees -- does the bound, then the walks)
+    const bool solo = gridDim.x == 1;
     if (blockIdx.x == 0) {
         const SmallBound b = small_bound(a, sm);
         if (threadIdx.x == 0) {
@@ -1692,7 +1671,8 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             ss->bound_w1 = b.k.w1;
             ss->bound_id = b.ok ? b.id : -1;
         }
-    } else {
+    }
+    if (blockIdx.x != 0 || solo) {
         if (threadIdx.x == 0) {
             sm.qctl[0] = 0u;
             sm.qctl[1] = 0u;
@@ -1701,8 +1681,9 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         // walkers queued per CTA: ~400 at C3, ~3 K at C4 on one GPU (overflow walks inline)
         constexpr int kQ = static_cast<int>(sizeof(sm.u.sort) / sizeof(int));
         const WalkQueue q{reinterpret_cast<int*>(&sm.u.sort), &sm.qctl[0], &sm.qctl[1], kQ};
-        phase_lock(a, tid - kPThreads, nthr - kPThreads);
-        phase_eff(a, tid - kPThreads, nthr - kPThreads, q);
+        const std::int64_t t0 = solo ? tid : tid - kPThreads, nt = solo ? nthr : nthr - kPThreads;
+        phase_lock(a, t0, nt);
+        phase_eff(a, t0, nt, q);
     }
     grid.sync();
     stamp(ss, nts);
