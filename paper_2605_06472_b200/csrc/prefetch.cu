@@ -164,24 +164,29 @@ struct Packer {
     unsigned long long vhi;
     unsigned int vid;
     int nhi, nid, nbits;
+    int dbits;  // digit width: ~8 candidates per bucket, 4..kPBits bits
     bool packed;
-    __device__ void init(const PfState* ps) {
+    __device__ void init(const PfState* ps, unsigned long long n) {
         vhi = __ldcg(&ps->or_hi) ^ __ldcg(&ps->and_hi);
         vid = __ldcg(&ps->or_id) ^ __ldcg(&ps->and_id);
         nhi = __popcll(vhi);
         nid = __popc(vid);
         nbits = nhi + nid;
         packed = nbits <= 64;
+        dbits = 4;
+        while (dbits < kPBits && (8ull << dbits) < n) ++dbits;
+        if (!packed && dbits > nhi) dbits = nhi;
     }
+    __device__ int bins() const { return 1 << dbits; }
     __device__ unsigned long long key(unsigned long long hi, unsigned int id) const {
         if (!packed) return hi;
         const unsigned long long ph = pext_runs(hi, vhi), pi = pext_runs(id, vid);
         return (nid == 64 ? 0ull : (ph << nid)) | pi;
     }
     __device__ unsigned int digit(unsigned long long key) const {
-        if (packed) return static_cast<unsigned int>(nbits <= kPBits ? key : key >> (nbits - kPBits));
+        if (packed) return static_cast<unsigned int>(nbits <= dbits ? key : key >> (nbits - dbits));
         const unsigned long long ph = pext_runs(key, vhi);
-        return static_cast<unsigned int>(ph >> (nhi - kPBits));
+        return static_cast<unsigned int>(ph >> (nhi - dbits));
     }
 };
 
@@ -452,7 +457,7 @@ __device__ __forceinline__ void pf_sort(const PfArgs& a, const Packer& pk, PfSme
     const int lane = threadIdx.x & 31;
     const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(kPT) + threadIdx.x) >> 5);
     const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(kPT)) >> 5);
-    for (int d = gwarp; d < kPBins; d += nwarps) {
+    for (int d = gwarp; d < pk.bins(); d += nwarps) {
         const unsigned int cnt = __ldcg(&a.hist[d]);
         if (cnt == 0u || cnt > 32u) continue;
         const unsigned int off = __ldcg(&a.seg_off[d]);
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kPT, 2) prefetch_plan_kernel(PfArgs a) {
         return;
     }
     Packer pk;
-    pk.init(a.ps);
+    pk.init(a.ps, n);
     pf_hist(a, pk, n, sm);
     grid.sync();
     pf_stamp(a.ps, 2);

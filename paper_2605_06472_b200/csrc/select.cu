@@ -322,6 +322,14 @@ struct SelArgs {
     unsigned long long* sm_cpre;
 };
 
+// Chain weight / size of head h: the members' scatter-adds (phase_chains)
+// plus the head itself, which does not add to its own counters.
+__device__ __forceinline__ unsigned long long chain_w(const SelArgs& a, int h) {
+    return __ldcg(&a.W[h]) + static_cast<unsigned long long>(a.len[h]);
+}
+__device__ __forceinline__ unsigned int chain_c(const SelArgs& a, int h) { return __ldcg(&a.C[h]) + 1u; }
+
+
 // record of heavy node j: max over its in-order device children's eff (the
 // shared prefix has thousands of children), block-wide; eff / sublock read
 // through L2 (written by other CTAs of the persistent kernel)
@@ -634,8 +642,10 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             if (a.he_recompute && ms[j] && !(fl[j] & kFlagRetired))
                 set_error(a.st, PBKV_EINVAL, kErrMissingForecast, n[j]);
             const unsigned long long l = static_cast<unsigned long long>(ln[j]);
-            atomicAdd(&a.W[e[j]], l);
-            atomicAdd(&a.C[e[j]], 1u);
+            if (e[j] != n[j]) {  // a head's own length / count are implicit (chain_w / chain_c)
+                atomicAdd(&a.W[e[j]], l);
+                atomicAdd(&a.C[e[j]], 1u);
+            }
             tok += l;
             cnt += e[j] == n[j] ? 1u : 0u;
         }
@@ -709,7 +719,7 @@ __device__ __forceinline__ void phase_hist(const SelArgs& a, const int* L, unsig
         xn = i + stride < n_L ? __ldcg(&L[i + stride]) : 0;
         if (i < n_L) {
             d = key_bits(load_key(a.keys, x), x, lo, kDigitBits);
-            w = __ldcg(&a.W[x]);
+            w = chain_w(a, x);
         }
         // equal digits of a warp are summed first: skewed digit distributions
         // (e.g. every retired head in one bucket) would serialise on one bank
@@ -840,7 +850,7 @@ __device__ __forceinline__ void phase_compact(const SelArgs& a, const int* L, un
             const int lane = threadIdx.x & 31;
             const int leader = __ffs(peers) - 1;
             unsigned int basepos = 0;
-            const unsigned int cx = __ldcg(&a.C[x]);  // in flight with the cursor atomic
+            const unsigned int cx = chain_c(a, x);  // in flight with the cursor atomic
             if (lane == leader) basepos = atomicAdd(&cur[d], static_cast<unsigned int>(__popc(peers)));
             basepos = __shfl_sync(peers, basepos, leader);
             const unsigned int pos = off_sh[d] + basepos + __popc(peers & ((1u << lane) - 1u));
@@ -942,7 +952,7 @@ __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, in
                     if (packed) cz = __ldcg(&a.listSC[off + i]);
                 } else {
                     k = load_key(a.keys, x);
-                    if (packed) cz = __ldcg(&a.C[x]);
+                    if (packed) cz = chain_c(a, x);
                 }
                 if (packed) {  // k1 is free: it carries the chain sizes
                     k0[i] = pack_key(k, x, v0, v1, v2);
@@ -974,7 +984,7 @@ __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, in
                 if (in && part == 0) {
                     S2[off + r] = av;
                     a.listSC2[off + r] = packed ? static_cast<unsigned int>(k1[e])
-                                                : (has_sk ? __ldcg(&a.listSC[off + e]) : __ldcg(&a.C[av]));
+                                                : (has_sk ? __ldcg(&a.listSC[off + e]) : chain_c(a, av));
                 }
             }
             if (threadIdx.x == 0) atomicMax(&a.ss->dbg[3], gtimer() - tl1);
@@ -1010,7 +1020,7 @@ __device__ __forceinline__ void do_cut(const SelArgs& a) {
     const unsigned long long nS = __ldcg(&ss->n_S);
     const int cut = __ldcg(&ss->cut_head);
     const unsigned long long s0 = __ldcg(&a.start[nS - 1]);
-    const unsigned int c = __ldcg(&a.C[cut]);
+    const unsigned int c = chain_c(a, cut);
     if (__ldcg(&ss->take_all)) {
         ss->n_victims = s0 + c;
         ss->freed = __ldcg(&ss->total_tok);
@@ -1297,9 +1307,9 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         const int x = __ldcg(&a.low[i]);
         const unsigned long long pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
         const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kSBins - 1);
-        smem_add_u64(&sm.u.hist.w[d], __ldcg(&a.W[x]));
+        smem_add_u64(&sm.u.hist.w[d], chain_w(a, x));
         atomicAdd(&sm.u.hist.c[d], 1u);
-        atomicAdd(reinterpret_cast<unsigned int*>(sm.u.hist.cs) + d, __ldcg(&a.C[x]));  // < 2^24 (nodes)
+        atomicAdd(reinterpret_cast<unsigned int*>(sm.u.hist.cs) + d, chain_c(a, x));  // < 2^24 (nodes)
     }
     __syncthreads();
     // two global atomics per non-empty bin: the token weight, and the head
@@ -1516,7 +1526,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
                 x = __ldcg(&a.low[i]);
                 pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
                 d = static_cast<int>((pk >> lo) & (kSBins - 1));
-                cw = (__ldcg(&a.W[x]) << 24) | static_cast<unsigned long long>(__ldcg(&a.C[x]));
+                cw = (chain_w(a, x) << 24) | static_cast<unsigned long long>(chain_c(a, x));
             }
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             if (d >= 0) {
@@ -1790,7 +1800,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
             const Key2 k = load_key(a.keys, x);
             S[nS] = x;
             a.listSK[nS] = make_ulonglong2(k.w0, k.w1);
-            a.listSC[nS] = __ldcg(&a.C[x]);
+            a.listSC[nS] = chain_c(a, x);
             ss->n_S = nS + 1;
             ss->need_final = need;
             ss->n_pass = n_pass;
@@ -1979,7 +1989,7 @@ __global__ void rank_kernel(const int* sorted, const unsigned int* C, SelState* 
          i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
         const int h = sorted[i];
         rank[h] = static_cast<int>(i);
-        cnt[i] = C[h];
+        cnt[i] = C[h] + 1u;  // the head itself (see chain_c)
         if (i == n - 1 && ss->take_all) ss->cut_head = h;
     }
 }
