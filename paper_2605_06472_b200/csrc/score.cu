@@ -180,10 +180,14 @@ __global__ void __launch_bounds__(kLightThreads, PBKV_LIGHT_MINB) score_light_ke
             ka.sublock[n] = 0;
             ka.W[n] = 0;  // chain weight / size accumulators of the selection
             ka.C[n] = 0;
+            const bool dev = n != 0 && (fl & kFlagTierMask) == PBKV_TIER_DEVICE;
             if (light) {
                 ka.missing[n] = (miss || shorth) ? 1 : 0;
-                if (n != 0 && (fl & kFlagTierMask) == PBKV_TIER_DEVICE) write_key_v(ka, n, total, fl, last, ever);
+                if (dev) write_key_v(ka, n, total, fl, last, ever);
             }
+            // every other node's key is defined too (zero): the selection's
+            // batched loads read keys before they test the tier
+            if (!dev) reinterpret_cast<ulonglong2*>(ka.keys)[n] = make_ulonglong2(0ull, 0ull);
         }
     }
 }

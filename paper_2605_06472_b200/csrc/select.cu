@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kThreads) keys_cached_kernel(KeyArgs ka, std::
         ka.W[n] = 0;
         ka.C[n] = 0;
         if (n != 0 && (ka.flags[n] & kFlagTierMask) == PBKV_TIER_DEVICE) write_key(ka, n, ka.score_cached[n]);
+        else reinterpret_cast<ulonglong2*>(ka.keys)[n] = make_ulonglong2(0ull, 0ull);  // defined for batched loads
     }
 }
 
@@ -93,6 +94,7 @@ struct SelState {
     int shortfall, n_ts;
     unsigned int low_overflow;  // a CTA's low buffer overflowed: no small path
     unsigned int small_done;    // S1 CTAs finished (the last one lays out the buckets)
+    unsigned long long n_heads_seen;  // heads counted by the chains phase in small-cut mode
     unsigned int small_ok;      // 1 the small path proceeds, 2 it is abandoned
     unsigned int n_task;        // rank tasks of the small path's big buckets
     int bound_id;               // small-cut bound (key, id); -1: no small path
@@ -600,7 +602,8 @@ __device__ __forceinline__ void low_flush(const SelArgs& a, const LowSink& lk) {
 // heads (eligible n with eff(n) == n) walk their own chain -- the contiguous
 // eligible ancestors with the same eff -- for its token weight W and size C;
 // head list, eligible tokens, OR/AND of the head keys (first radix pass)
-__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh, const LowSink& lk) {
+__device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long long* sh, const LowSink& lk,
+                                             bool build_list) {
     // Every eligible node n belongs to the chain of eff(n) (the closed form
     // orders eligible nodes by (eff, d); the nodes sharing an eff form a
     // contiguous eligible ancestor path from it), so the chain weight W[h] and
@@ -608,7 +611,7 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     // Heads (eff(n) == n) are appended with one atomic per CTA and iteration.
     constexpr int kBatch = 4;
     SelState* ss = a.ss;
-    unsigned long long tok = 0;
+    unsigned long long tok = 0, n_seen = 0;
     unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
     for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes;
@@ -648,6 +651,25 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
             }
             tok += l;
             cnt += e[j] == n[j] ? 1u : 0u;
+        }
+        if (!build_list) {  // small-cut mode: heads are counted; only the low ones are listed
+            n_seen += cnt;
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (!elig[j] || e[j] != n[j]) continue;
+                const int h = n[j];
+                const Key2 k = load_key(a.keys, h);
+                if (!key_less(lk.tk, lk.tid, k, h)) {  // a low head
+                    const unsigned int q = atomicAdd(lk.cnt, 1u);
+                    if (q < static_cast<unsigned int>(kLowSh)) lk.buf[q] = h;
+                    for (int wd = 0; wd < 3; ++wd) {
+                        const unsigned long long x = key_word(k, h, wd);
+                        smem_or_u64(&lk.orand[wd], x);
+                        smem_and_u64(&lk.orand[3 + wd], x);
+                    }
+                }
+            }
+            continue;
         }
         // CTA-wide exclusive offsets of the heads, one global atomic per CTA
         unsigned int* wcount = reinterpret_cast<unsigned int*>(sh);
@@ -696,8 +718,40 @@ __device__ __forceinline__ void phase_chains(const SelArgs& a, unsigned long lon
     }
     const unsigned long long blk = block_reduce_bits(tok, SumOp(), sh);
     if (threadIdx.x == 0 && blk) atomicAdd(&ss->total_tok, blk);
-    flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
+    if (build_list) {
+        flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
+    } else {
+        const unsigned long long hs = block_reduce_bits(n_seen, SumOp(), sh);
+        if (threadIdx.x == 0 && hs) atomicAdd(&ss->n_heads_seen, hs);
+    }
     if (lk.on) low_flush(a, lk);
+}
+
+// The head list and its key OR / AND, for the full radix path when the
+// chains phase ran in small-cut mode (it only counted the heads)
+__device__ __forceinline__ void phase_heads(const SelArgs& a, unsigned long long* sh) {
+    SelState* ss = a.ss;
+    unsigned long long or3[3] = {0, 0, 0}, and3[3] = {~0ull, ~0ull, ~0ull};
+    const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t base = blockIdx.x * static_cast<std::int64_t>(blockDim.x); base < a.n_nodes; base += nthr) {
+        const std::int64_t i = base + threadIdx.x;
+        const int n = static_cast<int>(i < a.n_nodes ? i : 0);
+        const bool head = i < a.n_nodes && n != 0 &&
+                          (a.flags[n] & (kFlagTierMask | kFlagOutOfOrder)) == PBKV_TIER_DEVICE &&
+                          !__ldcg(&a.sublock[n]) && __ldcg(&a.eff[n]) == n;
+        unsigned int* wcount = reinterpret_cast<unsigned int*>(sh);
+        const long long slot = block_append(&ss->n_L[0], head, wcount, sh + 31);
+        if (head) {
+            a.heads[slot] = n;
+            const Key2 k = load_key(a.keys, n);
+            for (int wd = 0; wd < 3; ++wd) {
+                const unsigned long long x = key_word(k, n, wd);
+                or3[wd] |= x;
+                and3[wd] &= x;
+            }
+        }
+    }
+    flush_orand(or3, and3, ss->or_L[0], ss->and_L[0], sh);
 }
 
 // per-CTA weight and count histograms of the next digit over the candidates
@@ -1710,15 +1764,16 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         const LowSink lk{bid >= 0, Key2{sm.bc[0], sm.bc[1]}, bid, reinterpret_cast<int*>(sm.u.sort.k0),
                          reinterpret_cast<unsigned int*>(sm.u.sort.val), sm.u.sort.k1};
         __syncthreads();
-        phase_chains(a, sm.sh, lk);
+        phase_chains(a, sm.sh, lk, !lk.on);
     }
     grid.sync();
     stamp(ss, nts);
+    const bool listed = __ldcg(&ss->bound_id) < 0;  // the chains phase built the head list
 
     // shared scalars are read once per CTA and broadcast through shared memory
     // (thousands of threads reading one L2 line serialise on its slice)
     if (threadIdx.x == 0) {
-        sm.bc[0] = __ldcg(&ss->n_L[0]);
+        sm.bc[0] = listed ? __ldcg(&ss->n_L[0]) : __ldcg(&ss->n_heads_seen);
         sm.bc[1] = __ldcg(&ss->total_tok);
     }
     __syncthreads();
@@ -1737,7 +1792,12 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         return;
     }
     const bool take_all = total_tok < static_cast<unsigned long long>(a.needed);
-    if (!take_all && __ldcg(&ss->bound_id) >= 0 && small_path(a, sm, grid, nts, total_tok)) return;
+    if (!take_all && !listed && small_path(a, sm, grid, nts, total_tok)) return;
+    if (!listed) {  // the small-cut path did not apply: the head list for the paths below
+        phase_heads(a, sm.sh);
+        grid.sync();
+        stamp(ss, nts);
+    }
     int* S = a.listS;
     unsigned long long nS = 0;
     unsigned int max_bucket = 0;
