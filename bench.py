@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-pipeline", action="store_true", help="skip the config-2 predictor pipeline line")
     ap.add_argument("--no-sweep", action="store_true", help="skip the need sweep (0.1/1/10/50%%) and --no-defer line")
     ap.add_argument("--no-prefetch", action="store_true", help="skip the stage-4 prefetch plan object")
+    ap.add_argument("--sharded", action="store_true",
+                    help="the sharded config-4 path even with one rank (measures its exchange overhead)")
     return ap.parse_args()
 
 
@@ -399,6 +401,8 @@ def run_sharded(args, rank, world, local, dist, torch):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if os.environ.get("PBKV_PROFILE_SHARD"):
+        SH.PROFILE = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     k0, _ = sp.pol.launches()
     times = []
@@ -417,6 +421,8 @@ def run_sharded(args, rank, world, local, dist, torch):
             times.append(e0.elapsed_time(e1))
     dist.barrier()
     k1, _ = sp.pol.launches()
+    stage_ms = {k: statistics.mean(v) for k, v in SH.PROFILE.items()} if SH.PROFILE else None
+    SH.PROFILE = None
     # e2e: forecasts from (pageable) host memory + the decision, host wall
     e2e = []
     for _ in range(max(3, min(10, args.steps))):
@@ -458,6 +464,7 @@ def run_sharded(args, rank, world, local, dist, torch):
                     "what": "per rank: forecasts from host memory + the sharded decision (victims to the host); "
                             "max over ranks of the host wall"},
             "tree_build_s": build_s,
+            "stage_host_ms": stage_ms,
         }
         print(json.dumps(line))
     dist.barrier()
@@ -479,16 +486,18 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         backend = os.environ.get("PBKV_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (testing)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-
-    if world > 1:
         run_sharded(args, rank, world, local, dist, torch)
         return
 

@@ -279,6 +279,11 @@ def allgather_var(dist, t, world: int):
     return out.view(world, mx), lens
 
 
+# per-step host wall of the distributed decision's stages (ms), when set to a
+# dict (bench.py --sharded / PBKV_PROFILE_SHARD)
+PROFILE = None
+
+
 # ---- per-rank driver ------------------------------------------------------------------------
 class ShardedPolicy:
     """A rank's view of a sharded tree: its pbkv context plus the collective
@@ -454,7 +459,17 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     fixed-size header [candidate count | spine reports | spine product counts
     | spine products padded to the largest rank's], (2) one all-gather of the
     candidate records padded to the largest count.  Everything else is local."""
+    import time
+
     import torch
+
+    prof = PROFILE is not None
+    t0 = time.perf_counter()
+    marks = []
+
+    def mark(what):
+        if prof:
+            marks.append((what, time.perf_counter()))
 
     sp = rp.shard.spine
     dev = rp.dev
@@ -462,6 +477,7 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     loc = rp.local_ids(locked_set)
     ld = torch.from_numpy(loc if loc.size else np.zeros(1, np.int32)).to(dev)
     _, rep = rp.local_select(policy, score_mode, needed, ld.data_ptr(), loc.size, want_count=False)
+    mark("local_select")
     he_rc = policy == POLICY_HE and score_mode == SCORE_RECOMPUTE and sp.n > 0
     if he_rc:
         prod, pcnt = rp.spine_products()
@@ -486,6 +502,7 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
         parts = [torch.zeros(head.numel(), dtype=torch.uint8) for _ in range(world)]
         dist.all_gather(parts, head.cpu())
         hdr.copy_(torch.cat(parts))
+    mark("spine products + header all-gather")
     hdr = hdr.view(world, head.numel())
     nrep = sp.n * SPINE_DTYPE.itemsize
     meta = hdr[:, : 8 + nrep + 8 * sp.n].cpu().numpy()  # counts + reports + product counts (small)
@@ -509,6 +526,7 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
             allc.copy_(torch.cat(parts))
     else:
         allc = torch.zeros(rec, dtype=torch.uint8, device=dev)
+    mark("header readback + records all-gather")
     starts = [r * mx for r in range(world)] + [world * mx]
     n_cand = int(counts.sum())
 
@@ -554,10 +572,18 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
         maxrec = max(tuple(last[r, int(counts[r]) - 1][f] for f in ("w0", "w1", "eff_gid", "d"))
                      for r in range(world) if counts[r] > 0)
         fast = all(tuple(int(v) for v in (q["w0"], q["w1"], q["eff_gid"], q["d"])) > maxrec for q in lo)
+    mark("spine interval check")
     if fast:
         v, freed, sf = cut_with(lo)
         if int(v.numel()) <= n_cand and not sf:
-            return v.cpu().numpy().tolist(), freed, sf
+            out = v.cpu().numpy().tolist()
+            mark("merge + cut")
+            if prof:
+                prev = t0
+                for what, t in marks:
+                    PROFILE.setdefault(what, []).append(1e3 * (t - prev))
+                    prev = t
+            return out, freed, sf
     scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))  # exact chains
     v, freed, sf = cut_with(spine_records(sp, rep_all, scores, policy, locked_set))
     return v.cpu().numpy().tolist(), freed, sf

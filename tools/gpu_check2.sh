@@ -7,3 +7,5 @@ import json
 for r in json.load(open('gpurun_out/sim_latency.json')):
     print(r['scenario'], r['cell'], r['identical'], r['wall_s'], {op: (v['gpu_dropin'] or {}).get('p50_us') for op, v in r['per_call'].items()})
 "
+timeout 1200 compute-sanitizer --tool initcheck --print-limit 2000 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/san_init.log 2>&1
+echo "initcheck rc=$? $(grep 'ERROR SUMMARY' gpurun_out/san_init.log)"; grep "Device Frame" gpurun_out/san_init.log | sort | uniq -c | sort -rn | head -8
