@@ -393,7 +393,7 @@ def run_sharded(args, rank, world, local, dist, torch):
     sp = SH.ShardedPolicy(shard, num_agents=AGENTS, k=K, gamma=GAMMA, device=local)
     sp.pol.put_forecasts(wf, P)
     needed = max(1, int(args.needed_frac * used))
-    lk = [int(x) for x in locked.tolist()]
+    lk = np.ascontiguousarray(locked, dtype=np.int64)  # the decision's locked set (global ids)
 
     def step():
         return SH.global_select(sp, POLICY_HE, SCORE_RECOMPUTE, needed, lk, dist=dist, world=world)

@@ -319,6 +319,29 @@ class ShardedPolicy:
         self.pol._c(_abi.lib().pbkv_ctx_wait_stream(self.pol.handle,
                                                       C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)))
 
+    def locked_view(self, locked_gids):
+        """(device tensor of this shard's local ids among `locked_gids`, their
+        count, the locked spine gids) -- vectorised (sorted global ids,
+        searchsorted), and cached for the same array object (a serving loop
+        passing one locked array per decision pays this once per change)."""
+        import torch
+
+        c = getattr(self, "_lk_cache", None)
+        if c is not None and c[0] is locked_gids:
+            return c[1], c[2], c[3]
+        g = np.asarray(locked_gids, dtype=np.int64).ravel()
+        gids = self.shard.gids.astype(np.int64)
+        pos = np.searchsorted(gids, g)
+        ok = pos < gids.size
+        ok[ok] = gids[pos[ok]] == g[ok]
+        loc = np.unique(pos[ok]).astype(np.int32)
+        ld = torch.from_numpy(loc if loc.size else np.zeros(1, np.int32)).to(self.dev)
+        sp_gid = self.shard.spine.gid.astype(np.int64)
+        sp_locked = set(int(x) for x in sp_gid[np.isin(sp_gid, g)]) if sp_gid.size else set()
+        if isinstance(locked_gids, np.ndarray):
+            self._lk_cache = (locked_gids, ld, int(loc.size), sp_locked)
+        return ld, int(loc.size), sp_locked
+
     def local_ids(self, gids) -> np.ndarray:
         """Local ids of the given global ids that this shard holds."""
         g = np.asarray(sorted(set(int(x) for x in gids)), dtype=np.int64)
@@ -386,7 +409,8 @@ class ShardedPolicy:
 
 def global_select(ranks: list[ShardedPolicy] | ShardedPolicy, policy: int, score_mode: int, needed: int,
                   locked_gids, dist=None, world: int = 1):
-    """One sharded eviction decision.  With dist=None, `ranks` is the list of
+    """One sharded eviction decision: (victim global ids as an int32 array in
+    eviction order, freed tokens, shortfall).  With dist=None, `ranks` is the list of
     every shard's ShardedPolicy in one process (logical shards); otherwise it
     is this rank's ShardedPolicy and the exchange goes through `dist`."""
     import torch
@@ -450,7 +474,7 @@ def global_select(ranks: list[ShardedPolicy] | ShardedPolicy, policy: int, score
                                                                                      dtype=torch.uint8,
                                                                                      device=me.dev)
     v, freed, sf = me.merge_cut(buf, [int(s) for s in starts], lens, needed)
-    return v.cpu().numpy().tolist(), freed, sf
+    return v.cpu().numpy(), freed, sf
 
 
 def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed: int, locked_gids, dist,
@@ -473,10 +497,8 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
 
     sp = rp.shard.spine
     dev = rp.dev
-    locked_set = set(int(x) for x in locked_gids)
-    loc = rp.local_ids(locked_set)
-    ld = torch.from_numpy(loc if loc.size else np.zeros(1, np.int32)).to(dev)
-    _, rep = rp.local_select(policy, score_mode, needed, ld.data_ptr(), loc.size, want_count=False)
+    ld, n_loc, locked_set = rp.locked_view(locked_gids)  # spine gids among the locked: all spine_records needs
+    _, rep = rp.local_select(policy, score_mode, needed, ld.data_ptr(), n_loc, want_count=False)
     mark("local_select")
     he_rc = policy == POLICY_HE and score_mode == SCORE_RECOMPUTE and sp.n > 0
     if he_rc:
@@ -540,7 +562,7 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
 
     if not he_rc:
         v, freed, sf = cut_with(spine_records(sp, rep_all, sp.score, policy, locked_set))
-        return v.cpu().numpy().tolist(), freed, sf
+        return v.cpu().numpy(), freed, sf
     # spine scores over every rank's products, rank (= WorkflowId) order
     prods = hdr[:, 8 + nrep + 8 * sp.n:].reshape(world, -1).view(torch.float64)
     pieces, offs = [], [0]
@@ -567,16 +589,18 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     hi = spine_records(sp, rep_all, A + B, policy, locked_set)
     fast = np.isfinite(A).all() and lo.size == hi.size and np.array_equal(lo["gid"], hi["gid"])
     if fast and n_cand and lo.size:
-        last = np.frombuffer(allc.view(world, mx * rec)[:, :].cpu().numpy().tobytes(),
-                             dtype=CAND_DTYPE).reshape(world, mx) if mx else None
-        maxrec = max(tuple(last[r, int(counts[r]) - 1][f] for f in ("w0", "w1", "eff_gid", "d"))
-                     for r in range(world) if counts[r] > 0)
+        # the last record of every rank's run (only those come to the host)
+        rr = [r for r in range(world) if counts[r] > 0]
+        idx = torch.tensor([(r * mx + int(counts[r]) - 1) * rec + b for r in rr for b in range(rec)],
+                           dtype=torch.int64, device=dev)
+        last = np.frombuffer(allc[idx].cpu().numpy().tobytes(), dtype=CAND_DTYPE)
+        maxrec = max(tuple(q[f] for f in ("w0", "w1", "eff_gid", "d")) for q in last)
         fast = all(tuple(int(v) for v in (q["w0"], q["w1"], q["eff_gid"], q["d"])) > maxrec for q in lo)
     mark("spine interval check")
     if fast:
         v, freed, sf = cut_with(lo)
         if int(v.numel()) <= n_cand and not sf:
-            out = v.cpu().numpy().tolist()
+            out = v.cpu().numpy()
             mark("merge + cut")
             if prof:
                 prev = t0
@@ -586,4 +610,4 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
             return out, freed, sf
     scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))  # exact chains
     v, freed, sf = cut_with(spine_records(sp, rep_all, scores, policy, locked_set))
-    return v.cpu().numpy().tolist(), freed, sf
+    return v.cpu().numpy(), freed, sf

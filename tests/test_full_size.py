@@ -120,7 +120,7 @@ def test_c4_sharded_8_ways_equals_single_and_oracle(gpu):
     single.mirror(t)
     single.put_forecasts(wf, P)
     want = single.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
-    assert (got[0], got[1], got[2]) == (want.victims, want.freed, want.shortfall)
+    assert (got[0].tolist(), got[1], got[2]) == (want.victims, want.freed, want.shortfall)
     s2 = soa.copy()
     s2.score[:] = Oracle.score_nodes(soa, wf, P, 8, 0.7)
     o = Oracle.select(s2, POLICY_HE, needed, locked)

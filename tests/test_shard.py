@@ -166,11 +166,11 @@ def test_sharded_equals_single(gpu, P, policy, mode):
         needed = max(1, int(frac * used))
         got = S.global_select(sps, policy, mode, needed, locked)
         want = single.select_victims(policy, needed, locked=locked, score_mode=mode)
-        assert got[0] == want.victims, f"P={P} frac={frac}: order differs"
+        assert got[0].tolist() == want.victims, f"P={P} frac={frac}: order differs"
         assert got[1] == want.freed and got[2] == want.shortfall
         if frac in (0.01, 0.5):
             o = Oracle.select(soa, policy, needed, locked)
-            assert got[0] == o.victims and got[1] == o.freed
+            assert got[0].tolist() == o.victims and got[1] == o.freed
 
 
 @pytest.mark.gpu
@@ -232,7 +232,8 @@ def _dist_gpu_worker(rank, world, port, q):
         out = []
         for frac in (0.01, 0.3, 2.0):
             needed = max(1, int(frac * used))
-            out.append(S.global_select(me, POLICY_HE, SCORE_RECOMPUTE, needed, locked, dist=dist, world=world))
+            v, fr, sf = S.global_select(me, POLICY_HE, SCORE_RECOMPUTE, needed, locked, dist=dist, world=world)
+            out.append((v.tolist(), fr, sf))
         want = None
         if rank == 0:
             single = Policy(num_agents=A, k=K, gamma=0.7)
