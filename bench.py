@@ -465,6 +465,7 @@ def run_sharded(args, rank, world, local, dist, torch):
                             "max over ranks of the host wall"},
             "tree_build_s": build_s,
             "stage_host_ms": stage_ms,
+            "defer": dict(zip(("fast", "exact"), sp.pol.defer_stats())),
         }
         print(json.dumps(line))
     dist.barrier()

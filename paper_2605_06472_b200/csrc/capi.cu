@@ -394,6 +394,9 @@ void classify_all(Context& c) {
     c.h_medium.clear();
     c.h_heavy.clear();
     for (std::int64_t i = 0; i < c.n; ++i) {
+        // a shard's spine nodes are scored from the exchanged products
+        // (shard.py), not by the local medium / heavy chains
+        if (static_cast<std::size_t>(i) < c.h_spine.size() && c.h_spine[static_cast<std::size_t>(i)]) continue;
         const NodeClass k = class_of(c, c.h_entries[static_cast<std::size_t>(i)]);
         if (k == kHeavy) c.h_heavy.push_back(static_cast<int>(i));
         else if (k == kMedium) c.h_medium.push_back(static_cast<int>(i));
@@ -847,6 +850,8 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     // class lists and heavy children, updated by the changed nodes only
     std::vector<int> newly_heavy;
     for (const ClassMove& m : cls_moves) {
+        if (static_cast<std::size_t>(m.id) < c.h_spine.size() && c.h_spine[static_cast<std::size_t>(m.id)])
+            continue;  // (classify_all)
         if (m.from == kMedium) erase_sorted(c.h_medium, m.id);
         if (m.from == kHeavy) {
             erase_sorted(c.h_heavy, m.id);
@@ -1753,6 +1758,8 @@ int pbkv_shard_set(pbkv_ctx* c, const int32_t* global_ids, const int32_t* spine,
                                   cudaMemcpyHostToDevice, c->stream));
         shard_apply_flags(*c);
         upload_children(*c, c->spine, c->sch_off, c->sch);
+        c->h_spine.assign(is_sp.begin(), is_sp.end());
+        classify_all(*c);  // the spine leaves the local medium / heavy chains
         PBKV_CUDA(cudaStreamSynchronize(c->stream));
     });
 }

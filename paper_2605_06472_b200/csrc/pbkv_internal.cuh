@@ -237,6 +237,7 @@ struct Context {
     std::int64_t n_hent = 0;
     std::vector<int> h_heavy;                 // heavy node ids, ascending (host copy)
     std::vector<int> h_medium;                // medium node ids, ascending (host copy)
+    std::vector<char> h_spine;                // sharded context: spine membership (not in the chain lists)
     // children of every heavy node, ascending ids: kept up to date by the
     // delta path (a parent change updates the two lists it touches)
     std::unordered_map<int, std::vector<int>> h_heavy_ch;

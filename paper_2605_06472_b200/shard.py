@@ -576,13 +576,14 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     # both lie within L * ulp(sum|x|) / 2 of the real sum.  If the spine
     # records are after every candidate record for both ends of the interval,
     # and the cut ends inside the candidates, the exact chains are not needed.
-    seg = torch.repeat_interleave(torch.arange(sp.n, device=dev),
-                                  torch.tensor(np.diff(offs), device=dev)) if offs[-1] else None
-    if seg is not None:
-        A = torch.zeros(sp.n, dtype=torch.float64, device=dev).index_add_(0, seg, x[: offs[-1]]).cpu().numpy()
-        Sa = torch.zeros(sp.n, dtype=torch.float64, device=dev).index_add_(0, seg, x[: offs[-1]].abs()).cpu().numpy()
-    else:
-        A = Sa = np.zeros(sp.n)
+    # (one copy of the spine products to the host; any-order sums there)
+    A = np.zeros(sp.n)
+    Sa = np.zeros(sp.n)
+    if offs[-1]:
+        xs = x[: offs[-1]].cpu().numpy()
+        seg = np.repeat(np.arange(sp.n), np.diff(offs))
+        A = np.bincount(seg, weights=xs, minlength=sp.n)
+        Sa = np.bincount(seg, weights=np.abs(xs), minlength=sp.n)
     L = np.diff(offs).astype(np.float64)
     B = np.array([2.0 * L[j] * np.ldexp(1.0, np.frexp(Sa[j])[1] - 53) if Sa[j] > 0 else 0.0 for j in range(sp.n)])
     lo = spine_records(sp, rep_all, A - B, policy, locked_set)
