@@ -58,18 +58,21 @@ __global__ void records_kernel(const int* victims, const long long* result, cons
 }
 
 // per spine node: the maximum key over the rank's device descendants (eff
-// after the selection's walk) and whether a locked node lies below
-__global__ void spine_report_kernel(const int* spine, int n_spine, const int* ch_off, const int* ch,
-                                    const Key2* keys, const int* eff, const int* sublock, const int* depth,
-                                    const int* gid, const std::uint8_t* flags, pbkv_spine_info* out) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// after the selection's walk) and whether a locked node lies below.  One CTA
+// per spine node strides over its children (the shared prefix has a child
+// per workflow group: a serial loop took 1 ms at config 4) and reduces.
+__global__ void __launch_bounds__(256) spine_report_kernel(const int* spine, int n_spine, const int* ch_off,
+                                                           const int* ch, const Key2* keys, const int* eff,
+                                                           const int* sublock, const int* depth, const int* gid,
+                                                           const std::uint8_t* flags, pbkv_spine_info* out) {
+    const int j = blockIdx.x;
     if (j >= n_spine) return;
     const int s = spine[j];
     // max over the in-order device children's eff (the walk stops below the
     // spine; spine children are combined on the host, shard.py)
     int e = -1;
     Key2 best{0, 0};
-    for (int q = ch_off[j]; q < ch_off[j + 1]; ++q) {
+    for (int q = ch_off[j] + static_cast<int>(threadIdx.x); q < ch_off[j + 1]; q += blockDim.x) {
         const int c = ch[q];
         if ((flags[c] & (kFlagTierMask | kFlagOutOfOrder)) != PBKV_TIER_DEVICE) continue;
         const int ec = eff[c];
@@ -77,6 +80,34 @@ __global__ void spine_report_kernel(const int* spine, int n_spine, const int* ch
         if (e < 0 || key_less(best, e, k, ec)) {
             e = ec;
             best = k;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long b0 = __shfl_xor_sync(0xffffffffu, best.w0, o);
+        const unsigned long long b1 = __shfl_xor_sync(0xffffffffu, best.w1, o);
+        const int be = __shfl_xor_sync(0xffffffffu, e, o);
+        const Key2 bk{b0, b1};
+        if (be >= 0 && (e < 0 || key_less(best, e, bk, be))) {
+            e = be;
+            best = bk;
+        }
+    }
+    __shared__ unsigned long long s0[8], s1[8];
+    __shared__ int se[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s0[warp] = best.w0;
+        s1[warp] = best.w1;
+        se[warp] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    e = -1;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        const Key2 bk{s0[w], s1[w]};
+        if (se[w] >= 0 && (e < 0 || key_less(best, e, bk, se[w]))) {
+            e = se[w];
+            best = bk;
         }
     }
     pbkv_spine_info r;
@@ -212,7 +243,7 @@ void shard_records(Context& c, long long* result_dev, pbkv_cand* out, long long 
 void shard_spine_report(Context& c, pbkv_spine_info* out) {
     const int n = static_cast<int>(c.spine.size());
     if (n == 0) return;
-    spine_report_kernel<<<(n + 127) / 128, 128, 0, c.stream>>>(c.spine_dev.p, n, c.sch_off.p, c.sch.p, c.keys.p,
+    spine_report_kernel<<<n, 256, 0, c.stream>>>(c.spine_dev.p, n, c.sch_off.p, c.sch.p, c.keys.p,
                                                                c.eff.p, c.sublock.p, c.depth.p, c.gid.p, c.flags.p,
                                                                out);
     PBKV_CUDA(cudaGetLastError());
