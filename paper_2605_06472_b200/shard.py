@@ -572,6 +572,7 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
             pieces.append(prods[r, b: b + int(cnt_all[r, j])])
         offs.append(offs[-1] + int(cnt_all[:, j].sum()))
     x = torch.cat(pieces) if pieces else torch.zeros(1, dtype=torch.float64, device=dev)
+    mark("spine products gathered")
     # fast path: the exact serial chain E and any-order sum A
     # both lie within L * ulp(sum|x|) / 2 of the real sum.  If the spine
     # records are after every candidate record for both ends of the interval,
@@ -584,11 +585,13 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
         seg = np.repeat(np.arange(sp.n), np.diff(offs))
         A = np.bincount(seg, weights=xs, minlength=sp.n)
         Sa = np.bincount(seg, weights=np.abs(xs), minlength=sp.n)
+    mark("spine interval sums")
     L = np.diff(offs).astype(np.float64)
     B = np.array([2.0 * L[j] * np.ldexp(1.0, np.frexp(Sa[j])[1] - 53) if Sa[j] > 0 else 0.0 for j in range(sp.n)])
     lo = spine_records(sp, rep_all, A - B, policy, locked_set)
     hi = spine_records(sp, rep_all, A + B, policy, locked_set)
     fast = np.isfinite(A).all() and lo.size == hi.size and np.array_equal(lo["gid"], hi["gid"])
+    mark("spine records (interval ends)")
     if fast and n_cand and lo.size:
         # the last record of every rank's run (only those come to the host)
         rr = [r for r in range(world) if counts[r] > 0]
