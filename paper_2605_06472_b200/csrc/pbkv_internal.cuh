@@ -295,6 +295,7 @@ struct Context {
     // small-cut path (select.cu): node sample, low list, histogram tables
     DevBuf<unsigned char> samp;
     DevBuf<int> low;
+    DevBuf<long long> cut_partial;  // sharded merge: per-CTA token sums
     DevBuf<unsigned long long> gbar;  // the persistent selection kernel's grid barrier
     DevBuf<unsigned int> small_u32;
     DevBuf<unsigned long long> small_u64;

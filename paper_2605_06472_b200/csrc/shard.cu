@@ -16,6 +16,8 @@
 // merge-path rank merge of the exchanged runs, single-CTA cut.
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pbkv {
@@ -175,41 +177,60 @@ __global__ void merge_runs_kernel(const pbkv_cand* src, const long long* run_sta
     }
 }
 
-// shortest prefix of the merged order with sum(len) >= needed (all if none)
-__global__ void __launch_bounds__(1024) merge_cut_kernel(const pbkv_cand* m, long long n, long long needed,
-                                                         int* victims, long long* result) {
-    using Scan = cub::BlockScan<long long, 1024>;
+// shortest prefix of the merged order with sum(len) >= needed (all if none),
+// in two launches over every SM: the tokens of each CTA's chunk, then each
+// CTA's prefix (the partial sums before it) and a block scan of its chunk --
+// element i is a victim iff the tokens before it are < needed; the element
+// that crosses `needed` (or the last CTA, when none does) writes the result
+constexpr int kCutT = 512;
+__global__ void __launch_bounds__(kCutT) cut_partials_kernel(const pbkv_cand* m, long long n, long long chunk,
+                                                             long long* partial) {
+    const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    long long s = 0;
+    for (long long i = b0 + threadIdx.x; i < b1; i += kCutT) s += m[i].len;
+    using Red = cub::BlockReduce<long long, kCutT>;
+    __shared__ typename Red::TempStorage tmp;
+    const long long t = Red(tmp).Sum(s);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void __launch_bounds__(kCutT) cut_apply_kernel(const pbkv_cand* m, long long n, long long chunk,
+                                                          const long long* partial, long long needed, int* victims,
+                                                          long long* result) {
+    using Scan = cub::BlockScan<long long, kCutT>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ long long cut_sh, freed_sh;
+    __shared__ long long pre_sh;
     if (threadIdx.x == 0) {
-        cut_sh = n;
-        freed_sh = 0;
+        long long p = 0;
+        for (unsigned int g = 0; g < blockIdx.x; ++g) p += partial[g];
+        pre_sh = p;
     }
     __syncthreads();
-    long long carry = 0;
-    for (long long c0 = 0; c0 < n; c0 += 1024) {
+    long long carry = pre_sh;
+    const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    if (carry >= needed) return;  // wholly after the cut
+    for (long long c0 = b0; c0 < b1; c0 += kCutT) {
         const long long i = c0 + threadIdx.x;
-        const long long v = i < n ? static_cast<long long>(m[i].len) : 0;
-        long long incl, agg;
-        Scan(tmp).InclusiveSum(v, incl, agg);
-        incl += carry;
-        const bool hit = i < n && incl >= needed && incl - v < needed;  // first index reaching needed
-        if (hit) {
-            cut_sh = i + 1;
-            freed_sh = incl;
-        }
+        const long long v = i < b1 ? static_cast<long long>(m[i].len) : 0;
+        long long excl, agg;
+        Scan(tmp).ExclusiveSum(v, excl, agg);
         __syncthreads();
+        excl += carry;
+        if (i < b1 && excl < needed) {
+            victims[i] = m[i].gid;
+            if (excl + v >= needed) {  // the cut
+                result[0] = i + 1;
+                result[1] = excl + v;
+                result[2] = 0;
+            }
+        }
         carry += agg;
-        if (cut_sh != n || carry >= needed) break;
+        if (carry >= needed) return;
     }
-    __syncthreads();
-    const long long cut = cut_sh;
-    const long long freed = cut == n && freed_sh == 0 ? carry : freed_sh;
-    for (long long i = threadIdx.x; i < cut; i += 1024) victims[i] = m[i].gid;
-    if (threadIdx.x == 0) {
-        result[0] = cut;
-        result[1] = freed;
-        result[2] = freed < needed ? 1 : 0;
+    if (blockIdx.x == gridDim.x - 1) {  // nothing reached `needed`: every record
+        result[0] = n;
+        result[1] = carry;
+        result[2] = carry < needed ? 1 : 0;
     }
 }
 
@@ -271,9 +292,20 @@ void shard_merge_cut(Context& c, const pbkv_cand* src, const long long* run_star
         PBKV_CUDA(cudaGetLastError());
         ++c.launches;
     }
-    merge_cut_kernel<<<1, 1024, 0, c.stream>>>(merged, total, needed, victims, result);
+    const long long chunk = std::max<long long>(4 * kCutT, (total + 295) / 296);
+    const unsigned int g = static_cast<unsigned int>(std::max<long long>(1, (total + chunk - 1) / chunk));
+    c.cut_partial.reserve(g);
+    if (total == 0) {  // nothing to take: the empty cut
+        PBKV_CUDA(cudaMemsetAsync(result, 0, 2 * sizeof(long long), c.stream));
+        const long long one = needed > 0 ? 1 : 0;
+        PBKV_CUDA(cudaMemcpyAsync(result + 2, &one, sizeof one, cudaMemcpyHostToDevice, c.stream));
+        PBKV_CUDA(cudaStreamSynchronize(c.stream));
+        return;
+    }
+    cut_partials_kernel<<<g, kCutT, 0, c.stream>>>(merged, total, chunk, c.cut_partial.p);
+    cut_apply_kernel<<<g, kCutT, 0, c.stream>>>(merged, total, chunk, c.cut_partial.p, needed, victims, result);
     PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
+    c.launches += 2;
 }
 
 }  // namespace pbkv

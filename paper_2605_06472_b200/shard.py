@@ -577,14 +577,15 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     # both lie within L * ulp(sum|x|) / 2 of the real sum.  If the spine
     # records are after every candidate record for both ends of the interval,
     # and the cut ends inside the candidates, the exact chains are not needed.
-    # (one copy of the spine products to the host; any-order sums there)
+    # any-order sums per spine node on the device, one small readback
     A = np.zeros(sp.n)
     Sa = np.zeros(sp.n)
-    if offs[-1]:
-        xs = x[: offs[-1]].cpu().numpy()
-        seg = np.repeat(np.arange(sp.n), np.diff(offs))
-        A = np.bincount(seg, weights=xs, minlength=sp.n)
-        Sa = np.bincount(seg, weights=np.abs(xs), minlength=sp.n)
+    segs = [j for j in range(sp.n) if offs[j + 1] > offs[j]]
+    if segs:
+        sums = torch.stack([x[offs[j]: offs[j + 1]].sum() for j in segs] +
+                           [x[offs[j]: offs[j + 1]].abs().sum() for j in segs]).cpu().numpy()
+        A[segs] = sums[: len(segs)]
+        Sa[segs] = sums[len(segs):]
     mark("spine interval sums")
     L = np.diff(offs).astype(np.float64)
     B = np.array([2.0 * L[j] * np.ldexp(1.0, np.frexp(Sa[j])[1] - 53) if Sa[j] > 0 else 0.0 for j in range(sp.n)])
