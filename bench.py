@@ -92,14 +92,18 @@ def churn_batch(rng, t, live: list[int], victims: np.ndarray, n_wf: int, n_inser
     synthetic generator's token namespaces (csrc/host/ops.hpp): the previous
     decision's first victims demoted (in eviction order each is a device
     leaf), then inserts and matches of live workflows along their own
-    shared + group + private paths, then one termination."""
+    shared + group + private paths, then one termination.  Returns the op
+    stream and the workflows whose state changed (the ones the simulator's
+    refresh_workflow re-forecasts, simulator.hpp:430-435)."""
     from paper_2605_06472_b200.ops import OpStream
 
     ops = OpStream()
+    touched = []
     for v in victims[:n_demote].tolist():
         ops.demote(int(v))
     for j in range(n_insert + n_match):
         w = int(live[int(rng.integers(len(live)))])
+        touched.append(w)
         toks = [(1 << 60) | i for i in range(32)] + [(2 << 60) | ((w // 16) << 20) | i for i in range(8)]
         toks.append((3 << 60) | w)
         toks += [int(x) for x in rng.integers(0, 4, size=int(rng.integers(1, 11)))]
@@ -111,7 +115,8 @@ def churn_batch(rng, t, live: list[int], victims: np.ndarray, n_wf: int, n_inser
     if len(live) > 1:
         w = live.pop(int(rng.integers(len(live))))
         ops.terminate(w)
-    return ops, None
+        touched.append(w)
+    return ops, sorted(set(touched))
 
 
 class ClockSampler:
@@ -688,21 +693,36 @@ def main():
     # takes a serving-loop batch of mutations (churn_batch: inserts of live
     # workflows, a termination, the previous decision's first victims
     # demoted); the timed call then uploads only the changed nodes
-    # (pbkv_mirror_sync -> pbkv_mirror_delta), the forecasts from ordinary
-    # (pageable) host memory, and takes the decision with a host locked list
-    # and host victim output.
+    # (pbkv_mirror_sync -> pbkv_mirror_delta), re-puts the forecasts of the
+    # workflows the batch touched (the simulator's refresh_workflow,
+    # simulator.hpp:430-435, fresh rows from ordinary pageable host memory)
+    # and drops the terminated one's (simulator.hpp:617), and takes the
+    # decision with a host locked list and host victim output.
+    import workloads as WL
+
     rng_e2e = np.random.default_rng(4242)
     live = [int(w) for w in wf.tolist() if w >= int(0.3 * n_wf)]
+    row_of = {int(w): i for i, w in enumerate(wf.tolist())}
+    P = P.copy()  # refreshed rows are written into the host forecast table
     pol.sync(t)  # the tracked tree's first sync is a full upload
     e2e_ms = []
     e2e_wall = []
     delta_nodes = []
+    delta_fc = []
     n_victims_e2e = 0
     last_victims = np.zeros(0, dtype=np.int32)
+    dropped = []
     for it in range(args.warmup + max(1, args.steps)):
-        ops, n_changed = churn_batch(rng_e2e, t, live, last_victims, n_wf)
+        ops, touched = churn_batch(rng_e2e, t, live, last_victims, n_wf)
         t.apply_ops(ops.words)
         ids = t.log(pos_prev)[1] if it else None
+        live_set = set(live)
+        gone = [w for w in touched if w not in live_set]
+        fresh = [w for w in touched if w in live_set]
+        rows = np.array([row_of[w] for w in fresh], dtype=np.int64)
+        P[rows] = WL.random_forecasts(rng_e2e, rows.size, K, AGENTS + 1)
+        wf_d = wf[rows]
+        P_d = np.ascontiguousarray(P[rows])
         flush.fill_(1)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -711,7 +731,9 @@ def main():
         e0.record(stream)
         pol.sync(t)
         tw1 = time.perf_counter()
-        pol.put_forecasts(wf, P)
+        if gone:
+            pol.drop_forecasts(gone)
+        pol.put_forecasts(wf_d, P_d)
         tw2 = time.perf_counter()
         sel = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
         e1.record(stream)
@@ -723,12 +745,24 @@ def main():
             e2e_wall.append((tw1 - tw0, tw2 - tw1, tw3 - tw2))
             e2e_ms.append(max(e0.elapsed_time(e1), 1e3 * (tw3 - tw0)))
             delta_nodes.append(len(ids) if ids is not None else 0)
+            delta_fc.append(int(P_d.nbytes + wf_d.nbytes + 8 * len(gone)))
+        dropped += gone
         n_victims_e2e = len(sel)
+    # the same decision when every forecast is re-put (host wall of the upload alone)
+    keep = np.array([i for i, w in enumerate(wf.tolist()) if w not in set(dropped)], dtype=np.int64)
+    wf_all, P_all = wf[keep], np.ascontiguousarray(P[keep])
+    put_all = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        pol.put_forecasts(wf_all, P_all)
+        torch.cuda.synchronize()
+        put_all.append(1e3 * (time.perf_counter() - w0))
     # the last e2e decision, checked against a fresh device-resident decision
     # on a full re-mirror of the same tree (victim ids in order)
     pol_chk = Policy(num_agents=AGENTS, k=K, gamma=GAMMA, device=local)
     pol_chk.mirror(t.export())
-    pol_chk.put_forecasts(wf, P)
+    pol_chk.put_forecasts(wf_all, P_all)
     chk = pol_chk.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
     assert np.array_equal(chk.victim_ids, sel.victim_ids) and chk.freed == sel.freed, \
         "e2e decision (incremental mirror) differs from a full re-mirror"
@@ -831,15 +865,20 @@ def main():
         "pipeline_c2": pipeline_c2(torch, dev) if not args.no_pipeline else None,
         "cpu_baseline": cpu,
         "e2e": {"value": total_nodes / (e2e * 1e-3), "unit": "nodes/s",
-                "h2d_bytes_per_step": int(P.nbytes + 8 * wf.size + 4 * locked.size
+                "h2d_bytes_per_step": int(statistics.mean(delta_fc) + 4 * locked.size
                                           + statistics.mean(delta_nodes) * (56 + 16 * E / N)),
                 "d2h_bytes_per_step": int(4 * n_victims_e2e + 24), "ms_per_step": e2e,
                 "p99_ms": float(np.percentile(e2e_ms, 99)),
                 "what": "per decision: tree delta sync (pbkv_mirror_sync of the nodes changed by a churn batch: "
                         "16 inserts + 8 matches of live workflows, 1 termination, the previous decision's first 64 "
-                        "victims demoted) + forecasts from pageable host memory + select with host locked list / "
+                        "victims demoted) + the touched workflows' forecasts re-put from pageable host memory "
+                        "(refresh_workflow) and the terminated one's dropped + select with host locked list / "
                         "host victims; max(device events, host wall)",
                 "delta_nodes_mean": statistics.mean(delta_nodes),
+                "forecast_bytes_mean": statistics.mean(delta_fc),
+                "put_all_forecasts_ms": statistics.median(put_all),
+                "ms_per_step_all_forecasts_est": e2e - 1e3 * statistics.median(w[1] for w in e2e_wall)
+                                             + statistics.median(put_all),
                 "mirror_verified": mirror_ok,
                 "host_wall_ms": {"sync": 1e3 * statistics.median(w[0] for w in e2e_wall),
                                  "put_forecasts": 1e3 * statistics.median(w[1] for w in e2e_wall),

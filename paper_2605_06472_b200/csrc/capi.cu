@@ -662,10 +662,8 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     if (prof) lap("start");
     need(c.n >= 1, "no tree mirrored");
     need(n_rec == 0 || d, "null delta records");
-    // the last record of a node wins
-    std::unordered_map<int, std::int64_t> last_of;
-    last_of.reserve(static_cast<std::size_t>(n_rec) * 2);
     int max_id = -1;
+    bool ascending = true;  // the tracked tree's batches: distinct ids, ascending
     for (std::int64_t i = 0; i < n_rec; ++i) {
         const pbkv_node_delta& r = d[i];
         need(r.id >= 0 && r.id < INT_MAX - 1, "delta: node id out of range");
@@ -675,16 +673,31 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
         for (std::int64_t e = r.acc_begin + 1; e < r.acc_end; ++e)
             if (acc_wf[e] <= acc_wf[e - 1]) invalid("tree delta: access entries must ascend by workflow id");
         if (r.depth < 0 || r.depth >= (1 << 24)) invalid("tree delta: bad depth");
-        last_of[r.id] = i;
+        if (i > 0 && r.id <= d[i - 1].id) ascending = false;
         max_id = std::max(max_id, r.id);
+    }
+    // records ordered by id, the last record of a node winning
+    std::vector<std::int64_t> order(static_cast<std::size_t>(n_rec));
+    for (std::int64_t i = 0; i < n_rec; ++i) order[static_cast<std::size_t>(i)] = i;
+    if (!ascending) {
+        std::stable_sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) { return d[a].id < d[b].id; });
+        std::size_t w = 0;
+        for (std::size_t k = 0; k < order.size(); ++k) {
+            if (k + 1 < order.size() && d[order[k + 1]].id == d[order[k]].id) continue;
+            order[w++] = order[k];
+        }
+        order.resize(w);
     }
     const std::int64_t n_old = c.n;
     const std::int64_t n_new = std::max<std::int64_t>(n_old, static_cast<std::int64_t>(max_id) + 1);
-    for (std::int64_t id = n_old; id < n_new; ++id)
-        need(last_of.count(static_cast<int>(id)) != 0, "delta: appended node ids must be dense");
-    for (const auto& [id, i] : last_of) {
+    {  // distinct ids below n_new: the appended ones are dense iff there are n_new - n_old of them
+        std::int64_t appended = 0;
+        for (std::int64_t i : order) appended += d[i].id >= n_old ? 1 : 0;
+        need(appended == n_new - n_old, "delta: appended node ids must be dense");
+    }
+    for (std::int64_t i : order) {
         const pbkv_node_delta& r = d[i];
-        if (id == 0) {
+        if (r.id == 0) {
             need(r.parent == -1, "delta: the root has no parent");
         } else if (r.parent < 0 || r.parent >= n_new) {
             invalid("tree delta: parent out of range");
@@ -692,14 +705,9 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     }
     if (!c.spine.empty()) {  // sharded shards keep their global-id map: no structural updates
         need(n_new == n_old, "delta: sharded contexts cannot append nodes");
-        for (const auto& [id, i] : last_of)
-            need(d[i].parent == c.h_parent[static_cast<std::size_t>(id)], "delta: sharded contexts cannot move nodes");
+        for (std::int64_t i : order)
+            need(d[i].parent == c.h_parent[static_cast<std::size_t>(d[i].id)], "delta: sharded contexts cannot move nodes");
     }
-    // order records by id (appended nodes last, ascending)
-    std::vector<std::int64_t> order;
-    order.reserve(last_of.size());
-    for (const auto& [id, i] : last_of) order.push_back(i);
-    std::sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) { return d[a].id < d[b].id; });
 
     lap("validate+order");
     // grow the mirror (keeping contents) and the host copies
@@ -744,6 +752,19 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
     std::vector<std::pair<int, int>> reparented;  // (node, old parent) (-2: fresh)
     std::int64_t E = c.E, q = 0;
     for (std::size_t k = 0; k < order.size(); ++k) {
+        if (k + 8 < order.size()) {  // sparse ids over 1M-entry host arrays: one miss per array per node
+            const std::size_t f = static_cast<std::size_t>(d[order[k + 8]].id);
+            if (f < c.h_entries.size()) {
+                __builtin_prefetch(&c.h_entries[f], 1);
+                __builtin_prefetch(&c.h_acc_beg[f], 1);
+                __builtin_prefetch(&c.h_acc_cap[f], 1);
+                __builtin_prefetch(&c.h_parent[f], 1);
+                __builtin_prefetch(&c.h_depth[f], 1);
+                __builtin_prefetch(&c.h_flags[f], 1);
+                __builtin_prefetch(&c.h_last[f], 1);
+                __builtin_prefetch(&c.h_len[f], 1);
+            }
+        }
         const pbkv_node_delta& r = d[order[k]];
         const std::size_t id = static_cast<std::size_t>(r.id);
         const bool fresh = r.id >= n_old;

@@ -292,6 +292,11 @@ struct Context {
     DevBuf<ulonglong2> listSK;
     DevBuf<unsigned int> listSC, listSC2;
     DevBuf<unsigned int> big;  // [2 * n]: (offset, count) of buckets sorted by rank counting
+    // oversized-bucket refinement of the selection (select.cu refine_buckets)
+    DevBuf<unsigned int> rf_u32;         // descriptors [2][2][cap] + histograms [2][cap][2048]
+    DevBuf<unsigned long long> rf_orand; // [2][cap][6]
+    DevBuf<unsigned int> rf_small;       // [2 * n]
+    DevBuf<ulonglong2> rf_tmpk;          // [n]
     // small-cut path (select.cu): node sample, low list, histogram tables
     DevBuf<unsigned char> samp;
     DevBuf<int> low;

@@ -103,6 +103,9 @@ struct SelState {
     unsigned long long n_low;   // heads at or below the sample bound
     unsigned long long or_low[3], and_low[3];
     unsigned long long est_low; // the sample's estimate of n_low (diagnostics)
+    unsigned int n_rf[2];       // oversized buckets being refined, by round parity
+    unsigned int n_rsmall;      // pieces of <= 32 heads the refinement produced
+    unsigned int rf_rounds;     // refinement rounds run (diagnostics)
     unsigned long long ts[40];  // %globaltimer after each phase (diagnostics)
     unsigned long long dbg[8];  // per-CTA maxima of phase work (diagnostics)
 };
@@ -223,6 +226,36 @@ __device__ __forceinline__ long long block_append(unsigned long long* counter, b
     return slot;
 }
 
+// exclusive prefix of one value per thread over the CTA; *total = the sum
+__device__ __forceinline__ unsigned int block_excl_u32(unsigned int v, unsigned long long* sh, unsigned int* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    __syncthreads();
+    if (lane == 31) sh[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const unsigned int s = lane < nw ? static_cast<unsigned int>(sh[lane]) : 0u;
+        unsigned int si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int t = __shfl_up_sync(0xffffffffu, si, o);
+            if (lane >= o) si += t;
+        }
+        if (lane < nw) sh[lane] = si - s;
+        if (lane == 31) sh[31] = si;
+    }
+    __syncthreads();
+    const unsigned int r = static_cast<unsigned int>(sh[w]) + inc - v;
+    if (total) *total = static_cast<unsigned int>(sh[31]);
+    __syncthreads();
+    return r;
+}
+
 // order-preserving packing of the varying bits of (w0, w1, id) into 64 bits;
 // the masks are walked a run of consecutive set bits at a time (the varying
 // bits are typically one or two runs per word: timestamp and id low bits)
@@ -245,6 +278,34 @@ __device__ __forceinline__ unsigned long long pack_key(const Key2& k, int id, un
     ext(k.w1, v1);
     ext(static_cast<unsigned long long>(static_cast<unsigned int>(id)), v2);
     return r;
+}
+
+// the same packing into 128 bits (hi, lo) for keys with 64..128 varying bits
+__device__ __forceinline__ void pack_key2(const Key2& k, int id, unsigned long long v0, unsigned long long v1,
+                                          unsigned long long v2, unsigned long long& hi, unsigned long long& lo) {
+    hi = 0;
+    lo = 0;
+    auto ext = [&](unsigned long long word, unsigned long long mask) {
+        while (mask) {
+            const int h = 63 - __clzll(static_cast<long long>(mask));
+            const unsigned long long above_cleared = ~mask & ((h == 63) ? ~0ull : ((1ull << (h + 1)) - 1ull));
+            const int l = above_cleared ? 64 - __clzll(static_cast<long long>(above_cleared)) : 0;
+            const int len = h - l + 1;
+            const unsigned long long run = (len == 64) ? ~0ull : ((1ull << len) - 1ull);
+            const unsigned long long bits = (word >> l) & run;
+            if (len == 64) {
+                hi = lo;
+                lo = bits;
+            } else {
+                hi = (hi << len) | (lo >> (64 - len));
+                lo = (lo << len) | bits;
+            }
+            mask &= ~(run << l);
+        }
+    };
+    ext(k.w0, v0);
+    ext(k.w1, v1);
+    ext(static_cast<unsigned long long>(static_cast<unsigned int>(id)), v2);
 }
 
 // one sampled eligible node (eff phase): key, id, token length
@@ -322,6 +383,14 @@ struct SelArgs {
     unsigned long long* sm_cs;
     unsigned long long* sm_wpre;
     unsigned long long* sm_cpre;
+    // oversized-bucket refinement (refine_buckets)
+    unsigned int rf_cap;        // bucket descriptors per round parity
+    unsigned int* rf_off;       // [2][rf_cap] bucket start in S
+    unsigned int* rf_cnt;       // [2][rf_cap] bucket size
+    unsigned int* rf_hist;      // [2][rf_cap][kBins] digit counts, then placement cursors
+    unsigned long long* rf_orand;  // [2][rf_cap][6] OR / AND of the key words
+    unsigned int* rf_small;     // [2 * n] (offset, count) of pieces with <= 32 heads
+    ulonglong2* rf_tmpk;        // [n] keys in flight (the scatter's staging)
 };
 
 // Chain weight / size of head h: the members' scatter-adds (phase_chains)
@@ -965,85 +1034,146 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S,
     }
 }
 
-// Buckets with > 32 heads: every element's rank is the number of smaller keys
-// in its bucket, counted from shared memory by 8 threads per element.  Tasks
-// are (bucket, chunk of 64 elements), spread over every CTA -- no barrier-
-// heavy single-CTA sort (a 1024-element bitonic took ~35 us in one CTA).
-constexpr int kRankChunk = 64;
-constexpr int kBigSh = 512;  // bucket-list entries cached in shared memory
+// Buckets with > 32 heads (at most kRankCap): every element's rank is the
+// number of smaller keys in its bucket, counted from shared memory by
+// kRankTpe threads per element.  Tasks are (bucket, chunk of kRankChunk
+// elements), task t on CTA t mod gridDim.x; a CTA finds its tasks through the
+// chunk-count prefix of the bucket list, a tile of kPThreads buckets at a
+// time.  The keys of a bucket are packed over the bucket's own varying bits
+// into one word when they fit, else two (one or two compares per pair).
+constexpr int kRankChunk = 128;
+constexpr int kRankTpe = kPThreads / kRankChunk;  // threads per ranked element
 __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, int* S2, unsigned int n_big,
                                               unsigned long long* k0, unsigned long long* k1, int* val,
-                                              bool packed, bool has_sk, unsigned long long v0,
-                                              unsigned long long v1, unsigned long long v2) {
-    // the bucket list is read once into shared memory (a serial walk of L2
-    // loads per CTA cost ~1 us per bucket)
-    __shared__ unsigned int big_sh[2 * kBigSh];
-    const bool cached = n_big <= static_cast<unsigned int>(kBigSh);
-    if (cached) {
+                                              bool has_sk, unsigned long long* sh) {
+    __shared__ unsigned int tile_sh[3 * kPThreads];  // per bucket of the tile: first task, offset, count
+    __shared__ unsigned long long red_sh[kPThreads / 32 + 1][6];
+    unsigned int* tp = tile_sh;
+    unsigned int* toff = tile_sh + kPThreads;
+    unsigned int* tcnt = tile_sh + 2 * kPThreads;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned int T = 0;  // first task of the tile
+    for (unsigned int b0 = 0; b0 < n_big; b0 += blockDim.x) {
+        const unsigned int bb = b0 + threadIdx.x;
+        const unsigned int m = min(static_cast<unsigned int>(blockDim.x), n_big - b0);
+        unsigned int off = 0, cnt = 0;
+        if (bb < n_big) {
+            off = __ldcg(&a.big[2 * bb]);
+            cnt = __ldcg(&a.big[2 * bb + 1]);
+        }
+        unsigned int tile_tasks = 0;
+        const unsigned int ex = block_excl_u32((cnt + kRankChunk - 1) / kRankChunk, sh, &tile_tasks);
+        tp[threadIdx.x] = ex;
+        toff[threadIdx.x] = off;
+        tcnt[threadIdx.x] = cnt;
         __syncthreads();
-        for (unsigned int i = threadIdx.x; i < 2 * n_big; i += blockDim.x) big_sh[i] = __ldcg(&a.big[i]);
-        __syncthreads();
-    }
-    unsigned int task = 0;
-    for (unsigned int b = 0; b < n_big; ++b) {
-        const unsigned int off = cached ? big_sh[2 * b] : __ldcg(&a.big[2 * b]);
-        const unsigned int cnt = cached ? big_sh[2 * b + 1] : __ldcg(&a.big[2 * b + 1]);
-        const unsigned int nch = (cnt + kRankChunk - 1) / kRankChunk;
-        // this CTA's chunks of bucket b: c with (task + c) % gridDim.x == blockIdx.x
-        unsigned int c = (blockIdx.x + gridDim.x - task % gridDim.x) % gridDim.x;
-        if (c < nch) {
-            __syncthreads();
+        // this CTA's first task at or after T
+        unsigned int t = T + (blockIdx.x + gridDim.x - T % gridDim.x) % gridDim.x;
+        for (; t < T + tile_tasks; t += gridDim.x) {
+            const unsigned int loc = t - T;
+            unsigned int lo = 0, hi = m - 1;  // last bucket of the tile whose first task is <= loc
+            while (lo < hi) {
+                const unsigned int mid = (lo + hi + 1) >> 1;
+                if (tp[mid] <= loc) lo = mid;
+                else hi = mid - 1;
+            }
+            const unsigned int boff = toff[lo], bcnt = tcnt[lo], c = loc - tp[lo];
             const unsigned long long tl0 = gtimer();
-            // the bucket's ids, keys and chain sizes: coalesced reads of S / SK / SC
-            // (the head list of take_all has no SK / SC: gathered instead)
-            for (unsigned int i = threadIdx.x; i < cnt; i += blockDim.x) {
-                const int x = __ldcg(&S[off + i]);
+            // the bucket's ids and keys: coalesced reads of S / SK (the head
+            // list of take_all has no SK: gathered instead); OR / AND of the
+            // key words on the way
+            unsigned long long o[3] = {0, 0, 0}, n3[3] = {~0ull, ~0ull, ~0ull};
+            for (unsigned int i = threadIdx.x; i < bcnt; i += blockDim.x) {
+                const int x = __ldcg(&S[boff + i]);
                 Key2 k;
-                unsigned int cz = 0;
                 if (has_sk) {
-                    const ulonglong2 kk = __ldcg(&a.listSK[off + i]);
+                    const ulonglong2 kk = __ldcg(&a.listSK[boff + i]);
                     k = Key2{kk.x, kk.y};
-                    if (packed) cz = __ldcg(&a.listSC[off + i]);
                 } else {
                     k = load_key(a.keys, x);
-                    if (packed) cz = chain_c(a, x);
                 }
-                if (packed) {  // k1 is free: it carries the chain sizes
-                    k0[i] = pack_key(k, x, v0, v1, v2);
-                    k1[i] = cz;
-                } else {
-                    k0[i] = k.w0;
-                    k1[i] = k.w1;
-                }
+                k0[i] = k.w0;
+                k1[i] = k.w1;
                 val[i] = x;
+                for (int w = 0; w < 3; ++w) {
+                    o[w] |= key_word(k, x, w);
+                    n3[w] &= key_word(k, x, w);
+                }
+            }
+            for (int w = 0; w < 3; ++w) {
+#pragma unroll
+                for (int q = 16; q > 0; q >>= 1) {
+                    o[w] |= __shfl_xor_sync(0xffffffffu, o[w], q);
+                    n3[w] &= __shfl_xor_sync(0xffffffffu, n3[w], q);
+                }
+            }
+            if (lane == 0)
+                for (int w = 0; w < 3; ++w) {
+                    red_sh[warp][w] = o[w];
+                    red_sh[warp][3 + w] = n3[w];
+                }
+            __syncthreads();
+            if (threadIdx.x < 6) {
+                unsigned long long r = threadIdx.x < 3 ? 0ull : ~0ull;
+                for (int q = 0; q < nw; ++q) r = threadIdx.x < 3 ? (r | red_sh[q][threadIdx.x]) : (r & red_sh[q][threadIdx.x]);
+                red_sh[kPThreads / 32][threadIdx.x] = r;
+            }
+            __syncthreads();
+            const unsigned long long v0 = red_sh[kPThreads / 32][0] ^ red_sh[kPThreads / 32][3];
+            const unsigned long long v1 = red_sh[kPThreads / 32][1] ^ red_sh[kPThreads / 32][4];
+            const unsigned long long v2 = (red_sh[kPThreads / 32][2] ^ red_sh[kPThreads / 32][5]) & 0xffffffffull;
+            const int vbits = __popcll(v0) + __popcll(v1) + __popcll(v2);
+            const bool packed = vbits <= 64;               // one word; k1 carries the chain sizes
+            const bool packed2 = !packed && vbits <= 128;  // two words (hi, lo)
+            if (packed) {
+                for (unsigned int i = threadIdx.x; i < bcnt; i += blockDim.x) {
+                    const int x = val[i];
+                    k0[i] = pack_key(Key2{k0[i], k1[i]}, x, v0, v1, v2);
+                    k1[i] = has_sk ? __ldcg(&a.listSC[boff + i]) : chain_c(a, x);
+                }
+            } else if (packed2) {
+                for (unsigned int i = threadIdx.x; i < bcnt; i += blockDim.x) {
+                    unsigned long long h, l;
+                    pack_key2(Key2{k0[i], k1[i]}, val[i], v0, v1, v2, h, l);
+                    k0[i] = h;
+                    k1[i] = l;
+                }
             }
             __syncthreads();
             const unsigned long long tl1 = gtimer();
             if (threadIdx.x == 0) atomicMax(&a.ss->dbg[2], tl1 - tl0);
-            for (; c < nch; c += gridDim.x) {
-                const unsigned int e = c * kRankChunk + threadIdx.x / 8, part = threadIdx.x % 8;
-                const bool in = e < cnt;
+            {
+                const unsigned int e = c * kRankChunk + threadIdx.x / kRankTpe, part = threadIdx.x % kRankTpe;
+                const bool in = e < bcnt;
                 const unsigned long long a0 = in ? k0[e] : 0ull, a1 = in && !packed ? k1[e] : 0ull;
                 const int av = in ? val[e] : -1;
                 unsigned int r = 0;
                 if (in && packed) {  // distinct 64-bit order-preserving keys: one compare each
 #pragma unroll 4
-                    for (unsigned int q = part; q < cnt; q += 8) r += k0[q] < a0 ? 1u : 0u;
+                    for (unsigned int q = part; q < bcnt; q += kRankTpe) r += k0[q] < a0 ? 1u : 0u;
+                } else if (in && packed2) {  // distinct 128-bit keys, branch-free
+#pragma unroll 4
+                    for (unsigned int q = part; q < bcnt; q += kRankTpe) {
+                        const unsigned long long h = k0[q];
+                        r += (h < a0 || (h == a0 && k1[q] < a1)) ? 1u : 0u;
+                    }
                 } else if (in) {
-                    for (unsigned int q = part; q < cnt; q += 8) r += sk_less(k0[q], k1[q], val[q], a0, a1, av) ? 1u : 0u;
+                    for (unsigned int q = part; q < bcnt; q += kRankTpe)
+                        r += sk_less(k0[q], k1[q], val[q], a0, a1, av) ? 1u : 0u;
                 }
-                r += __shfl_xor_sync(0xffffffffu, r, 1);
-                r += __shfl_xor_sync(0xffffffffu, r, 2);
-                r += __shfl_xor_sync(0xffffffffu, r, 4);
+#pragma unroll
+                for (int q = 1; q < kRankTpe; q <<= 1) r += __shfl_xor_sync(0xffffffffu, r, q);
                 if (in && part == 0) {
-                    S2[off + r] = av;
-                    a.listSC2[off + r] = packed ? static_cast<unsigned int>(k1[e])
-                                                : (has_sk ? __ldcg(&a.listSC[off + e]) : chain_c(a, av));
+                    S2[boff + r] = av;
+                    a.listSC2[boff + r] = packed ? static_cast<unsigned int>(k1[e])
+                                                 : (has_sk ? __ldcg(&a.listSC[boff + e]) : chain_c(a, av));
                 }
             }
             if (threadIdx.x == 0) atomicMax(&a.ss->dbg[3], gtimer() - tl1);
+            __syncthreads();  // the next task reloads the bucket arrays
         }
-        task += nch;
+        T += tile_tasks;
+        __syncthreads();  // the next tile overwrites the tile arrays
     }
 }
 
@@ -1695,6 +1825,298 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
     return true;
 }
 
+// ---- oversized buckets: MSD refinement ------------------------------
+// Rank counting costs O(cnt^2) per bucket, so a bucket of S with more than
+// kRankCap heads is split first: by a digit window (up to 11 bits) that
+// starts at its own top varying key bit, sized for pieces of ~2^kRfPieceLog
+// heads, round after round until every piece fits.  A round is OR/AND of the
+// key words -> digit histogram -> piece offsets -> scatter -> copy back (five
+// grid phases), with shared-memory aggregation per CTA (a CTA's contiguous
+// slice of the round's heads covers one bucket or a few).  Pieces of <= 32
+// heads go to the warp sorts, of <= kRankCap to the rank-counting sorts,
+// larger ones to the next round.  A round consumes at least the bucket's top
+// varying bit, and every live bucket holds more than kRankCap heads, so a
+// round has at most n / (kRankCap + 1) buckets.
+constexpr int kRankCap = 1024;
+constexpr int kRfPieceLog = 8;                                 // digit width aimed at ~256-head pieces
+constexpr int kRfSh = static_cast<int>(sizeof(unsigned long long) * 2 * kBucketCap + sizeof(int) * kBucketCap) /
+                      8;                                         // descriptors cached per CTA (prefix, offset)
+constexpr int kRfLoc = 64;                                     // buckets one CTA's slice may span
+
+// largest j with pre[j] <= v (pre strictly ascending, pre[0] = 0)
+__device__ __forceinline__ unsigned int rf_find(const unsigned int* pre, unsigned int n, unsigned int v) {
+    unsigned int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const unsigned int mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= v) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void rf_init_bucket(const SelArgs& a, int par, unsigned int q, unsigned int off,
+                                               unsigned int cnt) {
+    const std::size_t b = static_cast<std::size_t>(par) * a.rf_cap + q;
+    a.rf_off[b] = off;
+    a.rf_cnt[b] = cnt;
+    for (int w = 0; w < 3; ++w) {
+        a.rf_orand[b * 6 + w] = 0ull;
+        a.rf_orand[b * 6 + 3 + w] = ~0ull;
+    }
+}
+
+// Splits every bucket of S above kRankCap (all CTAs).  take_all: S is the
+// unsorted head list (no keys listed yet), one bucket.  Returns false (grid-
+// uniform) when a round has more buckets than a CTA caches: the caller falls
+// back to the device-wide sort.
+__device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar& grid, int& nts, bool take_all,
+                               unsigned long long nS) {
+    __shared__ unsigned int lo_sh[kRfLoc];       // (window low bit << 4) | width, per local bucket
+    __shared__ unsigned int oa_sh[kRfLoc][12];   // OR / AND of the key words, 32-bit halves
+    SelState* ss = a.ss;
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    int* S = a.listS;
+    if (take_all) {  // the head list with its keys and chain sizes, as the compaction lists S
+        for (std::int64_t i = tid; i < static_cast<std::int64_t>(nS); i += nthr) {
+            const int x = __ldcg(&a.heads[i]);
+            const Key2 k = load_key(a.keys, x);
+            S[i] = x;
+            a.listSK[i] = make_ulonglong2(k.w0, k.w1);
+            a.listSC[i] = chain_c(a, x);
+        }
+        if (tid == 0) {
+            ss->s_is_heads = 0;
+            ss->n_rf[0] = 1;
+            rf_init_bucket(a, 0, 0, 0u, static_cast<unsigned int>(nS));
+        }
+    } else if (blockIdx.x == 0) {  // oversized buckets leave the rank-sort list (count 0: no tasks)
+        const unsigned int nb = __ldcg(&ss->n_big);
+        for (unsigned int q = threadIdx.x; q < nb; q += blockDim.x) {
+            const unsigned int cnt = __ldcg(&a.big[2 * q + 1]);
+            if (cnt > static_cast<unsigned int>(kRankCap)) {
+                const unsigned int r = atomicAdd(&ss->n_rf[0], 1u);
+                if (r < a.rf_cap) rf_init_bucket(a, 0, r, __ldcg(&a.big[2 * q]), cnt);
+                a.big[2 * q + 1] = 0u;
+            }
+        }
+    }
+    grid.sync();
+    stamp(ss, nts);
+    unsigned int* pre = reinterpret_cast<unsigned int*>(&sm.u.sort);  // [kRfSh]
+    unsigned int* offs = pre + kRfSh;                                  // [kRfSh]
+    unsigned int* hloc = sm.off;                                       // [kBins] this CTA's digit counts / cursors
+    for (int par = 0;; par ^= 1) {
+        const int nx = par ^ 1;
+        if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->n_rf[par]);
+        __syncthreads();
+        const unsigned int n = static_cast<unsigned int>(sm.bc[0]);
+        __syncthreads();
+        if (n == 0) break;
+        if (n > static_cast<unsigned int>(kRfSh) || n > a.rf_cap) return false;
+        const std::size_t rb = static_cast<std::size_t>(par) * a.rf_cap;
+        // the round's descriptors and their prefix, per CTA
+        unsigned int total = 0;
+        for (unsigned int t0 = 0; t0 < n; t0 += blockDim.x) {
+            const unsigned int j = t0 + threadIdx.x;
+            const unsigned int c = j < n ? __ldcg(&a.rf_cnt[rb + j]) : 0u;
+            unsigned int tile = 0;
+            const unsigned int ex = block_excl_u32(c, sm.sh, &tile);
+            if (j < n) {
+                pre[j] = total + ex;
+                offs[j] = __ldcg(&a.rf_off[rb + j]);
+            }
+            total += tile;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            ss->n_rf[nx] = 0;
+            ss->rf_rounds += 1;
+        }
+        // this round's histogram rows, zeroed (read after the next barrier)
+        for (unsigned int j = blockIdx.x; j < n; j += gridDim.x)
+            for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x)
+                a.rf_hist[(rb + j) * kBins + d] = 0u;
+        // this CTA's contiguous slice of the round's heads and the buckets it spans
+        const unsigned int chunk = (total + gridDim.x - 1) / gridDim.x;
+        if (chunk / (kRankCap + 1) + 2 > static_cast<unsigned int>(kRfLoc)) return false;
+        const unsigned int v0 = min(total, blockIdx.x * chunk), v1 = min(total, v0 + chunk);
+        const unsigned int j0 = v0 < v1 ? rf_find(pre, n, v0) : 0u;
+        const unsigned int nloc = v0 < v1 ? rf_find(pre, n, v1 - 1) - j0 + 1 : 0u;
+        const bool single = nloc == 1;
+        for (unsigned int t = threadIdx.x; t < nloc * 12; t += blockDim.x)
+            oa_sh[t / 12][t % 12] = (t % 12) < 6 ? 0u : ~0u;
+        __syncthreads();
+        // (A) OR / AND of the key words per bucket: warp, then CTA, then one
+        // global atomic per word and bucket
+        for (unsigned int vb = v0; vb < v1; vb += blockDim.x) {
+            const unsigned int v = vb + threadIdx.x;
+            const bool in = v < v1;
+            unsigned int j = 0;
+            Key2 k{0, 0};
+            int x = 0;
+            if (in) {
+                j = rf_find(pre, n, v);
+                const unsigned int i = offs[j] + (v - pre[j]);
+                const ulonglong2 kk = __ldcg(&a.listSK[i]);
+                k = Key2{kk.x, kk.y};
+                x = __ldcg(&S[i]);
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, in ? j : 0xffffffffu);
+            const bool lead = in && lane == __ffs(peers) - 1;
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+                const unsigned long long kw = key_word(k, x, w);
+                const unsigned int ohi = __reduce_or_sync(peers, static_cast<unsigned int>(kw >> 32));
+                const unsigned int olo = __reduce_or_sync(peers, static_cast<unsigned int>(kw));
+                const unsigned int ahi = __reduce_and_sync(peers, static_cast<unsigned int>(kw >> 32));
+                const unsigned int alo = __reduce_and_sync(peers, static_cast<unsigned int>(kw));
+                if (lead) {
+                    unsigned int* o = oa_sh[j - j0];
+                    atomicOr(&o[2 * w], ohi);
+                    atomicOr(&o[2 * w + 1], olo);
+                    atomicAnd(&o[6 + 2 * w], ahi);
+                    atomicAnd(&o[6 + 2 * w + 1], alo);
+                }
+            }
+        }
+        __syncthreads();
+        for (unsigned int t = threadIdx.x; t < nloc * 6; t += blockDim.x) {
+            const unsigned int jj = t / 6, w = t % 6;
+            const unsigned long long val = (static_cast<unsigned long long>(oa_sh[jj][2 * w]) << 32) | oa_sh[jj][2 * w + 1];
+            unsigned long long* g = a.rf_orand + (rb + j0 + jj) * 6 + w;
+            if (w < 3) atomicOr(g, val);
+            else atomicAnd(g, val);
+        }
+        grid.sync();
+        stamp(ss, nts);
+        // (B) each bucket's digit window from its top varying bit down, wide
+        // enough for ~2^kRfPieceLog-head pieces; digit counts (in shared
+        // memory when the slice lies in one bucket)
+        for (unsigned int jj = threadIdx.x; jj < nloc; jj += blockDim.x) {
+            const unsigned int j = j0 + jj;
+            const int top = top_varying_bit_cg(a.rf_orand + (rb + j) * 6, a.rf_orand + (rb + j) * 6 + 3);
+            const unsigned int cnt = (j + 1 < n ? pre[j + 1] : total) - pre[j];
+            const int nb = min(kDigitBits, max(1, (32 - __clz(static_cast<int>(cnt - 1))) - kRfPieceLog));
+            lo_sh[jj] = (static_cast<unsigned int>(max(0, top - nb + 1)) << 4) | static_cast<unsigned int>(nb);
+        }
+        if (single)
+            for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x) hloc[d] = 0u;
+        __syncthreads();
+        for (unsigned int vb = v0; vb < v1; vb += blockDim.x) {
+            const unsigned int v = vb + threadIdx.x;
+            const bool in = v < v1;
+            unsigned int key = 0xffffffffu, j = 0, d = 0;
+            if (in) {
+                j = rf_find(pre, n, v);
+                const unsigned int i = offs[j] + (v - pre[j]);
+                const ulonglong2 kk = __ldcg(&a.listSK[i]);
+                const unsigned int lw = lo_sh[j - j0];
+                d = key_bits(Key2{kk.x, kk.y}, __ldcg(&S[i]), static_cast<int>(lw >> 4), static_cast<int>(lw & 15u));
+                key = (j << kDigitBits) | d;
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (in && lane == __ffs(peers) - 1) {
+                if (single) atomicAdd(&hloc[d], static_cast<unsigned int>(__popc(peers)));
+                else atomicAdd(&a.rf_hist[(rb + j) * kBins + d], static_cast<unsigned int>(__popc(peers)));
+            }
+        }
+        __syncthreads();
+        if (single)
+            for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x)
+                if (hloc[d]) atomicAdd(&a.rf_hist[(rb + j0) * kBins + d], hloc[d]);
+        grid.sync();
+        stamp(ss, nts);
+        // (C) piece offsets (the histogram rows become placement cursors) and
+        // the pieces' lists: warp sorts, rank sorts, next round
+        for (unsigned int j = blockIdx.x; j < n; j += gridDim.x) {
+            unsigned int* row = a.rf_hist + (rb + j) * kBins;
+            constexpr int kPer = kBins / kPThreads;
+            unsigned int c[kPer], s4 = 0;
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                c[q] = __ldcg(&row[threadIdx.x * kPer + q]);
+                s4 += c[q];
+            }
+            unsigned int at = offs[j] + block_excl_u32(s4, sm.sh, nullptr);
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                row[threadIdx.x * kPer + q] = at;
+                if (c[q] == 0u) {
+                } else if (c[q] <= 32u) {
+                    const unsigned int r = atomicAdd(&ss->n_rsmall, 1u);
+                    a.rf_small[2 * r] = at;
+                    a.rf_small[2 * r + 1] = c[q];
+                } else if (c[q] <= static_cast<unsigned int>(kRankCap)) {
+                    const unsigned int r = atomicAdd(&ss->n_big, 1u);
+                    a.big[2 * r] = at;
+                    a.big[2 * r + 1] = c[q];
+                } else {
+                    const unsigned int r = atomicAdd(&ss->n_rf[nx], 1u);
+                    if (r < a.rf_cap) rf_init_bucket(a, nx, r, at, c[q]);
+                }
+                at += c[q];
+            }
+        }
+        grid.sync();
+        stamp(ss, nts);
+        // (D) scatter into the pieces (staging: S2, the key buffer, SC2); a
+        // one-bucket slice reserves its ranges with one atomic per digit
+        if (single) {
+            for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x)
+                if (hloc[d]) hloc[d] = atomicAdd(&a.rf_hist[(rb + j0) * kBins + d], hloc[d]);
+            __syncthreads();
+        }
+        for (unsigned int vb = v0; vb < v1; vb += blockDim.x) {
+            const unsigned int v = vb + threadIdx.x;
+            const bool in = v < v1;
+            unsigned int key = 0xffffffffu, j = 0, d = 0, i = 0;
+            Key2 k{0, 0};
+            int x = 0;
+            if (in) {
+                j = rf_find(pre, n, v);
+                i = offs[j] + (v - pre[j]);
+                const ulonglong2 kk = __ldcg(&a.listSK[i]);
+                k = Key2{kk.x, kk.y};
+                x = __ldcg(&S[i]);
+                const unsigned int lw = lo_sh[j - j0];
+                d = key_bits(k, x, static_cast<int>(lw >> 4), static_cast<int>(lw & 15u));
+                key = (j << kDigitBits) | d;
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            const int leader = __ffs(peers) - 1;
+            unsigned int base = 0;
+            if (in && lane == leader)
+                base = single ? atomicAdd(&hloc[d], static_cast<unsigned int>(__popc(peers)))
+                              : atomicAdd(&a.rf_hist[(rb + j) * kBins + d], static_cast<unsigned int>(__popc(peers)));
+            base = __shfl_sync(peers, base, leader);
+            if (in) {
+                const unsigned int pos = base + __popc(peers & ((1u << lane) - 1u));
+                a.listS2[pos] = x;
+                a.rf_tmpk[pos] = make_ulonglong2(k.w0, k.w1);
+                a.listSC2[pos] = __ldcg(&a.listSC[i]);
+            }
+        }
+        grid.sync();
+        stamp(ss, nts);
+        // (E) copy back
+        for (unsigned int vb = v0; vb < v1; vb += blockDim.x) {
+            const unsigned int v = vb + threadIdx.x;
+            if (v < v1) {
+                const unsigned int j = rf_find(pre, n, v);
+                const unsigned int i = offs[j] + (v - pre[j]);
+                S[i] = __ldcg(&a.listS2[i]);
+                a.listSK[i] = __ldcg(&a.rf_tmpk[i]);
+                a.listSC[i] = __ldcg(&a.listSC2[i]);
+            }
+        }
+        grid.sync();
+        stamp(ss, nts);
+    }
+    return true;
+}
+
 __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PersistSmem& sm = *reinterpret_cast<PersistSmem*>(smem_raw);
@@ -1875,53 +2297,47 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     grid.sync();
     stamp(ss, nts);
 
-    // ---- sort every bucket of S (one CTA per bucket, shared memory) ------------------
-    if (threadIdx.x == 0) {
-        sm.bc[0] = __ldcg(&ss->or_S[0]) ^ __ldcg(&ss->and_S[0]);
-        sm.bc[1] = __ldcg(&ss->or_S[1]) ^ __ldcg(&ss->and_S[1]);
-        sm.bc[2] = (__ldcg(&ss->or_S[2]) ^ __ldcg(&ss->and_S[2])) & 0xffffffffull;
-    }
-    __syncthreads();
-    const unsigned long long v0 = sm.bc[0], v1 = sm.bc[1], v2 = sm.bc[2];
-    __syncthreads();
-    if (max_bucket > static_cast<unsigned int>(kBucketCap)) {
-        if (tid == 0) {
-            ss->host_sort = 1;  // device-wide sort driven from the host
-            ss->max_bucket = static_cast<int>(max_bucket);
+    // ---- sort every bucket of S (rank counting over every CTA, warp sorts) ------------
+    const bool refined = max_bucket > static_cast<unsigned int>(kRankCap);
+    if (refined) {
+        if (tid == 0) ss->max_bucket = static_cast<int>(max_bucket);
+        if (!refine_buckets(a, sm, grid, nts, take_all, nS)) {
+            if (tid == 0) ss->host_sort = 1;  // device-wide sort driven from the host (> 16 M nodes)
+            return;
         }
-        return;
+        S = a.listS;
     }
-    // the varying bits of S fit 64 bits (the common case): buckets rank on packed keys
-    const bool packed = __popcll(v0) + __popcll(v1) + __popcll(v2) <= 64;
     int* S2 = a.listS2;
-    if (take_all) {
+    if (take_all && !refined) {
         if (tid == 0 && nS > 0) {  // the whole head list is one bucket
             a.big[0] = 0u;
             a.big[1] = static_cast<unsigned int>(nS);
         }
         grid.sync();
-        rank_sort_big(a, S, S2, nS > 0 ? 1u : 0u, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val, packed,
-                      false, v0, v1, v2);
+        rank_sort_big(a, S, S2, nS > 0 ? 1u : 0u, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val, false, sm.sh);
     } else {
         const unsigned long long t0 = gtimer();
         if (threadIdx.x == 0) sm.bc[3] = __ldcg(&ss->n_big);
         __syncthreads();
         const unsigned int n_big = static_cast<unsigned int>(sm.bc[3]);
-        rank_sort_big(a, S, S2, n_big, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val, packed, true, v0,
-                      v1, v2);
+        rank_sort_big(a, S, S2, n_big, sm.u.sort.k0, sm.u.sort.k1, sm.u.sort.val, true, sm.sh);
         const unsigned long long t1 = gtimer();
         if (threadIdx.x == 0) {
             atomicMax(&ss->dbg[0], t1 - t0);
             atomicMax(&ss->dbg[4], static_cast<unsigned long long>(n_big));
         }
         // small buckets: one warp each; singletons and the cut head are copied
+        // (the compaction's buckets, then the refinement's pieces)
+        if (threadIdx.x == 0) sm.bc[2] = refined ? __ldcg(&ss->n_rsmall) : 0ull;
+        __syncthreads();
         const int nb = n_pass * kBins;
+        const int nbr = nb + static_cast<int>(sm.bc[2]);
         const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
         const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(blockDim.x)) >> 5);
-        for (int j = gwarp; j < nb; j += nwarps) {
-            const unsigned int cnt = __ldcg(&a.seg_cnt[j]);
+        for (int j = gwarp; j < nbr; j += nwarps) {
+            const unsigned int cnt = j < nb ? __ldcg(&a.seg_cnt[j]) : __ldcg(&a.rf_small[2 * (j - nb) + 1]);
             if (cnt == 0u || cnt > 32u) continue;
-            const unsigned int off = __ldcg(&a.seg_off[j]);
+            const unsigned int off = j < nb ? __ldcg(&a.seg_off[j]) : __ldcg(&a.rf_small[2 * (j - nb)]);
             if (cnt == 1u) {
                 if ((threadIdx.x & 31) == 0) {
                     S2[off] = __ldcg(&S[off]);
@@ -1931,7 +2347,7 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
                 warp_sort_bucket(a, S, S2, off, cnt);
             }
         }
-        if (tid == 0) {  // the cut head (its own bucket)
+        if (tid == 0 && !take_all) {  // the cut head (its own bucket)
             S2[nS - 1] = __ldcg(&S[nS - 1]);
             a.listSC2[nS - 1] = __ldcg(&a.listSC[nS - 1]);
         }
@@ -1947,17 +2363,32 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     stamp(ss, nts);
 
     // ---- chain starts: start[p] = sum of the chain sizes before S2[p] ----------------
-    // every CTA scans its own slice of S2; the prefix before the slice is
-    // recomputed redundantly by each CTA (sum of C over S2[0, c0)), which for
-    // the sizes a decision selects is cheaper than a single-CTA scan
+    // every CTA scans its own slice of S2.  The prefix before the slice is
+    // recomputed redundantly by each CTA (sum of C over S2[0, c0)) for the
+    // sizes a decision usually selects; above 64 K heads the slice sums go
+    // through global memory instead (one more grid phase)
     {
         using Scan = cub::BlockScan<unsigned long long, kPThreads>;
         const bool spread = nS <= 65536ull;
-        const unsigned long long per = spread ? (nS + gridDim.x - 1) / gridDim.x : nS;
-        const unsigned long long c0 = spread ? blockIdx.x * per : 0ull;
-        const unsigned long long c1 = spread ? min(nS, c0 + per) : (blockIdx.x == 0 ? nS : 0ull);
+        const unsigned long long per = (nS + gridDim.x - 1) / gridDim.x;
+        const unsigned long long c0 = min(nS, blockIdx.x * per);
+        const unsigned long long c1 = min(nS, c0 + per);
         unsigned long long carry = 0;
-        if (spread && c0 < c1) {
+        if (!spread) {
+            unsigned long long loc = 0;
+            for (unsigned long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) loc += __ldcg(&a.listSC2[i]);
+            loc = block_reduce_bits(loc, SumOp(), sm.sh);
+            if (threadIdx.x == 0) a.hist_w[blockIdx.x] = loc;  // (the radix passes' histograms are done)
+            grid.sync();
+            stamp(ss, nts);
+            unsigned long long pre = 0;
+            for (unsigned int q = threadIdx.x; q < blockIdx.x; q += blockDim.x) pre += __ldcg(&a.hist_w[q]);
+            carry = block_reduce_bits(pre, SumOp(), sm.sh);
+            if (threadIdx.x == 0) sm.bc[2] = carry;
+            __syncthreads();
+            carry = sm.bc[2];
+            __syncthreads();
+        } else if (c0 < c1) {
             unsigned long long pre = 0;
             // batches of 8 independent loads per thread (the prefix is L2-latency bound)
             for (unsigned long long i0 = static_cast<unsigned long long>(threadIdx.x) * 8; i0 < c0;
@@ -2239,6 +2670,20 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.sm_wpre = c.small_u64.p + 2 * kBins;
         a.sm_cpre = c.small_u64.p + 3 * kBins;
     }
+    {  // oversized-bucket refinement: a round has at most n / (kRankCap + 1) buckets
+        const std::size_t cap = static_cast<std::size_t>(c.n) / (kRankCap + 1) + 2;
+        c.rf_u32.reserve(4 * cap + 2 * cap * kBins);
+        c.rf_orand.reserve(2 * cap * 6);
+        c.rf_small.reserve(2 * static_cast<std::size_t>(c.n) + 2);
+        c.rf_tmpk.reserve(static_cast<std::size_t>(c.n) + 1);
+        a.rf_cap = static_cast<unsigned int>(cap);
+        a.rf_off = c.rf_u32.p;
+        a.rf_cnt = c.rf_u32.p + 2 * cap;
+        a.rf_hist = c.rf_u32.p + 4 * cap;
+        a.rf_orand = c.rf_orand.p;
+        a.rf_small = c.rf_small.p;
+        a.rf_tmpk = c.rf_tmpk.p;
+    }
     if (c.report_deferred) {  // the deferred-heavy reports are written in place, to pinned memory
         const std::size_t nh = static_cast<std::size_t>(c.n_heavy);
         const std::size_t bytes = (nh + 1) * sizeof(HeavyReport);
@@ -2282,12 +2727,12 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         std::fprintf(stderr,
                      "[pbkv select] n_heads=%llu total_tok=%llu take_all=%d host_sort=%d n_S=%llu n_pass=%d "
                      "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
-                     "path=%d low_ovf=%u n_low=%llu est_low=%llu n_big=%u "
+                     "path=%d low_ovf=%u n_low=%llu est_low=%llu n_big=%u rf_rounds=%u n_rsmall=%u "
                      "dbg(ns): sortCTA=%llu sortWarp=%llu chainstart=%llu maxbucket=%llu nbig=%llu eff=%llu "
                      "chains=%llu nbits=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
                      hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->path,
-                     hs->low_overflow, hs->n_low, hs->est_low, hs->n_big, hs->dbg[0],
+                     hs->low_overflow, hs->n_low, hs->est_low, hs->n_big, hs->rf_rounds, hs->n_rsmall, hs->dbg[0],
                      hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6], hs->dbg[7]);
     if (hs->host_sort) {
         // ---- fallback: device-wide sort of the selected heads -----------------------------

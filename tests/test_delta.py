@@ -137,3 +137,75 @@ def test_plain_mirror_then_sync_is_full():
     pol.mirror(t.export())
     pol.sync(t)
     assert pol.verify(t) == -1
+
+
+def _records(soa, ids):
+    """caller-built pbkv_node_delta records of `ids` from a snapshot"""
+    from paper_2605_06472_b200._abi import NODE_DELTA_DTYPE
+
+    r = np.zeros(len(ids), dtype=NODE_DELTA_DTYPE)
+    wf, bits = [], []
+    for k, i in enumerate(ids):
+        r[k]["id"], r[k]["parent"], r[k]["len"] = i, soa.parent[i], soa.len[i]
+        r[k]["ever_tagged"], r[k]["depth"] = soa.ever_tagged[i], soa.depth[i]
+        r[k]["tier"], r[k]["retired"] = soa.tier[i], soa.retired[i]
+        r[k]["last_access"], r[k]["score"] = soa.last_access[i], soa.score[i]
+        a, b = int(soa.acc_off[i]), int(soa.acc_off[i + 1])
+        r[k]["acc_begin"] = len(wf)
+        wf += soa.acc_wf[a:b].tolist()
+        bits += soa.acc_bits[a:b].tolist()
+        r[k]["acc_end"] = len(wf)
+    return r, np.array(wf, dtype=np.int64), np.array(bits, dtype=np.uint64)
+
+
+def _totals(soa):
+    keys = ("device_capacity", "device_used", "retired_device_tokens", "host_capacity", "host_used")
+    return {k: int(soa.scalars[k]) for k in keys}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_caller_delta_unordered_with_stale_duplicates(seed):
+    """pbkv_mirror_delta on caller-built batches in any order, with stale
+    records of the same node earlier in the batch: the last record wins."""
+    rng = np.random.default_rng(9500 + seed)
+    t = HostTree()
+    live, nxt = _grow(rng, t)
+    pol = Policy(num_agents=4, k=3, gamma=0.7, device=0)
+    pol.mirror(t.export())
+    pos = t.log_end()
+    for b in range(6):
+        before = t.export()
+        t.apply_ops(WL.churn_ops(rng, before, live, nxt).words)
+        cur = t.export()
+        end, ids = t.log(pos)
+        pos = end
+        stale = [i for i in ids if i < before.n_nodes][: max(1, len(ids) // 3)]
+        r_old, w_old, b_old = _records(before, stale) if stale else _records(cur, [])
+        r_new, w_new, b_new = _records(cur, ids)
+        perm = rng.permutation(len(r_new))
+        r_new = r_new[perm]
+        r_old["acc_begin"] += w_new.size
+        r_old["acc_end"] += w_new.size
+        recs = np.concatenate([r_old, r_new])  # stale first (they lose), then the current ones shuffled
+        wf_all = np.concatenate([w_new, w_old]) if w_old.size else w_new
+        bits_all = np.concatenate([b_new, b_old]) if b_old.size else b_new
+        pol.apply_delta(recs, wf_all, bits_all, _totals(cur))
+        assert pol.verify(cur) == -1, f"batch {b}"
+    _decision_matches_oracle(pol, t.export(), rng)
+
+
+@pytest.mark.gpu
+def test_caller_delta_rejects_sparse_append():
+    from paper_2605_06472_b200.api import PbkvError
+
+    rng = np.random.default_rng(3)
+    t = HostTree()
+    _grow(rng, t)
+    soa = t.export()
+    pol = Policy(num_agents=4, k=3, device=0)
+    pol.mirror(soa)
+    r, w, b = _records(soa, [1])
+    r["id"] = soa.n_nodes + 1  # skips id n_nodes
+    with pytest.raises(PbkvError, match="dense"):
+        pol.apply_delta(r, w, b, _totals(soa))

@@ -48,7 +48,9 @@ def test_c3_scores_bit_exact(c3):
     assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
 
 
-@pytest.mark.parametrize("frac", [0.001, 0.01, 0.1, 0.5])
+# 0.5 / 0.9: buckets of S beyond one CTA's sort (the MSD refinement, select.cu
+# refine_buckets); 2.0: every head taken (take_all) with a shortfall
+@pytest.mark.parametrize("frac", [0.001, 0.01, 0.1, 0.5, 0.9, 2.0])
 def test_c3_victims_equal_oracle(c3, frac):
     t, soa, wf, P, locked, pol = c3
     s = soa.copy()
@@ -56,7 +58,9 @@ def test_c3_victims_equal_oracle(c3, frac):
     used = int(soa.len[soa.tier == 0][1:].sum())
     needed = max(1, int(frac * used))
     o = Oracle.select(s, POLICY_HE, needed, locked)
+    lib0 = pol.launches()[1]
     g = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+    assert pol.launches()[1] == lib0, "library kernels on the selection path"
     assert (g.freed, g.shortfall) == (o.freed, o.shortfall)
     assert g.victims == o.victims
     # properties of the cut
@@ -64,7 +68,20 @@ def test_c3_victims_equal_oracle(c3, frac):
     assert np.unique(v).size == v.size
     assert np.all(soa.tier[v] == 0) and np.all(v != 0)
     assert int(soa.len[v].sum()) == g.freed
-    assert g.freed >= needed and int(soa.len[v[:-1]].sum()) < needed
+    if not g.shortfall:
+        assert g.freed >= needed and int(soa.len[v[:-1]].sum()) < needed
+
+
+@pytest.mark.parametrize("frac", [0.5, 2.0])
+def test_c3_lru_large_cuts_equal_oracle(c3, frac):
+    from paper_2605_06472_b200._abi import POLICY_LRU
+
+    t, soa, wf, P, locked, pol = c3
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    needed = max(1, int(frac * used))
+    o = Oracle.select(soa, POLICY_LRU, needed, locked)
+    g = pol.select_victims(POLICY_LRU, needed, locked=locked)
+    assert (g.victims, g.freed, g.shortfall) == (o.victims, o.freed, o.shortfall)
 
 
 def test_c3_exact_path_equals_fast_path(c3):

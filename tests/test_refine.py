@@ -1,0 +1,47 @@
+"""Large cuts on mid-size trees (select.cu
+refine_buckets): buckets of the selected heads beyond one CTA's sort
+(> 4096 heads sharing their top key digits -- e.g. every retired head at
+score 0, or coarse forecasts tying thousands of scores) are split on the
+device round after round.  Victim order, freed and shortfall must equal the
+oracle for every policy, with and without locks, including take-all cuts
+(need above every evictable token), and no library kernel may run."""
+import numpy as np
+import pytest
+
+import workloads as WL
+from oracle import Oracle
+from paper_2605_06472_b200._abi import POLICY_HE, POLICY_LAE, POLICY_LRU, SCORE_RECOMPUTE
+from paper_2605_06472_b200.api import HostTree, Policy
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_large_cuts_equal_oracle(gpu, seed):
+    rng = np.random.default_rng(7700 + seed)
+    t = HostTree()
+    t.synth(n_nodes=int(rng.integers(40_000, 90_000)), n_workflows=int(rng.integers(256, 1024)), agents=8,
+            retired_frac=float(rng.choice([0.3, 0.6, 0.9])), seed=int(rng.integers(1 << 30)))
+    soa = t.export()
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    K = 4
+    P = WL.random_forecasts(rng, wf.size, K, 9, coarse=bool(seed % 2))
+    pol = Policy(num_agents=8, k=K, gamma=0.7)
+    pol.mirror(t)
+    pol.put_forecasts(wf, P)
+    s = soa.copy()
+    s.score[:] = Oracle.score_nodes(soa, wf, P, K, 0.7)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    locked = WL.random_locked(soa, rng, 0.02)
+    lib0 = pol.launches()[1]
+    for frac in (0.6, 0.97, 3.0):
+        needed = max(1, int(frac * used))
+        for lk in ([], locked):
+            o = Oracle.select(s, POLICY_HE, needed, lk)
+            g = pol.select_victims_hierarchical(needed, locked=lk, score_mode=SCORE_RECOMPUTE)
+            assert (g.victims, g.freed, g.shortfall) == (o.victims, o.freed, o.shortfall), ("he", frac)
+            for pid in (POLICY_LRU, POLICY_LAE):
+                o = Oracle.select(s, pid, needed, lk)
+                g = pol.select_victims(pid, needed, locked=lk)
+                assert (g.victims, g.freed, g.shortfall) == (o.victims, o.freed, o.shortfall), (pid, frac)
+    assert pol.launches()[1] == lib0, "library kernels on the selection path"
