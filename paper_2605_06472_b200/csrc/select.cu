@@ -1036,18 +1036,25 @@ __device__ __forceinline__ void warp_sort_bucket(const SelArgs& a, const int* S,
 
 // Buckets with > 32 heads (at most kRankCap): every element's rank is the
 // number of smaller keys in its bucket, counted from shared memory by
-// kRankTpe threads per element.  Tasks are (bucket, chunk of kRankChunk
+// kRankParts threads per group of kRankQuad elements.  Tasks are (bucket, chunk of kRankChunk
 // elements), task t on CTA t mod gridDim.x; a CTA finds its tasks through the
 // chunk-count prefix of the bucket list, a tile of kPThreads buckets at a
 // time.  The keys of a bucket are packed over the bucket's own varying bits
 // into one word when they fit, else two (one or two compares per pair).
+constexpr int kRankCap = 256;  // larger buckets are split first (refine_buckets)
+static_assert(kRankCap + (3 * kPThreads) / 2 + 6 * (kPThreads / 32 + 1) <= kBucketCap, "rank scratch exceeds k0");
 constexpr int kRankChunk = 128;
-constexpr int kRankTpe = kPThreads / kRankChunk;  // threads per ranked element
+constexpr int kRankQuad = 4;                                   // elements ranked per thread
+constexpr int kRankParts = kPThreads * kRankQuad / kRankChunk;  // threads per element group (16)
 __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, int* S2, unsigned int n_big,
                                               unsigned long long* k0, unsigned long long* k1, int* val,
                                               bool has_sk, unsigned long long* sh) {
-    __shared__ unsigned int tile_sh[3 * kPThreads];  // per bucket of the tile: first task, offset, count
-    __shared__ unsigned long long red_sh[kPThreads / 32 + 1][6];
+    // the bucket arrays hold at most kRankCap keys: the tile of the bucket
+    // list and the mask reduction live above them (no static shared memory:
+    // the L1 share of the eff walk's gathers stays larger)
+    unsigned int* tile_sh = reinterpret_cast<unsigned int*>(k0 + kRankCap);  // [3 * kPThreads]
+    unsigned long long (*red_sh)[6] =
+        reinterpret_cast<unsigned long long (*)[6]>(k0 + kRankCap + (3 * kPThreads) / 2);  // [kPThreads / 32 + 1][6]
     unsigned int* tp = tile_sh;
     unsigned int* toff = tile_sh + kPThreads;
     unsigned int* tcnt = tile_sh + 2 * kPThreads;
@@ -1142,31 +1149,55 @@ __device__ __forceinline__ void rank_sort_big(const SelArgs& a, const int* S, in
             __syncthreads();
             const unsigned long long tl1 = gtimer();
             if (threadIdx.x == 0) atomicMax(&a.ss->dbg[2], tl1 - tl0);
-            {
-                const unsigned int e = c * kRankChunk + threadIdx.x / kRankTpe, part = threadIdx.x % kRankTpe;
-                const bool in = e < bcnt;
-                const unsigned long long a0 = in ? k0[e] : 0ull, a1 = in && !packed ? k1[e] : 0ull;
-                const int av = in ? val[e] : -1;
-                unsigned int r = 0;
-                if (in && packed) {  // distinct 64-bit order-preserving keys: one compare each
-#pragma unroll 4
-                    for (unsigned int q = part; q < bcnt; q += kRankTpe) r += k0[q] < a0 ? 1u : 0u;
-                } else if (in && packed2) {  // distinct 128-bit keys, branch-free
-#pragma unroll 4
-                    for (unsigned int q = part; q < bcnt; q += kRankTpe) {
+            {  // kRankQuad elements per thread group, each loaded key compared against all of them
+                const unsigned int g = threadIdx.x / kRankParts, part = threadIdx.x % kRankParts;
+                const unsigned int e0 = c * kRankChunk + g * kRankQuad;
+                unsigned long long x0[kRankQuad], x1[kRankQuad];
+                unsigned int r[kRankQuad];
+#pragma unroll
+                for (int j = 0; j < kRankQuad; ++j) {
+                    const unsigned int e = e0 + j;
+                    x0[j] = e < bcnt ? k0[e] : 0ull;
+                    x1[j] = e < bcnt ? k1[e] : 0ull;
+                    r[j] = 0;
+                }
+                if (packed) {  // distinct 64-bit order-preserving keys: one compare each
+#pragma unroll 2
+                    for (unsigned int q = part; q < bcnt; q += kRankParts) {
                         const unsigned long long h = k0[q];
-                        r += (h < a0 || (h == a0 && k1[q] < a1)) ? 1u : 0u;
+#pragma unroll
+                        for (int j = 0; j < kRankQuad; ++j) r[j] += h < x0[j] ? 1u : 0u;
                     }
-                } else if (in) {
-                    for (unsigned int q = part; q < bcnt; q += kRankTpe)
-                        r += sk_less(k0[q], k1[q], val[q], a0, a1, av) ? 1u : 0u;
+                } else if (packed2) {  // distinct 128-bit keys, branch-free
+#pragma unroll 2
+                    for (unsigned int q = part; q < bcnt; q += kRankParts) {
+                        const unsigned long long h = k0[q], l = k1[q];
+#pragma unroll
+                        for (int j = 0; j < kRankQuad; ++j) r[j] += (h < x0[j] || (h == x0[j] && l < x1[j])) ? 1u : 0u;
+                    }
+                } else {
+                    for (unsigned int q = part; q < bcnt; q += kRankParts)
+#pragma unroll
+                        for (int j = 0; j < kRankQuad; ++j) {
+                            const unsigned int e = e0 + j;
+                            r[j] += e < bcnt && sk_less(k0[q], k1[q], val[q], x0[j], x1[j], val[e]) ? 1u : 0u;
+                        }
                 }
 #pragma unroll
-                for (int q = 1; q < kRankTpe; q <<= 1) r += __shfl_xor_sync(0xffffffffu, r, q);
-                if (in && part == 0) {
-                    S2[boff + r] = av;
-                    a.listSC2[boff + r] = packed ? static_cast<unsigned int>(k1[e])
-                                                 : (has_sk ? __ldcg(&a.listSC[boff + e]) : chain_c(a, av));
+                for (int j = 0; j < kRankQuad; ++j)
+#pragma unroll
+                    for (int q = 1; q < kRankParts; q <<= 1) r[j] += __shfl_xor_sync(0xffffffffu, r[j], q);
+                if (part == 0) {
+#pragma unroll
+                    for (int j = 0; j < kRankQuad; ++j) {
+                        const unsigned int e = e0 + j;
+                        if (e < bcnt) {
+                            const int av = val[e];
+                            S2[boff + r[j]] = av;
+                            a.listSC2[boff + r[j]] = packed ? static_cast<unsigned int>(k1[e])
+                                                            : (has_sk ? __ldcg(&a.listSC[boff + e]) : chain_c(a, av));
+                        }
+                    }
                 }
             }
             if (threadIdx.x == 0) atomicMax(&a.ss->dbg[3], gtimer() - tl1);
@@ -1837,11 +1868,12 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
 // larger ones to the next round.  A round consumes at least the bucket's top
 // varying bit, and every live bucket holds more than kRankCap heads, so a
 // round has at most n / (kRankCap + 1) buckets.
-constexpr int kRankCap = 1024;
-constexpr int kRfPieceLog = 8;                                 // digit width aimed at ~256-head pieces
-constexpr int kRfSh = static_cast<int>(sizeof(unsigned long long) * 2 * kBucketCap + sizeof(int) * kBucketCap) /
-                      8;                                         // descriptors cached per CTA (prefix, offset)
+constexpr int kRfPieceLog = 7;                                 // digit width aimed at ~128-head pieces
+constexpr int kRfSh = 8192;                                   // descriptors cached per CTA (prefix, offset)
 constexpr int kRfLoc = 64;                                     // buckets one CTA's slice may span
+static_assert(2 * kRfSh * 4 + kRfLoc * 13 * 4 <= static_cast<int>(sizeof(unsigned long long) * 2 * kBucketCap +
+                                                                  sizeof(int) * kBucketCap),
+              "refinement scratch exceeds the sort arrays");
 
 // largest j with pre[j] <= v (pre strictly ascending, pre[0] = 0)
 __device__ __forceinline__ unsigned int rf_find(const unsigned int* pre, unsigned int n, unsigned int v) {
@@ -1871,8 +1903,6 @@ __device__ __forceinline__ void rf_init_bucket(const SelArgs& a, int par, unsign
 // back to the device-wide sort.
 __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar& grid, int& nts, bool take_all,
                                unsigned long long nS) {
-    __shared__ unsigned int lo_sh[kRfLoc];       // (window low bit << 4) | width, per local bucket
-    __shared__ unsigned int oa_sh[kRfLoc][12];   // OR / AND of the key words, 32-bit halves
     SelState* ss = a.ss;
     const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
     const std::int64_t nthr = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
@@ -1906,6 +1936,8 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
     stamp(ss, nts);
     unsigned int* pre = reinterpret_cast<unsigned int*>(&sm.u.sort);  // [kRfSh]
     unsigned int* offs = pre + kRfSh;                                  // [kRfSh]
+    unsigned int* lo_sh = offs + kRfSh;  // [kRfLoc] (window low bit << 4) | width, per local bucket
+    unsigned int (*oa_sh)[12] = reinterpret_cast<unsigned int (*)[12]>(lo_sh + kRfLoc);  // OR / AND halves
     unsigned int* hloc = sm.off;                                       // [kBins] this CTA's digit counts / cursors
     for (int par = 0;; par ^= 1) {
         const int nx = par ^ 1;

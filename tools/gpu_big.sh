@@ -7,3 +7,5 @@ PBKV_DEBUG_SELECT=1 timeout 300 python bench.py --steps 3 --warmup 3 --no-pipeli
 grep "pbkv select" gpurun_out/big.log | tail -1 | cut -c1-400
 python tools/show_bench.py gpurun_out/big.log 2>/dev/null | head -3
 done
+timeout 300 python bench.py --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch > gpurun_out/bench_c3.log 2>&1
+python tools/show_bench.py gpurun_out/bench_c3.log 2>/dev/null | head -12
