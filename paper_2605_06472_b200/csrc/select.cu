@@ -10,18 +10,18 @@
 // The whole selection after the keys is ONE persistent kernel (two 512-thread
 // CTAs per SM, co-resident by cooperative launch, phases separated by grid
 // barriers):
-//   lock marks -> eff (CAS walk-up) -> chains (each head walks its own chain:
-//   token weight W[h], size C[h]; no atomics) -> weighted MSD radix select on
-//   the head keys: 11-bit digits at the top varying bit of the surviving
-//   candidates, per-CTA partial histograms reduced across the grid; heads
-//   below the chosen digit are placed into their digit's bucket of the
-//   selected list S (counting sort), so S is ordered bucket by bucket ->
-//   every bucket sorted by one CTA in shared memory (bitonic on
-//   order-preserving packed keys) -> chain starts (scan of chain sizes) ->
-//   chain scatter -> cut.
-// No host round trip in the common case.  A bucket larger than one CTA's
-// sort (or keys with >= 64 varying bits) falls back to a device-wide CUB
-// sort of S driven from the host.
+//   lock marks + eff (queued CAS walk-ups) + the small-cut bound from a node
+//   sample -> chains (scatter-added weight W and size C per head) ->
+//   small-cut path: the heads at or below the bound bucketed by one 9-bit
+//   digit and ranked in place, each selected head scattering its own chain;
+//   or the full radix path: weighted MSD radix select on the head keys
+//   (11-bit digits at the top varying bit of the surviving candidates),
+//   heads below the chosen digit placed into their digit's bucket of the
+//   selected list S -> oversized buckets split in place (refine_buckets) ->
+//   every bucket ranked (warp sorts <= 32, rank-counting tasks <= 256) ->
+//   chain starts (scan of chain sizes) -> chain scatter -> cut.
+// No host round trip.  The CUB device sort below the kernel is the last
+// resort of a refinement round with more than kRfSh buckets (> 2 M heads).
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
