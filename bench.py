@@ -684,7 +684,7 @@ def main():
         prefetch["round"] = {
             "what": "pbkv_prefetch_round over the plan's selected candidates with device_free = 0 (host wall of "
                     "the public call: one hierarchical decision + the per-candidate retired-prefix scan)",
-            "candidates": int(sel_ids.size), "promoted": int(sum(prom)), "victims": int(sum(len(v) for v in vics)),
+            "candidates": int(sel_ids.size), "promoted": int(sum(prom)), "victims": int(vics.flat.size),
             "ms_mean": statistics.mean(rw), "ms_p99": float(np.percentile(rw, 99))}
         prefetch["_round_first"] = (int(sel_ids[0]) if sel_ids.size else None, sel_ids)
 

@@ -91,6 +91,50 @@ class VictimSelection:
         return f"VictimSelection(victims={self.victims!r}, freed={self.freed}, shortfall={self.shortfall})"
 
 
+class RoundVictims:
+    """The victims demoted before each candidate of a prefetch round, as one
+    flat array with per-candidate ends; indexes and compares like the list of
+    lists the reference loop produces (simulator.hpp:649-672)."""
+
+    __slots__ = ("flat", "ends")
+
+    def __init__(self, flat: np.ndarray, ends: np.ndarray):
+        self.flat = flat
+        self.ends = ends
+
+    def __len__(self) -> int:
+        return int(self.ends.size)
+
+    def __getitem__(self, i: int) -> list[int]:
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        b = int(self.ends[i - 1]) if i else 0
+        return self.flat[b: int(self.ends[i])].tolist()
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, RoundVictims):
+            return np.array_equal(self.flat, other.flat) and np.array_equal(self.ends, other.ends)
+        try:
+            if len(other) != len(self):
+                return False
+            lens = np.diff(np.concatenate([[0], self.ends]))
+            if any(len(o) != int(l) for o, l in zip(other, lens)):
+                return False
+            flat = [int(v) for o in other for v in o]
+            return np.array_equal(self.flat, np.asarray(flat, dtype=self.flat.dtype))
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"RoundVictims({list(self)!r})"
+
+
 class PrefetchPlan:
     """policies.hpp:170-177.
 
@@ -454,18 +498,14 @@ class Policy:
         decision: (promoted flags, victims demoted before each candidate)."""
         sel = np.ascontiguousarray(np.asarray(selected, dtype=np.int32))
         n = int(sel.size)
-        prom = np.zeros(max(n, 1), dtype=np.int32)
-        vend = np.zeros(max(n, 1), dtype=np.int64)
+        prom = np.empty(max(n, 1), dtype=np.int32)
+        vend = np.empty(max(n, 1), dtype=np.int64)
         cap = max(int(self.n_nodes), 1)
-        vict = np.zeros(cap, dtype=np.int32)
+        vict = np.empty(cap, dtype=np.int32)
         nv = C.c_int64()
         self._c(_abi.lib().pbkv_prefetch_round(self._h, ptr(sel, C.c_int32), n, int(device_free), ptr(prom, C.c_int32),
                                                 ptr(vend, C.c_int64), ptr(vict, C.c_int32), cap, C.byref(nv)))
-        out, b = [], 0
-        for i in range(n):
-            out.append(vict[b:vend[i]].tolist())
-            b = int(vend[i])
-        return prom[:n].tolist(), out
+        return prom[:n].tolist(), RoundVictims(vict[: nv.value].copy(), vend[:n].copy())
 
     def plan_conservative_prefetch(self, bandwidth: int, step_duration: int = 1) -> PrefetchPlan:
         """policies.hpp:220-224"""

@@ -58,6 +58,12 @@ void poison_slot(Context& c, std::size_t slot) {
     PBKV_CUDA(cudaMemsetAsync(c.Pg.p + slot * row, 0xFF, row * sizeof(double), c.stream));
 }
 
+// zero a device buffer's elements [from, capacity)
+template <class T>
+void zero_tail(DevBuf<T>& b, std::size_t from, cudaStream_t st) {
+    if (b.p && from < b.cap) PBKV_CUDA(cudaMemsetAsync(b.p + from, 0, (b.cap - from) * sizeof(T), st));
+}
+
 int slot_for(Context& c, std::int64_t wf) {
     // dense ids (the simulator allocates WorkflowIds monotonically) hit a
     // direct table; others fall back to the hash map
@@ -508,6 +514,10 @@ void mirror_full(Context& c, const pbkv_tree_soa& s) {
     c.acc_slot.reserve(static_cast<std::size_t>(E) + 1);
     c.acc_bits.reserve(static_cast<std::size_t>(E) + 1);
     cudaStream_t st = c.stream;
+    // the pool above the packed entries (where deltas allocate) is defined:
+    // the audit (pbkv_mirror_verify) copies the pool whole
+    zero_tail(c.acc_slot, static_cast<std::size_t>(E), st);
+    zero_tail(c.acc_bits, static_cast<std::size_t>(E), st);
     PBKV_CUDA(cudaMemcpyAsync(c.parent.p, s.parent, n * sizeof(int), cudaMemcpyHostToDevice, st));
     PBKV_CUDA(cudaMemcpyAsync(c.len.p, s.len, n * sizeof(int), cudaMemcpyHostToDevice, st));
     PBKV_CUDA(cudaMemcpyAsync(c.ever.p, s.ever_tagged, n * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -630,6 +640,8 @@ void repack_pool(Context& c) {
     bits_new.reserve(slot_new.cap);
     rng_new.reserve(std::max<std::size_t>(c.acc_rng.cap, nz));
     nb_d.reserve(nz);
+    zero_tail(slot_new, top, c.stream);
+    zero_tail(bits_new, top, c.stream);
     PBKV_CUDA(cudaMemcpyAsync(nb_d.p, nb.data(), nz * sizeof(unsigned int), cudaMemcpyHostToDevice, c.stream));
     pool_repack_kernel<<<grid_for(c.n, 256), 256, 0, c.stream>>>(c.acc_rng.p, nb_d.p, c.n, c.acc_slot.p,
                                                                 c.acc_bits.p, slot_new.p, bits_new.p, rng_new.p);
@@ -830,6 +842,8 @@ void mirror_delta(Context& c, const pbkv_node_delta* d, std::int64_t n_rec, cons
         const std::size_t keep = c.acc_slot.cap;
         c.acc_slot.grow_keep(static_cast<std::size_t>(c.pool_top), keep, st);
         c.acc_bits.grow_keep(static_cast<std::size_t>(c.pool_top), keep, st);
+        zero_tail(c.acc_slot, keep, st);  // segment slack stays defined
+        zero_tail(c.acc_bits, keep, st);
     }
     // one pinned blob, one copy, one kernel
     auto align16 = [](std::size_t x) { return (x + 15) & ~std::size_t(15); };

@@ -2703,7 +2703,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.sm_cpre = c.small_u64.p + 3 * kBins;
     }
     {  // oversized-bucket refinement: a round has at most n / (kRankCap + 1) buckets
-        const std::size_t cap = static_cast<std::size_t>(c.n) / (kRankCap + 1) + 2;
+        // (a round above kRfSh buckets takes the fallback: no larger tables)
+        const std::size_t cap = std::min<std::size_t>(static_cast<std::size_t>(c.n) / (kRankCap + 1) + 2, kRfSh);
         c.rf_u32.reserve(4 * cap + 2 * cap * kBins);
         c.rf_orand.reserve(2 * cap * 6);
         c.rf_small.reserve(2 * static_cast<std::size_t>(c.n) + 2);

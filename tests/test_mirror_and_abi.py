@@ -109,3 +109,15 @@ def test_mirror_errors_are_validation_errors():
         from paper_2605_06472_b200.ops import OpStream
 
         t.apply_ops(OpStream().insert(list(range(200)), 1, 0).words)
+
+
+def test_round_victims_behaves_like_list_of_lists():
+    import numpy as np
+
+    from paper_2605_06472_b200.api import RoundVictims
+
+    rv = RoundVictims(np.array([5, 6, 7, 9], dtype=np.int32), np.array([0, 2, 2, 4], dtype=np.int64))
+    want = [[], [5, 6], [], [7, 9]]
+    assert rv == want and list(rv) == want and len(rv) == 4 and rv[-1] == [7, 9]
+    assert rv != [[], [5, 6], [], [7]] and rv != [[5], [6], [], [7, 9]] and rv != want[:3]
+    assert RoundVictims(np.zeros(0, np.int32), np.zeros(0, np.int64)) == []
