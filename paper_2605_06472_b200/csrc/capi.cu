@@ -79,6 +79,8 @@ int slot_for(Context& c, std::int64_t wf) {
     c.Pg.grow_keep(need_slots * c.K * c.V1, old * c.K * c.V1, c.stream);
     poison_slot(c, s_new_slot(c));
     c.gs.grow_keep(need_slots * c.K, old * c.K, c.stream);
+    // the new slot's gamma-weighted survival row (set by its first forecast)
+    PBKV_CUDA(cudaMemsetAsync(c.gs.p + old * c.K, 0xFF, static_cast<std::size_t>(c.K) * sizeof(double), c.stream));
     std::size_t old_cap = c.fstate.cap;
     c.fstate.grow_keep(need_slots, old, c.stream);
     if (c.fstate.cap != old_cap)
