@@ -380,6 +380,17 @@ struct DeltaBatch {
         wf.clear();
         bits.clear();
         for (std::size_t k = 0; k < ids.size(); ++k) {
+            if (k + kAhead < ids.size()) {  // scattered nodes: their lines (a Node spans three) in flight early
+                const char* q = reinterpret_cast<const char*>(&t.node(ids[k + kAhead]));
+                __builtin_prefetch(q);
+                __builtin_prefetch(q + 64);
+                __builtin_prefetch(q + 128);
+                __builtin_prefetch(&t.depths()[static_cast<std::size_t>(ids[k + kAhead])]);
+            }
+            if (k + kAhead / 2 < ids.size()) {  // the first entry of the access map, once its header is cached
+                const auto& acc = t.node(ids[k + kAhead / 2]).access;
+                if (!acc.empty()) __builtin_prefetch(&*acc.begin());
+            }
             const CacheTree::Node& nd = t.node(ids[k]);
             pbkv_node_delta& r = nodes[k];
             std::memset(&r, 0, sizeof r);
@@ -401,6 +412,7 @@ struct DeltaBatch {
         }
         totals = totals_of(t);
     }
+    static constexpr std::size_t kAhead = 16;
 };
 
 /// Brings the context's mirror of `t` up to date.  (uid, pos) is the

@@ -2182,12 +2182,14 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     // barrier (it initialised it above).
     // (a grid of one CTA -- small trees -- does the bound, then the walks)
     const bool solo = gridDim.x == 1;
+    const unsigned long long tp0 = gtimer();
     if (blockIdx.x == 0) {
         const SmallBound b = small_bound(a, sm);
         if (threadIdx.x == 0) {
             ss->bound_w0 = b.k.w0;
             ss->bound_w1 = b.k.w1;
             ss->bound_id = b.ok ? b.id : -1;
+            ss->dbg[5] = gtimer() - tp0;  // (diagnostics: the bound's time)
         }
     }
     if (blockIdx.x != 0 || solo) {
@@ -2201,7 +2203,11 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
         const WalkQueue q{reinterpret_cast<int*>(&sm.u.sort), &sm.qctl[0], &sm.qctl[1], kQ};
         const std::int64_t t0 = solo ? tid : tid - kPThreads, nt = solo ? nthr : nthr - kPThreads;
         phase_lock(a, t0, nt);
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&ss->dbg[7], gtimer() - tp0);  // (diagnostics: the slowest lock marking)
         phase_eff(a, t0, nt, q);
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&ss->dbg[6], gtimer() - tp0);  // (diagnostics: the slowest walking CTA)
     }
     grid.sync();
     stamp(ss, nts);
@@ -2761,8 +2767,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
                      "[pbkv select] n_heads=%llu total_tok=%llu take_all=%d host_sort=%d n_S=%llu n_pass=%d "
                      "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
                      "path=%d low_ovf=%u n_low=%llu est_low=%llu n_big=%u rf_rounds=%u n_rsmall=%u "
-                     "dbg(ns): sortCTA=%llu sortWarp=%llu chainstart=%llu maxbucket=%llu nbig=%llu eff=%llu "
-                     "chains=%llu nbits=%llu\n",
+                     "dbg(ns): sortCTA=%llu sortWarp=%llu loadpack=%llu rank=%llu nbig=%llu bound=%llu "
+                     "walk_end=%llu lock_end=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
                      hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->path,
                      hs->low_overflow, hs->n_low, hs->est_low, hs->n_big, hs->rf_rounds, hs->n_rsmall, hs->dbg[0],
