@@ -302,6 +302,7 @@ struct Context {
     DevBuf<int> low;
     DevBuf<long long> cut_partial;  // sharded merge: per-CTA token sums
     DevBuf<unsigned long long> gbar;  // the persistent selection kernel's grid barrier
+    int gbar_grid = 0;                // the grid size the counter is a multiple of (0: zero it first)
     DevBuf<unsigned int> small_u32;
     DevBuf<unsigned long long> small_u64;
     DevBuf<unsigned long long> hist_w, part_w;

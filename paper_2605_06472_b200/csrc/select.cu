@@ -383,6 +383,12 @@ struct SelArgs {
     unsigned long long* sm_cs;
     unsigned long long* sm_wpre;
     unsigned long long* sm_cpre;
+    // the fused epilogue (select_epilogue): pinned host destinations
+    DevStatus* h_st;
+    SelState* h_ss;
+    int* h_vict;                // null: the victims stay on the device
+    long long h_cap;
+    std::uint8_t* flags_w;      // the deferral is cleared in place
     // oversized-bucket refinement (refine_buckets)
     unsigned int rf_cap;        // bucket descriptors per round parity
     unsigned int* rf_off;       // [2][rf_cap] bucket start in S
@@ -2149,7 +2155,7 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
     return true;
 }
 
-__global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs a) {
+__device__ __forceinline__ void select_body(const SelArgs& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PersistSmem& sm = *reinterpret_cast<PersistSmem*>(smem_raw);
     const GridBar grid{a.gbar};
@@ -2479,6 +2485,40 @@ __global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs
     stamp(ss, nts);
 }
 
+// The decision's epilogue, after the last phase (every CTA): the victim ids
+// (16-byte stores, when they fit h_cap; larger cuts are copied by DMA), the
+// status word and the selection state straight into pinned host memory, and
+// the heavy-node deferral cleared unless the host-sort fallback still needs it.
+__device__ __forceinline__ void select_epilogue(const SelArgs& a) {
+    const SelState* ss = a.ss;
+    if (a.h_vict && !__ldcg(&ss->host_sort)) {
+        const long long nv = static_cast<long long>(__ldcg(&ss->n_victims));
+        if (nv <= a.h_cap) {
+            const long long n4 = nv >> 2;
+            const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+            const long long nt = static_cast<long long>(gridDim.x) * blockDim.x;
+            for (long long i = t; i < n4; i += nt)
+                reinterpret_cast<int4*>(a.h_vict)[i] = __ldcg(reinterpret_cast<const int4*>(a.victims) + i);
+            for (long long i = 4 * n4 + t; i < nv; i += nt) a.h_vict[i] = __ldcg(a.victims + i);
+        }
+    }
+    if (blockIdx.x != 0) return;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ss);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.h_ss);
+    for (unsigned int i = threadIdx.x; i < sizeof(SelState) / 8; i += blockDim.x) dst[i] = __ldcg(src + i);
+    if (threadIdx.x == 0) *a.h_st = *a.st;
+    if (__ldcg(&ss->host_sort)) return;
+    for (int i = threadIdx.x; i < a.n_report; i += blockDim.x)
+        a.flags_w[a.heavy[i]] &= static_cast<std::uint8_t>(~kFlagDeferred);
+}
+
+__global__ void __launch_bounds__(kPThreads, 2) select_persistent_kernel(SelArgs a) {
+    select_body(a);
+    const GridBar grid{a.gbar};
+    grid.sync();  // every phase's writes (victims, result, state) before the epilogue reads them
+    select_epilogue(a);
+}
+
 // ---- fallback path (a bucket larger than one CTA's sort) -----------------------------
 __global__ void pack_keys_kernel(const int* S, const Key2* keys, const SelState* ss, unsigned long long* out,
                                  int* ids) {
@@ -2576,36 +2616,6 @@ __global__ void __launch_bounds__(256) heavy_report_kernel(const int* heavy, int
 }
 }  // namespace
 
-// Last kernel of a decision: the status word and the selection state are
-// stored straight into pinned host memory (no device->host copy operations on
-// the critical path), and the heavy-node deferral is cleared unless the
-// host-sort fallback still needs it.
-// With h_vict, the victim ids too (when they fit h_cap; the host copies
-// larger cuts by DMA).
-__global__ void __launch_bounds__(256) decision_epilogue_kernel(const DevStatus* st, const SelState* ss,
-                                                                DevStatus* h_st, SelState* h_ss, std::uint8_t* flags,
-                                                                const int* heavy, int n_clear, const int* victims,
-                                                                int* h_vict, long long h_cap) {
-    if (h_vict) {  // every CTA: 16-byte stores over the victim ids
-        const long long nv = static_cast<long long>(__ldcg(&ss->n_victims));
-        if (!__ldcg(&ss->host_sort) && nv <= h_cap) {
-            const long long n4 = nv >> 2;
-            const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-            const long long nt = static_cast<long long>(gridDim.x) * blockDim.x;
-            for (long long i = t; i < n4; i += nt)
-                reinterpret_cast<int4*>(h_vict)[i] = __ldcg(reinterpret_cast<const int4*>(victims) + i);
-            for (long long i = 4 * n4 + t; i < nv; i += nt) h_vict[i] = __ldcg(victims + i);
-        }
-    }
-    if (blockIdx.x != 0) return;
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ss);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(h_ss);
-    for (unsigned int i = threadIdx.x; i < sizeof(SelState) / 8; i += blockDim.x) dst[i] = __ldcg(src + i);
-    if (threadIdx.x == 0) *h_st = *st;
-    if (__ldcg(&ss->host_sort)) return;
-    for (int i = threadIdx.x; i < n_clear; i += blockDim.x) flags[heavy[i]] &= static_cast<std::uint8_t>(~kFlagDeferred);
-}
-
 void launch_heavy_report(Context& c, long long* result_dev, HeavyReport* out, double* approx_out) {
     const int n = static_cast<int>(c.n_heavy);
     heavy_report_kernel<<<n + 1, 256, 0, c.stream>>>(c.heavy.p, n, c.hch_off.p, c.hch.p, c.keys.p,
@@ -2694,8 +2704,13 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         c.small_u32.reserve(7 * kBins);
         c.small_u64.reserve(4 * kBins);
         a.samp = reinterpret_cast<SampRec*>(c.samp.p);
-        c.gbar.reserve(1);  // the grid barrier's arrival counter, zeroed per launch (grid sizes vary)
-        PBKV_CUDA(cudaMemsetAsync(c.gbar.p, 0, sizeof(unsigned long long), c.stream));
+        // the grid barrier's arrival counter: every launch leaves it at a
+        // multiple of its grid size, so it is zeroed only when the grid changes
+        c.gbar.reserve(1);
+        if (c.gbar_grid != grid) {
+            PBKV_CUDA(cudaMemsetAsync(c.gbar.p, 0, sizeof(unsigned long long), c.stream));
+            c.gbar_grid = grid;
+        }
         a.gbar = c.gbar.p;
         a.low = c.low.p;
         a.sm_c = c.small_u32.p;
@@ -2736,6 +2751,11 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.approx = c.happrox.p;
         a.approx_out = reinterpret_cast<double*>(c.hreport_h.p + bytes);
     }
+    a.h_st = c.hstatus.p;
+    a.h_ss = hs;
+    a.h_vict = c.epi_vict;
+    a.h_cap = c.epi_cap;
+    a.flags_w = c.flags.p;
     void* args[] = {&a};
     if (c.timing) {
         PBKV_CUDA(cudaEventRecord(c.kev[2], c.stream));
@@ -2745,14 +2765,8 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
                                           dim3(kPThreads), args, sizeof(PersistSmem), c.stream));
     if (c.timing) PBKV_CUDA(cudaEventRecord(c.kev[3], c.stream));
     ++c.launches;
-    // status + selection state to the host, and the deferral cleared (unless
-    // the host-sort fallback below still needs it), before the host wakes up
-    decision_epilogue_kernel<<<c.epi_vict ? 8 : 1, 256, 0, c.stream>>>(c.status.p, ss, c.hstatus.p, hs, c.flags.p,
-                                                                        c.heavy.p,
-                                                      c.report_deferred ? static_cast<int>(c.n_heavy) : 0,
-                                                      c.vid_out.p, c.epi_vict, c.epi_cap);
-    PBKV_CUDA(cudaGetLastError());
-    ++c.launches;
+    // (the kernel's own epilogue stored the status, the selection state and
+    // the victims into pinned memory and cleared the deferral)
     PBKV_CUDA(cudaStreamSynchronize(c.stream));
     {
         const DevStatus st = *c.hstatus.p;  // a copy: raising may reuse the pinned word
