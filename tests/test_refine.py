@@ -10,7 +10,7 @@ import pytest
 
 import workloads as WL
 from oracle import Oracle
-from paper_2605_06472_b200._abi import POLICY_HE, POLICY_LAE, POLICY_LRU, SCORE_RECOMPUTE
+from paper_2605_06472_b200._abi import POLICY_HE, POLICY_KVFLOW, POLICY_LAE, POLICY_LRU, SCORE_RECOMPUTE
 from paper_2605_06472_b200.api import HostTree, Policy
 
 pytestmark = pytest.mark.gpu
@@ -44,4 +44,47 @@ def test_large_cuts_equal_oracle(gpu, seed):
                 o = Oracle.select(s, pid, needed, lk)
                 g = pol.select_victims(pid, needed, locked=lk)
                 assert (g.victims, g.freed, g.shortfall) == (o.victims, o.freed, o.shortfall), (pid, frac)
+    # KVFlow (steps-to-execution keys, policies.hpp kvflow): remaining agent
+    # sequences for every live workflow
+    remaining = {int(w): [int(a) for a in rng.integers(0, 8, size=int(rng.integers(0, 6)))] for w in wf.tolist()}
+    for frac in (0.6, 3.0):
+        needed = max(1, int(frac * used))
+        o = Oracle.select(s, POLICY_KVFLOW, needed, locked, remaining=remaining)
+        g = pol.select_victims(POLICY_KVFLOW, needed, remaining=remaining, locked=locked)
+        assert (g.victims, g.freed, g.shortfall) == (o.victims, o.freed, o.shortfall), ("kvflow", frac)
     assert pol.launches()[1] == lib0, "library kernels on the selection path"
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_sharded_large_cuts_equal_single(gpu, seed):
+    """Node-set shards (logical ranks on one GPU, shard.py) at large cuts:
+    every shard's local selection refines its own oversized buckets; the
+    merged decision equals the single-context one and the oracle."""
+    from paper_2605_06472_b200 import shard as S
+
+    rng = np.random.default_rng(7900 + seed)
+    t = HostTree()
+    t.synth(n_nodes=int(rng.integers(60_000, 120_000)), n_workflows=512, agents=8, seed=int(rng.integers(1 << 30)))
+    soa = t.export()
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, 4, 9)
+    locked = WL.pinned_paths(soa, rng, 0.01)
+    sps = []
+    for s in S.partition(soa, 4):
+        sp = S.ShardedPolicy(s, num_agents=8, k=4, gamma=0.7)
+        mine = (wf >= s.wf_lo) & (wf < s.wf_hi)
+        sp.pol.put_forecasts(wf[mine], P[mine])
+        sps.append(sp)
+    single = Policy(num_agents=8, k=4, gamma=0.7)
+    single.mirror(t)
+    single.put_forecasts(wf, P)
+    s2 = soa.copy()
+    s2.score[:] = Oracle.score_nodes(soa, wf, P, 4, 0.7)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    for frac in (0.5, 0.95):
+        needed = max(1, int(frac * used))
+        got = S.global_select(sps, POLICY_HE, SCORE_RECOMPUTE, needed, locked)
+        want = single.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+        assert (got[0].tolist(), got[1], got[2]) == (want.victims, want.freed, want.shortfall), frac
+        o = Oracle.select(s2, POLICY_HE, needed, locked)
+        assert (o.victims, o.freed, o.shortfall) == (want.victims, want.freed, want.shortfall), frac
