@@ -733,7 +733,7 @@ def main():
         tw1 = time.perf_counter()
         if gone:
             pol.drop_forecasts(gone)
-        pol.put_forecasts(wf_d, P_d)
+        pol.put_forecasts(wf_d, P_d, validate_now=False)  # validated on the device, raised by the select
         tw2 = time.perf_counter()
         sel = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
         e1.record(stream)

@@ -353,14 +353,17 @@ class Policy:
         self._c(_abi.lib().pbkv_mirror_set_scores(self._h, ptr(i, C.c_int32), ptr(s, C.c_double), int(i.size)))
 
     # ---- forecasts -----------------------------------------------------------------
-    def put_forecasts(self, wf_ids: Sequence[int], probs: np.ndarray) -> None:
-        """probs: [n, horizon, outcomes] float64 (Forecast rows, forecast.hpp:19)."""
+    def put_forecasts(self, wf_ids: Sequence[int], probs: np.ndarray, validate_now: bool = True) -> None:
+        """probs: [n, horizon, outcomes] float64 (Forecast rows, forecast.hpp:19).
+        validate_now=False (pbkv_forecast_put_async, the C++ shim's mode): no
+        synchronisation; a validation error (forecast.hpp:25-34) is raised by
+        the next call that reads the status word."""
         w = np.ascontiguousarray(wf_ids, dtype=np.int64)
         p = np.ascontiguousarray(probs, dtype=np.float64)
         if p.ndim != 3 or p.shape[0] != w.size:
             raise ValueError("probs must be [n_workflows, horizon, outcomes]")
-        self._c(_abi.lib().pbkv_forecast_put(self._h, ptr(w, C.c_int64), int(w.size), int(p.shape[1]),
-                                             int(p.shape[2]), ptr(p, C.c_double)))
+        fn = _abi.lib().pbkv_forecast_put if validate_now else _abi.lib().pbkv_forecast_put_async
+        self._c(fn(self._h, ptr(w, C.c_int64), int(w.size), int(p.shape[1]), int(p.shape[2]), ptr(p, C.c_double)))
 
     def drop_forecasts(self, wf_ids: Iterable[int]) -> None:
         w = np.ascontiguousarray(list(wf_ids), dtype=np.int64)

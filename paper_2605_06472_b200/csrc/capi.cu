@@ -1458,7 +1458,7 @@ int pbkv_forecast_drop(pbkv_ctx* c, const int64_t* wf, int64_t n) {
             PBKV_CUDA(cudaMemsetAsync(c->fstate.p + it->second, 0, 1, c->stream));
             poison_slot(*c, static_cast<std::size_t>(it->second));
         }
-        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        // stream-ordered: every later call on the context sees the drop
     });
 }
 

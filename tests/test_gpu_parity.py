@@ -191,6 +191,30 @@ def test_synthetic_config_parity(gpu, n_nodes, n_wf, K):
         assert g.selected == o.selected and g.selected_tokens == o.selected_tokens
 
 
+def test_async_forecast_put_and_drop(gpu):
+    """put_forecasts(validate_now=False) (the shim's pbkv_forecast_put_async):
+    the validation error surfaces at the next call that reads the status word,
+    with the reference's message; a drop is stream-ordered (no sync) and the
+    next decision sees the forecast missing."""
+    from paper_2605_06472_b200.ops import OpStream
+
+    t = HostTree()
+    t.apply_ops(OpStream().insert([1, 2], 7, 0).insert([3], 8, 1).words)
+    pol = Policy(num_agents=2, k=1, gamma=0.7)
+    pol.mirror(t)
+    pol.put_forecasts([7, 8], np.array([[[0.5, 0.3, 0.2]], [[0.5, 0.3, 0.2]]]))
+    ok = pol.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
+    pol.put_forecasts([7], np.array([[[1.1, -0.1, 0.0]]]), validate_now=False)  # returns without the check
+    with pytest.raises(ValidationError, match="negative forecast probability"):
+        pol.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
+    pol.put_forecasts([7], np.array([[[0.5, 0.3, 0.2]]]), validate_now=False)
+    again = pol.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
+    assert (again.victims, again.freed) == (ok.victims, ok.freed)
+    pol.drop_forecasts([8])
+    with pytest.raises(ValidationError, match="missing forecast for active workflow 8"):
+        pol.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
+
+
 def test_errors_match_reference(gpu):
     t = HostTree()
     from paper_2605_06472_b200.ops import OpStream
