@@ -388,6 +388,7 @@ struct SelArgs {
     SelState* h_ss;
     int* h_vict;                // null: the victims stay on the device
     long long h_cap;
+    int no_refine;              // (tests) take the device-wide-sort fallback instead of refining
     std::uint8_t* flags_w;      // the deferral is cleared in place
     // oversized-bucket refinement (refine_buckets)
     unsigned int rf_cap;        // bucket descriptors per round parity
@@ -2345,7 +2346,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     const bool refined = max_bucket > static_cast<unsigned int>(kRankCap);
     if (refined) {
         if (tid == 0) ss->max_bucket = static_cast<int>(max_bucket);
-        if (!refine_buckets(a, sm, grid, nts, take_all, nS)) {
+        if (a.no_refine || !refine_buckets(a, sm, grid, nts, take_all, nS)) {
             if (tid == 0) ss->host_sort = 1;  // device-wide sort driven from the host (> 16 M nodes)
             return;
         }
@@ -2750,6 +2751,10 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.rep_out = reinterpret_cast<HeavyReport*>(c.hreport_h.p);
         a.approx = c.happrox.p;
         a.approx_out = reinterpret_cast<double*>(c.hreport_h.p + bytes);
+    }
+    {  // (tests: PBKV_SELECT_NO_REFINE=1 exercises the device-wide-sort fallback)
+        const char* e = std::getenv("PBKV_SELECT_NO_REFINE");
+        a.no_refine = e && e[0] == '1' ? 1 : 0;
     }
     a.h_st = c.hstatus.p;
     a.h_ss = hs;

@@ -88,3 +88,31 @@ def test_sharded_large_cuts_equal_single(gpu, seed):
         assert (got[0].tolist(), got[1], got[2]) == (want.victims, want.freed, want.shortfall), frac
         o = Oracle.select(s2, POLICY_HE, needed, locked)
         assert (o.victims, o.freed, o.shortfall) == (want.victims, want.freed, want.shortfall), frac
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_device_sort_fallback_equals_oracle(gpu, seed, monkeypatch):
+    """The last resort of the full radix path (a refinement round with more
+    buckets than a CTA caches: the CUB device sort of S driven from the
+    host), forced: same victims as the oracle, take-all included."""
+    monkeypatch.setenv("PBKV_SELECT_NO_REFINE", "1")
+    rng = np.random.default_rng(7800 + seed)
+    t = HostTree()
+    t.synth(n_nodes=50_000, n_workflows=512, agents=8, retired_frac=0.6, seed=int(rng.integers(1 << 30)))
+    soa = t.export()
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, 4, 9)
+    pol = Policy(num_agents=8, k=4, gamma=0.7)
+    pol.mirror(t)
+    pol.put_forecasts(wf, P)
+    s = soa.copy()
+    s.score[:] = Oracle.score_nodes(soa, wf, P, 4, 0.7)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    locked = WL.random_locked(soa, rng, 0.02)
+    lib0 = pol.launches()[1]
+    for frac in (0.7, 3.0):
+        needed = max(1, int(frac * used))
+        o = Oracle.select(s, POLICY_HE, needed, locked)
+        g = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+        assert (g.victims, g.freed, g.shortfall) == (o.victims, o.freed, o.shortfall), frac
+    assert pol.launches()[1] > lib0, "the fallback did not run"
