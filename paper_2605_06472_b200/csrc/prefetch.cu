@@ -706,6 +706,12 @@ __global__ void __launch_bounds__(kPT, 2) prefetch_plan_kernel(PfArgs a) {
         if (t < 2 && iv < nn) a.h_val[iv] = dec_value(__ldcg(&a.s_hi[iv]));
         if (is < nf) a.h_sel[is] = __ldcg(&a.s_id[is]);
     }
+    __syncthreads();
+    if (threadIdx.x == 32) {  // (diagnostics: the store phase's end, latest CTA)
+        unsigned long long tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        atomicMax(&a.ps->ts[6], tnow);
+    }
 }
 
 int plan_grid(Context& c, std::int64_t n_nodes) {
@@ -807,9 +813,10 @@ void run_prefetch_plan(Context& c, long long budget, PrefetchOut* out) {
         PfState h{};
         PBKV_CUDA(cudaMemcpy(&h, a.ps, sizeof h, cudaMemcpyDeviceToHost));
         std::fprintf(stderr, "[pbkv plan] grid=%d n_cand=%llu n_big=%u f=%llu min_len=%d us: cand %.1f hist %.1f "
-                     "scatter %.1f sort %.1f tail %.1f\n", plan_grid(c, c.n), h.n_cand, h.n_big, h.f, h.min_len,
+                     "scatter %.1f sort %.1f tail %.1f store %.1f\n", plan_grid(c, c.n), h.n_cand, h.n_big, h.f, h.min_len,
                      (h.ts[1] - h.ts[0]) * 1e-3, (h.ts[2] - h.ts[1]) * 1e-3, (h.ts[3] - h.ts[2]) * 1e-3,
-                     (h.ts[4] - h.ts[3]) * 1e-3, (h.ts[5] - h.ts[4]) * 1e-3);
+                     (h.ts[4] - h.ts[3]) * 1e-3, (h.ts[5] - h.ts[4]) * 1e-3,
+                     h.ts[6] > h.ts[4] ? (h.ts[6] - h.ts[4]) * 1e-3 : 0.0);
     }
     out->ctr = a.h_ctr;
     out->cand = a.h_cand;

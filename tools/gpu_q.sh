@@ -1,2 +1,2 @@
 cd /root/repo
-timeout 900 python -m pytest tests/test_refine.py -x -q 2>&1 | tail -3
+timeout 300 python tools/plan_probe.py c3 2>&1 | grep "pbkv plan" | tail -3
