@@ -1131,12 +1131,13 @@ SelectCounts select_core(Context& c, int policy, int score_mode, std::int64_t ne
     record(c, 0);
     const bool recompute = score_mode == PBKV_SCORE_RECOMPUTE && policy == PBKV_POLICY_HE;
     const bool defer = recompute && c.defer_heavy && c.n_heavy > 0 && c.spine.empty();
-    launch_decision_prologue(c, defer);  // status reset (+ the deferral)
     if (defer) {
-        launch_score_decision(c, policy);
+        launch_score_decision(c, policy);  // (its prologue: status reset + the deferral)
     } else if (recompute) {
+        launch_decision_prologue(c, false, c.stream);  // status reset
         launch_score_all(c, c.score_rc.p, true, policy, false);
     } else {
+        launch_decision_prologue(c, false, c.stream);
         launch_keys_cached(c, policy);
     }
     record(c, 1);

@@ -384,7 +384,7 @@ void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64
 void launch_keys_cached(Context& c, int policy);
 void launch_score_decision(Context& c, int policy);  // Eq. 2 + keys with heavy chains deferred
 void launch_set_deferred(Context& c, bool on, const int* skip_if = nullptr);
-void launch_decision_prologue(Context& c, bool defer);
+void launch_decision_prologue(Context& c, bool defer, cudaStream_t st);
 void raise_status(Context& c, const DevStatus& s);
 struct HeavyReport {  // one per heavy node, then one tail record (select.cu)
     unsigned long long w0, w1;  // key of eff(h) over its non-deferred descendants / of the tail head

@@ -803,12 +803,12 @@ void launch_set_deferred(Context& c, bool on, const int* skip_if) {
     ++c.launches;
 }
 
-void launch_decision_prologue(Context& c, bool defer) {
+void launch_decision_prologue(Context& c, bool defer, cudaStream_t st) {
     const int nh = defer ? static_cast<int>(c.n_heavy) : 0;
     const int nm = defer ? static_cast<int>(c.n_heavy + c.n_medium) : 0;
     if (defer) c.happrox.reserve(static_cast<std::size_t>(2 * c.n_heavy) + 2);
     const int n = std::max(1, std::max(nh, nm));
-    decision_prologue_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.status_pending ? nullptr : c.status.p, c.flags.p,
+    decision_prologue_kernel<<<(n + 255) / 256, 256, 0, st>>>(c.status_pending ? nullptr : c.status.p, c.flags.p,
                                                                       c.keys.p, c.heavy.p, nh, defer ? 1 : 0, c.hmiss.p,
                                                                       nm, c.happrox.p);
     PBKV_CUDA(cudaGetLastError());
@@ -825,14 +825,22 @@ void launch_score_decision(Context& c, int policy) {
     const bool side = c.n_heavy + c.n_medium > 0;
     // the light pass is enqueued first (every API call before it delays its
     // start); the side stream forks off the same point, has the higher
-    // priority for SM slots, and joins after it
-    if (side) PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    // priority for SM slots, and joins after it.  The decision's prologue
+    // (status reset, the deferral marks, hmiss / approx zeroed) runs at the
+    // head of the side stream: the light pass reads none of it (no status
+    // writes at report_missing 0, no keys of heavy nodes), the side stream's
+    // kernels and the selection (after the join) read all of it.
+    if (side) {
+        PBKV_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    } else {
+        launch_decision_prologue(c, true, c.stream);
+    }
     launch_light<true>(c, s, ka, 0);
     PBKV_CUDA(cudaGetLastError());
     ++c.launches;
     if (side) {
-        // hmiss / approx were zeroed and the deferral set by decision_prologue_kernel
         PBKV_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        launch_decision_prologue(c, true, c.side);
         heavy_products_kernel<<<grid_cap(c.n_hent * c.K, 256), 256, 0, c.side>>>(
             s, c.hent.p, c.hent_node.p, c.n_hent, c.hxs.p, c.hmiss.p, c.happrox.p, static_cast<int>(c.n_heavy));
         PBKV_CUDA(cudaGetLastError());
