@@ -354,6 +354,12 @@ int pbkv_shard_spine_products(pbkv_ctx* ctx, double* out_dev, int64_t* counts);
 /* Exact serial FP64 chains: out[b] = RN-sum of x_dev[off[b], off[b+1]) in
  * order (off, out on the host). */
 int pbkv_chain_sum(pbkv_ctx* ctx, const double* x_dev, const int64_t* off, int n_seg, double* out);
+/* Any-order sums of x_dev over pieces: out[2j] = sum, out[2j+1] = sum of
+ * magnitudes over the pieces [pieces[2q], pieces[2q+1]) for q in
+ * [out_off[j], out_off[j+1]) (host arrays; one synchronisation).  The
+ * sharded decision's interval test of the spine scores. */
+int pbkv_interval_sums(pbkv_ctx* ctx, const double* x_dev, const int64_t* pieces, const int64_t* out_off, int n_out,
+                       double* out);
 /* Merge of exchanged record runs (each sorted) and the cut at `needed`:
  * victims_dev receives global ids in eviction order; result_dev = int64[3]
  * {n_victims, freed, shortfall}. */

@@ -230,6 +230,7 @@ def lib() -> C.CDLL:
         "pbkv_ctx_wait_stream": ([vp, vp], C.c_int),
         "pbkv_prefetch_round": ([vp, _i32p, C.c_int64, C.c_int64, _i32p, _i64p, _i32p, C.c_int64, _i64p], C.c_int),
         "pbkv_plan_fetch": ([vp, _i32p, _f64p, C.c_int64, _i32p, C.c_int64], C.c_int),
+        "pbkv_interval_sums": ([vp, vp, _i64p, _i64p, C.c_int, _f64p], C.c_int),
         "pbkv_predictor_load": ([vp, C.POINTER(PredictorCfg), C.POINTER(PredictorWeights)], C.c_int),
         "pbkv_predict": ([vp, _i64p, C.c_int64, _i64p, _i32p, vp, C.c_int, _f64p], C.c_int),
         "pbkv_tree_create": ([C.POINTER(vp), C.c_int64, C.c_int64], C.c_int),

@@ -1867,6 +1867,35 @@ int pbkv_chain_sum(pbkv_ctx* c, const double* x_dev, const int64_t* off, int n_s
     });
 }
 
+int pbkv_interval_sums(pbkv_ctx* c, const double* x_dev, const int64_t* pieces, const int64_t* out_off, int n_out,
+                       double* out) {
+    return api(c, [&] {
+        need(c && pieces && out_off && out && n_out >= 0, "null argument");
+        if (n_out == 0) return;
+        need(out_off[0] == 0, "out_off must start at 0");
+        const int64_t np = out_off[n_out];
+        for (int j = 0; j < n_out; ++j) need(out_off[j + 1] >= out_off[j], "out_off must not decrease");
+        for (int64_t q = 0; q < np; ++q) need(pieces[2 * q] >= 0 && pieces[2 * q + 1] >= pieces[2 * q], "bad piece");
+        need(np == 0 || x_dev, "null array");
+        set_device(*c);
+        // pieces and offsets through one pinned staging blob; sums straight into pinned memory
+        const std::size_t b_p = static_cast<std::size_t>(2 * np) * sizeof(long long);
+        const std::size_t b_o = (static_cast<std::size_t>(n_out) + 1) * sizeof(long long);
+        const std::size_t b_r = static_cast<std::size_t>(2 * n_out) * sizeof(double);
+        c->his.reserve(b_p + b_o + b_r);
+        c->dis.reserve(b_p + b_o + 8);
+        unsigned char* h = c->his.p;
+        if (b_p) std::memcpy(h, pieces, b_p);
+        std::memcpy(h + b_p, out_off, b_o);
+        PBKV_CUDA(cudaMemcpyAsync(c->dis.p, h, b_p + b_o, cudaMemcpyHostToDevice, c->stream));
+        double* res = reinterpret_cast<double*>(h + b_p + b_o);
+        launch_interval_sums(*c, x_dev, reinterpret_cast<const long long*>(c->dis.p),
+                             reinterpret_cast<const long long*>(c->dis.p + b_p), n_out, res);
+        PBKV_CUDA(cudaStreamSynchronize(c->stream));
+        std::memcpy(out, res, b_r);
+    });
+}
+
 int pbkv_merge_cut(pbkv_ctx* c, const pbkv_cand* runs_dev, const int64_t* run_start, const int64_t* run_len,
                    int n_runs, int64_t needed, int32_t* victims_dev, int64_t* result_dev) {
     return api(c, [&] {

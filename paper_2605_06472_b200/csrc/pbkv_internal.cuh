@@ -301,6 +301,8 @@ struct Context {
     DevBuf<unsigned char> samp;
     DevBuf<int> low;
     DevBuf<long long> cut_partial;  // sharded merge: per-CTA token sums
+    PinBuf<unsigned char> his;        // pbkv_interval_sums: pinned pieces, offsets and sums
+    DevBuf<unsigned char> dis;
     DevBuf<unsigned long long> gbar;  // the persistent selection kernel's grid barrier
     int gbar_grid = 0;                // the grid size the counter is a multiple of (0: zero it first)
     DevBuf<unsigned int> small_u32;
@@ -380,6 +382,8 @@ void launch_forecast_prepare(Context& c, const double* stage, const long long* s
 void launch_score_all(Context& c, double* out, bool write_keys, int policy, bool report_missing);
 void launch_score_ids(Context& c, const int* ids_dev, const int* h_ids, std::int64_t n, double* out, bool value_only);
 void launch_chain_sum(Context& c, const double* x, const long long* off, int n_seg, double* out);
+void launch_interval_sums(Context& c, const double* x, const long long* pieces, const long long* out_off, int n_out,
+                          double* out_host);
 void launch_gather_f64(Context& c, const double* src, const int* ids, std::int64_t n, double* dst);
 void launch_keys_cached(Context& c, int policy);
 void launch_score_decision(Context& c, int policy);  // Eq. 2 + keys with heavy chains deferred

@@ -308,4 +308,52 @@ void shard_merge_cut(Context& c, const pbkv_cand* src, const long long* run_star
     c.launches += 2;
 }
 
+
+// ---- interval sums of the exchanged spine products (shard.py fast path) -------------
+// Output j: the sum and the sum of magnitudes of x over its pieces
+// [pieces[2q], pieces[2q+1]) for q in [out_off[j], out_off[j+1]), any order
+// within a piece (block reduction), pieces in order: deterministic.  One CTA
+// per output; the results go straight to pinned host memory.
+namespace {
+constexpr int kIsT = 256;
+__global__ void __launch_bounds__(kIsT) interval_sums_kernel(const double* x, const long long* pieces,
+                                                            const long long* out_off, double* out) {
+    __shared__ double red[2][kIsT / 32];
+    const int j = blockIdx.x;
+    double s = 0.0, sa = 0.0;
+    for (long long q = out_off[j]; q < out_off[j + 1]; ++q) {
+        for (long long i = pieces[2 * q] + threadIdx.x; i < pieces[2 * q + 1]; i += kIsT) {
+            const double v = __ldg(x + i);
+            s += v;
+            sa += fabs(v);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = s;
+        red[1][threadIdx.x >> 5] = sa;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, ta = 0.0;
+        for (int w = 0; w < kIsT / 32; ++w) {
+            t += red[0][w];
+            ta += red[1][w];
+        }
+        out[2 * j] = t;
+        out[2 * j + 1] = ta;
+    }
+}
+}  // namespace
+
+void launch_interval_sums(Context& c, const double* x, const long long* pieces, const long long* out_off, int n_out,
+                          double* out_host) {
+    interval_sums_kernel<<<n_out, kIsT, 0, c.stream>>>(x, pieces, out_off, out_host);
+    PBKV_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
 }  // namespace pbkv

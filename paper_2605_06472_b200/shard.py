@@ -390,6 +390,18 @@ class ShardedPolicy:
                                               ptr(off, C.c_int64), int(off.size - 1), ptr(out, C.c_double)))
         return out[: offsets.size - 1]
 
+    def interval_sums(self, x_ptr: int, pieces: np.ndarray, out_off: np.ndarray) -> np.ndarray:
+        """pbkv_interval_sums: [n_out, 2] (sum, sum of magnitudes) of the
+        double array at device address x_ptr over each output's pieces."""
+        pc = np.ascontiguousarray(pieces, dtype=np.int64).reshape(-1)
+        oo = np.ascontiguousarray(out_off, dtype=np.int64)
+        n_out = int(oo.size - 1)
+        out = np.zeros(max(2 * n_out, 1), dtype=np.float64)
+        self.order_after_torch()
+        self.pol._c(_abi.lib().pbkv_interval_sums(self.pol.handle, C.c_void_p(x_ptr), ptr(pc if pc.size else np.zeros(2, np.int64), C.c_int64),
+                                                  ptr(oo, C.c_int64), n_out, ptr(out, C.c_double)))
+        return out[: 2 * n_out].reshape(n_out, 2)
+
     def merge_cut(self, runs_dev, starts: list[int], lens: list[int], needed: int):
         import torch
 
@@ -563,29 +575,29 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
     if not he_rc:
         v, freed, sf = cut_with(spine_records(sp, rep_all, sp.score, policy, locked_set))
         return v.cpu().numpy(), freed, sf
-    # spine scores over every rank's products, rank (= WorkflowId) order
-    prods = hdr[:, 8 + nrep + 8 * sp.n:].reshape(world, -1).view(torch.float64)
-    pieces, offs = [], [0]
+    # spine scores over every rank's products, rank (= WorkflowId) order:
+    # spine node j's products are rank r's piece [b_rj, b_rj + cnt_all[r, j])
+    # of its header row (in doubles from the header's base address)
+    row = head.numel()
+    pstart = 8 + nrep + 8 * sp.n
+    assert row % 8 == 0 and pstart % 8 == 0
+    bj = np.concatenate([np.zeros((world, 1), np.int64), np.cumsum(cnt_all, axis=1)], axis=1) if sp.n else None
+    pieces = np.array([[(r * row + pstart) // 8 + int(bj[r, j]), (r * row + pstart) // 8 + int(bj[r, j + 1])]
+                       for j in range(sp.n) for r in range(world)], dtype=np.int64).reshape(-1, 2)
+    offs = [0]
     for j in range(sp.n):
-        for r in range(world):
-            b = int(cnt_all[r, :j].sum())
-            pieces.append(prods[r, b: b + int(cnt_all[r, j])])
         offs.append(offs[-1] + int(cnt_all[:, j].sum()))
-    x = torch.cat(pieces) if pieces else torch.zeros(1, dtype=torch.float64, device=dev)
     mark("spine products gathered")
     # fast path: the exact serial chain E and any-order sum A
     # both lie within L * ulp(sum|x|) / 2 of the real sum.  If the spine
     # records are after every candidate record for both ends of the interval,
     # and the cut ends inside the candidates, the exact chains are not needed.
-    # any-order sums per spine node on the device, one small readback
-    A = np.zeros(sp.n)
-    Sa = np.zeros(sp.n)
-    segs = [j for j in range(sp.n) if offs[j + 1] > offs[j]]
-    if segs:
-        sums = torch.stack([x[offs[j]: offs[j + 1]].sum() for j in segs] +
-                           [x[offs[j]: offs[j + 1]].abs().sum() for j in segs]).cpu().numpy()
-        A[segs] = sums[: len(segs)]
-        Sa[segs] = sums[len(segs):]
+    # any-order sums per spine node on the device (pbkv_interval_sums), one
+    # synchronisation
+    sums = rp.interval_sums(hdr.data_ptr(), pieces, np.arange(0, world * sp.n + 1, world, dtype=np.int64)) \
+        if sp.n else np.zeros((0, 2))
+    A = sums[:, 0].copy()
+    Sa = sums[:, 1].copy()
     mark("spine interval sums")
     L = np.diff(offs).astype(np.float64)
     B = np.array([2.0 * L[j] * np.ldexp(1.0, np.frexp(Sa[j])[1] - 53) if Sa[j] > 0 else 0.0 for j in range(sp.n)])
@@ -613,6 +625,11 @@ def _global_select_dist(rp: ShardedPolicy, policy: int, score_mode: int, needed:
                     PROFILE.setdefault(what, []).append(1e3 * (t - prev))
                     prev = t
             return out, freed, sf
-    scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))  # exact chains
+    # exact chains (the interval could not place the spine): the products in
+    # rank order, then one serial chain per spine node
+    prods = hdr[:, pstart:].reshape(world, -1).view(torch.float64)
+    parts = [prods[r, int(bj[r, j]): int(bj[r, j + 1])] for j in range(sp.n) for r in range(world)]
+    x = torch.cat(parts) if parts else torch.zeros(1, dtype=torch.float64, device=dev)
+    scores = rp.chain_sums(x, np.array(offs, dtype=np.int64))
     v, freed, sf = cut_with(spine_records(sp, rep_all, scores, policy, locked_set))
     return v.cpu().numpy(), freed, sf

@@ -270,3 +270,47 @@ def test_dist_exchange_two_ranks_equals_single(gpu):
     want = res[0][2]
     for rank, out, _ in res:
         assert [tuple(o) for o in out] == [tuple(w) for w in want], f"rank {rank} differs from single"
+
+
+@pytest.mark.gpu
+def test_interval_sums_bound(gpu):
+    """pbkv_interval_sums (the sharded fast path's any-order spine sums):
+    every output within its interval bound L * ulp(sum|x|) of the exact sum,
+    over pieces scattered in the array (empty pieces and outputs included)."""
+    import math
+
+    import torch
+
+    from paper_2605_06472_b200 import shard as SH
+
+    from paper_2605_06472_b200.api import Policy
+
+    rng = np.random.default_rng(3)
+    x = np.r_[rng.random(50000) * 2.0 ** rng.integers(-20, 4, 50000), rng.random(3000) * 1e-200]
+    pol = Policy(num_agents=4, k=3)
+
+    class _P:
+        pass
+
+    h = _P()
+    h.pol = pol
+    h.dev = torch.device("cuda", 0)
+    h.order_after_torch = lambda: SH.ShardedPolicy.order_after_torch(h)
+    xt = torch.from_numpy(x).cuda()
+    n_out = 7
+    pieces, out_off = [], [0]
+    for j in range(n_out):
+        for _ in range(int(rng.integers(0, 4))):
+            a = int(rng.integers(0, x.size))
+            b = min(x.size, a + int(rng.integers(0, 20000)))
+            pieces.append((a, b))
+        out_off.append(len(pieces))
+    got = SH.ShardedPolicy.interval_sums(h, xt.data_ptr(), np.array(pieces, dtype=np.int64).reshape(-1, 2),
+                                         np.array(out_off, dtype=np.int64))
+    for j in range(n_out):
+        vals = np.concatenate([x[a:b] for a, b in pieces[out_off[j]:out_off[j + 1]]] or [np.zeros(0)])
+        exact, mag = math.fsum(vals.tolist()), math.fsum(np.abs(vals).tolist())
+        L = max(vals.size, 1)
+        bound = 2.0 * L * (np.spacing(mag) if mag > 0 else 0.0)
+        assert abs(got[j, 0] - exact) <= bound, (j, got[j, 0], exact, bound)
+        assert abs(got[j, 1] - mag) <= bound, (j, got[j, 1], mag, bound)

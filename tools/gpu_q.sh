@@ -1,5 +1,3 @@
 cd /root/repo
-for v in base var_so/libpbkv_kg1_m4.so var_so/libpbkv_kg1_m5.so var_so/libpbkv_kg2_m5.so; do
-  if [ "$v" = base ]; then unset PBKV_LIB; else export PBKV_LIB=$PWD/$v; fi
-  timeout 300 python bench.py --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep > gpurun_out/bv.log 2>&1; echo "$v"; python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | head -1
-done
+timeout 900 python -m pytest tests/test_shard.py tests/test_full_size.py -x -q -k "shard or interval or dist or c4" 2>&1 | tail -2
+grep -E "Error|assert|FAILED|^E " /dev/null
