@@ -1,2 +1,11 @@
 cd /root/repo
-PBKV_PROFILE_SHARD=1 timeout 600 python bench.py --sharded --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bsh.log 2>&1; tail -1 gpurun_out/bsh.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], json.dumps(d.get('stage_host_ms'), indent=0))"
+for i in 1 2; do
+timeout 900 python bench.py --no-sweep --no-prefetch --no-pipeline --no-cpu-baseline > gpurun_out/bd.log 2>&1
+python -c "
+import json
+d=json.loads(open('gpurun_out/bd.log').read().strip().splitlines()[-1]); print('run', $i, d['ms_per_step'], d['p50_decision_ms'], d['stage_ms']['total'])"
+done
+timeout 900 python bench.py > gpurun_out/bd.log 2>&1
+python -c "
+import json
+d=json.loads(open('gpurun_out/bd.log').read().strip().splitlines()[-1]); print('default', d['ms_per_step'], d['p50_decision_ms'], d['stage_ms']['total'])"
