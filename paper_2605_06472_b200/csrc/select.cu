@@ -21,7 +21,8 @@
 //   every bucket ranked (warp sorts <= 32, rank-counting tasks <= 256) ->
 //   chain starts (scan of chain sizes) -> chain scatter -> cut.
 // No host round trip.  The CUB device sort below the kernel is the last
-// resort of a refinement round with more than kRfSh buckets (> 2 M heads).
+// resort of a refinement round whose per-CTA slices would span more than
+// kRfLoc buckets (tens of millions of selected heads).
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -394,7 +395,7 @@ struct SelArgs {
     unsigned int rf_cap;        // bucket descriptors per round parity
     unsigned int* rf_off;       // [2][rf_cap] bucket start in S
     unsigned int* rf_cnt;       // [2][rf_cap] bucket size
-    unsigned int* rf_hist;      // [2][rf_cap][kBins] digit counts, then placement cursors
+    unsigned int* rf_hist;      // [kRfSh][kBins] digit counts, then placement cursors (one window)
     unsigned long long* rf_orand;  // [2][rf_cap][6] OR / AND of the key words
     unsigned int* rf_small;     // [2 * n] (offset, count) of pieces with <= 32 heads
     ulonglong2* rf_tmpk;        // [n] keys in flight (the scatter's staging)
@@ -1877,7 +1878,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
 // round has at most n / (kRankCap + 1) buckets.
 constexpr int kRfPieceLog = 7;                                 // digit width aimed at ~128-head pieces
 constexpr int kRfSh = 8192;                                   // descriptors cached per CTA (prefix, offset)
-constexpr int kRfLoc = 64;                                     // buckets one CTA's slice may span
+constexpr int kRfLoc = 256;                                    // buckets one CTA's slice may span
 static_assert(2 * kRfSh * 4 + kRfLoc * 13 * 4 <= static_cast<int>(sizeof(unsigned long long) * 2 * kBucketCap +
                                                                   sizeof(int) * kBucketCap),
               "refinement scratch exceeds the sort arrays");
@@ -1905,9 +1906,10 @@ __device__ __forceinline__ void rf_init_bucket(const SelArgs& a, int par, unsign
 }
 
 // Splits every bucket of S above kRankCap (all CTAs).  take_all: S is the
-// unsorted head list (no keys listed yet), one bucket.  Returns false (grid-
-// uniform) when a round has more buckets than a CTA caches: the caller falls
-// back to the device-wide sort.
+// unsorted head list (no keys listed yet), one bucket.  A round with more
+// buckets than a CTA caches (kRfSh) runs window by window.  Returns false
+// (grid-uniform) only when a CTA's slice would span more than kRfLoc
+// buckets: the caller falls back to the device-wide sort.
 __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar& grid, int& nts, bool take_all,
                                unsigned long long nS) {
     SelState* ss = a.ss;
@@ -1950,12 +1952,16 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
         const int nx = par ^ 1;
         if (threadIdx.x == 0) sm.bc[0] = __ldcg(&ss->n_rf[par]);
         __syncthreads();
-        const unsigned int n = static_cast<unsigned int>(sm.bc[0]);
+        const unsigned int nr = static_cast<unsigned int>(sm.bc[0]);
         __syncthreads();
-        if (n == 0) break;
-        if (n > static_cast<unsigned int>(kRfSh) || n > a.rf_cap) return false;
-        const std::size_t rb = static_cast<std::size_t>(par) * a.rf_cap;
-        // the round's descriptors and their prefix, per CTA
+        if (nr == 0) break;
+        if (nr > a.rf_cap) return false;
+        // the round's buckets, a window of at most kRfSh at a time (the
+        // descriptors a CTA caches; the histogram rows are per window)
+        for (unsigned int jb = 0; jb < nr; jb += kRfSh) {
+        const unsigned int n = min(static_cast<unsigned int>(kRfSh), nr - jb);
+        const std::size_t rb = static_cast<std::size_t>(par) * a.rf_cap + jb;  // the window's descriptors
+        // the window's descriptors and their prefix, per CTA
         unsigned int total = 0;
         for (unsigned int t0 = 0; t0 < n; t0 += blockDim.x) {
             const unsigned int j = t0 + threadIdx.x;
@@ -1969,14 +1975,14 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
             total += tile;
         }
         __syncthreads();
-        if (threadIdx.x == 0 && blockIdx.x == 0) {
+        if (threadIdx.x == 0 && blockIdx.x == 0 && jb == 0) {
             ss->n_rf[nx] = 0;
             ss->rf_rounds += 1;
         }
-        // this round's histogram rows, zeroed (read after the next barrier)
+        // the window's histogram rows, zeroed (read after the next barrier)
         for (unsigned int j = blockIdx.x; j < n; j += gridDim.x)
             for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x)
-                a.rf_hist[(rb + j) * kBins + d] = 0u;
+                a.rf_hist[static_cast<std::size_t>(j) * kBins + d] = 0u;
         // this CTA's contiguous slice of the round's heads and the buckets it spans
         const unsigned int chunk = (total + gridDim.x - 1) / gridDim.x;
         if (chunk / (kRankCap + 1) + 2 > static_cast<unsigned int>(kRfLoc)) return false;
@@ -2058,19 +2064,19 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
             const unsigned peers = __match_any_sync(0xffffffffu, key);
             if (in && lane == __ffs(peers) - 1) {
                 if (single) atomicAdd(&hloc[d], static_cast<unsigned int>(__popc(peers)));
-                else atomicAdd(&a.rf_hist[(rb + j) * kBins + d], static_cast<unsigned int>(__popc(peers)));
+                else atomicAdd(&a.rf_hist[static_cast<std::size_t>(j) * kBins + d], static_cast<unsigned int>(__popc(peers)));
             }
         }
         __syncthreads();
         if (single)
             for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x)
-                if (hloc[d]) atomicAdd(&a.rf_hist[(rb + j0) * kBins + d], hloc[d]);
+                if (hloc[d]) atomicAdd(&a.rf_hist[static_cast<std::size_t>(j0) * kBins + d], hloc[d]);
         grid.sync();
         stamp(ss, nts);
         // (C) piece offsets (the histogram rows become placement cursors) and
         // the pieces' lists: warp sorts, rank sorts, next round
         for (unsigned int j = blockIdx.x; j < n; j += gridDim.x) {
-            unsigned int* row = a.rf_hist + (rb + j) * kBins;
+            unsigned int* row = a.rf_hist + static_cast<std::size_t>(j) * kBins;
             constexpr int kPer = kBins / kPThreads;
             unsigned int c[kPer], s4 = 0;
 #pragma unroll
@@ -2104,7 +2110,7 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
         // one-bucket slice reserves its ranges with one atomic per digit
         if (single) {
             for (unsigned int d = threadIdx.x; d < static_cast<unsigned int>(kBins); d += blockDim.x)
-                if (hloc[d]) hloc[d] = atomicAdd(&a.rf_hist[(rb + j0) * kBins + d], hloc[d]);
+                if (hloc[d]) hloc[d] = atomicAdd(&a.rf_hist[static_cast<std::size_t>(j0) * kBins + d], hloc[d]);
             __syncthreads();
         }
         for (unsigned int vb = v0; vb < v1; vb += blockDim.x) {
@@ -2128,7 +2134,7 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
             unsigned int base = 0;
             if (in && lane == leader)
                 base = single ? atomicAdd(&hloc[d], static_cast<unsigned int>(__popc(peers)))
-                              : atomicAdd(&a.rf_hist[(rb + j) * kBins + d], static_cast<unsigned int>(__popc(peers)));
+                              : atomicAdd(&a.rf_hist[static_cast<std::size_t>(j) * kBins + d], static_cast<unsigned int>(__popc(peers)));
             base = __shfl_sync(peers, base, leader);
             if (in) {
                 const unsigned int pos = base + __popc(peers & ((1u << lane) - 1u));
@@ -2152,6 +2158,7 @@ __device__ bool refine_buckets(const SelArgs& a, PersistSmem& sm, const GridBar&
         }
         grid.sync();
         stamp(ss, nts);
+        }  // window
     }
     return true;
 }
@@ -2725,9 +2732,10 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
         a.sm_cpre = c.small_u64.p + 3 * kBins;
     }
     {  // oversized-bucket refinement: a round has at most n / (kRankCap + 1) buckets
-        // (a round above kRfSh buckets takes the fallback: no larger tables)
-        const std::size_t cap = std::min<std::size_t>(static_cast<std::size_t>(c.n) / (kRankCap + 1) + 2, kRfSh);
-        c.rf_u32.reserve(4 * cap + 2 * cap * kBins);
+        // (descriptors for every bucket of a round; histogram rows for one
+        // window of kRfSh buckets)
+        const std::size_t cap = static_cast<std::size_t>(c.n) / (kRankCap + 1) + 2;
+        c.rf_u32.reserve(4 * cap + static_cast<std::size_t>(kRfSh) * kBins);
         c.rf_orand.reserve(2 * cap * 6);
         c.rf_small.reserve(2 * static_cast<std::size_t>(c.n) + 2);
         c.rf_tmpk.reserve(static_cast<std::size_t>(c.n) + 1);

@@ -142,3 +142,30 @@ def test_c4_sharded_8_ways_equals_single_and_oracle(gpu):
     s2.score[:] = Oracle.score_nodes(soa, wf, P, 8, 0.7)
     o = Oracle.select(s2, POLICY_HE, needed, locked)
     assert (o.victims, o.freed, o.shortfall) == (want.victims, want.freed, want.shortfall)
+
+
+def test_c4_large_cut_equals_oracle(gpu):
+    """BASELINE config 4 on one context at 90% of the device tokens: the
+    refinement's rounds exceed one window of bucket descriptors (select.cu
+    refine_buckets), no library kernel runs, and the victims equal the
+    oracle's."""
+    t = HostTree()
+    t.synth(n_nodes=8_000_000, n_workflows=16384, agents=16, seed=4)
+    soa = t.export()
+    rng = np.random.default_rng(4)
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, 8, 17)
+    locked = WL.pinned_paths(soa, rng, 0.01)
+    pol = Policy(num_agents=16, k=8, gamma=0.7)
+    pol.mirror(t)
+    pol.put_forecasts(wf, P)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    needed = int(0.9 * used)
+    lib0 = pol.launches()[1]
+    g = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+    assert pol.launches()[1] == lib0, "library kernels on the selection path"
+    s2 = soa.copy()
+    s2.score[:] = Oracle.score_nodes(soa, wf, P, 8, 0.7)
+    o = Oracle.select(s2, POLICY_HE, needed, locked)
+    assert (g.freed, g.shortfall) == (o.freed, o.shortfall)
+    assert np.array_equal(g.victim_ids, np.asarray(o.victims, dtype=np.int32))
