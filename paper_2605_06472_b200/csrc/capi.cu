@@ -281,6 +281,24 @@ void erase_sorted(std::vector<int>& v, int x) {
 // Host arrays bound for device buffers, copied through one pinned staging
 // buffer (c.hclass) with no host synchronisation: the next batch waits for
 // ev_class before it rewrites the staging.
+// byte ranges of one device blob copied into up to eight tables (one CTA each;
+// 16-byte units: blob offsets are 16-byte aligned, table buffers 256-byte)
+struct ScatterDesc {
+    int n;
+    unsigned char* dst[8];
+    std::size_t off[8];
+    std::size_t bytes[8];
+};
+__global__ void __launch_bounds__(256) scatter_blob_kernel(const unsigned char* blob, ScatterDesc d) {
+    const int i = blockIdx.x;
+    const unsigned char* src = blob + d.off[i];
+    unsigned char* dst = d.dst[i];
+    const std::size_t n16 = d.bytes[i] >> 4;
+    for (std::size_t q = threadIdx.x; q < n16; q += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(src)[q];
+    for (std::size_t q = (n16 << 4) + threadIdx.x; q < d.bytes[i]; q += blockDim.x) dst[q] = src[q];
+}
+
 struct ClassStager {
     Context& c;
     struct Item {
@@ -298,6 +316,8 @@ struct ClassStager {
         items.push_back(Item{d.p, v.data(), v.size() * sizeof(T)});
         total += (v.size() * sizeof(T) + 15) & ~std::size_t(15);
     }
+    // one pinned blob, one H2D copy, one kernel scattering it into the
+    // tables (seven copy calls cost ~25 us of host time per mirror delta)
     void flush() {
         if (c.class_pending) {
             PBKV_CUDA(cudaEventSynchronize(c.ev_class));
@@ -305,14 +325,23 @@ struct ClassStager {
         }
         if (items.empty()) return;
         c.hclass.reserve(total);
+        c.dclass.reserve(total);
+        ScatterDesc d{};
         std::size_t o = 0;
         for (const Item& it : items) {
             std::memcpy(c.hclass.p + o, it.src, it.bytes);
-            PBKV_CUDA(cudaMemcpyAsync(it.dst, c.hclass.p + o, it.bytes, cudaMemcpyHostToDevice, c.stream));
+            d.dst[d.n] = static_cast<unsigned char*>(it.dst);
+            d.off[d.n] = o;
+            d.bytes[d.n] = it.bytes;
+            ++d.n;
             o += (it.bytes + 15) & ~std::size_t(15);
         }
+        PBKV_CUDA(cudaMemcpyAsync(c.dclass.p, c.hclass.p, o, cudaMemcpyHostToDevice, c.stream));
         PBKV_CUDA(cudaEventRecord(c.ev_class, c.stream));
         c.class_pending = true;
+        scatter_blob_kernel<<<static_cast<unsigned int>(d.n), 256, 0, c.stream>>>(c.dclass.p, d);
+        PBKV_CUDA(cudaGetLastError());
+        ++c.launches;
     }
 };
 

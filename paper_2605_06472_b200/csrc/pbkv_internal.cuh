@@ -212,6 +212,7 @@ struct Context {
     // staging of the class tables (medium / heavy lists, products list,
     // heavy children): reused once ev_class has passed
     PinBuf<unsigned char> hclass;
+    DevBuf<unsigned char> dclass;  // the class tables' upload blob (ClassStager)
     cudaEvent_t ev_class = nullptr;
     cudaEvent_t ev_caller = nullptr;  // pbkv_ctx_wait_stream
     bool class_pending = false;
