@@ -109,6 +109,7 @@ struct SelState {
     unsigned int rf_rounds;     // refinement rounds run (diagnostics)
     unsigned long long ts[40];  // %globaltimer after each phase (diagnostics)
     unsigned long long dbg[8];  // per-CTA maxima of phase work (diagnostics)
+    unsigned long long dbg2[4]; // small path: S1 histogram (max CTA), S1 layout (last CTA) (diagnostics)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1518,6 +1519,7 @@ __device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
 // S1: histogram of the low heads (count, chain weight, chain size per 11-bit digit)
 __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long n_low, int lo, unsigned long long v0,
                                            unsigned long long v1, unsigned long long v2, PersistSmem& sm) {
+    const unsigned long long th0 = gtimer();
     for (int b = threadIdx.x; b < kSBins; b += blockDim.x) {
         sm.u.hist.w[b] = 0;
         sm.u.hist.c[b] = 0;
@@ -1551,9 +1553,13 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     // the low heads, the list of buckets ranked by tiles and their first tasks
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) sm.bc[0] = atomicAdd(&a.ss->small_done, 1u);
+    if (threadIdx.x == 0) {
+        sm.bc[0] = atomicAdd(&a.ss->small_done, 1u);
+        atomicMax(&a.ss->dbg2[0], gtimer() - th0);
+    }
     __syncthreads();
     if (sm.bc[0] != gridDim.x - 1) return;
+    const unsigned long long tl0 = gtimer();
     // one bin per thread (kSBins == kPThreads): warp scans, the warps' totals
     // through shared memory -- two block barriers per scan stage, coalesced
     // loads and stores, a handful of registers
@@ -1656,6 +1662,7 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         a.ss->n_task = static_cast<unsigned int>(tt);
         a.ss->small_ok = 1;
         a.ss->path = 1;
+        a.ss->dbg2[1] = gtimer() - tl0;
     }
 }
 
@@ -2795,11 +2802,11 @@ SelectCounts run_select(Context& c, const int* locked_dev, std::int64_t n_locked
                      "cut_head=%d need_final=%llu max_bucket=%d n_victims=%llu freed=%llu shortfall=%d grid=%d "
                      "path=%d low_ovf=%u n_low=%llu est_low=%llu n_big=%u rf_rounds=%u n_rsmall=%u "
                      "dbg(ns): sortCTA=%llu sortWarp=%llu loadpack=%llu rank=%llu nbig=%llu bound=%llu "
-                     "walk_end=%llu lock_end=%llu\n",
+                     "walk_end=%llu lock_end=%llu s1_hist=%llu s1_layout=%llu\n",
                      hs->n_L[0], hs->total_tok, hs->take_all, hs->host_sort, hs->n_S, hs->n_pass, hs->cut_head,
                      hs->need_final, hs->max_bucket, hs->n_victims, hs->freed, hs->shortfall, grid, hs->path,
                      hs->low_overflow, hs->n_low, hs->est_low, hs->n_big, hs->rf_rounds, hs->n_rsmall, hs->dbg[0],
-                     hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6], hs->dbg[7]);
+                     hs->dbg[1], hs->dbg[2], hs->dbg[3], hs->dbg[4], hs->dbg[5], hs->dbg[6], hs->dbg[7], hs->dbg2[0], hs->dbg2[1]);
     if (hs->host_sort) {
         // ---- fallback: device-wide sort of the selected heads -----------------------------
         const std::int64_t nS = static_cast<std::int64_t>(hs->n_S);
