@@ -1289,7 +1289,7 @@ struct GridBar {
                 asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
                 if (v >= target) break;
                 __nanosleep(ns);
-                ns = ns < 256 ? ns * 2 : 256;
+                ns = ns < 128 ? ns * 2 : 128;
             }
         }
         __syncthreads();

@@ -1,5 +1,7 @@
 cd /root/repo
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_full_size.py tests/test_refine.py tests/test_shard.py -x -q 2>&1 | tail -2
-for c in c3 c2 c4; do
-timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep > gpurun_out/b.log 2>&1; python tools/show_bench.py gpurun_out/b.log 2>/dev/null | head -2
+for rep in 1 2; do
+for v in base var_so/libpbkv_ns64.so var_so/libpbkv_ns128.so var_so/libpbkv_ns512.so; do
+  if [ "$v" = base ]; then unset PBKV_LIB; else export PBKV_LIB=$PWD/$v; fi
+  timeout 300 python bench.py --steps 30 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep > gpurun_out/bv.log 2>&1; echo "$v $(python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | head -1 | cut -c1-200)"
+done
 done
