@@ -1,7 +1,7 @@
 cd /root/repo
-for rep in 1 2; do
-for v in base var_so/libpbkv_ns64.so var_so/libpbkv_ns128.so var_so/libpbkv_ns512.so; do
+for c in c3 c4; do
+for v in base var_so/libpbkv_s2_w4.so var_so/libpbkv_s6_w4.so var_so/libpbkv_s4_w8.so var_so/libpbkv_s4_w2.so; do
   if [ "$v" = base ]; then unset PBKV_LIB; else export PBKV_LIB=$PWD/$v; fi
-  timeout 300 python bench.py --steps 30 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep > gpurun_out/bv.log 2>&1; echo "$v $(python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | head -1 | cut -c1-200)"
+  timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep > gpurun_out/bv.log 2>&1; echo "$c $v $(python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | sed -n 2p)"
 done
 done
