@@ -1,7 +1,5 @@
 cd /root/repo
-for c in c3 c4; do
-for v in base var_so/libpbkv_s2_w4.so var_so/libpbkv_s6_w4.so var_so/libpbkv_s4_w8.so var_so/libpbkv_s4_w2.so; do
-  if [ "$v" = base ]; then unset PBKV_LIB; else export PBKV_LIB=$PWD/$v; fi
-  timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep > gpurun_out/bv.log 2>&1; echo "$c $v $(python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | sed -n 2p)"
-done
-done
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_gpu.log)"
+grep -E "^(FAILED|ERROR)" gpurun_out/pytest_gpu.log | head
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; python tools/show_bench.py gpurun_out/bench_default.log 2>/dev/null | head -3
