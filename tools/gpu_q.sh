@@ -1,5 +1,6 @@
 cd /root/repo
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_gpu.log)"
-grep -E "^(FAILED|ERROR)" gpurun_out/pytest_gpu.log | head
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; python tools/show_bench.py gpurun_out/bench_default.log 2>/dev/null | head -3
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_full_size.py tests/test_defer.py tests/test_refine.py tests/test_shard.py -x -q 2>&1 | tail -2
+for f in 0.01 0.05 0.1; do
+timeout 300 python bench.py --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-sweep --no-prefetch --needed-frac $f > gpurun_out/bf.log 2>&1
+echo "$f $(python tools/show_bench.py gpurun_out/bf.log 2>/dev/null | head -2 | tr '\n' ' ' | cut -c1-250)"
+done
