@@ -253,3 +253,44 @@ def test_errors_match_reference(gpu):
             pol3.score_all()
         with pytest.raises(ValidationError, match="missing forecast for active workflow 9"):
             pol3.select_victims_hierarchical(1, score_mode=SCORE_RECOMPUTE)
+
+
+def test_ctx_wait_stream_orders_device_inputs(gpu):
+    """pbkv_ctx_wait_stream: a locked list written late on a torch stream
+    (behind a 50 ms spin) is seen by a device-input decision enqueued after
+    the wait -- no host synchronisation, same victims as the host-input call."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2605_06472_b200 import _abi
+
+    t = HostTree()
+    t.synth(n_nodes=20000, n_workflows=128, agents=8, seed=5)
+    soa = t.export()
+    rng = np.random.default_rng(5)
+    wf = np.array(WL.workflows_of(soa), dtype=np.int64)
+    P = WL.random_forecasts(rng, wf.size, 4, 9)
+    pol = Policy(num_agents=8, k=4, gamma=0.7)
+    pol.mirror(t)
+    pol.put_forecasts(wf, P)
+    locked = np.asarray(WL.pinned_paths(soa, rng, 0.05), dtype=np.int32)
+    used = int(soa.len[soa.tier == 0][1:].sum())
+    needed = used // 3
+    want = pol.select_victims_hierarchical(needed, locked=locked, score_mode=SCORE_RECOMPUTE)
+    dev = torch.device("cuda", 0)
+    src = torch.from_numpy(locked).to(dev)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream(device=dev)
+    locked_d = torch.zeros_like(src)
+    victims = torch.zeros(soa.n_nodes, dtype=torch.int32, device=dev)
+    res = torch.zeros(3, dtype=torch.int64, device=dev)
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(100_000_000)  # ~50 ms of spinning before the write
+        locked_d.copy_(src)
+    pol._c(_abi.lib().pbkv_ctx_wait_stream(pol.handle, C.c_void_p(s.cuda_stream)))
+    pol.select_dev(POLICY_HE, SCORE_RECOMPUTE, needed, locked_d.data_ptr(), int(locked.size), victims.data_ptr(),
+                   soa.n_nodes, res.data_ptr())
+    torch.cuda.synchronize()
+    nv, freed, sf = (int(x) for x in res.cpu().tolist())
+    assert (victims[:nv].cpu().tolist(), freed, bool(sf)) == (want.victims, want.freed, want.shortfall)
