@@ -152,6 +152,7 @@ struct alignas(16) Key2 {
 struct HeadKey {
     unsigned long long w0, w1;
     unsigned int id;
+    unsigned int pad;  // written (zero): the sort moves whole 8-byte words
 };
 
 // a prefetch plan in pinned host memory (prefetch.cu run_prefetch_plan):

@@ -2555,7 +2555,7 @@ __global__ void gather_headkeys_kernel(const int* S, const Key2* keys, const Sel
          i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
         const int x = S[i];
         const Key2 k = load_key(keys, x);
-        out[i] = HeadKey{k.w0, k.w1, static_cast<unsigned int>(x)};
+        out[i] = HeadKey{k.w0, k.w1, static_cast<unsigned int>(x), 0u};
     }
 }
 
