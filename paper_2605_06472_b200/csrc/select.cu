@@ -55,8 +55,10 @@ constexpr int kScanIPT = 8;       // chain-start scan: items per thread per chun
 // small-cut path: a node sample bounds the cut from above;
 // the low heads are bucketed by a 9-bit digit (one bin per thread of the
 // layout scan)
-constexpr int kSBits = 9;
-constexpr int kSBins = 1 << kSBits;
+constexpr int kSBits = 9;           // digit of the small path (512 bins, one per layout thread) ...
+constexpr int kSBitsWide = 11;      // ... or 2048 bins when the low list is long
+constexpr unsigned long long kSWideAt = 65536;  // low heads from which the wide digit is used
+constexpr int kChunkS = 512 / 8;    // small-path rank task: 64 heads, 8 threads each (kPThreads = 512)
 constexpr int kSamp = 2048;            // sample records (the eff phase appends ~1024)
 constexpr unsigned int kSampTarget = 1024;
 constexpr long long kSmallMax = 1 << 18;  // estimated heads below the bound for the small path
@@ -1517,10 +1519,13 @@ __device__ SmallBound small_bound(const SelArgs& a, PersistSmem& sm) {
 }
 
 // S1: histogram of the low heads (count, chain weight, chain size per 11-bit digit)
-__device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long n_low, int lo, unsigned long long v0,
-                                           unsigned long long v1, unsigned long long v2, PersistSmem& sm) {
+template <int kNBins>
+__device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long n_low, int lo,
+                                           unsigned long long v0, unsigned long long v1, unsigned long long v2,
+                                           PersistSmem& sm) {
+    constexpr int nbins = kNBins;
     const unsigned long long th0 = gtimer();
-    for (int b = threadIdx.x; b < kSBins; b += blockDim.x) {
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
         sm.u.hist.w[b] = 0;
         sm.u.hist.c[b] = 0;
         sm.u.hist.cs[b] = 0;
@@ -1531,7 +1536,7 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
          i += stride) {
         const int x = __ldcg(&a.low[i]);
         const unsigned long long pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
-        const unsigned int d = static_cast<unsigned int>(pk >> lo) & (kSBins - 1);
+        const unsigned int d = static_cast<unsigned int>(pk >> lo) & static_cast<unsigned int>(nbins - 1);
         smem_add_u64(&sm.u.hist.w[d], chain_w(a, x));
         atomicAdd(&sm.u.hist.c[d], 1u);
         atomicAdd(reinterpret_cast<unsigned int*>(sm.u.hist.cs) + d, chain_c(a, x));  // < 2^24 (nodes)
@@ -1541,7 +1546,7 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     // count with the chain-size sum packed in one word (both < 2^32: they
     // count nodes)
     const unsigned int* csum = reinterpret_cast<const unsigned int*>(sm.u.hist.cs);
-    for (int b = threadIdx.x; b < kSBins; b += blockDim.x) {
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
         const unsigned int c = sm.u.hist.c[b];
         if (c) {
             atomicAdd(&a.sm_w[b], sm.u.hist.w[b]);
@@ -1560,22 +1565,145 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     __syncthreads();
     if (sm.bc[0] != gridDim.x - 1) return;
     const unsigned long long tl0 = gtimer();
-    // one bin per thread (kSBins == kPThreads): warp scans, the warps' totals
-    // through shared memory -- two block barriers per scan stage, coalesced
-    // loads and stores, a handful of registers
-    static_assert(kSBins == kPThreads, "the layout maps one bin to one thread");
+    if constexpr (nbins == kPThreads) {  // the narrow digit: one bin per thread, in registers
+        // one bin per thread: warp scans, the warps' totals
+        // through shared memory -- two block barriers per scan stage, coalesced
+        // loads and stores, a handful of registers
+        __threadfence();
+        const int d = threadIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        constexpr int kW = kPThreads / 32;
+        unsigned long long* wt = sm.u.hist.w;  // [kW][4] warp totals (the histogram is no longer needed)
+        const unsigned long long packed = __ldcg(&a.sm_cs[d]);
+        const unsigned long long vw = __ldcg(&a.sm_w[d]);
+        const unsigned int vc = static_cast<unsigned int>(packed >> 32);
+        const unsigned long long vs = packed & 0xffffffffull;
+        // stage 1: counts, tokens, chain sizes (exclusive prefixes), max count
+        unsigned long long xc = vc, xw = vw, xs = vs;
+        unsigned int mx = vc;
+    #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long yc = __shfl_up_sync(0xffffffffu, xc, o);
+            const unsigned long long yw = __shfl_up_sync(0xffffffffu, xw, o);
+            const unsigned long long ys = __shfl_up_sync(0xffffffffu, xs, o);
+            if (lane >= o) {
+                xc += yc;
+                xw += yw;
+                xs += ys;
+            }
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 31) {
+            wt[warp * 4 + 0] = xc;
+            wt[warp * 4 + 1] = xw;
+            wt[warp * 4 + 2] = xs;
+            wt[warp * 4 + 3] = mx;
+        }
+        __syncthreads();
+        unsigned long long pc = 0, pw = 0, ps = 0, tw = 0;
+        unsigned int mxa = 0;
+        for (int w = 0; w < kW; ++w) {
+            if (w < warp) {
+                pc += wt[w * 4 + 0];
+                pw += wt[w * 4 + 1];
+                ps += wt[w * 4 + 2];
+            }
+            tw += wt[w * 4 + 1];
+            mxa = max(mxa, static_cast<unsigned int>(wt[w * 4 + 3]));
+        }
+        const unsigned long long ex_c = pc + xc - vc, ex_w = pw + xw - vw, ex_s = ps + xs - vs;
+        const unsigned long long need = static_cast<unsigned long long>(a.needed);
+        if (!(tw >= need && mxa <= static_cast<unsigned int>(kBucketCap))) {  // uniform
+            if (threadIdx.x == 0) {
+                a.ss->small_ok = 2;
+                a.ss->path = tw >= need ? 4 : 3;  // bucket too large / bound too low
+                a.ss->dbg[5] = tw;
+                a.ss->dbg[6] = mxa;
+            }
+            return;
+        }
+        // stage 2: the buckets ranked by tiles (> 32 heads, not wholly after the
+        // cut): their list positions and first rank tasks
+        const bool big = vc > 32u && ex_w < need;
+        const unsigned long long tk = big ? (vc + kChunkS - 1) / kChunkS : 0u;
+        unsigned long long xb = big ? 1u : 0u, xt = tk;
+    #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long yb = __shfl_up_sync(0xffffffffu, xb, o);
+            const unsigned long long yt = __shfl_up_sync(0xffffffffu, xt, o);
+            if (lane >= o) {
+                xb += yb;
+                xt += yt;
+            }
+        }
+        __syncthreads();  // wt is rewritten
+        if (lane == 31) {
+            wt[warp * 4 + 0] = xb;
+            wt[warp * 4 + 1] = xt;
+        }
+        __syncthreads();
+        unsigned long long pb = 0, pt = 0, tb = 0, tt = 0;
+        for (int w = 0; w < kW; ++w) {
+            if (w < warp) {
+                pb += wt[w * 4 + 0];
+                pt += wt[w * 4 + 1];
+            }
+            tb += wt[w * 4 + 0];
+            tt += wt[w * 4 + 1];
+        }
+        a.sm_c[d] = vc;
+        a.sm_off[d] = static_cast<unsigned int>(ex_c);
+        a.sm_wpre[d] = ex_w;
+        a.sm_cpre[d] = ex_s;
+        if (big) {
+            const unsigned long long q = pb + xb - 1u;
+            a.sm_big[3 * q] = static_cast<unsigned int>(d);
+            a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
+            a.sm_big[3 * q + 2] = vc;
+            a.sm_task[q] = static_cast<unsigned int>(pt + xt - tk);
+        }
+        if (threadIdx.x == 0) {
+            a.ss->n_big = static_cast<unsigned int>(tb);
+            a.ss->n_task = static_cast<unsigned int>(tt);
+            a.ss->small_ok = 1;
+            a.ss->path = 1;
+            a.ss->dbg2[1] = gtimer() - tl0;
+        }
+    } else {
+    // kPer = nbins / kPThreads consecutive bins per thread (4): thread
+    // sums, warp scans, the warps' totals through shared memory; the bins'
+    // values are re-read from L2 in each pass (no per-bin register arrays)
     __threadfence();
-    const int d = threadIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int kChunkS = kPThreads / 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kPer = nbins / kPThreads;
+    const int d0 = threadIdx.x * kPer;
     constexpr int kW = kPThreads / 32;
-    unsigned long long* wt = sm.u.hist.w;  // [kW][4] warp totals (the histogram is no longer needed)
-    const unsigned long long packed = __ldcg(&a.sm_cs[d]);
-    const unsigned long long vw = __ldcg(&a.sm_w[d]);
-    const unsigned int vc = static_cast<unsigned int>(packed >> 32);
-    const unsigned long long vs = packed & 0xffffffffull;
+    // the CTA's own histogram is flushed: its shared arrays hold the global
+    // bins (each thread its own, read once from L2) and the warp totals
+    unsigned long long* bw_sh = sm.u.hist.w;   // [nbins] tokens
+    unsigned long long* bcs_sh = sm.u.hist.cs;  // [nbins] count << 32 | chain sizes
+    unsigned long long* wt = reinterpret_cast<unsigned long long*>(sm.u.hist.c);  // [kW][4] warp totals
+    for (int i = 0; i < kPer; ++i) {
+        bw_sh[d0 + i] = __ldcg(&a.sm_w[d0 + i]);
+        bcs_sh[d0 + i] = __ldcg(&a.sm_cs[d0 + i]);
+    }
+    auto bin = [&](int d, unsigned long long& vc, unsigned long long& vw, unsigned long long& vs) {
+        const unsigned long long packed = bcs_sh[d];
+        vw = bw_sh[d];
+        vc = packed >> 32;
+        vs = packed & 0xffffffffull;
+    };
     // stage 1: counts, tokens, chain sizes (exclusive prefixes), max count
-    unsigned long long xc = vc, xw = vw, xs = vs;
-    unsigned int mx = vc;
+    unsigned long long tc = 0, tw_ = 0, ts = 0;
+    unsigned int mx = 0;
+    for (int i = 0; i < kPer; ++i) {
+        unsigned long long vc, vw, vs;
+        bin(d0 + i, vc, vw, vs);
+        tc += vc;
+        tw_ += vw;
+        ts += vs;
+        mx = max(mx, static_cast<unsigned int>(vc));
+    }
+    unsigned long long xc = tc, xw = tw_, xs = ts;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long yc = __shfl_up_sync(0xffffffffu, xc, o);
@@ -1606,7 +1734,7 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         tw += wt[w * 4 + 1];
         mxa = max(mxa, static_cast<unsigned int>(wt[w * 4 + 3]));
     }
-    const unsigned long long ex_c = pc + xc - vc, ex_w = pw + xw - vw, ex_s = ps + xs - vs;
+    const unsigned long long bc0 = pc + xc - tc, bw0 = pw + xw - tw_, bs0 = ps + xs - ts;  // the thread's first bin
     const unsigned long long need = static_cast<unsigned long long>(a.needed);
     if (!(tw >= need && mxa <= static_cast<unsigned int>(kBucketCap))) {  // uniform
         if (threadIdx.x == 0) {
@@ -1619,9 +1747,20 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
     }
     // stage 2: the buckets ranked by tiles (> 32 heads, not wholly after the
     // cut): their list positions and first rank tasks
-    const bool big = vc > 32u && ex_w < need;
-    const unsigned long long tk = big ? (vc + kChunkS - 1) / kChunkS : 0u;
-    unsigned long long xb = big ? 1u : 0u, xt = tk;
+    unsigned long long nbt = 0, ntt = 0;
+    {
+        unsigned long long ew = bw0;
+        for (int i = 0; i < kPer; ++i) {
+            unsigned long long vc, vw, vs;
+            bin(d0 + i, vc, vw, vs);
+            if (vc > 32u && ew < need) {
+                nbt += 1;
+                ntt += (vc + kChunkS - 1) / kChunkS;
+            }
+            ew += vw;
+        }
+    }
+    unsigned long long xb = nbt, xt = ntt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long yb = __shfl_up_sync(0xffffffffu, xb, o);
@@ -1646,16 +1785,28 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         tb += wt[w * 4 + 0];
         tt += wt[w * 4 + 1];
     }
-    a.sm_c[d] = vc;
-    a.sm_off[d] = static_cast<unsigned int>(ex_c);
-    a.sm_wpre[d] = ex_w;
-    a.sm_cpre[d] = ex_s;
-    if (big) {
-        const unsigned long long q = pb + xb - 1u;
-        a.sm_big[3 * q] = static_cast<unsigned int>(d);
-        a.sm_big[3 * q + 1] = static_cast<unsigned int>(ex_c);
-        a.sm_big[3 * q + 2] = vc;
-        a.sm_task[q] = static_cast<unsigned int>(pt + xt - tk);
+    {
+        unsigned long long ec = bc0, ew = bw0, es = bs0, q = pb + xb - nbt, tq = pt + xt - ntt;
+        for (int i = 0; i < kPer; ++i) {
+            const int d = d0 + i;
+            unsigned long long vc, vw, vs;
+            bin(d, vc, vw, vs);
+            a.sm_c[d] = static_cast<unsigned int>(vc);
+            a.sm_off[d] = static_cast<unsigned int>(ec);
+            a.sm_wpre[d] = ew;
+            a.sm_cpre[d] = es;
+            if (vc > 32u && ew < need) {
+                a.sm_big[3 * q] = static_cast<unsigned int>(d);
+                a.sm_big[3 * q + 1] = static_cast<unsigned int>(ec);
+                a.sm_big[3 * q + 2] = static_cast<unsigned int>(vc);
+                a.sm_task[q] = static_cast<unsigned int>(tq);
+                ++q;
+                tq += (vc + kChunkS - 1) / kChunkS;
+            }
+            ec += vc;
+            ew += vw;
+            es += vs;
+        }
     }
     if (threadIdx.x == 0) {
         a.ss->n_big = static_cast<unsigned int>(tb);
@@ -1663,6 +1814,7 @@ __device__ __forceinline__ void small_hist(const SelArgs& a, unsigned long long 
         a.ss->small_ok = 1;
         a.ss->path = 1;
         a.ss->dbg2[1] = gtimer() - tl0;
+    }
     }
 }
 
@@ -1735,8 +1887,13 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
         }
         return false;
     }
-    const int lo = nbits > kSBits ? nbits - kSBits : 0;
-    small_hist(a, n_low, lo, v0, v1, v2, sm);
+    const int sb = n_low > kSWideAt ? kSBitsWide : kSBits;  // uniform: every CTA read the same n_low
+    const int nbins = 1 << sb;
+    const int lo = nbits > sb ? nbits - sb : 0;
+    if (sb == kSBits)
+        small_hist<1 << kSBits>(a, n_low, lo, v0, v1, v2, sm);
+    else
+        small_hist<1 << kSBitsWide>(a, n_low, lo, v0, v1, v2, sm);
     grid.sync();
     stamp(ss, nts);
     // S2: the layout the last S1 CTA wrote; the check that the cut lies among
@@ -1755,7 +1912,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
             if (i < n_low) {
                 x = __ldcg(&a.low[i]);
                 pk = pack_key(load_key(a.keys, x), x, v0, v1, v2);
-                d = static_cast<int>((pk >> lo) & (kSBins - 1));
+                d = static_cast<int>((pk >> lo) & static_cast<unsigned long long>(nbins - 1));
                 cw = (chain_w(a, x) << 24) | static_cast<unsigned long long>(chain_c(a, x));
             }
             const unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -1779,7 +1936,7 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
         const int lane = threadIdx.x & 31;
         const int gwarp = static_cast<int>((blockIdx.x * static_cast<unsigned int>(blockDim.x) + threadIdx.x) >> 5);
         const int nwarps = static_cast<int>((gridDim.x * static_cast<unsigned int>(blockDim.x)) >> 5);
-        for (int d = gwarp; d < kSBins; d += nwarps) {
+        for (int d = gwarp; d < nbins; d += nwarps) {
             const unsigned int cnt = __ldcg(&a.sm_c[d]);
             if (cnt == 0u || cnt > 32u) continue;
             const unsigned long long wpre = __ldcg(&a.sm_wpre[d]);
@@ -1816,7 +1973,6 @@ __device__ bool small_path(const SelArgs& a, PersistSmem& sm, const GridBar& gri
         for (unsigned int q = threadIdx.x; q < n_big; q += blockDim.x) sm.off[q] = __ldcg(&a.sm_task[q]);
         __syncthreads();
         if (n_big > 0) {
-            constexpr int kChunkS = kPThreads / 8;
             unsigned int held = ~0u;
             for (unsigned int t = blockIdx.x; t < static_cast<unsigned int>(ttot); t += gridDim.x) {
                 unsigned int blo = 0, bhi = n_big - 1;  // last bucket whose first task is <= t

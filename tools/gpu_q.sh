@@ -1,5 +1,10 @@
 cd /root/repo
-O=gpurun_out/san; mkdir -p $O
-timeout 1500 compute-sanitizer --tool initcheck --print-limit 5 python -m pytest -q -x -m gpu "tests/test_shard.py::test_interval_sums_bound" "tests/test_gpu_parity.py::test_ctx_wait_stream_orders_device_inputs" "tests/test_prefetch_round.py::test_prefetch_round_equals_reference_loop[7]" "tests/test_refine.py::test_device_sort_fallback_equals_oracle[0]" > $O/final_initcheck.log 2>&1
-echo "initcheck rc=$? $(grep -E 'ERROR SUMMARY|passed|failed' $O/final_initcheck.log | tail -2 | tr '\n' ' ')"
-grep -A4 "Uninitialized" $O/final_initcheck.log | head -12
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_full_size.py tests/test_defer.py tests/test_refine.py -x -q 2>&1 | tail -1
+for rep in 1 2; do
+for v in base var_so/libpbkv_head.so; do
+  if [ "$v" = base ]; then unset PBKV_LIB; else export PBKV_LIB=$PWD/$v; fi
+  for f in 0.01 0.1; do
+  timeout 300 python bench.py --steps 30 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep --needed-frac $f > gpurun_out/bv.log 2>&1; echo "$f $v $(python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | head -2 | tr '\n' ' ' | cut -c1-230)"
+  done
+done
+done
