@@ -1,8 +1,7 @@
 cd /root/repo
-O=gpurun_out/r2final; mkdir -p $O
-timeout 1500 python -m pytest tests -x -q -m gpu > $O/pytest_gpu.log 2>&1; echo "pytest rc=$? $(tail -1 $O/pytest_gpu.log)"
-python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?; tail -1 $O/smoke.log
-timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench_c3.log 2>&1; echo c3 rc=$?
-timeout 600 python bench.py --config c2 --steps 20 --warmup 5 --no-cpu-baseline --no-pipeline > $O/bench_c2.log 2>&1; echo c2 rc=$?
-timeout 900 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu-baseline --no-pipeline --no-sweep > $O/bench_c4.log 2>&1; echo c4 rc=$?
-timeout 900 python bench.py --sharded --steps 10 --warmup 3 > $O/bench_c4_sharded.log 2>&1; echo c4sh rc=$?
+for f in 0.1 0.2 0.3; do
+for v in base var_so/libpbkv_sm19.so var_so/libpbkv_sm20.so; do
+  if [ "$v" = base ]; then unset PBKV_LIB; else export PBKV_LIB=$PWD/$v; fi
+  PBKV_DEBUG_SELECT=1 timeout 300 python bench.py --steps 20 --warmup 5 --no-pipeline --no-cpu-baseline --no-prefetch --no-sweep --needed-frac $f > gpurun_out/bv.log 2>&1; echo "$f $v $(grep 'pbkv select' gpurun_out/bv.log | tail -1 | grep -o 'path=[0-9]*') $(python tools/show_bench.py gpurun_out/bv.log 2>/dev/null | head -1 | cut -c1-120)"
+done
+done
